@@ -1,0 +1,162 @@
+/*
+ * fieldtess_cuda.h -- C-ABI of the B200 (sm_100a) layered-field engine.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `fieldtess` (arXiv 1804.09152).  The reference has no native code: its
+ * compute layer is a set of numba kernels that take raw numpy arrays and
+ * write into caller-preallocated outputs, signalling errors through flag
+ * arrays (`fieldtess/_kernels.py`).  Every entry point below replaces one
+ * stage of that pipeline (citations are `path:line` under the reference's
+ * `pkg/src/fieldtess/`).
+ *
+ * Conventions
+ *   - `extern "C"`, plain pointers and sizes, no exceptions cross the ABI.
+ *   - All matrices are CSC exactly as the reference stores them
+ *     (`sparse.py:27-57`): int32 `col_ptr[n_cols+1]`, int32 `row_idx[cap]`,
+ *     values `double` (FT_F64) or `float` (FT_F32).  The layered field PHI is
+ *     (n_cells+1) x n_vertices: column = vertex, row 0 = base layer,
+ *     row r = cell r-1 (`field.py:95-130`).
+ *   - The Laplacian is passed as `lap.mat_t` (L^T in CSC), which is
+ *     byte-identical to L in CSR with ascending neighbour index including
+ *     the diagonal (`mesh.py:379-431`).
+ *   - Every pointer argument except the host-side `ft_params*` is DEVICE
+ *     memory owned by the caller.  Calls only enqueue work on `stream`
+ *     (a `cudaStream_t`, passed as void*); results are read by the caller.
+ *   - Return value: FT_OK or an FT_ERR_* code; `ft_last_error()` returns a
+ *     thread-local message for the last failure.
+ */
+#ifndef FIELDTESS_CUDA_H
+#define FIELDTESS_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FT_ABI_VERSION 1
+
+/* return codes (mapped onto the reference's TessError subclasses,
+ * `errors.py:9-75`, by the Python host layer) */
+#define FT_OK              0
+#define FT_ERR_SHAPE       1  /* ShapeError                                  */
+#define FT_ERR_NUMERICAL   2  /* NumericalBlowupError(column, step)          */
+#define FT_ERR_CAPACITY    3  /* output capacity too small: grow >=1.2x, retry
+                                 (ensure_capacity, sparse.py:212-232)        */
+#define FT_ERR_CUDA        4  /* CUDA runtime failure                        */
+#define FT_ERR_PATTERN     5  /* PatternViolationError (sparse.py:389-394)   */
+#define FT_ERR_ARG         6  /* bad argument (null pointer, bad dtype, ...)  */
+
+/* value dtypes */
+#define FT_F64 0   /* EXACT mode: bitwise identical to the reference       */
+#define FT_F32 1   /* FAST mode: fp32 storage, fp64 in-register arithmetic  */
+
+/* Laplacian flags */
+#define FT_LAP_EXPLICIT 0  /* use the stored values                           */
+#define FT_LAP_UNIFORM  1  /* values are exactly 1.0/deg(j) off-diagonal and
+                              -1.0 on the diagonal (mesh.py:392-400): they are
+                              recomputed in registers and never read          */
+
+/* device status codes written into ft_step_stats.status */
+#define FT_STATUS_OK        0
+#define FT_STATUS_NAN       1
+#define FT_STATUS_PATTERN   2
+#define FT_STATUS_OVERFLOW  3
+#define FT_STATUS_CONVERGED 4
+#define FT_STATUS_MAXSTEPS  5
+
+/* CouplingParams (field.py:34-71).  Host memory. */
+typedef struct {
+    double w, a, e, e_base, mu, dt;
+} ft_params;
+
+/* Sparse matrix in CSC.  `values` dtype given by the call's dtype argument. */
+typedef struct {
+    int32_t  n_rows;
+    int32_t  n_cols;
+    int32_t* col_ptr;     /* [n_cols+1]                                   */
+    int32_t* row_idx;     /* [capacity]                                   */
+    void*    values;      /* [capacity] double or float                   */
+    int64_t  capacity;
+} ft_csc;
+
+/* One step's statistics, device resident.  Mirrors StepStats
+ * (field.py:74-92) plus the error flags the reference signals through
+ * `nan_col` / `bad_col` arrays (_kernels.py:165-176, 231-233). */
+typedef struct {
+    double  max_delta;        /* max_j max_p |v' - phi_old|  (field.py:271)  */
+    double  base_mass;        /* sum_j base mass             (field.py:270)  */
+    int64_t nnz_phi;          /* nnz of the output field                     */
+    int64_t nnz_skel;         /* interest-skeleton nnz of the step           */
+    int32_t status;           /* FT_STATUS_*                                 */
+    int32_t nan_col;          /* first column that produced NaN, or -1       */
+    int32_t bad_col;          /* first column with a pattern violation, -1   */
+    int32_t bad_row;          /* offending row in `bad_col`                  */
+    int32_t bad_is_lt;        /* 0: violation in PHI, 1: in Lt               */
+    int32_t step;             /* 1-based step index within the call         */
+    int64_t reserved;
+} ft_step_stats;
+
+/* -- library ------------------------------------------------------------- */
+int         ft_abi_version(void);
+const char* ft_last_error(void);
+
+/* Bytes of the per-field-size scratch `workspace` (tile status words,
+ * tile partial sums, device control block).  The workspace must be zeroed
+ * once with ft_workspace_init before first use and is then reused by every
+ * ft_step / ft_evolve call with the same n_vertices. */
+size_t ft_workspace_bytes(int32_t n_vertices);
+int    ft_workspace_init(void* workspace, size_t bytes, void* stream);
+
+/* -- the fused Euler step ------------------------------------------------ */
+/* One explicit Euler step PHI_out = step(PHI_in) in a single fused pass.
+ * Replaces the whole pipeline of field.step (field.py:198-286):
+ *   sparse.spgemm (sparse.py:279-330; _kernels.py:14-74)      Lt = PHI L^T
+ *   sparse.build_skeleton (sparse.py:345-371; _kernels.py:96-150)
+ *   sparse.expand_to_skeleton x2 (sparse.py:374-396; _kernels.py:153-176)
+ *   _kernels.update_kernel (_kernels.py:179-238)
+ *   _kernels.column_sums_counts + normalize_compact (_kernels.py:241-282)
+ * `stats` (device, one record) receives the statistics.  If the output
+ * does not fit `out->capacity`, stats->status = FT_STATUS_OVERFLOW and
+ * stats->nnz_phi holds the required size (the input is left intact). */
+int ft_step(const ft_csc* lap_t, int32_t lap_flags,
+            const ft_csc* phi_in, ft_csc* phi_out, int32_t dtype,
+            const ft_params* params, void* workspace, size_t ws_bytes,
+            ft_step_stats* stats, void* stream);
+
+/* The two halves of ft_step, for callers that time the fused kernel on its
+ * own (bench.py): ft_step_kernel enqueues only the fused kernel (statistics
+ * stay in the workspace accumulators), ft_step_finalize reduces them into
+ * `stats` and resets the accumulators.  ft_step == kernel + finalize. */
+int ft_step_kernel(const ft_csc* lap_t, int32_t lap_flags,
+                   const ft_csc* phi_in, ft_csc* phi_out, int32_t dtype,
+                   const ft_params* params, void* workspace, size_t ws_bytes,
+                   void* stream);
+int ft_step_finalize(void* workspace, size_t ws_bytes, int32_t n_vertices,
+                     ft_step_stats* stats, void* stream);
+
+/* Up to `max_steps` steps alternating between buffers a and b (a holds the
+ * input), stopping on the device as soon as a step converges
+ * (max_delta < tol and base_mass < base_threshold; field.py:316-317), or on
+ * NaN / pattern violation / capacity overflow.  Replaces the loop of
+ * field.evolve (field.py:289-321).  `trace` (device, max_steps records)
+ * receives one ft_step_stats per executed step; `control` (device, 4 x
+ * int64) receives {steps_done, status, needed_capacity, reserved}.
+ * The call is asynchronous and captured into CUDA graphs internally. */
+int ft_evolve(const ft_csc* lap_t, int32_t lap_flags,
+              ft_csc* phi_a, ft_csc* phi_b, int32_t dtype,
+              const ft_params* params, int32_t max_steps, double tol,
+              double base_threshold, void* workspace, size_t ws_bytes,
+              ft_step_stats* trace, int64_t* control, void* stream);
+
+/* -- labels -------------------------------------------------------------- */
+/* Per-vertex argmax cell id; ties -> lowest cell; the base row wins only
+ * if strictly greater -> -1 (UNCLAIMED).  Replaces field.sharp_labels
+ * (field.py:324-356).  labels: int64[n_cols]. */
+int ft_labels(const ft_csc* phi, int32_t dtype, int64_t* labels, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIELDTESS_CUDA_H */

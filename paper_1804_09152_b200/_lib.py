@@ -1,0 +1,134 @@
+"""ctypes binding of the C-ABI library ``libfieldtess_cuda.so``.
+
+The library is the only compute backend: there is no CPU fallback.  If it is
+missing or fails to load, every compute entry point raises immediately.
+The structures mirror ``include/fieldtess_cuda.h`` field for field.
+"""
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfieldtess_cuda.so")
+
+FT_OK = 0
+FT_ERR_SHAPE = 1
+FT_ERR_NUMERICAL = 2
+FT_ERR_CAPACITY = 3
+FT_ERR_CUDA = 4
+FT_ERR_PATTERN = 5
+FT_ERR_ARG = 6
+
+FT_F64 = 0
+FT_F32 = 1
+
+FT_LAP_EXPLICIT = 0
+FT_LAP_UNIFORM = 1
+
+FT_STATUS_OK = 0
+FT_STATUS_NAN = 1
+FT_STATUS_PATTERN = 2
+FT_STATUS_OVERFLOW = 3
+FT_STATUS_CONVERGED = 4
+FT_STATUS_MAXSTEPS = 5
+
+ABI_VERSION = 1
+
+
+class FtParams(ctypes.Structure):
+    _fields_ = [("w", ctypes.c_double), ("a", ctypes.c_double),
+                ("e", ctypes.c_double), ("e_base", ctypes.c_double),
+                ("mu", ctypes.c_double), ("dt", ctypes.c_double)]
+
+
+class FtCsc(ctypes.Structure):
+    _fields_ = [("n_rows", ctypes.c_int32), ("n_cols", ctypes.c_int32),
+                ("col_ptr", ctypes.c_void_p), ("row_idx", ctypes.c_void_p),
+                ("values", ctypes.c_void_p), ("capacity", ctypes.c_int64)]
+
+
+class FtStepStats(ctypes.Structure):
+    _fields_ = [("max_delta", ctypes.c_double), ("base_mass", ctypes.c_double),
+                ("nnz_phi", ctypes.c_int64), ("nnz_skel", ctypes.c_int64),
+                ("status", ctypes.c_int32), ("nan_col", ctypes.c_int32),
+                ("bad_col", ctypes.c_int32), ("bad_row", ctypes.c_int32),
+                ("bad_is_lt", ctypes.c_int32), ("step", ctypes.c_int32),
+                ("reserved", ctypes.c_int64)]
+
+
+STATS_BYTES = ctypes.sizeof(FtStepStats)
+assert STATS_BYTES == 64
+
+# numpy view of a device stats array copied to the host
+import numpy as _np  # noqa: E402
+
+STATS_DTYPE = _np.dtype([("max_delta", "<f8"), ("base_mass", "<f8"),
+                         ("nnz_phi", "<i8"), ("nnz_skel", "<i8"),
+                         ("status", "<i4"), ("nan_col", "<i4"),
+                         ("bad_col", "<i4"), ("bad_row", "<i4"),
+                         ("bad_is_lt", "<i4"), ("step", "<i4"),
+                         ("reserved", "<i8")])
+assert STATS_DTYPE.itemsize == STATS_BYTES
+
+# every symbol include/fieldtess_cuda.h declares
+EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
+           "ft_workspace_init", "ft_step", "ft_step_kernel", "ft_step_finalize",
+           "ft_evolve", "ft_labels")
+
+_lib = None
+
+
+class LibraryMissing(RuntimeError):
+    """The CUDA library is not built or cannot be loaded (no CPU fallback)."""
+
+
+def _declare(lib):
+    vp = ctypes.c_void_p
+    P = ctypes.POINTER
+    lib.ft_abi_version.restype = ctypes.c_int
+    lib.ft_last_error.restype = ctypes.c_char_p
+    lib.ft_workspace_bytes.argtypes = [ctypes.c_int32]
+    lib.ft_workspace_bytes.restype = ctypes.c_size_t
+    lib.ft_workspace_init.argtypes = [vp, ctypes.c_size_t, vp]
+    lib.ft_workspace_init.restype = ctypes.c_int
+    lib.ft_step.argtypes = [P(FtCsc), ctypes.c_int32, P(FtCsc), P(FtCsc),
+                            ctypes.c_int32, P(FtParams), vp, ctypes.c_size_t,
+                            vp, vp]
+    lib.ft_step.restype = ctypes.c_int
+    lib.ft_step_kernel.argtypes = [P(FtCsc), ctypes.c_int32, P(FtCsc), P(FtCsc),
+                                   ctypes.c_int32, P(FtParams), vp, ctypes.c_size_t, vp]
+    lib.ft_step_kernel.restype = ctypes.c_int
+    lib.ft_step_finalize.argtypes = [vp, ctypes.c_size_t, ctypes.c_int32, vp, vp]
+    lib.ft_step_finalize.restype = ctypes.c_int
+    lib.ft_evolve.argtypes = [P(FtCsc), ctypes.c_int32, P(FtCsc), P(FtCsc),
+                              ctypes.c_int32, P(FtParams), ctypes.c_int32,
+                              ctypes.c_double, ctypes.c_double, vp,
+                              ctypes.c_size_t, vp, vp, vp]
+    lib.ft_evolve.restype = ctypes.c_int
+    lib.ft_labels.argtypes = [P(FtCsc), ctypes.c_int32, vp, vp]
+    lib.ft_labels.restype = ctypes.c_int
+
+
+def lib():
+    """The loaded library; raises :class:`LibraryMissing` loudly if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise LibraryMissing(
+                f"{LIB_PATH} is not built: run `make -C "
+                f"{os.path.join(_HERE, 'csrc')}` (or __graft_entry__.build()); "
+                "there is no CPU fallback")
+        try:
+            handle = ctypes.CDLL(LIB_PATH)
+        except OSError as exc:
+            raise LibraryMissing(f"cannot load {LIB_PATH}: {exc}") from exc
+        _declare(handle)
+        if handle.ft_abi_version() != ABI_VERSION:
+            raise LibraryMissing("libfieldtess_cuda.so ABI version mismatch")
+        _lib = handle
+    return _lib
+
+
+def last_error():
+    msg = lib().ft_last_error()
+    return msg.decode() if msg else ""

@@ -1,0 +1,626 @@
+"""Layered-field engine on the GPU: seeding, the fused Euler step, evolve.
+
+Public API identical to the reference (pkg/src/fieldtess/field.py:34-404):
+``CouplingParams``, ``StepStats``, ``LayeredField``, ``init_field``,
+``step``, ``evolve``, ``sharp_labels``, ``band_vertex_fraction``,
+``save_field`` / ``load_field``, ``StepWorkspace``, ``UNCLAIMED``.
+
+What changes underneath: the field lives in HBM as CSC (``DeviceCSC``) and
+one call of the C-ABI ``ft_step`` runs the whole pipeline of the reference
+step (spgemm -> skeleton -> expand -> update -> normalise/compact) as a
+single fused kernel; ``evolve`` runs its loop on the device (``ft_evolve``)
+with the convergence test evaluated there, reading statistics back once.
+
+Precision: ``"exact"`` (default) stores float64 and is bitwise identical to
+the reference; ``"fast"`` stores float32 and computes in float64.  Choose
+per field (``init_field(..., precision=)``) or globally with
+:func:`set_default_precision`.
+"""
+
+import ctypes
+import json
+from dataclasses import asdict, dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import (BackendError, DuplicateSeedError, NumericalBlowupError,
+                     PatternViolationError, ShapeError)
+from .sparse import INDEX, DeviceCSC, SparseMat
+
+UNCLAIMED = -1
+BASE_EXHAUSTION_PER_VERTEX = 1e-9       # field.py:31
+
+_PRECISIONS = ("exact", "fast")
+_default_precision = "exact"
+
+
+def set_default_precision(precision):
+    """Select the storage precision of new fields: "exact" | "fast"."""
+    global _default_precision
+    if precision not in _PRECISIONS:
+        raise ShapeError(f"precision must be one of {_PRECISIONS}")
+    _default_precision = precision
+
+
+def get_default_precision():
+    return _default_precision
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _value_dtype(precision):
+    torch = _torch()
+    return torch.float64 if precision == "exact" else torch.float32
+
+
+def _ft_dtype(precision):
+    return _lib.FT_F64 if precision == "exact" else _lib.FT_F32
+
+
+def _device():
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise BackendError("no CUDA device: the engine has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream_handle():
+    return ctypes.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+
+def _check(rc, where):
+    if rc != _lib.FT_OK:
+        msg = _lib.last_error()
+        if rc == _lib.FT_ERR_SHAPE:
+            raise ShapeError(msg or where)
+        raise BackendError(f"{where} failed (code {rc}): {msg}")
+
+
+# ---------------------------------------------------------------------------
+# parameter / statistics records
+
+
+@dataclass
+class CouplingParams:
+    """Scalar couplings of the update rule (field.py:34-71): pair penalty
+    ``w``, gradient coupling ``a``, band interaction ``e`` (``e_base`` against
+    the base layer), mobility ``mu`` and the Euler time step ``dt``."""
+
+    w: float = 0.2
+    a: float = 1.0
+    e: float = 0.3
+    e_base: float = 0.2
+    mu: float = 0.2
+    dt: float = 5.0
+
+    def validate(self):
+        if min(self.w, self.a, self.mu, self.dt) <= 0:
+            raise ShapeError("w, a, mu, dt must be positive")
+        if self.e < 0 or self.e_base < 0:
+            raise ShapeError("e, e_base must be non-negative")
+        return self
+
+    def to_dict(self):
+        return asdict(self)
+
+    @classmethod
+    def from_dict(cls, d):
+        return cls(**{k: float(v) for k, v in d.items()})
+
+    def ft_params(self):
+        return _lib.FtParams(float(self.w), float(self.a), float(self.e),
+                             float(self.e_base), float(self.mu), float(self.dt))
+
+
+@dataclass
+class StepStats:
+    """Per-step diagnostics (field.py:74-92).  The fused kernel has no
+    internal phase boundaries: its device time is reported in
+    ``spgemm_time`` (the other phase fields stay 0) so ``total_time`` is the
+    step time.  ``nnz_skel`` is the interest-skeleton size (layer-nnz
+    updates of the step)."""
+
+    max_delta: float
+    nnz_phi: int
+    base_mass: float
+    spgemm_time: float = 0.0
+    skeleton_time: float = 0.0
+    expand_time: float = 0.0
+    update_time: float = 0.0
+    normalize_time: float = 0.0
+    realloc_count: int = 0
+    converged: bool = False
+    nnz_skel: int = 0
+
+    @property
+    def total_time(self):
+        return (self.spgemm_time + self.skeleton_time + self.expand_time
+                + self.update_time + self.normalize_time)
+
+
+# ---------------------------------------------------------------------------
+# the field
+
+
+class LayeredField:
+    """The sparse multi-layer field: base layer row 0, cell c in row c+1.
+
+    ``phi`` is the host :class:`SparseMat` view (materialised lazily from the
+    device copy); the device CSC is created on first use.
+    """
+
+    def __init__(self, phi, seed_vertices, step_count=0, precision=None):
+        self._host = None
+        self._dev = None
+        if isinstance(phi, DeviceCSC):
+            self._dev = phi
+            torch = _torch()
+            self.precision = "exact" if phi.values.dtype == torch.float64 else "fast"
+        else:
+            self._host = phi
+            self.precision = precision or _default_precision
+        if self.precision not in _PRECISIONS:
+            raise ShapeError(f"precision must be one of {_PRECISIONS}")
+        self.seed_vertices = np.asarray(seed_vertices, dtype=np.int64)
+        self.step_count = int(step_count)
+
+    # storage ---------------------------------------------------------------
+
+    @property
+    def phi(self):
+        if self._host is None:
+            self._host = self._dev.to_host()
+        return self._host
+
+    @phi.setter
+    def phi(self, value):
+        self._host = value
+        self._dev = None
+
+    def device_phi(self):
+        """The device CSC of the field (uploaded on first use)."""
+        if self._dev is None:
+            self._dev = DeviceCSC.from_host(self._host, _value_dtype(self.precision), _device())
+        return self._dev
+
+    def _shape(self):
+        m = self._dev if self._dev is not None else self._host
+        return m.n_rows, m.n_cols
+
+    @property
+    def n_cells(self):
+        return self._shape()[0] - 1
+
+    @property
+    def n_vertices(self):
+        return self._shape()[1]
+
+    def copy(self):
+        out = LayeredField(self.phi.copy(), self.seed_vertices.copy(), self.step_count,
+                           precision=self.precision)
+        return out
+
+    def base_mass(self):
+        phi = self.phi
+        nnz = phi.nnz
+        return float(phi.values[:nnz][phi.row_idx[:nnz] == 0].sum())
+
+    def column_sums(self):
+        phi = self.phi
+        sums = np.zeros(self.n_vertices)
+        np.add.at(sums, phi.entry_columns(), phi.values[:phi.nnz])
+        return sums
+
+    def cell_row(self, cell):
+        if not 0 <= cell < self.n_cells:
+            raise ShapeError(f"cell {cell} out of range")
+        return cell + 1
+
+    def __repr__(self):
+        nnz = self._dev.nnz if self._dev is not None else self._host.nnz
+        return (f"LayeredField({self.n_cells} cells, {self.n_vertices} vertices, "
+                f"nnz={nnz}, steps={self.step_count}, {self.precision})")
+
+
+def init_field(mesh, seeds, precision=None):
+    """Seed the field: each seed claims itself plus its one-ring; vertices
+    claimed k times get 1/k per claimant; unclaimed vertices carry base 1.0
+    (field.py:137-166).  Vectorised: no per-seed Python loop."""
+    seeds = np.asarray(seeds, dtype=np.int64).ravel()
+    if seeds.size != np.unique(seeds).size:
+        raise DuplicateSeedError("duplicate-seed: seed list has repeats")
+    n_v = mesh.n_vertices
+    if seeds.size and (seeds.min() < 0 or seeds.max() >= n_v):
+        raise ShapeError("seed vertex index out of range")
+    nptr = np.asarray(mesh.neighbor_ptr, dtype=np.int64)
+    nidx = np.asarray(mesh.neighbor_idx, dtype=np.int64)
+    deg = nptr[seeds + 1] - nptr[seeds]
+    # claimed vertex list per seed: the seed, then its sorted one-ring
+    seg = np.cumsum(deg + 1) - (deg + 1)
+    total = int((deg + 1).sum())
+    cl_row = np.repeat(np.arange(1, seeds.size + 1, dtype=np.int64), deg + 1)
+    pos_in = np.arange(total, dtype=np.int64) - np.repeat(seg, deg + 1)
+    starts = np.repeat(nptr[seeds], deg + 1)
+    is_seed = pos_in == 0
+    cl_col = np.where(is_seed, np.repeat(seeds, deg + 1),
+                      nidx[np.minimum(starts + pos_in - 1, max(nidx.size - 1, 0))]
+                      if nidx.size else 0)
+    claims = np.bincount(cl_col, minlength=n_v)
+    per_col = np.where(claims == 0, 1, claims)
+    col_ptr = np.zeros(n_v + 1, dtype=np.int64)
+    np.cumsum(per_col, out=col_ptr[1:])
+    row_idx = np.zeros(int(col_ptr[-1]), dtype=INDEX)
+    vals = np.ones(int(col_ptr[-1]))
+    # claims sorted by (column, row); each lands at col_ptr[col] + rank
+    order = np.argsort(cl_col * np.int64(seeds.size + 1) + cl_row, kind="stable")
+    sc, sr = cl_col[order], cl_row[order]
+    rank = np.arange(sc.size, dtype=np.int64) - np.repeat(
+        np.cumsum(claims[claims > 0]) - claims[claims > 0], claims[claims > 0])
+    dst = col_ptr[sc] + rank
+    row_idx[dst] = sr
+    vals[dst] = 1.0 / claims[sc]
+    phi = SparseMat(seeds.size + 1, n_v, col_ptr.astype(INDEX), row_idx, vals, check=False)
+    return LayeredField(phi, seeds, precision=precision)
+
+
+# ---------------------------------------------------------------------------
+# device-side Laplacian and workspace
+
+
+class _DeviceLap:
+    def __init__(self, lap_t, flags, n_v):
+        self.lap_t = lap_t     # dict precision -> DeviceCSC
+        self.flags = flags
+        self.n_v = n_v
+
+
+def _uniform_values_exact(mat_t):
+    """True when L^T holds exactly the uniform weights: 1.0/deg(j) on the
+    off-diagonal of column j and -1.0 on its diagonal (mesh.py:392-400)."""
+    n = mat_t.n_cols
+    cp = np.asarray(mat_t.col_ptr, dtype=np.int64)
+    nnz = int(cp[-1])
+    rows = np.asarray(mat_t.row_idx[:nnz], dtype=np.int64)
+    vals = np.asarray(mat_t.values[:nnz], dtype=np.float64)
+    cols = np.repeat(np.arange(n, dtype=np.int64), np.diff(cp))
+    cnt = np.diff(cp)
+    if np.any(cnt < 2):
+        return False
+    diag = rows == cols
+    if np.bincount(cols[diag], minlength=n).max(initial=0) != 1 or diag.sum() != n:
+        return False
+    want = np.where(diag, -1.0, 1.0 / (cnt[cols] - 1).astype(np.float64))
+    return bool(np.array_equal(vals, want))
+
+
+def _with_diagonal(mat_t):
+    """L^T with an explicit (zero) diagonal entry wherever one is missing,
+    so the fused step always meets PHI(:, j) through u == j.  A zero weight
+    adds +0.0 to the accumulator, which leaves every nonzero Lt entry
+    bitwise unchanged."""
+    n = mat_t.n_cols
+    cp = np.asarray(mat_t.col_ptr, dtype=np.int64)
+    nnz = int(cp[-1])
+    rows = np.asarray(mat_t.row_idx[:nnz], dtype=np.int64)
+    cols = np.repeat(np.arange(n, dtype=np.int64), np.diff(cp))
+    has = np.zeros(n, dtype=bool)
+    has[cols[rows == cols]] = True
+    if has.all():
+        return mat_t
+    miss = np.flatnonzero(~has)
+    return SparseMat.from_triplets(mat_t.n_rows, n, np.concatenate([rows, miss]),
+                                   np.concatenate([cols, miss]),
+                                   np.concatenate([np.asarray(mat_t.values[:nnz]),
+                                                   np.zeros(miss.size)]))
+
+
+def device_laplacian(lap, precision):
+    """Upload ``lap.mat_t`` once per Laplacian object (cached on it)."""
+    key = (id(lap.mat_t), int(lap.mat_t.col_ptr[lap.mat_t.n_cols]))
+    cache = getattr(lap, "_ft_device", None)
+    if cache is None or cache[0] != key:
+        mat_t = _with_diagonal(lap.mat_t)
+        flags = _lib.FT_LAP_UNIFORM if _uniform_values_exact(mat_t) else _lib.FT_LAP_EXPLICIT
+        dl = _DeviceLap({}, flags, mat_t.n_cols)
+        dl.host = mat_t
+        cache = (key, dl)
+        try:
+            lap._ft_device = cache
+        except AttributeError:
+            pass
+    dl = cache[1]
+    if precision not in dl.lap_t:
+        dl.lap_t[precision] = DeviceCSC.from_host(dl.host, _value_dtype(precision), _device())
+    return dl
+
+
+class StepWorkspace:
+    """Reusable device buffers for the step pipeline: the look-back /
+    statistics workspace, the statistics record and a spare output CSC
+    (field.py:169-189).  With a shared workspace the input field's storage is
+    recycled as a later output (only the newest field stays valid)."""
+
+    def __init__(self):
+        self.ws = None
+        self.ws_n = -1
+        self.stats = None
+        self.spare = None
+        self.realloc_count = 0
+
+    def prepare(self, n_v, device):
+        torch = _torch()
+        if self.ws is None or self.ws_n != n_v:
+            nbytes = int(_lib.lib().ft_workspace_bytes(n_v))
+            self.ws = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+            self.ws_n = n_v
+        if self.stats is None:
+            self.stats = torch.zeros(_lib.STATS_BYTES, dtype=torch.uint8, device=device)
+
+    def take_output(self, like, capacity):
+        sp = self.spare
+        self.spare = None
+        if (sp is not None and sp is not like and sp.n_cols == like.n_cols
+                and sp.n_rows == like.n_rows and sp.values.dtype == like.values.dtype):
+            if sp.grow(capacity):
+                self.realloc_count += 1
+            return sp
+        return DeviceCSC.allocate(like.n_rows, like.n_cols, capacity, like.values.dtype,
+                                  like.values.device)
+
+
+def _initial_capacity(dphi):
+    # nnz can grow by one ring per step; leave ample headroom so overflow
+    # (which costs a re-run) is rare; growth is still by >= 1.2x
+    return max(2 * dphi.nnz + dphi.n_cols // 8, 1024)
+
+
+def _stats_from_bytes(buf):
+    return np.frombuffer(buf, dtype=_lib.STATS_DTYPE)
+
+
+def _raise_step_error(rec, field_step_count):
+    status = int(rec["status"])
+    if status == _lib.FT_STATUS_PATTERN:
+        raise PatternViolationError(
+            f"pattern-violation: nonzero at ({int(rec['bad_row'])}, {int(rec['bad_col'])}) "
+            "outside the skeleton")
+    if status == _lib.FT_STATUS_NAN:
+        raise NumericalBlowupError(int(rec["nan_col"]), field_step_count + 1)
+
+
+# ---------------------------------------------------------------------------
+# step / evolve
+
+
+def step(field, lap, params, workspace=None):
+    """One explicit Euler step; returns ``(new_field, StepStats)``
+    (field.py:198-286), executed as one fused GPU kernel."""
+    torch = _torch()
+    params.validate()
+    ws = workspace if workspace is not None else StepWorkspace()
+    n_v = field.n_vertices
+    if lap.mat.n_rows != n_v:
+        raise ShapeError("Laplacian size does not match field")
+    dphi = field.device_phi()
+    device = dphi.values.device
+    dl = device_laplacian(lap, field.precision)
+    ws.prepare(n_v, device)
+    out = ws.take_output(dphi, _initial_capacity(dphi))
+    reallocs = ws.realloc_count
+    ws.realloc_count = 0
+    lap_c = dl.lap_t[field.precision].ft_csc()
+    prm = params.ft_params()
+    stream = _stream_handle()
+    lib = _lib.lib()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    while True:
+        in_c = dphi.ft_csc()
+        out_c = out.ft_csc()
+        ev0.record()
+        rc = lib.ft_step(ctypes.byref(lap_c), dl.flags, ctypes.byref(in_c),
+                         ctypes.byref(out_c), _ft_dtype(field.precision),
+                         ctypes.byref(prm), ctypes.c_void_p(ws.ws.data_ptr()),
+                         ws.ws.numel(), ctypes.c_void_p(ws.stats.data_ptr()), stream)
+        ev1.record()
+        _check(rc, "ft_step")
+        rec = _stats_from_bytes(ws.stats.cpu().numpy().tobytes())[0]
+        if int(rec["status"]) == _lib.FT_STATUS_OVERFLOW:
+            out.grow(int(rec["nnz_phi"]))
+            reallocs += 1
+            continue
+        break
+    _raise_step_error(rec, field.step_count)
+    out.nnz = int(rec["nnz_phi"])
+    ws.spare = dphi if workspace is not None else None
+    new_field = LayeredField(out, field.seed_vertices, field.step_count + 1)
+    stats = StepStats(max_delta=float(rec["max_delta"]), nnz_phi=int(rec["nnz_phi"]),
+                      base_mass=float(rec["base_mass"]),
+                      spgemm_time=ev0.elapsed_time(ev1) * 1e-3,
+                      realloc_count=reallocs, nnz_skel=int(rec["nnz_skel"]))
+    return new_field, stats
+
+
+def evolve(field, lap, params, max_steps=1000, tol=1e-4, workspace=None, on_step=None):
+    """Step until converged or ``max_steps`` (field.py:289-321).
+
+    Converged: max_delta < tol and base mass < 1e-9 per vertex.  Without an
+    ``on_step`` callback the whole loop runs on the device (``ft_evolve``):
+    the stop test is evaluated by the GPU after every step and statistics are
+    read back once.  The caller's input field is never recycled.
+    """
+    if max_steps < 1:
+        raise ShapeError("max_steps must be >= 1")
+    params.validate()
+    ws = workspace if workspace is not None else StepWorkspace()
+    base_threshold = BASE_EXHAUSTION_PER_VERTEX * field.n_vertices
+    if on_step is not None:
+        return _evolve_host(field, lap, params, max_steps, tol, ws, on_step, base_threshold)
+    return _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold)
+
+
+def _evolve_host(field, lap, params, max_steps, tol, ws, on_step, base_threshold):
+    trace = []
+    cur = field
+    first = field.device_phi()
+    for _ in range(max_steps):
+        cur, st = step(cur, lap, params, workspace=ws)
+        if ws.spare is first:
+            ws.spare = None          # never recycle the caller's storage
+        on_step(cur, st)
+        st.converged = st.max_delta < tol and st.base_mass < base_threshold
+        trace.append(st)
+        if st.converged:
+            break
+    return cur, trace
+
+
+def _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold):
+    torch = _torch()
+    n_v = field.n_vertices
+    if lap.mat.n_rows != n_v:
+        raise ShapeError("Laplacian size does not match field")
+    src = field.device_phi()
+    device = src.values.device
+    dl = device_laplacian(lap, field.precision)
+    ws.prepare(n_v, device)
+    cap = _initial_capacity(src)
+    a = src.clone(capacity=cap)               # the caller's buffer stays intact
+    b = ws.take_output(src, cap)
+    trace_dev = torch.zeros(max_steps * _lib.STATS_BYTES, dtype=torch.uint8, device=device)
+    control = torch.zeros(4, dtype=torch.int64, device=device)
+    lap_c = dl.lap_t[field.precision].ft_csc()
+    prm = params.ft_params()
+    stream = _stream_handle()
+    lib = _lib.lib()
+    trace = []
+    done = 0
+    reallocs = 0
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    while True:
+        remaining = max_steps - done
+        a_c, b_c = a.ft_csc(), b.ft_csc()
+        ev0.record()
+        rc = lib.ft_evolve(ctypes.byref(lap_c), dl.flags, ctypes.byref(a_c), ctypes.byref(b_c),
+                           _ft_dtype(field.precision), ctypes.byref(prm), remaining,
+                           float(tol), float(base_threshold), ctypes.c_void_p(ws.ws.data_ptr()),
+                           ws.ws.numel(), ctypes.c_void_p(trace_dev.data_ptr()),
+                           ctypes.c_void_p(control.data_ptr()), stream)
+        ev1.record()
+        _check(rc, "ft_evolve")
+        ctl = control.cpu().numpy()
+        n, status = int(ctl[0]), int(ctl[1])
+        recs = _stats_from_bytes(trace_dev[:(n + 1) * _lib.STATS_BYTES].cpu().numpy().tobytes()
+                                 if n < remaining else
+                                 trace_dev[:n * _lib.STATS_BYTES].cpu().numpy().tobytes())
+        per_step = ev0.elapsed_time(ev1) * 1e-3 / max(n, 1)
+        for k in range(n):
+            r = recs[k]
+            trace.append(StepStats(max_delta=float(r["max_delta"]), nnz_phi=int(r["nnz_phi"]),
+                                   base_mass=float(r["base_mass"]), spgemm_time=per_step,
+                                   nnz_skel=int(r["nnz_skel"]),
+                                   converged=int(r["status"]) == _lib.FT_STATUS_CONVERGED))
+        cur, other = (a, b) if n % 2 == 0 else (b, a)
+        done += n
+        if n:
+            cur.nnz = int(recs[n - 1]["nnz_phi"])
+        if status == _lib.FT_STATUS_OVERFLOW:
+            other.grow(int(ctl[2]))
+            reallocs += 1
+            a, b = cur, other
+            continue
+        if status in (_lib.FT_STATUS_NAN, _lib.FT_STATUS_PATTERN):
+            _raise_step_error(recs[n], field.step_count + done)
+        break
+    if trace:
+        trace[-1].realloc_count = reallocs
+    ws.spare = other
+    return LayeredField(cur, field.seed_vertices, field.step_count + done), trace
+
+
+# ---------------------------------------------------------------------------
+# labels and small host utilities
+
+
+def sharp_labels(field):
+    """Per-vertex argmax cell id (ties -> lowest id); UNCLAIMED (-1) where
+    the base strictly dominates (field.py:324-356).  GPU kernel
+    ``ft_labels``; returns a host int64 array."""
+    torch = _torch()
+    dphi = field.device_phi()
+    labels = torch.empty(max(dphi.n_cols, 1), dtype=torch.int64, device=dphi.values.device)
+    c = dphi.ft_csc()
+    rc = _lib.lib().ft_labels(ctypes.byref(c), _ft_dtype(field.precision),
+                              ctypes.c_void_p(labels.data_ptr()), _stream_handle())
+    _check(rc, "ft_labels")
+    return labels[:dphi.n_cols].cpu().numpy()
+
+
+def band_vertex_fraction(field):
+    """Fraction of vertices carrying two or more cell layers (field.py:359-366)."""
+    phi = field.phi
+    nnz = phi.nnz
+    cols = phi.entry_columns()[phi.row_idx[:nnz] != 0]
+    counts = np.bincount(cols, minlength=phi.n_cols)
+    return float((counts >= 2).sum()) / max(phi.n_cols, 1)
+
+
+def save_field(field, params, path, extra_header=None):
+    """Snapshot: ``#FIELD {json}`` header, ``rows cols nnz``, then one
+    ``row col repr(value)`` line per entry (field.py:372-387)."""
+    header = {"seeds": [int(s) for s in field.seed_vertices],
+              "step_count": field.step_count, "params": params.to_dict()}
+    if extra_header:
+        header.update(extra_header)
+    phi = field.phi
+    nnz = phi.nnz
+    cols = phi.entry_columns()
+    with open(path, "w") as fh:
+        fh.write(f"#FIELD {json.dumps(header, sort_keys=True)}\n")
+        fh.write(f"{phi.n_rows} {phi.n_cols} {nnz}\n")
+        fh.writelines(f"{r} {c} {v!r}\n" for r, c, v in
+                      zip(phi.row_idx[:nnz].tolist(), cols.tolist(),
+                          phi.values[:nnz].tolist()))
+
+
+def load_field(path):
+    """Read a :func:`save_field` snapshot; returns ``(field, params)``."""
+    with open(path) as fh:
+        first = fh.readline()
+        if not first.startswith("#FIELD "):
+            raise ShapeError(f"{path}: not a field snapshot")
+        header = json.loads(first[len("#FIELD "):])
+        phi = read_triplets_stream(fh)
+    params = CouplingParams.from_dict(header["params"])
+    return LayeredField(phi, np.asarray(header["seeds"], dtype=np.int64),
+                        header.get("step_count", 0)), params
+
+
+def read_triplets_stream(fh):
+    header = None
+    rows, cols, vals = [], [], []
+    for lineno, raw in enumerate(fh, 2):
+        line = raw.strip()
+        if not line or line.startswith("#"):
+            continue
+        parts = line.split()
+        if len(parts) != 3:
+            raise ShapeError(f"line {lineno}: bad triplet {'header' if header is None else 'entry'}")
+        if header is None:
+            header = tuple(int(x) for x in parts)
+            continue
+        rows.append(int(parts[0]))
+        cols.append(int(parts[1]))
+        vals.append(float(parts[2]))
+    if header is None:
+        raise ShapeError("empty triplet file")
+    n_rows, n_cols, nnz = header
+    if len(rows) != nnz:
+        raise ShapeError(f"header says {nnz} entries, found {len(rows)}")
+    return SparseMat.from_triplets(n_rows, n_cols, rows, cols, vals)
+

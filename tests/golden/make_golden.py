@@ -1,0 +1,288 @@
+"""Generate golden fixtures by running the REFERENCE package in this container.
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py [--big]
+
+The reference (``fieldtess``, pure Python + numba) is imported from
+``oracle/_ref/py`` (pip-installed by ``make -C oracle ref``) or directly from
+``/root/reference/pkg/src``.  It does not exist on the GPU box, so every
+fixture the tests need is written here as a small ``.npz`` / ``.json`` and
+committed.  Nothing in the product imports this script.
+
+Fixtures
+--------
+step_cases.npz   single steps from the reference's own TestStepOracle inputs
+                 (test_field.py:80-122): star hand case, 6 random fields
+                 (rng 33), a 5-step torus 9x9 run, plus random params.
+c1_traj.npz      config C1: icosphere-4, 64 seeds (sample_seed_vertices rng 0),
+                 PHI snapshots at steps 0,1,2,10,100,500 and the stats trace.
+torus_traj.npz   torus 64x64, 24 seeds: snapshots at 0,1,60,300.
+labels.npz       sharp_labels on C1 snapshots + hand cases.
+seeds.json       sample_seed_vertices outputs (rng 0) for several meshes.
+meshes.json      SHA-256 digests of generator outputs (faces / positions /
+                 L^T arrays) for icosphere 0..7 and a few tori.
+c1_dual.json     dual-mesh products on C1 after 500 steps (API path).
+--big: c2_traj.npz (icosphere-7, 1024 seeds, steps 0/100/1000) and
+       c2_lloyd.json (5 Lloyd iterations, max_steps 1000).
+"""
+
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+for cand in (os.path.join(REPO, "oracle", "_ref", "py"), "/root/reference/pkg/src"):
+    if os.path.isdir(os.path.join(cand, "fieldtess")):
+        sys.path.insert(0, cand)
+        break
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+
+import fieldtess as ft  # noqa: E402  (the reference)
+from fieldtess.cli import sample_seed_vertices  # noqa: E402
+from fieldtess.field import LayeredField, StepWorkspace, step  # noqa: E402
+
+
+def csc_arrays(prefix, m):
+    nnz = m.nnz
+    return {f"{prefix}_shape": np.array([m.n_rows, m.n_cols], dtype=np.int64),
+            f"{prefix}_ptr": m.col_ptr.astype(np.int32).copy(),
+            f"{prefix}_idx": m.row_idx[:nnz].astype(np.int32).copy(),
+            f"{prefix}_val": m.values[:nnz].astype(np.float64).copy()}
+
+
+def params_array(p):
+    return np.array([p.w, p.a, p.e, p.e_base, p.mu, p.dt], dtype=np.float64)
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def star_mesh():
+    pos = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [-1, 0, 0], [0, -1, 0]], dtype=float)
+    faces = [[0, 1, 2], [0, 2, 3], [0, 3, 4], [0, 4, 1]]
+    return ft.TriMesh(pos, faces)
+
+
+def make_step_cases():
+    out = {}
+    cases = []
+    # star hand case (test_field.py:80-89)
+    mesh = star_mesh()
+    lap = ft.build_laplacian(mesh, "uniform")
+    phi = np.zeros((2, 5))
+    phi[1, 0] = 1.0
+    phi[1, 1] = 0.4
+    phi[0] = 1.0 - phi[1]
+    cases.append(("star", lap, phi, ft.CouplingParams()))
+    # random fields (test_field.py:91-107)
+    grid9 = ft.gen_periodic_grid(9, 9)
+    lap9 = ft.build_laplacian(grid9, "uniform")
+    rng = np.random.default_rng(33)
+    for trial in range(6):
+        n_cells = int(rng.integers(1, 5))
+        phi = np.zeros((n_cells + 1, 81))
+        for r in range(1, n_cells + 1):
+            support = rng.choice(81, size=rng.integers(3, 20), replace=False)
+            phi[r, support] = rng.random(support.size)
+        sums = phi.sum(axis=0)
+        phi[0] = np.maximum(1.0 - sums, 0.0)
+        phi /= phi.sum(axis=0, keepdims=True)
+        params = ft.CouplingParams(w=0.2, a=1.0, e=float(rng.uniform(0, 0.5)),
+                                   e_base=float(rng.uniform(0, 0.5)),
+                                   mu=float(rng.uniform(0.05, 0.4)),
+                                   dt=float(rng.uniform(1, 5)))
+        cases.append((f"rand{trial}", lap9, phi, params))
+    # many-cell dense-ish columns (exercise the wide-window path): 12 cells
+    rng = np.random.default_rng(5)
+    phi = np.zeros((13, 81))
+    for r in range(1, 13):
+        support = rng.choice(81, size=40, replace=False)
+        phi[r, support] = rng.random(support.size)
+    phi[0] = np.maximum(1.0 - phi.sum(axis=0), 0.0)
+    phi /= phi.sum(axis=0, keepdims=True)
+    cases.append(("wide12", lap9, phi, ft.CouplingParams()))
+    # cotan Laplacian on icosphere-2 with 5 seeds, a few steps in
+    ico2 = ft.gen_icosphere(2)
+    lapc = ft.build_laplacian(ico2, "cotan-clamped")
+    fld = ft.init_field(ico2, [0, 17, 40, 90, 130])
+    for _ in range(3):
+        fld, _ = step(fld, lapc, ft.CouplingParams())
+    cases.append(("cotan_ico2", lapc, fld.phi.to_dense(), ft.CouplingParams()))
+
+    names = []
+    for name, lap, phi, params in cases:
+        fld = LayeredField(ft.SparseMat.from_dense(phi), np.arange(phi.shape[0] - 1))
+        res, stats = step(fld, lap, params)
+        out.update(csc_arrays(f"{name}_in", fld.phi))
+        out.update(csc_arrays(f"{name}_lapt", lap.mat_t))
+        out.update(csc_arrays(f"{name}_out", res.phi))
+        out[f"{name}_params"] = params_array(params)
+        out[f"{name}_stats"] = np.array([stats.max_delta, stats.base_mass, stats.nnz_phi])
+        names.append(name)
+    # 5-step run on the 9x9 torus, seeds [20, 60] (test_field.py:109-122)
+    fld = ft.init_field(grid9, [20, 60])
+    out.update(csc_arrays("multi_in", fld.phi))
+    out.update(csc_arrays("multi_lapt", lap9.mat_t))
+    ws = StepWorkspace()
+    cur = fld
+    for _ in range(5):
+        cur, _ = step(cur, lap9, ft.CouplingParams(), workspace=ws)
+    out.update(csc_arrays("multi_out", cur.phi.copy()))
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "step_cases.npz"), **out)
+    print("step_cases:", names)
+
+
+def trajectory(mesh, seeds, snaps, path, max_step):
+    lap = ft.build_laplacian(mesh, "uniform")
+    fld = ft.init_field(mesh, seeds)
+    out = {"seeds": np.asarray(seeds, dtype=np.int64)}
+    out.update(csc_arrays("lapt", lap.mat_t))
+    out.update(csc_arrays("s0", fld.phi))
+    trace = []
+    ws = StepWorkspace()
+    cur = fld
+    t0 = time.time()
+    for k in range(1, max_step + 1):
+        cur, st = step(cur, lap, ft.CouplingParams(), workspace=ws)
+        trace.append((st.max_delta, st.base_mass, st.nnz_phi))
+        if k in snaps:
+            out.update(csc_arrays(f"s{k}", cur.phi.copy()))
+    out["snaps"] = np.array([0] + sorted(snaps), dtype=np.int64)
+    out["trace"] = np.array(trace)
+    out["labels_final"] = ft.sharp_labels(cur)
+    np.savez_compressed(path, **out)
+    print(os.path.basename(path), f"{time.time() - t0:.1f}s", "nnz", cur.phi.nnz)
+    return cur
+
+
+def make_labels_cases():
+    out = {}
+    cases = {
+        "argmax": ({0: {4: 0.9, 8: 0.1}}, 9, 2),
+        "base": ({0: {0: 1.0}}, 9, 1),
+        "tie": ({0: {3: 0.5, 6: 0.5}}, 9, 1),
+        "basetie": ({0: {0: 0.5, 2: 0.5}, 1: {0: 0.6, 1: 0.2, 3: 0.2}}, 4, 2),
+        "zeros": ({0: {0: 0.0, 1: 0.0}, 1: {}}, 3, 2),
+    }
+    for name, (columns, n_rows, n_cols) in cases.items():
+        dense = np.zeros((n_rows, n_cols))
+        for col, entries in columns.items():
+            for row, val in entries.items():
+                dense[row, col] = val
+        # keep explicit zeros like the reference test helpers would not:
+        m = ft.SparseMat.from_triplets(
+            n_rows, n_cols,
+            [r for c, e in columns.items() for r in e],
+            [c for c, e in columns.items() for _ in e],
+            [v for c, e in columns.items() for v in e.values()])
+        fld = LayeredField(m, np.arange(n_rows - 1))
+        out.update(csc_arrays(name, m))
+        out[f"{name}_labels"] = ft.sharp_labels(fld)
+    out["names"] = np.array(list(cases))
+    np.savez_compressed(os.path.join(HERE, "labels.npz"), **out)
+
+
+def make_seeds_and_meshes():
+    seeds = {}
+    meshes = {}
+    for name, mesh, count in [("ico4", ft.gen_icosphere(4), 64),
+                              ("ico5", ft.gen_icosphere(5), 300),
+                              ("torus64", ft.gen_periodic_grid(64, 64), 24),
+                              ("torus40x30", ft.gen_periodic_grid(40, 30), 50)]:
+        seeds[name] = sample_seed_vertices(mesh, count, 0).tolist()
+    for s in range(0, 8):
+        mesh = ft.gen_icosphere(s)
+        lap = ft.build_laplacian(mesh, "uniform")
+        meshes[f"ico{s}"] = {
+            "n_vertices": mesh.n_vertices, "n_faces": mesh.n_faces,
+            "faces": sha(mesh.faces.astype(np.int32)),
+            "positions": sha(mesh.positions.astype(np.float64)),
+            "lapt_ptr": sha(lap.mat_t.col_ptr.astype(np.int32)),
+            "lapt_idx": sha(lap.mat_t.row_idx[:lap.mat_t.nnz].astype(np.int32)),
+            "lapt_val": sha(lap.mat_t.values[:lap.mat_t.nnz].astype(np.float64)),
+            "face_area": sha(mesh.face_area.astype(np.float64)),
+            "vertex_area": sha(mesh.vertex_area.astype(np.float64)),
+        }
+    for nx, ny in [(3, 3), (9, 9), (64, 64), (40, 30), (200, 150)]:
+        mesh = ft.gen_periodic_grid(nx, ny)
+        lap = ft.build_laplacian(mesh, "uniform")
+        meshes[f"torus{nx}x{ny}"] = {
+            "n_vertices": mesh.n_vertices, "n_faces": mesh.n_faces,
+            "faces": sha(mesh.faces.astype(np.int32)),
+            "positions": sha(mesh.positions.astype(np.float64)),
+            "lapt_ptr": sha(lap.mat_t.col_ptr.astype(np.int32)),
+            "lapt_idx": sha(lap.mat_t.row_idx[:lap.mat_t.nnz].astype(np.int32)),
+            "lapt_val": sha(lap.mat_t.values[:lap.mat_t.nnz].astype(np.float64)),
+            "face_area": sha(mesh.face_area.astype(np.float64)),
+            "vertex_area": sha(mesh.vertex_area.astype(np.float64)),
+        }
+    with open(os.path.join(HERE, "seeds.json"), "w") as fh:
+        json.dump(seeds, fh)
+    with open(os.path.join(HERE, "meshes.json"), "w") as fh:
+        json.dump(meshes, fh, indent=1, sort_keys=True)
+    return seeds
+
+
+def make_c1_dual(fld, mesh):
+    from fieldtess import dual as dualmod
+    a_v = dualmod.vertex_adjacency(fld, 0.25)
+    a_t = dualmod.triangle_adjacency(fld, mesh, 0.25)
+    cur = dualmod.confirm_candidates(fld, mesh, a_v, a_t, 0.25)
+    dm = dualmod.build_dual(cur, np.zeros((fld.n_cells, 3)))
+    res = {
+        "a_v": sorted(map(list, a_v.pairs())),
+        "a_t": sorted(map(list, a_t.pairs())),
+        "curated": sorted(map(list, cur.pairs())),
+        "dropped": [[int(i), int(j), r] for i, j, r in cur.dropped],
+        "triples": sorted(map(list, cur.junction_triples)),
+        "triangles": sorted(map(sorted, dm.triangles.tolist())),
+        "spurious": [list(map(int, t)) for t in dm.spurious_removed],
+        "euler": int(dm.euler_characteristic()),
+    }
+    with open(os.path.join(HERE, "c1_dual.json"), "w") as fh:
+        json.dump(res, fh)
+    print("c1_dual: triangles", len(res["triangles"]), "euler", res["euler"])
+
+
+def make_c2(seeds_c2):
+    mesh = ft.gen_icosphere(7)
+    trajectory(mesh, seeds_c2, {100, 1000}, os.path.join(HERE, "c2_traj.npz"), 1000)
+    from fieldtess.lloyd import LloydState, lloyd_iterate
+    lap = ft.build_laplacian(mesh, "uniform")
+    t0 = time.time()
+    state = lloyd_iterate(LloydState(seeds=np.asarray(seeds_c2)), mesh, lap,
+                          ft.CouplingParams(), n_iter=5, max_steps=1000)
+    hist = [{k: rec[k] for k in ("iteration", "seeds", "area_variance", "steps",
+                                 "reseed_misses", "seed_collisions")}
+            for rec in state.history]
+    with open(os.path.join(HERE, "c2_lloyd.json"), "w") as fh:
+        json.dump({"history": hist, "wall_s": time.time() - t0}, fh)
+    print("c2_lloyd", f"{time.time() - t0:.1f}s")
+
+
+def main():
+    make_step_cases()
+    make_labels_cases()
+    seeds = make_seeds_and_meshes()
+    ico4 = ft.gen_icosphere(4)
+    c1 = trajectory(ico4, seeds["ico4"], {1, 2, 10, 100, 500},
+                    os.path.join(HERE, "c1_traj.npz"), 500)
+    make_c1_dual(c1, ico4)
+    trajectory(ft.gen_periodic_grid(64, 64), seeds["torus64"], {1, 60, 300},
+               os.path.join(HERE, "torus_traj.npz"), 300)
+    if "--big" in sys.argv:
+        mesh = ft.gen_icosphere(7)
+        seeds_c2 = sample_seed_vertices(mesh, 1024, 0)
+        with open(os.path.join(HERE, "seeds_c2.json"), "w") as fh:
+            json.dump(seeds_c2.tolist(), fh)
+        make_c2(seeds_c2)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,206 @@
+"""Parity of the CUDA hot path (through the public API -> C-ABI) against the
+reference's golden vectors and the C oracle.  EXACT mode must be bitwise."""
+
+import numpy as np
+import pytest
+
+import paper_1804_09152_b200 as ft
+from conftest import P, assert_csc_equal, csc_from, golden_npz
+from oracle import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+DEFAULT = ft.CouplingParams()
+
+
+def as_sparse(c):
+    return ft.SparseMat(c.n_rows, c.n_cols, c.col_ptr, c.row_idx, c.values, check=False)
+
+
+class _Lap:
+    """Minimal Laplacian-like object (duck-typed like the reference's)."""
+
+    def __init__(self, lapt):
+        self.mat_t = as_sparse(lapt)
+        self.mat = ft.transpose(self.mat_t)
+        self.scheme = "given"
+
+
+@pytest.fixture(scope="module")
+def cases():
+    return golden_npz("step_cases.npz")
+
+
+def test_step_cases_bitwise(cases):
+    for name in cases["names"]:
+        prm = ft.CouplingParams(*[float(x) for x in cases[f"{name}_params"]])
+        inp = csc_from(cases, f"{name}_in")
+        fld = ft.LayeredField(as_sparse(inp), np.arange(inp.n_rows - 1))
+        out, st = ft.step(fld, _Lap(csc_from(cases, f"{name}_lapt")), prm)
+        assert_csc_equal(out.phi, csc_from(cases, f"{name}_out"))
+        ref = cases[f"{name}_stats"]
+        assert st.max_delta == ref[0], name
+        assert abs(st.base_mass - ref[1]) <= 1e-12 * max(1.0, abs(ref[1])), name
+        assert st.nnz_phi == ref[2]
+
+
+def test_multi_step_with_workspace(cases):
+    inp = csc_from(cases, "multi_in")
+    lap = _Lap(csc_from(cases, "multi_lapt"))
+    cur = ft.LayeredField(as_sparse(inp), [20, 60])
+    ws = ft.StepWorkspace()
+    for _ in range(5):
+        cur, _ = ft.step(cur, lap, DEFAULT, workspace=ws)
+    assert_csc_equal(cur.phi, csc_from(cases, "multi_out"))
+
+
+@pytest.mark.parametrize("traj", ["c1_traj.npz", "torus_traj.npz"])
+def test_trajectory_bitwise_device_evolve(traj):
+    t = golden_npz(traj)
+    lap = _Lap(csc_from(t, "lapt"))
+    cur = ft.LayeredField(as_sparse(csc_from(t, "s0")), t["seeds"])
+    prev = 0
+    all_stats = []
+    for k in t["snaps"][1:]:
+        cur, trace = ft.evolve(cur, lap, DEFAULT, max_steps=int(k) - prev, tol=0.0)
+        assert len(trace) == int(k) - prev
+        all_stats += trace
+        prev = int(k)
+        assert cur.step_count == prev
+        assert_csc_equal(cur.phi, csc_from(t, f"s{k}"))
+    tr = t["trace"]
+    for k, st in enumerate(all_stats):
+        assert st.max_delta == tr[k, 0] and st.nnz_phi == tr[k, 2], k
+        assert abs(st.base_mass - tr[k, 1]) <= 1e-12 * max(1.0, tr[k, 1]), k
+    assert np.array_equal(ft.sharp_labels(cur), t["labels_final"])
+
+
+def test_trajectory_bitwise_step_loop():
+    t = golden_npz("c1_traj.npz")
+    lap = _Lap(csc_from(t, "lapt"))
+    cur = ft.LayeredField(as_sparse(csc_from(t, "s0")), t["seeds"])
+    ws = ft.StepWorkspace()
+    for k in range(1, 101):
+        cur, st = ft.step(cur, lap, DEFAULT, workspace=ws)
+        assert st.nnz_phi == t["trace"][k - 1, 2]
+        if k in t["snaps"]:
+            assert_csc_equal(cur.phi, csc_from(t, f"s{k}"))
+
+
+def test_generated_mesh_and_seeding_end_to_end():
+    """Product generators + seeding + device evolve == C oracle, bitwise."""
+    mesh = ft.gen_periodic_grid(200, 150)
+    lap = ft.build_laplacian(mesh)
+    rng = np.random.default_rng(3)
+    seeds = rng.choice(mesh.n_vertices, size=120, replace=False)
+    fld = ft.init_field(mesh, seeds)
+    out, trace = ft.evolve(fld, lap, DEFAULT, max_steps=40, tol=0.0)
+    ref, rtrace = po.evolve_c(po.Csc.of(fld.phi), po.Csc.of(lap.mat_t), DEFAULT, 40, n_threads=4)
+    assert_csc_equal(out.phi, ref)
+    assert [s.max_delta for s in trace] == [s["max_delta"] for s in rtrace]
+
+
+def test_fast_mode_single_step_tolerance():
+    """FAST (fp32 storage) from identical inputs: |d| <= 1e-5|ref| + 2e-7."""
+    t = golden_npz("c1_traj.npz")
+    lap = _Lap(csc_from(t, "lapt"))
+    for k in (10, 100):
+        inp = csc_from(t, f"s{k}")
+        f32 = ft.LayeredField(as_sparse(inp), t["seeds"], precision="fast")
+        out, _ = ft.step(f32, lap, DEFAULT)
+        # oracle fed the same fp32-rounded input
+        rounded = po.Csc(inp.n_rows, inp.n_cols, inp.col_ptr, inp.row_idx,
+                         inp.values.astype(np.float32).astype(np.float64))
+        ref, _ = po.step_c(rounded, csc_from(t, "lapt"), DEFAULT)
+        got = out.phi.to_dense()
+        want = ref.to_dense()
+        assert np.all(np.abs(got - want) <= 1e-5 * np.abs(want) + 2e-7)
+
+
+def test_fast_mode_trajectory_labels():
+    t = golden_npz("c1_traj.npz")
+    lap = _Lap(csc_from(t, "lapt"))
+    cur = ft.LayeredField(as_sparse(csc_from(t, "s0")), t["seeds"], precision="fast")
+    cur, _ = ft.evolve(cur, lap, DEFAULT, max_steps=500, tol=0.0)
+    agree = np.mean(ft.sharp_labels(cur) == t["labels_final"])
+    assert agree >= 0.9999
+
+
+def test_labels_golden():
+    g = golden_npz("labels.npz")
+    for name in g["names"]:
+        c = csc_from(g, name)
+        fld = ft.LayeredField(as_sparse(c), np.arange(c.n_rows - 1))
+        assert np.array_equal(ft.sharp_labels(fld), g[f"{name}_labels"]), name
+
+
+def test_numerical_blowup_reported():
+    mesh = ft.gen_periodic_grid(9, 9)
+    fld = ft.init_field(mesh, [40])
+    with pytest.raises(ft.errors.NumericalBlowupError, match="numerical-blowup") as ei:
+        ft.step(fld, ft.build_laplacian(mesh), ft.CouplingParams(a=float("inf")))
+    ref_cols = []
+    out, st = po.step_c(po.Csc.of(fld.phi), po.Csc.of(ft.build_laplacian(mesh).mat_t),
+                        ft.CouplingParams(a=float("inf")))
+    assert ei.value.column == st["nan_col"] and ei.value.step == 1
+    del ref_cols, out
+
+
+def test_pattern_violation_reported():
+    mesh = ft.gen_periodic_grid(6, 6)
+    dense = np.zeros((2, 36))
+    dense[0] = 1.0
+    dense[1, 5] = -0.25
+    fld = ft.LayeredField(ft.SparseMat.from_dense(dense), [5])
+    with pytest.raises(ft.errors.PatternViolationError, match="pattern-violation"):
+        ft.step(fld, ft.build_laplacian(mesh), DEFAULT)
+
+
+def test_overflow_regrows_and_matches(monkeypatch):
+    """A deliberately tiny output buffer must be grown and the step redone."""
+    from paper_1804_09152_b200 import field as fmod
+    monkeypatch.setattr(fmod, "_initial_capacity", lambda d: 8)
+    t = golden_npz("c1_traj.npz")
+    lap = _Lap(csc_from(t, "lapt"))
+    inp = as_sparse(csc_from(t, "s10"))
+    fld = ft.LayeredField(inp, t["seeds"], step_count=10)
+    out, st = ft.step(fld, lap, DEFAULT)
+    assert st.realloc_count >= 1
+    ref, _ = po.step_c(po.Csc.of(inp), csc_from(t, "lapt"), DEFAULT)
+    assert_csc_equal(out.phi, ref)
+    # and inside the device evolve loop
+    out2, trace = ft.evolve(fld, lap, DEFAULT, max_steps=20, tol=0.0)
+    ref2, _ = po.evolve_c(po.Csc.of(inp), csc_from(t, "lapt"), DEFAULT, 20)
+    assert_csc_equal(out2.phi, ref2)
+
+
+def test_converged_input_returns_after_one_step():
+    mesh = ft.gen_periodic_grid(9, 9)
+    lap = ft.build_laplacian(mesh)
+    dense = np.zeros((2, 81))
+    dense[1] = 1.0
+    fld = ft.LayeredField(ft.SparseMat.from_dense(dense), [0])
+    out, trace = ft.evolve(fld, lap, DEFAULT, max_steps=50)
+    assert len(trace) == 1 and trace[0].converged and trace[0].max_delta == 0.0
+    assert np.array_equal(out.phi.to_dense(), dense)
+
+
+def test_evolve_input_stays_valid_and_on_step():
+    mesh = ft.gen_periodic_grid(9, 9)
+    lap = ft.build_laplacian(mesh)
+    fld = ft.init_field(mesh, [40])
+    before = fld.phi.to_dense()
+    seen = []
+    out, trace = ft.evolve(fld, lap, DEFAULT, max_steps=30, on_step=lambda f, s: seen.append(f.step_count))
+    assert seen == list(range(1, 31)) and len(trace) == 30
+    assert np.array_equal(fld.phi.to_dense(), before)
+    out2, _ = ft.evolve(fld, lap, DEFAULT, max_steps=30)
+    assert np.array_equal(out.phi.to_dense(), out2.phi.to_dense())
+
+
+def test_four_symmetric_seeds_exhaust_base():
+    mesh = ft.gen_periodic_grid(50, 50)
+    lap = ft.build_laplacian(mesh)
+    seeds = [50 * 12 + 12, 50 * 12 + 37, 50 * 37 + 12, 50 * 37 + 37]
+    out, trace = ft.evolve(ft.init_field(mesh, seeds), lap, DEFAULT, max_steps=2500)
+    assert trace[-1].converged and trace[-1].base_mass < 1e-9 * mesh.n_vertices
