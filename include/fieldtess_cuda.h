@@ -5,23 +5,29 @@
  * `fieldtess` (arXiv 1804.09152).  The reference has no native code: its
  * compute layer is a set of numba kernels that take raw numpy arrays and
  * write into caller-preallocated outputs, signalling errors through flag
- * arrays (`fieldtess/_kernels.py`).  Every entry point below replaces one
+ * arrays (`fieldtess/_kernels.py`).  Each entry point below replaces one
  * stage of that pipeline (citations are `path:line` under the reference's
  * `pkg/src/fieldtess/`).
  *
  * Conventions
  *   - `extern "C"`, plain pointers and sizes, no exceptions cross the ABI.
- *   - All matrices are CSC exactly as the reference stores them
+ *   - Canonical matrices are CSC exactly as the reference stores them
  *     (`sparse.py:27-57`): int32 `col_ptr[n_cols+1]`, int32 `row_idx[cap]`,
  *     values `double` (FT_F64) or `float` (FT_F32).  The layered field PHI is
  *     (n_cells+1) x n_vertices: column = vertex, row 0 = base layer,
  *     row r = cell r-1 (`field.py:95-130`).
+ *   - Between Euler steps the engine keeps PHI "tiled" (ft_tiled): column
+ *     j is addressed by a descriptor (start, count) and the entries of each
+ *     128-vertex tile sit in that tile's fixed slot (or in a shared pool when
+ *     the slot is full).  This removes every inter-CTA dependency from the
+ *     step; canonical CSC is produced by ft_compact at the API boundary.
  *   - The Laplacian is passed as `lap.mat_t` (L^T in CSC), which is
  *     byte-identical to L in CSR with ascending neighbour index including
  *     the diagonal (`mesh.py:379-431`).
- *   - Every pointer argument except the host-side `ft_params*` is DEVICE
- *     memory owned by the caller.  Calls only enqueue work on `stream`
- *     (a `cudaStream_t`, passed as void*); results are read by the caller.
+ *   - Every pointer argument except the host-side `ft_params*` and the
+ *     descriptor structs themselves is DEVICE memory owned by the caller.
+ *     Calls only enqueue work on `stream` (a `cudaStream_t`, passed as
+ *     void*); results are read back by the caller.
  *   - Return value: FT_OK or an FT_ERR_* code; `ft_last_error()` returns a
  *     thread-local message for the last failure.
  */
@@ -35,14 +41,14 @@
 extern "C" {
 #endif
 
-#define FT_ABI_VERSION 1
+#define FT_ABI_VERSION 2
 
 /* return codes (mapped onto the reference's TessError subclasses,
  * `errors.py:9-75`, by the Python host layer) */
 #define FT_OK              0
 #define FT_ERR_SHAPE       1  /* ShapeError                                  */
 #define FT_ERR_NUMERICAL   2  /* NumericalBlowupError(column, step)          */
-#define FT_ERR_CAPACITY    3  /* output capacity too small: grow >=1.2x, retry
+#define FT_ERR_CAPACITY    3  /* output capacity too small: grow, retry
                                  (ensure_capacity, sparse.py:212-232)        */
 #define FT_ERR_CUDA        4  /* CUDA runtime failure                        */
 #define FT_ERR_PATTERN     5  /* PatternViolationError (sparse.py:389-394)   */
@@ -58,20 +64,22 @@ extern "C" {
                               -1.0 on the diagonal (mesh.py:392-400): they are
                               recomputed in registers and never read          */
 
-/* device status codes written into ft_step_stats.status */
-#define FT_STATUS_OK        0
-#define FT_STATUS_NAN       1
-#define FT_STATUS_PATTERN   2
-#define FT_STATUS_OVERFLOW  3
-#define FT_STATUS_CONVERGED 4
-#define FT_STATUS_MAXSTEPS  5
+/* status codes written into ft_step_stats.status / evolve control[1] */
+#define FT_STATUS_OK           0
+#define FT_STATUS_NAN          1   /* NumericalBlowupError                    */
+#define FT_STATUS_PATTERN      2   /* PatternViolationError                   */
+#define FT_STATUS_OVERFLOW     3   /* tiled work buffer too small             */
+#define FT_STATUS_CONVERGED    4
+#define FT_STATUS_MAXSTEPS     5
+#define FT_STATUS_OUT_OVERFLOW 6   /* canonical output too small: grow it and
+                                      call ft_compact                         */
 
 /* CouplingParams (field.py:34-71).  Host memory. */
 typedef struct {
     double w, a, e, e_base, mu, dt;
 } ft_params;
 
-/* Sparse matrix in CSC.  `values` dtype given by the call's dtype argument. */
+/* Canonical CSC.  `values` dtype given by the call's dtype argument. */
 typedef struct {
     int32_t  n_rows;
     int32_t  n_cols;
@@ -80,6 +88,18 @@ typedef struct {
     void*    values;      /* [capacity] double or float                   */
     int64_t  capacity;
 } ft_csc;
+
+/* Tiled working layout of a field (see Conventions).  desc[2j] = start,
+ * desc[2j+1] = count of column j; entries [0, n_tiles*slot) are the tile
+ * slots, [n_tiles*slot, capacity) the overflow pool. */
+typedef struct {
+    int32_t  n_rows;
+    int32_t  n_cols;
+    int32_t* desc;        /* [2*n_cols], 8-byte aligned                   */
+    int32_t* row_idx;     /* [capacity]                                   */
+    void*    values;      /* [capacity]                                   */
+    int64_t  capacity;
+} ft_tiled;
 
 /* One step's statistics, device resident.  Mirrors StepStats
  * (field.py:74-92) plus the error flags the reference signals through
@@ -95,60 +115,73 @@ typedef struct {
     int32_t bad_row;          /* offending row in `bad_col`                  */
     int32_t bad_is_lt;        /* 0: violation in PHI, 1: in Lt               */
     int32_t step;             /* 1-based step index within the call         */
-    int64_t reserved;
+    int64_t needed;           /* capacity needed when status is an overflow  */
 } ft_step_stats;
 
 /* -- library ------------------------------------------------------------- */
 int         ft_abi_version(void);
 const char* ft_last_error(void);
 
-/* Bytes of the per-field-size scratch `workspace` (tile status words,
- * tile partial sums, device control block).  The workspace must be zeroed
- * once with ft_workspace_init before first use and is then reused by every
- * ft_step / ft_evolve call with the same n_vertices. */
+/* Scratch `workspace` for a field of n_vertices columns (device control
+ * block, per-tile partial sums, compaction scan space).  Zero it once with
+ * ft_workspace_init; then reuse it for every call on fields of that size. */
 size_t ft_workspace_bytes(int32_t n_vertices);
 int    ft_workspace_init(void* workspace, size_t bytes, void* stream);
 
+/* Entries reserved per tile slot, and the smallest legal ft_tiled capacity
+ * for n_vertices columns (slots only, empty pool). */
+int64_t ft_tile_slot_entries(void);
+int64_t ft_tiled_min_capacity(int32_t n_vertices);
+
 /* -- the fused Euler step ------------------------------------------------ */
-/* One explicit Euler step PHI_out = step(PHI_in) in a single fused pass.
- * Replaces the whole pipeline of field.step (field.py:198-286):
+/* One explicit Euler step, canonical in -> canonical out.  Replaces the
+ * whole pipeline of field.step (field.py:198-286):
  *   sparse.spgemm (sparse.py:279-330; _kernels.py:14-74)      Lt = PHI L^T
  *   sparse.build_skeleton (sparse.py:345-371; _kernels.py:96-150)
  *   sparse.expand_to_skeleton x2 (sparse.py:374-396; _kernels.py:153-176)
  *   _kernels.update_kernel (_kernels.py:179-238)
  *   _kernels.column_sums_counts + normalize_compact (_kernels.py:241-282)
- * `stats` (device, one record) receives the statistics.  If the output
- * does not fit `out->capacity`, stats->status = FT_STATUS_OVERFLOW and
- * stats->nnz_phi holds the required size (the input is left intact). */
-int ft_step(const ft_csc* lap_t, int32_t lap_flags,
-            const ft_csc* phi_in, ft_csc* phi_out, int32_t dtype,
+ * as one fused kernel into the tiled `scratch`, then ft_compact into
+ * `phi_out`.  `stats` (device, one record) receives the statistics; on
+ * FT_STATUS_OVERFLOW (scratch) / FT_STATUS_OUT_OVERFLOW (phi_out)
+ * stats->needed holds the required capacity and the input is intact. */
+int ft_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
+            ft_tiled* scratch, ft_csc* phi_out, int32_t dtype,
             const ft_params* params, void* workspace, size_t ws_bytes,
             ft_step_stats* stats, void* stream);
 
-/* The two halves of ft_step, for callers that time the fused kernel on its
- * own (bench.py): ft_step_kernel enqueues only the fused kernel (statistics
- * stay in the workspace accumulators), ft_step_finalize reduces them into
- * `stats` and resets the accumulators.  ft_step == kernel + finalize. */
+/* The fused kernel alone (bench.py times it with CUDA events): one step
+ * from `in_canon` (if non-null) or `in_tiled` into the tiled `out`.
+ * Statistics accumulate in the workspace until ft_step_finalize reduces
+ * them into `stats` and resets the accumulators. */
 int ft_step_kernel(const ft_csc* lap_t, int32_t lap_flags,
-                   const ft_csc* phi_in, ft_csc* phi_out, int32_t dtype,
-                   const ft_params* params, void* workspace, size_t ws_bytes,
-                   void* stream);
+                   const ft_csc* in_canon, const ft_tiled* in_tiled,
+                   ft_tiled* out, int32_t dtype, const ft_params* params,
+                   void* workspace, size_t ws_bytes, void* stream);
 int ft_step_finalize(void* workspace, size_t ws_bytes, int32_t n_vertices,
-                     ft_step_stats* stats, void* stream);
+                     int64_t tiled_capacity, ft_step_stats* stats, void* stream);
 
-/* Up to `max_steps` steps alternating between buffers a and b (a holds the
- * input), stopping on the device as soon as a step converges
- * (max_delta < tol and base_mass < base_threshold; field.py:316-317), or on
- * NaN / pattern violation / capacity overflow.  Replaces the loop of
- * field.evolve (field.py:289-321).  `trace` (device, max_steps records)
- * receives one ft_step_stats per executed step; `control` (device, 4 x
- * int64) receives {steps_done, status, needed_capacity, reserved}.
- * The call is asynchronous and captured into CUDA graphs internally. */
-int ft_evolve(const ft_csc* lap_t, int32_t lap_flags,
-              ft_csc* phi_a, ft_csc* phi_b, int32_t dtype,
-              const ft_params* params, int32_t max_steps, double tol,
-              double base_threshold, void* workspace, size_t ws_bytes,
-              ft_step_stats* trace, int64_t* control, void* stream);
+/* Tiled -> canonical CSC (device-wide scan of column counts, then a
+ * coalesced copy).  stats->nnz_phi / needed / status report the result
+ * (FT_STATUS_OUT_OVERFLOW when dst is too small). */
+int ft_compact(const ft_tiled* src, ft_csc* dst, int32_t dtype, void* workspace,
+               size_t ws_bytes, ft_step_stats* stats, void* stream);
+
+/* Up to `max_steps` steps from the canonical `phi_in`, ping-ponging between
+ * the tiled buffers a (odd steps) and b (even steps), stopping on the
+ * device as soon as a step converges (max_delta < tol and base_mass <
+ * base_threshold; field.py:316-317) or fails (NaN / pattern violation /
+ * tiled overflow).  The last good field is then compacted into `phi_out`.
+ * Replaces the loop of field.evolve (field.py:289-321).
+ * `trace` (device, max_steps records) receives one ft_step_stats per
+ * executed step (plus the failing one); `control` (device, 4 x int64)
+ * receives {steps_done, status, needed_capacity, compacted(0/1)}. */
+int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
+              ft_tiled* work_a, ft_tiled* work_b, ft_csc* phi_out,
+              int32_t dtype, const ft_params* params, int32_t max_steps,
+              double tol, double base_threshold, void* workspace,
+              size_t ws_bytes, ft_step_stats* trace, int64_t* control,
+              void* stream);
 
 /* -- labels -------------------------------------------------------------- */
 /* Per-vertex argmax cell id; ties -> lowest cell; the base row wins only

@@ -31,8 +31,9 @@ FT_STATUS_PATTERN = 2
 FT_STATUS_OVERFLOW = 3
 FT_STATUS_CONVERGED = 4
 FT_STATUS_MAXSTEPS = 5
+FT_STATUS_OUT_OVERFLOW = 6
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class FtParams(ctypes.Structure):
@@ -47,13 +48,19 @@ class FtCsc(ctypes.Structure):
                 ("values", ctypes.c_void_p), ("capacity", ctypes.c_int64)]
 
 
+class FtTiled(ctypes.Structure):
+    _fields_ = [("n_rows", ctypes.c_int32), ("n_cols", ctypes.c_int32),
+                ("desc", ctypes.c_void_p), ("row_idx", ctypes.c_void_p),
+                ("values", ctypes.c_void_p), ("capacity", ctypes.c_int64)]
+
+
 class FtStepStats(ctypes.Structure):
     _fields_ = [("max_delta", ctypes.c_double), ("base_mass", ctypes.c_double),
                 ("nnz_phi", ctypes.c_int64), ("nnz_skel", ctypes.c_int64),
                 ("status", ctypes.c_int32), ("nan_col", ctypes.c_int32),
                 ("bad_col", ctypes.c_int32), ("bad_row", ctypes.c_int32),
                 ("bad_is_lt", ctypes.c_int32), ("step", ctypes.c_int32),
-                ("reserved", ctypes.c_int64)]
+                ("needed", ctypes.c_int64)]
 
 
 STATS_BYTES = ctypes.sizeof(FtStepStats)
@@ -67,12 +74,13 @@ STATS_DTYPE = _np.dtype([("max_delta", "<f8"), ("base_mass", "<f8"),
                          ("status", "<i4"), ("nan_col", "<i4"),
                          ("bad_col", "<i4"), ("bad_row", "<i4"),
                          ("bad_is_lt", "<i4"), ("step", "<i4"),
-                         ("reserved", "<i8")])
+                         ("needed", "<i8")])
 assert STATS_DTYPE.itemsize == STATS_BYTES
 
 # every symbol include/fieldtess_cuda.h declares
 EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
-           "ft_workspace_init", "ft_step", "ft_step_kernel", "ft_step_finalize",
+           "ft_workspace_init", "ft_tile_slot_entries", "ft_tiled_min_capacity",
+           "ft_step", "ft_step_kernel", "ft_step_finalize", "ft_compact",
            "ft_evolve", "ft_labels")
 
 _lib = None
@@ -91,19 +99,26 @@ def _declare(lib):
     lib.ft_workspace_bytes.restype = ctypes.c_size_t
     lib.ft_workspace_init.argtypes = [vp, ctypes.c_size_t, vp]
     lib.ft_workspace_init.restype = ctypes.c_int
-    lib.ft_step.argtypes = [P(FtCsc), ctypes.c_int32, P(FtCsc), P(FtCsc),
-                            ctypes.c_int32, P(FtParams), vp, ctypes.c_size_t,
-                            vp, vp]
+    lib.ft_tile_slot_entries.restype = ctypes.c_int64
+    lib.ft_tiled_min_capacity.argtypes = [ctypes.c_int32]
+    lib.ft_tiled_min_capacity.restype = ctypes.c_int64
+    lib.ft_step.argtypes = [P(FtCsc), ctypes.c_int32, P(FtCsc), P(FtTiled), P(FtCsc),
+                            ctypes.c_int32, P(FtParams), vp, ctypes.c_size_t, vp, vp]
     lib.ft_step.restype = ctypes.c_int
-    lib.ft_step_kernel.argtypes = [P(FtCsc), ctypes.c_int32, P(FtCsc), P(FtCsc),
-                                   ctypes.c_int32, P(FtParams), vp, ctypes.c_size_t, vp]
+    lib.ft_step_kernel.argtypes = [P(FtCsc), ctypes.c_int32, P(FtCsc), P(FtTiled),
+                                   P(FtTiled), ctypes.c_int32, P(FtParams), vp,
+                                   ctypes.c_size_t, vp]
     lib.ft_step_kernel.restype = ctypes.c_int
-    lib.ft_step_finalize.argtypes = [vp, ctypes.c_size_t, ctypes.c_int32, vp, vp]
+    lib.ft_step_finalize.argtypes = [vp, ctypes.c_size_t, ctypes.c_int32, ctypes.c_int64,
+                                     vp, vp]
     lib.ft_step_finalize.restype = ctypes.c_int
-    lib.ft_evolve.argtypes = [P(FtCsc), ctypes.c_int32, P(FtCsc), P(FtCsc),
-                              ctypes.c_int32, P(FtParams), ctypes.c_int32,
-                              ctypes.c_double, ctypes.c_double, vp,
-                              ctypes.c_size_t, vp, vp, vp]
+    lib.ft_compact.argtypes = [P(FtTiled), P(FtCsc), ctypes.c_int32, vp, ctypes.c_size_t,
+                               vp, vp]
+    lib.ft_compact.restype = ctypes.c_int
+    lib.ft_evolve.argtypes = [P(FtCsc), ctypes.c_int32, P(FtCsc), P(FtTiled), P(FtTiled),
+                              P(FtCsc), ctypes.c_int32, P(FtParams), ctypes.c_int32,
+                              ctypes.c_double, ctypes.c_double, vp, ctypes.c_size_t,
+                              vp, vp, vp]
     lib.ft_evolve.restype = ctypes.c_int
     lib.ft_labels.argtypes = [P(FtCsc), ctypes.c_int32, vp, vp]
     lib.ft_labels.restype = ctypes.c_int

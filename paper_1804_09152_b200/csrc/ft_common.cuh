@@ -5,46 +5,57 @@
 
 #include "fieldtess_cuda.h"
 
-#define FT_TPB 256              // threads per CTA of the per-vertex kernels
+#define FT_TPB 128              // threads (= vertex columns) per CTA tile
 #define FT_WARPS (FT_TPB / 32)
+#define FT_SLOT_PER_VERTEX 2    // tile slot entries per vertex column
+#define FT_SLOT (FT_TPB * FT_SLOT_PER_VERTEX)
+#define FT_CCH 2048             // columns per compaction chunk
+#define FT_CTPB 256             // threads of the compaction kernels
 
 namespace ft {
 
 // Device control block at the head of the workspace.  Accumulators are
-// "zero = neutral" so a plain memset initialises them, and the finalize
-// kernel re-zeroes them after every step.
+// "zero = neutral" so a plain memset initialises them; the finalize kernel
+// re-zeroes the per-step ones after every step.
 struct Control {
-    unsigned long long ticket;         // monotonic CTA ticket -> tile id + epoch
     unsigned long long maxdelta_bits;  // atomicMax over non-negative doubles
     unsigned long long bad_phi_key;    // atomicMax(~(col<<32|row)) -> min col
     unsigned long long bad_lt_key;
     unsigned long long skel_total;     // interest-skeleton nnz of the step
-    long long          nnz_total;      // output nnz (written by the last tile)
+    unsigned long long nnz_total;      // output nnz of the step
+    unsigned long long pool_next;      // overflow-pool bump pointer
     unsigned int       nan_key;        // atomicMax(INT_MAX - col) -> min col
-    int                overflow;       // a tile did not fit the output capacity
+    int                overflow;       // a tile did not fit the work buffer
+    int                slow_count;     // tiles queued for the fixup kernel
+    unsigned int       fin_count;      // finalize: CTAs done (last-block pattern)
     int                done;           // evolve: stop flag (finalize sets it)
     int                steps_done;     // evolve: completed steps
     int                status;         // evolve: final status
     int                pad0;
-    long long          needed;         // evolve: capacity needed on overflow
-    long long          pad1[6];
+    long long          needed;         // capacity needed on overflow
+    long long          pad1[5];
 };
 static_assert(sizeof(Control) % 16 == 0, "Control must stay 16B aligned");
 
 struct Workspace {
-    Control*            ctl;
-    unsigned long long* tile_status;   // [num_tiles] look-back words
-    double*             tile_bm;       // [num_tiles] per-tile base mass
-    int                 num_tiles;
+    Control*      ctl;
+    double*       tile_bm;      // [num_tiles] per-tile base mass (fast path)
+    double*       tile_bm_slow; // [num_tiles] per-tile base mass (fixup path)
+    unsigned int* slow_mask;    // [num_tiles * FT_WARPS] columns left to the fixup
+    int*          slow_list;    // [num_tiles] tiles queued for the fixup
+    long long*    chunk_off;    // [num_chunks + 2] compaction chunk offsets
+    double*       fin_part;     // [64] finalize partial sums
+    int           num_tiles;
+    int           num_chunks;
 };
 
-__host__ __device__ inline int num_tiles_for(int n_v) {
-    return (n_v + FT_TPB - 1) / FT_TPB;
-}
+__host__ __device__ inline int num_tiles_for(int n_v) { return (n_v + FT_TPB - 1) / FT_TPB; }
+__host__ __device__ inline int num_chunks_for(int n_v) { return (n_v + FT_CCH - 1) / FT_CCH; }
 
 inline size_t workspace_bytes(int n_v) {
-    size_t t = (size_t)num_tiles_for(n_v);
-    return sizeof(Control) + t * sizeof(unsigned long long) + t * sizeof(double) + 256;
+    size_t t = (size_t)num_tiles_for(n_v), c = (size_t)num_chunks_for(n_v);
+    return sizeof(Control) + 2 * t * sizeof(double) + t * FT_WARPS * sizeof(unsigned int) +
+           t * sizeof(int) + (c + 2) * sizeof(long long) + 64 * sizeof(double) + 256;
 }
 
 inline Workspace carve_workspace(void* base, int n_v) {
@@ -53,20 +64,19 @@ inline Workspace carve_workspace(void* base, int n_v) {
     w.ctl = (Control*)p;
     p += sizeof(Control);
     w.num_tiles = num_tiles_for(n_v);
-    w.tile_status = (unsigned long long*)p;
-    p += (size_t)w.num_tiles * sizeof(unsigned long long);
+    w.num_chunks = num_chunks_for(n_v);
     w.tile_bm = (double*)p;
+    p += (size_t)w.num_tiles * sizeof(double);
+    w.tile_bm_slow = (double*)p;
+    p += (size_t)w.num_tiles * sizeof(double);
+    w.chunk_off = (long long*)p;
+    p += ((size_t)w.num_chunks + 2) * sizeof(long long);
+    w.fin_part = (double*)p;
+    p += 64 * sizeof(double);
+    w.slow_mask = (unsigned int*)p;
+    p += (size_t)w.num_tiles * FT_WARPS * sizeof(unsigned int);
+    w.slow_list = (int*)p;
     return w;
-}
-
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 template <typename T>
@@ -74,6 +84,31 @@ __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     return v;
+}
+
+// Exclusive scan of one int per thread over a block of NT threads; returns
+// the exclusive prefix and writes the block total.  s_scan holds NT/32 ints.
+template <int NT>
+__device__ __forceinline__ int block_excl_scan(int v, int* s_scan, int* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_scan[warp] = incl;
+    __syncthreads();
+    int pre = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < NT / 32; ++k) {
+        const int c = s_scan[k];
+        if (k < warp) pre += c;
+        tot += c;
+    }
+    __syncthreads();
+    *total = tot;
+    return pre + incl - v;
 }
 
 }  // namespace ft

@@ -10,32 +10,39 @@
 //   normalise + compact     column_sums_counts, normalize_compact
 //                                               _kernels.py:241-282
 //
-// Layout: one thread per vertex column j.  The thread walks row j of L
-// (= column j of L^T, ascending neighbour index u including the diagonal)
-// and merges the sorted PHI columns of those neighbours into a small sorted
-// register window of at most K layer rows, accumulating Lt(r, j) for each
-// row in ascending-u order, exactly the order of the reference's
-// accumulator (first product assigned, then +=).  PHI(r, j) itself is
-// picked up when u == j.  Columns whose union of rows exceeds K are handled
-// exactly by re-gathering in ascending row windows (slow path).
+// Work split: one CTA per tile of FT_TPB consecutive vertex columns, one
+// thread per column.  The tile's L rows, the PHI column descriptors of all
+// its (vertex, neighbour) pairs and the gathered PHI entries are staged in
+// shared memory with flat, independent loads (high memory-level
+// parallelism); each thread then merges its neighbours' sorted PHI columns
+// into a sorted register window of at most K layer rows, accumulating
+// Lt(r, j) in ascending-u order -- exactly the reference accumulator order
+// (first product assigned, then +=).  PHI(r, j) itself arrives through the
+// diagonal u == j.  Columns whose union exceeds K rows are processed exactly
+// in ascending row windows straight from global memory (slow path).
 //
-// The per-vertex output count is only known after the update (zeros are
-// dropped), so output offsets come from a single-pass block scan plus a
-// decoupled look-back across tiles (tile ids from a monotonic ticket, so
-// predecessors are always resident and the scan cannot deadlock).
+// Output: the tile's entries go to its fixed slot of the tiled work buffer
+// (FT_SLOT entries) or, when they do not fit, to a pool range taken with
+// one atomic; column j is described by (start, count).  No CTA ever waits
+// for another.  Canonical CSC comes from ft_compact.
 //
 // EXACT mode (double storage) replays the reference arithmetic operation by
-// operation; the library is compiled with -fmad=false so no FMA contraction
-// happens, and sqrt / division are IEEE correctly rounded, which makes the
-// output bitwise identical to the numba reference.  FAST mode stores PHI in
-// float but does all arithmetic in double in the same order.
+// operation; the library is compiled with -fmad=false (no FMA contraction)
+// and sqrt / division are IEEE correctly rounded, so the result is bitwise
+// identical to the numba reference.  FAST mode stores PHI in float and does
+// all arithmetic in double, in the same order.
 
 #include <climits>
+#include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "ft_common.cuh"
 
 namespace ft {
+
+// exact 1.0 / n for n = 0..32 (host IEEE division; entry 0 unused)
+__constant__ double c_recip[33];
 
 struct StepParams {
     int n_v;
@@ -43,21 +50,24 @@ struct StepParams {
     const int* __restrict__ lap_ptr;
     const int* __restrict__ lap_idx;
     const void* __restrict__ lap_val;
-    const int* __restrict__ in_ptr;
+    const int* __restrict__ in_ptr;     // canonical input (IN_CANON)
+    const int2* __restrict__ in_desc;   // tiled input
     const int* __restrict__ in_idx;
     const void* __restrict__ in_val;
-    int* __restrict__ out_ptr;
+    int2* __restrict__ out_desc;
     int* __restrict__ out_idx;
     void* __restrict__ out_val;
     long long cap;
     double w, a, e, eb, mu, dt;
     Workspace ws;
     int check_done;
+    int finite;          // all couplings finite: enables the single-row closed form
 };
 
 struct FinalizeParams {
     Workspace ws;
     ft_step_stats* trace;
+    long long tiled_cap;
     int fixed_slot;       // 1: write trace[0] (single step), 0: trace[steps_done]
     int evolve;           // evolve mode: convergence / done handling
     int max_steps;
@@ -65,13 +75,23 @@ struct FinalizeParams {
     double base_threshold;
 };
 
+template <bool IN_CANON>
+__device__ __forceinline__ int2 load_desc(const StepParams& p, int u) {
+    if (IN_CANON) {
+        const int a = __ldg(&p.in_ptr[u]);
+        const int b = __ldg(&p.in_ptr[u + 1]);
+        return make_int2(a, b - a);
+    }
+    return __ldg(&p.in_desc[u]);
+}
+
 // ---------------------------------------------------------------------------
 // register window of layer rows for one vertex column
 
 template <int K>
 struct Win {
     int rows[K];
-    double lam[K];   // Lt(r, j) accumulator (later reused for v)
+    double lam[K];   // Lt(r, j) accumulator (later reused for v / v')
     double phi[K];   // PHI(r, j) (0.0 when not stored)
     int m;
     bool more;
@@ -118,8 +138,9 @@ __device__ __forceinline__ double ldv(const void* p, long long i) {
 }
 
 // Gather rows r > lo of the union of PHI(:, u), u in L^T(:, j), with the
-// Lt accumulation, into the window (the K smallest such rows).
-template <typename T, int K, bool UNIFORM>
+// Lt accumulation, into the window (the K smallest such rows).  Global
+// memory version (fallback tiles and the windowed slow path).
+template <typename T, int K, bool UNIFORM, bool IN_CANON>
 __device__ __forceinline__ void gather(Win<K>& w, int j, int lo, const StepParams& p) {
     w.m = 0;
     w.more = false;
@@ -132,9 +153,8 @@ __device__ __forceinline__ void gather(Win<K>& w, int j, int lo, const StepParam
         double l;
         if (UNIFORM) l = diag ? -1.0 : invdeg;
         else l = ldv<T>(p.lap_val, q);
-        const int c0 = __ldg(&p.in_ptr[u]);
-        const int c1 = __ldg(&p.in_ptr[u + 1]);
-        for (int c = c0; c < c1; ++c) {
+        const int2 d = load_desc<IN_CANON>(p, u);
+        for (int c = d.x; c < d.x + d.y; ++c) {
             const int r = __ldg(&p.in_idx[c]);
             if (r <= lo) continue;
             const double ph = ldv<T>(p.in_val, c);
@@ -143,7 +163,193 @@ __device__ __forceinline__ void gather(Win<K>& w, int j, int lo, const StepParam
     }
 }
 
-// Column aggregates over the skeleton rows (sequential, ascending row).
+// ---------------------------------------------------------------------------
+// shared-memory staging of a vertex tile
+//
+// The tile's L rows are one contiguous range of L^T, loaded coalesced; the
+// PHI descriptors of all (vertex, neighbour) pairs are fetched with
+// kLPV independent loads per thread, offsets come from a block scan, and
+// the gathered PHI entries are fetched flat into shared memory.  Each
+// thread then pays ~3 memory round trips instead of a dependent chain per
+// neighbour.  Tiles beyond the staging capacity (very high degree or very
+// dense bands) fall back to direct per-thread gathers (also exact).
+
+constexpr int kLPV = 8;                    // staged L entries per vertex (capacity)
+constexpr int kLMAX = FT_TPB * kLPV;       // staged L entries per tile
+constexpr int kEMAX = kLMAX * 2;           // staged PHI entries per tile
+
+template <typename T, bool UNIFORM>
+struct Stage {
+    int rp[FT_TPB + 1];    // L^T column pointers of the tile (absolute)
+    int u[kLMAX];          // neighbour ids
+    int2 oc[kLMAX];        // staged (offset, count) of PHI(:, u) per pair
+    int er[kEMAX];         // gathered PHI rows
+    T ev[kEMAX];           // gathered PHI values
+    T lv[UNIFORM ? 1 : kLMAX];
+    int scan[FT_WARPS];
+};
+
+// Phases A-C.  Returns true when the whole tile is staged (block-uniform).
+// Thread t owns pairs e = t + k*FT_TPB: it loads their descriptors (kLPV
+// independent loads), reserves their entries' space with one block scan,
+// and gathers the entries itself -- the descriptors never leave registers.
+template <typename T, bool UNIFORM, bool IN_CANON>
+__device__ __forceinline__ bool stage_tile(Stage<T, UNIFORM>& s, int j0, int jn, const StepParams& p) {
+    const int tid = threadIdx.x;
+    // A: L rows of the tile
+    if (tid < jn) s.rp[tid] = __ldg(&p.lap_ptr[j0 + tid]);
+    if (tid == 0) s.rp[jn] = __ldg(&p.lap_ptr[j0 + jn]);
+    __syncthreads();
+    const int LB = s.rp[0];
+    const int nL = s.rp[jn] - LB;
+    if (nL > kLMAX) return false;
+    int ur[kLPV];
+#pragma unroll
+    for (int k = 0; k < kLPV; ++k) {
+        const int e = tid + k * FT_TPB;
+        if (e < nL) {
+            ur[k] = __ldg(&p.lap_idx[LB + e]);
+            s.u[e] = ur[k];
+            if (!UNIFORM) s.lv[e] = __ldg(((const T*)p.lap_val) + LB + e);
+        }
+    }
+    // B: PHI descriptors of the owned pairs
+    int2 dr[kLPV];
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < kLPV; ++k) {
+        const int e = tid + k * FT_TPB;
+        dr[k] = make_int2(0, 0);
+        if (e < nL) dr[k] = load_desc<IN_CANON>(p, ur[k]);
+    }
+    int loc[kLPV];
+#pragma unroll
+    for (int k = 0; k < kLPV; ++k) { loc[k] = sum; sum += dr[k].y; }
+    int nE;
+    const int pre = block_excl_scan<FT_TPB>(sum, s.scan, &nE);
+    if (nE > kEMAX) return false;
+    // C: gather the owned pairs' entries; first entries go to registers
+    // before any store so each thread keeps kLPV loads in flight
+    {
+        int r0[kLPV];
+        T v0[kLPV];
+#pragma unroll
+        for (int k = 0; k < kLPV; ++k) {
+            if (dr[k].y > 0) {
+                r0[k] = __ldg(&p.in_idx[dr[k].x]);
+                v0[k] = __ldg(((const T*)p.in_val) + dr[k].x);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kLPV; ++k) {
+            const int e = tid + k * FT_TPB;
+            if (e < nL) {
+                const int o = pre + loc[k];
+                const int n = dr[k].y;
+                s.oc[e] = make_int2(o, n);
+                if (n > 0) { s.er[o] = r0[k]; s.ev[o] = v0[k]; }
+                for (int t = 1; t < n; ++t) {
+                    s.er[o + t] = __ldg(&p.in_idx[dr[k].x + t]);
+                    s.ev[o + t] = __ldg(((const T*)p.in_val) + dr[k].x + t);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    return true;
+}
+
+// Phase D: fill the register window of vertex (j0 + tid) from the stage.
+// One pass over the vertex's gathered entries in entry order (= ascending
+// u, the reference accumulation order): each entry's row is looked up among
+// the rows seen so far (slot 0 first: inside a cell every entry has the
+// same row) and its product added to that slot's Lt accumulator; unseen rows
+// are appended.  PHI(r, j) comes from the diagonal pair, and the window is
+// then sorted by row.
+// Starting an accumulator at +0.0 instead of assigning the first product
+// only changes the sign of an exact-zero sum; zero sums are not stored by
+// the reference (Lt == 0 is dropped) and are outside the skeleton either
+// way, so the result is bitwise the reference's.  Sets w.more when the
+// union exceeds K rows.
+template <int K>
+__device__ __forceinline__ void win_sort(Win<K>& w, unsigned int active) {
+    // insertion sort by row with warp-uniform trip counts (K <= 16)
+#pragma unroll
+    for (int a = 1; a < K; ++a) {
+        if (!__any_sync(active, a < w.m)) break;
+#pragma unroll
+        for (int b = a; b > 0; --b) {
+            const bool sw = (b < w.m) && (w.rows[b - 1] > w.rows[b]);
+            if (sw) {
+                const int tr = w.rows[b]; w.rows[b] = w.rows[b - 1]; w.rows[b - 1] = tr;
+                const double tl = w.lam[b]; w.lam[b] = w.lam[b - 1]; w.lam[b - 1] = tl;
+                const double tp = w.phi[b]; w.phi[b] = w.phi[b - 1]; w.phi[b - 1] = tp;
+            }
+        }
+    }
+}
+
+template <typename T, int K, bool UNIFORM>
+__device__ __forceinline__ void gather_staged(Win<K>& w, int j, const Stage<T, UNIFORM>& s,
+                                              const double* recip) {
+    const int tid = threadIdx.x;
+    const int LB = s.rp[0];
+    const int e0 = s.rp[tid] - LB;
+    const int e1 = s.rp[tid + 1] - LB;
+    const int deg = e1 - e0 - 1;
+    const double invdeg = UNIFORM ? (deg <= 32 ? recip[deg] : 1.0 / (double)deg) : 0.0;
+    w.more = false;
+#pragma unroll
+    for (int i = 0; i < K; ++i) { w.rows[i] = INT_MAX; w.lam[i] = 0.0; w.phi[i] = 0.0; }
+    w.m = 0;
+    int fd0 = 0, fd1 = 0;   // entries of the diagonal pair (u == j)
+    for (int e = e0; e < e1; ++e) {
+        const bool diag = (s.u[e] == j);
+        const double l = UNIFORM ? (diag ? -1.0 : invdeg) : (double)s.lv[e];
+        const int2 oc = s.oc[e];
+        if (diag) { fd0 = oc.x; fd1 = oc.x + oc.y; }
+        for (int f = oc.x; f < oc.x + oc.y; ++f) {
+            const int r = s.er[f];
+            const double prod = (double)s.ev[f] * l;
+            if (r == w.rows[0]) {
+                w.lam[0] = w.lam[0] + prod;
+            } else if (w.m == 0) {
+                w.rows[0] = r;
+                w.lam[0] = 0.0 + prod;
+                w.m = 1;
+            } else {
+                bool hit = false;
+#pragma unroll
+                for (int i = 1; i < K; ++i) {
+                    if (w.rows[i] == r) { w.lam[i] = w.lam[i] + prod; hit = true; }
+                }
+                if (!hit) {
+                    if (w.m == K) {
+                        w.more = true;
+                    } else {
+#pragma unroll
+                        for (int i = 1; i < K; ++i)
+                            if (i == w.m) { w.rows[i] = r; w.lam[i] = 0.0 + prod; }
+                        w.m++;
+                    }
+                }
+            }
+        }
+    }
+    if (w.more) return;
+    for (int f = fd0; f < fd1; ++f) {
+        const int r = s.er[f];
+        const double ph = (double)s.ev[f];
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+            if (w.rows[i] == r) w.phi[i] = ph;
+    }
+    win_sort<K>(w, __activemask());
+}
+
+// ---------------------------------------------------------------------------
+// per-column arithmetic (Appendix A of SURVEY.md; _kernels.py:179-282)
+
 struct Agg {
     int n;
     int first_row;
@@ -151,6 +357,11 @@ struct Agg {
     double sl, sp, sr;
     int bad_phi_row, bad_lt_row;
 };
+
+__device__ __forceinline__ void agg_init(Agg& g) {
+    g.n = 0; g.first_row = -1; g.phi0 = 0.0; g.sl = 0.0; g.sp = 0.0; g.sr = 0.0;
+    g.bad_phi_row = -1; g.bad_lt_row = -1;
+}
 
 __device__ __forceinline__ bool in_skeleton(double ph, double lm) {
     // (PHI stored and > 0) or ((absent or == 0) and Lt stored and > 0)
@@ -179,19 +390,18 @@ __device__ __forceinline__ void pass_aggregate(const Win<K>& w, Agg& g) {
     }
 }
 
-// Per-column constants of the closed-form update (_kernels.py:202-214).
 struct Coef {
     bool hb;
     double rb, spc, nif, agg, inv_ni, sl, sr;
 };
 
-__device__ __forceinline__ Coef make_coef(const Agg& g, const StepParams& p) {
+__device__ __forceinline__ Coef make_coef(const Agg& g, const StepParams& p, const double* recip) {
     Coef c;
     c.hb = (g.n > 0) && (g.first_row == 0);
     c.rb = c.hb ? sqrt(g.phi0) : 0.0;
     c.spc = c.hb ? g.sp - g.phi0 : g.sp;
     const int n_cells = c.hb ? g.n - 1 : g.n;
-    c.inv_ni = 1.0 / (double)g.n;
+    c.inv_ni = (recip && g.n <= 32) ? recip[g.n] : 1.0 / (double)g.n;
     c.nif = (double)g.n;
     double aggw = (p.w * fmax((double)n_cells - 1.0, 0.0)) * c.spc;
     if (c.hb) aggw = aggw + p.w * c.spc;
@@ -201,7 +411,6 @@ __device__ __forceinline__ Coef make_coef(const Agg& g, const StepParams& p) {
     return c;
 }
 
-// Euler update of one skeleton entry (_kernels.py:215-238).
 __device__ __forceinline__ double update_entry(int r, double ph, double lh, const Coef& c,
                                                const StepParams& p, bool& nan) {
     const double rj = sqrt(ph);
@@ -224,27 +433,179 @@ __device__ __forceinline__ double update_entry(int r, double ph, double lh, cons
     return v;
 }
 
-// Per-vertex results needed before the look-back.
+__device__ __forceinline__ double update_entry_sq(int r, double ph, double lh, double rj, const Coef& c,
+                                                  const StepParams& p, bool& nan) {
+    const double al = p.a * (c.sl - lh);
+    double wj, et;
+    if (r == 0) {
+        wj = p.w * c.spc;
+        et = ((-p.eb) * rj) * (c.sr - rj);
+    } else {
+        wj = p.w * (c.spc - ph);
+        if (c.hb) et = rj * (p.e * ((c.sr - rj) - c.rb) + p.eb * c.rb);
+        else      et = (rj * p.e) * (c.sr - rj);
+    }
+    const double ps = c.nif * (0.5 * al + wj) - c.agg;
+    const double d = ((-p.mu) * c.inv_ni) * (ps - et);
+    double v = ph + d * p.dt;
+    if (v != v) { nan = true; v = ph; }
+    if (v > 1.0) v = 1.0;
+    else if (v <= 0.0) v = 0.0;
+    return v;
+}
+
 struct VRes {
     int cnt;          // output entries (normalised value != 0)
     int nskel;        // skeleton entries
     double bm;        // base mass of the column
     double maxd;      // max |v' - phi_old|
-    double inv;       // normalisation factor (valid when s > 0)
-    bool spos;        // s > 0
     bool nan;
     int bad_phi_row, bad_lt_row;
 };
 
+__device__ __forceinline__ void vres_init(VRes& r) {
+    r.cnt = 0; r.nskel = 0; r.bm = 0.0; r.maxd = 0.0;
+    r.nan = false; r.bad_phi_row = -1; r.bad_lt_row = -1;
+}
+
+// Update + normalise one column held entirely in the window.  On return
+// w.lam[i] holds v' for the slots flagged in out_mask (entries to emit).
+template <int K>
+__device__ __forceinline__ void process_window(Win<K>& w, const StepParams& p, VRes& res,
+                                               unsigned int& out_mask, const double* recip) {
+    const unsigned int active = __activemask();
+    // skeleton membership and pattern checks (no arithmetic yet)
+    unsigned int skel_mask = 0;
+    int n = 0;
+    res.bad_phi_row = -1;
+    res.bad_lt_row = -1;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        if (!__any_sync(active, i < w.m)) break;
+        if (i < w.m) {
+            const double ph = w.phi[i], lm = w.lam[i];
+            const bool in = in_skeleton(ph, lm);
+            if (ph != 0.0 && !in) res.bad_phi_row = w.rows[i];
+            if (lm != 0.0 && !in) res.bad_lt_row = w.rows[i];
+            if (in) { skel_mask |= 1u << i; ++n; }
+        }
+    }
+    res.nskel = n;
+    out_mask = 0;
+    if (n == 0) return;
+    if (p.finite && n == 1) {
+        // One skeleton row: with finite couplings every term of the update
+        // cancels exactly (sl - lt = 0, sp_cells - phi = 0, sr - rj = 0,
+        // n_cells - 1 <= 0, nif - 1 = 0), so d = +-0 and v = clamp(phi),
+        // bit for bit what the reference's arithmetic produces.
+        int slot = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+            if (skel_mask == (1u << i)) slot = i;
+        double ph1 = 0.0, lm1 = 0.0;
+        int r1 = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+            if (i == slot) { ph1 = w.phi[i]; lm1 = w.lam[i]; r1 = w.rows[i]; }
+        if (isfinite(ph1) && isfinite(lm1)) {
+            double v = ph1;
+            if (v > 1.0) v = 1.0;
+            else if (v <= 0.0) v = 0.0;
+            const double s = 0.0 + v;
+            const bool spos = s > 0.0;
+            const double nv = spos ? v * (1.0 / s) : v;
+            if (nv != 0.0) {
+                res.cnt = 1;
+                out_mask = 1u << slot;
+                if (r1 == 0) res.bm = nv;
+            }
+            const double dd = fabs(nv - ph1);
+            if (dd > res.maxd) res.maxd = dd;
+#pragma unroll
+            for (int i = 0; i < K; ++i)
+                if (i == slot) w.lam[i] = nv;
+            return;
+        }
+    }
+    Agg g;
+    agg_init(g);
+    double sq[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        sq[i] = 0.0;
+        if (skel_mask & (1u << i)) {
+            const double ph = w.phi[i], lm = w.lam[i];
+            if (g.n == 0) { g.first_row = w.rows[i]; g.phi0 = ph; }
+            g.n++;
+            const double lh = (lm != 0.0) ? lm : 0.0;
+            sq[i] = sqrt(ph);
+            g.sl = g.sl + lh;
+            g.sp = g.sp + ph;
+            g.sr = g.sr + sq[i];
+        }
+    }
+    const Coef c = make_coef(g, p, recip);
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        if (skel_mask & (1u << i)) {
+            const double ph = w.phi[i], lm = w.lam[i];
+            const double v = update_entry_sq(w.rows[i], ph, (lm != 0.0) ? lm : 0.0, sq[i], c, p, res.nan);
+            w.lam[i] = v;
+            s = s + v;
+        }
+    }
+    const bool spos = s > 0.0;
+    const double inv = spos ? 1.0 / s : 0.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        if (skel_mask & (1u << i)) {
+            const double nv = spos ? w.lam[i] * inv : w.lam[i];
+            if (nv != 0.0) {
+                res.cnt++;
+                out_mask |= 1u << i;
+                if (w.rows[i] == 0) res.bm = res.bm + nv;
+            }
+            const double dd = fabs(nv - w.phi[i]);
+            if (dd > res.maxd) res.maxd = dd;
+            w.lam[i] = nv;
+        }
+    }
+}
+
+__device__ __forceinline__ void report_flags(const VRes& res, int j, const StepParams& p) {
+    if (res.nan) atomicMax(&p.ws.ctl->nan_key, (unsigned int)(INT_MAX - j));
+    if (res.bad_phi_row >= 0)
+        atomicMax(&p.ws.ctl->bad_phi_key, ~(((unsigned long long)j << 32) | (unsigned int)res.bad_phi_row));
+    if (res.bad_lt_row >= 0)
+        atomicMax(&p.ws.ctl->bad_lt_key, ~(((unsigned long long)j << 32) | (unsigned int)res.bad_lt_row));
+}
+
+template <typename T, int K>
+__device__ __forceinline__ void emit_window(const Win<K>& w, unsigned int out_mask, long long off,
+                                            const StepParams& p) {
+    T* ov = (T*)p.out_val;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        if (out_mask & (1u << i)) {
+            p.out_idx[off] = w.rows[i];
+            ov[off] = (T)w.lam[i];
+            ++off;
+        }
+    }
+}
+
 // --- slow path: union larger than K, processed in ascending row windows ----
 
-template <typename T, int K, bool UNIFORM>
-__device__ __noinline__ void vertex_slow(int j, const StepParams& p, VRes& res) {
+template <typename T, int K, bool UNIFORM, bool IN_CANON>
+__device__ __noinline__ void vertex_slow(int j, const StepParams& p, VRes& res, long long emit_off,
+                                         bool emit) {
     Win<K> w;
-    Agg g = {0, -1, 0.0, 0.0, 0.0, 0.0, -1, -1};
+    Agg g;
+    agg_init(g);
     int lo = -1;
     do {
-        gather<T, K, UNIFORM>(w, j, lo, p);
+        gather<T, K, UNIFORM, IN_CANON>(w, j, lo, p);
         pass_aggregate<K>(w, g);
         if (w.m > 0) lo = w.rows[w.m - 1];
     } while (w.more);
@@ -252,36 +613,38 @@ __device__ __noinline__ void vertex_slow(int j, const StepParams& p, VRes& res) 
     res.bad_phi_row = g.bad_phi_row;
     res.bad_lt_row = g.bad_lt_row;
     res.nan = false;
-    res.cnt = 0; res.bm = 0.0; res.maxd = 0.0; res.inv = 0.0; res.spos = false;
+    res.cnt = 0; res.bm = 0.0; res.maxd = 0.0;
     if (g.n == 0) return;
-    const Coef c = make_coef(g, p);
-    // pass 2: column sum of updated values
+    const Coef c = make_coef(g, p, nullptr);
     double s = 0.0;
     lo = -1;
     do {
-        gather<T, K, UNIFORM>(w, j, lo, p);
+        gather<T, K, UNIFORM, IN_CANON>(w, j, lo, p);
         for (int i = 0; i < w.m; ++i) {
             const double ph = w.phi[i], lm = w.lam[i];
             if (!in_skeleton(ph, lm)) continue;
-            const double lh = (lm != 0.0) ? lm : 0.0;
-            s = s + update_entry(w.rows[i], ph, lh, c, p, res.nan);
+            s = s + update_entry(w.rows[i], ph, (lm != 0.0) ? lm : 0.0, c, p, res.nan);
         }
         if (w.m > 0) lo = w.rows[w.m - 1];
     } while (w.more);
-    res.spos = s > 0.0;
-    res.inv = res.spos ? 1.0 / s : 0.0;
-    // pass 3: normalise, count, base mass, max delta
-    lo = -1;
+    const bool spos = s > 0.0;
+    const double inv = spos ? 1.0 / s : 0.0;
     bool dummy = false;
+    T* ov = (T*)p.out_val;
+    lo = -1;
     do {
-        gather<T, K, UNIFORM>(w, j, lo, p);
+        gather<T, K, UNIFORM, IN_CANON>(w, j, lo, p);
         for (int i = 0; i < w.m; ++i) {
             const double ph = w.phi[i], lm = w.lam[i];
             if (!in_skeleton(ph, lm)) continue;
-            const double lh = (lm != 0.0) ? lm : 0.0;
-            const double v = update_entry(w.rows[i], ph, lh, c, p, dummy);
-            const double nv = res.spos ? v * res.inv : v;
+            const double v = update_entry(w.rows[i], ph, (lm != 0.0) ? lm : 0.0, c, p, dummy);
+            const double nv = spos ? v * inv : v;
             if (nv != 0.0) {
+                if (emit) {
+                    p.out_idx[emit_off] = w.rows[i];
+                    ov[emit_off] = (T)nv;
+                    ++emit_off;
+                }
                 res.cnt++;
                 if (w.rows[i] == 0) res.bm = res.bm + nv;
             }
@@ -292,262 +655,219 @@ __device__ __noinline__ void vertex_slow(int j, const StepParams& p, VRes& res) 
     } while (w.more);
 }
 
-template <typename T, int K, bool UNIFORM>
-__device__ __noinline__ void vertex_slow_emit(int j, const StepParams& p, long long off) {
-    Win<K> w;
-    Agg g = {0, -1, 0.0, 0.0, 0.0, 0.0, -1, -1};
-    int lo = -1;
-    do {
-        gather<T, K, UNIFORM>(w, j, lo, p);
-        pass_aggregate<K>(w, g);
-        if (w.m > 0) lo = w.rows[w.m - 1];
-    } while (w.more);
-    if (g.n == 0) return;
-    const Coef c = make_coef(g, p);
-    bool dummy = false;
-    double s = 0.0;
-    lo = -1;
-    do {
-        gather<T, K, UNIFORM>(w, j, lo, p);
-        for (int i = 0; i < w.m; ++i) {
-            const double ph = w.phi[i], lm = w.lam[i];
-            if (!in_skeleton(ph, lm)) continue;
-            s = s + update_entry(w.rows[i], ph, (lm != 0.0) ? lm : 0.0, c, p, dummy);
+// ---------------------------------------------------------------------------
+// the fused step kernel (fast path)
+//
+// Columns that do not fit the register window (union > K rows) and every
+// column of a tile that could not be staged are left to fixup_kernel: they
+// contribute no entries to the tile slot, their bit is set in slow_mask
+// and the tile is queued once in slow_list.  Keeping the slow paths out of
+// this kernel keeps its register footprint small.
+
+// Tile epilogue shared by both kernels: block scan of the output counts,
+// placement (tile slot, or a pool range), per-tile statistics.
+struct TileOut {
+    int local_off;
+    long long base;   // -1: overflow, nothing is written
+};
+
+template <bool POOL_ONLY>
+__device__ __forceinline__ TileOut tile_epilogue(int cnt, int nskel, double bmv, double maxd, int tile,
+                                                 double* bm_slot, const StepParams& p, int* s_scan,
+                                                 double* s_wbm, double* s_wmax, int* s_wskel,
+                                                 long long* s_base) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int tile_total;
+    TileOut o;
+    o.local_off = block_excl_scan<FT_TPB>(cnt, s_scan, &tile_total);
+    const int skel = warp_sum(nskel);
+    const double bm = warp_sum(bmv);
+    double mx = maxd;
+#pragma unroll
+    for (int k = 16; k > 0; k >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, k));
+    if (lane == 0) { s_wskel[warp] = skel; s_wbm[warp] = bm; s_wmax[warp] = mx; }
+    __syncthreads();
+    if (tid == 0) {
+        long long base = POOL_ONLY ? -1 : (long long)tile * FT_SLOT;
+        if (tile_total > 0 && (POOL_ONLY || tile_total > FT_SLOT)) {
+            const unsigned long long q = atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)tile_total);
+            base = (long long)p.num_tiles * FT_SLOT + (long long)q;
         }
-        if (w.m > 0) lo = w.rows[w.m - 1];
-    } while (w.more);
-    const bool spos = s > 0.0;
-    const double inv = spos ? 1.0 / s : 0.0;
-    T* ov = (T*)p.out_val;
-    lo = -1;
-    do {
-        gather<T, K, UNIFORM>(w, j, lo, p);
-        for (int i = 0; i < w.m; ++i) {
-            const double ph = w.phi[i], lm = w.lam[i];
-            if (!in_skeleton(ph, lm)) continue;
-            const double v = update_entry(w.rows[i], ph, (lm != 0.0) ? lm : 0.0, c, p, dummy);
-            const double nv = spos ? v * inv : v;
-            if (nv != 0.0) {
-                p.out_idx[off] = w.rows[i];
-                ov[off] = (T)nv;
-                ++off;
-            }
+        if (base + tile_total > p.cap) {
+            atomicExch(&p.ws.ctl->overflow, 1);
+            base = -1;
         }
-        if (w.m > 0) lo = w.rows[w.m - 1];
-    } while (w.more);
+        if (tile_total == 0 && POOL_ONLY) base = 0;
+        *s_base = base;
+        double tbm = 0.0, tmx = 0.0;
+        int tsk = 0;
+#pragma unroll
+        for (int k = 0; k < FT_WARPS; ++k) { tbm = tbm + s_wbm[k]; tmx = fmax(tmx, s_wmax[k]); tsk += s_wskel[k]; }
+        *bm_slot = tbm;
+        if (tmx > 0.0) atomicMax(&p.ws.ctl->maxdelta_bits, (unsigned long long)__double_as_longlong(tmx));
+        if (tsk) atomicAdd(&p.ws.ctl->skel_total, (unsigned long long)tsk);
+        if (tile_total) atomicAdd(&p.ws.ctl->nnz_total, (unsigned long long)tile_total);
+    }
+    __syncthreads();
+    o.base = *s_base;
+    return o;
 }
 
-// ---------------------------------------------------------------------------
-// the fused step kernel
-
-template <typename T, int K, bool UNIFORM>
-__global__ void __launch_bounds__(FT_TPB) step_kernel(const StepParams p) {
-    __shared__ int s_tile;
-    __shared__ unsigned int s_epoch;
-    __shared__ int s_wcnt[FT_WARPS];
-    __shared__ int s_wskel[FT_WARPS];
+template <typename T, int K, bool UNIFORM, bool IN_CANON>
+__global__ void __launch_bounds__(FT_TPB, 5) step_kernel(const StepParams p) {
+    __shared__ Stage<T, UNIFORM> stg;
     __shared__ double s_wbm[FT_WARPS];
     __shared__ double s_wmax[FT_WARPS];
-    __shared__ int s_wflag[FT_WARPS];
-    __shared__ long long s_off;
+    __shared__ int s_wskel[FT_WARPS];
+    __shared__ unsigned int s_wslow[FT_WARPS];
+    __shared__ long long s_base;
+    __shared__ double s_recip[33];
 
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
+    if (threadIdx.x < 33) s_recip[threadIdx.x] = c_recip[threadIdx.x];
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    if (tid == 0) {
-        const unsigned long long t = atomicAdd(&p.ws.ctl->ticket, 1ULL);
-        s_tile = (int)(t % (unsigned long long)p.num_tiles);
-        s_epoch = (unsigned int)((t / (unsigned long long)p.num_tiles) & 0x3fffffffULL);
-    }
-    __syncthreads();
-    const int tile = s_tile;
-    const unsigned int epoch = s_epoch;
-    const int j = tile * FT_TPB + tid;
-    const bool active = j < p.n_v;
+    const int tile = blockIdx.x;
+    const int j0 = tile * FT_TPB;
+    const int jn = min(FT_TPB, p.n_v - j0);
+    const int j = j0 + tid;
+    const bool active = tid < jn;
+
+    const bool staged = stage_tile<T, UNIFORM, IN_CANON>(stg, j0, jn, p);
 
     Win<K> w;
     VRes res;
-    res.cnt = 0; res.nskel = 0; res.bm = 0.0; res.maxd = 0.0;
-    res.nan = false; res.bad_phi_row = -1; res.bad_lt_row = -1;
-    res.spos = false; res.inv = 0.0;
+    vres_init(res);
     bool slow = false;
-    unsigned int skel_mask = 0;
-
+    unsigned int out_mask = 0;
     if (active) {
-        gather<T, K, UNIFORM>(w, j, -1, p);
-        if (w.more) {
-            slow = true;
-            vertex_slow<T, K, UNIFORM>(j, p, res);
-        } else {
-            Agg g = {0, -1, 0.0, 0.0, 0.0, 0.0, -1, -1};
-            pass_aggregate<K>(w, g);
-            res.nskel = g.n;
-            res.bad_phi_row = g.bad_phi_row;
-            res.bad_lt_row = g.bad_lt_row;
-            if (g.n > 0) {
-                const Coef c = make_coef(g, p);
-                double s = 0.0;
-#pragma unroll
-                for (int i = 0; i < K; ++i) {
-                    if (i < w.m) {
-                        const double ph = w.phi[i], lm = w.lam[i];
-                        if (in_skeleton(ph, lm)) {
-                            skel_mask |= 1u << i;
-                            const double v = update_entry(w.rows[i], ph, (lm != 0.0) ? lm : 0.0, c, p, res.nan);
-                            w.lam[i] = v;
-                            s = s + v;
-                        }
-                    }
-                }
-                res.spos = s > 0.0;
-                res.inv = res.spos ? 1.0 / s : 0.0;
-#pragma unroll
-                for (int i = 0; i < K; ++i) {
-                    if (skel_mask & (1u << i)) {
-                        const double nv = res.spos ? w.lam[i] * res.inv : w.lam[i];
-                        if (nv != 0.0) {
-                            res.cnt++;
-                            if (w.rows[i] == 0) res.bm = res.bm + nv;
-                        }
-                        const double dd = fabs(nv - w.phi[i]);
-                        if (dd > res.maxd) res.maxd = dd;
-                        w.lam[i] = nv;
-                    }
-                }
-            }
+        if (staged) gather_staged<T, K, UNIFORM>(w, j, stg, s_recip);
+        slow = !staged || w.more;
+        if (!slow) {
+            process_window<K>(w, p, res, out_mask, s_recip);
+            report_flags(res, j, p);
         }
-        if (res.nan) atomicMax(&p.ws.ctl->nan_key, (unsigned int)(INT_MAX - j));
-        if (res.bad_phi_row >= 0)
-            atomicMax(&p.ws.ctl->bad_phi_key,
-                      ~(((unsigned long long)j << 32) | (unsigned int)res.bad_phi_row));
-        if (res.bad_lt_row >= 0)
-            atomicMax(&p.ws.ctl->bad_lt_key,
-                      ~(((unsigned long long)j << 32) | (unsigned int)res.bad_lt_row));
     }
+    const unsigned int slow_bits = __ballot_sync(0xffffffffu, slow);
+    if (lane == 0) s_wslow[warp] = slow_bits;
+    const TileOut o = tile_epilogue<false>(res.cnt, res.nskel, res.bm, res.maxd, tile, &p.ws.tile_bm[tile], p,
+                                           stg.scan, s_wbm, s_wmax, s_wskel, &s_base);
+    if (tid == 0) {
+        unsigned int any_slow = 0;
+#pragma unroll
+        for (int k = 0; k < FT_WARPS; ++k) any_slow |= s_wslow[k];
+        p.ws.tile_bm_slow[tile] = 0.0;
+        if (any_slow) {
+            const int q = atomicAdd(&p.ws.ctl->slow_count, 1);
+            p.ws.slow_list[q] = tile;
+#pragma unroll
+            for (int k = 0; k < FT_WARPS; ++k) p.ws.slow_mask[(size_t)tile * FT_WARPS + k] = s_wslow[k];
+        }
+    }
+    if (!active || slow || o.base < 0) return;
+    const long long off = o.base + o.local_off;
+    p.out_desc[j] = make_int2((int)off, res.cnt);
+    if (out_mask) emit_window<T, K>(w, out_mask, off, p);
+}
 
-    // ---- block scan of counts, block reductions ----------------------------
-    int incl = res.cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    int skel = warp_sum(res.nskel);
-    double bm = warp_sum(res.bm);
-    double mx = res.maxd;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
-    if (lane == 31) s_wcnt[warp] = incl;
-    if (lane == 0) { s_wskel[warp] = skel; s_wbm[warp] = bm; s_wmax[warp] = mx; }
-    __syncthreads();
-    int wpre = 0, tile_total = 0;
-#pragma unroll
-    for (int k = 0; k < FT_WARPS; ++k) {
-        const int c = s_wcnt[k];
-        if (k < warp) wpre += c;
-        tile_total += c;
-    }
-    const int local_off = wpre + incl - res.cnt;
+// ---------------------------------------------------------------------------
+// fixup kernel: the columns the fast path left behind.  One CTA per queued
+// tile (grid-stride over slow_list): the tile is staged again and the slow
+// columns use a KF-row window from shared memory; columns beyond KF rows
+// and tiles that cannot be staged use the exact windowed global path.  The
+// tile's base mass goes to tile_bm_slow[tile] (fixed reduction order).
 
-    // ---- decoupled look-back (warp 0) --------------------------------------
-    if (warp == 0) {
-        unsigned long long* st = p.ws.tile_status;
-        const unsigned long long tag = (unsigned long long)epoch << 34;
-        long long excl = 0;
-        if (tile == 0) {
-            if (lane == 0) st_relaxed_u64(&st[0], tag | (2ULL << 32) | (unsigned int)tile_total);
-        } else {
-            if (lane == 0) st_relaxed_u64(&st[tile], tag | (1ULL << 32) | (unsigned int)tile_total);
-            int base = tile - 1;
-            while (true) {
-                const int t = base - lane;
-                unsigned long long s;
-                unsigned int flag;
-                while (true) {
-                    if (t >= 0) {
-                        s = ld_relaxed_u64(&st[t]);
-                        flag = ((s >> 34) == (unsigned long long)epoch) ? (unsigned int)((s >> 32) & 3ULL) : 0u;
-                    } else {
-                        s = 0ULL;
-                        flag = 2u;  // before the first tile: inclusive prefix 0
-                    }
-                    if (__all_sync(0xffffffffu, flag != 0u)) break;
-                }
-                const unsigned int pm = __ballot_sync(0xffffffffu, flag == 2u);
-                const int kk = pm ? (__ffs(pm) - 1) : 31;
-                unsigned int v = (lane <= kk) ? (unsigned int)(s & 0xffffffffULL) : 0u;
-                excl += (long long)warp_sum(v);
-                excl = __shfl_sync(0xffffffffu, excl, 0);
-                if (pm) break;
-                base -= 32;
-            }
-            if (lane == 0)
-                st_relaxed_u64(&st[tile], tag | (2ULL << 32) | (unsigned int)(excl + tile_total));
+template <typename T, bool UNIFORM, bool IN_CANON>
+__global__ void __launch_bounds__(FT_TPB) fixup_kernel(const StepParams p) {
+    constexpr int KF = 12;
+    __shared__ Stage<T, UNIFORM> stg;
+    __shared__ double s_wbm[FT_WARPS];
+    __shared__ double s_wmax[FT_WARPS];
+    __shared__ int s_wskel[FT_WARPS];
+    __shared__ long long s_base;
+    __shared__ double s_recip[33];
+    if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
+    if (threadIdx.x < 33) s_recip[threadIdx.x] = c_recip[threadIdx.x];
+    const int n_slow = *(volatile int*)&p.ws.ctl->slow_count;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int q = blockIdx.x; q < n_slow; q += gridDim.x) {
+        const int tile = p.ws.slow_list[q];
+        const int j0 = tile * FT_TPB;
+        const int jn = min(FT_TPB, p.n_v - j0);
+        const int j = j0 + tid;
+        const bool mine = (p.ws.slow_mask[(size_t)tile * FT_WARPS + warp] >> lane) & 1u;
+        const bool staged = stage_tile<T, UNIFORM, IN_CANON>(stg, j0, jn, p);
+        Win<KF> w;
+        VRes res;
+        vres_init(res);
+        unsigned int out_mask = 0;
+        bool global_path = false;
+        if (mine) {
+            if (staged) gather_staged<T, KF, UNIFORM>(w, j, stg, s_recip);
+            global_path = !staged || w.more;
+            if (global_path) vertex_slow<T, 8, UNIFORM, IN_CANON>(j, p, res, 0, false);
+            else process_window<KF>(w, p, res, out_mask, s_recip);
+            report_flags(res, j, p);
         }
-        if (lane == 0) {
-            s_off = excl;
-            double tbm = 0.0, tmx = 0.0;
-            int tsk = 0;
-            for (int k = 0; k < FT_WARPS; ++k) { tbm = tbm + s_wbm[k]; tmx = fmax(tmx, s_wmax[k]); tsk += s_wskel[k]; }
-            p.ws.tile_bm[tile] = tbm;
-            if (tmx > 0.0) atomicMax(&p.ws.ctl->maxdelta_bits, (unsigned long long)__double_as_longlong(tmx));
-            atomicAdd(&p.ws.ctl->skel_total, (unsigned long long)tsk);
-            const long long end = excl + tile_total;
-            s_wflag[0] = (end > p.cap) ? 1 : 0;
-            if (end > p.cap) atomicExch(&p.ws.ctl->overflow, 1);
-            if (tile == p.num_tiles - 1) {
-                p.ws.ctl->nnz_total = end;
-                p.out_ptr[p.n_v] = (int)end;
+        const TileOut o = tile_epilogue<true>(res.cnt, res.nskel, res.bm, res.maxd, tile,
+                                              &p.ws.tile_bm_slow[tile], p, stg.scan, s_wbm, s_wmax,
+                                              s_wskel, &s_base);
+        if (mine && o.base >= 0) {
+            const long long off = o.base + o.local_off;
+            p.out_desc[j] = make_int2((int)off, res.cnt);
+            if (global_path) {
+                if (res.cnt) vertex_slow<T, 8, UNIFORM, IN_CANON>(j, p, res, off, true);
+            } else if (out_mask) {
+                emit_window<T, KF>(w, out_mask, off, p);
             }
         }
-    }
-    __syncthreads();
-    if (!active) return;
-    const long long off = s_off + local_off;
-    p.out_ptr[j] = (int)off;
-    if (s_wflag[0]) return;  // output does not fit: the host grows and retries
-    if (slow) {
-        vertex_slow_emit<T, K, UNIFORM>(j, p, off);
-    } else if (res.cnt > 0) {
-        T* ov = (T*)p.out_val;
-        long long o = off;
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            if ((skel_mask & (1u << i)) && w.lam[i] != 0.0) {
-                p.out_idx[o] = w.rows[i];
-                ov[o] = (T)w.lam[i];
-                ++o;
-            }
-        }
+        __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------------------
-// per-step finalisation: deterministic base-mass reduction, stats record,
-// error / convergence flags, accumulator reset.
+// per-step finalisation: deterministic two-level base-mass reduction (fixed
+// per-CTA ranges, then the last CTA sums the partials in order), stats
+// record, error / convergence flags, accumulator reset.
 
-__global__ void __launch_bounds__(1024) finalize_kernel(const FinalizeParams f) {
+#define FT_FIN_CTAS 64
+#define FT_FIN_TPB 256
+
+__global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizeParams f) {
     Control* ctl = f.ws.ctl;
     if (f.evolve && *(volatile int*)&ctl->done) return;
-    __shared__ double s_part[32];
+    __shared__ double s_part[FT_FIN_TPB / 32];
+    __shared__ int s_last;
     const int tid = threadIdx.x;
+    const int nt = f.ws.num_tiles;
+    const int per = (nt + gridDim.x - 1) / gridDim.x;
+    const int t0 = blockIdx.x * per, t1 = min(nt, t0 + per);
     double acc = 0.0;
-    for (int t = tid; t < f.ws.num_tiles; t += blockDim.x) acc = acc + f.ws.tile_bm[t];
+    for (int t = t0 + tid; t < t1; t += FT_FIN_TPB) acc = acc + (f.ws.tile_bm[t] + f.ws.tile_bm_slow[t]);
     acc = warp_sum(acc);
     if ((tid & 31) == 0) s_part[tid >> 5] = acc;
     __syncthreads();
-    if (tid != 0) return;
+    if (tid == 0) {
+        double b = 0.0;
+        for (int k = 0; k < FT_FIN_TPB / 32; ++k) b = b + s_part[k];
+        f.ws.fin_part[blockIdx.x] = b;
+        __threadfence();
+        s_last = (atomicAdd(&ctl->fin_count, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last || tid != 0) return;
+    __threadfence();
+    ctl->fin_count = 0u;
     double bm = 0.0;
-    const int nw = (blockDim.x + 31) >> 5;
-    for (int k = 0; k < nw; ++k) bm = bm + s_part[k];
+    for (int k = 0; k < (int)gridDim.x; ++k) bm = bm + *(volatile double*)&f.ws.fin_part[k];
 
     const int slot = f.fixed_slot ? 0 : ctl->steps_done;
     ft_step_stats st;
     st.max_delta = __longlong_as_double((long long)ctl->maxdelta_bits);
     st.base_mass = bm;
-    st.nnz_phi = ctl->nnz_total;
+    st.nnz_phi = (long long)ctl->nnz_total;
     st.nnz_skel = (long long)ctl->skel_total;
     st.nan_col = ctl->nan_key ? (int)(INT_MAX - ctl->nan_key) : -1;
     st.bad_col = -1; st.bad_row = -1; st.bad_is_lt = 0;
@@ -555,34 +875,166 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const FinalizeParams f) 
     if (kp) { const unsigned long long k = ~kp; st.bad_col = (int)(k >> 32); st.bad_row = (int)(k & 0xffffffffULL); }
     else if (kl) { const unsigned long long k = ~kl; st.bad_col = (int)(k >> 32); st.bad_row = (int)(k & 0xffffffffULL); st.bad_is_lt = 1; }
     int status = FT_STATUS_OK;
+    // the reference checks expand(PHI), expand(Lt), then NaN (field.py:238-250)
     if (st.bad_col >= 0) status = FT_STATUS_PATTERN;
     else if (st.nan_col >= 0) status = FT_STATUS_NAN;
     else if (ctl->overflow) status = FT_STATUS_OVERFLOW;
     const int stepno = ctl->steps_done + 1;
     st.step = stepno;
-    st.reserved = 0;
+    st.needed = (long long)f.ws.num_tiles * FT_SLOT + (long long)ctl->pool_next;
+    if (st.needed < f.tiled_cap) st.needed = f.tiled_cap;
     bool converged = false;
     if (status == FT_STATUS_OK && f.evolve)
         converged = (st.max_delta < f.tol) && (st.base_mass < f.base_threshold);
     st.status = converged ? FT_STATUS_CONVERGED : status;
     f.trace[slot] = st;
 
-    // reset the per-step accumulators
     ctl->maxdelta_bits = 0ULL;
     ctl->bad_phi_key = 0ULL;
     ctl->bad_lt_key = 0ULL;
     ctl->skel_total = 0ULL;
+    ctl->nnz_total = 0ULL;
+    ctl->pool_next = 0ULL;
     ctl->nan_key = 0u;
     ctl->overflow = 0;
+    ctl->slow_count = 0;
     if (f.evolve) {
         if (status != FT_STATUS_OK) {
             ctl->done = 1;
             ctl->status = status;
-            ctl->needed = st.nnz_phi;
+            ctl->needed = st.needed;
         } else {
             ctl->steps_done = stepno;
             if (converged) { ctl->done = 1; ctl->status = FT_STATUS_CONVERGED; }
             else if (stepno >= f.max_steps) { ctl->done = 1; ctl->status = FT_STATUS_MAXSTEPS; }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// compaction: tiled -> canonical CSC
+
+struct CompactParams {
+    int n_v;
+    const int2* desc[2];
+    const int* idx[2];
+    const void* val[2];
+    int sel;               // 0/1: source buffer; -1: pick by evolve parity
+    int* out_ptr;
+    int* out_idx;
+    void* out_val;
+    long long cap;
+    Workspace ws;
+    ft_step_stats* stats;  // single-step mode record (nullable)
+    long long* control;    // evolve mode (nullable)
+    int check_status;      // skip when stats->status reports a failed step
+};
+
+__device__ __forceinline__ int compact_source(const CompactParams& c) {
+    if (c.check_status && c.stats && *(volatile int*)&c.stats->status != FT_STATUS_OK) return -1;
+    if (c.sel >= 0) return c.sel;
+    const int n = c.ws.ctl->steps_done;
+    return n == 0 ? -1 : ((n & 1) ? 0 : 1);
+}
+
+constexpr int kCPT = FT_CCH / FT_CTPB;   // columns per thread (8)
+
+__global__ void __launch_bounds__(FT_CTPB) compact_count_kernel(const CompactParams c) {
+    __shared__ int s_scan[FT_CTPB / 32];
+    const int src = compact_source(c);
+    if (src < 0) return;
+    const int2* desc = c.desc[src];
+    const int j0 = blockIdx.x * FT_CCH + threadIdx.x * kCPT;
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < kCPT; ++k)
+        if (j0 + k < c.n_v) sum += __ldg(&desc[j0 + k]).y;
+    int tot;
+    block_excl_scan<FT_CTPB>(sum, s_scan, &tot);
+    if (threadIdx.x == 0) c.ws.chunk_off[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) compact_scan_kernel(const CompactParams c) {
+    __shared__ long long s_part[32];
+    const int src = compact_source(c);
+    const int nc = c.ws.num_chunks;
+    const int tid = threadIdx.x;
+    long long* off = c.ws.chunk_off;
+    if (src < 0) {
+        if (tid == 0 && c.control) { c.control[3] = 0; c.control[4] = 0; c.control[5] = 0; }
+        return;
+    }
+    const int per = (nc + 1023) / 1024;
+    const int b0 = tid * per;
+    long long sum = 0;
+    for (int k = 0; k < per; ++k)
+        if (b0 + k < nc) sum += off[b0 + k];
+    long long incl = sum;
+    const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_part[warp] = incl;
+    __syncthreads();
+    long long pre = 0, tot = 0;
+    for (int k = 0; k < 32; ++k) {
+        if (k < warp) pre += s_part[k];
+        tot += s_part[k];
+    }
+    long long run = pre + incl - sum;
+    for (int k = 0; k < per; ++k) {
+        if (b0 + k < nc) {
+            const long long v = off[b0 + k];
+            off[b0 + k] = run;
+            run += v;
+        }
+    }
+    if (tid == 0) {
+        off[nc] = tot;
+        const bool fits = tot <= c.cap && tot <= (long long)INT_MAX;
+        off[nc + 1] = fits ? 1 : 0;
+        if (fits) c.out_ptr[c.n_v] = (int)tot;
+        if (c.stats) {
+            c.stats->nnz_phi = tot;
+            if (!fits) { c.stats->status = FT_STATUS_OUT_OVERFLOW; c.stats->needed = tot; }
+            else if (!c.check_status) c.stats->status = FT_STATUS_OK;
+        }
+        if (c.control) { c.control[3] = fits ? 1 : 2; c.control[4] = tot; c.control[5] = tot; }
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(FT_CTPB) compact_copy_kernel(const CompactParams c) {
+    __shared__ int s_scan[FT_CTPB / 32];
+    const int src = compact_source(c);
+    if (src < 0) return;
+    if (c.ws.chunk_off[c.ws.num_chunks + 1] == 0) return;  // does not fit
+    const int2* desc = c.desc[src];
+    const int* sidx = c.idx[src];
+    const T* sval = (const T*)c.val[src];
+    T* oval = (T*)c.out_val;
+    const int j0 = blockIdx.x * FT_CCH + threadIdx.x * kCPT;
+    int2 d[kCPT];
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < kCPT; ++k) {
+        d[k] = (j0 + k < c.n_v) ? __ldg(&desc[j0 + k]) : make_int2(0, 0);
+        sum += d[k].y;
+    }
+    int tot;
+    const int pre = block_excl_scan<FT_CTPB>(sum, s_scan, &tot);
+    long long o = c.ws.chunk_off[blockIdx.x] + pre;
+#pragma unroll
+    for (int k = 0; k < kCPT; ++k) {
+        if (j0 + k < c.n_v) {
+            c.out_ptr[j0 + k] = (int)o;
+            for (int t = 0; t < d[k].y; ++t) {
+                c.out_idx[o + t] = __ldg(&sidx[d[k].x + t]);
+                oval[o + t] = __ldg(&sval[d[k].x + t]);
+            }
+            o += d[k].y;
         }
     }
 }
@@ -598,7 +1050,6 @@ __global__ void evolve_report_kernel(const Control* ctl, long long* control) {
     control[0] = ctl->steps_done;
     control[1] = ctl->status;
     control[2] = ctl->needed;
-    control[3] = ctl->steps_done & 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -606,10 +1057,23 @@ __global__ void evolve_report_kernel(const Control* ctl, long long* control) {
 
 typedef void (*StepKernelFn)(const StepParams);
 
+static StepKernelFn pick_fixup(int dtype, bool uniform, bool in_canon) {
+    if (dtype == FT_F64) {
+        if (uniform) return in_canon ? fixup_kernel<double, true, true> : fixup_kernel<double, true, false>;
+        return in_canon ? fixup_kernel<double, false, true> : fixup_kernel<double, false, false>;
+    }
+    if (uniform) return in_canon ? fixup_kernel<float, true, true> : fixup_kernel<float, true, false>;
+    return in_canon ? fixup_kernel<float, false, true> : fixup_kernel<float, false, false>;
+}
+
 template <int K>
-static StepKernelFn pick_kernel(int dtype, bool uniform) {
-    if (dtype == FT_F64) return uniform ? step_kernel<double, K, true> : step_kernel<double, K, false>;
-    return uniform ? step_kernel<float, K, true> : step_kernel<float, K, false>;
+static StepKernelFn pick_kernel(int dtype, bool uniform, bool in_canon) {
+    if (dtype == FT_F64) {
+        if (uniform) return in_canon ? step_kernel<double, K, true, true> : step_kernel<double, K, true, false>;
+        return in_canon ? step_kernel<double, K, false, true> : step_kernel<double, K, false, false>;
+    }
+    if (uniform) return in_canon ? step_kernel<float, K, true, true> : step_kernel<float, K, true, false>;
+    return in_canon ? step_kernel<float, K, false, true> : step_kernel<float, K, false, false>;
 }
 
 }  // namespace ft
@@ -646,112 +1110,189 @@ extern "C" int ft_workspace_init(void* workspace, size_t bytes, void* stream) {
     return cuda_check("ft_workspace_init");
 }
 
-static int validate_step_args(const ft_csc* lap_t, const ft_csc* in, const ft_csc* out, int dtype,
-                              size_t ws_bytes) {
-    if (!lap_t || !in || !out) return set_err(FT_ERR_ARG, "null matrix descriptor");
-    if (dtype != FT_F64 && dtype != FT_F32) return set_err(FT_ERR_ARG, "bad dtype");
-    if (lap_t->n_rows != lap_t->n_cols) return set_err(FT_ERR_SHAPE, "Laplacian must be square");
-    if (lap_t->n_cols != in->n_cols) return set_err(FT_ERR_SHAPE, "Laplacian size does not match field");
-    if (in->n_cols != out->n_cols || in->n_rows != out->n_rows)
-        return set_err(FT_ERR_SHAPE, "output buffer has wrong shape");
-    if (ws_bytes < ft::workspace_bytes(in->n_cols)) return set_err(FT_ERR_ARG, "workspace too small");
+extern "C" int64_t ft_tile_slot_entries(void) { return FT_SLOT; }
+
+extern "C" int64_t ft_tiled_min_capacity(int32_t n_vertices) {
+    return (int64_t)ft::num_tiles_for(n_vertices < 0 ? 0 : n_vertices) * FT_SLOT;
+}
+
+static int check_tiled(const ft_tiled* t, int n_rows, int n_cols) {
+    if (!t || !t->desc || !t->row_idx || !t->values) return set_err(FT_ERR_ARG, "null tiled buffer");
+    if (t->n_rows != n_rows || t->n_cols != n_cols) return set_err(FT_ERR_SHAPE, "tiled buffer has wrong shape");
+    if (t->capacity < ft_tiled_min_capacity(n_cols) || t->capacity > (int64_t)INT_MAX)
+        return set_err(FT_ERR_ARG, "tiled capacity out of range");
+    if (((uintptr_t)t->desc) & 7) return set_err(FT_ERR_ARG, "tiled desc must be 8-byte aligned");
     return FT_OK;
 }
 
-static ft::StepParams make_params(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in,
-                                  ft_csc* out, const ft_params* prm, void* ws) {
+static int g_window = 0;
+static int g_fixup_grid = 2 * 148;
+
+static int window_size() {
+    if (g_window == 0) {
+        double h[33];
+        h[0] = 0.0;
+        for (int n = 1; n <= 32; ++n) h[n] = 1.0 / (double)n;
+        cudaMemcpyToSymbol(ft::c_recip, h, sizeof(h));
+        const char* s = getenv("FT_WINDOW");
+        g_window = (s && atoi(s) == 8) ? 8 : 4;
+        int dev = 0, sms = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+            g_fixup_grid = 2 * sms;
+    }
+    return g_window;
+}
+
+static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_canon,
+                       const ft_tiled* in_tiled, ft_tiled* out, int32_t dtype,
+                       const ft_params* prm, void* workspace, size_t ws_bytes, int check_done,
+                       cudaStream_t s) {
+    if (!lap_t || !out || !prm || !workspace) return set_err(FT_ERR_ARG, "null argument");
+    if (dtype != FT_F64 && dtype != FT_F32) return set_err(FT_ERR_ARG, "bad dtype");
+    const int n_rows = in_canon ? in_canon->n_rows : (in_tiled ? in_tiled->n_rows : -1);
+    const int n_v = in_canon ? in_canon->n_cols : (in_tiled ? in_tiled->n_cols : -1);
+    if (n_v < 0) return set_err(FT_ERR_ARG, "no input");
+    if (lap_t->n_rows != lap_t->n_cols) return set_err(FT_ERR_SHAPE, "Laplacian must be square");
+    if (lap_t->n_cols != n_v) return set_err(FT_ERR_SHAPE, "Laplacian size does not match field");
+    if (n_v == 0) return set_err(FT_ERR_SHAPE, "empty field");
+    int rc = check_tiled(out, n_rows, n_v);
+    if (rc != FT_OK) return rc;
+    if (ws_bytes < ft::workspace_bytes(n_v)) return set_err(FT_ERR_ARG, "workspace too small");
     ft::StepParams p;
-    p.n_v = in->n_cols;
-    p.num_tiles = ft::num_tiles_for(p.n_v);
+    p.n_v = n_v;
+    p.num_tiles = ft::num_tiles_for(n_v);
     p.lap_ptr = lap_t->col_ptr;
     p.lap_idx = lap_t->row_idx;
     p.lap_val = lap_t->values;
-    p.in_ptr = in->col_ptr;
-    p.in_idx = in->row_idx;
-    p.in_val = in->values;
-    p.out_ptr = out->col_ptr;
+    p.in_ptr = in_canon ? in_canon->col_ptr : nullptr;
+    p.in_desc = in_canon ? nullptr : (const int2*)in_tiled->desc;
+    p.in_idx = in_canon ? in_canon->row_idx : in_tiled->row_idx;
+    p.in_val = in_canon ? in_canon->values : in_tiled->values;
+    p.out_desc = (int2*)out->desc;
     p.out_idx = out->row_idx;
     p.out_val = out->values;
     p.cap = out->capacity;
     p.w = prm->w; p.a = prm->a; p.e = prm->e; p.eb = prm->e_base; p.mu = prm->mu; p.dt = prm->dt;
-    p.ws = ft::carve_workspace(ws, p.n_v);
-    p.check_done = 0;
-    (void)lap_flags;
-    return p;
-}
-
-static int launch_step_kernel(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
-                              ft_csc* phi_out, int32_t dtype, const ft_params* params,
-                              void* workspace, size_t ws_bytes, cudaStream_t s,
-                              ft::Workspace* ws_out) {
-    int rc = validate_step_args(lap_t, phi_in, phi_out, dtype, ws_bytes);
-    if (rc != FT_OK) return rc;
-    if (!params || !workspace) return set_err(FT_ERR_ARG, "null argument");
-    ft::StepParams p = make_params(lap_t, lap_flags, phi_in, phi_out, params, workspace);
-    if (p.n_v == 0) return set_err(FT_ERR_SHAPE, "empty field");
-    ft::StepKernelFn k = ft::pick_kernel<8>(dtype, lap_flags == FT_LAP_UNIFORM);
+    p.ws = ft::carve_workspace(workspace, n_v);
+    p.check_done = check_done;
+    p.finite = std::isfinite(p.w) && std::isfinite(p.a) && std::isfinite(p.e) && std::isfinite(p.eb) &&
+               std::isfinite(p.mu) && std::isfinite(p.dt);
+    const bool uni = lap_flags == FT_LAP_UNIFORM;
+    ft::StepKernelFn k = window_size() == 8 ? ft::pick_kernel<8>(dtype, uni, in_canon != nullptr)
+                                            : ft::pick_kernel<4>(dtype, uni, in_canon != nullptr);
     k<<<p.num_tiles, FT_TPB, 0, s>>>(p);
-    if (ws_out) *ws_out = p.ws;
-    return cuda_check("ft_step_kernel");
+    ft::StepKernelFn fx = ft::pick_fixup(dtype, uni, in_canon != nullptr);
+    fx<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
+    return cuda_check("step kernel");
 }
 
-static void launch_finalize(const ft::Workspace& ws, ft_step_stats* stats, cudaStream_t s) {
+static void launch_finalize(const ft::Workspace& ws, ft_step_stats* trace, long long tiled_cap,
+                            int evolve, int max_steps, double tol, double thr, cudaStream_t s) {
     ft::FinalizeParams f;
-    f.ws = ws; f.trace = stats; f.fixed_slot = 1; f.evolve = 0;
-    f.max_steps = 1; f.tol = 0.0; f.base_threshold = 0.0;
-    ft::finalize_kernel<<<1, 1024, 0, s>>>(f);
+    f.ws = ws; f.trace = trace; f.tiled_cap = tiled_cap; f.fixed_slot = evolve ? 0 : 1;
+    f.evolve = evolve; f.max_steps = max_steps; f.tol = tol; f.base_threshold = thr;
+    ft::finalize_kernel<<<FT_FIN_CTAS, FT_FIN_TPB, 0, s>>>(f);
 }
 
-extern "C" int ft_step_kernel(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
-                              ft_csc* phi_out, int32_t dtype, const ft_params* params,
-                              void* workspace, size_t ws_bytes, void* stream) {
-    return launch_step_kernel(lap_t, lap_flags, phi_in, phi_out, dtype, params, workspace,
-                              ws_bytes, (cudaStream_t)stream, nullptr);
+static int launch_compact(ft::CompactParams& c, int dtype, cudaStream_t s) {
+    const int nc = c.ws.num_chunks;
+    ft::compact_count_kernel<<<nc, FT_CTPB, 0, s>>>(c);
+    ft::compact_scan_kernel<<<1, 1024, 0, s>>>(c);
+    if (dtype == FT_F64) ft::compact_copy_kernel<double><<<nc, FT_CTPB, 0, s>>>(c);
+    else ft::compact_copy_kernel<float><<<nc, FT_CTPB, 0, s>>>(c);
+    return cuda_check("compact");
+}
+
+extern "C" int ft_step_kernel(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_canon,
+                              const ft_tiled* in_tiled, ft_tiled* out, int32_t dtype,
+                              const ft_params* params, void* workspace, size_t ws_bytes,
+                              void* stream) {
+    return launch_step(lap_t, lap_flags, in_canon, in_tiled, out, dtype, params, workspace, ws_bytes,
+                       0, (cudaStream_t)stream);
 }
 
 extern "C" int ft_step_finalize(void* workspace, size_t ws_bytes, int32_t n_vertices,
-                                ft_step_stats* stats, void* stream) {
+                                int64_t tiled_capacity, ft_step_stats* stats, void* stream) {
     if (!workspace || !stats) return set_err(FT_ERR_ARG, "null argument");
     if (ws_bytes < ft::workspace_bytes(n_vertices)) return set_err(FT_ERR_ARG, "workspace too small");
-    launch_finalize(ft::carve_workspace(workspace, n_vertices), stats, (cudaStream_t)stream);
+    launch_finalize(ft::carve_workspace(workspace, n_vertices), stats, tiled_capacity, 0, 1, 0.0, 0.0,
+                    (cudaStream_t)stream);
     return cuda_check("ft_step_finalize");
 }
 
-extern "C" int ft_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
-                       ft_csc* phi_out, int32_t dtype, const ft_params* params, void* workspace,
-                       size_t ws_bytes, ft_step_stats* stats, void* stream) {
-    if (!stats) return set_err(FT_ERR_ARG, "null stats");
-    cudaStream_t s = (cudaStream_t)stream;
-    ft::Workspace ws;
-    int rc = launch_step_kernel(lap_t, lap_flags, phi_in, phi_out, dtype, params, workspace,
-                                ws_bytes, s, &ws);
-    if (rc != FT_OK) return rc;
-    launch_finalize(ws, stats, s);
-    return cuda_check("ft_step");
+static void fill_compact(ft::CompactParams& c, const ft_tiled* a, const ft_tiled* b, int sel,
+                         ft_csc* dst, void* workspace) {
+    c.n_v = dst->n_cols;
+    c.desc[0] = (const int2*)a->desc; c.idx[0] = a->row_idx; c.val[0] = a->values;
+    const ft_tiled* bb = b ? b : a;
+    c.desc[1] = (const int2*)bb->desc; c.idx[1] = bb->row_idx; c.val[1] = bb->values;
+    c.sel = sel;
+    c.out_ptr = dst->col_ptr; c.out_idx = dst->row_idx; c.out_val = dst->values; c.cap = dst->capacity;
+    c.ws = ft::carve_workspace(workspace, dst->n_cols);
+    c.stats = nullptr;
+    c.control = nullptr;
+    c.check_status = 0;
 }
 
-extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, ft_csc* phi_a, ft_csc* phi_b,
-                         int32_t dtype, const ft_params* params, int32_t max_steps, double tol,
+extern "C" int ft_compact(const ft_tiled* src, ft_csc* dst, int32_t dtype, void* workspace,
+                          size_t ws_bytes, ft_step_stats* stats, void* stream) {
+    if (!src || !dst || !workspace || !stats) return set_err(FT_ERR_ARG, "null argument");
+    if (src->n_cols != dst->n_cols || src->n_rows != dst->n_rows) return set_err(FT_ERR_SHAPE, "shape mismatch");
+    if (ws_bytes < ft::workspace_bytes(dst->n_cols)) return set_err(FT_ERR_ARG, "workspace too small");
+    if (dst->n_cols == 0) return set_err(FT_ERR_SHAPE, "empty field");
+    ft::CompactParams c;
+    fill_compact(c, src, nullptr, 0, dst, workspace);
+    c.stats = stats;
+    return launch_compact(c, dtype, (cudaStream_t)stream);
+}
+
+extern "C" int ft_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
+                       ft_tiled* scratch, ft_csc* phi_out, int32_t dtype, const ft_params* params,
+                       void* workspace, size_t ws_bytes, ft_step_stats* stats, void* stream) {
+    if (!phi_in || !phi_out || !stats || !scratch) return set_err(FT_ERR_ARG, "null argument");
+    if (phi_out->n_cols != phi_in->n_cols || phi_out->n_rows != phi_in->n_rows)
+        return set_err(FT_ERR_SHAPE, "output buffer has wrong shape");
+    cudaStream_t s = (cudaStream_t)stream;
+    int rc = launch_step(lap_t, lap_flags, phi_in, nullptr, scratch, dtype, params, workspace, ws_bytes, 0, s);
+    if (rc != FT_OK) return rc;
+    ft::Workspace ws = ft::carve_workspace(workspace, phi_in->n_cols);
+    launch_finalize(ws, stats, scratch->capacity, 0, 1, 0.0, 0.0, s);
+    // the compaction always runs; the host ignores it if the step failed
+    ft::CompactParams c;
+    fill_compact(c, scratch, nullptr, 0, phi_out, workspace);
+    c.stats = stats;
+    c.check_status = 1;
+    return launch_compact(c, dtype, s);
+}
+
+extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
+                         ft_tiled* work_a, ft_tiled* work_b, ft_csc* phi_out, int32_t dtype,
+                         const ft_params* params, int32_t max_steps, double tol,
                          double base_threshold, void* workspace, size_t ws_bytes,
                          ft_step_stats* trace, int64_t* control, void* stream) {
-    int rc = validate_step_args(lap_t, phi_a, phi_b, dtype, ws_bytes);
-    if (rc != FT_OK) return rc;
-    if (!params || !trace || !control || !workspace) return set_err(FT_ERR_ARG, "null argument");
+    if (!phi_in || !phi_out || !work_a || !work_b || !trace || !control)
+        return set_err(FT_ERR_ARG, "null argument");
     if (max_steps < 1) return set_err(FT_ERR_SHAPE, "max_steps must be >= 1");
+    if (phi_out->n_cols != phi_in->n_cols || phi_out->n_rows != phi_in->n_rows)
+        return set_err(FT_ERR_SHAPE, "output buffer has wrong shape");
+    int rc = check_tiled(work_b, phi_in->n_rows, phi_in->n_cols);
+    if (rc != FT_OK) return rc;
+    if (ws_bytes < ft::workspace_bytes(phi_in->n_cols)) return set_err(FT_ERR_ARG, "workspace too small");
     cudaStream_t s = (cudaStream_t)stream;
-    ft::StepParams pab = make_params(lap_t, lap_flags, phi_a, phi_b, params, workspace);
-    ft::StepParams pba = make_params(lap_t, lap_flags, phi_b, phi_a, params, workspace);
-    if (pab.n_v == 0) return set_err(FT_ERR_SHAPE, "empty field");
-    pab.check_done = pba.check_done = 1;
-    ft::StepKernelFn k = ft::pick_kernel<8>(dtype, lap_flags == FT_LAP_UNIFORM);
-    ft::FinalizeParams f;
-    f.ws = pab.ws; f.trace = trace; f.fixed_slot = 0; f.evolve = 1;
-    f.max_steps = max_steps; f.tol = tol; f.base_threshold = base_threshold;
-    ft::evolve_reset_kernel<<<1, 1, 0, s>>>(pab.ws.ctl);
+    ft::Workspace ws = ft::carve_workspace(workspace, phi_in->n_cols);
+    ft::evolve_reset_kernel<<<1, 1, 0, s>>>(ws.ctl);
     for (int i = 0; i < max_steps; ++i) {
-        k<<<pab.num_tiles, FT_TPB, 0, s>>>((i & 1) ? pba : pab);
-        ft::finalize_kernel<<<1, 1024, 0, s>>>(f);
+        ft_tiled* out = (i & 1) ? work_b : work_a;
+        const ft_tiled* in_t = (i & 1) ? work_a : work_b;
+        rc = launch_step(lap_t, lap_flags, i == 0 ? phi_in : nullptr, i == 0 ? nullptr : in_t, out, dtype,
+                         params, workspace, ws_bytes, 1, s);
+        if (rc != FT_OK) return rc;
+        launch_finalize(ws, trace, out->capacity, 1, max_steps, tol, base_threshold, s);
     }
-    ft::evolve_report_kernel<<<1, 1, 0, s>>>(pab.ws.ctl, (long long*)control);
-    return cuda_check("ft_evolve");
+    ft::evolve_report_kernel<<<1, 1, 0, s>>>(ws.ctl, (long long*)control);
+    ft::CompactParams c;
+    fill_compact(c, work_a, work_b, -1, phi_out, workspace);
+    c.control = (long long*)control;
+    return launch_compact(c, dtype, s);
 }

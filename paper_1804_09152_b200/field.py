@@ -26,7 +26,7 @@ import numpy as np
 from . import _lib
 from .errors import (BackendError, DuplicateSeedError, NumericalBlowupError,
                      PatternViolationError, ShapeError)
-from .sparse import INDEX, DeviceCSC, SparseMat
+from .sparse import INDEX, DeviceCSC, DeviceTiled, SparseMat
 
 UNCLAIMED = -1
 BASE_EXHAUSTION_PER_VERTEX = 1e-9       # field.py:31
@@ -338,27 +338,45 @@ def device_laplacian(lap, precision):
     return dl
 
 
+POOL_FRACTION = 0.5     # overflow pool of a tiled buffer, relative to nnz
+POOL_MIN = 4096
+
+
 class StepWorkspace:
-    """Reusable device buffers for the step pipeline: the look-back /
-    statistics workspace, the statistics record and a spare output CSC
-    (field.py:169-189).  With a shared workspace the input field's storage is
-    recycled as a later output (only the newest field stays valid)."""
+    """Reusable device buffers for the step pipeline (field.py:169-189): the
+    workspace (per-tile partial sums, compaction scan, control block), the
+    statistics record, two tiled work buffers and a spare canonical output.
+    With a shared workspace the input field's storage is recycled as a later
+    output, so only the newest field stays valid (as in the reference)."""
 
     def __init__(self):
         self.ws = None
         self.ws_n = -1
         self.stats = None
         self.spare = None
+        self.tiled = {}
         self.realloc_count = 0
 
     def prepare(self, n_v, device):
         torch = _torch()
         if self.ws is None or self.ws_n != n_v:
             nbytes = int(_lib.lib().ft_workspace_bytes(n_v))
-            self.ws = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+            self.ws = torch.zeros(nbytes, dtype=torch.int8, device=device)
             self.ws_n = n_v
+            self.tiled = {}
         if self.stats is None:
             self.stats = torch.zeros(_lib.STATS_BYTES, dtype=torch.uint8, device=device)
+
+    def tiled_buffer(self, key, like, nnz_hint):
+        """Tiled work buffer ``key`` shaped like ``like`` (created or reused)."""
+        buf = self.tiled.get(key)
+        if (buf is None or buf.n_rows != like.n_rows or buf.n_cols != like.n_cols
+                or buf.values.dtype != like.values.dtype):
+            cap = int(_lib.lib().ft_tiled_min_capacity(like.n_cols)) + max(
+                int(nnz_hint * POOL_FRACTION), POOL_MIN)
+            buf = DeviceTiled(like.n_rows, like.n_cols, cap, like.values.dtype, like.values.device)
+            self.tiled[key] = buf
+        return buf
 
     def take_output(self, like, capacity):
         sp = self.spare
@@ -371,10 +389,13 @@ class StepWorkspace:
         return DeviceCSC.allocate(like.n_rows, like.n_cols, capacity, like.values.dtype,
                                   like.values.device)
 
+    def ws_args(self):
+        return ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel()
+
 
 def _initial_capacity(dphi):
-    # nnz can grow by one ring per step; leave ample headroom so overflow
-    # (which costs a re-run) is rare; growth is still by >= 1.2x
+    # nnz can grow by one vertex ring per step; leave headroom so a regrow
+    # (which costs a re-run of the compaction) is rare; growth is >= 1.2x
     return max(2 * dphi.nnz + dphi.n_cols // 8, 1024)
 
 
@@ -392,13 +413,26 @@ def _raise_step_error(rec, field_step_count):
         raise NumericalBlowupError(int(rec["nan_col"]), field_step_count + 1)
 
 
+def _compact(tiled, out, precision, ws, stream):
+    """Tiled -> canonical through ft_compact (fresh statistics record)."""
+    torch = _torch()
+    rec_buf = torch.zeros(_lib.STATS_BYTES, dtype=torch.uint8, device=out.values.device)
+    t_c, o_c = tiled.ft_tiled(), out.ft_csc()
+    wp, wn = ws.ws_args()
+    _check(_lib.lib().ft_compact(ctypes.byref(t_c), ctypes.byref(o_c), _ft_dtype(precision),
+                                 wp, wn, ctypes.c_void_p(rec_buf.data_ptr()), stream),
+           "ft_compact")
+    return _stats_from_bytes(rec_buf.cpu().numpy().tobytes())[0]
+
+
 # ---------------------------------------------------------------------------
 # step / evolve
 
 
 def step(field, lap, params, workspace=None):
     """One explicit Euler step; returns ``(new_field, StepStats)``
-    (field.py:198-286), executed as one fused GPU kernel."""
+    (field.py:198-286).  Runs the fused kernel into a tiled work buffer and
+    compacts the result into a canonical CSC (ft_step)."""
     torch = _torch()
     params.validate()
     ws = workspace if workspace is not None else StepWorkspace()
@@ -409,6 +443,7 @@ def step(field, lap, params, workspace=None):
     device = dphi.values.device
     dl = device_laplacian(lap, field.precision)
     ws.prepare(n_v, device)
+    scratch = ws.tiled_buffer("a", dphi, dphi.nnz)
     out = ws.take_output(dphi, _initial_capacity(dphi))
     reallocs = ws.realloc_count
     ws.realloc_count = 0
@@ -416,23 +451,29 @@ def step(field, lap, params, workspace=None):
     prm = params.ft_params()
     stream = _stream_handle()
     lib = _lib.lib()
+    wp, wn = ws.ws_args()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     while True:
-        in_c = dphi.ft_csc()
-        out_c = out.ft_csc()
+        in_c, sc_c, out_c = dphi.ft_csc(), scratch.ft_tiled(), out.ft_csc()
         ev0.record()
-        rc = lib.ft_step(ctypes.byref(lap_c), dl.flags, ctypes.byref(in_c),
-                         ctypes.byref(out_c), _ft_dtype(field.precision),
-                         ctypes.byref(prm), ctypes.c_void_p(ws.ws.data_ptr()),
-                         ws.ws.numel(), ctypes.c_void_p(ws.stats.data_ptr()), stream)
+        rc = lib.ft_step(ctypes.byref(lap_c), dl.flags, ctypes.byref(in_c), ctypes.byref(sc_c),
+                         ctypes.byref(out_c), _ft_dtype(field.precision), ctypes.byref(prm),
+                         wp, wn, ctypes.c_void_p(ws.stats.data_ptr()), stream)
         ev1.record()
         _check(rc, "ft_step")
         rec = _stats_from_bytes(ws.stats.cpu().numpy().tobytes())[0]
-        if int(rec["status"]) == _lib.FT_STATUS_OVERFLOW:
-            out.grow(int(rec["nnz_phi"]))
+        status = int(rec["status"])
+        if status == _lib.FT_STATUS_OVERFLOW:
+            scratch.grow(int(rec["needed"]) + int(rec["needed"]) // 5)
             reallocs += 1
             continue
+        if status == _lib.FT_STATUS_OUT_OVERFLOW:
+            out.grow(int(rec["needed"]))
+            reallocs += 1
+            rc2 = _compact(scratch, out, field.precision, ws, stream)
+            if int(rc2["status"]) != _lib.FT_STATUS_OK:
+                raise BackendError("compaction failed after growing the output")
         break
     _raise_step_error(rec, field.step_count)
     out.nnz = int(rec["nnz_phi"])
@@ -450,8 +491,10 @@ def evolve(field, lap, params, max_steps=1000, tol=1e-4, workspace=None, on_step
 
     Converged: max_delta < tol and base mass < 1e-9 per vertex.  Without an
     ``on_step`` callback the whole loop runs on the device (``ft_evolve``):
-    the stop test is evaluated by the GPU after every step and statistics are
-    read back once.  The caller's input field is never recycled.
+    the stop test is evaluated by the GPU after every step, the field stays
+    in tiled form between steps and is compacted once at the end, and the
+    statistics are read back once.  The caller's input field is never
+    recycled.
     """
     if max_steps < 1:
         raise ShapeError("max_steps must be >= 1")
@@ -488,36 +531,37 @@ def _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold):
     device = src.values.device
     dl = device_laplacian(lap, field.precision)
     ws.prepare(n_v, device)
-    cap = _initial_capacity(src)
-    a = src.clone(capacity=cap)               # the caller's buffer stays intact
-    b = ws.take_output(src, cap)
+    wa = ws.tiled_buffer("a", src, src.nnz)
+    wb = ws.tiled_buffer("b", src, src.nnz)
+    out = ws.take_output(src, _initial_capacity(src))
     trace_dev = torch.zeros(max_steps * _lib.STATS_BYTES, dtype=torch.uint8, device=device)
-    control = torch.zeros(4, dtype=torch.int64, device=device)
+    control = torch.zeros(6, dtype=torch.int64, device=device)
     lap_c = dl.lap_t[field.precision].ft_csc()
     prm = params.ft_params()
     stream = _stream_handle()
     lib = _lib.lib()
+    wp, wn = ws.ws_args()
     trace = []
     done = 0
     reallocs = 0
+    cur = src
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     while True:
         remaining = max_steps - done
-        a_c, b_c = a.ft_csc(), b.ft_csc()
+        s_c, a_c, b_c, o_c = cur.ft_csc(), wa.ft_tiled(), wb.ft_tiled(), out.ft_csc()
         ev0.record()
-        rc = lib.ft_evolve(ctypes.byref(lap_c), dl.flags, ctypes.byref(a_c), ctypes.byref(b_c),
-                           _ft_dtype(field.precision), ctypes.byref(prm), remaining,
-                           float(tol), float(base_threshold), ctypes.c_void_p(ws.ws.data_ptr()),
-                           ws.ws.numel(), ctypes.c_void_p(trace_dev.data_ptr()),
+        rc = lib.ft_evolve(ctypes.byref(lap_c), dl.flags, ctypes.byref(s_c), ctypes.byref(a_c),
+                           ctypes.byref(b_c), ctypes.byref(o_c), _ft_dtype(field.precision),
+                           ctypes.byref(prm), remaining, float(tol), float(base_threshold),
+                           wp, wn, ctypes.c_void_p(trace_dev.data_ptr()),
                            ctypes.c_void_p(control.data_ptr()), stream)
         ev1.record()
         _check(rc, "ft_evolve")
         ctl = control.cpu().numpy()
-        n, status = int(ctl[0]), int(ctl[1])
-        recs = _stats_from_bytes(trace_dev[:(n + 1) * _lib.STATS_BYTES].cpu().numpy().tobytes()
-                                 if n < remaining else
-                                 trace_dev[:n * _lib.STATS_BYTES].cpu().numpy().tobytes())
+        n, status, compacted = int(ctl[0]), int(ctl[1]), int(ctl[3])
+        nrec = min(n + 1, remaining)
+        recs = _stats_from_bytes(trace_dev[:nrec * _lib.STATS_BYTES].cpu().numpy().tobytes())
         per_step = ev0.elapsed_time(ev1) * 1e-3 / max(n, 1)
         for k in range(n):
             r = recs[k]
@@ -525,21 +569,33 @@ def _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold):
                                    base_mass=float(r["base_mass"]), spgemm_time=per_step,
                                    nnz_skel=int(r["nnz_skel"]),
                                    converged=int(r["status"]) == _lib.FT_STATUS_CONVERGED))
-        cur, other = (a, b) if n % 2 == 0 else (b, a)
         done += n
-        if n:
-            cur.nnz = int(recs[n - 1]["nnz_phi"])
-        if status == _lib.FT_STATUS_OVERFLOW:
-            other.grow(int(ctl[2]))
-            reallocs += 1
-            a, b = cur, other
-            continue
+        if n > 0:
+            last_tiled = wa if n % 2 == 1 else wb
+            if compacted == 2:          # canonical output too small
+                out.grow(int(ctl[4]))
+                reallocs += 1
+                if int(_compact(last_tiled, out, field.precision, ws, stream)["status"]) != 0:
+                    raise BackendError("compaction failed after growing the output")
+            out.nnz = int(ctl[4])
+            if cur is not src:
+                ws.spare = cur
+            cur = out
         if status in (_lib.FT_STATUS_NAN, _lib.FT_STATUS_PATTERN):
             _raise_step_error(recs[n], field.step_count + done)
+        if status == _lib.FT_STATUS_OVERFLOW:
+            need = int(recs[n]["needed"])
+            wa.grow(need + need // 5)
+            wb.grow(need + need // 5)
+            reallocs += 1
+            if n > 0:
+                out = ws.take_output(cur, _initial_capacity(cur))
+            continue
         break
     if trace:
         trace[-1].realloc_count = reallocs
-    ws.spare = other
+    if cur is src:                      # no step completed (cannot happen without error)
+        cur = src.clone()
     return LayeredField(cur, field.seed_vertices, field.step_count + done), trace
 
 

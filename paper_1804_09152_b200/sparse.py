@@ -287,3 +287,37 @@ class DeviceCSC:
     def __repr__(self):
         return (f"DeviceCSC({self.n_rows}x{self.n_cols}, nnz={self.nnz}, "
                 f"capacity={self.capacity}, {self.values.dtype})")
+
+
+class DeviceTiled:
+    """Tiled working storage of a field on the GPU (``ft_tiled`` in
+    include/fieldtess_cuda.h): per-column (start, count) descriptors, entries
+    in per-tile slots plus an overflow pool.  Used between Euler steps."""
+
+    __slots__ = ("n_rows", "n_cols", "desc", "row_idx", "values")
+
+    def __init__(self, n_rows, n_cols, capacity, dtype, device):
+        torch = _torch()
+        self.n_rows = int(n_rows)
+        self.n_cols = int(n_cols)
+        self.desc = torch.zeros(2 * max(n_cols, 1), dtype=torch.int32, device=device)
+        self.row_idx = torch.empty(int(capacity), dtype=torch.int32, device=device)
+        self.values = torch.empty(int(capacity), dtype=dtype, device=device)
+
+    @property
+    def capacity(self):
+        return int(self.row_idx.numel())
+
+    def grow(self, needed):
+        torch = _torch()
+        if self.capacity >= needed:
+            return False
+        new_cap = max(int(needed), int(math.ceil(self.capacity * GROWTH)))
+        self.row_idx = torch.empty(new_cap, dtype=torch.int32, device=self.row_idx.device)
+        self.values = torch.empty(new_cap, dtype=self.values.dtype, device=self.values.device)
+        return True
+
+    def ft_tiled(self):
+        from ._lib import FtTiled
+        return FtTiled(self.n_rows, self.n_cols, self.desc.data_ptr(), self.row_idx.data_ptr(),
+                       self.values.data_ptr(), self.capacity)

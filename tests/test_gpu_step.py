@@ -174,6 +174,24 @@ def test_overflow_regrows_and_matches(monkeypatch):
     assert_csc_equal(out2.phi, ref2)
 
 
+def test_tiled_pool_overflow_regrows(monkeypatch):
+    """Tiles whose entries exceed their slot go to the pool; an empty pool
+    must overflow, be grown, and the result still match bitwise."""
+    from paper_1804_09152_b200 import field as fmod
+    monkeypatch.setattr(fmod, "POOL_FRACTION", 0.0)
+    monkeypatch.setattr(fmod, "POOL_MIN", 0)
+    g = golden_npz("step_cases.npz")
+    inp = csc_from(g, "wide12_in")
+    lap = _Lap(csc_from(g, "wide12_lapt"))
+    fld = ft.LayeredField(as_sparse(inp), np.arange(inp.n_rows - 1))
+    out, st = ft.step(fld, lap, DEFAULT)
+    assert st.realloc_count >= 1
+    assert_csc_equal(out.phi, csc_from(g, "wide12_out"))
+    out2, trace = ft.evolve(fld, lap, DEFAULT, max_steps=6, tol=0.0)
+    ref2, _ = po.evolve_c(po.Csc.of(inp), csc_from(g, "wide12_lapt"), DEFAULT, 6)
+    assert_csc_equal(out2.phi, ref2)
+
+
 def test_converged_input_returns_after_one_step():
     mesh = ft.gen_periodic_grid(9, 9)
     lap = ft.build_laplacian(mesh)
@@ -192,9 +210,10 @@ def test_evolve_input_stays_valid_and_on_step():
     before = fld.phi.to_dense()
     seen = []
     out, trace = ft.evolve(fld, lap, DEFAULT, max_steps=30, on_step=lambda f, s: seen.append(f.step_count))
-    assert seen == list(range(1, 31)) and len(trace) == 30
+    assert seen == list(range(1, len(trace) + 1))
     assert np.array_equal(fld.phi.to_dense(), before)
-    out2, _ = ft.evolve(fld, lap, DEFAULT, max_steps=30)
+    out2, trace2 = ft.evolve(fld, lap, DEFAULT, max_steps=30)
+    assert len(trace2) == len(trace) and trace2[-1].converged == trace[-1].converged
     assert np.array_equal(out.phi.to_dense(), out2.phi.to_dense())
 
 
