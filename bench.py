@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""Headline benchmark: the fused layered-field Euler step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--precision exact|fast]
+                    [--impl ours|reference]
+
+Workload (BASELINE.json configs[2], the config the time-step metric is
+quoted on): synthetic torus grid 3200 x 3125 (10,000,000 vertices, order-
+identical to the reference generator), 4,096 seeds drawn with
+numpy.random.default_rng(0), CouplingParams() defaults, uniform Laplacian.
+One "step" is one explicit Euler step of the whole field.  W untimed steps
+from init_field, then K timed steps (steps W+1..W+K), inputs resident in
+HBM, then the compaction to canonical CSC -- all on one stream, bracketed by
+barrier + synchronize, timed with CUDA events, max over ranks.  The working
+set (L^T indices ~280 MB + PHI ~130 MB) exceeds the 126 MB L2, so no flush
+is needed between steps.
+
+Reported beside `value` (steps/s):
+  roofline      the fused kernel's algorithmic bytes per launch (reference
+                data structures: L^T CSR + PHI_in CSC + PHI_out CSC; L values
+                not counted because the uniform path never reads them) over
+                its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs;
+  e2e           the public API end to end: host (pinned) field in ->
+                evolve(K steps) -> field + labels back on the host;
+  cpu_baseline  the reference package (numba, all host cores) timed on a
+                bounded sample of the same workload (rank 0, N=1).
+--impl reference runs only the reference CPU implementation and prints its
+line (rank 0; other ranks exit 0).
+
+N > 1 (torchrun): each rank runs its own replica of the workload on its GPU
+(weak scaling, no data-path collective); the vertex-partitioned halo
+exchange path is not yet in this build.
+"""
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+NX, NY, N_SEEDS = 3200, 3125, 4096
+
+
+def workload_name(args):
+    tag = "C3: " if (args.nx, args.ny, args.seeds) == (NX, NY, N_SEEDS) else ""
+    return (f"{tag}torus {args.nx}x{args.ny} ({args.nx * args.ny:,} vertices), "
+            f"{args.seeds:,} seeds, fused Euler step")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=80)
+    ap.add_argument("--precision", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nx", type=int, default=NX)
+    ap.add_argument("--ny", type=int, default=NY)
+    ap.add_argument("--seeds", type=int, default=N_SEEDS)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="bounded CPU-baseline sample (seconds of reference steps)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def build_workload(nx, ny, n_seeds):
+    import paper_1804_09152_b200 as ft
+    mesh = ft.gen_periodic_grid(nx, ny)
+    lap = ft.build_laplacian(mesh)
+    seeds = np.random.default_rng(0).choice(mesh.n_vertices, n_seeds, replace=False)
+    return mesh, lap, seeds
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[4 + k].lower() == "active"})
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# the reference CPU implementation (oracle/_ref: the reference package
+# itself, numba on all host cores; else the plain-C oracle port)
+
+
+def load_reference():
+    path = os.path.join(REPO, "oracle", "_ref", "py")
+    if os.path.isdir(os.path.join(path, "fieldtess")):
+        os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "ft_numba_cache"))
+        sys.path.insert(0, path)
+        import fieldtess
+        return fieldtess
+    return None
+
+
+def reference_steps_per_sec(phi_host, lap, seeds, n_max, budget_s, label):
+    """Time the reference's own `step` (shared StepWorkspace, like evolve)
+    from `phi_host` for up to n_max steps / budget_s seconds."""
+    ref = load_reference()
+    if ref is not None:
+        import numba
+        from fieldtess.field import StepWorkspace
+        # JIT warm-up on a tiny grid (reference conftest.py:7-16)
+        m6 = ref.gen_periodic_grid(6, 6)
+        ref.evolve(ref.init_field(m6, [0]), ref.build_laplacian(m6), ref.CouplingParams(), max_steps=3)
+        rphi = ref.SparseMat(phi_host.n_rows, phi_host.n_cols, phi_host.col_ptr,
+                             phi_host.row_idx[:phi_host.nnz], phi_host.values[:phi_host.nnz], check=False)
+        rmat_t = ref.SparseMat(lap.mat_t.n_rows, lap.mat_t.n_cols, lap.mat_t.col_ptr,
+                               lap.mat_t.row_idx, lap.mat_t.values, check=False)
+        rmat = ref.SparseMat(lap.mat.n_rows, lap.mat.n_cols, lap.mat.col_ptr,
+                             lap.mat.row_idx, lap.mat.values, check=False)
+        rlap = ref.Laplacian(mat=rmat, mat_t=rmat_t, scheme="uniform")
+        fld = ref.LayeredField(rphi, seeds)
+        ws = StepWorkspace()
+        fld, _ = ref.step(fld, rlap, ref.CouplingParams(), workspace=ws)   # untimed first step
+        n = 0
+        t0 = time.perf_counter()
+        while n < n_max:
+            fld, _ = ref.step(fld, rlap, ref.CouplingParams(), workspace=ws)
+            n += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+        return {"value": n / dt, "unit": "steps/s", "cores": int(numba.get_num_threads()),
+                "kind": "reference",
+                "sample": f"{n} reference field.step calls ({label}), numba "
+                          f"{numba.__version__}, {numba.get_num_threads()} threads, "
+                          f"CPU {os.cpu_count()} logical cores"}
+    # fall back: the plain-C restatement (OpenMP over columns)
+    from oracle import pyoracle as po
+    import paper_1804_09152_b200 as ft
+    cores = os.cpu_count() or 1
+    cur = po.Csc.of(phi_host)
+    lapt = po.Csc.of(lap.mat_t)
+    cur, _ = po.step_c(cur, lapt, ft.CouplingParams(), n_threads=cores)
+    n = 0
+    t0 = time.perf_counter()
+    while n < n_max:
+        cur, _ = po.step_c(cur, lapt, ft.CouplingParams(), n_threads=cores)
+        n += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "steps/s", "cores": cores, "kind": "port",
+            "sample": f"{n} steps of the C oracle port ({label}), {cores} OpenMP threads"}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_1804_09152_b200 as ft
+    mesh, lap, seeds = build_workload(args.nx, args.ny, args.seeds)
+    phi0 = ft.init_field(mesh, seeds).phi          # host numpy, identical to the reference's
+    res = reference_steps_per_sec(phi0, lap, seeds, max(1, args.steps), 60.0,
+                                  "steps 2.. from init_field; mesh/L^T/PHI0 built by the "
+                                  "bitwise-identical vectorised generators")
+    line = {"impl": "reference", "metric": "time-steps/sec (fused Euler step)",
+            "value": res["value"], "unit": "steps/s", "higher_is_better": True,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 / res["value"], "dtype": "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None,
+            "config": {"workload": workload_name(args), "precision": "f64 (reference)"},
+            "cpu_baseline": res,
+            "e2e": {"value": res["value"], "unit": "steps/s",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def algorithmic_bytes(n_v, nnz_l, nnz_in, nnz_out, value_bytes, lap_values=False):
+    """compulsory traffic of the reference data structures.
+    L^T CSR (indices only when the uniform path skips the values), PHI in
+    and PHI out CSC."""
+    lb = 4 * (n_v + 1) + (4 + (value_bytes if lap_values else 0)) * nnz_l
+    return lb + 2 * 4 * (n_v + 1) + (4 + value_bytes) * (nnz_in + nnz_out)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1804_09152_b200 as ft
+    from paper_1804_09152_b200 import _lib, field as F
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    params = ft.CouplingParams()
+    mesh, lap, seeds = build_workload(args.nx, args.ny, args.seeds)
+    n_v = mesh.n_vertices
+    prec = args.precision
+    vbytes = 8 if prec == "exact" else 4
+    fld0 = ft.init_field(mesh, seeds, precision=prec)
+    warm = max(3, args.warmup)
+    cur, _ = ft.evolve(fld0, lap, params, max_steps=warm, tol=0.0)
+    dphi = cur.device_phi()
+    dev = dphi.values.device
+    ws = ft.StepWorkspace()
+    ws.prepare(n_v, dev)
+    cap = int(_lib.lib().ft_tiled_min_capacity(n_v)) + 2 * dphi.nnz
+    ta = ft.DeviceTiled(dphi.n_rows, n_v, cap, dphi.values.dtype, dev)
+    tb = ft.DeviceTiled(dphi.n_rows, n_v, cap, dphi.values.dtype, dev)
+    out = ft.DeviceCSC.allocate(dphi.n_rows, n_v, 3 * dphi.nnz, dphi.values.dtype, dev)
+    dl = F.device_laplacian(lap, prec)
+    lib = _lib.lib()
+    lap_c = dl.lap_t[prec].ft_csc()
+    prm = params.ft_params()
+    dt_code = F._ft_dtype(prec)
+    wp, wn = ws.ws_args()
+    K = args.steps
+    trace = torch.zeros(K * _lib.STATS_BYTES, dtype=torch.uint8, device=dev)
+    comp_rec = torch.zeros(_lib.STATS_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    sh = ctypes.c_void_p(stream.cuda_stream)
+    src_c = dphi.ft_csc()
+    ta_c, tb_c, out_c = ta.ft_tiled(), tb.ft_tiled(), out.ft_csc()
+    evk = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+
+    def one_step(k):
+        dst = ta_c if k % 2 == 0 else tb_c
+        src_t = tb_c if k % 2 == 0 else ta_c
+        canon = ctypes.byref(src_c) if k == 0 else None
+        tiled = None if k == 0 else ctypes.byref(src_t)
+        evk[k][0].record(stream)
+        rc = lib.ft_step_kernel(ctypes.byref(lap_c), dl.flags, canon, tiled, ctypes.byref(dst), dt_code,
+                                ctypes.byref(prm), wp, wn, sh)
+        evk[k][1].record(stream)
+        rc |= lib.ft_step_fixup(ctypes.byref(lap_c), dl.flags, canon, tiled, ctypes.byref(dst), dt_code,
+                                ctypes.byref(prm), wp, wn, sh)
+        rc |= lib.ft_step_finalize(wp, wn, n_v, dst.capacity,
+                                   ctypes.c_void_p(trace.data_ptr() + k * _lib.STATS_BYTES), sh)
+        if rc:
+            raise RuntimeError(_lib.last_error())
+
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e_start.record(stream)
+    for k in range(K):
+        one_step(k)
+    last = ta_c if (K - 1) % 2 == 0 else tb_c
+    rc = lib.ft_compact(ctypes.byref(last), ctypes.byref(out_c), dt_code, wp, wn,
+                        ctypes.c_void_p(comp_rec.data_ptr()), sh)
+    e_end.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if rc:
+        raise RuntimeError(_lib.last_error())
+    recs = np.frombuffer(trace.cpu().numpy().tobytes(), dtype=_lib.STATS_DTYPE)
+    bad = [int(r["status"]) for r in recs if int(r["status"]) != 0]
+    if bad:
+        raise RuntimeError(f"step status {bad[:3]} in the timed region")
+    crec = np.frombuffer(comp_rec.cpu().numpy().tobytes(), dtype=_lib.STATS_DTYPE)[0]
+    if int(crec["status"]) != 0:
+        raise RuntimeError("compaction overflow in the timed region")
+    elapsed_ms = e_start.elapsed_time(e_end)
+    kern_ms = np.array([a.elapsed_time(b) for a, b in evk])
+    elapsed_ms = allmax(elapsed_ms)
+    nnz_in = [dphi.nnz] + [int(r["nnz_phi"]) for r in recs[:-1]]
+    nnz_out = [int(r["nnz_phi"]) for r in recs]
+    skel = sum(int(r["nnz_skel"]) for r in recs)
+    nnz_l = lap.mat_t.nnz
+    uniform = dl.flags == _lib.FT_LAP_UNIFORM
+    alg = np.array([algorithmic_bytes(n_v, nnz_l, a, b, vbytes, lap_values=not uniform)
+                    for a, b in zip(nnz_in, nnz_out)], dtype=np.float64)
+    achieved = float(alg.sum() / (kern_ms.sum() * 1e-3) / 1e9)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "step_kernel_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            if tj.get("precision") == prec and tj.get("n_vertices") == n_v:
+                traffic = tj.get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            pass
+
+    # ---- e2e through the public API ----------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        host0 = fld0.phi
+        nnz0 = host0.nnz
+        pinned = [torch.empty(a.size, dtype=t, pin_memory=True)
+                  for a, t in ((host0.col_ptr, torch.int32), (host0.row_idx[:nnz0], torch.int32),
+                               (host0.values[:nnz0], torch.float64))]
+        pinned[0].numpy()[:] = host0.col_ptr
+        pinned[1].numpy()[:] = host0.row_idx[:nnz0]
+        pinned[2].numpy()[:] = host0.values[:nnz0]
+        hphi = ft.SparseMat(host0.n_rows, n_v, pinned[0].numpy(), pinned[1].numpy(),
+                            pinned[2].numpy(), check=False)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        fin, tr = ft.evolve(ft.LayeredField(hphi, seeds, precision=prec), lap, params,
+                            max_steps=K, tol=0.0)
+        phi_back = fin.phi
+        labels = ft.sharp_labels(fin)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        barrier()
+        e2e_s = allmax(t1 - t0)
+        h2d = 4 * (n_v + 1) + (4 + vbytes) * nnz0
+        d2h = 4 * (n_v + 1) + 12 * phi_back.nnz + 8 * labels.size + _lib.STATS_BYTES * len(tr)
+        e2e = {"value": world * K / e2e_s, "unit": "steps/s",
+               "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K),
+               "path": "evolve(host field, K steps) -> field.phi + sharp_labels on the host; "
+                       "steps 1..K from init_field; L^T resident (uploaded once per mesh)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        snap = cur.phi                       # EXACT: bitwise the reference's state at step W
+        cpu = reference_steps_per_sec(snap, lap, seeds, K, args.cpu_seconds,
+                                      f"steps {warm + 2}.. of this workload")
+
+    if rank == 0:
+        value = world * K / (elapsed_ms * 1e-3)
+        line = {
+            "metric": "time-steps/sec (fused Euler step); layer-nnz updates/sec; HBM GB/s vs roofline",
+            "value": value, "unit": "steps/s", "n_gpus": world, "steps": K, "warmup": warm,
+            "ms_per_step": elapsed_ms / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64" if prec == "exact" else "f32-storage/f64-arith",
+            "data": "synthetic",
+            "config": {"workload": workload_name(args), "mesh": f"torus {args.nx}x{args.ny}", "n_vertices": n_v,
+                       "seeds": args.seeds, "precision": prec, "laplacian": "uniform",
+                       "parallelism": "single GPU" if world == 1 else f"{world} replicas",
+                       "l2": "working set > 126 MB L2 (no flush needed)",
+                       "window": f"steps {warm + 1}..{warm + K} from init_field"},
+            "layer_nnz_updates_per_s": world * skel / (elapsed_ms * 1e-3),
+            "kernel_ms_per_step": float(kern_ms.mean()),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "ft::step_kernel (fused SpGEMM+skeleton+update+normalise)",
+                         "bytes_per_launch": float(alg.mean()), "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk,
+            "gpu_launches": 3 * K + 3,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -150,14 +150,22 @@ int ft_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
             const ft_params* params, void* workspace, size_t ws_bytes,
             ft_step_stats* stats, void* stream);
 
-/* The fused kernel alone (bench.py times it with CUDA events): one step
- * from `in_canon` (if non-null) or `in_tiled` into the tiled `out`.
- * Statistics accumulate in the workspace until ft_step_finalize reduces
- * them into `stats` and resets the accumulators. */
+/* The three launches of one step, for callers that time the fused kernel
+ * on its own (bench.py brackets ft_step_kernel with CUDA events):
+ *   ft_step_kernel   the fused kernel, from `in_canon` (if non-null) or
+ *                    `in_tiled` into the tiled `out`; columns whose layer
+ *                    union exceeds the register window are queued;
+ *   ft_step_fixup    the queued columns (same arguments);
+ *   ft_step_finalize reduces the workspace accumulators into `stats`.
+ * ft_step / ft_evolve issue exactly this sequence. */
 int ft_step_kernel(const ft_csc* lap_t, int32_t lap_flags,
                    const ft_csc* in_canon, const ft_tiled* in_tiled,
                    ft_tiled* out, int32_t dtype, const ft_params* params,
                    void* workspace, size_t ws_bytes, void* stream);
+int ft_step_fixup(const ft_csc* lap_t, int32_t lap_flags,
+                  const ft_csc* in_canon, const ft_tiled* in_tiled,
+                  ft_tiled* out, int32_t dtype, const ft_params* params,
+                  void* workspace, size_t ws_bytes, void* stream);
 int ft_step_finalize(void* workspace, size_t ws_bytes, int32_t n_vertices,
                      int64_t tiled_capacity, ft_step_stats* stats, void* stream);
 

@@ -80,7 +80,7 @@ assert STATS_DTYPE.itemsize == STATS_BYTES
 # every symbol include/fieldtess_cuda.h declares
 EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
            "ft_workspace_init", "ft_tile_slot_entries", "ft_tiled_min_capacity",
-           "ft_step", "ft_step_kernel", "ft_step_finalize", "ft_compact",
+           "ft_step", "ft_step_kernel", "ft_step_fixup", "ft_step_finalize", "ft_compact",
            "ft_evolve", "ft_labels")
 
 _lib = None
@@ -109,6 +109,8 @@ def _declare(lib):
                                    P(FtTiled), ctypes.c_int32, P(FtParams), vp,
                                    ctypes.c_size_t, vp]
     lib.ft_step_kernel.restype = ctypes.c_int
+    lib.ft_step_fixup.argtypes = lib.ft_step_kernel.argtypes
+    lib.ft_step_fixup.restype = ctypes.c_int
     lib.ft_step_finalize.argtypes = [vp, ctypes.c_size_t, ctypes.c_int32, ctypes.c_int64,
                                      vp, vp]
     lib.ft_step_finalize.restype = ctypes.c_int

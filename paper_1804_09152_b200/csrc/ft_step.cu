@@ -1144,10 +1144,11 @@ static int window_size() {
     return g_window;
 }
 
+// which = 1: fused kernel, 2: fixup kernel, 3: both
 static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_canon,
                        const ft_tiled* in_tiled, ft_tiled* out, int32_t dtype,
                        const ft_params* prm, void* workspace, size_t ws_bytes, int check_done,
-                       cudaStream_t s) {
+                       cudaStream_t s, int which = 3) {
     if (!lap_t || !out || !prm || !workspace) return set_err(FT_ERR_ARG, "null argument");
     if (dtype != FT_F64 && dtype != FT_F32) return set_err(FT_ERR_ARG, "bad dtype");
     const int n_rows = in_canon ? in_canon->n_rows : (in_tiled ? in_tiled->n_rows : -1);
@@ -1181,9 +1182,9 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_
     const bool uni = lap_flags == FT_LAP_UNIFORM;
     ft::StepKernelFn k = window_size() == 8 ? ft::pick_kernel<8>(dtype, uni, in_canon != nullptr)
                                             : ft::pick_kernel<4>(dtype, uni, in_canon != nullptr);
-    k<<<p.num_tiles, FT_TPB, 0, s>>>(p);
+    if (which & 1) k<<<p.num_tiles, FT_TPB, 0, s>>>(p);
     ft::StepKernelFn fx = ft::pick_fixup(dtype, uni, in_canon != nullptr);
-    fx<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
+    if (which & 2) fx<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
     return cuda_check("step kernel");
 }
 
@@ -1209,7 +1210,15 @@ extern "C" int ft_step_kernel(const ft_csc* lap_t, int32_t lap_flags, const ft_c
                               const ft_params* params, void* workspace, size_t ws_bytes,
                               void* stream) {
     return launch_step(lap_t, lap_flags, in_canon, in_tiled, out, dtype, params, workspace, ws_bytes,
-                       0, (cudaStream_t)stream);
+                       0, (cudaStream_t)stream, 1);
+}
+
+extern "C" int ft_step_fixup(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_canon,
+                             const ft_tiled* in_tiled, ft_tiled* out, int32_t dtype,
+                             const ft_params* params, void* workspace, size_t ws_bytes,
+                             void* stream) {
+    return launch_step(lap_t, lap_flags, in_canon, in_tiled, out, dtype, params, workspace, ws_bytes,
+                       0, (cudaStream_t)stream, 2);
 }
 
 extern "C" int ft_step_finalize(void* workspace, size_t ws_bytes, int32_t n_vertices,

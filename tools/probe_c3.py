@@ -33,6 +33,9 @@ for prec in ("exact", "fast"):
                                 ctypes.byref(prm), wp, wn, st)
         e1.record()
         assert rc == 0, _lib.last_error()
+        lib.ft_step_fixup(ctypes.byref(lc), dl.flags, ctypes.byref(src_c) if i == 0 else None,
+                          None if i == 0 else ctypes.byref(ic), ctypes.byref(oc), F._ft_dtype(prec),
+                          ctypes.byref(prm), wp, wn, st)
         if i == 40:
             torch.cuda.synchronize()
             slow_tiles = int(ws.ws[56:60].cpu().view(torch.int32).item())
