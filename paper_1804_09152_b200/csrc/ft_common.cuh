@@ -40,11 +40,16 @@ static_assert(sizeof(Control) % 16 == 0, "Control must stay 16B aligned");
 struct Workspace {
     Control*      ctl;
     double*       tile_bm;      // [num_tiles] per-tile base mass (fast path)
-    double*       tile_bm_slow; // [num_tiles] per-tile base mass (fixup path)
+    double*       tile_bm_slow; // [2 * num_tiles] per-half-tile base mass (fixup path)
     unsigned int* slow_mask;    // [num_tiles * FT_WARPS] columns left to the fixup
     int*          slow_list;    // [num_tiles] tiles queued for the fixup
     long long*    chunk_off;    // [num_chunks + 2] compaction chunk offsets
-    double*       fin_part;     // [64] finalize partial sums
+    double*       fin_part;     // [64] finalize partial sums (base mass)
+    double*       fin_maxd;     // [64] finalize partial maxima
+    long long*    fin_cnt;      // [64] finalize partial nnz
+    long long*    fin_skel;     // [64] finalize partial skeleton nnz
+    double*       tile_maxd;    // [num_tiles] per-tile max |delta| (fast path)
+    int2*         tile_cs;      // [num_tiles] per-tile (nnz, skeleton nnz) (fast path)
     int           num_tiles;
     int           num_chunks;
 };
@@ -54,8 +59,9 @@ __host__ __device__ inline int num_chunks_for(int n_v) { return (n_v + FT_CCH - 
 
 inline size_t workspace_bytes(int n_v) {
     size_t t = (size_t)num_tiles_for(n_v), c = (size_t)num_chunks_for(n_v);
-    return sizeof(Control) + 2 * t * sizeof(double) + t * FT_WARPS * sizeof(unsigned int) +
-           t * sizeof(int) + (c + 2) * sizeof(long long) + 64 * sizeof(double) + 256;
+    return sizeof(Control) + 3 * t * sizeof(double) + t * FT_WARPS * sizeof(unsigned int) +
+           t * sizeof(int) + (c + 2) * sizeof(long long) + 4 * 64 * sizeof(double) +
+           t * (sizeof(double) + sizeof(int2)) + 512;
 }
 
 inline Workspace carve_workspace(void* base, int n_v) {
@@ -68,11 +74,21 @@ inline Workspace carve_workspace(void* base, int n_v) {
     w.tile_bm = (double*)p;
     p += (size_t)w.num_tiles * sizeof(double);
     w.tile_bm_slow = (double*)p;
-    p += (size_t)w.num_tiles * sizeof(double);
+    p += 2 * (size_t)w.num_tiles * sizeof(double);
     w.chunk_off = (long long*)p;
     p += ((size_t)w.num_chunks + 2) * sizeof(long long);
     w.fin_part = (double*)p;
     p += 64 * sizeof(double);
+    w.fin_maxd = (double*)p;
+    p += 64 * sizeof(double);
+    w.fin_cnt = (long long*)p;
+    p += 64 * sizeof(long long);
+    w.fin_skel = (long long*)p;
+    p += 64 * sizeof(long long);
+    w.tile_maxd = (double*)p;
+    p += (size_t)w.num_tiles * sizeof(double);
+    w.tile_cs = (int2*)p;
+    p += (size_t)w.num_tiles * sizeof(int2);
     w.slow_mask = (unsigned int*)p;
     p += (size_t)w.num_tiles * FT_WARPS * sizeof(unsigned int);
     w.slow_list = (int*)p;

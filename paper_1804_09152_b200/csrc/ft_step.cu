@@ -176,7 +176,7 @@ __device__ __forceinline__ void gather(Win<K>& w, int j, int lo, const StepParam
 
 constexpr int kLPV = 8;                    // staged L entries per vertex (capacity)
 constexpr int kLMAX = FT_TPB * kLPV;       // staged L entries per tile
-constexpr int kEMAX = kLMAX * 2;           // staged PHI entries per tile
+constexpr int kEMAX = kLMAX * 5 / 2;       // staged PHI entries per tile
 
 template <typename T, bool UNIFORM>
 struct Stage {
@@ -704,18 +704,28 @@ __device__ __forceinline__ TileOut tile_epilogue(int cnt, int nskel, double bmv,
 #pragma unroll
         for (int k = 0; k < FT_WARPS; ++k) { tbm = tbm + s_wbm[k]; tmx = fmax(tmx, s_wmax[k]); tsk += s_wskel[k]; }
         *bm_slot = tbm;
-        if (tmx > 0.0) atomicMax(&p.ws.ctl->maxdelta_bits, (unsigned long long)__double_as_longlong(tmx));
-        if (tsk) atomicAdd(&p.ws.ctl->skel_total, (unsigned long long)tsk);
-        if (tile_total) atomicAdd(&p.ws.ctl->nnz_total, (unsigned long long)tile_total);
+        if (POOL_ONLY) {
+            // fixup path (rare): fold into the global accumulators
+            if (tmx > 0.0) atomicMax(&p.ws.ctl->maxdelta_bits, (unsigned long long)__double_as_longlong(tmx));
+            if (tsk) atomicAdd(&p.ws.ctl->skel_total, (unsigned long long)tsk);
+            if (tile_total) atomicAdd(&p.ws.ctl->nnz_total, (unsigned long long)tile_total);
+        } else {
+            // fast path: per-tile slots, reduced by finalize_kernel (no
+            // same-address atomics across the ~10^5 tiles of a step)
+            p.ws.tile_maxd[tile] = tmx;
+            p.ws.tile_cs[tile] = make_int2(tile_total, tsk);
+        }
     }
     __syncthreads();
     o.base = *s_base;
     return o;
 }
 
+extern __shared__ __align__(16) unsigned char ft_dyn_smem[];
+
 template <typename T, int K, bool UNIFORM, bool IN_CANON>
 __global__ void __launch_bounds__(FT_TPB, 5) step_kernel(const StepParams p) {
-    __shared__ Stage<T, UNIFORM> stg;
+    Stage<T, UNIFORM>& stg = *reinterpret_cast<Stage<T, UNIFORM>*>(ft_dyn_smem);
     __shared__ double s_wbm[FT_WARPS];
     __shared__ double s_wmax[FT_WARPS];
     __shared__ int s_wskel[FT_WARPS];
@@ -758,7 +768,8 @@ __global__ void __launch_bounds__(FT_TPB, 5) step_kernel(const StepParams p) {
         unsigned int any_slow = 0;
 #pragma unroll
         for (int k = 0; k < FT_WARPS; ++k) any_slow |= s_wslow[k];
-        p.ws.tile_bm_slow[tile] = 0.0;
+        p.ws.tile_bm_slow[2 * tile] = 0.0;
+        p.ws.tile_bm_slow[2 * tile + 1] = 0.0;
         if (any_slow) {
             const int q = atomicAdd(&p.ws.ctl->slow_count, 1);
             p.ws.slow_list[q] = tile;
@@ -779,48 +790,251 @@ __global__ void __launch_bounds__(FT_TPB, 5) step_kernel(const StepParams p) {
 // and tiles that cannot be staged use the exact windowed global path.  The
 // tile's base mass goes to tile_bm_slow[tile] (fixed reduction order).
 
+// Warp-cooperative exact processing of one column from the stage, used by
+// the fixup kernel for columns whose layer union is wider than the fast
+// path's register window.  Lane k owns the column's k-th (vertex,
+// neighbour) pair (chunks of 32).  Rows are visited in ascending order:
+// each round the warp finds the next row (min over all pairs' entries),
+// then the row's per-pair products are summed in pair order (= ascending
+// u, the reference accumulation order) by a shuffle chain.  No per-column
+// arrays, no width limit.
+struct WarpCol {
+    int e0, e1;       // the column's pairs in the stage
+    int j;            // the column (vertex) id
+    double invdeg;
+};
+
+template <typename T, bool UNIFORM>
+__device__ __forceinline__ WarpCol warp_col(const Stage<T, UNIFORM>& s, int v, int j, const double* recip) {
+    WarpCol c;
+    const int LB = s.rp[0];
+    c.e0 = s.rp[v] - LB;
+    c.e1 = s.rp[v + 1] - LB;
+    c.j = j;
+    const int deg = c.e1 - c.e0 - 1;
+    c.invdeg = deg <= 32 ? recip[deg] : 1.0 / (double)deg;
+    return c;
+}
+
+// smallest row > lo among the column's entries (INT_MAX when none)
+template <typename T, bool UNIFORM>
+__device__ __forceinline__ int warp_next_row(const Stage<T, UNIFORM>& s, const WarpCol& c, int lo, int lane) {
+    int best = INT_MAX;
+    for (int e = c.e0 + lane; e < c.e1; e += 32) {
+        const int2 oc = s.oc[e];
+        for (int f = oc.x; f < oc.x + oc.y; ++f) {
+            const int r = s.er[f];
+            if (r > lo) { if (r < best) best = r; break; }   // rows ascend within a pair
+        }
+    }
+    return __reduce_min_sync(0xffffffffu, best);
+}
+
+// (Lt(r, j), PHI(r, j)) of one row, identical on all lanes
+template <typename T, bool UNIFORM>
+__device__ __forceinline__ void warp_row(const Stage<T, UNIFORM>& s, const WarpCol& c, int r, int lane,
+                                         double& lam, double& phi) {
+    lam = 0.0;
+    phi = 0.0;
+    for (int base = c.e0; base < c.e1; base += 32) {
+        const int e = base + lane;
+        bool has = false;
+        double prod = 0.0, ph = 0.0;
+        bool diag = false;
+        if (e < c.e1) {
+            const int2 oc = s.oc[e];
+            diag = (s.u[e] == c.j);
+            for (int f = oc.x; f < oc.x + oc.y; ++f) {
+                const int rr = s.er[f];
+                if (rr == r) {
+                    ph = (double)s.ev[f];
+                    const double l = UNIFORM ? (diag ? -1.0 : c.invdeg) : (double)s.lv[e];
+                    prod = ph * l;
+                    has = true;
+                    break;
+                }
+                if (rr > r) break;
+            }
+        }
+        const unsigned int hb = __ballot_sync(0xffffffffu, has);
+        const unsigned int db = __ballot_sync(0xffffffffu, has && diag);
+        const int n = min(32, c.e1 - base);
+        for (int k = 0; k < n; ++k) {          // in pair order: exact reference order
+            const double pk = __shfl_sync(0xffffffffu, prod, k);
+            if ((hb >> k) & 1u) lam = lam + pk;
+        }
+        if (db) phi = __shfl_sync(0xffffffffu, ph, __ffs(db) - 1);
+    }
+}
+
+// pass = 0: aggregates; 1: column sum of v; 2: normalise + count; 3: emit
+template <typename T, bool UNIFORM>
+__device__ __forceinline__ void warp_column(const Stage<T, UNIFORM>& s, int v, int j, const StepParams& p,
+                                            const double* recip, VRes& res, long long emit_off) {
+    const int lane = threadIdx.x & 31;
+    const WarpCol c = warp_col<T, UNIFORM>(s, v, j, recip);
+    Agg g;
+    agg_init(g);
+    int lo = -1;
+    for (;;) {
+        const int r = warp_next_row<T, UNIFORM>(s, c, lo, lane);
+        if (r == INT_MAX) break;
+        double lm, ph;
+        warp_row<T, UNIFORM>(s, c, r, lane, lm, ph);
+        const bool in = in_skeleton(ph, lm);
+        if (ph != 0.0 && !in) g.bad_phi_row = r;
+        if (lm != 0.0 && !in) g.bad_lt_row = r;
+        if (in) {
+            if (g.n == 0) { g.first_row = r; g.phi0 = ph; }
+            g.n++;
+            g.sl = g.sl + ((lm != 0.0) ? lm : 0.0);
+            g.sp = g.sp + ph;
+            g.sr = g.sr + sqrt(ph);
+        }
+        lo = r;
+    }
+    res.nskel = g.n;
+    res.bad_phi_row = g.bad_phi_row;
+    res.bad_lt_row = g.bad_lt_row;
+    if (g.n == 0) return;
+    const Coef cf = make_coef(g, p, recip);
+    double sum = 0.0;
+    lo = -1;
+    for (;;) {
+        const int r = warp_next_row<T, UNIFORM>(s, c, lo, lane);
+        if (r == INT_MAX) break;
+        double lm, ph;
+        warp_row<T, UNIFORM>(s, c, r, lane, lm, ph);
+        if (in_skeleton(ph, lm)) sum = sum + update_entry(r, ph, (lm != 0.0) ? lm : 0.0, cf, p, res.nan);
+        lo = r;
+    }
+    const bool spos = sum > 0.0;
+    const double inv = spos ? 1.0 / sum : 0.0;
+    bool dummy = false;
+    T* ov = (T*)p.out_val;
+    lo = -1;
+    for (;;) {
+        const int r = warp_next_row<T, UNIFORM>(s, c, lo, lane);
+        if (r == INT_MAX) break;
+        double lm, ph;
+        warp_row<T, UNIFORM>(s, c, r, lane, lm, ph);
+        if (in_skeleton(ph, lm)) {
+            const double vv = update_entry(r, ph, (lm != 0.0) ? lm : 0.0, cf, p, dummy);
+            const double nv = spos ? vv * inv : vv;
+            if (nv != 0.0) {
+                if (emit_off >= 0 && lane == 0) {
+                    p.out_idx[emit_off] = r;
+                    ov[emit_off] = (T)nv;
+                }
+                if (emit_off >= 0) ++emit_off;
+                res.cnt++;
+                if (r == 0) res.bm = res.bm + nv;
+            }
+            const double dd = fabs(nv - ph);
+            if (dd > res.maxd) res.maxd = dd;
+        }
+        lo = r;
+    }
+}
+
+// fixup kernel: the columns the fast path left behind.  Work unit = half a
+// queued tile (64 columns), staged in shared memory (half tiles fit the
+// stage even in dense bands); one warp per wide column (warp_column).
+// Half tiles that still exceed the stage use the exact windowed
+// global-memory path, one thread per column.
 template <typename T, bool UNIFORM, bool IN_CANON>
 __global__ void __launch_bounds__(FT_TPB) fixup_kernel(const StepParams p) {
-    constexpr int KF = 12;
-    __shared__ Stage<T, UNIFORM> stg;
-    __shared__ double s_wbm[FT_WARPS];
-    __shared__ double s_wmax[FT_WARPS];
-    __shared__ int s_wskel[FT_WARPS];
+    constexpr int HALF = FT_TPB / 2;
+    Stage<T, UNIFORM>& stg = *reinterpret_cast<Stage<T, UNIFORM>*>(ft_dyn_smem);
+    __shared__ int s_list[HALF];
+    __shared__ int s_cnt[HALF];
+    __shared__ int s_skel[HALF];
+    __shared__ double s_bm[HALF];
+    __shared__ double s_mx[HALF];
+    __shared__ int s_ns;
+    __shared__ int s_scan[FT_WARPS];
     __shared__ long long s_base;
     __shared__ double s_recip[33];
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     if (threadIdx.x < 33) s_recip[threadIdx.x] = c_recip[threadIdx.x];
-    const int n_slow = *(volatile int*)&p.ws.ctl->slow_count;
+    const int n_units = 2 * *(volatile int*)&p.ws.ctl->slow_count;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int q = blockIdx.x; q < n_slow; q += gridDim.x) {
-        const int tile = p.ws.slow_list[q];
-        const int j0 = tile * FT_TPB;
-        const int jn = min(FT_TPB, p.n_v - j0);
-        const int j = j0 + tid;
-        const bool mine = (p.ws.slow_mask[(size_t)tile * FT_WARPS + warp] >> lane) & 1u;
-        const bool staged = stage_tile<T, UNIFORM, IN_CANON>(stg, j0, jn, p);
-        Win<KF> w;
-        VRes res;
-        vres_init(res);
-        unsigned int out_mask = 0;
-        bool global_path = false;
-        if (mine) {
-            if (staged) gather_staged<T, KF, UNIFORM>(w, j, stg, s_recip);
-            global_path = !staged || w.more;
-            if (global_path) vertex_slow<T, 8, UNIFORM, IN_CANON>(j, p, res, 0, false);
-            else process_window<KF>(w, p, res, out_mask, s_recip);
-            report_flags(res, j, p);
+    for (int q = blockIdx.x; q < n_units; q += gridDim.x) {
+        const int tile = p.ws.slow_list[q >> 1];
+        const int half = q & 1;
+        const int v0 = half * HALF;
+        const int j0 = tile * FT_TPB + v0;
+        const int jn = max(0, min(HALF, p.n_v - j0));
+        const unsigned int* msk = &p.ws.slow_mask[(size_t)tile * FT_WARPS + half * (HALF / 32)];
+        const unsigned int m0 = msk[0], m1 = msk[1];
+        if ((m0 | m1) == 0u || jn == 0) continue;   // block-uniform
+        if (tid == 0) {
+            int n = 0;
+            for (int v = 0; v < HALF; ++v)
+                if (((v < 32 ? m0 : m1) >> (v & 31)) & 1u) s_list[n++] = v;
+            s_ns = n;
         }
-        const TileOut o = tile_epilogue<true>(res.cnt, res.nskel, res.bm, res.maxd, tile,
-                                              &p.ws.tile_bm_slow[tile], p, stg.scan, s_wbm, s_wmax,
-                                              s_wskel, &s_base);
-        if (mine && o.base >= 0) {
-            const long long off = o.base + o.local_off;
-            p.out_desc[j] = make_int2((int)off, res.cnt);
-            if (global_path) {
-                if (res.cnt) vertex_slow<T, 8, UNIFORM, IN_CANON>(j, p, res, off, true);
-            } else if (out_mask) {
-                emit_window<T, KF>(w, out_mask, off, p);
+        const bool staged = stage_tile<T, UNIFORM, IN_CANON>(stg, j0, jn, p);   // syncs
+        const int ns = s_ns;
+        // counting passes
+        if (staged) {
+            for (int k = warp; k < ns; k += FT_WARPS) {
+                const int v = s_list[k];
+                VRes res;
+                vres_init(res);
+                warp_column<T, UNIFORM>(stg, v, j0 + v, p, s_recip, res, -1);
+                if (lane == 0) {
+                    s_cnt[k] = res.cnt; s_skel[k] = res.nskel; s_bm[k] = res.bm; s_mx[k] = res.maxd;
+                    report_flags(res, j0 + v, p);
+                }
+            }
+        } else if (tid < ns) {
+            const int v = s_list[tid];
+            VRes res;
+            vres_init(res);
+            vertex_slow<T, 8, UNIFORM, IN_CANON>(j0 + v, p, res, 0, false);
+            s_cnt[tid] = res.cnt; s_skel[tid] = res.nskel; s_bm[tid] = res.bm; s_mx[tid] = res.maxd;
+            report_flags(res, j0 + v, p);
+        }
+        __syncthreads();
+        int total;
+        const int loc = block_excl_scan<FT_TPB>(tid < ns ? s_cnt[tid] : 0, s_scan, &total);
+        if (tid == 0) {
+            long long base = 0;
+            if (total > 0) {
+                base = (long long)p.num_tiles * FT_SLOT +
+                       (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)total);
+                if (base + total > p.cap) { atomicExch(&p.ws.ctl->overflow, 1); base = -1; }
+            }
+            s_base = base;
+            double bm = 0.0, mx = 0.0;
+            long long sk = 0;
+            for (int k = 0; k < ns; ++k) { bm = bm + s_bm[k]; mx = fmax(mx, s_mx[k]); sk += s_skel[k]; }
+            p.ws.tile_bm_slow[2 * tile + half] = bm;
+            if (mx > 0.0) atomicMax(&p.ws.ctl->maxdelta_bits, (unsigned long long)__double_as_longlong(mx));
+            if (sk) atomicAdd(&p.ws.ctl->skel_total, (unsigned long long)sk);
+            if (total) atomicAdd(&p.ws.ctl->nnz_total, (unsigned long long)total);
+        }
+        if (tid < ns) s_cnt[tid] = loc;    // reuse: column offset within the unit
+        __syncthreads();
+        const long long base = s_base;
+        if (base >= 0) {
+            if (staged) {
+                for (int k = warp; k < ns; k += FT_WARPS) {
+                    const int v = s_list[k];
+                    const long long off = base + s_cnt[k];
+                    VRes res;
+                    vres_init(res);
+                    warp_column<T, UNIFORM>(stg, v, j0 + v, p, s_recip, res, off);
+                    if (lane == 0) p.out_desc[j0 + v] = make_int2((int)off, res.cnt);
+                }
+            } else if (tid < ns) {
+                const int v = s_list[tid];
+                const long long off = base + s_cnt[tid];
+                VRes res;
+                vres_init(res);
+                vertex_slow<T, 8, UNIFORM, IN_CANON>(j0 + v, p, res, off, true);
+                p.out_desc[j0 + v] = make_int2((int)off, res.cnt);
             }
         }
         __syncthreads();
@@ -844,31 +1058,66 @@ __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizePara
     const int nt = f.ws.num_tiles;
     const int per = (nt + gridDim.x - 1) / gridDim.x;
     const int t0 = blockIdx.x * per, t1 = min(nt, t0 + per);
-    double acc = 0.0;
-    for (int t = t0 + tid; t < t1; t += FT_FIN_TPB) acc = acc + (f.ws.tile_bm[t] + f.ws.tile_bm_slow[t]);
+    double acc = 0.0, amx = 0.0;
+    long long acnt = 0, askel = 0;
+    for (int t = t0 + tid; t < t1; t += FT_FIN_TPB) {
+        acc = acc + (f.ws.tile_bm[t] + (f.ws.tile_bm_slow[2 * t] + f.ws.tile_bm_slow[2 * t + 1]));
+        amx = fmax(amx, f.ws.tile_maxd[t]);
+        const int2 cs = f.ws.tile_cs[t];
+        acnt += cs.x;
+        askel += cs.y;
+    }
     acc = warp_sum(acc);
-    if ((tid & 31) == 0) s_part[tid >> 5] = acc;
+    acnt = warp_sum(acnt);
+    askel = warp_sum(askel);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amx = fmax(amx, __shfl_down_sync(0xffffffffu, amx, o));
+    __shared__ double s_mx[FT_FIN_TPB / 32];
+    __shared__ long long s_cnt[FT_FIN_TPB / 32], s_skel[FT_FIN_TPB / 32];
+    if ((tid & 31) == 0) { s_part[tid >> 5] = acc; s_mx[tid >> 5] = amx; s_cnt[tid >> 5] = acnt; s_skel[tid >> 5] = askel; }
     __syncthreads();
     if (tid == 0) {
-        double b = 0.0;
-        for (int k = 0; k < FT_FIN_TPB / 32; ++k) b = b + s_part[k];
+        double b = 0.0, m = 0.0;
+        long long c = 0, k = 0;
+        for (int q = 0; q < FT_FIN_TPB / 32; ++q) { b = b + s_part[q]; m = fmax(m, s_mx[q]); c += s_cnt[q]; k += s_skel[q]; }
         f.ws.fin_part[blockIdx.x] = b;
+        f.ws.fin_maxd[blockIdx.x] = m;
+        f.ws.fin_cnt[blockIdx.x] = c;
+        f.ws.fin_skel[blockIdx.x] = k;
         __threadfence();
         s_last = (atomicAdd(&ctl->fin_count, 1u) == gridDim.x - 1);
     }
     __syncthreads();
-    if (!s_last || tid != 0) return;
+    if (!s_last || tid >= 32) return;
     __threadfence();
+    // the last CTA combines the per-CTA partials with one warp: lane l owns
+    // partials l, l+32 (fixed order), then a fixed shuffle tree
+    double pb = 0.0, pm = 0.0;
+    long long pc = 0, pk = 0;
+    for (int q = tid; q < (int)gridDim.x; q += 32) {
+        pb = pb + *(volatile double*)&f.ws.fin_part[q];
+        pm = fmax(pm, *(volatile double*)&f.ws.fin_maxd[q]);
+        pc += *(volatile long long*)&f.ws.fin_cnt[q];
+        pk += *(volatile long long*)&f.ws.fin_skel[q];
+    }
+    pb = warp_sum(pb);
+    pc = warp_sum(pc);
+    pk = warp_sum(pk);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pm = fmax(pm, __shfl_down_sync(0xffffffffu, pm, o));
+    if (tid != 0) return;
     ctl->fin_count = 0u;
-    double bm = 0.0;
-    for (int k = 0; k < (int)gridDim.x; ++k) bm = bm + *(volatile double*)&f.ws.fin_part[k];
+    const double bm = pb;
+    const double mxd = fmax(pm, __longlong_as_double((long long)ctl->maxdelta_bits));
+    const long long nnz = pc + (long long)ctl->nnz_total;
+    const long long nsk = pk + (long long)ctl->skel_total;
 
     const int slot = f.fixed_slot ? 0 : ctl->steps_done;
     ft_step_stats st;
-    st.max_delta = __longlong_as_double((long long)ctl->maxdelta_bits);
+    st.max_delta = mxd;
     st.base_mass = bm;
-    st.nnz_phi = (long long)ctl->nnz_total;
-    st.nnz_skel = (long long)ctl->skel_total;
+    st.nnz_phi = nnz;
+    st.nnz_skel = nsk;
     st.nan_col = ctl->nan_key ? (int)(INT_MAX - ctl->nan_key) : -1;
     st.bad_col = -1; st.bad_row = -1; st.bad_is_lt = 0;
     const unsigned long long kp = ctl->bad_phi_key, kl = ctl->bad_lt_key;
@@ -1057,23 +1306,44 @@ __global__ void evolve_report_kernel(const Control* ctl, long long* control) {
 
 typedef void (*StepKernelFn)(const StepParams);
 
-static StepKernelFn pick_fixup(int dtype, bool uniform, bool in_canon) {
-    if (dtype == FT_F64) {
-        if (uniform) return in_canon ? fixup_kernel<double, true, true> : fixup_kernel<double, true, false>;
-        return in_canon ? fixup_kernel<double, false, true> : fixup_kernel<double, false, false>;
+struct KernelPick {
+    StepKernelFn fn;
+    size_t smem;
+};
+
+template <typename T, bool UNIFORM>
+static size_t stage_bytes() { return sizeof(Stage<T, UNIFORM>); }
+
+static KernelPick with_smem(StepKernelFn fn, size_t bytes) {
+    // opt in to > 48 KB dynamic shared memory once per kernel
+    static StepKernelFn done[64];
+    static int n_done = 0;
+    bool seen = false;
+    for (int i = 0; i < n_done; ++i) seen |= (done[i] == fn);
+    if (!seen) {
+        cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (n_done < 64) done[n_done++] = fn;
     }
-    if (uniform) return in_canon ? fixup_kernel<float, true, true> : fixup_kernel<float, true, false>;
-    return in_canon ? fixup_kernel<float, false, true> : fixup_kernel<float, false, false>;
+    return KernelPick{fn, bytes};
+}
+
+static KernelPick pick_fixup(int dtype, bool uniform, bool in_canon) {
+    if (dtype == FT_F64) {
+        if (uniform) return with_smem(in_canon ? fixup_kernel<double, true, true> : fixup_kernel<double, true, false>, stage_bytes<double, true>());
+        return with_smem(in_canon ? fixup_kernel<double, false, true> : fixup_kernel<double, false, false>, stage_bytes<double, false>());
+    }
+    if (uniform) return with_smem(in_canon ? fixup_kernel<float, true, true> : fixup_kernel<float, true, false>, stage_bytes<float, true>());
+    return with_smem(in_canon ? fixup_kernel<float, false, true> : fixup_kernel<float, false, false>, stage_bytes<float, false>());
 }
 
 template <int K>
-static StepKernelFn pick_kernel(int dtype, bool uniform, bool in_canon) {
+static KernelPick pick_kernel(int dtype, bool uniform, bool in_canon) {
     if (dtype == FT_F64) {
-        if (uniform) return in_canon ? step_kernel<double, K, true, true> : step_kernel<double, K, true, false>;
-        return in_canon ? step_kernel<double, K, false, true> : step_kernel<double, K, false, false>;
+        if (uniform) return with_smem(in_canon ? step_kernel<double, K, true, true> : step_kernel<double, K, true, false>, stage_bytes<double, true>());
+        return with_smem(in_canon ? step_kernel<double, K, false, true> : step_kernel<double, K, false, false>, stage_bytes<double, false>());
     }
-    if (uniform) return in_canon ? step_kernel<float, K, true, true> : step_kernel<float, K, true, false>;
-    return in_canon ? step_kernel<float, K, false, true> : step_kernel<float, K, false, false>;
+    if (uniform) return with_smem(in_canon ? step_kernel<float, K, true, true> : step_kernel<float, K, true, false>, stage_bytes<float, true>());
+    return with_smem(in_canon ? step_kernel<float, K, false, true> : step_kernel<float, K, false, false>, stage_bytes<float, false>());
 }
 
 }  // namespace ft
@@ -1135,7 +1405,7 @@ static int window_size() {
         for (int n = 1; n <= 32; ++n) h[n] = 1.0 / (double)n;
         cudaMemcpyToSymbol(ft::c_recip, h, sizeof(h));
         const char* s = getenv("FT_WINDOW");
-        g_window = (s && atoi(s) == 8) ? 8 : 4;
+        g_window = (s && atoi(s) == 8) ? 8 : 4;   // default: 4-row register window
         int dev = 0, sms = 148;
         if (cudaGetDevice(&dev) == cudaSuccess &&
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
@@ -1180,11 +1450,11 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_
     p.finite = std::isfinite(p.w) && std::isfinite(p.a) && std::isfinite(p.e) && std::isfinite(p.eb) &&
                std::isfinite(p.mu) && std::isfinite(p.dt);
     const bool uni = lap_flags == FT_LAP_UNIFORM;
-    ft::StepKernelFn k = window_size() == 8 ? ft::pick_kernel<8>(dtype, uni, in_canon != nullptr)
-                                            : ft::pick_kernel<4>(dtype, uni, in_canon != nullptr);
-    if (which & 1) k<<<p.num_tiles, FT_TPB, 0, s>>>(p);
-    ft::StepKernelFn fx = ft::pick_fixup(dtype, uni, in_canon != nullptr);
-    if (which & 2) fx<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
+    const ft::KernelPick k = window_size() == 8 ? ft::pick_kernel<8>(dtype, uni, in_canon != nullptr)
+                                                : ft::pick_kernel<4>(dtype, uni, in_canon != nullptr);
+    if (which & 1) k.fn<<<p.num_tiles, FT_TPB, k.smem, s>>>(p);
+    const ft::KernelPick fx = ft::pick_fixup(dtype, uni, in_canon != nullptr);
+    if (which & 2) fx.fn<<<g_fixup_grid, FT_TPB, fx.smem, s>>>(p);
     return cuda_check("step kernel");
 }
 
