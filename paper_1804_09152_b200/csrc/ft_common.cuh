@@ -26,23 +26,25 @@ struct Control {
     unsigned long long pool_next;      // overflow-pool bump pointer
     unsigned int       nan_key;        // atomicMax(INT_MAX - col) -> min col
     int                overflow;       // a tile did not fit the work buffer
-    int                slow_count;     // tiles queued for the fixup kernel
+    int                slow_count;     // wide columns queued for tier 2
     unsigned int       fin_count;      // finalize: CTAs done (last-block pattern)
+    int                deep_count;     // tier-3 columns (stored at the tail of slow_list)
+    int                pad3;
     int                done;           // evolve: stop flag (finalize sets it)
     int                steps_done;     // evolve: completed steps
     int                status;         // evolve: final status
     int                pad0;
     long long          needed;         // capacity needed on overflow
-    long long          pad1[5];
+    long long          pad1[4];
 };
 static_assert(sizeof(Control) % 16 == 0, "Control must stay 16B aligned");
 
 struct Workspace {
     Control*      ctl;
     double*       tile_bm;      // [num_tiles] per-tile base mass (fast path)
-    double*       tile_bm_slow; // [2 * num_tiles] per-half-tile base mass (fixup path)
-    unsigned int* slow_mask;    // [num_tiles * FT_WARPS] columns left to the fixup
-    int*          slow_list;    // [num_tiles] tiles queued for the fixup
+    double*       vbm;          // [n_v] base mass of wide columns (tier 2)
+    unsigned int* slow_mask;    // [num_tiles * FT_WARPS] wide columns of each tile
+    int*          slow_list;    // [2 n_v] tier-2 queue, then the tier-3 queue at +n_v
     long long*    chunk_off;    // [num_chunks + 2] compaction chunk offsets
     double*       fin_part;     // [64] finalize partial sums (base mass)
     double*       fin_maxd;     // [64] finalize partial maxima
@@ -59,10 +61,15 @@ __host__ __device__ inline int num_chunks_for(int n_v) { return (n_v + FT_CCH - 
 
 inline size_t workspace_bytes(int n_v) {
     size_t t = (size_t)num_tiles_for(n_v), c = (size_t)num_chunks_for(n_v);
-    return sizeof(Control) + 3 * t * sizeof(double) + t * FT_WARPS * sizeof(unsigned int) +
-           t * sizeof(int) + (c + 2) * sizeof(long long) + 4 * 64 * sizeof(double) +
-           t * (sizeof(double) + sizeof(int2)) + 512;
+    const size_t v = (size_t)n_v;
+    return sizeof(Control) + t * sizeof(double) + v * sizeof(double) + t * FT_WARPS * sizeof(unsigned int) +
+           2 * v * sizeof(int) + (c + 2) * sizeof(long long) + 4 * 64 * sizeof(double) +
+           t * (sizeof(double) + sizeof(int2)) + 1024;
 }
+
+static_assert(FT_WARPS == 4, "slow_mask is read as one uint4 per tile");
+
+inline char* align16(char* p) { return (char*)(((uintptr_t)p + 15) & ~(uintptr_t)15); }
 
 inline Workspace carve_workspace(void* base, int n_v) {
     Workspace w;
@@ -73,8 +80,8 @@ inline Workspace carve_workspace(void* base, int n_v) {
     w.num_chunks = num_chunks_for(n_v);
     w.tile_bm = (double*)p;
     p += (size_t)w.num_tiles * sizeof(double);
-    w.tile_bm_slow = (double*)p;
-    p += 2 * (size_t)w.num_tiles * sizeof(double);
+    w.vbm = (double*)p;
+    p += (size_t)n_v * sizeof(double);
     w.chunk_off = (long long*)p;
     p += ((size_t)w.num_chunks + 2) * sizeof(long long);
     w.fin_part = (double*)p;
@@ -89,9 +96,11 @@ inline Workspace carve_workspace(void* base, int n_v) {
     p += (size_t)w.num_tiles * sizeof(double);
     w.tile_cs = (int2*)p;
     p += (size_t)w.num_tiles * sizeof(int2);
+    p = align16(p);
     w.slow_mask = (unsigned int*)p;
     p += (size_t)w.num_tiles * FT_WARPS * sizeof(unsigned int);
     w.slow_list = (int*)p;
+    p += 2 * (size_t)n_v * sizeof(int);
     return w;
 }
 

@@ -10,16 +10,14 @@
 //   normalise + compact     column_sums_counts, normalize_compact
 //                                               _kernels.py:241-282
 //
-// Work split: one CTA per tile of FT_TPB consecutive vertex columns, one
-// thread per column.  The tile's L rows, the PHI column descriptors of all
-// its (vertex, neighbour) pairs and the gathered PHI entries are staged in
-// shared memory with flat, independent loads (high memory-level
-// parallelism); each thread then merges its neighbours' sorted PHI columns
-// into a sorted register window of at most K layer rows, accumulating
-// Lt(r, j) in ascending-u order -- exactly the reference accumulator order
-// (first product assigned, then +=).  PHI(r, j) itself arrives through the
-// diagonal u == j.  Columns whose union exceeds K rows are processed exactly
-// in ascending row windows straight from global memory (slow path).
+// Work split: one thread per vertex column, 128-column tiles per CTA.  The
+// thread fetches its L row, the neighbours' column descriptors and their
+// first entries into registers (four rounds of independent loads), merges
+// the neighbours' sorted columns into a <= K-row window in ascending row
+// order, accumulating Lt(r, j) in ascending-u order -- exactly the
+// reference accumulator order.  PHI(r, j) itself arrives through the
+// diagonal u == j.  Wider columns go to a second kernel (tier 2) that runs
+// the exact windowed algorithm over a compacted list.
 //
 // Output: the tile's entries go to its fixed slot of the tiled work buffer
 // (FT_SLOT entries) or, when they do not fit, to a pool range taken with
@@ -36,6 +34,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "ft_common.cuh"
 
@@ -161,190 +160,6 @@ __device__ __forceinline__ void gather(Win<K>& w, int j, int lo, const StepParam
             win_insert<K>(w, r, ph * l, diag, ph);
         }
     }
-}
-
-// ---------------------------------------------------------------------------
-// shared-memory staging of a vertex tile
-//
-// The tile's L rows are one contiguous range of L^T, loaded coalesced; the
-// PHI descriptors of all (vertex, neighbour) pairs are fetched with
-// kLPV independent loads per thread, offsets come from a block scan, and
-// the gathered PHI entries are fetched flat into shared memory.  Each
-// thread then pays ~3 memory round trips instead of a dependent chain per
-// neighbour.  Tiles beyond the staging capacity (very high degree or very
-// dense bands) fall back to direct per-thread gathers (also exact).
-
-constexpr int kLPV = 8;                    // staged L entries per vertex (capacity)
-constexpr int kLMAX = FT_TPB * kLPV;       // staged L entries per tile
-constexpr int kEMAX = kLMAX * 5 / 2;       // staged PHI entries per tile
-
-template <typename T, bool UNIFORM>
-struct Stage {
-    int rp[FT_TPB + 1];    // L^T column pointers of the tile (absolute)
-    int u[kLMAX];          // neighbour ids
-    int2 oc[kLMAX];        // staged (offset, count) of PHI(:, u) per pair
-    int er[kEMAX];         // gathered PHI rows
-    T ev[kEMAX];           // gathered PHI values
-    T lv[UNIFORM ? 1 : kLMAX];
-    int scan[FT_WARPS];
-};
-
-// Phases A-C.  Returns true when the whole tile is staged (block-uniform).
-// Thread t owns pairs e = t + k*FT_TPB: it loads their descriptors (kLPV
-// independent loads), reserves their entries' space with one block scan,
-// and gathers the entries itself -- the descriptors never leave registers.
-template <typename T, bool UNIFORM, bool IN_CANON>
-__device__ __forceinline__ bool stage_tile(Stage<T, UNIFORM>& s, int j0, int jn, const StepParams& p) {
-    const int tid = threadIdx.x;
-    // A: L rows of the tile
-    if (tid < jn) s.rp[tid] = __ldg(&p.lap_ptr[j0 + tid]);
-    if (tid == 0) s.rp[jn] = __ldg(&p.lap_ptr[j0 + jn]);
-    __syncthreads();
-    const int LB = s.rp[0];
-    const int nL = s.rp[jn] - LB;
-    if (nL > kLMAX) return false;
-    int ur[kLPV];
-#pragma unroll
-    for (int k = 0; k < kLPV; ++k) {
-        const int e = tid + k * FT_TPB;
-        if (e < nL) {
-            ur[k] = __ldg(&p.lap_idx[LB + e]);
-            s.u[e] = ur[k];
-            if (!UNIFORM) s.lv[e] = __ldg(((const T*)p.lap_val) + LB + e);
-        }
-    }
-    // B: PHI descriptors of the owned pairs
-    int2 dr[kLPV];
-    int sum = 0;
-#pragma unroll
-    for (int k = 0; k < kLPV; ++k) {
-        const int e = tid + k * FT_TPB;
-        dr[k] = make_int2(0, 0);
-        if (e < nL) dr[k] = load_desc<IN_CANON>(p, ur[k]);
-    }
-    int loc[kLPV];
-#pragma unroll
-    for (int k = 0; k < kLPV; ++k) { loc[k] = sum; sum += dr[k].y; }
-    int nE;
-    const int pre = block_excl_scan<FT_TPB>(sum, s.scan, &nE);
-    if (nE > kEMAX) return false;
-    // C: gather the owned pairs' entries; first entries go to registers
-    // before any store so each thread keeps kLPV loads in flight
-    {
-        int r0[kLPV];
-        T v0[kLPV];
-#pragma unroll
-        for (int k = 0; k < kLPV; ++k) {
-            if (dr[k].y > 0) {
-                r0[k] = __ldg(&p.in_idx[dr[k].x]);
-                v0[k] = __ldg(((const T*)p.in_val) + dr[k].x);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < kLPV; ++k) {
-            const int e = tid + k * FT_TPB;
-            if (e < nL) {
-                const int o = pre + loc[k];
-                const int n = dr[k].y;
-                s.oc[e] = make_int2(o, n);
-                if (n > 0) { s.er[o] = r0[k]; s.ev[o] = v0[k]; }
-                for (int t = 1; t < n; ++t) {
-                    s.er[o + t] = __ldg(&p.in_idx[dr[k].x + t]);
-                    s.ev[o + t] = __ldg(((const T*)p.in_val) + dr[k].x + t);
-                }
-            }
-        }
-    }
-    __syncthreads();
-    return true;
-}
-
-// Phase D: fill the register window of vertex (j0 + tid) from the stage.
-// One pass over the vertex's gathered entries in entry order (= ascending
-// u, the reference accumulation order): each entry's row is looked up among
-// the rows seen so far (slot 0 first: inside a cell every entry has the
-// same row) and its product added to that slot's Lt accumulator; unseen rows
-// are appended.  PHI(r, j) comes from the diagonal pair, and the window is
-// then sorted by row.
-// Starting an accumulator at +0.0 instead of assigning the first product
-// only changes the sign of an exact-zero sum; zero sums are not stored by
-// the reference (Lt == 0 is dropped) and are outside the skeleton either
-// way, so the result is bitwise the reference's.  Sets w.more when the
-// union exceeds K rows.
-template <int K>
-__device__ __forceinline__ void win_sort(Win<K>& w, unsigned int active) {
-    // insertion sort by row with warp-uniform trip counts (K <= 16)
-#pragma unroll
-    for (int a = 1; a < K; ++a) {
-        if (!__any_sync(active, a < w.m)) break;
-#pragma unroll
-        for (int b = a; b > 0; --b) {
-            const bool sw = (b < w.m) && (w.rows[b - 1] > w.rows[b]);
-            if (sw) {
-                const int tr = w.rows[b]; w.rows[b] = w.rows[b - 1]; w.rows[b - 1] = tr;
-                const double tl = w.lam[b]; w.lam[b] = w.lam[b - 1]; w.lam[b - 1] = tl;
-                const double tp = w.phi[b]; w.phi[b] = w.phi[b - 1]; w.phi[b - 1] = tp;
-            }
-        }
-    }
-}
-
-template <typename T, int K, bool UNIFORM>
-__device__ __forceinline__ void gather_staged(Win<K>& w, int j, const Stage<T, UNIFORM>& s,
-                                              const double* recip) {
-    const int tid = threadIdx.x;
-    const int LB = s.rp[0];
-    const int e0 = s.rp[tid] - LB;
-    const int e1 = s.rp[tid + 1] - LB;
-    const int deg = e1 - e0 - 1;
-    const double invdeg = UNIFORM ? (deg <= 32 ? recip[deg] : 1.0 / (double)deg) : 0.0;
-    w.more = false;
-#pragma unroll
-    for (int i = 0; i < K; ++i) { w.rows[i] = INT_MAX; w.lam[i] = 0.0; w.phi[i] = 0.0; }
-    w.m = 0;
-    int fd0 = 0, fd1 = 0;   // entries of the diagonal pair (u == j)
-    for (int e = e0; e < e1; ++e) {
-        const bool diag = (s.u[e] == j);
-        const double l = UNIFORM ? (diag ? -1.0 : invdeg) : (double)s.lv[e];
-        const int2 oc = s.oc[e];
-        if (diag) { fd0 = oc.x; fd1 = oc.x + oc.y; }
-        for (int f = oc.x; f < oc.x + oc.y; ++f) {
-            const int r = s.er[f];
-            const double prod = (double)s.ev[f] * l;
-            if (r == w.rows[0]) {
-                w.lam[0] = w.lam[0] + prod;
-            } else if (w.m == 0) {
-                w.rows[0] = r;
-                w.lam[0] = 0.0 + prod;
-                w.m = 1;
-            } else {
-                bool hit = false;
-#pragma unroll
-                for (int i = 1; i < K; ++i) {
-                    if (w.rows[i] == r) { w.lam[i] = w.lam[i] + prod; hit = true; }
-                }
-                if (!hit) {
-                    if (w.m == K) {
-                        w.more = true;
-                    } else {
-#pragma unroll
-                        for (int i = 1; i < K; ++i)
-                            if (i == w.m) { w.rows[i] = r; w.lam[i] = 0.0 + prod; }
-                        w.m++;
-                    }
-                }
-            }
-        }
-    }
-    if (w.more) return;
-    for (int f = fd0; f < fd1; ++f) {
-        const int r = s.er[f];
-        const double ph = (double)s.ev[f];
-#pragma unroll
-        for (int i = 0; i < K; ++i)
-            if (w.rows[i] == r) w.phi[i] = ph;
-    }
-    win_sort<K>(w, __activemask());
 }
 
 // ---------------------------------------------------------------------------
@@ -656,15 +471,9 @@ __device__ __noinline__ void vertex_slow(int j, const StepParams& p, VRes& res, 
 }
 
 // ---------------------------------------------------------------------------
-// the fused step kernel (fast path)
-//
-// Columns that do not fit the register window (union > K rows) and every
-// column of a tile that could not be staged are left to fixup_kernel: they
-// contribute no entries to the tile slot, their bit is set in slow_mask
-// and the tile is queued once in slow_list.  Keeping the slow paths out of
-// this kernel keeps its register footprint small.
+// output placement
 
-// Tile epilogue shared by both kernels: block scan of the output counts,
+// Tile epilogue: block scan of the output counts,
 // placement (tile slot, or a pool range), per-tile statistics.
 struct TileOut {
     int local_off;
@@ -721,323 +530,308 @@ __device__ __forceinline__ TileOut tile_epilogue(int cnt, int nskel, double bmv,
     return o;
 }
 
-extern __shared__ __align__(16) unsigned char ft_dyn_smem[];
+// ---------------------------------------------------------------------------
+// tier 1: the fused step kernel
+//
+// One thread per vertex column, everything in registers: the L row (<= kMD
+// entries), the neighbours' column descriptors and their first two entries
+// are fetched in four rounds of independent loads (no shared-memory stage,
+// no barrier before the epilogue).  Columns whose neighbourhood carries a
+// single layer row (cell interiors, ~80% of columns) take the exact
+// single-row closed form (process_window) and need no products at all; the
+// others build a <= K-row window by ascending-row passes over the register
+// entries, accumulating in (u, t) order = the reference order.  A column
+// with a longer L row, a neighbour holding more than two entries, or more
+// than K rows is "wide": it is queued (slow_list, slow_mask) for tier 2.
+
+constexpr int kMD = 8;
 
 template <typename T, int K, bool UNIFORM, bool IN_CANON>
-__global__ void __launch_bounds__(FT_TPB, 5) step_kernel(const StepParams p) {
-    Stage<T, UNIFORM>& stg = *reinterpret_cast<Stage<T, UNIFORM>*>(ft_dyn_smem);
+__global__ void __launch_bounds__(FT_TPB, 6) step_kernel(const StepParams p) {
     __shared__ double s_wbm[FT_WARPS];
     __shared__ double s_wmax[FT_WARPS];
     __shared__ int s_wskel[FT_WARPS];
     __shared__ unsigned int s_wslow[FT_WARPS];
+    __shared__ int s_scan[FT_WARPS];
     __shared__ long long s_base;
-    __shared__ double s_recip[33];
 
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
-    if (threadIdx.x < 33) s_recip[threadIdx.x] = c_recip[threadIdx.x];
-
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tile = blockIdx.x;
-    const int j0 = tile * FT_TPB;
-    const int jn = min(FT_TPB, p.n_v - j0);
-    const int j = j0 + tid;
-    const bool active = tid < jn;
+    const int j = tile * FT_TPB + tid;
+    const bool active = j < p.n_v;
 
-    const bool staged = stage_tile<T, UNIFORM, IN_CANON>(stg, j0, jn, p);
+    int n = 0, q0 = 0;
+    bool wide = false;
+    if (active) {
+        q0 = __ldg(&p.lap_ptr[j]);
+        n = __ldg(&p.lap_ptr[j + 1]) - q0;
+        if (n > kMD || n < 1) { wide = true; n = 0; }
+    }
+    int u[kMD];
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) u[k] = (k < n) ? __ldg(&p.lap_idx[q0 + k]) : -1;
+    double lv[UNIFORM ? 1 : kMD];
+    if (!UNIFORM) {
+#pragma unroll
+        for (int k = 0; k < kMD; ++k) lv[k] = (k < n) ? ldv<T>(p.lap_val, q0 + k) : 0.0;
+    }
+    int2 d[kMD];
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
+    int kd = -1;
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) {
+        if (u[k] == j) kd = k;
+        wide |= d[k].y > 2;
+    }
+    if (active && kd < 0) wide = true;
+    int r0[kMD], r1[kMD];
+    T v0[kMD], v1[kMD];
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) {
+        r0[k] = INT_MAX; r1[k] = INT_MAX; v0[k] = (T)0; v1[k] = (T)0;
+        if (!wide && d[k].y > 0) { r0[k] = __ldg(&p.in_idx[d[k].x]); v0[k] = __ldg(((const T*)p.in_val) + d[k].x); }
+        if (!wide && d[k].y > 1) { r1[k] = __ldg(&p.in_idx[d[k].x + 1]); v1[k] = __ldg(((const T*)p.in_val) + d[k].x + 1); }
+    }
 
-    Win<K> w;
     VRes res;
     vres_init(res);
-    bool slow = false;
+    Win<K> w;
+    w.m = 0;
     unsigned int out_mask = 0;
-    if (active) {
-        if (staged) gather_staged<T, K, UNIFORM>(w, j, stg, s_recip);
-        slow = !staged || w.more;
-        if (!slow) {
-            process_window<K>(w, p, res, out_mask, s_recip);
+    if (active && !wide) {
+        const double invdeg = UNIFORM ? (n - 1 <= 32 ? c_recip[n - 1] : 1.0 / (double)(n - 1)) : 0.0;
+        int lo = -1;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            int r = INT_MAX;
+#pragma unroll
+            for (int k = 0; k < kMD; ++k) {
+                if (r0[k] > lo && r0[k] < r) r = r0[k];
+                if (r1[k] > lo && r1[k] < r) r = r1[k];
+            }
+            double lam = 0.0, ph = 0.0;
+            if (r != INT_MAX) {
+#pragma unroll
+                for (int k = 0; k < kMD; ++k) {
+                    const double l = UNIFORM ? ((k == kd) ? -1.0 : invdeg) : lv[k];
+                    if (r0[k] == r) { lam = lam + (double)v0[k] * l; if (k == kd) ph = (double)v0[k]; }
+                    if (r1[k] == r) { lam = lam + (double)v1[k] * l; if (k == kd) ph = (double)v1[k]; }
+                }
+                w.m = i + 1;
+                lo = r;
+            }
+            w.rows[i] = r;
+            w.lam[i] = lam;
+            w.phi[i] = ph;
+        }
+        bool more = false;
+#pragma unroll
+        for (int k = 0; k < kMD; ++k) more |= (r0[k] > lo && r0[k] != INT_MAX) || (r1[k] > lo && r1[k] != INT_MAX);
+        if (more) {
+            wide = true;
+        } else {
+            process_window<K>(w, p, res, out_mask, c_recip);
             report_flags(res, j, p);
         }
     }
-    const unsigned int slow_bits = __ballot_sync(0xffffffffu, slow);
-    if (lane == 0) s_wslow[warp] = slow_bits;
-    const TileOut o = tile_epilogue<false>(res.cnt, res.nskel, res.bm, res.maxd, tile, &p.ws.tile_bm[tile], p,
-                                           stg.scan, s_wbm, s_wmax, s_wskel, &s_base);
-    if (tid == 0) {
-        unsigned int any_slow = 0;
-#pragma unroll
-        for (int k = 0; k < FT_WARPS; ++k) any_slow |= s_wslow[k];
-        p.ws.tile_bm_slow[2 * tile] = 0.0;
-        p.ws.tile_bm_slow[2 * tile + 1] = 0.0;
-        if (any_slow) {
-            const int q = atomicAdd(&p.ws.ctl->slow_count, 1);
-            p.ws.slow_list[q] = tile;
-#pragma unroll
-            for (int k = 0; k < FT_WARPS; ++k) p.ws.slow_mask[(size_t)tile * FT_WARPS + k] = s_wslow[k];
-        }
+    if (wide) vres_init(res);
+
+    // queue the wide columns for tier 2 (one atomic per warp)
+    const unsigned int wbits = __ballot_sync(0xffffffffu, wide && active);
+    if (wbits) {
+        int qb = 0;
+        if (lane == 0) qb = atomicAdd(&p.ws.ctl->slow_count, __popc(wbits));
+        qb = __shfl_sync(0xffffffffu, qb, 0);
+        if (wide && active) p.ws.slow_list[qb + __popc(wbits & ((1u << lane) - 1u))] = j;
     }
-    if (!active || slow || o.base < 0) return;
+    if (lane == 0) {
+        s_wslow[warp] = wbits;
+        p.ws.slow_mask[(size_t)tile * FT_WARPS + warp] = wbits;
+    }
+    const TileOut o = tile_epilogue<false>(res.cnt, res.nskel, res.bm, res.maxd, tile, &p.ws.tile_bm[tile], p,
+                                           s_scan, s_wbm, s_wmax, s_wskel, &s_base);
+    if (!active || wide || o.base < 0) return;
     const long long off = o.base + o.local_off;
     p.out_desc[j] = make_int2((int)off, res.cnt);
     if (out_mask) emit_window<T, K>(w, out_mask, off, p);
 }
 
 // ---------------------------------------------------------------------------
-// fixup kernel: the columns the fast path left behind.  One CTA per queued
-// tile (grid-stride over slow_list): the tile is staged again and the slow
-// columns use a KF-row window from shared memory; columns beyond KF rows
-// and tiles that cannot be staged use the exact windowed global path.  The
-// tile's base mass goes to tile_bm_slow[tile] (fixed reduction order).
+// tier 2: the queued wide columns, one thread each over the compacted list
+// (full warps), with the exact windowed global-memory algorithm
+// (vertex_slow: no width limit).  Output space comes from the pool (one
+// atomic per warp); the column's base mass goes to vbm[j] so the finalize
+// reduction can add it in a fixed order.
 
-// Warp-cooperative exact processing of one column from the stage, used by
-// the fixup kernel for columns whose layer union is wider than the fast
-// path's register window.  Lane k owns the column's k-th (vertex,
-// neighbour) pair (chunks of 32).  Rows are visited in ascending order:
-// each round the warp finds the next row (min over all pairs' entries),
-// then the row's per-pair products are summed in pair order (= ascending
-// u, the reference accumulation order) by a shuffle chain.  No per-column
-// arrays, no width limit.
-struct WarpCol {
-    int e0, e1;       // the column's pairs in the stage
-    int j;            // the column (vertex) id
-    double invdeg;
-};
-
-template <typename T, bool UNIFORM>
-__device__ __forceinline__ WarpCol warp_col(const Stage<T, UNIFORM>& s, int v, int j, const double* recip) {
-    WarpCol c;
-    const int LB = s.rp[0];
-    c.e0 = s.rp[v] - LB;
-    c.e1 = s.rp[v + 1] - LB;
-    c.j = j;
-    const int deg = c.e1 - c.e0 - 1;
-    c.invdeg = deg <= 32 ? recip[deg] : 1.0 / (double)deg;
-    return c;
-}
-
-// smallest row > lo among the column's entries (INT_MAX when none)
-template <typename T, bool UNIFORM>
-__device__ __forceinline__ int warp_next_row(const Stage<T, UNIFORM>& s, const WarpCol& c, int lo, int lane) {
-    int best = INT_MAX;
-    for (int e = c.e0 + lane; e < c.e1; e += 32) {
-        const int2 oc = s.oc[e];
-        for (int f = oc.x; f < oc.x + oc.y; ++f) {
-            const int r = s.er[f];
-            if (r > lo) { if (r < best) best = r; break; }   // rows ascend within a pair
-        }
-    }
-    return __reduce_min_sync(0xffffffffu, best);
-}
-
-// (Lt(r, j), PHI(r, j)) of one row, identical on all lanes
-template <typename T, bool UNIFORM>
-__device__ __forceinline__ void warp_row(const Stage<T, UNIFORM>& s, const WarpCol& c, int r, int lane,
-                                         double& lam, double& phi) {
-    lam = 0.0;
-    phi = 0.0;
-    for (int base = c.e0; base < c.e1; base += 32) {
-        const int e = base + lane;
-        bool has = false;
-        double prod = 0.0, ph = 0.0;
-        bool diag = false;
-        if (e < c.e1) {
-            const int2 oc = s.oc[e];
-            diag = (s.u[e] == c.j);
-            for (int f = oc.x; f < oc.x + oc.y; ++f) {
-                const int rr = s.er[f];
-                if (rr == r) {
-                    ph = (double)s.ev[f];
-                    const double l = UNIFORM ? (diag ? -1.0 : c.invdeg) : (double)s.lv[e];
-                    prod = ph * l;
-                    has = true;
-                    break;
-                }
-                if (rr > r) break;
-            }
-        }
-        const unsigned int hb = __ballot_sync(0xffffffffu, has);
-        const unsigned int db = __ballot_sync(0xffffffffu, has && diag);
-        const int n = min(32, c.e1 - base);
-        for (int k = 0; k < n; ++k) {          // in pair order: exact reference order
-            const double pk = __shfl_sync(0xffffffffu, prod, k);
-            if ((hb >> k) & 1u) lam = lam + pk;
-        }
-        if (db) phi = __shfl_sync(0xffffffffu, ph, __ffs(db) - 1);
-    }
-}
-
-// pass = 0: aggregates; 1: column sum of v; 2: normalise + count; 3: emit
-template <typename T, bool UNIFORM>
-__device__ __forceinline__ void warp_column(const Stage<T, UNIFORM>& s, int v, int j, const StepParams& p,
-                                            const double* recip, VRes& res, long long emit_off) {
-    const int lane = threadIdx.x & 31;
-    const WarpCol c = warp_col<T, UNIFORM>(s, v, j, recip);
-    Agg g;
-    agg_init(g);
+// Gather for tier 2: up to kMD L entries (descriptors in registers), any
+// number of entries per neighbour column (re-read from L1 in every row
+// pass), up to K rows.  Returns false when the column exceeds kMD or K (the
+// caller then uses vertex_slow).
+template <typename T, int K, bool UNIFORM, bool IN_CANON>
+__device__ __forceinline__ bool gather_wide(int j, const StepParams& p, Win<K>& w) {
+    const int q0 = __ldg(&p.lap_ptr[j]);
+    const int n = __ldg(&p.lap_ptr[j + 1]) - q0;
+    if (n > kMD || n < 1) return false;
+    int u[kMD];
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) u[k] = (k < n) ? __ldg(&p.lap_idx[q0 + k]) : -1;
+    int2 d[kMD];
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
+    int kd = -1;
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) if (u[k] == j) kd = k;
+    if (kd < 0) return false;
+    const int* __restrict__ gi = p.in_idx;
+    const T* __restrict__ gv = (const T*)p.in_val;
+    const double invdeg = UNIFORM ? (n - 1 <= 32 ? c_recip[n - 1] : 1.0 / (double)(n - 1)) : 0.0;
     int lo = -1;
-    for (;;) {
-        const int r = warp_next_row<T, UNIFORM>(s, c, lo, lane);
-        if (r == INT_MAX) break;
-        double lm, ph;
-        warp_row<T, UNIFORM>(s, c, r, lane, lm, ph);
-        const bool in = in_skeleton(ph, lm);
-        if (ph != 0.0 && !in) g.bad_phi_row = r;
-        if (lm != 0.0 && !in) g.bad_lt_row = r;
-        if (in) {
-            if (g.n == 0) { g.first_row = r; g.phi0 = ph; }
-            g.n++;
-            g.sl = g.sl + ((lm != 0.0) ? lm : 0.0);
-            g.sp = g.sp + ph;
-            g.sr = g.sr + sqrt(ph);
-        }
-        lo = r;
-    }
-    res.nskel = g.n;
-    res.bad_phi_row = g.bad_phi_row;
-    res.bad_lt_row = g.bad_lt_row;
-    if (g.n == 0) return;
-    const Coef cf = make_coef(g, p, recip);
-    double sum = 0.0;
-    lo = -1;
-    for (;;) {
-        const int r = warp_next_row<T, UNIFORM>(s, c, lo, lane);
-        if (r == INT_MAX) break;
-        double lm, ph;
-        warp_row<T, UNIFORM>(s, c, r, lane, lm, ph);
-        if (in_skeleton(ph, lm)) sum = sum + update_entry(r, ph, (lm != 0.0) ? lm : 0.0, cf, p, res.nan);
-        lo = r;
-    }
-    const bool spos = sum > 0.0;
-    const double inv = spos ? 1.0 / sum : 0.0;
-    bool dummy = false;
-    T* ov = (T*)p.out_val;
-    lo = -1;
-    for (;;) {
-        const int r = warp_next_row<T, UNIFORM>(s, c, lo, lane);
-        if (r == INT_MAX) break;
-        double lm, ph;
-        warp_row<T, UNIFORM>(s, c, r, lane, lm, ph);
-        if (in_skeleton(ph, lm)) {
-            const double vv = update_entry(r, ph, (lm != 0.0) ? lm : 0.0, cf, p, dummy);
-            const double nv = spos ? vv * inv : vv;
-            if (nv != 0.0) {
-                if (emit_off >= 0 && lane == 0) {
-                    p.out_idx[emit_off] = r;
-                    ov[emit_off] = (T)nv;
-                }
-                if (emit_off >= 0) ++emit_off;
-                res.cnt++;
-                if (r == 0) res.bm = res.bm + nv;
+    w.m = 0;
+#pragma unroll
+    for (int i = 0; i <= K; ++i) {
+        int rr = INT_MAX;
+#pragma unroll
+        for (int k = 0; k < kMD; ++k) {
+            for (int t = 0; t < d[k].y; ++t) {
+                const int x = __ldg(&gi[d[k].x + t]);
+                if (x > lo) { if (x < rr) rr = x; break; }   // rows ascend in a column
             }
-            const double dd = fabs(nv - ph);
-            if (dd > res.maxd) res.maxd = dd;
         }
-        lo = r;
+        if (i == K) return rr == INT_MAX;     // more than K rows?
+        double lam = 0.0, ph = 0.0;
+        if (rr != INT_MAX) {
+#pragma unroll
+            for (int k = 0; k < kMD; ++k) {
+                const double l = UNIFORM ? ((k == kd) ? -1.0 : invdeg) : ldv<T>(p.lap_val, q0 + k);
+                for (int t = 0; t < d[k].y; ++t) {
+                    const int x = __ldg(&gi[d[k].x + t]);
+                    if (x == rr) {
+                        const double vv = (double)__ldg(&gv[d[k].x + t]);
+                        lam = lam + vv * l;
+                        if (k == kd) ph = vv;
+                    }
+                    if (x >= rr) break;
+                }
+            }
+            w.m = i + 1;
+            lo = rr;
+        }
+        w.rows[i] = rr;
+        w.lam[i] = lam;
+        w.phi[i] = ph;
+    }
+    return true;
+}
+
+// warp-aggregated pool allocation + statistics for one batch of columns
+template <typename T, int K>
+__device__ __forceinline__ long long pool_place(int cnt, const VRes& res, const StepParams& p, int lane,
+                                                bool& fits, int& excl) {
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+    long long base = 0;
+    if (lane == 31 && wtot > 0)
+        base = (long long)p.num_tiles * FT_SLOT +
+               (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)wtot);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    fits = base + wtot <= p.cap;
+    if (lane == 31 && !fits) atomicExch(&p.ws.ctl->overflow, 1);
+    const int skel = warp_sum(res.nskel);
+    double mx = res.maxd;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+    if (lane == 0) {
+        if (mx > 0.0) atomicMax(&p.ws.ctl->maxdelta_bits, (unsigned long long)__double_as_longlong(mx));
+        if (skel) atomicAdd(&p.ws.ctl->skel_total, (unsigned long long)skel);
+        if (wtot) atomicAdd(&p.ws.ctl->nnz_total, (unsigned long long)wtot);
+    }
+    excl = incl - cnt;
+    return base;
+}
+
+template <typename T, bool UNIFORM, bool IN_CANON>
+__global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p) {
+    constexpr int KW = 8;
+    if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
+    const int n_wide = *(volatile int*)&p.ws.ctl->slow_count;
+    const int lane = threadIdx.x & 31;
+    const int stride = gridDim.x * FT_TPB;
+    const int rounds = (n_wide + stride - 1) / stride;
+    for (int rnd = 0; rnd < rounds; ++rnd) {
+        const int i = rnd * stride + blockIdx.x * FT_TPB + threadIdx.x;
+        const bool mine = i < n_wide;
+        const int j = mine ? p.ws.slow_list[i] : 0;
+        VRes res;
+        vres_init(res);
+        Win<KW> w;
+        unsigned int out_mask = 0;
+        bool deep = false;
+        if (mine) {
+            deep = !gather_wide<T, KW, UNIFORM, IN_CANON>(j, p, w);
+            if (!deep) {
+                process_window<KW>(w, p, res, out_mask, c_recip);
+                report_flags(res, j, p);
+            }
+        }
+        // tier 3: beyond the tier-2 window (queued at the tail of slow_list)
+        const unsigned int db = __ballot_sync(0xffffffffu, deep);
+        if (db) {
+            int qb = 0;
+            if (lane == 0) qb = atomicAdd(&p.ws.ctl->deep_count, __popc(db));
+            qb = __shfl_sync(0xffffffffu, qb, 0);
+            if (deep) p.ws.slow_list[p.n_v + qb + __popc(db & ((1u << lane) - 1u))] = j;
+            vres_init(res);
+        }
+        bool fits;
+        int excl;
+        const long long base = pool_place<T, KW>(deep ? 0 : res.cnt, res, p, lane, fits, excl);
+        if (mine && !deep) {
+            p.ws.vbm[j] = res.bm;
+            if (fits) {
+                const long long off = base + excl;
+                p.out_desc[j] = make_int2((int)off, res.cnt);
+                if (out_mask) emit_window<T, KW>(w, out_mask, off, p);
+            }
+        }
     }
 }
 
-// fixup kernel: the columns the fast path left behind.  Work unit = half a
-// queued tile (64 columns), staged in shared memory (half tiles fit the
-// stage even in dense bands); one warp per wide column (warp_column).
-// Half tiles that still exceed the stage use the exact windowed
-// global-memory path, one thread per column.
+// tier 3: exact windowed global-memory algorithm (no width limit)
 template <typename T, bool UNIFORM, bool IN_CANON>
-__global__ void __launch_bounds__(FT_TPB) fixup_kernel(const StepParams p) {
-    constexpr int HALF = FT_TPB / 2;
-    Stage<T, UNIFORM>& stg = *reinterpret_cast<Stage<T, UNIFORM>*>(ft_dyn_smem);
-    __shared__ int s_list[HALF];
-    __shared__ int s_cnt[HALF];
-    __shared__ int s_skel[HALF];
-    __shared__ double s_bm[HALF];
-    __shared__ double s_mx[HALF];
-    __shared__ int s_ns;
-    __shared__ int s_scan[FT_WARPS];
-    __shared__ long long s_base;
-    __shared__ double s_recip[33];
+__global__ void __launch_bounds__(FT_TPB) deep_kernel(const StepParams p) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
-    if (threadIdx.x < 33) s_recip[threadIdx.x] = c_recip[threadIdx.x];
-    const int n_units = 2 * *(volatile int*)&p.ws.ctl->slow_count;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int q = blockIdx.x; q < n_units; q += gridDim.x) {
-        const int tile = p.ws.slow_list[q >> 1];
-        const int half = q & 1;
-        const int v0 = half * HALF;
-        const int j0 = tile * FT_TPB + v0;
-        const int jn = max(0, min(HALF, p.n_v - j0));
-        const unsigned int* msk = &p.ws.slow_mask[(size_t)tile * FT_WARPS + half * (HALF / 32)];
-        const unsigned int m0 = msk[0], m1 = msk[1];
-        if ((m0 | m1) == 0u || jn == 0) continue;   // block-uniform
-        if (tid == 0) {
-            int n = 0;
-            for (int v = 0; v < HALF; ++v)
-                if (((v < 32 ? m0 : m1) >> (v & 31)) & 1u) s_list[n++] = v;
-            s_ns = n;
+    const int n_deep = *(volatile int*)&p.ws.ctl->deep_count;
+    const int lane = threadIdx.x & 31;
+    const int stride = gridDim.x * FT_TPB;
+    const int rounds = (n_deep + stride - 1) / stride;
+    for (int rnd = 0; rnd < rounds; ++rnd) {
+        const int i = rnd * stride + blockIdx.x * FT_TPB + threadIdx.x;
+        const bool mine = i < n_deep;
+        const int j = mine ? p.ws.slow_list[p.n_v + i] : 0;
+        VRes res;
+        vres_init(res);
+        if (mine) {
+            vertex_slow<T, 8, UNIFORM, IN_CANON>(j, p, res, 0, false);
+            report_flags(res, j, p);
         }
-        const bool staged = stage_tile<T, UNIFORM, IN_CANON>(stg, j0, jn, p);   // syncs
-        const int ns = s_ns;
-        // counting passes
-        if (staged) {
-            for (int k = warp; k < ns; k += FT_WARPS) {
-                const int v = s_list[k];
-                VRes res;
-                vres_init(res);
-                warp_column<T, UNIFORM>(stg, v, j0 + v, p, s_recip, res, -1);
-                if (lane == 0) {
-                    s_cnt[k] = res.cnt; s_skel[k] = res.nskel; s_bm[k] = res.bm; s_mx[k] = res.maxd;
-                    report_flags(res, j0 + v, p);
-                }
-            }
-        } else if (tid < ns) {
-            const int v = s_list[tid];
-            VRes res;
-            vres_init(res);
-            vertex_slow<T, 8, UNIFORM, IN_CANON>(j0 + v, p, res, 0, false);
-            s_cnt[tid] = res.cnt; s_skel[tid] = res.nskel; s_bm[tid] = res.bm; s_mx[tid] = res.maxd;
-            report_flags(res, j0 + v, p);
-        }
-        __syncthreads();
-        int total;
-        const int loc = block_excl_scan<FT_TPB>(tid < ns ? s_cnt[tid] : 0, s_scan, &total);
-        if (tid == 0) {
-            long long base = 0;
-            if (total > 0) {
-                base = (long long)p.num_tiles * FT_SLOT +
-                       (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)total);
-                if (base + total > p.cap) { atomicExch(&p.ws.ctl->overflow, 1); base = -1; }
-            }
-            s_base = base;
-            double bm = 0.0, mx = 0.0;
-            long long sk = 0;
-            for (int k = 0; k < ns; ++k) { bm = bm + s_bm[k]; mx = fmax(mx, s_mx[k]); sk += s_skel[k]; }
-            p.ws.tile_bm_slow[2 * tile + half] = bm;
-            if (mx > 0.0) atomicMax(&p.ws.ctl->maxdelta_bits, (unsigned long long)__double_as_longlong(mx));
-            if (sk) atomicAdd(&p.ws.ctl->skel_total, (unsigned long long)sk);
-            if (total) atomicAdd(&p.ws.ctl->nnz_total, (unsigned long long)total);
-        }
-        if (tid < ns) s_cnt[tid] = loc;    // reuse: column offset within the unit
-        __syncthreads();
-        const long long base = s_base;
-        if (base >= 0) {
-            if (staged) {
-                for (int k = warp; k < ns; k += FT_WARPS) {
-                    const int v = s_list[k];
-                    const long long off = base + s_cnt[k];
-                    VRes res;
-                    vres_init(res);
-                    warp_column<T, UNIFORM>(stg, v, j0 + v, p, s_recip, res, off);
-                    if (lane == 0) p.out_desc[j0 + v] = make_int2((int)off, res.cnt);
-                }
-            } else if (tid < ns) {
-                const int v = s_list[tid];
-                const long long off = base + s_cnt[tid];
-                VRes res;
-                vres_init(res);
-                vertex_slow<T, 8, UNIFORM, IN_CANON>(j0 + v, p, res, off, true);
-                p.out_desc[j0 + v] = make_int2((int)off, res.cnt);
+        bool fits;
+        int excl;
+        const long long base = pool_place<T, 8>(res.cnt, res, p, lane, fits, excl);
+        if (mine) {
+            p.ws.vbm[j] = res.bm;
+            if (fits) {
+                const long long off = base + excl;
+                p.out_desc[j] = make_int2((int)off, res.cnt);
+                if (res.cnt) vertex_slow<T, 8, UNIFORM, IN_CANON>(j, p, res, off, true);
             }
         }
-        __syncthreads();
     }
 }
 
@@ -1061,7 +855,19 @@ __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizePara
     double acc = 0.0, amx = 0.0;
     long long acnt = 0, askel = 0;
     for (int t = t0 + tid; t < t1; t += FT_FIN_TPB) {
-        acc = acc + (f.ws.tile_bm[t] + (f.ws.tile_bm_slow[2 * t] + f.ws.tile_bm_slow[2 * t + 1]));
+        double tb = f.ws.tile_bm[t];
+        const uint4 mk = *reinterpret_cast<const uint4*>(&f.ws.slow_mask[(size_t)t * FT_WARPS]);
+        const unsigned int mw[4] = {mk.x, mk.y, mk.z, mk.w};
+#pragma unroll
+        for (int k = 0; k < FT_WARPS; ++k) {
+            unsigned int m = mw[k];
+            while (m) {   // wide columns of the tile, in vertex order
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                tb = tb + f.ws.vbm[(size_t)t * FT_TPB + k * 32 + b];
+            }
+        }
+        acc = acc + tb;
         amx = fmax(amx, f.ws.tile_maxd[t]);
         const int2 cs = f.ws.tile_cs[t];
         acnt += cs.x;
@@ -1147,6 +953,7 @@ __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizePara
     ctl->nan_key = 0u;
     ctl->overflow = 0;
     ctl->slow_count = 0;
+    ctl->deep_count = 0;
     if (f.evolve) {
         if (status != FT_STATUS_OK) {
             ctl->done = 1;
@@ -1306,44 +1113,32 @@ __global__ void evolve_report_kernel(const Control* ctl, long long* control) {
 
 typedef void (*StepKernelFn)(const StepParams);
 
-struct KernelPick {
-    StepKernelFn fn;
-    size_t smem;
-};
-
-template <typename T, bool UNIFORM>
-static size_t stage_bytes() { return sizeof(Stage<T, UNIFORM>); }
-
-static KernelPick with_smem(StepKernelFn fn, size_t bytes) {
-    // opt in to > 48 KB dynamic shared memory once per kernel
-    static StepKernelFn done[64];
-    static int n_done = 0;
-    bool seen = false;
-    for (int i = 0; i < n_done; ++i) seen |= (done[i] == fn);
-    if (!seen) {
-        cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-        if (n_done < 64) done[n_done++] = fn;
-    }
-    return KernelPick{fn, bytes};
-}
-
-static KernelPick pick_fixup(int dtype, bool uniform, bool in_canon) {
-    if (dtype == FT_F64) {
-        if (uniform) return with_smem(in_canon ? fixup_kernel<double, true, true> : fixup_kernel<double, true, false>, stage_bytes<double, true>());
-        return with_smem(in_canon ? fixup_kernel<double, false, true> : fixup_kernel<double, false, false>, stage_bytes<double, false>());
-    }
-    if (uniform) return with_smem(in_canon ? fixup_kernel<float, true, true> : fixup_kernel<float, true, false>, stage_bytes<float, true>());
-    return with_smem(in_canon ? fixup_kernel<float, false, true> : fixup_kernel<float, false, false>, stage_bytes<float, false>());
-}
-
 template <int K>
-static KernelPick pick_kernel(int dtype, bool uniform, bool in_canon) {
+static StepKernelFn pick_step(int dtype, bool uniform, bool in_canon) {
     if (dtype == FT_F64) {
-        if (uniform) return with_smem(in_canon ? step_kernel<double, K, true, true> : step_kernel<double, K, true, false>, stage_bytes<double, true>());
-        return with_smem(in_canon ? step_kernel<double, K, false, true> : step_kernel<double, K, false, false>, stage_bytes<double, false>());
+        if (uniform) return in_canon ? step_kernel<double, K, true, true> : step_kernel<double, K, true, false>;
+        return in_canon ? step_kernel<double, K, false, true> : step_kernel<double, K, false, false>;
     }
-    if (uniform) return with_smem(in_canon ? step_kernel<float, K, true, true> : step_kernel<float, K, true, false>, stage_bytes<float, true>());
-    return with_smem(in_canon ? step_kernel<float, K, false, true> : step_kernel<float, K, false, false>, stage_bytes<float, false>());
+    if (uniform) return in_canon ? step_kernel<float, K, true, true> : step_kernel<float, K, true, false>;
+    return in_canon ? step_kernel<float, K, false, true> : step_kernel<float, K, false, false>;
+}
+
+static StepKernelFn pick_deep(int dtype, bool uniform, bool in_canon) {
+    if (dtype == FT_F64) {
+        if (uniform) return in_canon ? deep_kernel<double, true, true> : deep_kernel<double, true, false>;
+        return in_canon ? deep_kernel<double, false, true> : deep_kernel<double, false, false>;
+    }
+    if (uniform) return in_canon ? deep_kernel<float, true, true> : deep_kernel<float, true, false>;
+    return in_canon ? deep_kernel<float, false, true> : deep_kernel<float, false, false>;
+}
+
+static StepKernelFn pick_wide(int dtype, bool uniform, bool in_canon) {
+    if (dtype == FT_F64) {
+        if (uniform) return in_canon ? wide_kernel<double, true, true> : wide_kernel<double, true, false>;
+        return in_canon ? wide_kernel<double, false, true> : wide_kernel<double, false, false>;
+    }
+    if (uniform) return in_canon ? wide_kernel<float, true, true> : wide_kernel<float, true, false>;
+    return in_canon ? wide_kernel<float, false, true> : wide_kernel<float, false, false>;
 }
 
 }  // namespace ft
@@ -1396,7 +1191,7 @@ static int check_tiled(const ft_tiled* t, int n_rows, int n_cols) {
 }
 
 static int g_window = 0;
-static int g_fixup_grid = 2 * 148;
+static int g_fixup_grid = 4 * 148;
 
 static int window_size() {
     if (g_window == 0) {
@@ -1405,11 +1200,11 @@ static int window_size() {
         for (int n = 1; n <= 32; ++n) h[n] = 1.0 / (double)n;
         cudaMemcpyToSymbol(ft::c_recip, h, sizeof(h));
         const char* s = getenv("FT_WINDOW");
-        g_window = (s && atoi(s) == 8) ? 8 : 4;   // default: 4-row register window
+        g_window = (s && atoi(s) == 4) ? 4 : 2;   // default: 2-row register window
         int dev = 0, sms = 148;
         if (cudaGetDevice(&dev) == cudaSuccess &&
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
-            g_fixup_grid = 2 * sms;
+            g_fixup_grid = 4 * sms;
     }
     return g_window;
 }
@@ -1450,11 +1245,14 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_
     p.finite = std::isfinite(p.w) && std::isfinite(p.a) && std::isfinite(p.e) && std::isfinite(p.eb) &&
                std::isfinite(p.mu) && std::isfinite(p.dt);
     const bool uni = lap_flags == FT_LAP_UNIFORM;
-    const ft::KernelPick k = window_size() == 8 ? ft::pick_kernel<8>(dtype, uni, in_canon != nullptr)
-                                                : ft::pick_kernel<4>(dtype, uni, in_canon != nullptr);
-    if (which & 1) k.fn<<<p.num_tiles, FT_TPB, k.smem, s>>>(p);
-    const ft::KernelPick fx = ft::pick_fixup(dtype, uni, in_canon != nullptr);
-    if (which & 2) fx.fn<<<g_fixup_grid, FT_TPB, fx.smem, s>>>(p);
+    const bool ic = in_canon != nullptr;
+    const ft::StepKernelFn k = window_size() == 4 ? ft::pick_step<4>(dtype, uni, ic)
+                                                  : ft::pick_step<2>(dtype, uni, ic);
+    if (which & 1) k<<<p.num_tiles, FT_TPB, 0, s>>>(p);
+    if (which & 2) {
+        ft::pick_wide(dtype, uni, ic)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
+        ft::pick_deep(dtype, uni, ic)<<<g_fixup_grid / 4, FT_TPB, 0, s>>>(p);
+    }
     return cuda_check("step kernel");
 }
 
