@@ -197,6 +197,36 @@ int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
  * (field.py:324-356).  labels: int64[n_cols]. */
 int ft_labels(const ft_csc* phi, int32_t dtype, int64_t* labels, void* stream);
 
+/* -- Lloyd step ---------------------------------------------------------- */
+/* Faces per layer row: the pattern (and values) of the reference's
+ * faces_by_cell product  M^T * PHI^T  (lloyd.py:21-28): face f is in row r
+ * when sum_{v in f, ascending} PHI(r, v) != 0, faces ascending per row.
+ * Two calls: cell_faces == NULL counts (cell_ptr[n_rows+1] filled, the
+ * caller allocates cell_ptr[n_rows] entries), then the fill.  Rows below
+ * min_row are skipped (min_row = 1: cells only).  scratch: int32[2*n_rows].
+ * *big_flag (device) != 0 when a row holds more than 16384 faces and was
+ * left unsorted (the caller sorts those segments).  PHI must be FT_F64. */
+int ft_faces_by_cell(const ft_csc* phi, int32_t min_row, int32_t n_faces,
+                     const int32_t* faces, int32_t* cell_ptr, int32_t* cell_faces,
+                     double* cell_values, int32_t* scratch, int32_t* big_flag,
+                     void* stream);
+
+/* Per cell c (layer row c+1): approximate centroid and normal
+ * (approx_centroid, lloyd.py:42-64) and the back-projected seed vertex
+ * (backproject, lloyd.py:67-112), with numpy's exact reduction orders.
+ * status[c]: 0 ok, 1 vanished, 2 degenerate, 3 null normal, 4 ray miss;
+ * hit_vertex[c] = vertex id or -1.  period: the 2 lattice vectors of a
+ * torus mesh as 6 doubles in HOST memory, or NULL.  seeds: int64[n_cells]
+ * (device).  All other pointers are device memory. */
+int ft_lloyd_centroids(const double* positions, int32_t n_vertices,
+                       const int32_t* faces, int32_t n_faces,
+                       const double* face_area, const double* face_bary,
+                       const double* face_normal, const double* period,
+                       int32_t n_cells, const int32_t* cell_ptr,
+                       const int32_t* cell_faces, const int64_t* seeds,
+                       double* point, double* normal, int32_t* status,
+                       int32_t* hit_vertex, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -309,3 +309,34 @@ def init_field_np(neighbor_ptr, neighbor_idx, n_v, seeds):
         col_ptr.append(len(rows))
     return Csc(seeds.size + 1, n_v, np.array(col_ptr), np.array(rows),
                np.array(vals))
+
+
+# ---------------------------------------------------------------------------
+# Lloyd: faces per layer row (lloyd.py:21-28 via sparse.spgemm)
+
+
+def faces_by_cell_np(phi, faces):
+    """Pattern and values of M^T Phi^T: face f in row r when the sum over
+    its vertices (ascending) of PHI(r, v) is nonzero; rows of the result are
+    the layer rows (including the base row 0), faces ascending.  Literal
+    per-face loop."""
+    phi = Csc.of(phi)
+    n_f = faces.shape[0]
+    per_row = {}
+    for f in range(n_f):
+        acc = {}
+        for v in sorted(int(x) for x in faces[f]):
+            rows, vals = phi.column(v)
+            for r, x in zip(rows.tolist(), vals.tolist()):
+                acc[r] = acc[r] + x if r in acc else x
+        for r, x in acc.items():
+            if x != 0.0:
+                per_row.setdefault(r, []).append((f, x))
+    ptr = [0]
+    idx, val = [], []
+    for r in range(phi.n_rows):
+        for f, x in per_row.get(r, []):
+            idx.append(f)
+            val.append(x)
+        ptr.append(len(idx))
+    return np.array(ptr, dtype=np.int32), np.array(idx, dtype=np.int32), np.array(val)

@@ -81,7 +81,7 @@ assert STATS_DTYPE.itemsize == STATS_BYTES
 EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
            "ft_workspace_init", "ft_tile_slot_entries", "ft_tiled_min_capacity",
            "ft_step", "ft_step_kernel", "ft_step_fixup", "ft_step_finalize", "ft_compact",
-           "ft_evolve", "ft_labels")
+           "ft_evolve", "ft_labels", "ft_faces_by_cell", "ft_lloyd_centroids")
 
 _lib = None
 
@@ -124,6 +124,12 @@ def _declare(lib):
     lib.ft_evolve.restype = ctypes.c_int
     lib.ft_labels.argtypes = [P(FtCsc), ctypes.c_int32, vp, vp]
     lib.ft_labels.restype = ctypes.c_int
+    i32 = ctypes.c_int32
+    lib.ft_faces_by_cell.argtypes = [P(FtCsc), i32, i32, vp, vp, vp, vp, vp, vp, vp]
+    lib.ft_faces_by_cell.restype = ctypes.c_int
+    lib.ft_lloyd_centroids.argtypes = [vp, i32, vp, i32, vp, vp, vp, vp, i32, vp, vp, vp,
+                                       vp, vp, vp, vp, vp]
+    lib.ft_lloyd_centroids.restype = ctypes.c_int
 
 
 def lib():

@@ -250,6 +250,36 @@ def make_c1_dual(fld, mesh):
     print("c1_dual: triangles", len(res["triangles"]), "euler", res["euler"])
 
 
+def make_cell_geometry(name, mesh, fld):
+    """Reference approx_centroid / backproject for every cell of fld."""
+    from fieldtess import lloyd as L
+    prod = L.faces_by_cell(fld, mesh)
+    n = fld.n_cells
+    pts = np.full((n, 3), np.nan)
+    nrm = np.full((n, 3), np.nan)
+    status = np.zeros(n, dtype=np.int64)
+    hit = np.full(n, -1, dtype=np.int64)
+    for c in range(n):
+        try:
+            faces = L.cell_triangles(fld, mesh, c, product=prod)
+            p, q = L.approx_centroid(fld, mesh, c, faces=faces)
+            pts[c], nrm[c] = p, q
+            h = L.backproject(p, q, fld, mesh, c, faces=faces)
+            if h is None:
+                status[c] = 4
+            else:
+                hit[c] = h
+        except ft.errors.VanishedCellError:
+            status[c] = 1
+        except ft.errors.DegenerateCellError:
+            status[c] = 2
+        except ft.errors.NullNormalError:
+            status[c] = 3
+    out = {f"{name}_point": pts, f"{name}_normal": nrm, f"{name}_status": status, f"{name}_hit": hit}
+    out.update(csc_arrays(f"{name}_fbc", prod))
+    return out
+
+
 def make_c2(seeds_c2):
     mesh = ft.gen_icosphere(7)
     trajectory(mesh, seeds_c2, {100, 1000}, os.path.join(HERE, "c2_traj.npz"), 1000)
@@ -274,8 +304,12 @@ def main():
     c1 = trajectory(ico4, seeds["ico4"], {1, 2, 10, 100, 500},
                     os.path.join(HERE, "c1_traj.npz"), 500)
     make_c1_dual(c1, ico4)
-    trajectory(ft.gen_periodic_grid(64, 64), seeds["torus64"], {1, 60, 300},
-               os.path.join(HERE, "torus_traj.npz"), 300)
+    geo = make_cell_geometry("c1", ico4, c1)
+    torus = ft.gen_periodic_grid(64, 64)
+    tfld = trajectory(torus, seeds["torus64"], {1, 60, 300},
+                      os.path.join(HERE, "torus_traj.npz"), 300)
+    geo.update(make_cell_geometry("torus", torus, tfld))
+    np.savez_compressed(os.path.join(HERE, "cell_geometry.npz"), **geo)
     if "--big" in sys.argv:
         mesh = ft.gen_icosphere(7)
         seeds_c2 = sample_seed_vertices(mesh, 1024, 0)

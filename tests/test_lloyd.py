@@ -1,0 +1,90 @@
+"""Lloyd step parity: faces per cell, centroids / normals, back-projected
+seeds (bitwise against the reference's own functions, tests/golden/
+cell_geometry.npz) and the C2 5-iteration Lloyd history (c2_lloyd.json)."""
+
+import numpy as np
+import pytest
+
+import paper_1804_09152_b200 as ft
+from conftest import csc_from, golden_json, golden_npz
+
+
+def _field(traj, snap):
+    t = golden_npz(traj)
+    c = csc_from(t, f"s{snap}")
+    return ft.LayeredField(ft.SparseMat(c.n_rows, c.n_cols, c.col_ptr, c.row_idx, c.values,
+                                        check=False), t["seeds"], step_count=snap)
+
+
+CASES = [("c1", "c1_traj.npz", 500, lambda: ft.gen_icosphere(4)),
+         ("torus", "torus_traj.npz", 300, lambda: ft.gen_periodic_grid(64, 64))]
+
+
+@pytest.mark.parametrize("name,traj,snap,mk", CASES)
+def test_host_helpers_match_reference(name, traj, snap, mk):
+    """The host single-cell helpers restate the reference exactly."""
+    g = golden_npz("cell_geometry.npz")
+    mesh, fld = mk(), _field(traj, snap)
+    prod = ft.SparseMat(*g[f"{name}_fbc_shape"], g[f"{name}_fbc_ptr"], g[f"{name}_fbc_idx"],
+                        g[f"{name}_fbc_val"], check=False)
+    for c in range(fld.n_cells):
+        st = int(g[f"{name}_status"][c])
+        if st == 1:
+            with pytest.raises(ft.errors.VanishedCellError):
+                ft.cell_triangles(fld, mesh, c, product=prod)
+            continue
+        faces = ft.cell_triangles(fld, mesh, c, product=prod)
+        p, n = ft.approx_centroid(fld, mesh, c, faces=faces)
+        assert np.array_equal(p, g[f"{name}_point"][c]) and np.array_equal(n, g[f"{name}_normal"][c])
+        h = ft.backproject(p, n, fld, mesh, c, faces=faces)
+        assert (h if h is not None else -1) == g[f"{name}_hit"][c]
+
+
+def test_oracle_faces_by_cell_matches_reference():
+    from oracle import pyoracle as po
+    g = golden_npz("cell_geometry.npz")
+    mesh, fld = ft.gen_icosphere(4), _field("c1_traj.npz", 500)
+    ptr, idx, val = po.faces_by_cell_np(po.Csc.of(fld.phi), mesh.faces)
+    assert np.array_equal(ptr, g["c1_fbc_ptr"]) and np.array_equal(idx, g["c1_fbc_idx"])
+    assert np.array_equal(val, g["c1_fbc_val"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,traj,snap,mk", CASES)
+def test_device_faces_by_cell(name, traj, snap, mk):
+    g = golden_npz("cell_geometry.npz")
+    prod = ft.faces_by_cell(_field(traj, snap), mk())
+    assert np.array_equal(prod.col_ptr, g[f"{name}_fbc_ptr"])
+    assert np.array_equal(prod.row_idx[:prod.nnz], g[f"{name}_fbc_idx"])
+    assert np.array_equal(prod.values[:prod.nnz], g[f"{name}_fbc_val"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,traj,snap,mk", CASES)
+def test_device_cell_geometry_bitwise(name, traj, snap, mk):
+    from paper_1804_09152_b200.lloyd import cell_geometry
+    g = golden_npz("cell_geometry.npz")
+    point, normal, status, hit = cell_geometry(_field(traj, snap), mk())
+    ok = g[f"{name}_status"] == 0
+    assert np.array_equal(status, g[f"{name}_status"])
+    assert np.array_equal(point[ok], g[f"{name}_point"][ok])
+    assert np.array_equal(normal[ok], g[f"{name}_normal"][ok])
+    assert np.array_equal(hit, g[f"{name}_hit"])
+
+
+@pytest.mark.gpu
+def test_lloyd_c2_five_iterations_match_reference():
+    """BASELINE configs[1]: icosphere-7, 1024 seeds, 5 Lloyd iterations."""
+    ref = golden_json("c2_lloyd.json")["history"]
+    seeds = np.asarray(golden_json("seeds_c2.json"), dtype=np.int64)
+    mesh = ft.gen_icosphere(7)
+    lap = ft.build_laplacian(mesh)
+    state = ft.lloyd_iterate(ft.LloydState(seeds=seeds), mesh, lap, ft.CouplingParams(),
+                             n_iter=5, max_steps=1000)
+    assert len(state.history) == len(ref) == 6
+    for got, want in zip(state.history, ref):
+        assert got["seeds"] == want["seeds"], got["iteration"]
+        assert got["steps"] == want["steps"]
+        assert got["reseed_misses"] == want["reseed_misses"]
+        assert got["seed_collisions"] == want["seed_collisions"]
+        assert got["area_variance"] == want["area_variance"]
