@@ -227,6 +227,23 @@ int ft_lloyd_centroids(const double* positions, int32_t n_vertices,
                        double* point, double* normal, int32_t* status,
                        int32_t* hit_vertex, void* stream);
 
+/* -- dual-mesh adjacency products --------------------------------------- */
+/* One pass over vertices and faces of a (FT_F64) field collects, as keys in
+ * four device hash sets (capacity: a power of two; empty slot = ~0):
+ *   set_v  A_v pairs i<j (key i*n_cells+j): cells sharing a vertex with
+ *          phi >= threshold                          (dual.py:60-91)
+ *   set_t  A_t pairs: cells sharing a face of B = PHIbar M   (dual.py:94-99)
+ *   set_x  A_t pairs whose threshold isolines cross inside a shared face of
+ *          positive area                             (dual.py:107-215)
+ *   set_3  junction triples i<j<k (key (i*n+j)*n+k) of every face with >= 3
+ *          cells                                     (dual.py:223-231)
+ * n_faces == 0 computes set_v only.  *overflow (device): 1 = a set is full,
+ * 2 = a vertex/face carries more than 32 thresholded cells. */
+int ft_dual_products(const ft_csc* phi, int32_t n_faces, const int32_t* faces,
+                     const double* face_area, double threshold, uint64_t* set_v,
+                     uint64_t* set_t, uint64_t* set_x, uint64_t* set_3,
+                     int64_t set_capacity, int32_t* overflow, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -340,3 +340,67 @@ def faces_by_cell_np(phi, faces):
             val.append(x)
         ptr.append(len(idx))
     return np.array(ptr, dtype=np.int32), np.array(idx, dtype=np.int32), np.array(val)
+
+
+# ---------------------------------------------------------------------------
+# dual: boolean products, crossing tests, junction triples (dual.py:60-233)
+
+
+def dual_products_np(phi, faces, face_area, threshold):
+    """Literal restatement: A_v pairs, A_t pairs, A_t pairs whose isolines
+    cross in some shared positive-area face, and junction triples."""
+    phi = Csc.of(phi)
+    n_v = phi.n_cols
+    cells_of_v = []
+    for v in range(n_v):
+        rows, vals = phi.column(v)
+        cells_of_v.append(sorted(int(r) - 1 for r, x in zip(rows, vals) if r >= 1 and x >= threshold))
+    pv, pt, px, tri = set(), set(), set(), set()
+    for cl in cells_of_v:
+        for a in range(len(cl)):
+            for b in range(a + 1, len(cl)):
+                pv.add((cl[a], cl[b]))
+    emb = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0]])
+
+    def seg(values):
+        rel = values - threshold
+        pts = []
+        for a, b in ((0, 1), (1, 2), (2, 0)):
+            if rel[a] * rel[b] < 0.0:
+                s = rel[a] / (rel[a] - rel[b])
+                if not np.isfinite(s):
+                    return None
+                pts.append(emb[a] + s * (emb[b] - emb[a]))
+        return pts if len(pts) == 2 else None
+
+    def orient(a, b, c):
+        d = (b[0] - a[0]) * (c[1] - a[1]) - (b[1] - a[1]) * (c[0] - a[0])
+        return int(d > 0.0) - int(d < 0.0)
+
+    def onseg(a, b, c):
+        return min(a[0], b[0]) <= c[0] <= max(a[0], b[0]) and min(a[1], b[1]) <= c[1] <= max(a[1], b[1])
+
+    def inter(p, q):
+        o1, o2, o3, o4 = orient(p[0], p[1], q[0]), orient(p[0], p[1], q[1]), orient(q[0], q[1], p[0]), orient(q[0], q[1], p[1])
+        return ((o1 != o2 and o3 != o4) or (o1 == 0 and onseg(p[0], p[1], q[0])) or (o2 == 0 and onseg(p[0], p[1], q[1]))
+                or (o3 == 0 and onseg(q[0], q[1], p[0])) or (o4 == 0 and onseg(q[0], q[1], p[1])))
+
+    def get(r, v):
+        rows, vals = phi.column(v)
+        k = np.searchsorted(rows, r)
+        return float(vals[k]) if k < rows.size and rows[k] == r else 0.0
+
+    for f in range(faces.shape[0]):
+        cl = sorted(set(c for v in faces[f] for c in cells_of_v[int(v)]))
+        for a in range(len(cl)):
+            for b in range(a + 1, len(cl)):
+                pt.add((cl[a], cl[b]))
+                if face_area[f] > 0.0:
+                    vi = np.array([get(cl[a] + 1, int(v)) for v in faces[f]])
+                    vj = np.array([get(cl[b] + 1, int(v)) for v in faces[f]])
+                    si, sj = seg(vi), seg(vj)
+                    if si is not None and sj is not None and inter(si, sj):
+                        px.add((cl[a], cl[b]))
+                for c in range(b + 1, len(cl)):
+                    tri.add((cl[a], cl[b], cl[c]))
+    return sorted(pv), sorted(pt), sorted(px), sorted(tri)

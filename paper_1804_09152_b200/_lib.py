@@ -81,7 +81,8 @@ assert STATS_DTYPE.itemsize == STATS_BYTES
 EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
            "ft_workspace_init", "ft_tile_slot_entries", "ft_tiled_min_capacity",
            "ft_step", "ft_step_kernel", "ft_step_fixup", "ft_step_finalize", "ft_compact",
-           "ft_evolve", "ft_labels", "ft_faces_by_cell", "ft_lloyd_centroids")
+           "ft_evolve", "ft_labels", "ft_faces_by_cell", "ft_lloyd_centroids",
+           "ft_dual_products")
 
 _lib = None
 
@@ -130,6 +131,9 @@ def _declare(lib):
     lib.ft_lloyd_centroids.argtypes = [vp, i32, vp, i32, vp, vp, vp, vp, i32, vp, vp, vp,
                                        vp, vp, vp, vp, vp]
     lib.ft_lloyd_centroids.restype = ctypes.c_int
+    lib.ft_dual_products.argtypes = [P(FtCsc), i32, vp, vp, ctypes.c_double, vp, vp, vp, vp,
+                                     ctypes.c_int64, vp, vp]
+    lib.ft_dual_products.restype = ctypes.c_int
 
 
 def lib():

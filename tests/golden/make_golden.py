@@ -229,7 +229,7 @@ def make_seeds_and_meshes():
     return seeds
 
 
-def make_c1_dual(fld, mesh):
+def make_c1_dual(fld, mesh, name="c1_dual.json"):
     from fieldtess import dual as dualmod
     a_v = dualmod.vertex_adjacency(fld, 0.25)
     a_t = dualmod.triangle_adjacency(fld, mesh, 0.25)
@@ -245,9 +245,9 @@ def make_c1_dual(fld, mesh):
         "spurious": [list(map(int, t)) for t in dm.spurious_removed],
         "euler": int(dm.euler_characteristic()),
     }
-    with open(os.path.join(HERE, "c1_dual.json"), "w") as fh:
+    with open(os.path.join(HERE, name), "w") as fh:
         json.dump(res, fh)
-    print("c1_dual: triangles", len(res["triangles"]), "euler", res["euler"])
+    print(name, "triangles", len(res["triangles"]), "euler", res["euler"])
 
 
 def make_cell_geometry(name, mesh, fld):
@@ -282,7 +282,8 @@ def make_cell_geometry(name, mesh, fld):
 
 def make_c2(seeds_c2):
     mesh = ft.gen_icosphere(7)
-    trajectory(mesh, seeds_c2, {100, 1000}, os.path.join(HERE, "c2_traj.npz"), 1000)
+    c2 = trajectory(mesh, seeds_c2, {100, 1000}, os.path.join(HERE, "c2_traj.npz"), 1000)
+    make_c1_dual(c2, mesh, "c2_dual.json")
     from fieldtess.lloyd import LloydState, lloyd_iterate
     lap = ft.build_laplacian(mesh, "uniform")
     t0 = time.time()

@@ -1,0 +1,69 @@
+"""Dual-mesh extraction parity: device adjacency products + host curation
+against the reference's outputs on C1 (icosphere-4, 64 seeds, 500 steps)
+and C2 (icosphere-7, 1024 seeds, 1000 steps) -- tests/golden/c{1,2}_dual.json."""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_1804_09152_b200 as ft
+from conftest import GOLDEN, csc_from, golden_json, golden_npz
+
+
+def _field(traj, snap):
+    t = golden_npz(traj)
+    c = csc_from(t, f"s{snap}")
+    return ft.LayeredField(ft.SparseMat(c.n_rows, c.n_cols, c.col_ptr, c.row_idx, c.values,
+                                        check=False), t["seeds"], step_count=snap)
+
+
+def test_oracle_dual_products_match_reference():
+    from oracle import pyoracle as po
+    ref = golden_json("c1_dual.json")
+    mesh, fld = ft.gen_icosphere(4), _field("c1_traj.npz", 500)
+    pv, pt, px, tri = po.dual_products_np(fld.phi, mesh.faces, mesh.face_area, 0.25)
+    assert [list(p) for p in pv] == ref["a_v"]
+    assert [list(p) for p in pt] == ref["a_t"]
+    assert [list(t) for t in tri] == ref["triples"]
+    confirmed = set(map(tuple, ref["curated"])) - set(map(tuple, ref["a_v"]))
+    assert confirmed <= set(px)
+    for i, j, why in ref["dropped"]:
+        if why == "no-intersection":
+            assert (i, j) not in set(px)
+
+
+def test_segments_intersect_cases():
+    from paper_1804_09152_b200.dual import segments_intersect
+    p = np.array([[0.0, 0.0], [1.0, 1.0]])
+    assert segments_intersect(p, np.array([[0.0, 1.0], [1.0, 0.0]]))
+    assert not segments_intersect(p, np.array([[2.0, 2.0], [3.0, 3.5]]))
+    assert segments_intersect(p, np.array([[1.0, 1.0], [2.0, 0.0]]))   # touching counts
+
+
+def _check_case(name, traj, snap, mesh):
+    ref = golden_json(name)
+    fld = _field(traj, snap)
+    a_v = ft.vertex_adjacency(fld, 0.25)
+    a_t = ft.triangle_adjacency(fld, mesh, 0.25)
+    assert sorted(map(list, a_v.pairs())) == ref["a_v"]
+    assert sorted(map(list, a_t.pairs())) == ref["a_t"]
+    cur = ft.confirm_candidates(fld, mesh, a_v, a_t, 0.25)
+    assert sorted(map(list, cur.pairs())) == ref["curated"]
+    assert [[int(i), int(j), w] for i, j, w in cur.dropped] == ref["dropped"]
+    assert sorted(map(list, cur.junction_triples)) == ref["triples"]
+    dm = ft.build_dual(cur, np.zeros((fld.n_cells, 3)))
+    assert sorted(map(sorted, dm.triangles.tolist())) == ref["triangles"]
+    assert [list(map(int, t)) for t in dm.spurious_removed] == ref["spurious"]
+    assert int(dm.euler_characteristic()) == ref["euler"]
+
+
+@pytest.mark.gpu
+def test_dual_c1_matches_reference():
+    _check_case("c1_dual.json", "c1_traj.npz", 500, ft.gen_icosphere(4))
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "c2_dual.json")), reason="no C2 dual golden")
+def test_dual_c2_matches_reference():
+    _check_case("c2_dual.json", "c2_traj.npz", 1000, ft.gen_icosphere(7))
