@@ -1343,6 +1343,62 @@ extern "C" int ft_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi
     return launch_compact(c, dtype, s);
 }
 
+// The steady part of evolve (steps 1, 2, ...: a -> b, b -> a) repeats with
+// period 2, so kGraphSteps steps are captured once into a CUDA graph and
+// replayed; steps past max_steps / convergence are device-side no-ops (the
+// kernels test the done flag).  Graphs are cached by their full launch
+// configuration.
+constexpr int kGraphSteps = 16;
+
+struct GraphKey {
+    const void* ptrs[12];
+    long long caps[3];
+    double prm[8];
+    int ints[5];
+    bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
+};
+
+struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    bool used;
+};
+
+static GraphEntry g_graphs[8];
+static int g_graph_next = 0;
+
+// private non-blocking stream for capture and replay (the caller's stream may
+// be the legacy default stream, which cannot be captured); ordered against the
+// caller's stream with events
+static cudaStream_t g_gstream = nullptr;
+static cudaEvent_t g_gev[2];
+
+static int graph_stream_init() {
+    if (g_gstream) return FT_OK;
+    if (cudaStreamCreateWithFlags(&g_gstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_gev[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_gev[1], cudaEventDisableTiming) != cudaSuccess) {
+        g_gstream = nullptr;
+        return FT_ERR_CUDA;
+    }
+    return FT_OK;
+}
+
+static cudaGraphExec_t graph_lookup(const GraphKey& k) {
+    for (auto& e : g_graphs)
+        if (e.used && e.key == k) return e.exec;
+    return nullptr;
+}
+
+static void graph_store(const GraphKey& k, cudaGraphExec_t exec) {
+    GraphEntry& e = g_graphs[g_graph_next];
+    g_graph_next = (g_graph_next + 1) % 8;
+    if (e.used) cudaGraphExecDestroy(e.exec);
+    e.key = k;
+    e.exec = exec;
+    e.used = true;
+}
+
 extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
                          ft_tiled* work_a, ft_tiled* work_b, ft_csc* phi_out, int32_t dtype,
                          const ft_params* params, int32_t max_steps, double tol,
@@ -1359,13 +1415,62 @@ extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* p
     cudaStream_t s = (cudaStream_t)stream;
     ft::Workspace ws = ft::carve_workspace(workspace, phi_in->n_cols);
     ft::evolve_reset_kernel<<<1, 1, 0, s>>>(ws.ctl);
-    for (int i = 0; i < max_steps; ++i) {
-        ft_tiled* out = (i & 1) ? work_b : work_a;
-        const ft_tiled* in_t = (i & 1) ? work_a : work_b;
-        rc = launch_step(lap_t, lap_flags, i == 0 ? phi_in : nullptr, i == 0 ? nullptr : in_t, out, dtype,
-                         params, workspace, ws_bytes, 1, s);
-        if (rc != FT_OK) return rc;
-        launch_finalize(ws, trace, out->capacity, 1, max_steps, tol, base_threshold, s);
+    // step 0: canonical input -> a
+    rc = launch_step(lap_t, lap_flags, phi_in, nullptr, work_a, dtype, params, workspace, ws_bytes, 1, s);
+    if (rc != FT_OK) return rc;
+    launch_finalize(ws, trace, work_a->capacity, 1, max_steps, tol, base_threshold, s);
+    const int rest = max_steps - 1;
+    if (rest > 0 && rest < kGraphSteps) {
+        for (int i = 1; i < max_steps; ++i) {
+            ft_tiled* out = (i & 1) ? work_b : work_a;
+            const ft_tiled* in_t = (i & 1) ? work_a : work_b;
+            rc = launch_step(lap_t, lap_flags, nullptr, in_t, out, dtype, params, workspace, ws_bytes, 1, s);
+            if (rc != FT_OK) return rc;
+            launch_finalize(ws, trace, out->capacity, 1, max_steps, tol, base_threshold, s);
+        }
+    } else if (rest > 0) {
+        GraphKey k;
+        memset(&k, 0, sizeof(k));
+        if (graph_stream_init() != FT_OK) return cuda_check("ft_evolve(graph stream)");
+        cudaStream_t gs = g_gstream;
+        const void* ptrs[12] = {lap_t->col_ptr, lap_t->row_idx, lap_t->values, work_a->desc, work_a->row_idx,
+                                work_a->values, work_b->desc, work_b->row_idx, work_b->values, workspace,
+                                trace, nullptr};
+        memcpy(k.ptrs, ptrs, sizeof(ptrs));
+        k.caps[0] = work_a->capacity; k.caps[1] = work_b->capacity; k.caps[2] = (long long)ws_bytes;
+        const double prm[8] = {params->w, params->a, params->e, params->e_base, params->mu, params->dt, tol,
+                               base_threshold};
+        memcpy(k.prm, prm, sizeof(prm));
+        const int ints[5] = {lap_flags, dtype, max_steps, phi_in->n_cols, phi_in->n_rows};
+        memcpy(k.ints, ints, sizeof(ints));
+        cudaGraphExec_t exec = graph_lookup(k);
+        if (!exec) {
+            cudaGraph_t graph;
+            if (cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+                return cuda_check("ft_evolve(begin capture)");
+            for (int i = 1; i <= kGraphSteps; ++i) {
+                ft_tiled* out = (i & 1) ? work_b : work_a;
+                const ft_tiled* in_t = (i & 1) ? work_a : work_b;
+                const int r2 = launch_step(lap_t, lap_flags, nullptr, in_t, out, dtype, params, workspace,
+                                           ws_bytes, 1, gs);
+                if (r2 != FT_OK) rc = r2;
+                launch_finalize(ws, trace, out->capacity, 1, max_steps, tol, base_threshold, gs);
+            }
+            const cudaError_t ec = cudaStreamEndCapture(gs, &graph);
+            if (ec != cudaSuccess || rc != FT_OK)
+                return rc != FT_OK ? rc : cuda_check("ft_evolve(end capture)");
+            if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+                cudaGraphDestroy(graph);
+                return cuda_check("ft_evolve(instantiate)");
+            }
+            cudaGraphDestroy(graph);
+            graph_store(k, exec);
+        }
+        cudaEventRecord(g_gev[0], s);
+        cudaStreamWaitEvent(gs, g_gev[0], 0);
+        for (int done = 0; done < rest; done += kGraphSteps) cudaGraphLaunch(exec, gs);
+        cudaEventRecord(g_gev[1], gs);
+        cudaStreamWaitEvent(s, g_gev[1], 0);
     }
     ft::evolve_report_kernel<<<1, 1, 0, s>>>(ws.ctl, (long long*)control);
     ft::CompactParams c;
