@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define FT_ABI_VERSION 2
+#define FT_ABI_VERSION 3
 
 /* return codes (mapped onto the reference's TessError subclasses,
  * `errors.py:9-75`, by the Python host layer) */
@@ -73,6 +73,8 @@ extern "C" {
 #define FT_STATUS_MAXSTEPS     5
 #define FT_STATUS_OUT_OVERFLOW 6   /* canonical output too small: grow it and
                                       call ft_compact                         */
+#define FT_STATUS_HALO_OVERFLOW 7  /* partitioned field: a halo column holds
+                                      more entries than the exchange slots    */
 
 /* CouplingParams (field.py:34-71).  Host memory. */
 typedef struct {
@@ -190,6 +192,75 @@ int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
               double tol, double base_threshold, void* workspace,
               size_t ws_bytes, ft_step_stats* trace, int64_t* control,
               void* stream);
+
+/* -- partitioned fields (one rank per GPU) ------------------------------- */
+/* A field of n_vertices columns split into contiguous owned column ranges,
+ * one per rank.  Every rank keeps two tiled buffers over ALL columns (global
+ * descriptors) in which its owned columns and its halo (the non-owned
+ * columns its owned L^T columns read) are valid; one Euler step is
+ *   ft_domain_step     owned columns -> out (entries [0, step_capacity))
+ *   ft_halo_pack       per peer: the owned columns the peer reads -> message
+ *   (all-gather of the per-rank records; ncclAllGather)
+ *   ft_domain_combine  global statistics + the evolve stop test, identical
+ *                      on every rank (fixed rank order)
+ *   (message exchange with the peers; ncclSend / ncclRecv)
+ *   ft_halo_unpack     per peer: message -> halo columns of out (entries
+ *                      from step_capacity on, `slots` per column)
+ * Every launch is a device-side no-op once the control block's done flag is
+ * set (converged / max steps / failure), so a host loop may enqueue steps
+ * ahead and read ft_domain_control only every few steps.  The owned columns
+ * are bitwise identical to the single-GPU ft_evolve.  Host reference:
+ * paper_1804_09152_b200/distributed.py (the reference is single-process). */
+typedef struct {
+    int32_t col_begin;       /* first owned column (global index)          */
+    int32_t col_count;       /* number of owned columns                    */
+    int64_t step_capacity;   /* entries the step may use in `out`          */
+} ft_domain;
+
+#define FT_HALO_FORCE 1      /* pack / unpack even when done is set         */
+
+/* One step of the owned columns (all tiers) plus the local statistics
+ * record.  lap_rows: the owned columns of L^T (n_rows = n_vertices, n_cols
+ * = col_count, global row indices).  workspace: ft_workspace_bytes(
+ * col_count).  `record` (device) receives the local ft_step_stats. */
+int ft_domain_step(const ft_csc* lap_rows, int32_t lap_flags, const ft_tiled* in,
+                   ft_tiled* out, int32_t dtype, const ft_params* params,
+                   const ft_domain* dom, void* workspace, size_t ws_bytes,
+                   ft_step_stats* record, void* stream);
+
+/* Size of a halo message for n columns: int32 counts[n], then int32
+ * rows[n*slots], then values[n*slots] (dtype). */
+int64_t ft_halo_bytes(int32_t n_cols, int32_t slots, int32_t dtype);
+
+/* Pack columns cols[0..n) (device int32) of `src` into `msg`.  Skipped when
+ * done is set or record->status is not OK (unless FT_HALO_FORCE).  A column
+ * with more than `slots` entries turns record->status into
+ * FT_STATUS_HALO_OVERFLOW and raises *need (device int32) to its count. */
+int ft_halo_pack(const ft_tiled* src, const int32_t* cols, int32_t n, int32_t slots,
+                 int32_t dtype, void* msg, ft_step_stats* record, int32_t* need,
+                 void* workspace, int32_t flags, void* stream);
+
+/* Column cols[i] of `dst` <- message entry i, stored at entries
+ * [region + i*slots, region + i*slots + count).  Skipped when done is set
+ * (unless FT_HALO_FORCE). */
+int ft_halo_unpack(ft_tiled* dst, const int32_t* cols, int32_t n, int32_t slots,
+                   int32_t dtype, const void* msg, int64_t region, void* workspace,
+                   int32_t flags, void* stream);
+
+/* Global record from the all-gathered per-rank records (device, `world`
+ * records in rank order): max of max_delta, base_mass summed in rank
+ * order, nnz sums, the failure of the lowest rank by priority pattern >
+ * NaN > overflow > halo overflow.  Applies the stop test of ft_evolve
+ * (field.py:316-317) and writes trace[steps_done]; `needed` is the local
+ * rank's. */
+int ft_domain_combine(const ft_step_stats* records, int32_t world, int32_t rank,
+                      int32_t max_steps, double tol, double base_threshold,
+                      void* workspace, ft_step_stats* trace, void* stream);
+
+/* Control block: out (device int64[3]) <- {steps_done, status, needed};
+ * with set_steps >= 0 first resets it to steps_done = set_steps, not done,
+ * status OK (rewind after a capacity failure). */
+int ft_domain_control(void* workspace, int32_t set_steps, int64_t* out, void* stream);
 
 /* -- labels -------------------------------------------------------------- */
 /* Per-vertex argmax cell id; ties -> lowest cell; the base row wins only

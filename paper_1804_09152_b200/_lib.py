@@ -32,8 +32,11 @@ FT_STATUS_OVERFLOW = 3
 FT_STATUS_CONVERGED = 4
 FT_STATUS_MAXSTEPS = 5
 FT_STATUS_OUT_OVERFLOW = 6
+FT_STATUS_HALO_OVERFLOW = 7
 
-ABI_VERSION = 2
+FT_HALO_FORCE = 1
+
+ABI_VERSION = 3
 
 
 class FtParams(ctypes.Structure):
@@ -52,6 +55,11 @@ class FtTiled(ctypes.Structure):
     _fields_ = [("n_rows", ctypes.c_int32), ("n_cols", ctypes.c_int32),
                 ("desc", ctypes.c_void_p), ("row_idx", ctypes.c_void_p),
                 ("values", ctypes.c_void_p), ("capacity", ctypes.c_int64)]
+
+
+class FtDomain(ctypes.Structure):
+    _fields_ = [("col_begin", ctypes.c_int32), ("col_count", ctypes.c_int32),
+                ("step_capacity", ctypes.c_int64)]
 
 
 class FtStepStats(ctypes.Structure):
@@ -82,7 +90,8 @@ EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
            "ft_workspace_init", "ft_tile_slot_entries", "ft_tiled_min_capacity",
            "ft_step", "ft_step_kernel", "ft_step_fixup", "ft_step_finalize", "ft_compact",
            "ft_evolve", "ft_labels", "ft_faces_by_cell", "ft_lloyd_centroids",
-           "ft_dual_products")
+           "ft_dual_products", "ft_domain_step", "ft_halo_bytes", "ft_halo_pack",
+           "ft_halo_unpack", "ft_domain_combine", "ft_domain_control")
 
 _lib = None
 
@@ -134,6 +143,21 @@ def _declare(lib):
     lib.ft_dual_products.argtypes = [P(FtCsc), i32, vp, vp, ctypes.c_double, vp, vp, vp, vp,
                                      ctypes.c_int64, vp, vp]
     lib.ft_dual_products.restype = ctypes.c_int
+    lib.ft_domain_step.argtypes = [P(FtCsc), i32, P(FtTiled), P(FtTiled), i32, P(FtParams),
+                                   P(FtDomain), vp, ctypes.c_size_t, vp, vp]
+    lib.ft_domain_step.restype = ctypes.c_int
+    lib.ft_halo_bytes.argtypes = [i32, i32, i32]
+    lib.ft_halo_bytes.restype = ctypes.c_int64
+    lib.ft_halo_pack.argtypes = [P(FtTiled), vp, i32, i32, i32, vp, vp, vp, vp, i32, vp]
+    lib.ft_halo_pack.restype = ctypes.c_int
+    lib.ft_halo_unpack.argtypes = [P(FtTiled), vp, i32, i32, i32, vp, ctypes.c_int64, vp, i32,
+                                   vp]
+    lib.ft_halo_unpack.restype = ctypes.c_int
+    lib.ft_domain_combine.argtypes = [vp, i32, i32, i32, ctypes.c_double, ctypes.c_double, vp,
+                                      vp, vp]
+    lib.ft_domain_combine.restype = ctypes.c_int
+    lib.ft_domain_control.argtypes = [vp, i32, vp, vp]
+    lib.ft_domain_control.restype = ctypes.c_int
 
 
 def lib():

@@ -44,7 +44,8 @@ namespace ft {
 __constant__ double c_recip[33];
 
 struct StepParams {
-    int n_v;
+    int n_v;             // owned columns (the whole field outside domain mode)
+    int j_base;          // global index of the first owned column
     int num_tiles;
     const int* __restrict__ lap_ptr;
     const int* __restrict__ lap_idx;
@@ -143,8 +144,8 @@ template <typename T, int K, bool UNIFORM, bool IN_CANON>
 __device__ __forceinline__ void gather(Win<K>& w, int j, int lo, const StepParams& p) {
     w.m = 0;
     w.more = false;
-    const int q0 = __ldg(&p.lap_ptr[j]);
-    const int q1 = __ldg(&p.lap_ptr[j + 1]);
+    const int q0 = __ldg(&p.lap_ptr[j - p.j_base]);   // L rows are local to the domain
+    const int q1 = __ldg(&p.lap_ptr[j - p.j_base + 1]);
     const double invdeg = UNIFORM ? 1.0 / (double)(q1 - q0 - 1) : 0.0;
     for (int q = q0; q < q1; ++q) {
         const int u = __ldg(&p.lap_idx[q]);
@@ -558,14 +559,15 @@ __global__ void __launch_bounds__(FT_TPB, 6) step_kernel(const StepParams p) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tile = blockIdx.x;
-    const int j = tile * FT_TPB + tid;
-    const bool active = j < p.n_v;
+    const int jl = tile * FT_TPB + tid;   // local column
+    const int j = p.j_base + jl;          // global column
+    const bool active = jl < p.n_v;
 
     int n = 0, q0 = 0;
     bool wide = false;
     if (active) {
-        q0 = __ldg(&p.lap_ptr[j]);
-        n = __ldg(&p.lap_ptr[j + 1]) - q0;
+        q0 = __ldg(&p.lap_ptr[jl]);
+        n = __ldg(&p.lap_ptr[jl + 1]) - q0;
         if (n > kMD || n < 1) { wide = true; n = 0; }
     }
     int u[kMD];
@@ -671,8 +673,8 @@ __global__ void __launch_bounds__(FT_TPB, 6) step_kernel(const StepParams p) {
 // caller then uses vertex_slow).
 template <typename T, int K, bool UNIFORM, bool IN_CANON>
 __device__ __forceinline__ bool gather_wide(int j, const StepParams& p, Win<K>& w) {
-    const int q0 = __ldg(&p.lap_ptr[j]);
-    const int n = __ldg(&p.lap_ptr[j + 1]) - q0;
+    const int q0 = __ldg(&p.lap_ptr[j - p.j_base]);
+    const int n = __ldg(&p.lap_ptr[j - p.j_base + 1]) - q0;
     if (n > kMD || n < 1) return false;
     int u[kMD];
 #pragma unroll
@@ -786,14 +788,16 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p) {
             int qb = 0;
             if (lane == 0) qb = atomicAdd(&p.ws.ctl->deep_count, __popc(db));
             qb = __shfl_sync(0xffffffffu, qb, 0);
-            if (deep) p.ws.slow_list[p.n_v + qb + __popc(db & ((1u << lane) - 1u))] = j;
-            vres_init(res);
+            if (deep) {
+                p.ws.slow_list[p.n_v + qb + __popc(db & ((1u << lane) - 1u))] = j;
+                vres_init(res);    // only the columns handed to tier 3
+            }
         }
         bool fits;
         int excl;
         const long long base = pool_place<T, KW>(deep ? 0 : res.cnt, res, p, lane, fits, excl);
         if (mine && !deep) {
-            p.ws.vbm[j] = res.bm;
+            p.ws.vbm[j - p.j_base] = res.bm;
             if (fits) {
                 const long long off = base + excl;
                 p.out_desc[j] = make_int2((int)off, res.cnt);
@@ -825,7 +829,7 @@ __global__ void __launch_bounds__(FT_TPB) deep_kernel(const StepParams p) {
         int excl;
         const long long base = pool_place<T, 8>(res.cnt, res, p, lane, fits, excl);
         if (mine) {
-            p.ws.vbm[j] = res.bm;
+            p.ws.vbm[j - p.j_base] = res.bm;
             if (fits) {
                 const long long off = base + excl;
                 p.out_desc[j] = make_int2((int)off, res.cnt);
@@ -1181,10 +1185,10 @@ extern "C" int64_t ft_tiled_min_capacity(int32_t n_vertices) {
     return (int64_t)ft::num_tiles_for(n_vertices < 0 ? 0 : n_vertices) * FT_SLOT;
 }
 
-static int check_tiled(const ft_tiled* t, int n_rows, int n_cols) {
+static int check_tiled(const ft_tiled* t, int n_rows, int n_cols, int n_own) {
     if (!t || !t->desc || !t->row_idx || !t->values) return set_err(FT_ERR_ARG, "null tiled buffer");
     if (t->n_rows != n_rows || t->n_cols != n_cols) return set_err(FT_ERR_SHAPE, "tiled buffer has wrong shape");
-    if (t->capacity < ft_tiled_min_capacity(n_cols) || t->capacity > (int64_t)INT_MAX)
+    if (t->capacity < ft_tiled_min_capacity(n_own) || t->capacity > (int64_t)INT_MAX)
         return set_err(FT_ERR_ARG, "tiled capacity out of range");
     if (((uintptr_t)t->desc) & 7) return set_err(FT_ERR_ARG, "tiled desc must be 8-byte aligned");
     return FT_OK;
@@ -1210,24 +1214,35 @@ static int window_size() {
 }
 
 // which = 1: fused kernel, 2: fixup kernel, 3: both
+// dom == nullptr: the whole field; otherwise the owned column range of a
+// partitioned field (lap_t then holds the owned columns of L^T only and the
+// workspace is sized for the owned columns)
 static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_canon,
                        const ft_tiled* in_tiled, ft_tiled* out, int32_t dtype,
                        const ft_params* prm, void* workspace, size_t ws_bytes, int check_done,
-                       cudaStream_t s, int which = 3) {
+                       cudaStream_t s, int which = 3, const ft_domain* dom = nullptr) {
     if (!lap_t || !out || !prm || !workspace) return set_err(FT_ERR_ARG, "null argument");
     if (dtype != FT_F64 && dtype != FT_F32) return set_err(FT_ERR_ARG, "bad dtype");
     const int n_rows = in_canon ? in_canon->n_rows : (in_tiled ? in_tiled->n_rows : -1);
     const int n_v = in_canon ? in_canon->n_cols : (in_tiled ? in_tiled->n_cols : -1);
     if (n_v < 0) return set_err(FT_ERR_ARG, "no input");
-    if (lap_t->n_rows != lap_t->n_cols) return set_err(FT_ERR_SHAPE, "Laplacian must be square");
-    if (lap_t->n_cols != n_v) return set_err(FT_ERR_SHAPE, "Laplacian size does not match field");
     if (n_v == 0) return set_err(FT_ERR_SHAPE, "empty field");
-    int rc = check_tiled(out, n_rows, n_v);
+    const int j_base = dom ? dom->col_begin : 0;
+    const int n_own = dom ? dom->col_count : n_v;
+    if (dom && (j_base < 0 || n_own < 1 || (long long)j_base + n_own > n_v))
+        return set_err(FT_ERR_SHAPE, "domain outside the field");
+    if (lap_t->n_rows != n_v || lap_t->n_cols != n_own)
+        return set_err(FT_ERR_SHAPE, "Laplacian size does not match field");
+    int rc = check_tiled(out, n_rows, n_v, dom ? n_own : n_v);
     if (rc != FT_OK) return rc;
-    if (ws_bytes < ft::workspace_bytes(n_v)) return set_err(FT_ERR_ARG, "workspace too small");
+    const long long step_cap = dom ? dom->step_capacity : out->capacity;
+    if (step_cap < ft_tiled_min_capacity(n_own) || step_cap > out->capacity)
+        return set_err(FT_ERR_ARG, "domain step capacity out of range");
+    if (ws_bytes < ft::workspace_bytes(n_own)) return set_err(FT_ERR_ARG, "workspace too small");
     ft::StepParams p;
-    p.n_v = n_v;
-    p.num_tiles = ft::num_tiles_for(n_v);
+    p.n_v = n_own;
+    p.j_base = j_base;
+    p.num_tiles = ft::num_tiles_for(n_own);
     p.lap_ptr = lap_t->col_ptr;
     p.lap_idx = lap_t->row_idx;
     p.lap_val = lap_t->values;
@@ -1238,9 +1253,9 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_
     p.out_desc = (int2*)out->desc;
     p.out_idx = out->row_idx;
     p.out_val = out->values;
-    p.cap = out->capacity;
+    p.cap = step_cap;
     p.w = prm->w; p.a = prm->a; p.e = prm->e; p.eb = prm->e_base; p.mu = prm->mu; p.dt = prm->dt;
-    p.ws = ft::carve_workspace(workspace, n_v);
+    p.ws = ft::carve_workspace(workspace, n_own);
     p.check_done = check_done;
     p.finite = std::isfinite(p.w) && std::isfinite(p.a) && std::isfinite(p.e) && std::isfinite(p.eb) &&
                std::isfinite(p.mu) && std::isfinite(p.dt);
@@ -1409,7 +1424,7 @@ extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* p
     if (max_steps < 1) return set_err(FT_ERR_SHAPE, "max_steps must be >= 1");
     if (phi_out->n_cols != phi_in->n_cols || phi_out->n_rows != phi_in->n_rows)
         return set_err(FT_ERR_SHAPE, "output buffer has wrong shape");
-    int rc = check_tiled(work_b, phi_in->n_rows, phi_in->n_cols);
+    int rc = check_tiled(work_b, phi_in->n_rows, phi_in->n_cols, phi_in->n_cols);
     if (rc != FT_OK) return rc;
     if (ws_bytes < ft::workspace_bytes(phi_in->n_cols)) return set_err(FT_ERR_ARG, "workspace too small");
     cudaStream_t s = (cudaStream_t)stream;
@@ -1477,4 +1492,22 @@ extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* p
     fill_compact(c, work_a, work_b, -1, phi_out, workspace);
     c.control = (long long*)control;
     return launch_compact(c, dtype, s);
+}
+
+// ---------------------------------------------------------------------------
+// partitioned field: one step of the owned columns (the halo kernels and the
+// combine live in ft_domain.cu)
+
+extern "C" int ft_domain_step(const ft_csc* lap_rows, int32_t lap_flags, const ft_tiled* in,
+                              ft_tiled* out, int32_t dtype, const ft_params* params,
+                              const ft_domain* dom, void* workspace, size_t ws_bytes,
+                              ft_step_stats* record, void* stream) {
+    if (!in || !dom || !record) return set_err(FT_ERR_ARG, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int rc = launch_step(lap_rows, lap_flags, nullptr, in, out, dtype, params, workspace, ws_bytes, 1, s,
+                               3, dom);
+    if (rc != FT_OK) return rc;
+    launch_finalize(ft::carve_workspace(workspace, dom->col_count), record, dom->step_capacity, 0, 1, 0.0, 0.0,
+                    s);
+    return cuda_check("ft_domain_step");
 }

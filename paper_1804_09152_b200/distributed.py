@@ -1,0 +1,601 @@
+"""Partitioned fields: one rank per GPU, vertex row-partition + halo exchange.
+
+The reference evolves one field in one process (pkg/src/fieldtess/field.py:
+289-321).  Column j of a new field reads only the columns u of L^T(:, j)
+(its one-ring, _kernels.py:14-74), so a field whose vertices are split into
+contiguous owned ranges steps independently per range given the one-ring
+halo of the range.  Per Euler step every rank runs
+
+    ft_domain_step      its owned columns (the single-GPU kernels, unchanged)
+    ft_halo_pack        the owned columns each peer reads -> one message/peer
+    all-gather          the per-rank statistics records (NCCL)
+    ft_domain_combine   global max |delta|, base mass, stop test (fixed order)
+    send / recv         the halo messages (NCCL over NVLink)
+    ft_halo_unpack      the peers' messages -> the halo columns
+
+with no host synchronisation: the stop test runs on every GPU from the
+same gathered records, so the ranks stop at the same step, and the host only
+reads the control block every ``sync_every`` steps.  The owned columns are
+bitwise identical to the single-GPU :func:`field.evolve`; the global base
+mass is summed in rank order (rounding may differ from the one-GPU
+reduction tree at the 1e-16 relative level).
+
+Two transports share one driver: :class:`TorchTransport` (torch.distributed;
+NCCL for CUDA tensors, gloo for CPU tensors) for one rank per process, and
+:class:`LoopbackTransport` for several ranks of one process on one device
+(sequential, no rank waits for another inside a kernel), used by the tests.
+"""
+
+import ctypes
+import time
+
+import numpy as np
+
+from . import _lib
+from .errors import BackendError, ShapeError
+from .field import (BASE_EXHAUSTION_PER_VERTEX, POOL_FRACTION, POOL_MIN, StepStats, _check,
+                    _ft_dtype, _raise_step_error, _stats_from_bytes, _stream_handle,
+                    _value_dtype)
+from .sparse import INDEX, GROWTH, DeviceCSC, DeviceTiled, SparseMat
+
+DEFAULT_SLOTS = 7      # halo message entries per column (grows on demand)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+# ---------------------------------------------------------------------------
+# partition and halo plan (host)
+
+
+class Partition:
+    """Contiguous owned vertex ranges: rank r owns [bounds[r], bounds[r+1])."""
+
+    def __init__(self, bounds):
+        b = np.asarray(bounds, dtype=np.int64)
+        if b.ndim != 1 or b.size < 2 or b[0] != 0 or np.any(np.diff(b) < 1):
+            raise ShapeError("partition bounds must start at 0 and increase strictly")
+        self.bounds = b
+
+    @classmethod
+    def even(cls, n_vertices, world, align=1):
+        """Near-equal ranges, boundaries rounded to multiples of ``align``
+        (e.g. a grid row, so the halo is whole rows)."""
+        if world < 1 or n_vertices < world:
+            raise ShapeError("need 1 <= world <= n_vertices")
+        units = -(-n_vertices // align)
+        cuts = [min(n_vertices, (units * r // world) * align) for r in range(world + 1)]
+        cuts[-1] = n_vertices
+        return cls(cuts)
+
+    @property
+    def world(self):
+        return self.bounds.size - 1
+
+    @property
+    def n_vertices(self):
+        return int(self.bounds[-1])
+
+    def range(self, rank):
+        return int(self.bounds[rank]), int(self.bounds[rank + 1])
+
+    def owner(self, cols):
+        return np.searchsorted(self.bounds, np.asarray(cols), side="right") - 1
+
+
+class HaloPlan:
+    """Which columns a rank receives from / sends to each peer.
+
+    ``recv[q]``: sorted global columns owned by q that this rank's owned L^T
+    columns read; ``send[q]``: this rank's owned columns q reads."""
+
+    def __init__(self, rank, partition, recv, send):
+        self.rank = rank
+        self.partition = partition
+        self.recv = {int(q): np.asarray(v, dtype=np.int32) for q, v in recv.items() if len(v)}
+        self.send = {int(q): np.asarray(v, dtype=np.int32) for q, v in send.items() if len(v)}
+
+    @staticmethod
+    def needed(rank, partition, lap_idx):
+        """recv lists from the owned L^T columns' row indices."""
+        b, e = partition.range(rank)
+        need = np.unique(np.asarray(lap_idx, dtype=np.int64))
+        halo = need[(need < b) | (need >= e)]
+        own = partition.owner(halo)
+        return {int(q): halo[own == q] for q in np.unique(own)}
+
+    @property
+    def halo_cols(self):
+        return int(sum(v.size for v in self.recv.values()))
+
+    @property
+    def peers(self):
+        return sorted(set(self.recv) | set(self.send))
+
+
+def build_plans(problems, transport):
+    """Halo plans of the local ranks (a host collective over all ranks)."""
+    recvs = [HaloPlan.needed(p.rank, p.partition, p.lap_idx) for p in problems]
+    sends = transport.exchange_lists(recvs)
+    return [HaloPlan(p.rank, p.partition, r, s) for p, r, s in zip(problems, recvs, sends)]
+
+
+class LocalProblem:
+    """What one rank holds: the owned columns of L^T (CSC with global row
+    indices, n_rows = n_vertices) and the initial field on its owned + halo
+    columns (``cols`` sorted, CSC-like ``col_ptr`` / ``row_idx`` /
+    ``values`` over them)."""
+
+    def __init__(self, rank, partition, n_rows, lap_ptr, lap_idx, lap_val, lap_flags, cols,
+                 col_ptr, row_idx, values):
+        self.rank = rank
+        self.partition = partition
+        self.n_rows = int(n_rows)
+        self.lap_ptr = np.ascontiguousarray(lap_ptr, dtype=INDEX)
+        self.lap_idx = np.ascontiguousarray(lap_idx, dtype=INDEX)
+        self.lap_val = np.ascontiguousarray(lap_val, dtype=np.float64)
+        self.lap_flags = int(lap_flags)
+        self.cols = np.ascontiguousarray(cols, dtype=np.int64)
+        self.col_ptr = np.ascontiguousarray(col_ptr, dtype=np.int64)
+        self.row_idx = np.ascontiguousarray(row_idx, dtype=INDEX)
+        self.values = np.ascontiguousarray(values, dtype=np.float64)
+        b, e = partition.range(rank)
+        if self.lap_ptr.size != e - b + 1:
+            raise ShapeError("L^T columns do not match the owned range")
+
+
+def local_problem(field_phi, lap, partition, rank):
+    """Slice a host field (SparseMat) and a Laplacian for one rank."""
+    from .field import _uniform_values_exact, _with_diagonal
+    mat_t = _with_diagonal(lap.mat_t)
+    flags = _lib.FT_LAP_UNIFORM if _uniform_values_exact(mat_t) else _lib.FT_LAP_EXPLICIT
+    b, e = partition.range(rank)
+    cp = np.asarray(mat_t.col_ptr, dtype=np.int64)
+    q0, q1 = int(cp[b]), int(cp[e])
+    lap_ptr = cp[b:e + 1] - q0
+    lap_idx = np.asarray(mat_t.row_idx[q0:q1])
+    lap_val = np.asarray(mat_t.values[q0:q1], dtype=np.float64)
+    need = np.unique(lap_idx.astype(np.int64))
+    cols = np.union1d(np.arange(b, e, dtype=np.int64), need)
+    fcp = np.asarray(field_phi.col_ptr, dtype=np.int64)
+    cnt = fcp[cols + 1] - fcp[cols]
+    col_ptr = np.zeros(cols.size + 1, dtype=np.int64)
+    np.cumsum(cnt, out=col_ptr[1:])
+    src = np.repeat(fcp[cols], cnt) + (np.arange(int(col_ptr[-1])) - np.repeat(col_ptr[:-1], cnt))
+    return LocalProblem(rank, partition, field_phi.n_rows, lap_ptr, lap_idx, lap_val, flags, cols,
+                        col_ptr, np.asarray(field_phi.row_idx)[src],
+                        np.asarray(field_phi.values, dtype=np.float64)[src])
+
+
+# torus stencil of gen_periodic_grid (vertex (i, j) -> j*nx + i; faces
+# (v00, v10, v01), (v10, v11, v01)): the one-ring of (i, j)
+_GRID_RING = ((1, 0), (-1, 0), (0, 1), (0, -1), (1, -1), (-1, 1))
+
+
+def _grid_ring(v, nx, ny):
+    i, j = v % nx, v // nx
+    return np.stack([((j + dj) % ny) * nx + (i + di) % nx for di, dj in _GRID_RING], axis=1)
+
+
+def periodic_grid_problem(nx, ny, seeds, partition, rank):
+    """The rank-local problem of ``init_field(gen_periodic_grid(nx, ny),
+    seeds)`` with the uniform Laplacian, built from the lattice stencil
+    without the global mesh (weak-scaling runs whose global mesh does not
+    fit one host process).  Identical to :func:`local_problem` on the
+    globally built objects (tests/test_distributed.py)."""
+    b, e = partition.range(rank)
+    n_v = nx * ny
+    if partition.n_vertices != n_v:
+        raise ShapeError("partition does not cover the grid")
+    own = np.arange(b, e, dtype=np.int64)
+    ring = _grid_ring(own, nx, ny)
+    lt = np.sort(np.concatenate([own[:, None], ring], axis=1), axis=1)
+    deg = 6
+    lap_idx = lt.reshape(-1)
+    lap_val = np.where(lt == own[:, None], -1.0, 1.0 / deg).reshape(-1)
+    lap_ptr = np.arange(0, 7 * own.size + 1, 7, dtype=np.int64)
+    need = np.unique(lap_idx)
+    cols = np.union1d(own, need)
+    # seeds claim themselves and their one-ring (field.py:137-166): rows =
+    # seed position + 1, 1/k for a vertex claimed k times
+    seeds = np.asarray(seeds, dtype=np.int64).ravel()
+    if seeds.size != np.unique(seeds).size:
+        from .errors import DuplicateSeedError
+        raise DuplicateSeedError("duplicate-seed: seed list has repeats")
+    cl_col = np.concatenate([seeds[:, None], _grid_ring(seeds, nx, ny)], axis=1).reshape(-1)
+    cl_row = np.repeat(np.arange(1, seeds.size + 1, dtype=np.int64), 7)
+    pos = np.searchsorted(cols, cl_col)
+    keep = (pos < cols.size) & (cols[np.minimum(pos, cols.size - 1)] == cl_col)
+    cl_col, cl_row, pos = cl_col[keep], cl_row[keep], pos[keep]
+    claims = np.bincount(pos, minlength=cols.size)
+    per = np.where(claims == 0, 1, claims)
+    col_ptr = np.zeros(cols.size + 1, dtype=np.int64)
+    np.cumsum(per, out=col_ptr[1:])
+    row_idx = np.zeros(int(col_ptr[-1]), dtype=INDEX)
+    vals = np.ones(int(col_ptr[-1]))
+    order = np.lexsort((cl_row, pos))
+    sp, sr = pos[order], cl_row[order]
+    first = np.searchsorted(sp, sp, side="left")
+    dst = col_ptr[sp] + (np.arange(sp.size) - first)
+    row_idx[dst] = sr
+    vals[dst] = 1.0 / claims[sp]
+    return LocalProblem(rank, partition, seeds.size + 1, lap_ptr, lap_idx, lap_val,
+                        _lib.FT_LAP_UNIFORM, cols, col_ptr, row_idx, vals)
+
+
+# ---------------------------------------------------------------------------
+# transports
+
+
+class TorchTransport:
+    """One rank per process over torch.distributed (NCCL for CUDA tensors,
+    gloo for CPU tensors).  ``ranks`` is always this process's single rank."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+
+    def exchange_lists(self, recvs):
+        (recv,) = recvs
+        allr = [None] * self.world
+        self.dist.all_gather_object(allr, {q: v for q, v in recv.items()}, group=self.group)
+        return [{q: allr[q][self.rank] for q in range(self.world)
+                 if q != self.rank and self.rank in allr[q]}]
+
+    def all_gather(self, ranks):
+        (r,) = ranks
+        if self.nccl:
+            self.dist.all_gather_into_tensor(r.gathered, r.record, group=self.group)
+        else:
+            self.dist.all_gather(list(r.gathered.chunk(self.world)), r.record, group=self.group)
+
+    def exchange(self, ranks):
+        (r,) = ranks
+        d = self.dist
+        ops = []
+        for q in r.plan.peers:
+            if q in r.plan.send:
+                ops.append(d.P2POp(d.isend, r.send_msg[q], q, group=self.group))
+            if q in r.plan.recv:
+                ops.append(d.P2POp(d.irecv, r.recv_msg[q], q, group=self.group))
+        if ops:
+            for req in d.batch_isend_irecv(ops):
+                req.wait()
+
+    def max_int(self, values):
+        torch = _torch()
+        (v,) = values
+        dev = "cuda" if self.nccl else "cpu"
+        t = torch.tensor([int(v)], dtype=torch.int64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return int(t.item())
+
+
+class LoopbackTransport:
+    """All ranks live in this process (one device): collectives are copies.
+    The ranks' kernels run one after another; none waits on another."""
+
+    def exchange_lists(self, recvs):
+        sends = [dict() for _ in recvs]
+        for r, recv in enumerate(recvs):
+            for q, cols in recv.items():
+                sends[q][r] = cols
+        return sends
+
+    def all_gather(self, ranks):
+        torch = _torch()
+        cat = torch.cat([r.record for r in ranks])
+        for r in ranks:
+            r.gathered.copy_(cat)
+
+    def exchange(self, ranks):
+        for r in ranks:
+            for q in r.plan.recv:
+                r.recv_msg[q].copy_(ranks[q].send_msg[r.rank])
+
+    def max_int(self, values):
+        return max(int(v) for v in values)
+
+
+# ---------------------------------------------------------------------------
+# one rank's device state
+
+
+class DomainRank:
+    """Device state of one rank: owned L^T columns, two tiled buffers over
+    all columns (owned + halo valid), workspace, records, halo messages."""
+
+    def __init__(self, problem, plan, precision="exact", slots=DEFAULT_SLOTS, device=None):
+        torch = _torch()
+        if device is None:
+            if not torch.cuda.is_available():
+                raise BackendError("no CUDA device: the engine has no CPU fallback")
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = device
+        self.lib = _lib.lib()
+        self.rank = problem.rank
+        self.partition = problem.partition
+        self.world = problem.partition.world
+        self.plan = plan
+        self.precision = precision
+        self.ftd = _ft_dtype(precision)
+        self.vdtype = _value_dtype(precision)
+        self.n_rows = problem.n_rows
+        self.n_v = problem.partition.n_vertices
+        self.col_begin, e = problem.partition.range(problem.rank)
+        self.n_own = e - self.col_begin
+        lap = SparseMat(self.n_v, self.n_own, problem.lap_ptr, problem.lap_idx, problem.lap_val,
+                        check=False)
+        self.lap = DeviceCSC.from_host(lap, self.vdtype, device)
+        self.lap_c = self.lap.ft_csc()
+        self.lap_flags = problem.lap_flags
+        self.ws = torch.zeros(int(self.lib.ft_workspace_bytes(self.n_own)), dtype=torch.int8,
+                              device=device)
+        self.record = torch.zeros(_lib.STATS_BYTES, dtype=torch.uint8, device=device)
+        self.gathered = torch.zeros(self.world * _lib.STATS_BYTES, dtype=torch.uint8, device=device)
+        self.need = torch.zeros(1, dtype=torch.int32, device=device)
+        self.ctl_out = torch.zeros(3, dtype=torch.int64, device=device)
+        self.trace = None
+        # halo layout: peers ascending, columns of a peer consecutive
+        self.recv_cols = {q: torch.from_numpy(v).to(device) for q, v in plan.recv.items()}
+        self.send_cols = {q: torch.from_numpy(v).to(device) for q, v in plan.send.items()}
+        self.recv_off = {}
+        off = 0
+        for q in sorted(plan.recv):
+            self.recv_off[q] = off
+            off += plan.recv[q].size
+        self.n_halo = off
+        own_mask = (problem.cols >= self.col_begin) & (problem.cols < e)
+        own_nnz = int(np.sum(np.diff(problem.col_ptr)[own_mask]))
+        self.step_cap = int(self.lib.ft_tiled_min_capacity(self.n_own)) + max(
+            int(own_nnz * POOL_FRACTION), POOL_MIN)
+        self.slots = int(slots)
+        self.bufs = [None, None]
+        self.meta = [None, None]       # (ft_tiled struct, step_capacity, slots) per buffer
+        self._alloc_messages()
+        self._upload(problem)
+        self.reallocs = 0
+
+    # -- buffers -------------------------------------------------------------
+
+    def _alloc_messages(self):
+        torch = _torch()
+        hb = self.lib.ft_halo_bytes
+        self.send_msg = {q: torch.zeros(int(hb(v.size, self.slots, self.ftd)), dtype=torch.uint8,
+                                        device=self.device) for q, v in self.plan.send.items()}
+        self.recv_msg = {q: torch.zeros(int(hb(v.size, self.slots, self.ftd)), dtype=torch.uint8,
+                                        device=self.device) for q, v in self.plan.recv.items()}
+
+    def _need_capacity(self):
+        return self.step_cap + self.n_halo * self.slots
+
+    def _buffer(self, k, capacity):
+        """Buffer k with at least ``capacity`` entries.  A grown buffer keeps
+        its contents: launches enqueued after a failed step (device no-ops)
+        may grow the buffer that holds the state the host rewinds to."""
+        buf = self.bufs[k]
+        if buf is None or buf.capacity < capacity:
+            old = buf
+            if old is not None:
+                self.reallocs += 1
+                capacity = max(capacity, int(old.capacity * GROWTH))
+            buf = DeviceTiled(self.n_rows, self.n_v, capacity, self.vdtype, self.device)
+            if old is not None:
+                buf.desc.copy_(old.desc)
+                buf.row_idx[:old.capacity].copy_(old.row_idx)
+                buf.values[:old.capacity].copy_(old.values)
+            self.bufs[k] = buf
+        return buf
+
+    def _upload(self, problem):
+        torch = _torch()
+        nnz = int(problem.col_ptr[-1])
+        buf = self._buffer(0, max(self._need_capacity(), nnz, 1))
+        cols = torch.from_numpy(problem.cols).to(self.device)
+        desc = buf.desc.view(-1, 2)
+        starts = torch.from_numpy(problem.col_ptr[:-1].astype(np.int32)).to(self.device)
+        counts = torch.from_numpy(np.diff(problem.col_ptr).astype(np.int32)).to(self.device)
+        desc[cols, 0] = starts
+        desc[cols, 1] = counts
+        if nnz:
+            buf.row_idx[:nnz].copy_(torch.from_numpy(problem.row_idx[:nnz]).to(self.device))
+            buf.values[:nnz].copy_(torch.from_numpy(problem.values[:nnz]).to(self.device,
+                                                                               self.vdtype))
+        self.meta[0] = (buf.ft_tiled(), 0, self.slots)
+        self._buffer(1, self._need_capacity())
+        self.meta[1] = None
+
+    def _as_output(self, k):
+        """Buffer k about to receive a step: large enough for the current step
+        capacity and halo slots (contents discarded when reallocated)."""
+        buf = self._buffer(k, self._need_capacity())
+        self.meta[k] = (buf.ft_tiled(), self.step_cap, self.slots)
+        return self.meta[k]
+
+    # -- the per-step launches (all asynchronous) ----------------------------
+
+    def begin(self, max_steps, steps_done=0):
+        torch = _torch()
+        if self.trace is None or self.trace.numel() < max_steps * _lib.STATS_BYTES:
+            self.trace = torch.zeros(max_steps * _lib.STATS_BYTES, dtype=torch.uint8,
+                                     device=self.device)
+        self.set_control(steps_done)
+
+    def launch_step(self, i, prm, stream):
+        lib = self.lib
+        in_t = self.meta[i % 2][0]
+        out_t, step_cap, slots = self._as_output((i + 1) % 2)
+        dom = _lib.FtDomain(self.col_begin, self.n_own, step_cap)
+        wp, wn = ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel()
+        rec = ctypes.c_void_p(self.record.data_ptr())
+        _check(lib.ft_domain_step(ctypes.byref(self.lap_c), self.lap_flags, ctypes.byref(in_t),
+                                  ctypes.byref(out_t), self.ftd, ctypes.byref(prm),
+                                  ctypes.byref(dom), wp, wn, rec, stream), "ft_domain_step")
+        for q, cols in self.send_cols.items():
+            _check(lib.ft_halo_pack(ctypes.byref(out_t), ctypes.c_void_p(cols.data_ptr()),
+                                    cols.numel(), slots, self.ftd,
+                                    ctypes.c_void_p(self.send_msg[q].data_ptr()), rec,
+                                    ctypes.c_void_p(self.need.data_ptr()), wp, 0, stream),
+                   "ft_halo_pack")
+
+    def launch_combine(self, max_steps, tol, base_threshold, stream):
+        _check(self.lib.ft_domain_combine(ctypes.c_void_p(self.gathered.data_ptr()), self.world,
+                                          self.rank, max_steps, float(tol), float(base_threshold),
+                                          ctypes.c_void_p(self.ws.data_ptr()),
+                                          ctypes.c_void_p(self.trace.data_ptr()), stream),
+               "ft_domain_combine")
+
+    def launch_unpack(self, i, stream, flags=0):
+        out_t, step_cap, slots = self.meta[(i + 1) % 2]
+        for q, cols in self.recv_cols.items():
+            _check(self.lib.ft_halo_unpack(ctypes.byref(out_t), ctypes.c_void_p(cols.data_ptr()),
+                                           cols.numel(), slots, self.ftd,
+                                           ctypes.c_void_p(self.recv_msg[q].data_ptr()),
+                                           step_cap + self.recv_off[q] * slots,
+                                           ctypes.c_void_p(self.ws.data_ptr()), flags, stream),
+                   "ft_halo_unpack")
+
+    # -- control -------------------------------------------------------------
+
+    def set_control(self, steps_done):
+        _check(self.lib.ft_domain_control(ctypes.c_void_p(self.ws.data_ptr()), int(steps_done),
+                                          ctypes.c_void_p(self.ctl_out.data_ptr()),
+                                          _stream_handle()), "ft_domain_control")
+
+    def read_control(self):
+        _check(self.lib.ft_domain_control(ctypes.c_void_p(self.ws.data_ptr()), -1,
+                                          ctypes.c_void_p(self.ctl_out.data_ptr()),
+                                          _stream_handle()), "ft_domain_control")
+        c = self.ctl_out.cpu().numpy()
+        return int(c[0]), int(c[1]), int(c[2])
+
+    def read_trace(self, n):
+        if n <= 0:
+            return _stats_from_bytes(b"")
+        return _stats_from_bytes(self.trace[:n * _lib.STATS_BYTES].cpu().numpy().tobytes())
+
+    def grow_step_capacity(self, needed):
+        if needed > self.step_cap:
+            self.step_cap = max(int(needed), int(self.step_cap * GROWTH))
+
+    def set_slots(self, need):
+        if need > self.slots:
+            self.slots = int(need)
+            self._alloc_messages()
+        self.need.zero_()
+
+    # -- results -------------------------------------------------------------
+
+    def owned_field(self, steps_done):
+        """The owned columns after ``steps_done`` steps as a DeviceCSC
+        (n_rows x n_own), compacted from the tiled buffer."""
+        torch = _torch()
+        tiled_t = self.meta[steps_done % 2][0]
+        buf = self.bufs[steps_done % 2]
+        src = _lib.FtTiled(self.n_rows, self.n_own,
+                           buf.desc.data_ptr() + 8 * self.col_begin, buf.row_idx.data_ptr(),
+                           buf.values.data_ptr(), tiled_t.capacity)
+        cap = max(1, int(buf.desc.view(-1, 2)[self.col_begin:self.col_begin + self.n_own, 1]
+                         .sum().item()))
+        out = DeviceCSC.allocate(self.n_rows, self.n_own, cap, self.vdtype, self.device)
+        o_c = out.ft_csc()
+        rec = torch.zeros(_lib.STATS_BYTES, dtype=torch.uint8, device=self.device)
+        _check(self.lib.ft_compact(ctypes.byref(src), ctypes.byref(o_c), self.ftd,
+                                   ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel(),
+                                   ctypes.c_void_p(rec.data_ptr()), _stream_handle()),
+               "ft_compact")
+        r = _stats_from_bytes(rec.cpu().numpy().tobytes())[0]
+        if int(r["status"]) != _lib.FT_STATUS_OK:
+            raise BackendError("compaction of the owned columns failed")
+        out.nnz = int(r["nnz_phi"])
+        return out
+
+
+# ---------------------------------------------------------------------------
+# the driver
+
+
+def evolve_partitioned(ranks, transport, params, max_steps=1000, tol=1e-4,
+                       base_threshold=None, sync_every=16):
+    """Evolve a partitioned field (one :class:`DomainRank` per local rank)
+    until converged or ``max_steps`` steps, exactly as :func:`field.evolve`
+    (field.py:289-321).  Returns ``(steps_done, trace)``; the fields stay on
+    the devices (:meth:`DomainRank.owned_field`)."""
+    if max_steps < 1:
+        raise ShapeError("max_steps must be >= 1")
+    params.validate()
+    n_v = ranks[0].n_v
+    thr = BASE_EXHAUSTION_PER_VERTEX * n_v if base_threshold is None else base_threshold
+    prm = params.ft_params()
+    stream = _stream_handle()
+    for r in ranks:
+        r.begin(max_steps)
+    i = 0
+    while True:
+        end = min(i + sync_every, max_steps)
+        for s in range(i, end):
+            for r in ranks:
+                r.launch_step(s, prm, stream)
+            transport.all_gather(ranks)
+            for r in ranks:
+                r.launch_combine(max_steps, tol, thr, stream)
+            transport.exchange(ranks)
+            for r in ranks:
+                r.launch_unpack(s, stream)
+        ctl = [r.read_control() for r in ranks]
+        done, status = ctl[0][0], ctl[0][1]
+        if any(c[:2] != (done, status) for c in ctl):
+            raise BackendError("ranks disagree on the step count")
+        if status in (_lib.FT_STATUS_CONVERGED, _lib.FT_STATUS_MAXSTEPS):
+            break
+        if status == _lib.FT_STATUS_OK:
+            i = end
+            if i >= max_steps:
+                break
+            continue
+        if status == _lib.FT_STATUS_OVERFLOW:
+            for r, c in zip(ranks, ctl):
+                r.grow_step_capacity(c[2] + c[2] // 5)
+        elif status == _lib.FT_STATUS_HALO_OVERFLOW:
+            need = transport.max_int([int(r.need.item()) for r in ranks])
+            for r in ranks:
+                r.set_slots(need)
+        else:
+            _raise_step_error(ranks[0].read_trace(done + 1)[done], done)
+            raise BackendError(f"partitioned step failed with status {status}")
+        for r in ranks:                 # rewind: redo the failed step
+            r.set_control(done)
+        i = done
+    steps = ranks[0].read_control()[0]
+    recs = ranks[0].read_trace(steps)
+    trace = [StepStats(max_delta=float(x["max_delta"]), nnz_phi=int(x["nnz_phi"]),
+                       base_mass=float(x["base_mass"]), nnz_skel=int(x["nnz_skel"]),
+                       converged=int(x["status"]) == _lib.FT_STATUS_CONVERGED) for x in recs]
+    if trace:
+        trace[-1].realloc_count = sum(r.reallocs for r in ranks)
+    return steps, trace
+
+
+def gather_field(ranks, steps_done, n_rows=None):
+    """Host SparseMat of the whole field from local ranks covering every
+    owned range (loopback runs; a multi-process run gathers per rank)."""
+    parts = sorted(ranks, key=lambda r: r.col_begin)
+    ptrs, idx, vals = [np.zeros(1, dtype=np.int64)], [], []
+    base = 0
+    for r in parts:
+        h = r.owned_field(steps_done).to_host()
+        cp = np.asarray(h.col_ptr, dtype=np.int64)
+        ptrs.append(cp[1:] + base)
+        idx.append(np.asarray(h.row_idx[:cp[-1]]))
+        vals.append(np.asarray(h.values[:cp[-1]]))
+        base += int(cp[-1])
+    n = parts[-1].n_v
+    return SparseMat(n_rows or parts[0].n_rows, n, np.concatenate(ptrs),
+                     np.concatenate(idx) if idx else np.zeros(0, INDEX),
+                     np.concatenate(vals) if vals else np.zeros(0), check=False)

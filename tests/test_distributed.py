@@ -1,0 +1,287 @@
+"""Partitioned fields (vertex row-partition + halo exchange).
+
+CPU: the partition / halo-plan host logic, the lattice slab builder against
+the globally built mesh + Laplacian + init_field, and a world_size-2 gloo
+run of the exchange protocol (TorchTransport) with the oracle as the
+per-rank step, checked against the single-process oracle trajectory.
+GPU: several loopback ranks on one device through the CUDA path
+(ft_domain_step / ft_halo_* / ft_domain_combine) against the single-GPU
+evolve, bitwise.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_1804_09152_b200 as ft
+from paper_1804_09152_b200 import _lib
+from paper_1804_09152_b200 import distributed as D
+from oracle import pyoracle as O
+from conftest import P
+
+PARAMS = P([0.2, 1.0, 0.3, 0.2, 0.2, 5.0])
+
+
+def _grid_case(nx=16, ny=12, n_seeds=9, seed=3):
+    mesh = ft.gen_periodic_grid(nx, ny)
+    seeds = np.random.default_rng(seed).choice(nx * ny, n_seeds, replace=False)
+    return mesh, seeds
+
+
+def _same_problem(a, b):
+    for k in ("lap_ptr", "lap_idx", "lap_val", "cols", "col_ptr", "row_idx", "values"):
+        x, y = getattr(a, k), getattr(b, k)
+        assert x.shape == y.shape and np.array_equal(x, y), k
+    assert a.lap_flags == b.lap_flags and a.n_rows == b.n_rows
+
+
+def test_partition_even_and_owner():
+    p = D.Partition.even(100, 3)
+    assert list(p.bounds) == [0, 33, 66, 100] and p.world == 3
+    assert list(p.owner([0, 32, 33, 99])) == [0, 0, 1, 2]
+    q = D.Partition.even(12 * 10, 4, align=12)
+    assert all(b % 12 == 0 for b in q.bounds)
+    with pytest.raises(ft.errors.ShapeError):
+        D.Partition([0, 5, 5, 9])
+
+
+@pytest.mark.parametrize("world,align", [(1, 1), (2, 16), (3, 1), (4, 16), (5, 7)])
+def test_grid_slab_matches_global_build(world, align):
+    nx, ny = 16, 12
+    mesh, seeds = _grid_case(nx, ny, n_seeds=14)
+    seeds[:2] = [5, 6]                        # overlapping one-rings: split claims
+    fld = ft.init_field(mesh, seeds)
+    lap = ft.build_laplacian(mesh)
+    part = D.Partition.even(nx * ny, world, align=align)
+    for r in range(world):
+        _same_problem(D.periodic_grid_problem(nx, ny, seeds, part, r),
+                      D.local_problem(fld.phi, lap, part, r))
+
+
+def test_halo_plans_are_consistent():
+    mesh = ft.gen_icosphere(2)
+    seeds = np.arange(0, mesh.n_vertices, 17)
+    fld = ft.init_field(mesh, seeds)
+    lap = ft.build_laplacian(mesh)
+    part = D.Partition.even(mesh.n_vertices, 4)
+    probs = [D.local_problem(fld.phi, lap, part, r) for r in range(4)]
+    plans = D.build_plans(probs, D.LoopbackTransport())
+    for r, pl in enumerate(plans):
+        held = set(range(*part.range(r)))
+        for q, cols in pl.recv.items():
+            assert np.array_equal(plans[q].send[r], cols)
+            assert np.all(part.owner(cols) == q)
+            held |= set(cols.tolist())
+        assert held == set(probs[r].cols.tolist())
+
+
+def test_halo_message_layout():
+    for n, s, dt in [(0, 7, _lib.FT_F64), (3, 7, _lib.FT_F64), (5, 2, _lib.FT_F32), (1, 1, _lib.FT_F64)]:
+        assert _lib.lib().ft_halo_bytes(n, s, dt) == _msg_layout(n, s, dt)[-1]
+
+
+# -- gloo: the exchange protocol with the oracle as the per-rank step --------
+
+
+def _msg_layout(n, slots, dtype):
+    head = 4 * n * (1 + slots)
+    head = (head + 7) & ~7
+    vs = 8 if dtype == _lib.FT_F64 else 4
+    return 4 * n, head, head + vs * n * slots
+
+
+def _pack(cols, held, slots):
+    """numpy restatement of the ft_halo_pack message (f64)."""
+    n = len(cols)
+    rows_off, vals_off, total = _msg_layout(n, slots, _lib.FT_F64)
+    buf = np.zeros(total, dtype=np.uint8)
+    cnt = buf[:4 * n].view(np.int32)
+    rows = buf[rows_off:rows_off + 4 * n * slots].view(np.int32)
+    vals = buf[vals_off:].view(np.float64)
+    for i, c in enumerate(cols):
+        ri, va = held[int(c)]
+        assert ri.size <= slots
+        cnt[i] = ri.size
+        rows[i * slots:i * slots + ri.size] = ri
+        vals[i * slots:i * slots + ri.size] = va
+    return buf
+
+
+def _unpack(cols, buf, held, slots):
+    n = len(cols)
+    rows_off, vals_off, _ = _msg_layout(n, slots, _lib.FT_F64)
+    cnt = buf[:4 * n].view(np.int32)
+    rows = buf[rows_off:rows_off + 4 * n * slots].view(np.int32)
+    vals = buf[vals_off:].view(np.float64)
+    for i, c in enumerate(cols):
+        k = int(cnt[i])
+        held[int(c)] = (rows[i * slots:i * slots + k].copy(), vals[i * slots:i * slots + k].copy())
+
+
+class _HostRank:
+    """The attributes TorchTransport reads, over CPU tensors."""
+
+    def __init__(self, plan, world, slots):
+        import torch
+        self.plan = plan
+        self.record = torch.zeros(_lib.STATS_BYTES, dtype=torch.uint8)
+        self.gathered = torch.zeros(world * _lib.STATS_BYTES, dtype=torch.uint8)
+        self.send_msg = {q: torch.zeros(_msg_layout(len(c), slots, _lib.FT_F64)[-1], dtype=torch.uint8)
+                         for q, c in plan.send.items()}
+        self.recv_msg = {q: torch.zeros(_msg_layout(len(c), slots, _lib.FT_F64)[-1], dtype=torch.uint8)
+                         for q, c in plan.recv.items()}
+
+
+def _gloo_worker(rank, world, port, n_steps, out_q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nx, ny = 16, 12
+        mesh, seeds = _grid_case(nx, ny)
+        fld = ft.init_field(mesh, seeds)
+        lap_t = O.Csc.of(ft.field._with_diagonal(ft.build_laplacian(mesh).mat_t))
+        part = D.Partition.even(nx * ny, world, align=nx)
+        prob = D.periodic_grid_problem(nx, ny, seeds, part, rank)
+        tr = D.TorchTransport()
+        (plan,) = D.build_plans([prob], tr)
+        slots = 7
+        host = _HostRank(plan, world, slots)
+        held = {int(c): (prob.row_idx[prob.col_ptr[k]:prob.col_ptr[k + 1]],
+                         prob.values[prob.col_ptr[k]:prob.col_ptr[k + 1]])
+                for k, c in enumerate(prob.cols)}
+        b, e = part.range(rank)
+        ref = O.Csc.of(fld.phi)
+        n_v = nx * ny
+        for _ in range(n_steps):
+            # local step: the held columns in a global-size field, owned columns kept
+            cp = np.zeros(n_v + 1, dtype=np.int64)
+            for c, (ri, _v) in held.items():
+                cp[c + 1] = ri.size
+            cp = np.cumsum(cp)
+            ri = np.concatenate([held[c][0] if c in held else np.zeros(0, np.int32) for c in range(n_v)])
+            va = np.concatenate([held[c][1] if c in held else np.zeros(0) for c in range(n_v)])
+            loc = O.Csc(prob.n_rows, n_v, cp, ri, va)
+            nxt, _ = O.step_c(loc, lap_t, PARAMS)
+            ref, st = O.step_c(ref, lap_t, PARAMS)
+            new = {}
+            for c in range(b, e):
+                new[c] = nxt.column(c)
+                rr, rv = ref.column(c)
+                assert np.array_equal(new[c][0], rr) and np.array_equal(new[c][1], rv), (rank, c)
+            # local record: owned max |delta| and base mass (fixed order)
+            rec = np.zeros(1, dtype=_lib.STATS_DTYPE)
+            rec["nnz_phi"] = sum(v[0].size for v in new.values())
+            host.record.copy_(torch.from_numpy(rec.view(np.uint8).copy()))
+            tr.all_gather([host])
+            allrec = host.gathered.numpy().view(_lib.STATS_DTYPE)
+            assert int(allrec["nnz_phi"].sum()) == ref.nnz
+            # halo exchange
+            for q, cols in plan.send.items():
+                host.send_msg[q].copy_(torch.from_numpy(_pack(cols, new, slots)))
+            tr.exchange([host])
+            for q, cols in plan.recv.items():
+                _unpack(cols, host.recv_msg[q].numpy(), new, slots)
+            held = new
+        assert tr.max_int([rank + 5]) == world + 4
+        out_q.put((rank, "ok"))
+    except Exception as exc:                    # pragma: no cover - reported to the parent
+        out_q.put((rank, repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_gloo_two_ranks_exchange_protocol():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, 4, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}
+
+
+# -- GPU: loopback ranks through the CUDA path --------------------------------
+
+
+def _loopback(fld, lap, part, precision="exact", slots=D.DEFAULT_SLOTS):
+    probs = [D.local_problem(fld.phi, lap, part, r) for r in range(part.world)]
+    plans = D.build_plans(probs, D.LoopbackTransport())
+    return [D.DomainRank(p, pl, precision=precision, slots=slots) for p, pl in zip(probs, plans)]
+
+
+def _assert_same_field(a, b):
+    assert np.array_equal(np.asarray(a.col_ptr), np.asarray(b.col_ptr))
+    nnz = int(a.col_ptr[-1])
+    assert np.array_equal(np.asarray(a.row_idx[:nnz]), np.asarray(b.row_idx[:nnz]))
+    assert np.array_equal(np.asarray(a.values[:nnz]), np.asarray(b.values[:nnz]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,world", [("grid", 3), ("ico", 4)])
+def test_loopback_ranks_match_single_gpu(case, world):
+    if case == "grid":
+        mesh, seeds = _grid_case(40, 30, n_seeds=25)
+        part = D.Partition.even(mesh.n_vertices, world, align=40)
+        n_steps = 60
+    else:
+        mesh = ft.gen_icosphere(4)
+        seeds = np.random.default_rng(0).choice(mesh.n_vertices, 64, replace=False)
+        part = D.Partition.even(mesh.n_vertices, world)
+        n_steps = 120
+    lap = ft.build_laplacian(mesh)
+    fld = ft.init_field(mesh, seeds)
+    single, tr1 = ft.evolve(fld, lap, ft.CouplingParams(), max_steps=n_steps, tol=0.0)
+    ranks = _loopback(fld, lap, part)
+    steps, tr2 = D.evolve_partitioned(ranks, D.LoopbackTransport(), ft.CouplingParams(),
+                                      max_steps=n_steps, tol=0.0)
+    assert steps == n_steps and len(tr2) == n_steps
+    _assert_same_field(D.gather_field(ranks, steps), single.phi)
+    for a, b in zip(tr1, tr2):
+        assert a.max_delta == b.max_delta and a.nnz_phi == b.nnz_phi
+        assert abs(a.base_mass - b.base_mass) <= 1e-12 * max(1.0, a.base_mass)
+
+
+@pytest.mark.gpu
+def test_loopback_recovers_from_overflows(monkeypatch):
+    monkeypatch.setattr(D, "POOL_FRACTION", 0.0)
+    monkeypatch.setattr(D, "POOL_MIN", 1)
+    mesh, seeds = _grid_case(40, 30, n_seeds=25)
+    lap = ft.build_laplacian(mesh)
+    fld = ft.init_field(mesh, seeds)
+    part = D.Partition.even(mesh.n_vertices, 2, align=40)
+    single, _ = ft.evolve(fld, lap, ft.CouplingParams(), max_steps=40, tol=0.0)
+    ranks = _loopback(fld, lap, part, slots=1)
+    steps, tr = D.evolve_partitioned(ranks, D.LoopbackTransport(), ft.CouplingParams(),
+                                     max_steps=40, tol=0.0, sync_every=5)
+    assert steps == 40
+    assert all(r.slots > 1 for r in ranks)
+    _assert_same_field(D.gather_field(ranks, steps), single.phi)
+
+
+@pytest.mark.gpu
+def test_loopback_stops_with_single_gpu():
+    mesh = ft.gen_icosphere(3)
+    seeds = np.arange(0, mesh.n_vertices, 97)
+    lap = ft.build_laplacian(mesh)
+    fld = ft.init_field(mesh, seeds)
+    single, tr1 = ft.evolve(fld, lap, ft.CouplingParams(), max_steps=400, tol=1e-3)
+    ranks = _loopback(fld, lap, D.Partition.even(mesh.n_vertices, 2))
+    steps, tr2 = D.evolve_partitioned(ranks, D.LoopbackTransport(), ft.CouplingParams(),
+                                      max_steps=400, tol=1e-3)
+    assert steps == len(tr1) and tr2[-1].converged == tr1[-1].converged
+    _assert_same_field(D.gather_field(ranks, steps), single.phi)

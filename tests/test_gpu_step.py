@@ -100,6 +100,27 @@ def test_generated_mesh_and_seeding_end_to_end():
     assert [s.max_delta for s in trace] == [s["max_delta"] for s in rtrace]
 
 
+@pytest.mark.parametrize("subdiv,n_seeds", [(4, 64), (3, 64), (3, 160)])
+def test_high_band_density_all_tiers(subdiv, n_seeds):
+    """Dense bands (many columns with > 2 entries per neighbour and > 8 rows
+    in the union) route most columns through tiers 2 and 3; bitwise against
+    the C oracle, through the device evolve and the step loop."""
+    mesh = ft.gen_icosphere(subdiv)
+    lap = ft.build_laplacian(mesh)
+    seeds = np.random.default_rng(0).choice(mesh.n_vertices, n_seeds, replace=False)
+    fld = ft.init_field(mesh, seeds)
+    out, trace = ft.evolve(fld, lap, DEFAULT, max_steps=40, tol=0.0)
+    lt = po.Csc.of(ft.field._with_diagonal(lap.mat_t))
+    ref, rtrace = po.evolve_c(po.Csc.of(fld.phi), lt, DEFAULT, 40, n_threads=4)
+    assert_csc_equal(out.phi, ref)
+    assert [s.max_delta for s in trace] == [s["max_delta"] for s in rtrace]
+    cur = fld
+    for _ in range(12):
+        cur, _st = ft.step(cur, lap, DEFAULT)
+    ref12, _ = po.evolve_c(po.Csc.of(fld.phi), lt, DEFAULT, 12, n_threads=4)
+    assert_csc_equal(cur.phi, ref12)
+
+
 def test_fast_mode_single_step_tolerance():
     """FAST (fp32 storage) from identical inputs: |d| <= 1e-5|ref| + 2e-7."""
     t = golden_npz("c1_traj.npz")
