@@ -27,9 +27,15 @@ Reported beside `value` (steps/s):
 --impl reference runs only the reference CPU implementation and prints its
 line (rank 0; other ranks exit 0).
 
-N > 1 (torchrun): each rank runs its own replica of the workload on its GPU
-(weak scaling, no data-path collective); the vertex-partitioned halo
-exchange path is not yet in this build.
+N > 1 (torchrun, one rank per GPU over NCCL): weak scaling on ONE field --
+the torus grows to 3200 x (3125 N) vertices with 4096 N seeds (N = 1 is C3
+exactly), vertices are row-partitioned into N slabs of 10M, and every Euler
+step exchanges the one-ring halo rows with NCCL send/recv and all-gathers
+the step statistics (paper_1804_09152_b200/distributed.py).  `value` is in
+C3-equivalent steps/s (global steps/s x N, i.e. vertex-steps/s / 10M), so
+perfect weak scaling keeps value_N = N value_1.
+--emulate-ranks N runs that partitioned path with N loopback ranks on one
+GPU (sequential; for validating the code path, not a performance number).
 """
 
 import argparse
@@ -70,6 +76,8 @@ def parse():
                     help="bounded CPU-baseline sample (seconds of reference steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="run the partitioned path with N loopback ranks on one GPU")
     return ap.parse_args()
 
 
@@ -417,8 +425,147 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk,
-            "gpu_launches": 3 * K + 3,
+            "gpu_launches": 4 * K + 3,
         }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_partitioned(args, world, rank, local, emulate=0):
+    """N ranks step one weak-scaled torus (see the module docstring)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1804_09152_b200 as ft
+    from paper_1804_09152_b200 import _lib, distributed as D
+
+    W = emulate or world
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    nx, nyg = args.nx, args.ny * W
+    n_v = nx * nyg
+    n_seeds = args.seeds * W
+    seeds = np.random.default_rng(0).choice(n_v, n_seeds, replace=False)
+    part = D.Partition.even(n_v, W, align=nx)
+    mine = list(range(W)) if emulate else [rank]
+    probs = [D.periodic_grid_problem(nx, nyg, seeds, part, r) for r in mine]
+    transport = D.LoopbackTransport() if emulate else D.TorchTransport()
+    plans = D.build_plans(probs, transport)
+    prec = args.precision
+    vbytes = 8 if prec == "exact" else 4
+    params = ft.CouplingParams()
+    ranks = [D.DomainRank(p, pl, precision=prec) for p, pl in zip(probs, plans)]
+    warm = max(3, args.warmup)
+    D.evolve_partitioned(ranks, transport, params, max_steps=warm, tol=0.0)
+    K = args.steps
+    for r in ranks:
+        r.step_events = []
+    stream = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0.record(stream)
+    steps, tr = D.evolve_partitioned(ranks, transport, params, max_steps=K, tol=0.0)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    if steps != K:
+        raise RuntimeError(f"partitioned run stopped after {steps} of {K} steps")
+    elapsed_ms = allmax(e0.elapsed_time(e1))
+    r0 = ranks[0]
+    step_ms = np.array([a.elapsed_time(b) for r in ranks for a, b in r.step_events[-K * len(ranks):]])
+    for r in ranks:
+        r.step_events = None
+    nnz_out = np.array([t.nnz_phi for t in tr], dtype=np.float64) / W
+    nnz_in = np.concatenate([[nnz_out[0]], nnz_out[:-1]])
+    alg = np.array([algorithmic_bytes(r0.n_own, 7 * r0.n_own, a, b, vbytes)
+                    for a, b in zip(nnz_in, nnz_out)])
+    achieved = float(alg.mean() / (step_ms.mean() * 1e-3) / 1e9)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    skel = sum(t.nnz_skel for t in tr)
+    halo_cols = [r.n_halo for r in ranks]
+    msg_bytes = sum(int(m.numel()) for r in ranks for m in r.send_msg.values()) / len(ranks)
+
+    # e2e: host problem in -> K steps -> owned field + labels back on the host
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        ranks2 = [D.DomainRank(p, pl, precision=prec) for p, pl in zip(probs, plans)]
+        D.evolve_partitioned(ranks2, transport, params, max_steps=K, tol=0.0)
+        d2h = 0
+        for r in ranks2:
+            f = r.owned_field(r.steps_done)
+            h = f.to_host()
+            lab = r.owned_labels(field=f).cpu().numpy()
+            d2h += 4 * (r.n_own + 1) + (4 + vbytes) * h.nnz + 8 * lab.size
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        barrier()
+        e2e_s = allmax(t1 - t0)
+        h2d = sum(4 * (p.lap_ptr.size + p.lap_idx.size) + 8 * p.lap_val.size + 8 * p.cols.size
+                  + 4 * p.row_idx.size + vbytes * p.values.size for p in probs)
+        del ranks2
+        e2e = {"value": W * K / e2e_s, "unit": "steps/s",
+               "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K),
+               "path": "DomainRank(host slab problem) -> evolve_partitioned(K steps) -> owned "
+                       "field + labels on the host, per rank"}
+    if rank == 0:
+        value = W * K / (elapsed_ms * 1e-3)
+        line = {
+            "metric": "time-steps/sec (fused Euler step); layer-nnz updates/sec; HBM GB/s vs roofline",
+            "value": value, "unit": "steps/s (C3-equivalent: 10M-vertex steps)", "n_gpus": world,
+            "steps": K, "warmup": warm, "ms_per_step": elapsed_ms / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if prec == "exact" else "f32-storage/f64-arith", "data": "synthetic",
+            "config": {"workload": f"torus {nx}x{nyg} ({n_v:,} vertices), {n_seeds:,} seeds, "
+                                   f"vertex row-partition over {W} ranks + halo exchange",
+                       "n_vertices": n_v, "seeds": n_seeds, "precision": prec,
+                       "laplacian": "uniform", "parallelism": f"row-partition x{W} (NCCL halo)"
+                       if not emulate else f"{W} loopback ranks on 1 GPU (emulated)",
+                       "halo_columns_per_rank": halo_cols[0], "halo_message_bytes_per_rank": msg_bytes,
+                       "l2": "working set > 126 MB L2 (no flush needed)",
+                       "window": f"steps {warm + 1}..{warm + K} from init_field"},
+            "layer_nnz_updates_per_s": skel / (elapsed_ms * 1e-3),
+            "kernel_ms_per_step": float(step_ms.mean()),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "ft_domain_step (tiers 1-3 + local finalize) per rank",
+                         "bytes_per_launch": float(alg.mean())},
+            "cpu_baseline": None,
+            "e2e": e2e,
+            "clocks": clk,
+            # per step and rank: tiers 1-3 + finalize, one pack per peer sent to,
+            # the combine, one unpack per peer received from; one control
+            # snapshot per 16-step chunk
+            "gpu_launches": (5 + len(r0.send_msg) + len(r0.recv_msg)) * K + -(-K // 16),
+        }
+        if emulate:
+            line["emulated"] = True
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -426,8 +573,12 @@ def run_ours(args):
 
 def main():
     args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference_arm(args)
+    elif world > 1 or args.emulate_ranks:
+        run_partitioned(args, world, int(os.environ.get("RANK", "0")),
+                        int(os.environ.get("LOCAL_RANK", "0")), emulate=args.emulate_ranks)
     else:
         run_ours(args)
 

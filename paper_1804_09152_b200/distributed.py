@@ -27,7 +27,6 @@ NCCL for CUDA tensors, gloo for CPU tensors) for one rank per process, and
 """
 
 import ctypes
-import time
 
 import numpy as np
 
@@ -341,7 +340,13 @@ class DomainRank:
         self.gathered = torch.zeros(self.world * _lib.STATS_BYTES, dtype=torch.uint8, device=device)
         self.need = torch.zeros(1, dtype=torch.int32, device=device)
         self.ctl_out = torch.zeros(3, dtype=torch.int64, device=device)
+        # control snapshots in flight (device, pinned host, event) x 2
+        self.snap = [(torch.zeros(3, dtype=torch.int64, device=device),
+                      torch.zeros(3, dtype=torch.int64, pin_memory=True),
+                      torch.cuda.Event()) for _ in range(2)]
         self.trace = None
+        self.steps_done = 0            # steps completed by previous evolve calls
+        self.step_events = None        # list: (start, end) CUDA events per ft_domain_step
         # halo layout: peers ascending, columns of a peer consecutive
         self.recv_cols = {q: torch.from_numpy(v).to(device) for q, v in plan.recv.items()}
         self.send_cols = {q: torch.from_numpy(v).to(device) for q, v in plan.send.items()}
@@ -420,12 +425,15 @@ class DomainRank:
 
     # -- the per-step launches (all asynchronous) ----------------------------
 
-    def begin(self, max_steps, steps_done=0):
+    def begin(self, total_steps):
         torch = _torch()
-        if self.trace is None or self.trace.numel() < max_steps * _lib.STATS_BYTES:
-            self.trace = torch.zeros(max_steps * _lib.STATS_BYTES, dtype=torch.uint8,
+        if self.trace is None or self.trace.numel() < total_steps * _lib.STATS_BYTES:
+            old = self.trace
+            self.trace = torch.zeros(total_steps * _lib.STATS_BYTES, dtype=torch.uint8,
                                      device=self.device)
-        self.set_control(steps_done)
+            if old is not None:
+                self.trace[:old.numel()].copy_(old)
+        self.set_control(self.steps_done)
 
     def launch_step(self, i, prm, stream):
         lib = self.lib
@@ -434,9 +442,16 @@ class DomainRank:
         dom = _lib.FtDomain(self.col_begin, self.n_own, step_cap)
         wp, wn = ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel()
         rec = ctypes.c_void_p(self.record.data_ptr())
+        if self.step_events is not None:
+            torch = _torch()
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
+            self.step_events.append(ev)
         _check(lib.ft_domain_step(ctypes.byref(self.lap_c), self.lap_flags, ctypes.byref(in_t),
                                   ctypes.byref(out_t), self.ftd, ctypes.byref(prm),
                                   ctypes.byref(dom), wp, wn, rec, stream), "ft_domain_step")
+        if self.step_events is not None:
+            self.step_events[-1][1].record()
         for q, cols in self.send_cols.items():
             _check(lib.ft_halo_pack(ctypes.byref(out_t), ctypes.c_void_p(cols.data_ptr()),
                                     cols.numel(), slots, self.ftd,
@@ -473,6 +488,21 @@ class DomainRank:
                                           ctypes.c_void_p(self.ctl_out.data_ptr()),
                                           _stream_handle()), "ft_domain_control")
         c = self.ctl_out.cpu().numpy()
+        return int(c[0]), int(c[1]), int(c[2])
+
+    def snapshot(self, k):
+        """Asynchronous copy of the control block into snapshot slot k."""
+        dev, host, ev = self.snap[k]
+        _check(self.lib.ft_domain_control(ctypes.c_void_p(self.ws.data_ptr()), -1,
+                                          ctypes.c_void_p(dev.data_ptr()), _stream_handle()),
+               "ft_domain_control")
+        host.copy_(dev, non_blocking=True)
+        ev.record()
+
+    def snapshot_wait(self, k):
+        _dev, host, ev = self.snap[k]
+        ev.synchronize()
+        c = host.numpy()
         return int(c[0]), int(c[1]), int(c[2])
 
     def read_trace(self, n):
@@ -517,6 +547,19 @@ class DomainRank:
         return out
 
 
+    def owned_labels(self, steps_done=None, field=None):
+        """Argmax cell labels of the owned vertices (ft_labels, field.py:
+        324-356) as a device int64 tensor."""
+        torch = _torch()
+        f = field if field is not None else self.owned_field(
+            self.steps_done if steps_done is None else steps_done)
+        labels = torch.empty(max(self.n_own, 1), dtype=torch.int64, device=self.device)
+        c = f.ft_csc()
+        _check(self.lib.ft_labels(ctypes.byref(c), self.ftd, ctypes.c_void_p(labels.data_ptr()),
+                                  _stream_handle()), "ft_labels")
+        return labels[:self.n_own]
+
+
 # ---------------------------------------------------------------------------
 # the driver
 
@@ -524,9 +567,16 @@ class DomainRank:
 def evolve_partitioned(ranks, transport, params, max_steps=1000, tol=1e-4,
                        base_threshold=None, sync_every=16):
     """Evolve a partitioned field (one :class:`DomainRank` per local rank)
-    until converged or ``max_steps`` steps, exactly as :func:`field.evolve`
-    (field.py:289-321).  Returns ``(steps_done, trace)``; the fields stay on
-    the devices (:meth:`DomainRank.owned_field`)."""
+    by up to ``max_steps`` more steps, stopping when converged, exactly as
+    :func:`field.evolve` (field.py:289-321).  Returns ``(steps, trace)`` of
+    this call; the fields stay on the devices (:meth:`DomainRank.owned_field`)
+    and a later call resumes from them.
+
+    The host enqueues ``sync_every`` steps per chunk and reads the control
+    block of chunk c (an asynchronous snapshot) only after chunk c+1 is
+    enqueued, so the GPUs never wait for the host.  After a failed step the
+    remaining launches are device no-ops; the host grows what overflowed and
+    rewinds to the failed step."""
     if max_steps < 1:
         raise ShapeError("max_steps must be >= 1")
     params.validate()
@@ -534,31 +584,44 @@ def evolve_partitioned(ranks, transport, params, max_steps=1000, tol=1e-4,
     thr = BASE_EXHAUSTION_PER_VERTEX * n_v if base_threshold is None else base_threshold
     prm = params.ft_params()
     stream = _stream_handle()
+    s0 = ranks[0].steps_done
+    total = s0 + max_steps
     for r in ranks:
-        r.begin(max_steps)
-    i = 0
-    while True:
-        end = min(i + sync_every, max_steps)
+        r.begin(total)
+
+    def enqueue(i, end, slot):
         for s in range(i, end):
             for r in ranks:
                 r.launch_step(s, prm, stream)
             transport.all_gather(ranks)
             for r in ranks:
-                r.launch_combine(max_steps, tol, thr, stream)
+                r.launch_combine(total, tol, thr, stream)
             transport.exchange(ranks)
             for r in ranks:
                 r.launch_unpack(s, stream)
-        ctl = [r.read_control() for r in ranks]
+        for r in ranks:
+            r.snapshot(slot)
+
+    i = s0
+    inflight = []          # (snapshot slot, chunk end), oldest first
+    nslot = 0
+    while True:
+        while i < total and len(inflight) < 2:
+            end = min(i + sync_every, total)
+            enqueue(i, end, nslot)
+            inflight.append((nslot, end))
+            nslot ^= 1
+            i = end
+        slot, _end = inflight.pop(0)
+        ctl = [r.snapshot_wait(slot) for r in ranks]
         done, status = ctl[0][0], ctl[0][1]
         if any(c[:2] != (done, status) for c in ctl):
             raise BackendError("ranks disagree on the step count")
         if status in (_lib.FT_STATUS_CONVERGED, _lib.FT_STATUS_MAXSTEPS):
             break
         if status == _lib.FT_STATUS_OK:
-            i = end
-            if i >= max_steps:
-                break
             continue
+        _torch().cuda.synchronize()         # let the no-op launches drain
         if status == _lib.FT_STATUS_OVERFLOW:
             for r, c in zip(ranks, ctl):
                 r.grow_step_capacity(c[2] + c[2] // 5)
@@ -569,27 +632,31 @@ def evolve_partitioned(ranks, transport, params, max_steps=1000, tol=1e-4,
         else:
             _raise_step_error(ranks[0].read_trace(done + 1)[done], done)
             raise BackendError(f"partitioned step failed with status {status}")
-        for r in ranks:                 # rewind: redo the failed step
+        for r in ranks:                     # rewind: redo the failed step
             r.set_control(done)
         i = done
+        inflight = []
+    _torch().cuda.synchronize()
     steps = ranks[0].read_control()[0]
-    recs = ranks[0].read_trace(steps)
+    recs = ranks[0].read_trace(steps)[s0:]
+    for r in ranks:
+        r.steps_done = steps
     trace = [StepStats(max_delta=float(x["max_delta"]), nnz_phi=int(x["nnz_phi"]),
                        base_mass=float(x["base_mass"]), nnz_skel=int(x["nnz_skel"]),
                        converged=int(x["status"]) == _lib.FT_STATUS_CONVERGED) for x in recs]
     if trace:
         trace[-1].realloc_count = sum(r.reallocs for r in ranks)
-    return steps, trace
+    return steps - s0, trace
 
 
-def gather_field(ranks, steps_done, n_rows=None):
+def gather_field(ranks, steps_done=None, n_rows=None):
     """Host SparseMat of the whole field from local ranks covering every
     owned range (loopback runs; a multi-process run gathers per rank)."""
     parts = sorted(ranks, key=lambda r: r.col_begin)
     ptrs, idx, vals = [np.zeros(1, dtype=np.int64)], [], []
     base = 0
     for r in parts:
-        h = r.owned_field(steps_done).to_host()
+        h = r.owned_field(r.steps_done if steps_done is None else steps_done).to_host()
         cp = np.asarray(h.col_ptr, dtype=np.int64)
         ptrs.append(cp[1:] + base)
         idx.append(np.asarray(h.row_idx[:cp[-1]]))
