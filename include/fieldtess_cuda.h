@@ -63,6 +63,10 @@ extern "C" {
 #define FT_LAP_UNIFORM  1  /* values are exactly 1.0/deg(j) off-diagonal and
                               -1.0 on the diagonal (mesh.py:392-400): they are
                               recomputed in registers and never read          */
+#define FT_LAP_PACKED   2  /* with FT_LAP_UNIFORM: lap_t->values points to the
+                              packed neighbour table of ft_laplacian_pack (the
+                              uniform values are never read, so the slot
+                              carries the table); col_ptr / row_idx stay valid */
 
 /* status codes written into ft_step_stats.status / evolve control[1] */
 #define FT_STATUS_OK           0
@@ -134,6 +138,16 @@ int    ft_workspace_init(void* workspace, size_t bytes, void* stream);
  * for n_vertices columns (slots only, empty pool). */
 int64_t ft_tile_slot_entries(void);
 int64_t ft_tiled_min_capacity(int32_t n_vertices);
+
+/* Packed neighbour table of L^T for the tier-1 kernel: int16[n_cols][8],
+ * column j's entries as deltas u - (col_base + j) in stored order (the
+ * reference accumulation order), unused slots -32768.  A column with more
+ * than 8 entries or a delta outside int16 gets all slots -32768 and is read
+ * from col_ptr / row_idx (counted in *n_csr, device int32).  One coalesced
+ * 16-byte load per column replaces the col_ptr -> row_idx dependency chain.
+ * `pack` must be 16-byte aligned. */
+int ft_laplacian_pack(const ft_csc* lap_t, int32_t col_base, int16_t* pack, int32_t* n_csr,
+                      void* stream);
 
 /* -- the fused Euler step ------------------------------------------------ */
 /* One explicit Euler step, canonical in -> canonical out.  Replaces the

@@ -24,6 +24,7 @@ FT_F32 = 1
 
 FT_LAP_EXPLICIT = 0
 FT_LAP_UNIFORM = 1
+FT_LAP_PACKED = 2
 
 FT_STATUS_OK = 0
 FT_STATUS_NAN = 1
@@ -91,7 +92,7 @@ EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
            "ft_step", "ft_step_kernel", "ft_step_fixup", "ft_step_finalize", "ft_compact",
            "ft_evolve", "ft_labels", "ft_faces_by_cell", "ft_lloyd_centroids",
            "ft_dual_products", "ft_domain_step", "ft_halo_bytes", "ft_halo_pack",
-           "ft_halo_unpack", "ft_domain_combine", "ft_domain_control")
+           "ft_halo_unpack", "ft_domain_combine", "ft_domain_control", "ft_laplacian_pack")
 
 _lib = None
 
@@ -158,6 +159,8 @@ def _declare(lib):
     lib.ft_domain_combine.restype = ctypes.c_int
     lib.ft_domain_control.argtypes = [vp, i32, vp, vp]
     lib.ft_domain_control.restype = ctypes.c_int
+    lib.ft_laplacian_pack.argtypes = [P(FtCsc), i32, vp, vp, vp]
+    lib.ft_laplacian_pack.restype = ctypes.c_int
 
 
 def lib():

@@ -31,6 +31,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
+from . import field as F
 from .errors import BackendError, ShapeError
 from .field import (BASE_EXHAUSTION_PER_VERTEX, POOL_FRACTION, POOL_MIN, StepStats, _check,
                     _ft_dtype, _raise_step_error, _stats_from_bytes, _stream_handle,
@@ -334,6 +335,11 @@ class DomainRank:
         self.lap = DeviceCSC.from_host(lap, self.vdtype, device)
         self.lap_c = self.lap.ft_csc()
         self.lap_flags = problem.lap_flags
+        self.pack = None
+        if self.lap_flags == _lib.FT_LAP_UNIFORM and F.PACK_LAPLACIAN:
+            self.pack, _ = F.pack_laplacian(self.lap, col_base=self.col_begin)
+            self.lap_c.values = self.pack.data_ptr()
+            self.lap_flags |= _lib.FT_LAP_PACKED
         self.ws = torch.zeros(int(self.lib.ft_workspace_bytes(self.n_own)), dtype=torch.int8,
                               device=device)
         self.record = torch.zeros(_lib.STATS_BYTES, dtype=torch.uint8, device=device)

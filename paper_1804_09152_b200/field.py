@@ -274,8 +274,34 @@ def init_field(mesh, seeds, precision=None):
 class _DeviceLap:
     def __init__(self, lap_t, flags, n_v):
         self.lap_t = lap_t     # dict precision -> DeviceCSC
-        self.flags = flags
+        self.flags = flags     # FT_LAP_* of the stored values (UNIFORM / EXPLICIT)
         self.n_v = n_v
+        self.pack = None       # packed neighbour table (uniform Laplacians)
+        self.n_csr = 0         # columns the pack leaves to the CSR
+
+    def launch_flags(self):
+        return self.flags | (_lib.FT_LAP_PACKED if self.pack is not None else 0)
+
+    def ft_csc(self, precision):
+        """ft_csc of L^T for the step entry points: with FT_LAP_PACKED the
+        (never read) uniform values slot carries the packed table."""
+        c = self.lap_t[precision].ft_csc()
+        if self.pack is not None:
+            c.values = self.pack.data_ptr()
+        return c
+
+
+def pack_laplacian(lap_t, col_base=0):
+    """Device int16[n_cols][8] neighbour table (ft_laplacian_pack) of a
+    DeviceCSC L^T; returns (tensor, columns left to the CSR)."""
+    torch = _torch()
+    pack = torch.empty(max(lap_t.n_cols, 1) * 8, dtype=torch.int16, device=lap_t.col_ptr.device)
+    n_csr = torch.zeros(1, dtype=torch.int32, device=lap_t.col_ptr.device)
+    c = lap_t.ft_csc()
+    _check(_lib.lib().ft_laplacian_pack(ctypes.byref(c), int(col_base), ctypes.c_void_p(pack.data_ptr()),
+                                        ctypes.c_void_p(n_csr.data_ptr()), _stream_handle()),
+           "ft_laplacian_pack")
+    return pack, int(n_csr.item())
 
 
 def _uniform_values_exact(mat_t):
@@ -335,10 +361,13 @@ def device_laplacian(lap, precision):
     dl = cache[1]
     if precision not in dl.lap_t:
         dl.lap_t[precision] = DeviceCSC.from_host(dl.host, _value_dtype(precision), _device())
+        if dl.pack is None and dl.flags == _lib.FT_LAP_UNIFORM and PACK_LAPLACIAN:
+            dl.pack, dl.n_csr = pack_laplacian(dl.lap_t[precision])
     return dl
 
 
 POOL_FRACTION = 0.5     # overflow pool of a tiled buffer, relative to nnz
+PACK_LAPLACIAN = True   # uniform Laplacians: packed neighbour table for tier 1
 POOL_MIN = 4096
 
 
@@ -447,7 +476,7 @@ def step(field, lap, params, workspace=None):
     out = ws.take_output(dphi, _initial_capacity(dphi))
     reallocs = ws.realloc_count
     ws.realloc_count = 0
-    lap_c = dl.lap_t[field.precision].ft_csc()
+    lap_c = dl.ft_csc(field.precision)
     prm = params.ft_params()
     stream = _stream_handle()
     lib = _lib.lib()
@@ -457,7 +486,7 @@ def step(field, lap, params, workspace=None):
     while True:
         in_c, sc_c, out_c = dphi.ft_csc(), scratch.ft_tiled(), out.ft_csc()
         ev0.record()
-        rc = lib.ft_step(ctypes.byref(lap_c), dl.flags, ctypes.byref(in_c), ctypes.byref(sc_c),
+        rc = lib.ft_step(ctypes.byref(lap_c), dl.launch_flags(), ctypes.byref(in_c), ctypes.byref(sc_c),
                          ctypes.byref(out_c), _ft_dtype(field.precision), ctypes.byref(prm),
                          wp, wn, ctypes.c_void_p(ws.stats.data_ptr()), stream)
         ev1.record()
@@ -536,7 +565,7 @@ def _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold):
     out = ws.take_output(src, _initial_capacity(src))
     trace_dev = torch.zeros(max_steps * _lib.STATS_BYTES, dtype=torch.uint8, device=device)
     control = torch.zeros(6, dtype=torch.int64, device=device)
-    lap_c = dl.lap_t[field.precision].ft_csc()
+    lap_c = dl.ft_csc(field.precision)
     prm = params.ft_params()
     stream = _stream_handle()
     lib = _lib.lib()
@@ -551,7 +580,7 @@ def _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold):
         remaining = max_steps - done
         s_c, a_c, b_c, o_c = cur.ft_csc(), wa.ft_tiled(), wb.ft_tiled(), out.ft_csc()
         ev0.record()
-        rc = lib.ft_evolve(ctypes.byref(lap_c), dl.flags, ctypes.byref(s_c), ctypes.byref(a_c),
+        rc = lib.ft_evolve(ctypes.byref(lap_c), dl.launch_flags(), ctypes.byref(s_c), ctypes.byref(a_c),
                            ctypes.byref(b_c), ctypes.byref(o_c), _ft_dtype(field.precision),
                            ctypes.byref(prm), remaining, float(tol), float(base_threshold),
                            wp, wn, ctypes.c_void_p(trace_dev.data_ptr()),
