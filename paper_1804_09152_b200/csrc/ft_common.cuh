@@ -39,6 +39,8 @@ struct Control {
 };
 static_assert(sizeof(Control) % 16 == 0, "Control must stay 16B aligned");
 
+#define FT_FIN_MAX 1024   // finalize CTAs at most (partials in the workspace)
+
 struct Workspace {
     Control*      ctl;
     double*       tile_bm;      // [num_tiles] per-tile base mass (fast path)
@@ -46,10 +48,10 @@ struct Workspace {
     unsigned int* slow_mask;    // [num_tiles * FT_WARPS] wide columns of each tile
     int*          slow_list;    // [2 n_v] tier-2 queue, then the tier-3 queue at +n_v
     long long*    chunk_off;    // [num_chunks + 2] compaction chunk offsets
-    double*       fin_part;     // [64] finalize partial sums (base mass)
-    double*       fin_maxd;     // [64] finalize partial maxima
-    long long*    fin_cnt;      // [64] finalize partial nnz
-    long long*    fin_skel;     // [64] finalize partial skeleton nnz
+    double*       fin_part;     // [FT_FIN_MAX] finalize partial sums (base mass)
+    double*       fin_maxd;     // [FT_FIN_MAX] finalize partial maxima
+    long long*    fin_cnt;      // [FT_FIN_MAX] finalize partial nnz
+    long long*    fin_skel;     // [FT_FIN_MAX] finalize partial skeleton nnz
     double*       tile_maxd;    // [num_tiles] per-tile max |delta| (fast path)
     int2*         tile_cs;      // [num_tiles] per-tile (nnz, skeleton nnz) (fast path)
     int           num_tiles;
@@ -63,7 +65,7 @@ inline size_t workspace_bytes(int n_v) {
     size_t t = (size_t)num_tiles_for(n_v), c = (size_t)num_chunks_for(n_v);
     const size_t v = (size_t)n_v;
     return sizeof(Control) + t * sizeof(double) + v * sizeof(double) + t * FT_WARPS * sizeof(unsigned int) +
-           2 * v * sizeof(int) + (c + 2) * sizeof(long long) + 4 * 64 * sizeof(double) +
+           2 * v * sizeof(int) + (c + 2) * sizeof(long long) + 4 * FT_FIN_MAX * sizeof(double) +
            t * (sizeof(double) + sizeof(int2)) + 1024;
 }
 
@@ -85,13 +87,13 @@ inline Workspace carve_workspace(void* base, int n_v) {
     w.chunk_off = (long long*)p;
     p += ((size_t)w.num_chunks + 2) * sizeof(long long);
     w.fin_part = (double*)p;
-    p += 64 * sizeof(double);
+    p += FT_FIN_MAX * sizeof(double);
     w.fin_maxd = (double*)p;
-    p += 64 * sizeof(double);
+    p += FT_FIN_MAX * sizeof(double);
     w.fin_cnt = (long long*)p;
-    p += 64 * sizeof(long long);
+    p += FT_FIN_MAX * sizeof(long long);
     w.fin_skel = (long long*)p;
-    p += 64 * sizeof(long long);
+    p += FT_FIN_MAX * sizeof(long long);
     w.tile_maxd = (double*)p;
     p += (size_t)w.num_tiles * sizeof(double);
     w.tile_cs = (int2*)p;

@@ -1171,7 +1171,7 @@ __device__ __forceinline__ long long pool_place(int cnt, const VRes& res, const 
 
 template <typename T, bool UNIFORM, bool IN_CANON>
 __global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p) {
-    constexpr int KW = 8;
+    constexpr int KW = 8;      // wider unions go to tier 3
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     const int n_wide = *(volatile int*)&p.ws.ctl->slow_count;
     const int lane = threadIdx.x & 31;
@@ -1255,8 +1255,7 @@ __global__ void __launch_bounds__(FT_TPB) deep_kernel(const StepParams p) {
 // per-CTA ranges, then the last CTA sums the partials in order), stats
 // record, error / convergence flags, accumulator reset.
 
-#define FT_FIN_CTAS 64
-#define FT_FIN_TPB 256
+#define FT_FIN_TPB 128
 
 __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizeParams f) {
     Control* ctl = f.ws.ctl;
@@ -1309,24 +1308,29 @@ __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizePara
         s_last = (atomicAdd(&ctl->fin_count, 1u) == gridDim.x - 1);
     }
     __syncthreads();
-    if (!s_last || tid >= 32) return;
+    if (!s_last) return;
     __threadfence();
-    // the last CTA combines the per-CTA partials with one warp: lane l owns
-    // partials l, l+32 (fixed order), then a fixed shuffle tree
+    // the last CTA combines the per-CTA partials: thread t owns partials t,
+    // t + FT_FIN_TPB, ... (fixed order), then fixed shuffle / warp trees
     double pb = 0.0, pm = 0.0;
     long long pc = 0, pk = 0;
-    for (int q = tid; q < (int)gridDim.x; q += 32) {
-        pb = pb + *(volatile double*)&f.ws.fin_part[q];
-        pm = fmax(pm, *(volatile double*)&f.ws.fin_maxd[q]);
-        pc += *(volatile long long*)&f.ws.fin_cnt[q];
-        pk += *(volatile long long*)&f.ws.fin_skel[q];
+    for (int q = tid; q < (int)gridDim.x; q += FT_FIN_TPB) {
+        pb = pb + __ldcg(&f.ws.fin_part[q]);
+        pm = fmax(pm, __ldcg(&f.ws.fin_maxd[q]));
+        pc += __ldcg(&f.ws.fin_cnt[q]);
+        pk += __ldcg(&f.ws.fin_skel[q]);
     }
     pb = warp_sum(pb);
     pc = warp_sum(pc);
     pk = warp_sum(pk);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pm = fmax(pm, __shfl_down_sync(0xffffffffu, pm, o));
+    __syncthreads();
+    if ((tid & 31) == 0) { s_part[tid >> 5] = pb; s_mx[tid >> 5] = pm; s_cnt[tid >> 5] = pc; s_skel[tid >> 5] = pk; }
+    __syncthreads();
     if (tid != 0) return;
+    pb = 0.0; pm = 0.0; pc = 0; pk = 0;
+    for (int q = 0; q < FT_FIN_TPB / 32; ++q) { pb = pb + s_part[q]; pm = fmax(pm, s_mx[q]); pc += s_cnt[q]; pk += s_skel[q]; }
     ctl->fin_count = 0u;
     const double bm = pb;
     const double mxd = fmax(pm, __longlong_as_double((long long)ctl->maxdelta_bits));
@@ -1632,6 +1636,7 @@ static int check_tiled(const ft_tiled* t, int n_rows, int n_cols, int n_own) {
 static int g_window = 0;
 static int g_tier1 = 3;     // tier-1 variant: 3 classified in place (default), 1 window passes, 2 compacted
 static int g_fixup_grid = 4 * 148;
+static int g_fin_ctas = 4 * 148;   // finalize: ~one tile per thread at C3, <= FT_FIN_MAX
 
 static int window_size() {
     if (g_window == 0) {
@@ -1648,6 +1653,7 @@ static int window_size() {
         if (cudaGetDevice(&dev) == cudaSuccess &&
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
             g_fixup_grid = 4 * sms;
+        g_fin_ctas = 4 * sms < FT_FIN_MAX ? 4 * sms : FT_FIN_MAX;
     }
     return g_window;
 }
@@ -1720,7 +1726,8 @@ static void launch_finalize(const ft::Workspace& ws, ft_step_stats* trace, long 
     ft::FinalizeParams f;
     f.ws = ws; f.trace = trace; f.tiled_cap = tiled_cap; f.fixed_slot = evolve ? 0 : 1;
     f.evolve = evolve; f.max_steps = max_steps; f.tol = tol; f.base_threshold = thr;
-    ft::finalize_kernel<<<FT_FIN_CTAS, FT_FIN_TPB, 0, s>>>(f);
+    window_size();
+    ft::finalize_kernel<<<g_fin_ctas, FT_FIN_TPB, 0, s>>>(f);
 }
 
 static int launch_compact(ft::CompactParams& c, int dtype, cudaStream_t s) {
