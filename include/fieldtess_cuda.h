@@ -276,6 +276,17 @@ int ft_domain_combine(const ft_step_stats* records, int32_t world, int32_t rank,
  * status OK (rewind after a capacity failure). */
 int ft_domain_control(void* workspace, int32_t set_steps, int64_t* out, void* stream);
 
+/* -- quality metrics ------------------------------------------------------ */
+/* Distance from every point (n_points x 3 doubles) to the closest point of
+ * the triangles (tri_a / tri_b / tri_c: n_tri x 3 doubles each, the
+ * corners): the O(samples x triangles) core of the sampled Hausdorff metric.
+ * Replaces _kernels.point_triangle_distances (_kernels.py:285-366) bitwise,
+ * including its 1e300 initial minimum.  scratch: n_points uint64 (device).
+ * All pointers device memory. */
+int ft_point_triangle_distances(const double* points, int32_t n_points, const double* tri_a,
+                                const double* tri_b, const double* tri_c, int32_t n_tri,
+                                uint64_t* scratch, double* out, void* stream);
+
 /* -- labels -------------------------------------------------------------- */
 /* Per-vertex argmax cell id; ties -> lowest cell; the base row wins only
  * if strictly greater -> -1 (UNCLAIMED).  Replaces field.sharp_labels

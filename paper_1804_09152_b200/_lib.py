@@ -92,7 +92,8 @@ EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
            "ft_step", "ft_step_kernel", "ft_step_fixup", "ft_step_finalize", "ft_compact",
            "ft_evolve", "ft_labels", "ft_faces_by_cell", "ft_lloyd_centroids",
            "ft_dual_products", "ft_domain_step", "ft_halo_bytes", "ft_halo_pack",
-           "ft_halo_unpack", "ft_domain_combine", "ft_domain_control", "ft_laplacian_pack")
+           "ft_halo_unpack", "ft_domain_combine", "ft_domain_control", "ft_laplacian_pack",
+           "ft_point_triangle_distances")
 
 _lib = None
 
@@ -161,6 +162,8 @@ def _declare(lib):
     lib.ft_domain_control.restype = ctypes.c_int
     lib.ft_laplacian_pack.argtypes = [P(FtCsc), i32, vp, vp, vp]
     lib.ft_laplacian_pack.restype = ctypes.c_int
+    lib.ft_point_triangle_distances.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, vp]
+    lib.ft_point_triangle_distances.restype = ctypes.c_int
 
 
 def lib():

@@ -21,8 +21,14 @@ seeds.json       sample_seed_vertices outputs (rng 0) for several meshes.
 meshes.json      SHA-256 digests of generator outputs (faces / positions /
                  L^T arrays) for icosphere 0..7 and a few tori.
 c1_dual.json     dual-mesh products on C1 after 500 steps (API path).
+seeds_collide.json  sample_seed_vertices with many collisions (small meshes,
+                 seed counts near n_vertices, several rng seeds).
+analysis.npz     analysis.py metrics: voronoi labels / margin masks (torus,
+                 icosphere), triangle qualities of a dual mesh, area
+                 histogram, directed surface distances and hausdorff.
 --big: c2_traj.npz (icosphere-7, 1024 seeds, steps 0/100/1000) and
        c2_lloyd.json (5 Lloyd iterations, max_steps 1000).
+--only a,b: regenerate only the named groups (seeds_collide, analysis).
 """
 
 import hashlib
@@ -297,7 +303,69 @@ def make_c2(seeds_c2):
     print("c2_lloyd", f"{time.time() - t0:.1f}s")
 
 
+def make_seed_collisions():
+    out = {}
+    for name, mesh, count, seed in [("t20x15", ft.gen_periodic_grid(20, 15), 280, 3),
+                                    ("ico2", ft.gen_icosphere(2), 160, 7),
+                                    ("ico3", ft.gen_icosphere(3), 500, 11),
+                                    ("t9x7s", ft.gen_periodic_grid(9, 7, 0.5), 60, 1)]:
+        out[name] = {"count": count, "rng": seed,
+                     "seeds": sample_seed_vertices(mesh, count, seed).tolist()}
+    with open(os.path.join(HERE, "seeds_collide.json"), "w") as fh:
+        json.dump(out, fh)
+
+
+def make_analysis():
+    from fieldtess import analysis as an
+    from fieldtess.dual import build_dual
+    out = {}
+    torus = ft.gen_periodic_grid(20, 15)
+    rng = np.random.default_rng(5)
+    spos = torus.positions[rng.choice(torus.n_vertices, 9, replace=False)] + 0.1
+    out["tor_spos"] = spos
+    out["tor_labels"] = an.euclidean_voronoi_labels(torus, spos)
+    out["tor_margin"] = an.margin_mask(torus, spos, "euclidean")
+    ico = ft.gen_icosphere(3)
+    sv = rng.choice(ico.n_vertices, 12, replace=False)
+    out["ico_seeds"] = sv
+    out["ico_labels"] = an.sphere_voronoi_labels(ico, sv)
+    out["ico_margin"] = an.margin_mask(ico, sv, "sphere", factor=1.5)
+    # dual of an icosphere-3 field with 24 seeds after 200 steps
+    seeds = sample_seed_vertices(ico, 24, 2)
+    fld, _ = ft.evolve(ft.init_field(ico, seeds), ft.build_laplacian(ico), ft.CouplingParams(),
+                       max_steps=200)
+    from fieldtess import dual as dualmod
+    a_v = dualmod.vertex_adjacency(fld, 0.25)
+    a_t = dualmod.triangle_adjacency(fld, ico, 0.25)
+    cur = dualmod.confirm_candidates(fld, ico, a_v, a_t, 0.25)
+    dual = build_dual(cur, ico.positions[seeds])
+    q, ang = an.triangle_qualities(dual.positions, dual.triangles)
+    out["dual_seeds"] = seeds
+    out["dual_positions"] = np.asarray(dual.positions)
+    out["dual_triangles"] = np.asarray(dual.triangles)
+    out["dual_q"] = q
+    out["dual_angles"] = ang
+    rep = an.triangle_quality(dual)
+    out["dual_report"] = np.array([rep.mean_quality, rep.min_quality, rep.mean_min_angle,
+                                   rep.min_angle, rep.pct_below_30, rep.n_triangles,
+                                   rep.n_degenerate], dtype=np.float64)
+    areas = rng.random(50) * 3
+    cnt, edges = an.cell_area_histogram(areas)
+    out["hist_areas"], out["hist_counts"], out["hist_edges"] = areas, cnt, edges
+    ico4 = ft.gen_icosphere(4)
+    out["d_ab"] = an.directed_surface_distance(ico, ico4, 2000, 0)
+    out["d_ba"] = an.directed_surface_distance(ico4, ico, 2000, 1)
+    out["hausdorff_ico"] = np.array(an.hausdorff(ico, ico4, 2000, 0))
+    t2 = ft.gen_periodic_grid(21, 16)
+    out["d_tor"] = an.directed_surface_distance(torus, t2, 1500, 4)
+    np.savez_compressed(os.path.join(HERE, "analysis.npz"), **out)
+
+
 def main():
+    if "--only" in sys.argv:
+        for name in sys.argv[sys.argv.index("--only") + 1].split(","):
+            {"seeds_collide": make_seed_collisions, "analysis": make_analysis}[name]()
+        return
     make_step_cases()
     make_labels_cases()
     seeds = make_seeds_and_meshes()
@@ -311,6 +379,8 @@ def main():
                       os.path.join(HERE, "torus_traj.npz"), 300)
     geo.update(make_cell_geometry("torus", torus, tfld))
     np.savez_compressed(os.path.join(HERE, "cell_geometry.npz"), **geo)
+    make_seed_collisions()
+    make_analysis()
     if "--big" in sys.argv:
         mesh = ft.gen_icosphere(7)
         seeds_c2 = sample_seed_vertices(mesh, 1024, 0)
