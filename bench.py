@@ -305,9 +305,9 @@ def run_ours(args):
         evk[k][0].record(stream)
         rc = lib.ft_step_kernel(ctypes.byref(lap_c), dl.launch_flags(), canon, tiled, ctypes.byref(dst), dt_code,
                                 ctypes.byref(prm), wp, wn, sh)
-        evk[k][1].record(stream)
         rc |= lib.ft_step_fixup(ctypes.byref(lap_c), dl.launch_flags(), canon, tiled, ctypes.byref(dst), dt_code,
                                 ctypes.byref(prm), wp, wn, sh)
+        evk[k][1].record(stream)
         rc |= lib.ft_step_finalize(wp, wn, n_v, dst.capacity,
                                    ctypes.c_void_p(trace.data_ptr() + k * _lib.STATS_BYTES), sh)
         if rc:
@@ -422,13 +422,14 @@ def run_ours(args):
             "kernel_ms_per_step": float(kern_ms.mean()),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "ft::step_kernel (fused SpGEMM+skeleton+update+normalise)",
+                         "kernel": "the step's column kernels: tier 1 (classify + single-row closed form), "
+                                   "tier 1.5 (two-row update), tiers 2/3 (wide columns); finalize excluded",
                          "bytes_per_launch": float(alg.mean()), "peak_source": peak_src,
                          "lap_layout": lap_bytes_note},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk,
-            "gpu_launches": 4 * K + 3,
+            "gpu_launches": 5 * K + 3,   # tiers 1, 1.5, 2, 3 + finalize per step; compaction
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -562,10 +563,10 @@ def run_partitioned(args, world, rank, local, emulate=0):
             "cpu_baseline": None,
             "e2e": e2e,
             "clocks": clk,
-            # per step and rank: tiers 1-3 + finalize, one pack per peer sent to,
+            # per step and rank: tiers 1, 1.5, 2, 3 + finalize, one pack per peer sent to,
             # the combine, one unpack per peer received from; one control
             # snapshot per 16-step chunk
-            "gpu_launches": (5 + len(r0.send_msg) + len(r0.recv_msg)) * K + -(-K // 16),
+            "gpu_launches": (6 + len(r0.send_msg) + len(r0.recv_msg)) * K + -(-K // 16),
         }
         if emulate:
             line["emulated"] = True

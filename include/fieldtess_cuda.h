@@ -67,6 +67,9 @@ extern "C" {
                               packed neighbour table of ft_laplacian_pack (the
                               uniform values are never read, so the slot
                               carries the table); col_ptr / row_idx stay valid */
+#define FT_LAP_CHECK_FINITE 4  /* tiled input of unknown origin: check its
+                              values for NaN / Inf (automatic for canonical
+                              input and after any non-finite output)        */
 
 /* status codes written into ft_step_stats.status / evolve control[1] */
 #define FT_STATUS_OK           0

@@ -25,6 +25,7 @@ FT_F32 = 1
 FT_LAP_EXPLICIT = 0
 FT_LAP_UNIFORM = 1
 FT_LAP_PACKED = 2
+FT_LAP_CHECK_FINITE = 4
 
 FT_STATUS_OK = 0
 FT_STATUS_NAN = 1

@@ -28,12 +28,12 @@ struct Control {
     int                overflow;       // a tile did not fit the work buffer
     int                slow_count;     // wide columns queued for tier 2
     unsigned int       fin_count;      // finalize: CTAs done (last-block pattern)
-    int                deep_count;     // tier-3 columns (stored at the tail of slow_list)
-    int                pad3;
+    int                deep_count;     // tier-3 columns (slow_list + n_v)
+    int                gen_count;      // tier-1.5 columns (slow_list + 2 n_v)
     int                done;           // evolve: stop flag (finalize sets it)
     int                steps_done;     // evolve: completed steps
     int                status;         // evolve: final status
-    int                pad0;
+    unsigned int       nonfinite;      // sticky: a kernel wrote a non-finite value
     long long          needed;         // capacity needed on overflow
     long long          pad1[4];
 };
@@ -46,7 +46,7 @@ struct Workspace {
     double*       tile_bm;      // [num_tiles] per-tile base mass (fast path)
     double*       vbm;          // [n_v] base mass of wide columns (tier 2)
     unsigned int* slow_mask;    // [num_tiles * FT_WARPS] wide columns of each tile
-    int*          slow_list;    // [2 n_v] tier-2 queue, then the tier-3 queue at +n_v
+    int*          slow_list;    // [3 n_v] tier-2 queue, tier-3 queue at +n_v, tier-1.5 queue at +2 n_v
     long long*    chunk_off;    // [num_chunks + 2] compaction chunk offsets
     double*       fin_part;     // [FT_FIN_MAX] finalize partial sums (base mass)
     double*       fin_maxd;     // [FT_FIN_MAX] finalize partial maxima
@@ -54,6 +54,7 @@ struct Workspace {
     long long*    fin_skel;     // [FT_FIN_MAX] finalize partial skeleton nnz
     double*       tile_maxd;    // [num_tiles] per-tile max |delta| (fast path)
     int2*         tile_cs;      // [num_tiles] per-tile (nnz, skeleton nnz) (fast path)
+    int*          tile_gen;     // [num_tiles] tier-1.5 columns of the tile (list at slow_list + 2 n_v + 128 t)
     int           num_tiles;
     int           num_chunks;
 };
@@ -65,7 +66,7 @@ inline size_t workspace_bytes(int n_v) {
     size_t t = (size_t)num_tiles_for(n_v), c = (size_t)num_chunks_for(n_v);
     const size_t v = (size_t)n_v;
     return sizeof(Control) + t * sizeof(double) + v * sizeof(double) + t * FT_WARPS * sizeof(unsigned int) +
-           2 * v * sizeof(int) + (c + 2) * sizeof(long long) + 4 * FT_FIN_MAX * sizeof(double) +
+           (3 * v + FT_TPB) * sizeof(int) + t * sizeof(int) + (c + 2) * sizeof(long long) + 4 * FT_FIN_MAX * sizeof(double) +
            t * (sizeof(double) + sizeof(int2)) + 1024;
 }
 
@@ -98,11 +99,13 @@ inline Workspace carve_workspace(void* base, int n_v) {
     p += (size_t)w.num_tiles * sizeof(double);
     w.tile_cs = (int2*)p;
     p += (size_t)w.num_tiles * sizeof(int2);
+    w.tile_gen = (int*)p;
+    p += (size_t)w.num_tiles * sizeof(int);
     p = align16(p);
     w.slow_mask = (unsigned int*)p;
     p += (size_t)w.num_tiles * FT_WARPS * sizeof(unsigned int);
     w.slow_list = (int*)p;
-    p += 2 * (size_t)n_v * sizeof(int);
+    p += (3 * (size_t)n_v + FT_TPB) * sizeof(int);
     return w;
 }
 

@@ -30,7 +30,7 @@ struct HaloParams {
     long long region;    // unpack: first entry of the halo region
     ft_step_stats* record;
     int* need;
-    const Control* ctl;
+    Control* ctl;
     int force;
 };
 
@@ -69,10 +69,14 @@ __global__ void __launch_bounds__(256) halo_unpack_kernel(const HaloParams h) {
     const size_t o = (size_t)i * h.slots;
     T* v = (T*)h.val;
     const T* mv = (const T*)h.m_vals;
+    bool nf = false;
     for (int t = 0; t < c && t < h.slots; ++t) {
         h.idx[off + t] = h.m_rows[o + t];
         v[off + t] = mv[o + t];
+        nf |= !isfinite((double)mv[o + t]);
     }
+    // a peer's non-finite value: this rank's next step checks its inputs
+    if (nf) atomicOr(&h.ctl->nonfinite, 1u);
 }
 
 __device__ __forceinline__ int failure_rank(int status) {
@@ -155,7 +159,7 @@ static bool fill_halo(HaloParams& h, const ft_tiled* t, const int32_t* cols, int
     h.m_vals = m + ((4LL * n * (1 + slots) + 7) & ~7LL);   // 8-byte aligned values block
     h.region = 0;
     h.record = nullptr; h.need = nullptr;
-    h.ctl = (const Control*)workspace;    // the control block leads the workspace
+    h.ctl = (Control*)workspace;          // the control block leads the workspace
     h.force = flags & FT_HALO_FORCE;
     return true;
 }

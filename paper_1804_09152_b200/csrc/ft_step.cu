@@ -63,6 +63,7 @@ struct StepParams {
     Workspace ws;
     int check_done;
     int finite;          // all couplings finite: enables the single-row closed form
+    int force_check;     // FT_LAP_CHECK_FINITE: check tiled input values for NaN / Inf
 };
 
 struct FinalizeParams {
@@ -390,6 +391,80 @@ __device__ __forceinline__ void process_window(Win<K>& w, const StepParams& p, V
     }
 }
 
+// process_window<2> as straight-line code for a window of one or two rows
+// (the tier-1 general path): the same operations in the same order, so the
+// result is bitwise identical; no loops, masks or warp votes.
+__device__ __forceinline__ void process_two(Win<2>& w, const StepParams& p, VRes& res, unsigned int& out_mask) {
+    const bool h1 = w.m > 1;
+    const double ph0 = w.phi[0], lm0 = w.lam[0];
+    const double ph1 = h1 ? w.phi[1] : 0.0, lm1 = h1 ? w.lam[1] : 0.0;
+    const bool in0 = in_skeleton(ph0, lm0);
+    const bool in1 = h1 && in_skeleton(ph1, lm1);
+    res.bad_phi_row = -1;
+    res.bad_lt_row = -1;
+    if (ph0 != 0.0 && !in0) res.bad_phi_row = w.rows[0];
+    if (lm0 != 0.0 && !in0) res.bad_lt_row = w.rows[0];
+    if (h1 && ph1 != 0.0 && !in1) res.bad_phi_row = w.rows[1];
+    if (h1 && lm1 != 0.0 && !in1) res.bad_lt_row = w.rows[1];
+    const int n = (int)in0 + (int)in1;
+    res.nskel = n;
+    out_mask = 0;
+    if (n == 0) return;
+    if (n == 1) {
+        const double ph = in0 ? ph0 : ph1, lm = in0 ? lm0 : lm1;
+        if (p.finite && isfinite(ph) && isfinite(lm)) {      // single-row closed form
+            double v = ph;
+            if (v > 1.0) v = 1.0;
+            else if (v <= 0.0) v = 0.0;
+            const double s = 0.0 + v;
+            const double nv = s > 0.0 ? v * (1.0 / s) : v;
+            const int slot = in0 ? 0 : 1;
+            if (nv != 0.0) {
+                res.cnt = 1;
+                out_mask = 1u << slot;
+                if (w.rows[slot] == 0) res.bm = nv;
+            }
+            const double dd = fabs(nv - ph);
+            if (dd > res.maxd) res.maxd = dd;
+            w.lam[slot] = nv;
+            return;
+        }
+    }
+    // aggregates over the skeleton rows in row order (Appendix A)
+    const double sq0 = in0 ? sqrt(ph0) : 0.0;
+    const double sq1 = in1 ? sqrt(ph1) : 0.0;
+    const double lh0 = (lm0 != 0.0) ? lm0 : 0.0;
+    const double lh1 = (lm1 != 0.0) ? lm1 : 0.0;
+    Agg g;
+    agg_init(g);
+    if (in0) { g.first_row = w.rows[0]; g.phi0 = ph0; g.n = 1; g.sl = g.sl + lh0; g.sp = g.sp + ph0; g.sr = g.sr + sq0; }
+    if (in1) {
+        if (!in0) { g.first_row = w.rows[1]; g.phi0 = ph1; }
+        g.n += 1;
+        g.sl = g.sl + lh1; g.sp = g.sp + ph1; g.sr = g.sr + sq1;
+    }
+    const Coef c = make_coef(g, p, c_recip);
+    double v0 = 0.0, v1 = 0.0, s = 0.0;
+    if (in0) { v0 = update_entry_sq(w.rows[0], ph0, lh0, sq0, c, p, res.nan); s = s + v0; }
+    if (in1) { v1 = update_entry_sq(w.rows[1], ph1, lh1, sq1, c, p, res.nan); s = s + v1; }
+    const bool spos = s > 0.0;
+    const double inv = spos ? 1.0 / s : 0.0;
+    if (in0) {
+        const double nv = spos ? v0 * inv : v0;
+        if (nv != 0.0) { res.cnt++; out_mask |= 1u; if (w.rows[0] == 0) res.bm = res.bm + nv; }
+        const double dd = fabs(nv - ph0);
+        if (dd > res.maxd) res.maxd = dd;
+        w.lam[0] = nv;
+    }
+    if (in1) {
+        const double nv = spos ? v1 * inv : v1;
+        if (nv != 0.0) { res.cnt++; out_mask |= 2u; if (w.rows[1] == 0) res.bm = res.bm + nv; }
+        const double dd = fabs(nv - ph1);
+        if (dd > res.maxd) res.maxd = dd;
+        w.lam[1] = nv;
+    }
+}
+
 __device__ __forceinline__ void report_flags(const VRes& res, int j, const StepParams& p) {
     if (res.nan) atomicMax(&p.ws.ctl->nan_key, (unsigned int)(INT_MAX - j));
     if (res.bad_phi_row >= 0)
@@ -398,18 +473,23 @@ __device__ __forceinline__ void report_flags(const VRes& res, int j, const StepP
         atomicMax(&p.ws.ctl->bad_lt_key, ~(((unsigned long long)j << 32) | (unsigned int)res.bad_lt_row));
 }
 
+// writes the flagged window slots; a non-finite output value raises the
+// sticky nonfinite flag (tier 1 then checks its inputs' values)
 template <typename T, int K>
 __device__ __forceinline__ void emit_window(const Win<K>& w, unsigned int out_mask, long long off,
                                             const StepParams& p) {
     T* ov = (T*)p.out_val;
+    bool nf = false;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         if (out_mask & (1u << i)) {
             p.out_idx[off] = w.rows[i];
             ov[off] = (T)w.lam[i];
+            nf |= !isfinite(w.lam[i]);
             ++off;
         }
     }
+    if (nf) atomicOr(&p.ws.ctl->nonfinite, 1u);
 }
 
 // --- slow path: union larger than K, processed in ascending row windows ----
@@ -461,6 +541,7 @@ __device__ __noinline__ void vertex_slow(int j, const StepParams& p, VRes& res, 
                     p.out_idx[emit_off] = w.rows[i];
                     ov[emit_off] = (T)nv;
                     ++emit_off;
+                    if (!isfinite(nv)) atomicOr(&p.ws.ctl->nonfinite, 1u);
                 }
                 res.cnt++;
                 if (w.rows[i] == 0) res.bm = res.bm + nv;
@@ -820,13 +901,20 @@ __global__ void __launch_bounds__(FT_TPB, 6) step_kernel3(const StepParams p) {
     }
     if (wide) vres_init(res);
 
+    // tier-2 queue: one atomic per CTA
+    __shared__ int s_wq[FT_WARPS + 1];
     const unsigned int wbits = __ballot_sync(0xffffffffu, wide && active);
-    if (wbits) {
-        int qb = 0;
-        if (lane == 0) qb = atomicAdd(&p.ws.ctl->slow_count, __popc(wbits));
-        qb = __shfl_sync(0xffffffffu, qb, 0);
-        if (wide && active) p.ws.slow_list[qb + __popc(wbits & ((1u << lane) - 1u))] = j;
+    if (lane == 0) s_wq[warp] = __popc(wbits);
+    __syncthreads();
+    int wpre = 0, wtot = 0;
+#pragma unroll
+    for (int q = 0; q < FT_WARPS; ++q) {
+        if (q < warp) wpre += s_wq[q];
+        wtot += s_wq[q];
     }
+    if (tid == 0) s_wq[FT_WARPS] = wtot ? atomicAdd(&p.ws.ctl->slow_count, wtot) : 0;
+    __syncthreads();
+    if (wide && active) p.ws.slow_list[s_wq[FT_WARPS] + wpre + __popc(wbits & ((1u << lane) - 1u))] = j;
     if (lane == 0) p.ws.slow_mask[(size_t)tile * FT_WARPS + warp] = wbits;
     const TileOut o = tile_epilogue<false>(res.cnt, res.nskel, res.bm, res.maxd, tile, &p.ws.tile_bm[tile], p,
                                            s_scan, s_wbm, s_wmax, s_wskel, &s_base);
@@ -834,6 +922,136 @@ __global__ void __launch_bounds__(FT_TPB, 6) step_kernel3(const StepParams p) {
     const long long off = o.base + o.local_off;
     p.out_desc[j] = make_int2((int)off, res.cnt);
     if (out_mask) emit_window<T, 2>(w, out_mask, off, p);
+}
+
+// ---------------------------------------------------------------------------
+// tier 1, split (default): classification and the closed form only.
+//
+// A column whose neighbourhood is one layer row (every non-empty neighbour
+// holds one entry, of the column's own row; its phi > 0) is finished here
+// with the exact single-row closed form.  Everything else is queued: up to
+// two entries per neighbour for tier 1.5 (gen_kernel, the one-pass two-row
+// update on dense warps), more for tier 2.  So no warp runs the general
+// update for a few of its lanes.  The neighbours' VALUES are not read: the
+// closed form needs them only through the finiteness of Lt, and values this
+// library wrote are finite unless a kernel raised the sticky nonfinite flag
+// (the canonical input, FT_LAP_CHECK_FINITE and a raised flag switch the
+// check on).
+
+template <typename T, bool UNIFORM, bool IN_CANON, bool PACKED>
+__global__ void __launch_bounds__(FT_TPB, 8) step_kernel6(const StepParams p) {
+    __shared__ double s_wbm[FT_WARPS];
+    __shared__ double s_wmax[FT_WARPS];
+    __shared__ int s_wskel[FT_WARPS];
+    __shared__ int s_scan[FT_WARPS];
+    __shared__ long long s_base;
+
+    if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
+    const bool chk = IN_CANON || p.force_check || *(volatile unsigned int*)&p.ws.ctl->nonfinite;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tile = blockIdx.x;
+    const int jl = tile * FT_TPB + tid;
+    const int j = p.j_base + jl;
+    const bool active = jl < p.n_v;
+
+    int q0 = 0;
+    int u[kMD];
+    const int n = load_lrow<PACKED>(p, jl, j, active, u, q0);
+    bool wide = active && n == 0;
+    int2 d[kMD];
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
+    int kd = -1;
+    bool multi = false;
+    int2 dself = make_int2(0, 0);
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) {
+        if (u[k] == j) { kd = k; dself = d[k]; }
+        wide |= d[k].y > 2;
+        multi |= d[k].y > 1;
+    }
+    if (active && kd < 0) wide = true;
+    bool cand = active && !wide && !multi && p.finite && dself.y == 1;
+    int rs = INT_MAX;
+    double phs = 0.0;
+    if (cand) {
+        rs = __ldg(&p.in_idx[dself.x]);
+        phs = ldv<T>(p.in_val, dself.x);
+    }
+    bool same = true;
+#pragma unroll
+    for (int k = 0; k < kMD; ++k)
+        if (cand && d[k].y == 1 && k != kd) same &= __ldg(&p.in_idx[d[k].x]) == rs;
+    cand = cand && same && phs > 0.0;
+    if (chk && cand) {
+        bool fin = true;
+        double lam = 0.0;
+        const double invdeg = UNIFORM ? (n - 1 <= 32 ? c_recip[n - 1] : 1.0 / (double)(n - 1)) : 0.0;
+#pragma unroll
+        for (int k = 0; k < kMD; ++k) {
+            if (d[k].y == 1) {
+                const double v = ldv<T>(p.in_val, d[k].x);
+                fin &= isfinite(v);
+                const double l = UNIFORM ? ((k == kd) ? -1.0 : invdeg) : ldv<T>(p.lap_val, q0 + k);
+                lam = lam + v * l;
+            }
+        }
+        cand = fin && isfinite(lam);
+    }
+    const bool fast = cand;
+    const bool gen = active && !wide && !fast;
+
+    VRes res;
+    vres_init(res);
+    double nv = 0.0;
+    if (fast) {
+        double v = phs;
+        if (v > 1.0) v = 1.0;
+        const double s = 0.0 + v;
+        nv = v * (1.0 / s);
+        res.nskel = 1;
+        if (nv != 0.0) {
+            res.cnt = 1;
+            if (rs == 0) res.bm = nv;
+        }
+        res.maxd = fabs(nv - phs);
+    }
+    // queues without hot atomics: tier 1.5 (gen) columns into this tile's
+    // list (slow_list + 2 n_v + 128 tile, count tile_gen[tile]); tier 2
+    // (wide) columns into the global queue with one atomic per CTA
+    __shared__ int s_gq[FT_WARPS], s_wq[FT_WARPS + 1];
+    const unsigned int gbits = __ballot_sync(0xffffffffu, gen);
+    const unsigned int wbits = __ballot_sync(0xffffffffu, wide && active);
+    if (lane == 0) { s_gq[warp] = __popc(gbits); s_wq[warp] = __popc(wbits); }
+    __syncthreads();
+    int gpre = 0, wpre = 0, gtot = 0, wtot = 0;
+#pragma unroll
+    for (int q = 0; q < FT_WARPS; ++q) {
+        if (q < warp) { gpre += s_gq[q]; wpre += s_wq[q]; }
+        gtot += s_gq[q];
+        wtot += s_wq[q];
+    }
+    if (tid == 0) {
+        p.ws.tile_gen[tile] = gtot;
+        s_wq[FT_WARPS] = wtot ? atomicAdd(&p.ws.ctl->slow_count, wtot) : 0;
+    }
+    if (gen)
+        p.ws.slow_list[2 * p.n_v + tile * FT_TPB + gpre + __popc(gbits & ((1u << lane) - 1u))] = j;
+    __syncthreads();
+    if (wide && active) p.ws.slow_list[s_wq[FT_WARPS] + wpre + __popc(wbits & ((1u << lane) - 1u))] = j;
+    // tier-2 columns report their base mass through vbm (finalize, by mask);
+    // tier 1.5 adds its columns' base mass to tile_bm in a fixed order
+    if (lane == 0) p.ws.slow_mask[(size_t)tile * FT_WARPS + warp] = wbits;
+    const TileOut o = tile_epilogue<false>(res.cnt, res.nskel, res.bm, res.maxd, tile, &p.ws.tile_bm[tile], p,
+                                           s_scan, s_wbm, s_wmax, s_wskel, &s_base);
+    if (!fast || o.base < 0) return;
+    const long long off = o.base + o.local_off;
+    p.out_desc[j] = make_int2((int)off, res.cnt);
+    if (res.cnt) {
+        p.out_idx[off] = rs;
+        ((T*)p.out_val)[off] = (T)nv;
+        if (!isfinite(nv)) atomicOr(&p.ws.ctl->nonfinite, 1u);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1169,6 +1387,148 @@ __device__ __forceinline__ long long pool_place(int cnt, const VRes& res, const 
     return base;
 }
 
+// tier 1.5: the general columns (at most two entries per neighbour) that
+// tier 1 listed per tile, one warp per tile with the columns on its lanes:
+// the one-pass two-row update.  More than two rows -> tier 2.  Outputs go
+// right after the tile's tier-1 entries in its slot (the pool if they do
+// not fit), statistics into the tile's slots and vbm -- no hot atomics.
+template <typename T, bool UNIFORM, bool IN_CANON, bool PACKED>
+__global__ void __launch_bounds__(FT_TPB, 6) gen_kernel(const StepParams p) {
+    if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
+    const int lane = threadIdx.x & 31;
+    const int nwarps = gridDim.x * FT_WARPS;
+    for (int t = (blockIdx.x * FT_TPB + threadIdx.x) >> 5; t < p.num_tiles; t += nwarps) {
+        const int ng = p.ws.tile_gen[t];
+        if (ng == 0) continue;
+        const int2 cs = p.ws.tile_cs[t];
+        const bool in_slot = cs.x <= FT_SLOT;     // tier 1 placed the tile in its slot
+        int used = cs.x;
+        double tmx = 0.0, tbm = 0.0;
+        int tcnt = 0, tskel = 0;
+        for (int c0 = 0; c0 < ng; c0 += 32) {
+            const bool mine = c0 + lane < ng;
+            const int j = mine ? p.ws.slow_list[2 * p.n_v + t * FT_TPB + c0 + lane] : p.j_base;
+            const int jl = j - p.j_base;
+            int q0 = 0;
+            int u[kMD];
+            const int n = load_lrow<PACKED>(p, jl, j, mine, u, q0);
+            int2 d[kMD];
+#pragma unroll
+            for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
+            int kd = -1;
+#pragma unroll
+            for (int k = 0; k < kMD; ++k)
+                if (u[k] == j) kd = k;
+            int r0[kMD], r1[kMD];
+            T v0[kMD], v1[kMD];
+#pragma unroll
+            for (int k = 0; k < kMD; ++k) {
+                r0[k] = INT_MAX; r1[k] = INT_MAX; v0[k] = (T)0; v1[k] = (T)0;
+                if (d[k].y > 0) { r0[k] = __ldg(&p.in_idx[d[k].x]); v0[k] = __ldg(((const T*)p.in_val) + d[k].x); }
+                if (d[k].y > 1) { r1[k] = __ldg(&p.in_idx[d[k].x + 1]); v1[k] = __ldg(((const T*)p.in_val) + d[k].x + 1); }
+            }
+            int rlo = INT_MAX, rhi = -1;
+#pragma unroll
+            for (int k = 0; k < kMD; ++k) {
+                if (r0[k] != INT_MAX) { rlo = min(rlo, r0[k]); rhi = max(rhi, r0[k]); }
+                if (r1[k] != INT_MAX) { rlo = min(rlo, r1[k]); rhi = max(rhi, r1[k]); }
+            }
+            const double invdeg = UNIFORM ? (n - 1 <= 32 ? c_recip[n - 1] : 1.0 / (double)(n - 1)) : 0.0;
+            double l0 = 0.0, l1 = 0.0, p0 = 0.0, p1 = 0.0;
+            bool more = false;
+#pragma unroll
+            for (int k = 0; k < kMD; ++k) {
+                const double l = UNIFORM ? ((k == kd) ? -1.0 : invdeg)
+                                         : ((k < n) ? ldv<T>(p.lap_val, q0 + k) : 0.0);
+                const double a0 = (double)v0[k], a1 = (double)v1[k];
+                if (r0[k] == rlo) { l0 = l0 + a0 * l; if (k == kd) p0 = a0; }
+                else if (r0[k] == rhi) { l1 = l1 + a0 * l; if (k == kd) p1 = a0; }
+                else if (r0[k] != INT_MAX) more = true;
+                if (r1[k] == rlo) { l0 = l0 + a1 * l; if (k == kd) p0 = a1; }
+                else if (r1[k] == rhi) { l1 = l1 + a1 * l; if (k == kd) p1 = a1; }
+                else if (r1[k] != INT_MAX) more = true;
+            }
+            const bool wide = mine && (more || rlo == INT_MAX);
+            Win<2> w;
+            w.rows[0] = rlo; w.lam[0] = l0; w.phi[0] = p0;
+            w.rows[1] = rhi; w.lam[1] = l1; w.phi[1] = p1;
+            w.m = (rhi == rlo) ? 1 : 2;
+            if (w.m == 1) { w.rows[1] = INT_MAX; w.lam[1] = 0.0; w.phi[1] = 0.0; }
+            VRes res;
+            vres_init(res);
+            unsigned int out_mask = 0;
+            if (mine && !wide) {
+                process_two(w, p, res, out_mask);
+                report_flags(res, j, p);
+            }
+            const unsigned int wb = __ballot_sync(0xffffffffu, wide);
+            if (wb) {
+                int qb = 0;
+                if (lane == 0) qb = atomicAdd(&p.ws.ctl->slow_count, __popc(wb));
+                qb = __shfl_sync(0xffffffffu, qb, 0);
+                if (wide) {
+                    p.ws.slow_list[qb + __popc(wb & ((1u << lane) - 1u))] = j;
+                    // tier 2 reports this column's base mass through vbm
+                    const int lt = jl - t * FT_TPB;
+                    atomicOr(&p.ws.slow_mask[(size_t)t * FT_WARPS + (lt >> 5)], 1u << (lt & 31));
+                }
+            }
+            // placement: the tile slot after its entries, else the pool
+            const int cnt = (mine && !wide) ? res.cnt : 0;
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int wsum = __shfl_sync(0xffffffffu, incl, 31);
+            long long base;
+            if (in_slot && used + wsum <= FT_SLOT) {
+                base = (long long)t * FT_SLOT + used;
+                used += wsum;
+            } else {
+                base = 0;
+                if (lane == 31 && wsum > 0)
+                    base = (long long)p.num_tiles * FT_SLOT +
+                           (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)wsum);
+                base = __shfl_sync(0xffffffffu, base, 31);
+                if (base + wsum > p.cap) {
+                    if (lane == 0) atomicExch(&p.ws.ctl->overflow, 1);
+                    base = -1;
+                }
+            }
+            // base mass of the chunk, lane order (the tile's gen list is in
+            // vertex order): a fixed order, so the total is deterministic
+            double cbm = (mine && !wide) ? res.bm : 0.0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_down_sync(0xffffffffu, cbm, o);
+                if ((lane & (2 * o - 1)) == 0) cbm = cbm + y;
+            }
+            tbm = tbm + __shfl_sync(0xffffffffu, cbm, 0);
+            if (mine && !wide) {
+                if (base >= 0) {
+                    const long long off = base + incl - cnt;
+                    p.out_desc[j] = make_int2((int)off, res.cnt);
+                    if (out_mask) emit_window<T, 2>(w, out_mask, off, p);
+                }
+            }
+            tmx = fmax(tmx, res.maxd);
+            tcnt += cnt;
+            tskel += (mine && !wide) ? res.nskel : 0;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tmx = fmax(tmx, __shfl_down_sync(0xffffffffu, tmx, o));
+        tcnt = warp_sum(tcnt);
+        tskel = warp_sum(tskel);
+        if (lane == 0) {
+            p.ws.tile_maxd[t] = fmax(p.ws.tile_maxd[t], tmx);
+            p.ws.tile_cs[t] = make_int2(cs.x + tcnt, cs.y + tskel);
+            p.ws.tile_bm[t] = p.ws.tile_bm[t] + tbm;
+        }
+    }
+}
+
 template <typename T, bool UNIFORM, bool IN_CANON>
 __global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p) {
     constexpr int KW = 8;      // wider unions go to tier 3
@@ -1373,6 +1733,7 @@ __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizePara
     ctl->overflow = 0;
     ctl->slow_count = 0;
     ctl->deep_count = 0;
+    ctl->gen_count = 0;
     if (f.evolve) {
         if (status != FT_STATUS_OK) {
             ctl->done = 1;
@@ -1515,6 +1876,7 @@ __global__ void __launch_bounds__(FT_CTPB) compact_copy_kernel(const CompactPara
 }
 
 __global__ void evolve_reset_kernel(Control* ctl) {
+    ctl->nonfinite = 0u;    // step 0 reads the canonical input with full checks
     ctl->done = 0;
     ctl->steps_done = 0;
     ctl->status = FT_STATUS_OK;
@@ -1542,6 +1904,28 @@ static StepKernelFn pick_step_v1(int dtype, bool uniform, bool in_canon, bool pa
     if (uniform && packed) return in_canon ? step_kernel<float, K, true, true, true> : step_kernel<float, K, true, false, true>;
     if (uniform) return in_canon ? step_kernel<float, K, true, true, false> : step_kernel<float, K, true, false, false>;
     return in_canon ? step_kernel<float, K, false, true, false> : step_kernel<float, K, false, false, false>;
+}
+
+static StepKernelFn pick_step_v6(int dtype, bool uniform, bool in_canon, bool packed) {
+    if (dtype == FT_F64) {
+        if (uniform && packed) return in_canon ? step_kernel6<double, true, true, true> : step_kernel6<double, true, false, true>;
+        if (uniform) return in_canon ? step_kernel6<double, true, true, false> : step_kernel6<double, true, false, false>;
+        return in_canon ? step_kernel6<double, false, true, false> : step_kernel6<double, false, false, false>;
+    }
+    if (uniform && packed) return in_canon ? step_kernel6<float, true, true, true> : step_kernel6<float, true, false, true>;
+    if (uniform) return in_canon ? step_kernel6<float, true, true, false> : step_kernel6<float, true, false, false>;
+    return in_canon ? step_kernel6<float, false, true, false> : step_kernel6<float, false, false, false>;
+}
+
+static StepKernelFn pick_gen(int dtype, bool uniform, bool in_canon, bool packed) {
+    if (dtype == FT_F64) {
+        if (uniform && packed) return in_canon ? gen_kernel<double, true, true, true> : gen_kernel<double, true, false, true>;
+        if (uniform) return in_canon ? gen_kernel<double, true, true, false> : gen_kernel<double, true, false, false>;
+        return in_canon ? gen_kernel<double, false, true, false> : gen_kernel<double, false, false, false>;
+    }
+    if (uniform && packed) return in_canon ? gen_kernel<float, true, true, true> : gen_kernel<float, true, false, true>;
+    if (uniform) return in_canon ? gen_kernel<float, true, true, false> : gen_kernel<float, true, false, false>;
+    return in_canon ? gen_kernel<float, false, true, false> : gen_kernel<float, false, false, false>;
 }
 
 static StepKernelFn pick_step_v3(int dtype, bool uniform, bool in_canon, bool packed) {
@@ -1634,7 +2018,7 @@ static int check_tiled(const ft_tiled* t, int n_rows, int n_cols, int n_own) {
 }
 
 static int g_window = 0;
-static int g_tier1 = 3;     // tier-1 variant: 3 classified in place (default), 1 window passes, 2 compacted
+static int g_tier1 = 6;     // tier-1 variant: 6 split (default), 3 classified in place, 1 window passes, 2 compacted
 static int g_fixup_grid = 4 * 148;
 static int g_fin_ctas = 4 * 148;   // finalize: ~one tile per thread at C3, <= FT_FIN_MAX
 
@@ -1647,8 +2031,8 @@ static int window_size() {
         const char* s = getenv("FT_WINDOW");
         g_window = (s && atoi(s) == 4) ? 4 : 2;   // default: 2-row register window
         const char* t1 = getenv("FT_TIER1");
-        g_tier1 = t1 ? atoi(t1) : 3;
-        if (g_tier1 < 1 || g_tier1 > 3) g_tier1 = 3;
+        g_tier1 = t1 ? atoi(t1) : 6;
+        if (g_tier1 != 1 && g_tier1 != 2 && g_tier1 != 3) g_tier1 = 6;
         int dev = 0, sms = 148;
         if (cudaGetDevice(&dev) == cudaSuccess &&
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
@@ -1709,12 +2093,16 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_
     p.lap_pack = packed ? (const int4*)lap_t->values : nullptr;
     const bool ic = in_canon != nullptr;
     const int win = window_size();
+    p.force_check = (lap_flags & FT_LAP_CHECK_FINITE) != 0;
     const ft::StepKernelFn k = g_tier1 == 1 ? (win == 4 ? ft::pick_step_v1<4>(dtype, uni, ic, packed)
                                                         : ft::pick_step_v1<2>(dtype, uni, ic, packed))
                              : g_tier1 == 2 ? ft::pick_step_v2(dtype, uni, ic, packed)
-                                            : ft::pick_step_v3(dtype, uni, ic, packed);
+                             : g_tier1 == 3 ? ft::pick_step_v3(dtype, uni, ic, packed)
+                                            : ft::pick_step_v6(dtype, uni, ic, packed);
     if (which & 1) k<<<p.num_tiles, FT_TPB, 0, s>>>(p);
     if (which & 2) {
+        if (g_tier1 == 6)      // one warp per tile
+            ft::pick_gen(dtype, uni, ic, packed)<<<(p.num_tiles + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
         ft::pick_wide(dtype, uni, ic)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
         ft::pick_deep(dtype, uni, ic)<<<g_fixup_grid / 4, FT_TPB, 0, s>>>(p);
     }

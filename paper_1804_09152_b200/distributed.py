@@ -419,6 +419,8 @@ class DomainRank:
             buf.values[:nnz].copy_(torch.from_numpy(problem.values[:nnz]).to(self.device,
                                                                                self.vdtype))
         self.meta[0] = (buf.ft_tiled(), 0, self.slots)
+        # values of unknown origin: the first step checks them unless finite
+        self.first_check = not bool(np.all(np.isfinite(problem.values)))
         self._buffer(1, self._need_capacity())
         self.meta[1] = None
 
@@ -453,7 +455,8 @@ class DomainRank:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record()
             self.step_events.append(ev)
-        _check(lib.ft_domain_step(ctypes.byref(self.lap_c), self.lap_flags, ctypes.byref(in_t),
+        flags = self.lap_flags | (_lib.FT_LAP_CHECK_FINITE if (i == 0 and self.first_check) else 0)
+        _check(lib.ft_domain_step(ctypes.byref(self.lap_c), flags, ctypes.byref(in_t),
                                   ctypes.byref(out_t), self.ftd, ctypes.byref(prm),
                                   ctypes.byref(dom), wp, wn, rec, stream), "ft_domain_step")
         if self.step_events is not None:
