@@ -10,19 +10,25 @@
 //   normalise + compact     column_sums_counts, normalize_compact
 //                                               _kernels.py:241-282
 //
-// Work split: one thread per vertex column, 128-column tiles per CTA.  The
-// thread fetches its L row, the neighbours' column descriptors and their
-// first entries into registers (four rounds of independent loads), merges
-// the neighbours' sorted columns into a <= K-row window in ascending row
-// order, accumulating Lt(r, j) in ascending-u order -- exactly the
-// reference accumulator order.  PHI(r, j) itself arrives through the
-// diagonal u == j.  Wider columns go to a second kernel (tier 2) that runs
-// the exact windowed algorithm over a compacted list.
+// Work split, three tiers over 128-column tiles (one thread per vertex
+// column):
+//   tier 1    step_kernel6: classification from the neighbours'
+//             descriptors; a single-row neighbourhood (a cell interior,
+//             ~82% of the columns at C3) takes the exact closed form
+//             v' = v * (1 / (0 + v)); the others are listed per tile;
+//   tier 1.5  gen_kernel, one warp per tile: columns with at most two
+//             rows and two entries per neighbour, the update in one pass
+//             (rows = min / max of the candidates, Lt accumulated in
+//             ascending-u order -- exactly the reference accumulator order;
+//             PHI(r, j) arrives through the diagonal u == j);
+//   tier 2/3  wide_kernel / deep_kernel: wider columns, ascending-row
+//             windows of up to 8 rows / no limit.
 //
-// Output: the tile's entries go to its fixed slot of the tiled work buffer
-// (FT_SLOT entries) or, when they do not fit, to a pool range taken with
-// one atomic; column j is described by (start, count).  No CTA ever waits
-// for another.  Canonical CSC comes from ft_compact.
+// Output: tiles write to their fixed slot of the tiled work buffer
+// (FT_SLOT entries; tier 1.5 appends to it) or, when they do not fit, to a
+// pool range taken with one atomic; column j is described by (start,
+// count).  No CTA waits for another and no queue takes a same-address
+// atomic per warp.  Canonical CSC comes from ft_compact.
 //
 // EXACT mode (double storage) replays the reference arithmetic operation by
 // operation; the library is compiled with -fmad=false (no FMA contraction)
@@ -614,18 +620,10 @@ __device__ __forceinline__ TileOut tile_epilogue(int cnt, int nskel, double bmv,
 }
 
 // ---------------------------------------------------------------------------
-// tier 1: the fused step kernel
-//
-// One thread per vertex column, everything in registers: the L row (<= kMD
-// entries), the neighbours' column descriptors and their first two entries
-// are fetched in four rounds of independent loads (no shared-memory stage,
-// no barrier before the epilogue).  Columns whose neighbourhood carries a
-// single layer row (cell interiors, ~80% of columns) take the exact
-// single-row closed form (process_window) and need no products at all; the
-// others build a <= K-row window by ascending-row passes over the register
-// entries, accumulating in (u, t) order = the reference order.  A column
-// with a longer L row, a neighbour holding more than two entries, or more
-// than K rows is "wide": it is queued (slow_list, slow_mask) for tier 2.
+// tier 1 (see step_kernel6 below for the default split variant and
+// step_kernel3 for the in-place one): one thread per vertex column,
+// 128-column CTAs, the L row, the neighbours' descriptors and entries in
+// registers, no barrier before the tile epilogue.
 
 constexpr int kMD = 8;
 constexpr int kPackEmpty = -32768;
@@ -666,120 +664,13 @@ __device__ __forceinline__ int load_lrow(const StepParams& p, int jl, int j, boo
     return n;
 }
 
-template <typename T, int K, bool UNIFORM, bool IN_CANON, bool PACKED>
-__global__ void __launch_bounds__(FT_TPB, 6) step_kernel(const StepParams p) {
-    __shared__ double s_wbm[FT_WARPS];
-    __shared__ double s_wmax[FT_WARPS];
-    __shared__ int s_wskel[FT_WARPS];
-    __shared__ unsigned int s_wslow[FT_WARPS];
-    __shared__ int s_scan[FT_WARPS];
-    __shared__ long long s_base;
-
-    if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int tile = blockIdx.x;
-    const int jl = tile * FT_TPB + tid;   // local column
-    const int j = p.j_base + jl;          // global column
-    const bool active = jl < p.n_v;
-
-    int q0 = 0;
-    int u[kMD];
-    const int n = load_lrow<PACKED>(p, jl, j, active, u, q0);
-    bool wide = active && n == 0;
-    double lv[UNIFORM ? 1 : kMD];
-    if (!UNIFORM) {
-#pragma unroll
-        for (int k = 0; k < kMD; ++k) lv[k] = (k < n) ? ldv<T>(p.lap_val, q0 + k) : 0.0;
-    }
-    int2 d[kMD];
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
-    int kd = -1;
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) {
-        if (u[k] == j) kd = k;
-        wide |= d[k].y > 2;
-    }
-    if (active && kd < 0) wide = true;
-    int r0[kMD], r1[kMD];
-    T v0[kMD], v1[kMD];
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) {
-        r0[k] = INT_MAX; r1[k] = INT_MAX; v0[k] = (T)0; v1[k] = (T)0;
-        if (!wide && d[k].y > 0) { r0[k] = __ldg(&p.in_idx[d[k].x]); v0[k] = __ldg(((const T*)p.in_val) + d[k].x); }
-        if (!wide && d[k].y > 1) { r1[k] = __ldg(&p.in_idx[d[k].x + 1]); v1[k] = __ldg(((const T*)p.in_val) + d[k].x + 1); }
-    }
-
-    VRes res;
-    vres_init(res);
-    Win<K> w;
-    w.m = 0;
-    unsigned int out_mask = 0;
-    if (active && !wide) {
-        const double invdeg = UNIFORM ? (n - 1 <= 32 ? c_recip[n - 1] : 1.0 / (double)(n - 1)) : 0.0;
-        int lo = -1;
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            int r = INT_MAX;
-#pragma unroll
-            for (int k = 0; k < kMD; ++k) {
-                if (r0[k] > lo && r0[k] < r) r = r0[k];
-                if (r1[k] > lo && r1[k] < r) r = r1[k];
-            }
-            double lam = 0.0, ph = 0.0;
-            if (r != INT_MAX) {
-#pragma unroll
-                for (int k = 0; k < kMD; ++k) {
-                    const double l = UNIFORM ? ((k == kd) ? -1.0 : invdeg) : lv[k];
-                    if (r0[k] == r) { lam = lam + (double)v0[k] * l; if (k == kd) ph = (double)v0[k]; }
-                    if (r1[k] == r) { lam = lam + (double)v1[k] * l; if (k == kd) ph = (double)v1[k]; }
-                }
-                w.m = i + 1;
-                lo = r;
-            }
-            w.rows[i] = r;
-            w.lam[i] = lam;
-            w.phi[i] = ph;
-        }
-        bool more = false;
-#pragma unroll
-        for (int k = 0; k < kMD; ++k) more |= (r0[k] > lo && r0[k] != INT_MAX) || (r1[k] > lo && r1[k] != INT_MAX);
-        if (more) {
-            wide = true;
-        } else {
-            process_window<K>(w, p, res, out_mask, c_recip);
-            report_flags(res, j, p);
-        }
-    }
-    if (wide) vres_init(res);
-
-    // queue the wide columns for tier 2 (one atomic per warp)
-    const unsigned int wbits = __ballot_sync(0xffffffffu, wide && active);
-    if (wbits) {
-        int qb = 0;
-        if (lane == 0) qb = atomicAdd(&p.ws.ctl->slow_count, __popc(wbits));
-        qb = __shfl_sync(0xffffffffu, qb, 0);
-        if (wide && active) p.ws.slow_list[qb + __popc(wbits & ((1u << lane) - 1u))] = j;
-    }
-    if (lane == 0) {
-        s_wslow[warp] = wbits;
-        p.ws.slow_mask[(size_t)tile * FT_WARPS + warp] = wbits;
-    }
-    const TileOut o = tile_epilogue<false>(res.cnt, res.nskel, res.bm, res.maxd, tile, &p.ws.tile_bm[tile], p,
-                                           s_scan, s_wbm, s_wmax, s_wskel, &s_base);
-    if (!active || wide || o.base < 0) return;
-    const long long off = o.base + o.local_off;
-    p.out_desc[j] = make_int2((int)off, res.cnt);
-    if (out_mask) emit_window<T, K>(w, out_mask, off, p);
-}
-
 // ---------------------------------------------------------------------------
-// tier 1, v3 (default): in place, classified.  Every column first takes the
-// cheap classification of step_kernel2's phase A (single-row neighbourhood
-// -> exact closed form); the window code runs only when some lane of the
-// warp needs it, and then as ONE pass: with at most two distinct rows in the
-// neighbourhood they are the min and the max of the candidate rows, and both
-// Lt sums accumulate in the same (u, t) loop, in the reference order.
+// tier 1, in place (FT_TIER1=3): every column is classified first (single-
+// row neighbourhood -> the exact closed form); the window code runs only
+// when some lane of the warp needs it, and then as ONE pass: with at most
+// two distinct rows in the neighbourhood they are the min and the max of
+// the candidate rows, and both Lt sums accumulate in the same (u, t) loop,
+// in the reference order.  Measured 4% slower than the split variant at C3.
 
 template <typename T, bool UNIFORM, bool IN_CANON, bool PACKED>
 __global__ void __launch_bounds__(FT_TPB, 6) step_kernel3(const StepParams p) {
@@ -1051,241 +942,6 @@ __global__ void __launch_bounds__(FT_TPB, 8) step_kernel6(const StepParams p) {
         p.out_idx[off] = rs;
         ((T*)p.out_val)[off] = (T)nv;
         if (!isfinite(nv)) atomicOr(&p.ws.ctl->nonfinite, 1u);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// tier 1, classify-and-compact variant (FT_TIER1=2)
-//
-// Phase A, every column: the L row, the neighbours' descriptors and their
-// FIRST entry.  A column whose neighbourhood is one layer row r (every
-// non-empty neighbour holds exactly one entry, of row r; its own entry is
-// phi > 0; all values finite) takes the exact single-row closed form right
-// away (process_window, n == 1: v = clamp(phi), v' = v * (1/(0 + v))).
-// That is ~82% of the columns at C3 but only ~21% of the warps, so the other
-// columns are not processed in place (a warp would run the general path for
-// all its lanes): phase B compacts them, per CTA, into a shared-memory list
-// and dense warps re-gather them (L1-hot) and run the <= K-row window.
-// Results return to the owning thread through shared memory for the tile
-// scan and the emission.
-
-// One general column (<= kMD L entries, <= 2 entries per neighbour): the
-// ascending-row window of tier 1.  Returns false when the column has more
-// than K rows (it is then queued for tier 2).
-template <typename T, int K, bool UNIFORM, bool IN_CANON>
-__device__ __forceinline__ bool general_column(int j, int n, int kd, int q0, const int2* sd, const StepParams& p,
-                                               Win<K>& w, VRes& res, unsigned int& out_mask) {
-    double lv[UNIFORM ? 1 : kMD];
-    if (!UNIFORM) {
-#pragma unroll
-        for (int k = 0; k < kMD; ++k) lv[k] = (k < n) ? ldv<T>(p.lap_val, q0 + k) : 0.0;
-    }
-    int2 d[kMD];
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? sd[k] : make_int2(0, 0);
-    int r0[kMD], r1[kMD];
-    T v0[kMD], v1[kMD];
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) {
-        r0[k] = INT_MAX; r1[k] = INT_MAX; v0[k] = (T)0; v1[k] = (T)0;
-        if (d[k].y > 0) { r0[k] = __ldg(&p.in_idx[d[k].x]); v0[k] = __ldg(((const T*)p.in_val) + d[k].x); }
-        if (d[k].y > 1) { r1[k] = __ldg(&p.in_idx[d[k].x + 1]); v1[k] = __ldg(((const T*)p.in_val) + d[k].x + 1); }
-    }
-    const double invdeg = UNIFORM ? (n - 1 <= 32 ? c_recip[n - 1] : 1.0 / (double)(n - 1)) : 0.0;
-    int lo = -1;
-    w.m = 0;
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-        int r = INT_MAX;
-#pragma unroll
-        for (int k = 0; k < kMD; ++k) {
-            if (r0[k] > lo && r0[k] < r) r = r0[k];
-            if (r1[k] > lo && r1[k] < r) r = r1[k];
-        }
-        double lam = 0.0, ph = 0.0;
-        if (r != INT_MAX) {
-#pragma unroll
-            for (int k = 0; k < kMD; ++k) {
-                const double l = UNIFORM ? ((k == kd) ? -1.0 : invdeg) : lv[k];
-                if (r0[k] == r) { lam = lam + (double)v0[k] * l; if (k == kd) ph = (double)v0[k]; }
-                if (r1[k] == r) { lam = lam + (double)v1[k] * l; if (k == kd) ph = (double)v1[k]; }
-            }
-            w.m = i + 1;
-            lo = r;
-        }
-        w.rows[i] = r;
-        w.lam[i] = lam;
-        w.phi[i] = ph;
-    }
-    bool more = false;
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) more |= (r0[k] > lo && r0[k] != INT_MAX) || (r1[k] > lo && r1[k] != INT_MAX);
-    if (more) return false;
-    process_window<K>(w, p, res, out_mask, c_recip);
-    report_flags(res, j, p);
-    return true;
-}
-
-template <typename T, int K, bool UNIFORM, bool IN_CANON, bool PACKED>
-__global__ void __launch_bounds__(FT_TPB, 6) step_kernel2(const StepParams p) {
-    __shared__ double s_wbm[FT_WARPS];
-    __shared__ double s_wmax[FT_WARPS];
-    __shared__ int s_wskel[FT_WARPS];
-    __shared__ int s_scan[FT_WARPS];
-    __shared__ long long s_base;
-    __shared__ int s_ngen;
-    __shared__ short s_list[FT_TPB];          // general columns (local index in the tile)
-    __shared__ int s_cnt[FT_TPB];             // phase-B results, by local index
-    __shared__ int s_nskel[FT_TPB];
-    __shared__ double s_bm[FT_TPB];
-    __shared__ double s_maxd[FT_TPB];
-    __shared__ int s_orow[FT_TPB][K];
-    __shared__ double s_oval[FT_TPB][K];
-    __shared__ int2 s_desc[FT_TPB][kMD];      // phase-A descriptors of the general columns
-    __shared__ int s_meta[FT_TPB][3];         // n, kd, q0
-
-    if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int tile = blockIdx.x;
-    const int jl = tile * FT_TPB + tid;   // local column
-    const int j = p.j_base + jl;          // global column
-    const bool active = jl < p.n_v;
-    if (tid == 0) s_ngen = 0;
-    __syncthreads();
-
-    // ---- phase A: classify, closed form for single-row neighbourhoods ----
-    int q0 = 0;
-    int u[kMD];
-    const int n = load_lrow<PACKED>(p, jl, j, active, u, q0);
-    bool wide = active && n == 0;
-    int2 d[kMD];
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
-    int kd = -1;
-    bool multi = false;
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) {
-        if (u[k] == j) kd = k;
-        wide |= d[k].y > 2;
-        multi |= d[k].y > 1;
-    }
-    if (active && kd < 0) wide = true;
-    int r0[kMD];
-    T v0[kMD];
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) {
-        r0[k] = INT_MAX; v0[k] = (T)0;
-        if (!wide && !multi && d[k].y > 0) {
-            r0[k] = __ldg(&p.in_idx[d[k].x]);
-            v0[k] = __ldg(((const T*)p.in_val) + d[k].x);
-        }
-    }
-    int rs = INT_MAX;
-    double phs = 0.0;
-#pragma unroll
-    for (int k = 0; k < kMD; ++k)
-        if (k == kd) { rs = r0[k]; phs = (double)v0[k]; }
-    bool same = true, fin = true;
-    double lam = 0.0;
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) {
-        same &= (r0[k] == INT_MAX) || (r0[k] == rs);
-        fin &= isfinite((double)v0[k]);
-        if (!UNIFORM && k < n) lam = lam + (double)v0[k] * ldv<T>(p.lap_val, q0 + k);
-    }
-    // UNIFORM: |Lt| <= sum of |phi| * 1 over <= kMD finite entries, finite
-    const bool fast = active && !wide && !multi && p.finite && rs != INT_MAX && phs > 0.0 && same && fin &&
-                      (UNIFORM || isfinite(lam));
-    const bool gen = active && !wide && !fast;
-
-    VRes res;
-    vres_init(res);
-    double nv_fast = 0.0;
-    if (fast) {
-        double v = phs;
-        if (v > 1.0) v = 1.0;
-        const double s = 0.0 + v;
-        nv_fast = v * (1.0 / s);
-        res.nskel = 1;
-        if (nv_fast != 0.0) {
-            res.cnt = 1;
-            if (rs == 0) res.bm = nv_fast;
-        }
-        res.maxd = fabs(nv_fast - phs);
-    }
-    const unsigned int gbits = __ballot_sync(0xffffffffu, gen);
-    if (gbits) {
-        int gb = 0;
-        if (lane == 0) gb = atomicAdd(&s_ngen, __popc(gbits));
-        gb = __shfl_sync(0xffffffffu, gb, 0);
-        if (gen) s_list[gb + __popc(gbits & ((1u << lane) - 1u))] = (short)tid;
-    }
-    if (gen) {
-#pragma unroll
-        for (int k = 0; k < kMD; ++k) s_desc[tid][k] = d[k];
-        s_meta[tid][0] = n;
-        s_meta[tid][1] = kd;
-        s_meta[tid][2] = q0;
-    }
-    __syncthreads();
-
-    // ---- phase B: the general columns on dense warps ----
-    const int ngen = s_ngen;
-    for (int i = tid; i < ngen; i += FT_TPB) {
-        const int t = s_list[i];
-        Win<K> w;
-        VRes r2;
-        vres_init(r2);
-        unsigned int om = 0;
-        const bool ok = general_column<T, K, UNIFORM, IN_CANON>(p.j_base + tile * FT_TPB + t, s_meta[t][0],
-                                                                  s_meta[t][1], s_meta[t][2], s_desc[t], p, w,
-                                                                  r2, om);
-        int c = 0;
-        if (ok) {
-#pragma unroll
-            for (int q = 0; q < K; ++q)
-                if (om & (1u << q)) { s_orow[t][c] = w.rows[q]; s_oval[t][c] = w.lam[q]; ++c; }
-        }
-        s_cnt[t] = ok ? c : -1;
-        s_nskel[t] = r2.nskel;
-        s_bm[t] = r2.bm;
-        s_maxd[t] = r2.maxd;
-    }
-    __syncthreads();
-    if (gen) {
-        const int c = s_cnt[tid];
-        if (c < 0) {
-            wide = true;
-        } else {
-            res.cnt = c;
-            res.nskel = s_nskel[tid];
-            res.bm = s_bm[tid];
-            res.maxd = s_maxd[tid];
-        }
-    }
-
-    // queue the wide columns for tier 2 (one atomic per warp)
-    const unsigned int wbits = __ballot_sync(0xffffffffu, wide && active);
-    if (wbits) {
-        int qb = 0;
-        if (lane == 0) qb = atomicAdd(&p.ws.ctl->slow_count, __popc(wbits));
-        qb = __shfl_sync(0xffffffffu, qb, 0);
-        if (wide && active) p.ws.slow_list[qb + __popc(wbits & ((1u << lane) - 1u))] = j;
-    }
-    if (lane == 0) p.ws.slow_mask[(size_t)tile * FT_WARPS + warp] = wbits;
-    const TileOut o = tile_epilogue<false>(res.cnt, res.nskel, res.bm, res.maxd, tile, &p.ws.tile_bm[tile], p,
-                                           s_scan, s_wbm, s_wmax, s_wskel, &s_base);
-    if (!active || wide || o.base < 0) return;
-    long long off = o.base + o.local_off;
-    p.out_desc[j] = make_int2((int)off, res.cnt);
-    T* ov = (T*)p.out_val;
-    if (fast) {
-        if (res.cnt) { p.out_idx[off] = rs; ov[off] = (T)nv_fast; }
-    } else {
-        for (int q = 0; q < res.cnt; ++q) {
-            p.out_idx[off + q] = s_orow[tid][q];
-            ov[off + q] = (T)s_oval[tid][q];
-        }
     }
 }
 
@@ -1894,18 +1550,6 @@ __global__ void evolve_report_kernel(const Control* ctl, long long* control) {
 
 typedef void (*StepKernelFn)(const StepParams);
 
-template <int K>
-static StepKernelFn pick_step_v1(int dtype, bool uniform, bool in_canon, bool packed) {
-    if (dtype == FT_F64) {
-        if (uniform && packed) return in_canon ? step_kernel<double, K, true, true, true> : step_kernel<double, K, true, false, true>;
-        if (uniform) return in_canon ? step_kernel<double, K, true, true, false> : step_kernel<double, K, true, false, false>;
-        return in_canon ? step_kernel<double, K, false, true, false> : step_kernel<double, K, false, false, false>;
-    }
-    if (uniform && packed) return in_canon ? step_kernel<float, K, true, true, true> : step_kernel<float, K, true, false, true>;
-    if (uniform) return in_canon ? step_kernel<float, K, true, true, false> : step_kernel<float, K, true, false, false>;
-    return in_canon ? step_kernel<float, K, false, true, false> : step_kernel<float, K, false, false, false>;
-}
-
 static StepKernelFn pick_step_v6(int dtype, bool uniform, bool in_canon, bool packed) {
     if (dtype == FT_F64) {
         if (uniform && packed) return in_canon ? step_kernel6<double, true, true, true> : step_kernel6<double, true, false, true>;
@@ -1937,17 +1581,6 @@ static StepKernelFn pick_step_v3(int dtype, bool uniform, bool in_canon, bool pa
     if (uniform && packed) return in_canon ? step_kernel3<float, true, true, true> : step_kernel3<float, true, false, true>;
     if (uniform) return in_canon ? step_kernel3<float, true, true, false> : step_kernel3<float, true, false, false>;
     return in_canon ? step_kernel3<float, false, true, false> : step_kernel3<float, false, false, false>;
-}
-
-static StepKernelFn pick_step_v2(int dtype, bool uniform, bool in_canon, bool packed) {
-    if (dtype == FT_F64) {
-        if (uniform && packed) return in_canon ? step_kernel2<double, 2, true, true, true> : step_kernel2<double, 2, true, false, true>;
-        if (uniform) return in_canon ? step_kernel2<double, 2, true, true, false> : step_kernel2<double, 2, true, false, false>;
-        return in_canon ? step_kernel2<double, 2, false, true, false> : step_kernel2<double, 2, false, false, false>;
-    }
-    if (uniform && packed) return in_canon ? step_kernel2<float, 2, true, true, true> : step_kernel2<float, 2, true, false, true>;
-    if (uniform) return in_canon ? step_kernel2<float, 2, true, true, false> : step_kernel2<float, 2, true, false, false>;
-    return in_canon ? step_kernel2<float, 2, false, true, false> : step_kernel2<float, 2, false, false, false>;
 }
 
 static StepKernelFn pick_deep(int dtype, bool uniform, bool in_canon) {
@@ -2018,7 +1651,7 @@ static int check_tiled(const ft_tiled* t, int n_rows, int n_cols, int n_own) {
 }
 
 static int g_window = 0;
-static int g_tier1 = 6;     // tier-1 variant: 6 split (default), 3 classified in place, 1 window passes, 2 compacted
+static int g_tier1 = 6;     // tier-1 variant: 6 split (default), 3 in place (FT_TIER1=3)
 static int g_fixup_grid = 4 * 148;
 static int g_fin_ctas = 4 * 148;   // finalize: ~one tile per thread at C3, <= FT_FIN_MAX
 
@@ -2028,11 +1661,9 @@ static int window_size() {
         h[0] = 0.0;
         for (int n = 1; n <= 32; ++n) h[n] = 1.0 / (double)n;
         cudaMemcpyToSymbol(ft::c_recip, h, sizeof(h));
-        const char* s = getenv("FT_WINDOW");
-        g_window = (s && atoi(s) == 4) ? 4 : 2;   // default: 2-row register window
+        g_window = 2;
         const char* t1 = getenv("FT_TIER1");
-        g_tier1 = t1 ? atoi(t1) : 6;
-        if (g_tier1 != 1 && g_tier1 != 2 && g_tier1 != 3) g_tier1 = 6;
+        g_tier1 = (t1 && atoi(t1) == 3) ? 3 : 6;
         int dev = 0, sms = 148;
         if (cudaGetDevice(&dev) == cudaSuccess &&
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
@@ -2092,12 +1723,9 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_
     const bool packed = uni && (lap_flags & FT_LAP_PACKED) != 0;
     p.lap_pack = packed ? (const int4*)lap_t->values : nullptr;
     const bool ic = in_canon != nullptr;
-    const int win = window_size();
+    window_size();
     p.force_check = (lap_flags & FT_LAP_CHECK_FINITE) != 0;
-    const ft::StepKernelFn k = g_tier1 == 1 ? (win == 4 ? ft::pick_step_v1<4>(dtype, uni, ic, packed)
-                                                        : ft::pick_step_v1<2>(dtype, uni, ic, packed))
-                             : g_tier1 == 2 ? ft::pick_step_v2(dtype, uni, ic, packed)
-                             : g_tier1 == 3 ? ft::pick_step_v3(dtype, uni, ic, packed)
+    const ft::StepKernelFn k = g_tier1 == 3 ? ft::pick_step_v3(dtype, uni, ic, packed)
                                             : ft::pick_step_v6(dtype, uni, ic, packed);
     if (which & 1) k<<<p.num_tiles, FT_TPB, 0, s>>>(p);
     if (which & 2) {
