@@ -381,13 +381,19 @@ def run_ours(args):
         pinned[2].numpy()[:] = host0.values[:nnz0]
         hphi = ft.SparseMat(host0.n_rows, n_v, pinned[0].numpy(), pinned[1].numpy(),
                             pinned[2].numpy(), check=False)
+        def api_run():
+            fin, tr = ft.evolve(ft.LayeredField(hphi, seeds, precision=prec), lap, params,
+                                max_steps=K, tol=0.0)
+            return fin.phi, ft.sharp_labels(fin), tr
+
+        # one untimed call first: the host (pinned) and device caching
+        # allocators are warm, as for a service making repeated calls
+        warm_out = api_run()
+        del warm_out
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        fin, tr = ft.evolve(ft.LayeredField(hphi, seeds, precision=prec), lap, params,
-                            max_steps=K, tol=0.0)
-        phi_back = fin.phi
-        labels = ft.sharp_labels(fin)
+        phi_back, labels, tr = api_run()
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         barrier()
@@ -397,7 +403,8 @@ def run_ours(args):
         e2e = {"value": world * K / e2e_s, "unit": "steps/s",
                "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K),
                "path": "evolve(host field, K steps) -> field.phi + sharp_labels on the host; "
-                       "steps 1..K from init_field; L^T resident (uploaded once per mesh)"}
+                       "steps 1..K from init_field; L^T resident (uploaded once per mesh); "
+                       "second of two identical calls (allocators warm)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -643,7 +643,8 @@ def sharp_labels(field):
     rc = _lib.lib().ft_labels(ctypes.byref(c), _ft_dtype(field.precision),
                               ctypes.c_void_p(labels.data_ptr()), _stream_handle())
     _check(rc, "ft_labels")
-    return labels[:dphi.n_cols].cpu().numpy()
+    from .sparse import pinned_copy
+    return pinned_copy(labels[:dphi.n_cols])
 
 
 def band_vertex_fraction(field):

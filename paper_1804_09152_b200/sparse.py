@@ -193,6 +193,14 @@ def _torch():
     return torch
 
 
+def pinned_copy(t):
+    """Device tensor -> numpy array backed by pinned host memory."""
+    torch = _torch()
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h.numpy()
+
+
 class DeviceCSC:
     """CSC arrays resident on the GPU (torch CUDA tensors).
 
@@ -246,11 +254,14 @@ class DeviceCSC:
         return dev
 
     def to_host(self):
-        """Materialise as a host :class:`SparseMat` (float64 values)."""
+        """Materialise as a host :class:`SparseMat` (float64 values).  The
+        arrays are numpy views of pinned host tensors (one DMA each, at link
+        speed; torch's caching host allocator recycles them)."""
         nnz = self.nnz
-        cp = self.col_ptr.cpu().numpy()
-        ri = self.row_idx[:nnz].cpu().numpy()
-        va = self.values[:nnz].double().cpu().numpy()
+        cp = pinned_copy(self.col_ptr)
+        ri = pinned_copy(self.row_idx[:nnz])
+        va = pinned_copy(self.values[:nnz] if self.values.dtype == _torch().float64
+                         else self.values[:nnz].double())
         return SparseMat(self.n_rows, self.n_cols, cp, ri, va, check=False)
 
     def grow(self, needed):
