@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfieldtess_cuda.so")
+# FT_LIB overrides the library path (A/B measurements of two builds)
+LIB_PATH = os.environ.get("FT_LIB") or os.path.join(_HERE, "libfieldtess_cuda.so")
 
 FT_OK = 0
 FT_ERR_SHAPE = 1
