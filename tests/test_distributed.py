@@ -285,3 +285,44 @@ def test_loopback_stops_with_single_gpu():
                                       max_steps=400, tol=1e-3)
     assert steps == len(tr1) and tr2[-1].converged == tr1[-1].converged
     _assert_same_field(D.gather_field(ranks, steps), single.phi)
+
+
+@pytest.mark.gpu
+def test_loopback_fast_precision_and_cotan():
+    """FAST storage and an explicit (cotangent) Laplacian through the
+    partitioned path: owned columns equal the single-GPU evolve."""
+    mesh = ft.gen_icosphere(3)
+    seeds = np.random.default_rng(1).choice(mesh.n_vertices, 20, replace=False)
+    part = D.Partition.even(mesh.n_vertices, 3)
+    for scheme, precision in (("uniform", "fast"), ("cotan-clamped", "exact")):
+        lap = ft.build_laplacian(mesh, scheme)
+        fld = ft.init_field(mesh, seeds, precision=precision)
+        single, tr1 = ft.evolve(fld, lap, ft.CouplingParams(), max_steps=30, tol=0.0)
+        ranks = _loopback(fld, lap, part, precision=precision)
+        steps, tr2 = D.evolve_partitioned(ranks, D.LoopbackTransport(), ft.CouplingParams(),
+                                          max_steps=30, tol=0.0)
+        assert steps == 30
+        g = D.gather_field(ranks, steps)
+        s = single.phi
+        assert np.array_equal(np.asarray(g.col_ptr), np.asarray(s.col_ptr)), scheme
+        nnz = int(s.col_ptr[-1])
+        assert np.array_equal(np.asarray(g.row_idx[:nnz]), np.asarray(s.row_idx[:nnz]))
+        assert np.array_equal(np.asarray(g.values[:nnz]), np.asarray(s.values[:nnz]))
+        assert [a.max_delta for a in tr1] == [b.max_delta for b in tr2]
+
+
+@pytest.mark.gpu
+def test_loopback_nan_raises_like_single_gpu():
+    """A NaN coupling blows up on every rank: the lowest-rank failure is
+    reported as the reference's NumericalBlowupError."""
+    mesh = ft.gen_periodic_grid(24, 18)
+    seeds = np.random.default_rng(2).choice(mesh.n_vertices, 12, replace=False)
+    lap = ft.build_laplacian(mesh)
+    fld = ft.init_field(mesh, seeds)
+    bad = ft.CouplingParams(dt=float("nan"))
+    with pytest.raises(ft.errors.NumericalBlowupError) as e1:
+        ft.evolve(fld, lap, bad, max_steps=5, tol=0.0)
+    ranks = _loopback(fld, lap, D.Partition.even(mesh.n_vertices, 2, align=24))
+    with pytest.raises(ft.errors.NumericalBlowupError) as e2:
+        D.evolve_partitioned(ranks, D.LoopbackTransport(), bad, max_steps=5, tol=0.0)
+    assert str(e1.value) == str(e2.value)
