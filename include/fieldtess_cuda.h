@@ -232,6 +232,9 @@ typedef struct {
     int32_t col_begin;       /* first owned column (global index)          */
     int32_t col_count;       /* number of owned columns                    */
     int64_t step_capacity;   /* entries the step may use in `out`          */
+    const int32_t* report_ids;  /* nullable, device [col_count]: the caller's
+                                   vertex ids of the owned columns (a renumbered
+                                   partition); NaN / pattern errors report them */
 } ft_domain;
 
 #define FT_HALO_FORCE 1      /* pack / unpack even when done is set         */
@@ -266,8 +269,8 @@ int ft_halo_unpack(ft_tiled* dst, const int32_t* cols, int32_t n, int32_t slots,
 
 /* Global record from the all-gathered per-rank records (device, `world`
  * records in rank order): max of max_delta, base_mass summed in rank
- * order, nnz sums, the failure of the lowest rank by priority pattern >
- * NaN > overflow > halo overflow.  Applies the stop test of ft_evolve
+ * order, nnz sums; the failure of highest priority (pattern > NaN >
+ * overflow > halo overflow), reported at its lowest column over the ranks.  Applies the stop test of ft_evolve
  * (field.py:316-317) and writes trace[steps_done]; `needed` is the local
  * rank's. */
 int ft_domain_combine(const ft_step_stats* records, int32_t world, int32_t rank,

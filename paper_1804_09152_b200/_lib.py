@@ -62,7 +62,7 @@ class FtTiled(ctypes.Structure):
 
 class FtDomain(ctypes.Structure):
     _fields_ = [("col_begin", ctypes.c_int32), ("col_count", ctypes.c_int32),
-                ("step_capacity", ctypes.c_int64)]
+                ("step_capacity", ctypes.c_int64), ("report_ids", ctypes.c_void_p)]
 
 
 class FtStepStats(ctypes.Structure):

@@ -103,7 +103,12 @@ __global__ void combine_kernel(const ft_step_stats* rec, int world, int rank, in
         nnz += rec[r].nnz_phi;
         nsk += rec[r].nnz_skel;
         const int f = failure_rank(rec[r].status);
-        if (f > worst) { worst = f; wr = r; }
+        // the highest-priority failure, at its lowest column (the reference
+        // reports the first column of the whole field)
+        const int col = rec[r].status == FT_STATUS_NAN ? rec[r].nan_col : rec[r].bad_col;
+        const int wcol = wr < 0 ? INT_MAX
+                                : (rec[wr].status == FT_STATUS_NAN ? rec[wr].nan_col : rec[wr].bad_col);
+        if (f > worst || (f == worst && f > 0 && col >= 0 && col < wcol)) { worst = f; wr = r; }
     }
     st.max_delta = mxd;
     st.base_mass = bm;

@@ -70,6 +70,7 @@ struct StepParams {
     int check_done;
     int finite;          // all couplings finite: enables the single-row closed form
     int force_check;     // FT_LAP_CHECK_FINITE: check tiled input values for NaN / Inf
+    const int* report_ids;  // nullable: caller ids of the owned columns (error reports)
 };
 
 struct FinalizeParams {
@@ -472,6 +473,8 @@ __device__ __forceinline__ void process_two(Win<2>& w, const StepParams& p, VRes
 }
 
 __device__ __forceinline__ void report_flags(const VRes& res, int j, const StepParams& p) {
+    if (!res.nan && res.bad_phi_row < 0 && res.bad_lt_row < 0) return;
+    if (p.report_ids) j = __ldg(&p.report_ids[j - p.j_base]);   // the caller's vertex id
     if (res.nan) atomicMax(&p.ws.ctl->nan_key, (unsigned int)(INT_MAX - j));
     if (res.bad_phi_row >= 0)
         atomicMax(&p.ws.ctl->bad_phi_key, ~(((unsigned long long)j << 32) | (unsigned int)res.bad_phi_row));
@@ -1725,6 +1728,7 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_
     const bool ic = in_canon != nullptr;
     window_size();
     p.force_check = (lap_flags & FT_LAP_CHECK_FINITE) != 0;
+    p.report_ids = dom ? dom->report_ids : nullptr;
     const ft::StepKernelFn k = g_tier1 == 3 ? ft::pick_step_v3(dtype, uni, ic, packed)
                                             : ft::pick_step_v6(dtype, uni, ic, packed);
     if (which & 1) k<<<p.num_tiles, FT_TPB, 0, s>>>(p);

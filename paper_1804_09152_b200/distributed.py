@@ -146,11 +146,7 @@ class LocalProblem:
             raise ShapeError("L^T columns do not match the owned range")
 
 
-def local_problem(field_phi, lap, partition, rank):
-    """Slice a host field (SparseMat) and a Laplacian for one rank."""
-    from .field import _uniform_values_exact, _with_diagonal
-    mat_t = _with_diagonal(lap.mat_t)
-    flags = _lib.FT_LAP_UNIFORM if _uniform_values_exact(mat_t) else _lib.FT_LAP_EXPLICIT
+def _slice_problem(field_phi, mat_t, flags, partition, rank):
     b, e = partition.range(rank)
     cp = np.asarray(mat_t.col_ptr, dtype=np.int64)
     q0, q1 = int(cp[b]), int(cp[e])
@@ -167,6 +163,99 @@ def local_problem(field_phi, lap, partition, rank):
     return LocalProblem(rank, partition, field_phi.n_rows, lap_ptr, lap_idx, lap_val, flags, cols,
                         col_ptr, np.asarray(field_phi.row_idx)[src],
                         np.asarray(field_phi.values, dtype=np.float64)[src])
+
+
+def _laplacian_t(lap):
+    from .field import _uniform_values_exact, _with_diagonal
+    mat_t = _with_diagonal(lap.mat_t)
+    flags = _lib.FT_LAP_UNIFORM if _uniform_values_exact(mat_t) else _lib.FT_LAP_EXPLICIT
+    return mat_t, flags
+
+
+def local_problem(field_phi, lap, partition, rank, renumbering=None):
+    """Slice a host field (SparseMat) and a Laplacian for one rank; with a
+    :class:`Renumbering` the partition is over the renumbered vertices."""
+    if renumbering is not None:
+        return _slice_problem(renumbering.field(field_phi), renumbering.laplacian_t(lap),
+                              renumbering.lap_flags, partition, rank)
+    mat_t, flags = _laplacian_t(lap)
+    return _slice_problem(field_phi, mat_t, flags, partition, rank)
+
+
+# -- locality renumbering -------------------------------------------------------
+
+
+def _spread3(x):
+    """Spread the low 21 bits of x to every third bit (Morton code)."""
+    x = x.astype(np.uint64) & np.uint64(0x1FFFFF)
+    for shift, mask in ((32, 0x1F00000000FFFF), (16, 0x1F0000FF0000FF), (8, 0x100F00F00F00F00F),
+                        (4, 0x10C30C30C30C30C3), (2, 0x1249249249249249)):
+        x = (x | (x << np.uint64(shift))) & np.uint64(mask)
+    return x
+
+
+def morton_order(positions):
+    """Vertices sorted by the Morton (Z-order) code of their positions:
+    contiguous ranges of the order are compact patches of the surface."""
+    p = np.asarray(positions, dtype=np.float64)
+    lo = p.min(axis=0)
+    span = float((p.max(axis=0) - lo).max()) or 1.0
+    q = np.floor((p - lo) / span * (2 ** 21 - 1)).astype(np.uint64)
+    code = _spread3(q[:, 0]) | (_spread3(q[:, 1]) << np.uint64(1)) | (_spread3(q[:, 2]) << np.uint64(2))
+    return np.argsort(code, kind="stable")
+
+
+class Renumbering:
+    """A vertex renumbering for partitioning: new vertex k is old vertex
+    ``order[k]``.  Every L^T column keeps its entries in the ORIGINAL order
+    (the kernels accumulate in stored order, so the step stays bitwise the
+    reference's); only the indices change.  Layer rows (cells) do not."""
+
+    def __init__(self, order):
+        self.order = np.asarray(order, dtype=np.int64)
+        self.inverse = np.empty_like(self.order)
+        self.inverse[self.order] = np.arange(self.order.size)
+        self.lap_flags = None
+        self._lap = None
+
+    @classmethod
+    def morton(cls, mesh):
+        return cls(morton_order(mesh.positions))
+
+    def _columns(self, m, rows_map=None):
+        cp = np.asarray(m.col_ptr, dtype=np.int64)
+        cnt = cp[1:] - cp[:-1]
+        new_cnt = cnt[self.order]
+        new_cp = np.zeros(cnt.size + 1, dtype=np.int64)
+        np.cumsum(new_cnt, out=new_cp[1:])
+        src = np.repeat(cp[self.order], new_cnt) + (np.arange(int(new_cp[-1])) -
+                                                    np.repeat(new_cp[:-1], new_cnt))
+        rows = np.asarray(m.row_idx)[src]
+        if rows_map is not None:
+            rows = rows_map[rows]
+        return SparseMat(m.n_rows, m.n_cols, new_cp, rows, np.asarray(m.values, dtype=np.float64)[src],
+                         check=False)
+
+    def field(self, phi):
+        """PHI with its vertex columns renumbered."""
+        return self._columns(phi)
+
+    def laplacian_t(self, lap):
+        """L^T renumbered: column k = old column order[k], row indices mapped,
+        entries kept in the original order (cached per Laplacian)."""
+        if self._lap is None or self._lap[0] is not lap:
+            mat_t, flags = _laplacian_t(lap)
+            self.lap_flags = flags
+            self._lap = (lap, self._columns(mat_t, self.inverse))
+        return self._lap[1]
+
+    def restore(self, phi_new):
+        """A renumbered field back in the caller's vertex numbering."""
+        back = Renumbering(self.inverse)
+        return back._columns(phi_new)
+
+    def old_vertex(self, k):
+        return int(self.order[k]) if k >= 0 else k
 
 
 # torus stencil of gen_periodic_grid (vertex (i, j) -> j*nx + i; faces
@@ -311,13 +400,15 @@ class DomainRank:
     """Device state of one rank: owned L^T columns, two tiled buffers over
     all columns (owned + halo valid), workspace, records, halo messages."""
 
-    def __init__(self, problem, plan, precision="exact", slots=DEFAULT_SLOTS, device=None):
+    def __init__(self, problem, plan, precision="exact", slots=DEFAULT_SLOTS, device=None,
+                 renumbering=None):
         torch = _torch()
         if device is None:
             if not torch.cuda.is_available():
                 raise BackendError("no CUDA device: the engine has no CPU fallback")
             device = torch.device("cuda", torch.cuda.current_device())
         self.device = device
+        self.renumbering = renumbering
         self.lib = _lib.lib()
         self.rank = problem.rank
         self.partition = problem.partition
@@ -335,6 +426,11 @@ class DomainRank:
         self.lap = DeviceCSC.from_host(lap, self.vdtype, device)
         self.lap_c = self.lap.ft_csc()
         self.lap_flags = problem.lap_flags
+        # a renumbered partition reports NaN / pattern columns in the caller's ids
+        self.report_ids = None
+        if renumbering is not None:
+            ids = renumbering.order[self.col_begin:self.col_begin + self.n_own].astype(np.int32)
+            self.report_ids = torch.from_numpy(ids).to(device)
         self.pack = None
         if self.lap_flags == _lib.FT_LAP_UNIFORM and F.PACK_LAPLACIAN:
             self.pack, _ = F.pack_laplacian(self.lap, col_base=self.col_begin)
@@ -447,7 +543,8 @@ class DomainRank:
         lib = self.lib
         in_t = self.meta[i % 2][0]
         out_t, step_cap, slots = self._as_output((i + 1) % 2)
-        dom = _lib.FtDomain(self.col_begin, self.n_own, step_cap)
+        dom = _lib.FtDomain(self.col_begin, self.n_own, step_cap,
+                            self.report_ids.data_ptr() if self.report_ids is not None else None)
         wp, wn = ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel()
         rec = ctypes.c_void_p(self.record.data_ptr())
         if self.step_events is not None:
@@ -639,6 +736,7 @@ def evolve_partitioned(ranks, transport, params, max_steps=1000, tol=1e-4,
             for r in ranks:
                 r.set_slots(need)
         else:
+            # error columns are already in the caller's numbering (report_ids)
             _raise_step_error(ranks[0].read_trace(done + 1)[done], done)
             raise BackendError(f"partitioned step failed with status {status}")
         for r in ranks:                     # rewind: redo the failed step
@@ -658,7 +756,7 @@ def evolve_partitioned(ranks, transport, params, max_steps=1000, tol=1e-4,
     return steps - s0, trace
 
 
-def gather_field(ranks, steps_done=None, n_rows=None):
+def gather_field(ranks, steps_done=None, n_rows=None, renumbering=None):
     """Host SparseMat of the whole field from local ranks covering every
     owned range (loopback runs; a multi-process run gathers per rank)."""
     parts = sorted(ranks, key=lambda r: r.col_begin)
@@ -672,6 +770,7 @@ def gather_field(ranks, steps_done=None, n_rows=None):
         vals.append(np.asarray(h.values[:cp[-1]]))
         base += int(cp[-1])
     n = parts[-1].n_v
-    return SparseMat(n_rows or parts[0].n_rows, n, np.concatenate(ptrs),
-                     np.concatenate(idx) if idx else np.zeros(0, INDEX),
-                     np.concatenate(vals) if vals else np.zeros(0), check=False)
+    out = SparseMat(n_rows or parts[0].n_rows, n, np.concatenate(ptrs),
+                    np.concatenate(idx) if idx else np.zeros(0, INDEX),
+                    np.concatenate(vals) if vals else np.zeros(0), check=False)
+    return out if renumbering is None else renumbering.restore(out)

@@ -326,3 +326,53 @@ def test_loopback_nan_raises_like_single_gpu():
     with pytest.raises(ft.errors.NumericalBlowupError) as e2:
         D.evolve_partitioned(ranks, D.LoopbackTransport(), bad, max_steps=5, tol=0.0)
     assert str(e1.value) == str(e2.value)
+
+
+def test_morton_renumbering_shrinks_halos_and_round_trips():
+    mesh = ft.gen_icosphere(4)
+    fld = ft.init_field(mesh, np.random.default_rng(0).choice(mesh.n_vertices, 64, replace=False))
+    lap = ft.build_laplacian(mesh)
+    part = D.Partition.even(mesh.n_vertices, 4)
+    ren = D.Renumbering.morton(mesh)
+    halo = {}
+    for name, r in (("plain", None), ("morton", ren)):
+        probs = [D.local_problem(fld.phi, lap, part, k, renumbering=r) for k in range(4)]
+        halo[name] = sum(pl.halo_cols for pl in D.build_plans(probs, D.LoopbackTransport()))
+    assert halo["morton"] * 5 < halo["plain"]
+    back = ren.restore(ren.field(fld.phi))
+    assert np.array_equal(back.col_ptr, fld.phi.col_ptr)
+    assert np.array_equal(back.row_idx[:back.nnz], fld.phi.row_idx[:fld.phi.nnz])
+    assert np.array_equal(back.values[:back.nnz], fld.phi.values[:fld.phi.nnz])
+    # L^T columns keep their entries in the original order (accumulation order)
+    lt = ren.laplacian_t(lap)
+    j_new = 17
+    j_old = int(ren.order[j_new])
+    a, b = lt.col_ptr[j_new], lt.col_ptr[j_new + 1]
+    mt = ft.field._with_diagonal(lap.mat_t)
+    assert np.array_equal(ren.order[lt.row_idx[a:b]], mt.row_idx[mt.col_ptr[j_old]:mt.col_ptr[j_old + 1]])
+
+
+@pytest.mark.gpu
+def test_loopback_morton_renumbered_matches_single_gpu():
+    mesh = ft.gen_icosphere(4)
+    seeds = np.random.default_rng(0).choice(mesh.n_vertices, 64, replace=False)
+    lap = ft.build_laplacian(mesh)
+    fld = ft.init_field(mesh, seeds)
+    single, tr1 = ft.evolve(fld, lap, ft.CouplingParams(), max_steps=80, tol=0.0)
+    ren = D.Renumbering.morton(mesh)
+    part = D.Partition.even(mesh.n_vertices, 4)
+    probs = [D.local_problem(fld.phi, lap, part, r, renumbering=ren) for r in range(4)]
+    plans = D.build_plans(probs, D.LoopbackTransport())
+    ranks = [D.DomainRank(p, pl, renumbering=ren) for p, pl in zip(probs, plans)]
+    steps, tr2 = D.evolve_partitioned(ranks, D.LoopbackTransport(), ft.CouplingParams(), max_steps=80, tol=0.0)
+    assert steps == 80
+    _assert_same_field(D.gather_field(ranks, steps, renumbering=ren), single.phi)
+    assert [a.max_delta for a in tr1] == [b.max_delta for b in tr2]
+    # errors report the caller's vertex ids: same message as the single GPU
+    bad = ft.CouplingParams(dt=float("nan"))
+    with pytest.raises(ft.errors.NumericalBlowupError) as e1:
+        ft.evolve(fld, lap, bad, max_steps=3, tol=0.0)
+    ranks = [D.DomainRank(p, pl, renumbering=ren) for p, pl in zip(probs, plans)]
+    with pytest.raises(ft.errors.NumericalBlowupError) as e2:
+        D.evolve_partitioned(ranks, D.LoopbackTransport(), bad, max_steps=3, tol=0.0)
+    assert str(e1.value) == str(e2.value)
