@@ -436,7 +436,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk,
-            "gpu_launches": 5 * K + 3,   # tiers 1, 1.5, 2, 3 + finalize per step; compaction
+            "gpu_launches": 6 * K + 3,   # tiers 1, 1.5, 2a, 2b, 3 + finalize per step; compaction
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -570,10 +570,10 @@ def run_partitioned(args, world, rank, local, emulate=0):
             "cpu_baseline": None,
             "e2e": e2e,
             "clocks": clk,
-            # per step and rank: tiers 1, 1.5, 2, 3 + finalize, one pack per peer sent to,
+            # per step and rank: tiers 1, 1.5, 2a, 2b, 3 + finalize, one pack per peer sent to,
             # the combine, one unpack per peer received from; one control
             # snapshot per 16-step chunk
-            "gpu_launches": (6 + len(r0.send_msg) + len(r0.recv_msg)) * K + -(-K // 16),
+            "gpu_launches": (7 + len(r0.send_msg) + len(r0.recv_msg)) * K + -(-K // 16),
         }
         if emulate:
             line["emulated"] = True

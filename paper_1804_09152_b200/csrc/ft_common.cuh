@@ -35,7 +35,9 @@ struct Control {
     int                status;         // evolve: final status
     unsigned int       nonfinite;      // sticky: a kernel wrote a non-finite value
     long long          needed;         // capacity needed on overflow
-    long long          pad1[4];
+    int                wide8_count;    // tier-2b columns (slow_list + 3 n_v + FT_TPB)
+    int                pad2;
+    long long          pad1[3];
 };
 static_assert(sizeof(Control) % 16 == 0, "Control must stay 16B aligned");
 
@@ -46,7 +48,8 @@ struct Workspace {
     double*       tile_bm;      // [num_tiles] per-tile base mass (fast path)
     double*       vbm;          // [n_v] base mass of wide columns (tier 2)
     unsigned int* slow_mask;    // [num_tiles * FT_WARPS] wide columns of each tile
-    int*          slow_list;    // [3 n_v] tier-2 queue, tier-3 queue at +n_v, tier-1.5 queue at +2 n_v
+    int*          slow_list;    // tier-2 queue [0, n_v), tier-3 at +n_v, tier-1.5 lists at +2 n_v (128 per
+                                //   tile), tier-2b queue at +3 n_v + FT_TPB
     long long*    chunk_off;    // [num_chunks + 2] compaction chunk offsets
     double*       fin_part;     // [FT_FIN_MAX] finalize partial sums (base mass)
     double*       fin_maxd;     // [FT_FIN_MAX] finalize partial maxima
@@ -66,7 +69,7 @@ inline size_t workspace_bytes(int n_v) {
     size_t t = (size_t)num_tiles_for(n_v), c = (size_t)num_chunks_for(n_v);
     const size_t v = (size_t)n_v;
     return sizeof(Control) + t * sizeof(double) + v * sizeof(double) + t * FT_WARPS * sizeof(unsigned int) +
-           (3 * v + FT_TPB) * sizeof(int) + t * sizeof(int) + (c + 2) * sizeof(long long) + 4 * FT_FIN_MAX * sizeof(double) +
+           (4 * v + FT_TPB) * sizeof(int) + t * sizeof(int) + (c + 2) * sizeof(long long) + 4 * FT_FIN_MAX * sizeof(double) +
            t * (sizeof(double) + sizeof(int2)) + 1024;
 }
 
@@ -105,7 +108,7 @@ inline Workspace carve_workspace(void* base, int n_v) {
     w.slow_mask = (unsigned int*)p;
     p += (size_t)w.num_tiles * FT_WARPS * sizeof(unsigned int);
     w.slow_list = (int*)p;
-    p += (3 * (size_t)n_v + FT_TPB) * sizeof(int);
+    p += (4 * (size_t)n_v + FT_TPB) * sizeof(int);
     return w;
 }
 

@@ -1188,9 +1188,81 @@ __global__ void __launch_bounds__(FT_TPB, 6) gen_kernel(const StepParams p) {
     }
 }
 
+// tier 2a: the queued wide columns with at most three rows and at most
+// three entries per neighbour (~90% of them at C3): rows = min, max and the
+// one other candidate; the three Lt sums in one (u, t) pass.  Others go on
+// to tier 2b (the 8-row window) through slow_list + 3 n_v + FT_TPB.
 template <typename T, bool UNIFORM, bool IN_CANON>
-__global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p) {
-    constexpr int KW = 8;      // wider unions go to tier 3
+__device__ __forceinline__ bool wide3(int j, const StepParams& p, Win<3>& w) {
+    const int q0 = __ldg(&p.lap_ptr[j - p.j_base]);
+    const int n = __ldg(&p.lap_ptr[j - p.j_base + 1]) - q0;
+    if (n > kMD || n < 1) return false;
+    int u[kMD];
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) u[k] = (k < n) ? __ldg(&p.lap_idx[q0 + k]) : -1;
+    int2 d[kMD];
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
+    int kd = -1;
+    bool big = false;
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) {
+        if (u[k] == j) kd = k;
+        big |= d[k].y > 3;
+    }
+    if (kd < 0 || big) return false;
+    int rr[kMD][3];
+#pragma unroll
+    for (int k = 0; k < kMD; ++k)
+#pragma unroll
+        for (int t = 0; t < 3; ++t) rr[k][t] = (t < d[k].y) ? __ldg(&p.in_idx[d[k].x + t]) : INT_MAX;
+    int rlo = INT_MAX, rhi = -1;
+#pragma unroll
+    for (int k = 0; k < kMD; ++k)
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+            if (rr[k][t] != INT_MAX) { rlo = min(rlo, rr[k][t]); rhi = max(rhi, rr[k][t]); }
+    if (rlo == INT_MAX) return false;
+    const double invdeg = UNIFORM ? (n - 1 <= 32 ? c_recip[n - 1] : 1.0 / (double)(n - 1)) : 0.0;
+    double l0 = 0.0, l1 = 0.0, l2 = 0.0, p0 = 0.0, p1 = 0.0, p2 = 0.0;
+    int rmid = INT_MAX;
+    bool more = false;
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) {
+        const double l = UNIFORM ? ((k == kd) ? -1.0 : invdeg) : ((k < n) ? ldv<T>(p.lap_val, q0 + k) : 0.0);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            const int r = rr[k][t];
+            if (r == INT_MAX) continue;
+            const double a = ldv<T>(p.in_val, d[k].x + t);
+            if (r == rlo) { l0 = l0 + a * l; if (k == kd) p0 = a; }
+            else if (r == rhi) { l2 = l2 + a * l; if (k == kd) p2 = a; }
+            else {
+                if (rmid == INT_MAX) rmid = r;
+                if (r == rmid) { l1 = l1 + a * l; if (k == kd) p1 = a; }
+                else more = true;
+            }
+        }
+    }
+    if (more) return false;
+    if (rlo == rhi) {
+        w.m = 1;
+        w.rows[0] = rlo; w.lam[0] = l0; w.phi[0] = p0;
+    } else if (rmid == INT_MAX) {
+        w.m = 2;
+        w.rows[0] = rlo; w.lam[0] = l0; w.phi[0] = p0;
+        w.rows[1] = rhi; w.lam[1] = l2; w.phi[1] = p2;
+    } else {
+        w.m = 3;
+        w.rows[0] = rlo; w.lam[0] = l0; w.phi[0] = p0;
+        w.rows[1] = rmid; w.lam[1] = l1; w.phi[1] = p1;
+        w.rows[2] = rhi; w.lam[2] = l2; w.phi[2] = p2;
+    }
+    return true;
+}
+
+template <typename T, bool UNIFORM, bool IN_CANON>
+__global__ void __launch_bounds__(FT_TPB, 4) wide3_kernel(const StepParams p) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     const int n_wide = *(volatile int*)&p.ws.ctl->slow_count;
     const int lane = threadIdx.x & 31;
@@ -1200,6 +1272,55 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p) {
         const int i = rnd * stride + blockIdx.x * FT_TPB + threadIdx.x;
         const bool mine = i < n_wide;
         const int j = mine ? p.ws.slow_list[i] : 0;
+        VRes res;
+        vres_init(res);
+        Win<3> w;
+        w.m = 0;
+        unsigned int out_mask = 0;
+        bool on = false;
+        if (mine) {
+            on = !wide3<T, UNIFORM, IN_CANON>(j, p, w);
+            if (!on) {
+                process_window<3>(w, p, res, out_mask, c_recip);
+                report_flags(res, j, p);
+            }
+        }
+        const unsigned int ob = __ballot_sync(0xffffffffu, on);
+        if (ob) {
+            int qb = 0;
+            if (lane == 0) qb = atomicAdd(&p.ws.ctl->wide8_count, __popc(ob));
+            qb = __shfl_sync(0xffffffffu, qb, 0);
+            if (on) {
+                p.ws.slow_list[3 * p.n_v + FT_TPB + qb + __popc(ob & ((1u << lane) - 1u))] = j;
+                vres_init(res);
+            }
+        }
+        bool fits;
+        int excl;
+        const long long base = pool_place<T, 3>(on ? 0 : res.cnt, res, p, lane, fits, excl);
+        if (mine && !on) {
+            p.ws.vbm[j - p.j_base] = res.bm;
+            if (fits) {
+                const long long off = base + excl;
+                p.out_desc[j] = make_int2((int)off, res.cnt);
+                if (out_mask) emit_window<T, 3>(w, out_mask, off, p);
+            }
+        }
+    }
+}
+
+template <typename T, bool UNIFORM, bool IN_CANON>
+__global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p) {
+    constexpr int KW = 8;      // wider unions go to tier 3
+    if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
+    const int n_wide = *(volatile int*)&p.ws.ctl->wide8_count;   // tier-2a leftovers
+    const int lane = threadIdx.x & 31;
+    const int stride = gridDim.x * FT_TPB;
+    const int rounds = (n_wide + stride - 1) / stride;
+    for (int rnd = 0; rnd < rounds; ++rnd) {
+        const int i = rnd * stride + blockIdx.x * FT_TPB + threadIdx.x;
+        const bool mine = i < n_wide;
+        const int j = mine ? p.ws.slow_list[3 * p.n_v + FT_TPB + i] : 0;
         VRes res;
         vres_init(res);
         Win<KW> w;
@@ -1393,6 +1514,7 @@ __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizePara
     ctl->slow_count = 0;
     ctl->deep_count = 0;
     ctl->gen_count = 0;
+    ctl->wide8_count = 0;
     if (f.evolve) {
         if (status != FT_STATUS_OK) {
             ctl->done = 1;
@@ -1595,6 +1717,15 @@ static StepKernelFn pick_deep(int dtype, bool uniform, bool in_canon) {
     return in_canon ? deep_kernel<float, false, true> : deep_kernel<float, false, false>;
 }
 
+static StepKernelFn pick_wide3(int dtype, bool uniform, bool in_canon) {
+    if (dtype == FT_F64) {
+        if (uniform) return in_canon ? wide3_kernel<double, true, true> : wide3_kernel<double, true, false>;
+        return in_canon ? wide3_kernel<double, false, true> : wide3_kernel<double, false, false>;
+    }
+    if (uniform) return in_canon ? wide3_kernel<float, true, true> : wide3_kernel<float, true, false>;
+    return in_canon ? wide3_kernel<float, false, true> : wide3_kernel<float, false, false>;
+}
+
 static StepKernelFn pick_wide(int dtype, bool uniform, bool in_canon) {
     if (dtype == FT_F64) {
         if (uniform) return in_canon ? wide_kernel<double, true, true> : wide_kernel<double, true, false>;
@@ -1735,7 +1866,8 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_
     if (which & 2) {
         if (g_tier1 == 6)      // one warp per tile
             ft::pick_gen(dtype, uni, ic, packed)<<<(p.num_tiles + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
-        ft::pick_wide(dtype, uni, ic)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
+        ft::pick_wide3(dtype, uni, ic)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
+        ft::pick_wide(dtype, uni, ic)<<<g_fixup_grid / 4, FT_TPB, 0, s>>>(p);
         ft::pick_deep(dtype, uni, ic)<<<g_fixup_grid / 4, FT_TPB, 0, s>>>(p);
     }
     return cuda_check("step kernel");
