@@ -1052,7 +1052,7 @@ __device__ __forceinline__ long long pool_place(int cnt, const VRes& res, const 
 // right after the tile's tier-1 entries in its slot (the pool if they do
 // not fit), statistics into the tile's slots and vbm -- no hot atomics.
 template <typename T, bool UNIFORM, bool IN_CANON, bool PACKED>
-__global__ void __launch_bounds__(FT_TPB, 6) gen_kernel(const StepParams p) {
+__global__ void __launch_bounds__(FT_TPB, 8) gen_kernel(const StepParams p) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     const int lane = threadIdx.x & 31;
     const int nwarps = gridDim.x * FT_WARPS;
@@ -1078,13 +1078,12 @@ __global__ void __launch_bounds__(FT_TPB, 6) gen_kernel(const StepParams p) {
 #pragma unroll
             for (int k = 0; k < kMD; ++k)
                 if (u[k] == j) kd = k;
+            // rows in registers; values loaded in the accumulation pass
             int r0[kMD], r1[kMD];
-            T v0[kMD], v1[kMD];
 #pragma unroll
             for (int k = 0; k < kMD; ++k) {
-                r0[k] = INT_MAX; r1[k] = INT_MAX; v0[k] = (T)0; v1[k] = (T)0;
-                if (d[k].y > 0) { r0[k] = __ldg(&p.in_idx[d[k].x]); v0[k] = __ldg(((const T*)p.in_val) + d[k].x); }
-                if (d[k].y > 1) { r1[k] = __ldg(&p.in_idx[d[k].x + 1]); v1[k] = __ldg(((const T*)p.in_val) + d[k].x + 1); }
+                r0[k] = (d[k].y > 0) ? __ldg(&p.in_idx[d[k].x]) : INT_MAX;
+                r1[k] = (d[k].y > 1) ? __ldg(&p.in_idx[d[k].x + 1]) : INT_MAX;
             }
             int rlo = INT_MAX, rhi = -1;
 #pragma unroll
@@ -1099,7 +1098,8 @@ __global__ void __launch_bounds__(FT_TPB, 6) gen_kernel(const StepParams p) {
             for (int k = 0; k < kMD; ++k) {
                 const double l = UNIFORM ? ((k == kd) ? -1.0 : invdeg)
                                          : ((k < n) ? ldv<T>(p.lap_val, q0 + k) : 0.0);
-                const double a0 = (double)v0[k], a1 = (double)v1[k];
+                const double a0 = (r0[k] != INT_MAX) ? ldv<T>(p.in_val, d[k].x) : 0.0;
+                const double a1 = (r1[k] != INT_MAX) ? ldv<T>(p.in_val, d[k].x + 1) : 0.0;
                 if (r0[k] == rlo) { l0 = l0 + a0 * l; if (k == kd) p0 = a0; }
                 else if (r0[k] == rhi) { l1 = l1 + a0 * l; if (k == kd) p1 = a0; }
                 else if (r0[k] != INT_MAX) more = true;
