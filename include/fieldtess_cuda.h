@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define FT_ABI_VERSION 3
+#define FT_ABI_VERSION 4
 
 /* return codes (mapped onto the reference's TessError subclasses,
  * `errors.py:9-75`, by the Python host layer) */
@@ -108,6 +108,9 @@ typedef struct {
     int32_t* row_idx;     /* [capacity]                                   */
     void*    values;      /* [capacity]                                   */
     int64_t  capacity;
+    int32_t* sig;         /* [n_cols] row signature written with every
+                             column: its row if it holds one entry, -1 if
+                             more, -2 if none (the tier-1 classification)  */
 } ft_tiled;
 
 /* One step's statistics, device resident.  Mirrors StepStats

@@ -39,7 +39,7 @@ FT_STATUS_HALO_OVERFLOW = 7
 
 FT_HALO_FORCE = 1
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 
 class FtParams(ctypes.Structure):
@@ -57,7 +57,8 @@ class FtCsc(ctypes.Structure):
 class FtTiled(ctypes.Structure):
     _fields_ = [("n_rows", ctypes.c_int32), ("n_cols", ctypes.c_int32),
                 ("desc", ctypes.c_void_p), ("row_idx", ctypes.c_void_p),
-                ("values", ctypes.c_void_p), ("capacity", ctypes.c_int64)]
+                ("values", ctypes.c_void_p), ("capacity", ctypes.c_int64),
+                ("sig", ctypes.c_void_p)]
 
 
 class FtDomain(ctypes.Structure):

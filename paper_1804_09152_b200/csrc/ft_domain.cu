@@ -22,6 +22,7 @@ struct HaloParams {
     int2* desc;
     int* idx;
     void* val;
+    int* sig;            // row signatures (tier-1 classification)
     const int* cols;
     int n, slots;
     int* m_cnt;          // message: counts[n]
@@ -66,6 +67,7 @@ __global__ void __launch_bounds__(256) halo_unpack_kernel(const HaloParams h) {
     const int c = h.m_cnt[i];
     const long long off = h.region + (long long)i * h.slots;
     h.desc[h.cols[i]] = make_int2((int)off, c);
+    h.sig[h.cols[i]] = c == 1 ? h.m_rows[(size_t)i * h.slots] : (c == 0 ? -2 : -1);
     const size_t o = (size_t)i * h.slots;
     T* v = (T*)h.val;
     const T* mv = (const T*)h.m_vals;
@@ -154,9 +156,9 @@ __global__ void control_kernel(Control* ctl, int set_steps, long long* out) {
 
 static bool fill_halo(HaloParams& h, const ft_tiled* t, const int32_t* cols, int32_t n, int32_t slots,
                       int32_t dtype, const void* msg, void* workspace, int32_t flags) {
-    if (!t || !cols || !msg || !workspace || n < 0 || slots < 1) return false;
+    if (!t || !t->sig || !cols || !msg || !workspace || n < 0 || slots < 1) return false;
     if (dtype != FT_F64 && dtype != FT_F32) return false;
-    h.desc = (int2*)t->desc; h.idx = t->row_idx; h.val = t->values;
+    h.desc = (int2*)t->desc; h.idx = t->row_idx; h.val = t->values; h.sig = t->sig;
     h.cols = cols; h.n = n; h.slots = slots;
     char* m = (char*)msg;
     h.m_cnt = (int*)m;

@@ -61,9 +61,11 @@ struct StepParams {
     const int2* __restrict__ in_desc;   // tiled input
     const int* __restrict__ in_idx;
     const void* __restrict__ in_val;
+    const int* __restrict__ in_sig;     // tiled input: row signature per column
     int2* __restrict__ out_desc;
     int* __restrict__ out_idx;
     void* __restrict__ out_val;
+    int* __restrict__ out_sig;
     long long cap;
     double w, a, e, eb, mu, dt;
     Workspace ws;
@@ -170,6 +172,19 @@ __device__ __forceinline__ void gather(Win<K>& w, int j, int lo, const StepParam
             win_insert<K>(w, r, ph * l, diag, ph);
         }
     }
+}
+
+// row signature of an output column: its row if it holds one entry, -1 if
+// more, -2 if none (tier 1 classifies from the neighbours' signatures)
+__device__ __forceinline__ int sig_of(int cnt, int row1) { return cnt == 1 ? row1 : (cnt == 0 ? -2 : -1); }
+
+template <int K>
+__device__ __forceinline__ int window_row1(const int* rows, unsigned int out_mask) {
+    int r = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+        if (out_mask & (1u << i)) r = rows[i];
+    return r;
 }
 
 // ---------------------------------------------------------------------------
@@ -668,157 +683,6 @@ __device__ __forceinline__ int load_lrow(const StepParams& p, int jl, int j, boo
 }
 
 // ---------------------------------------------------------------------------
-// tier 1, in place (FT_TIER1=3): every column is classified first (single-
-// row neighbourhood -> the exact closed form); the window code runs only
-// when some lane of the warp needs it, and then as ONE pass: with at most
-// two distinct rows in the neighbourhood they are the min and the max of
-// the candidate rows, and both Lt sums accumulate in the same (u, t) loop,
-// in the reference order.  Measured 4% slower than the split variant at C3.
-
-template <typename T, bool UNIFORM, bool IN_CANON, bool PACKED>
-__global__ void __launch_bounds__(FT_TPB, 6) step_kernel3(const StepParams p) {
-    __shared__ double s_wbm[FT_WARPS];
-    __shared__ double s_wmax[FT_WARPS];
-    __shared__ int s_wskel[FT_WARPS];
-    __shared__ int s_scan[FT_WARPS];
-    __shared__ long long s_base;
-
-    if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int tile = blockIdx.x;
-    const int jl = tile * FT_TPB + tid;
-    const int j = p.j_base + jl;
-    const bool active = jl < p.n_v;
-
-    int q0 = 0;
-    int u[kMD];
-    const int n = load_lrow<PACKED>(p, jl, j, active, u, q0);
-    bool wide = active && n == 0;
-    int2 d[kMD];
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
-    int kd = -1;
-    bool multi = false;
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) {
-        if (u[k] == j) kd = k;
-        wide |= d[k].y > 2;
-        multi |= d[k].y > 1;
-    }
-    if (active && kd < 0) wide = true;
-    int r0[kMD], r1[kMD];
-    T v0[kMD], v1[kMD];
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) {
-        r0[k] = INT_MAX; r1[k] = INT_MAX; v0[k] = (T)0; v1[k] = (T)0;
-        if (!wide && d[k].y > 0) { r0[k] = __ldg(&p.in_idx[d[k].x]); v0[k] = __ldg(((const T*)p.in_val) + d[k].x); }
-        if (!wide && d[k].y > 1) { r1[k] = __ldg(&p.in_idx[d[k].x + 1]); v1[k] = __ldg(((const T*)p.in_val) + d[k].x + 1); }
-    }
-    // classification: one layer row in the whole neighbourhood?
-    int rs = INT_MAX;
-    double phs = 0.0;
-#pragma unroll
-    for (int k = 0; k < kMD; ++k)
-        if (k == kd) { rs = r0[k]; phs = (double)v0[k]; }
-    bool same = true, fin = true;
-    double lam_f = 0.0;
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) {
-        same &= (r0[k] == INT_MAX) || (r0[k] == rs);
-        fin &= isfinite((double)v0[k]);
-        if (!UNIFORM && k < n) lam_f = lam_f + (double)v0[k] * ldv<T>(p.lap_val, q0 + k);
-    }
-    const bool fast = active && !wide && !multi && p.finite && rs != INT_MAX && phs > 0.0 && same && fin &&
-                      (UNIFORM || isfinite(lam_f));
-
-    VRes res;
-    vres_init(res);
-    Win<2> w;
-    w.m = 0;
-    unsigned int out_mask = 0;
-    if (fast) {
-        double v = phs;
-        if (v > 1.0) v = 1.0;
-        const double s = 0.0 + v;
-        const double nv = v * (1.0 / s);
-        res.nskel = 1;
-        if (nv != 0.0) {
-            res.cnt = 1;
-            out_mask = 1u;
-            if (rs == 0) res.bm = nv;
-        }
-        res.maxd = fabs(nv - phs);
-        w.rows[0] = rs;
-        w.lam[0] = nv;
-        w.m = 1;
-    }
-    const bool gen = active && !wide && !fast;
-    if (__any_sync(0xffffffffu, gen)) {
-        if (gen) {
-            // the (at most two) rows: min and max of the candidates
-            int rlo = INT_MAX, rhi = -1;
-#pragma unroll
-            for (int k = 0; k < kMD; ++k) {
-                if (r0[k] != INT_MAX) { rlo = min(rlo, r0[k]); rhi = max(rhi, r0[k]); }
-                if (r1[k] != INT_MAX) { rlo = min(rlo, r1[k]); rhi = max(rhi, r1[k]); }
-            }
-            const double invdeg = UNIFORM ? (n - 1 <= 32 ? c_recip[n - 1] : 1.0 / (double)(n - 1)) : 0.0;
-            double l0 = 0.0, l1 = 0.0, p0 = 0.0, p1 = 0.0;
-            bool more = false;
-#pragma unroll
-            for (int k = 0; k < kMD; ++k) {
-                const double l = UNIFORM ? ((k == kd) ? -1.0 : invdeg)
-                                         : ((k < n) ? ldv<T>(p.lap_val, q0 + k) : 0.0);
-                const double a0 = (double)v0[k], a1 = (double)v1[k];
-                if (r0[k] == rlo) { l0 = l0 + a0 * l; if (k == kd) p0 = a0; }
-                else if (r0[k] == rhi) { l1 = l1 + a0 * l; if (k == kd) p1 = a0; }
-                else if (r0[k] != INT_MAX) more = true;
-                if (r1[k] == rlo) { l0 = l0 + a1 * l; if (k == kd) p0 = a1; }
-                else if (r1[k] == rhi) { l1 = l1 + a1 * l; if (k == kd) p1 = a1; }
-                else if (r1[k] != INT_MAX) more = true;
-            }
-            if (more || rlo == INT_MAX) {
-                wide = true;
-            } else {
-                w.rows[0] = rlo; w.lam[0] = l0; w.phi[0] = p0;
-                w.rows[1] = rhi; w.lam[1] = l1; w.phi[1] = p1;
-                w.m = (rhi == rlo) ? 1 : 2;
-                if (w.m == 1) { w.rows[1] = INT_MAX; w.lam[1] = 0.0; w.phi[1] = 0.0; }
-            }
-        }
-        if (__any_sync(0xffffffffu, gen && !wide)) {
-            if (gen && !wide) {
-                process_window<2>(w, p, res, out_mask, c_recip);
-                report_flags(res, j, p);
-            }
-        }
-    }
-    if (wide) vres_init(res);
-
-    // tier-2 queue: one atomic per CTA
-    __shared__ int s_wq[FT_WARPS + 1];
-    const unsigned int wbits = __ballot_sync(0xffffffffu, wide && active);
-    if (lane == 0) s_wq[warp] = __popc(wbits);
-    __syncthreads();
-    int wpre = 0, wtot = 0;
-#pragma unroll
-    for (int q = 0; q < FT_WARPS; ++q) {
-        if (q < warp) wpre += s_wq[q];
-        wtot += s_wq[q];
-    }
-    if (tid == 0) s_wq[FT_WARPS] = wtot ? atomicAdd(&p.ws.ctl->slow_count, wtot) : 0;
-    __syncthreads();
-    if (wide && active) p.ws.slow_list[s_wq[FT_WARPS] + wpre + __popc(wbits & ((1u << lane) - 1u))] = j;
-    if (lane == 0) p.ws.slow_mask[(size_t)tile * FT_WARPS + warp] = wbits;
-    const TileOut o = tile_epilogue<false>(res.cnt, res.nskel, res.bm, res.maxd, tile, &p.ws.tile_bm[tile], p,
-                                           s_scan, s_wbm, s_wmax, s_wskel, &s_base);
-    if (!active || wide || o.base < 0) return;
-    const long long off = o.base + o.local_off;
-    p.out_desc[j] = make_int2((int)off, res.cnt);
-    if (out_mask) emit_window<T, 2>(w, out_mask, off, p);
-}
-
-// ---------------------------------------------------------------------------
 // tier 1, split (default): classification and the closed form only.
 //
 // A column whose neighbourhood is one layer row (every non-empty neighbour
@@ -852,39 +716,63 @@ __global__ void __launch_bounds__(FT_TPB, 8) step_kernel6(const StepParams p) {
     int u[kMD];
     const int n = load_lrow<PACKED>(p, jl, j, active, u, q0);
     bool wide = active && n == 0;
-    int2 d[kMD];
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
     int kd = -1;
-    bool multi = false;
-    int2 dself = make_int2(0, 0);
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) {
-        if (u[k] == j) { kd = k; dself = d[k]; }
-        wide |= d[k].y > 2;
-        multi |= d[k].y > 1;
-    }
-    if (active && kd < 0) wide = true;
-    bool cand = active && !wide && !multi && p.finite && dself.y == 1;
-    int rs = INT_MAX;
-    double phs = 0.0;
-    if (cand) {
-        rs = __ldg(&p.in_idx[dself.x]);
-        phs = ldv<T>(p.in_val, dself.x);
-    }
-    bool same = true;
 #pragma unroll
     for (int k = 0; k < kMD; ++k)
-        if (cand && d[k].y == 1 && k != kd) same &= __ldg(&p.in_idx[d[k].x]) == rs;
-    cand = cand && same && phs > 0.0;
+        if (u[k] == j) kd = k;
+    if (active && kd < 0) wide = true;
+    int rs = INT_MAX;
+    double phs = 0.0;
+    bool cand;
+    if (IN_CANON) {
+        // canonical input: descriptors from col_ptr, rows by loads
+        int2 d[kMD];
+#pragma unroll
+        for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<true>(p, u[k]) : make_int2(0, 0);
+        bool multi = false;
+        int2 dself = make_int2(0, 0);
+#pragma unroll
+        for (int k = 0; k < kMD; ++k) {
+            if (k == kd) dself = d[k];
+            multi |= d[k].y > 1;
+        }
+        cand = active && !wide && !multi && p.finite && dself.y == 1;
+        if (cand) {
+            rs = __ldg(&p.in_idx[dself.x]);
+            phs = ldv<T>(p.in_val, dself.x);
+        }
+        bool same = true;
+#pragma unroll
+        for (int k = 0; k < kMD; ++k)
+            if (cand && d[k].y == 1 && k != kd) same &= __ldg(&p.in_idx[d[k].x]) == rs;
+        cand = cand && same && phs > 0.0;
+    } else {
+        // tiled input: the neighbours' row signatures (their own descriptors
+        // are not needed), the column's value through its descriptor
+        int sg[kMD];
+#pragma unroll
+        for (int k = 0; k < kMD; ++k) sg[k] = (k < n) ? __ldg(&p.in_sig[u[k]]) : -2;
+        const int2 dself = active ? __ldg(&p.in_desc[j]) : make_int2(0, 0);
+#pragma unroll
+        for (int k = 0; k < kMD; ++k)
+            if (k == kd) rs = sg[k];
+        cand = active && !wide && p.finite && rs >= 0;
+        bool same = true;
+#pragma unroll
+        for (int k = 0; k < kMD; ++k) same &= (sg[k] == -2) || (sg[k] == rs);
+        if (cand) phs = ldv<T>(p.in_val, dself.x);
+        cand = cand && same && phs > 0.0;
+    }
     if (chk && cand) {
+        // Lt(rs, j) must be finite for the closed form: read the values
         bool fin = true;
         double lam = 0.0;
         const double invdeg = UNIFORM ? (n - 1 <= 32 ? c_recip[n - 1] : 1.0 / (double)(n - 1)) : 0.0;
 #pragma unroll
         for (int k = 0; k < kMD; ++k) {
-            if (d[k].y == 1) {
-                const double v = ldv<T>(p.in_val, d[k].x);
+            const int2 dk = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
+            if (dk.y == 1) {
+                const double v = ldv<T>(p.in_val, dk.x);
                 fin &= isfinite(v);
                 const double l = UNIFORM ? ((k == kd) ? -1.0 : invdeg) : ldv<T>(p.lap_val, q0 + k);
                 lam = lam + v * l;
@@ -941,6 +829,7 @@ __global__ void __launch_bounds__(FT_TPB, 8) step_kernel6(const StepParams p) {
     if (!fast || o.base < 0) return;
     const long long off = o.base + o.local_off;
     p.out_desc[j] = make_int2((int)off, res.cnt);
+    p.out_sig[j] = sig_of(res.cnt, rs);
     if (res.cnt) {
         p.out_idx[off] = rs;
         ((T*)p.out_val)[off] = (T)nv;
@@ -1075,9 +964,12 @@ __global__ void __launch_bounds__(FT_TPB, 8) gen_kernel(const StepParams p) {
 #pragma unroll
             for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
             int kd = -1;
+            bool big = false;          // a neighbour with more than two entries
 #pragma unroll
-            for (int k = 0; k < kMD; ++k)
+            for (int k = 0; k < kMD; ++k) {
                 if (u[k] == j) kd = k;
+                big |= d[k].y > 2;
+            }
             // rows in registers; values loaded in the accumulation pass
             int r0[kMD], r1[kMD];
 #pragma unroll
@@ -1107,7 +999,7 @@ __global__ void __launch_bounds__(FT_TPB, 8) gen_kernel(const StepParams p) {
                 else if (r1[k] == rhi) { l1 = l1 + a1 * l; if (k == kd) p1 = a1; }
                 else if (r1[k] != INT_MAX) more = true;
             }
-            const bool wide = mine && (more || rlo == INT_MAX);
+            const bool wide = mine && (more || big || rlo == INT_MAX);
             Win<2> w;
             w.rows[0] = rlo; w.lam[0] = l0; w.phi[0] = p0;
             w.rows[1] = rhi; w.lam[1] = l1; w.phi[1] = p1;
@@ -1169,6 +1061,7 @@ __global__ void __launch_bounds__(FT_TPB, 8) gen_kernel(const StepParams p) {
                 if (base >= 0) {
                     const long long off = base + incl - cnt;
                     p.out_desc[j] = make_int2((int)off, res.cnt);
+                    p.out_sig[j] = sig_of(res.cnt, window_row1<2>(w.rows, out_mask));
                     if (out_mask) emit_window<T, 2>(w, out_mask, off, p);
                 }
             }
@@ -1303,6 +1196,7 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide3_kernel(const StepParams p) {
             if (fits) {
                 const long long off = base + excl;
                 p.out_desc[j] = make_int2((int)off, res.cnt);
+                p.out_sig[j] = sig_of(res.cnt, window_row1<3>(w.rows, out_mask));
                 if (out_mask) emit_window<T, 3>(w, out_mask, off, p);
             }
         }
@@ -1352,6 +1246,7 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p) {
             if (fits) {
                 const long long off = base + excl;
                 p.out_desc[j] = make_int2((int)off, res.cnt);
+                p.out_sig[j] = sig_of(res.cnt, window_row1<KW>(w.rows, out_mask));
                 if (out_mask) emit_window<T, KW>(w, out_mask, off, p);
             }
         }
@@ -1384,7 +1279,9 @@ __global__ void __launch_bounds__(FT_TPB) deep_kernel(const StepParams p) {
             if (fits) {
                 const long long off = base + excl;
                 p.out_desc[j] = make_int2((int)off, res.cnt);
-                if (res.cnt) vertex_slow<T, 8, UNIFORM, IN_CANON>(j, p, res, off, true);
+                const int total = res.cnt;
+                if (total) vertex_slow<T, 8, UNIFORM, IN_CANON>(j, p, res, off, true);
+                p.out_sig[j] = sig_of(total, total == 1 ? p.out_idx[off] : 0);
             }
         }
     }
@@ -1697,16 +1594,6 @@ static StepKernelFn pick_gen(int dtype, bool uniform, bool in_canon, bool packed
     return in_canon ? gen_kernel<float, false, true, false> : gen_kernel<float, false, false, false>;
 }
 
-static StepKernelFn pick_step_v3(int dtype, bool uniform, bool in_canon, bool packed) {
-    if (dtype == FT_F64) {
-        if (uniform && packed) return in_canon ? step_kernel3<double, true, true, true> : step_kernel3<double, true, false, true>;
-        if (uniform) return in_canon ? step_kernel3<double, true, true, false> : step_kernel3<double, true, false, false>;
-        return in_canon ? step_kernel3<double, false, true, false> : step_kernel3<double, false, false, false>;
-    }
-    if (uniform && packed) return in_canon ? step_kernel3<float, true, true, true> : step_kernel3<float, true, false, true>;
-    if (uniform) return in_canon ? step_kernel3<float, true, true, false> : step_kernel3<float, true, false, false>;
-    return in_canon ? step_kernel3<float, false, true, false> : step_kernel3<float, false, false, false>;
-}
 
 static StepKernelFn pick_deep(int dtype, bool uniform, bool in_canon) {
     if (dtype == FT_F64) {
@@ -1776,7 +1663,7 @@ extern "C" int64_t ft_tiled_min_capacity(int32_t n_vertices) {
 }
 
 static int check_tiled(const ft_tiled* t, int n_rows, int n_cols, int n_own) {
-    if (!t || !t->desc || !t->row_idx || !t->values) return set_err(FT_ERR_ARG, "null tiled buffer");
+    if (!t || !t->desc || !t->row_idx || !t->values || !t->sig) return set_err(FT_ERR_ARG, "null tiled buffer");
     if (t->n_rows != n_rows || t->n_cols != n_cols) return set_err(FT_ERR_SHAPE, "tiled buffer has wrong shape");
     if (t->capacity < ft_tiled_min_capacity(n_own) || t->capacity > (int64_t)INT_MAX)
         return set_err(FT_ERR_ARG, "tiled capacity out of range");
@@ -1785,7 +1672,6 @@ static int check_tiled(const ft_tiled* t, int n_rows, int n_cols, int n_own) {
 }
 
 static int g_window = 0;
-static int g_tier1 = 6;     // tier-1 variant: 6 split (default), 3 in place (FT_TIER1=3)
 static int g_fixup_grid = 4 * 148;
 static int g_fin_ctas = 4 * 148;   // finalize: ~one tile per thread at C3, <= FT_FIN_MAX
 
@@ -1796,8 +1682,6 @@ static int window_size() {
         for (int n = 1; n <= 32; ++n) h[n] = 1.0 / (double)n;
         cudaMemcpyToSymbol(ft::c_recip, h, sizeof(h));
         g_window = 2;
-        const char* t1 = getenv("FT_TIER1");
-        g_tier1 = (t1 && atoi(t1) == 3) ? 3 : 6;
         int dev = 0, sms = 148;
         if (cudaGetDevice(&dev) == cudaSuccess &&
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
@@ -1844,9 +1728,12 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_
     p.in_desc = in_canon ? nullptr : (const int2*)in_tiled->desc;
     p.in_idx = in_canon ? in_canon->row_idx : in_tiled->row_idx;
     p.in_val = in_canon ? in_canon->values : in_tiled->values;
+    p.in_sig = in_canon ? nullptr : in_tiled->sig;
+    if (!in_canon && !in_tiled->sig) return set_err(FT_ERR_ARG, "null tiled buffer");
     p.out_desc = (int2*)out->desc;
     p.out_idx = out->row_idx;
     p.out_val = out->values;
+    p.out_sig = out->sig;
     p.cap = step_cap;
     p.w = prm->w; p.a = prm->a; p.e = prm->e; p.eb = prm->e_base; p.mu = prm->mu; p.dt = prm->dt;
     p.ws = ft::carve_workspace(workspace, n_own);
@@ -1860,12 +1747,11 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_
     window_size();
     p.force_check = (lap_flags & FT_LAP_CHECK_FINITE) != 0;
     p.report_ids = dom ? dom->report_ids : nullptr;
-    const ft::StepKernelFn k = g_tier1 == 3 ? ft::pick_step_v3(dtype, uni, ic, packed)
-                                            : ft::pick_step_v6(dtype, uni, ic, packed);
+    const ft::StepKernelFn k = ft::pick_step_v6(dtype, uni, ic, packed);
     if (which & 1) k<<<p.num_tiles, FT_TPB, 0, s>>>(p);
     if (which & 2) {
-        if (g_tier1 == 6)      // one warp per tile
-            ft::pick_gen(dtype, uni, ic, packed)<<<(p.num_tiles + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
+        // tier 1.5, one warp per tile
+        ft::pick_gen(dtype, uni, ic, packed)<<<(p.num_tiles + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
         ft::pick_wide3(dtype, uni, ic)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
         ft::pick_wide(dtype, uni, ic)<<<g_fixup_grid / 4, FT_TPB, 0, s>>>(p);
         ft::pick_deep(dtype, uni, ic)<<<g_fixup_grid / 4, FT_TPB, 0, s>>>(p);
@@ -1969,7 +1855,7 @@ extern "C" int ft_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi
 constexpr int kGraphSteps = 16;
 
 struct GraphKey {
-    const void* ptrs[12];
+    const void* ptrs[14];
     long long caps[3];
     double prm[8];
     int ints[5];
@@ -2051,9 +1937,9 @@ extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* p
         memset(&k, 0, sizeof(k));
         if (graph_stream_init() != FT_OK) return cuda_check("ft_evolve(graph stream)");
         cudaStream_t gs = g_gstream;
-        const void* ptrs[12] = {lap_t->col_ptr, lap_t->row_idx, lap_t->values, work_a->desc, work_a->row_idx,
+        const void* ptrs[14] = {lap_t->col_ptr, lap_t->row_idx, lap_t->values, work_a->desc, work_a->row_idx,
                                 work_a->values, work_b->desc, work_b->row_idx, work_b->values, workspace,
-                                trace, nullptr};
+                                trace, work_a->sig, work_b->sig, nullptr};
         memcpy(k.ptrs, ptrs, sizeof(ptrs));
         k.caps[0] = work_a->capacity; k.caps[1] = work_b->capacity; k.caps[2] = (long long)ws_bytes;
         const double prm[8] = {params->w, params->a, params->e, params->e_base, params->mu, params->dt, tol,

@@ -495,6 +495,7 @@ class DomainRank:
             buf = DeviceTiled(self.n_rows, self.n_v, capacity, self.vdtype, self.device)
             if old is not None:
                 buf.desc.copy_(old.desc)
+                buf.sig.copy_(old.sig)
                 buf.row_idx[:old.capacity].copy_(old.row_idx)
                 buf.values[:old.capacity].copy_(old.values)
             self.bufs[k] = buf
@@ -510,6 +511,11 @@ class DomainRank:
         counts = torch.from_numpy(np.diff(problem.col_ptr).astype(np.int32)).to(self.device)
         desc[cols, 0] = starts
         desc[cols, 1] = counts
+        # row signatures (tier-1 classification): row of a single entry, -1 more, -2 none
+        cnt_h = np.diff(problem.col_ptr)
+        first = problem.row_idx[np.minimum(problem.col_ptr[:-1], max(nnz - 1, 0))] if nnz else np.zeros(cnt_h.size)
+        sig = np.where(cnt_h == 1, first, np.where(cnt_h == 0, -2, -1)).astype(np.int32)
+        buf.sig[cols] = torch.from_numpy(sig).to(self.device)
         if nnz:
             buf.row_idx[:nnz].copy_(torch.from_numpy(problem.row_idx[:nnz]).to(self.device))
             buf.values[:nnz].copy_(torch.from_numpy(problem.values[:nnz]).to(self.device,

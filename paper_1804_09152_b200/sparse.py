@@ -305,7 +305,7 @@ class DeviceTiled:
     include/fieldtess_cuda.h): per-column (start, count) descriptors, entries
     in per-tile slots plus an overflow pool.  Used between Euler steps."""
 
-    __slots__ = ("n_rows", "n_cols", "desc", "row_idx", "values")
+    __slots__ = ("n_rows", "n_cols", "desc", "row_idx", "values", "sig")
 
     def __init__(self, n_rows, n_cols, capacity, dtype, device):
         torch = _torch()
@@ -314,6 +314,8 @@ class DeviceTiled:
         self.desc = torch.zeros(2 * max(n_cols, 1), dtype=torch.int32, device=device)
         self.row_idx = torch.empty(int(capacity), dtype=torch.int32, device=device)
         self.values = torch.empty(int(capacity), dtype=dtype, device=device)
+        # row signature per column (row of a single entry, -1 more, -2 none)
+        self.sig = torch.full((max(n_cols, 1),), -2, dtype=torch.int32, device=device)
 
     @property
     def capacity(self):
@@ -331,4 +333,4 @@ class DeviceTiled:
     def ft_tiled(self):
         from ._lib import FtTiled
         return FtTiled(self.n_rows, self.n_cols, self.desc.data_ptr(), self.row_idx.data_ptr(),
-                       self.values.data_ptr(), self.capacity)
+                       self.values.data_ptr(), self.capacity, self.sig.data_ptr())
