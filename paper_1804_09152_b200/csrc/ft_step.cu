@@ -1085,14 +1085,12 @@ __global__ void __launch_bounds__(FT_TPB, 8) gen_kernel(const StepParams p) {
 // three entries per neighbour (~90% of them at C3): rows = min, max and the
 // one other candidate; the three Lt sums in one (u, t) pass.  Others go on
 // to tier 2b (the 8-row window) through slow_list + 3 n_v + FT_TPB.
-template <typename T, bool UNIFORM, bool IN_CANON>
+template <typename T, bool UNIFORM, bool IN_CANON, bool PACKED>
 __device__ __forceinline__ bool wide3(int j, const StepParams& p, Win<3>& w) {
-    const int q0 = __ldg(&p.lap_ptr[j - p.j_base]);
-    const int n = __ldg(&p.lap_ptr[j - p.j_base + 1]) - q0;
-    if (n > kMD || n < 1) return false;
+    int q0 = 0;
     int u[kMD];
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) u[k] = (k < n) ? __ldg(&p.lap_idx[q0 + k]) : -1;
+    const int n = load_lrow<PACKED>(p, j - p.j_base, j, true, u, q0);
+    if (n == 0) return false;
     int2 d[kMD];
 #pragma unroll
     for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
@@ -1154,7 +1152,7 @@ __device__ __forceinline__ bool wide3(int j, const StepParams& p, Win<3>& w) {
     return true;
 }
 
-template <typename T, bool UNIFORM, bool IN_CANON>
+template <typename T, bool UNIFORM, bool IN_CANON, bool PACKED>
 __global__ void __launch_bounds__(FT_TPB, 4) wide3_kernel(const StepParams p) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     const int n_wide = *(volatile int*)&p.ws.ctl->slow_count;
@@ -1172,7 +1170,7 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide3_kernel(const StepParams p) {
         unsigned int out_mask = 0;
         bool on = false;
         if (mine) {
-            on = !wide3<T, UNIFORM, IN_CANON>(j, p, w);
+            on = !wide3<T, UNIFORM, IN_CANON, PACKED>(j, p, w);
             if (!on) {
                 process_window<3>(w, p, res, out_mask, c_recip);
                 report_flags(res, j, p);
@@ -1604,13 +1602,15 @@ static StepKernelFn pick_deep(int dtype, bool uniform, bool in_canon) {
     return in_canon ? deep_kernel<float, false, true> : deep_kernel<float, false, false>;
 }
 
-static StepKernelFn pick_wide3(int dtype, bool uniform, bool in_canon) {
+static StepKernelFn pick_wide3(int dtype, bool uniform, bool in_canon, bool packed) {
     if (dtype == FT_F64) {
-        if (uniform) return in_canon ? wide3_kernel<double, true, true> : wide3_kernel<double, true, false>;
-        return in_canon ? wide3_kernel<double, false, true> : wide3_kernel<double, false, false>;
+        if (uniform && packed) return in_canon ? wide3_kernel<double, true, true, true> : wide3_kernel<double, true, false, true>;
+        if (uniform) return in_canon ? wide3_kernel<double, true, true, false> : wide3_kernel<double, true, false, false>;
+        return in_canon ? wide3_kernel<double, false, true, false> : wide3_kernel<double, false, false, false>;
     }
-    if (uniform) return in_canon ? wide3_kernel<float, true, true> : wide3_kernel<float, true, false>;
-    return in_canon ? wide3_kernel<float, false, true> : wide3_kernel<float, false, false>;
+    if (uniform && packed) return in_canon ? wide3_kernel<float, true, true, true> : wide3_kernel<float, true, false, true>;
+    if (uniform) return in_canon ? wide3_kernel<float, true, true, false> : wide3_kernel<float, true, false, false>;
+    return in_canon ? wide3_kernel<float, false, true, false> : wide3_kernel<float, false, false, false>;
 }
 
 static StepKernelFn pick_wide(int dtype, bool uniform, bool in_canon) {
@@ -1752,8 +1752,8 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_
     if (which & 2) {
         // tier 1.5, one warp per tile
         ft::pick_gen(dtype, uni, ic, packed)<<<(p.num_tiles + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
-        ft::pick_wide3(dtype, uni, ic)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
-        ft::pick_wide(dtype, uni, ic)<<<g_fixup_grid / 4, FT_TPB, 0, s>>>(p);
+        ft::pick_wide3(dtype, uni, ic, packed)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
+        ft::pick_wide(dtype, uni, ic)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
         ft::pick_deep(dtype, uni, ic)<<<g_fixup_grid / 4, FT_TPB, 0, s>>>(p);
     }
     return cuda_check("step kernel");
