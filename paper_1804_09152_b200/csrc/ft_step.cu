@@ -941,7 +941,7 @@ __device__ __forceinline__ long long pool_place(int cnt, const VRes& res, const 
 // right after the tile's tier-1 entries in its slot (the pool if they do
 // not fit), statistics into the tile's slots and vbm -- no hot atomics.
 template <typename T, bool UNIFORM, bool IN_CANON, bool PACKED>
-__global__ void __launch_bounds__(FT_TPB, 8) gen_kernel(const StepParams p) {
+__global__ void __launch_bounds__(FT_TPB, 10) gen_kernel(const StepParams p) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     const int lane = threadIdx.x & 31;
     const int nwarps = gridDim.x * FT_WARPS;
