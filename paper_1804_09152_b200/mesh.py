@@ -66,9 +66,9 @@ class TriMesh:
         self._cache["face_area"] = area
         self._cache["face_normal"] = np.where(nrm[:, None] > 0, cr / safe[:, None], 0.0)
         self._cache["face_barycenter"] = p[f[:, 0]] + (e1 + e2) / 3.0
-        va = np.zeros(p.shape[0])
-        np.add.at(va, f.ravel(), np.repeat(area / 3.0, 3))
-        self._cache["vertex_area"] = va
+        # bincount adds in input order per bin, exactly like np.add.at
+        self._cache["vertex_area"] = np.bincount(f.ravel(), weights=np.repeat(area / 3.0, 3),
+                                                 minlength=p.shape[0]).astype(np.float64)
         return self._cache
 
     def _incidences(self):
@@ -141,15 +141,41 @@ class TriMesh:
     def bbox_diagonal(self):
         return float(np.linalg.norm(self.positions.max(axis=0) - self.positions.min(axis=0)))
 
+    _WRAP_CHUNK = 1 << 20
+
     def wrap_deltas(self, deltas):
         """Shortest lattice representatives of difference vectors (identity on
-        non-periodic meshes); mesh.py:136-157."""
+        non-periodic meshes); mesh.py:136-157.  Row-wise, so large inputs go
+        in chunks (identical results, cache-sized temporaries)."""
         if self.period_vectors is None:
             return deltas
         deltas = np.atleast_2d(np.asarray(deltas, dtype=np.float64))
+        if deltas.shape[0] > self._WRAP_CHUNK:
+            return np.concatenate([self._wrap(deltas[i:i + self._WRAP_CHUNK])
+                                   for i in range(0, deltas.shape[0], self._WRAP_CHUNK)])
+        return self._wrap(deltas)
+
+    def _wrap(self, deltas):
         basis = self.period_vectors[:, :2].T
         frac = np.linalg.solve(basis, deltas[:, :2].T).T
         near = np.floor(frac + 0.5)
+        # A row with lattice coordinate 0 that is shorter than a quarter of the
+        # shortest lattice offset has (0, 0) as its strict minimum whatever the
+        # rounding: its result is deltas - 0 = deltas.  Only the others (faces
+        # across the seams) run the 9-candidate search.
+        if not hasattr(self, "_wrap_r2"):
+            offs = [np.array([di, dj]) @ self.period_vectors for di in (-1.0, 0.0, 1.0)
+                    for dj in (-1.0, 0.0, 1.0) if (di, dj) != (0.0, 0.0)]
+            self._wrap_r2 = (min(float(np.dot(o, o)) for o in offs) ** 0.5 / 4.0) ** 2
+        short = (near[:, 0] == 0) & (near[:, 1] == 0) & (np.einsum("ij,ij->i", deltas, deltas) < self._wrap_r2)
+        if short.all():
+            return deltas.copy()
+        out = deltas.copy()
+        rest = ~short
+        out[rest] = self._wrap_search(deltas[rest], near[rest])
+        return out
+
+    def _wrap_search(self, deltas, near):
         best = best_d2 = None
         for di in (-1.0, 0.0, 1.0):
             for dj in (-1.0, 0.0, 1.0):
