@@ -16,11 +16,14 @@
  *     values `double` (FT_F64) or `float` (FT_F32).  The layered field PHI is
  *     (n_cells+1) x n_vertices: column = vertex, row 0 = base layer,
  *     row r = cell r-1 (`field.py:95-130`).
- *   - Between Euler steps the engine keeps PHI "tiled" (ft_tiled): column
- *     j is addressed by a descriptor (start, count) and the entries of each
- *     128-vertex tile sit in that tile's fixed slot (or in a shared pool when
- *     the slot is full).  This removes every inter-CTA dependency from the
- *     step; canonical CSC is produced by ft_compact at the API boundary.
+ *   - Between Euler steps the engine keeps PHI in a hybrid layout
+ *     (ft_tiled): a column with at most two entries lives in four dense
+ *     per-column arrays (row signature, second row, first value, second
+ *     value); a wider column lives in an overflow pool.  A kernel reads a
+ *     neighbour's entries with no descriptor indirection and writes its own
+ *     column at a fixed address, so the step has no inter-CTA dependency
+ *     and no placement scan; canonical CSC is produced by ft_compact at the
+ *     API boundary.
  *   - The Laplacian is passed as `lap.mat_t` (L^T in CSC), which is
  *     byte-identical to L in CSR with ascending neighbour index including
  *     the diagonal (`mesh.py:379-431`).
@@ -41,7 +44,7 @@
 extern "C" {
 #endif
 
-#define FT_ABI_VERSION 4
+#define FT_ABI_VERSION 5
 
 /* return codes (mapped onto the reference's TessError subclasses,
  * `errors.py:9-75`, by the Python host layer) */
@@ -98,20 +101,29 @@ typedef struct {
     int64_t  capacity;
 } ft_csc;
 
-/* Tiled working layout of a field (see Conventions).  desc[2j] = start,
- * desc[2j+1] = count of column j; entries [0, n_tiles*slot) are the tile
- * slots, [n_tiles*slot, capacity) the overflow pool. */
+/* Hybrid working layout of a field (see Conventions).  Column j:
+ *   sig[j] == -1            no entry
+ *   0 <= sig[j] < 2^30      one entry: row sig[j], value v0[j]
+ *   sig[j] >= 2^30          two entries: rows sig[j] - 2^30 < aux[j],
+ *                           values v0[j], v1[j]
+ *   sig[j] <= -3            -sig[j] entries at pool_idx / pool_val
+ *                           [aux[j], aux[j] - sig[j])
+ * The dense arrays have n_cols entries; pool offsets index pool_idx /
+ * pool_val.  A view of a column range offsets the four dense pointers. */
 typedef struct {
     int32_t  n_rows;
     int32_t  n_cols;
-    int32_t* desc;        /* [2*n_cols], 8-byte aligned                   */
-    int32_t* row_idx;     /* [capacity]                                   */
-    void*    values;      /* [capacity]                                   */
-    int64_t  capacity;
-    int32_t* sig;         /* [n_cols] row signature written with every
-                             column: its row if it holds one entry, -1 if
-                             more, -2 if none (the tier-1 classification)  */
+    int32_t* sig;         /* [n_cols] row signature (see above)            */
+    int32_t* aux;         /* [n_cols] second row / pool offset             */
+    void*    v0;          /* [n_cols] first value (double or float)        */
+    void*    v1;          /* [n_cols] second value                         */
+    int32_t* pool_idx;    /* [capacity] rows of the pool columns           */
+    void*    pool_val;    /* [capacity] values of the pool columns         */
+    int64_t  capacity;    /* pool entries                                  */
 } ft_tiled;
+
+#define FT_SIG_PAIR  (1 << 30)
+#define FT_SIG_EMPTY (-1)
 
 /* One step's statistics, device resident.  Mirrors StepStats
  * (field.py:74-92) plus the error flags the reference signals through
@@ -140,10 +152,19 @@ const char* ft_last_error(void);
 size_t ft_workspace_bytes(int32_t n_vertices);
 int    ft_workspace_init(void* workspace, size_t bytes, void* stream);
 
-/* Entries reserved per tile slot, and the smallest legal ft_tiled capacity
- * for n_vertices columns (slots only, empty pool). */
+/* Entries reserved per tile slot (kept for ABI compatibility: 0, the
+ * hybrid layout has no slots), and the smallest legal ft_tiled pool
+ * capacity (0: a field with at most two entries per column needs no pool). */
 int64_t ft_tile_slot_entries(void);
 int64_t ft_tiled_min_capacity(int32_t n_vertices);
+
+/* Canonical CSC -> hybrid layout (columns with more than two entries take
+ * pool space with one atomic per warp).  A non-finite value raises the
+ * workspace's sticky non-finite flag, so the next step checks its inputs.
+ * stats->status = FT_STATUS_OVERFLOW and stats->needed when the pool is
+ * too small. */
+int ft_tiled_from_csc(const ft_csc* src, ft_tiled* dst, int32_t dtype, void* workspace,
+                      size_t ws_bytes, ft_step_stats* stats, void* stream);
 
 /* Packed neighbour table of L^T for the tier-1 kernel: int16[n_cols][8],
  * column j's entries as deltas u - (col_base + j) in stored order (the
@@ -163,29 +184,27 @@ int ft_laplacian_pack(const ft_csc* lap_t, int32_t col_base, int16_t* pack, int3
  *   sparse.expand_to_skeleton x2 (sparse.py:374-396; _kernels.py:153-176)
  *   _kernels.update_kernel (_kernels.py:179-238)
  *   _kernels.column_sums_counts + normalize_compact (_kernels.py:241-282)
- * as one fused kernel into the tiled `scratch`, then ft_compact into
- * `phi_out`.  `stats` (device, one record) receives the statistics; on
- * FT_STATUS_OVERFLOW (scratch) / FT_STATUS_OUT_OVERFLOW (phi_out)
- * stats->needed holds the required capacity and the input is intact. */
+ * as: ft_tiled_from_csc(phi_in -> scratch_in), the fused step kernels
+ * (scratch_in -> scratch_out), then ft_compact into `phi_out`.  `stats`
+ * (device, one record) receives the statistics; on FT_STATUS_OVERFLOW
+ * (scratch pools) / FT_STATUS_OUT_OVERFLOW (phi_out) stats->needed holds
+ * the required capacity and the input is intact. */
 int ft_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
-            ft_tiled* scratch, ft_csc* phi_out, int32_t dtype,
+            ft_tiled* scratch_in, ft_tiled* scratch_out, ft_csc* phi_out, int32_t dtype,
             const ft_params* params, void* workspace, size_t ws_bytes,
             ft_step_stats* stats, void* stream);
 
-/* The three launches of one step, for callers that time the fused kernel
- * on its own (bench.py brackets ft_step_kernel with CUDA events):
- *   ft_step_kernel   the fused kernel, from `in_canon` (if non-null) or
- *                    `in_tiled` into the tiled `out`; columns whose layer
- *                    union exceeds the register window are queued;
- *   ft_step_fixup    the queued columns (same arguments);
+/* The launches of one step from a hybrid-layout input, for callers that
+ * time the kernels on their own (bench.py brackets them with CUDA events):
+ *   ft_step_kernel   tier 1: classification and the single-row closed form
+ *                    (most columns), the rest listed per tile;
+ *   ft_step_fixup    tiers 1.5-3: the listed columns;
  *   ft_step_finalize reduces the workspace accumulators into `stats`.
- * ft_step / ft_evolve issue exactly this sequence. */
-int ft_step_kernel(const ft_csc* lap_t, int32_t lap_flags,
-                   const ft_csc* in_canon, const ft_tiled* in_tiled,
+ * ft_evolve issues exactly this sequence. */
+int ft_step_kernel(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* in,
                    ft_tiled* out, int32_t dtype, const ft_params* params,
                    void* workspace, size_t ws_bytes, void* stream);
-int ft_step_fixup(const ft_csc* lap_t, int32_t lap_flags,
-                  const ft_csc* in_canon, const ft_tiled* in_tiled,
+int ft_step_fixup(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* in,
                   ft_tiled* out, int32_t dtype, const ft_params* params,
                   void* workspace, size_t ws_bytes, void* stream);
 int ft_step_finalize(void* workspace, size_t ws_bytes, int32_t n_vertices,
@@ -197,8 +216,9 @@ int ft_step_finalize(void* workspace, size_t ws_bytes, int32_t n_vertices,
 int ft_compact(const ft_tiled* src, ft_csc* dst, int32_t dtype, void* workspace,
                size_t ws_bytes, ft_step_stats* stats, void* stream);
 
-/* Up to `max_steps` steps from the canonical `phi_in`, ping-ponging between
- * the tiled buffers a (odd steps) and b (even steps), stopping on the
+/* Up to `max_steps` steps from the canonical `phi_in` (converted into
+ * work_b), ping-ponging between the hybrid buffers a (odd steps) and b
+ * (even steps), stopping on the
  * device as soon as a step converges (max_delta < tol and base_mass <
  * base_threshold; field.py:316-317) or fails (NaN / pattern violation /
  * tiled overflow).  The last good field is then compacted into `phi_out`.
@@ -263,8 +283,9 @@ int ft_halo_pack(const ft_tiled* src, const int32_t* cols, int32_t n, int32_t sl
                  int32_t dtype, void* msg, ft_step_stats* record, int32_t* need,
                  void* workspace, int32_t flags, void* stream);
 
-/* Column cols[i] of `dst` <- message entry i, stored at entries
- * [region + i*slots, region + i*slots + count).  Skipped when done is set
+/* Column cols[i] of `dst` <- message entry i: in the dense arrays when it
+ * holds at most two entries, else at pool entries [region + i*slots,
+ * region + i*slots + count).  Skipped when done is set
  * (unless FT_HALO_FORCE). */
 int ft_halo_unpack(ft_tiled* dst, const int32_t* cols, int32_t n, int32_t slots,
                    int32_t dtype, const void* msg, int64_t region, void* workspace,

@@ -39,7 +39,7 @@ FT_STATUS_HALO_OVERFLOW = 7
 
 FT_HALO_FORCE = 1
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 
 class FtParams(ctypes.Structure):
@@ -56,9 +56,10 @@ class FtCsc(ctypes.Structure):
 
 class FtTiled(ctypes.Structure):
     _fields_ = [("n_rows", ctypes.c_int32), ("n_cols", ctypes.c_int32),
-                ("desc", ctypes.c_void_p), ("row_idx", ctypes.c_void_p),
-                ("values", ctypes.c_void_p), ("capacity", ctypes.c_int64),
-                ("sig", ctypes.c_void_p)]
+                ("sig", ctypes.c_void_p), ("aux", ctypes.c_void_p),
+                ("v0", ctypes.c_void_p), ("v1", ctypes.c_void_p),
+                ("pool_idx", ctypes.c_void_p), ("pool_val", ctypes.c_void_p),
+                ("capacity", ctypes.c_int64)]
 
 
 class FtDomain(ctypes.Structure):
@@ -91,7 +92,7 @@ assert STATS_DTYPE.itemsize == STATS_BYTES
 
 # every symbol include/fieldtess_cuda.h declares
 EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
-           "ft_workspace_init", "ft_tile_slot_entries", "ft_tiled_min_capacity",
+           "ft_workspace_init", "ft_tile_slot_entries", "ft_tiled_min_capacity", "ft_tiled_from_csc",
            "ft_step", "ft_step_kernel", "ft_step_fixup", "ft_step_finalize", "ft_compact",
            "ft_evolve", "ft_labels", "ft_faces_by_cell", "ft_lloyd_centroids",
            "ft_dual_products", "ft_domain_step", "ft_halo_bytes", "ft_halo_pack",
@@ -117,12 +118,14 @@ def _declare(lib):
     lib.ft_tile_slot_entries.restype = ctypes.c_int64
     lib.ft_tiled_min_capacity.argtypes = [ctypes.c_int32]
     lib.ft_tiled_min_capacity.restype = ctypes.c_int64
-    lib.ft_step.argtypes = [P(FtCsc), ctypes.c_int32, P(FtCsc), P(FtTiled), P(FtCsc),
+    lib.ft_tiled_from_csc.argtypes = [P(FtCsc), P(FtTiled), ctypes.c_int32, vp, ctypes.c_size_t,
+                                      vp, vp]
+    lib.ft_tiled_from_csc.restype = ctypes.c_int
+    lib.ft_step.argtypes = [P(FtCsc), ctypes.c_int32, P(FtCsc), P(FtTiled), P(FtTiled), P(FtCsc),
                             ctypes.c_int32, P(FtParams), vp, ctypes.c_size_t, vp, vp]
     lib.ft_step.restype = ctypes.c_int
-    lib.ft_step_kernel.argtypes = [P(FtCsc), ctypes.c_int32, P(FtCsc), P(FtTiled),
-                                   P(FtTiled), ctypes.c_int32, P(FtParams), vp,
-                                   ctypes.c_size_t, vp]
+    lib.ft_step_kernel.argtypes = [P(FtCsc), ctypes.c_int32, P(FtTiled), P(FtTiled),
+                                   ctypes.c_int32, P(FtParams), vp, ctypes.c_size_t, vp]
     lib.ft_step_kernel.restype = ctypes.c_int
     lib.ft_step_fixup.argtypes = lib.ft_step_kernel.argtypes
     lib.ft_step_fixup.restype = ctypes.c_int

@@ -7,8 +7,6 @@
 
 #define FT_TPB 128              // threads (= vertex columns) per CTA tile
 #define FT_WARPS (FT_TPB / 32)
-#define FT_SLOT_PER_VERTEX 2    // tile slot entries per vertex column
-#define FT_SLOT (FT_TPB * FT_SLOT_PER_VERTEX)
 #define FT_CCH 2048             // columns per compaction chunk
 #define FT_CTPB 256             // threads of the compaction kernels
 
@@ -23,9 +21,9 @@ struct Control {
     unsigned long long bad_lt_key;
     unsigned long long skel_total;     // interest-skeleton nnz of the step
     unsigned long long nnz_total;      // output nnz of the step
-    unsigned long long pool_next;      // overflow-pool bump pointer
+    unsigned long long pool_next;      // pool bump pointer of the step's output
     unsigned int       nan_key;        // atomicMax(INT_MAX - col) -> min col
-    int                overflow;       // a tile did not fit the work buffer
+    int                overflow;       // the output pool is too small
     int                slow_count;     // wide columns queued for tier 2
     unsigned int       fin_count;      // finalize: CTAs done (last-block pattern)
     int                deep_count;     // tier-3 columns (slow_list + n_v)
@@ -37,27 +35,34 @@ struct Control {
     long long          needed;         // capacity needed on overflow
     int                wide8_count;    // tier-2b columns (slow_list + 3 n_v + FT_TPB)
     int                pad2;
-    long long          pad1[3];
+    long long          conv_next;      // pool bump pointer of ft_tiled_from_csc
+    long long          pad1[2];
 };
 static_assert(sizeof(Control) % 16 == 0, "Control must stay 16B aligned");
 
 #define FT_FIN_MAX 1024   // finalize CTAs at most (partials in the workspace)
 
+// Statistics are kept per 32-column segment (one warp of tier 1) and per
+// 128-column tile (one warp of tier 1.5), so no kernel needs a CTA barrier
+// or a same-address atomic per warp; the finalize reduces them in a fixed
+// order.
 struct Workspace {
     Control*      ctl;
-    double*       tile_bm;      // [num_tiles] per-tile base mass (fast path)
-    double*       vbm;          // [n_v] base mass of wide columns (tier 2)
-    unsigned int* slow_mask;    // [num_tiles * FT_WARPS] wide columns of each tile
-    int*          slow_list;    // tier-2 queue [0, n_v), tier-3 at +n_v, tier-1.5 lists at +2 n_v (128 per
-                                //   tile), tier-2b queue at +3 n_v + FT_TPB
+    double*       seg_bm;       // [4 num_tiles] tier-1 base mass per segment
+    double*       seg_maxd;     // [4 num_tiles] tier-1 max |delta| per segment
+    int2*         seg_cs;       // [4 num_tiles] tier-1 (nnz, skeleton nnz) per segment
+    unsigned int* gen_mask;     // [4 num_tiles] tier-1.5 columns of each segment
+    unsigned int* slow_mask;    // [4 num_tiles] tier-2 columns of each segment
+    double*       gen_bm;       // [num_tiles] tier-1.5 base mass per tile
+    double*       gen_maxd;     // [num_tiles]
+    int2*         gen_cs;       // [num_tiles]
+    double*       vbm;          // [n_v] base mass of tier-2/3 columns
+    int*          slow_list;    // tier-2 queue [0, n_v), tier-3 at +n_v, tier-2b at +2 n_v
     long long*    chunk_off;    // [num_chunks + 2] compaction chunk offsets
     double*       fin_part;     // [FT_FIN_MAX] finalize partial sums (base mass)
     double*       fin_maxd;     // [FT_FIN_MAX] finalize partial maxima
     long long*    fin_cnt;      // [FT_FIN_MAX] finalize partial nnz
     long long*    fin_skel;     // [FT_FIN_MAX] finalize partial skeleton nnz
-    double*       tile_maxd;    // [num_tiles] per-tile max |delta| (fast path)
-    int2*         tile_cs;      // [num_tiles] per-tile (nnz, skeleton nnz) (fast path)
-    int*          tile_gen;     // [num_tiles] tier-1.5 columns of the tile (list at slow_list + 2 n_v + 128 t)
     int           num_tiles;
     int           num_chunks;
 };
@@ -66,14 +71,12 @@ __host__ __device__ inline int num_tiles_for(int n_v) { return (n_v + FT_TPB - 1
 __host__ __device__ inline int num_chunks_for(int n_v) { return (n_v + FT_CCH - 1) / FT_CCH; }
 
 inline size_t workspace_bytes(int n_v) {
-    size_t t = (size_t)num_tiles_for(n_v), c = (size_t)num_chunks_for(n_v);
-    const size_t v = (size_t)n_v;
-    return sizeof(Control) + t * sizeof(double) + v * sizeof(double) + t * FT_WARPS * sizeof(unsigned int) +
-           (4 * v + FT_TPB) * sizeof(int) + t * sizeof(int) + (c + 2) * sizeof(long long) + 4 * FT_FIN_MAX * sizeof(double) +
-           t * (sizeof(double) + sizeof(int2)) + 1024;
+    const size_t t = (size_t)num_tiles_for(n_v), c = (size_t)num_chunks_for(n_v), v = (size_t)n_v;
+    return sizeof(Control) + 4 * t * (8 + 8 + 8 + 4 + 4) + t * (8 + 8 + 8) + v * 8 + 3 * v * 4 +
+           (c + 2) * 8 + 4 * FT_FIN_MAX * 8 + 16 * 16;
 }
 
-static_assert(FT_WARPS == 4, "slow_mask is read as one uint4 per tile");
+static_assert(FT_WARPS == 4, "segment masks are read as one uint4 per tile");
 
 inline char* align16(char* p) { return (char*)(((uintptr_t)p + 15) & ~(uintptr_t)15); }
 
@@ -84,32 +87,66 @@ inline Workspace carve_workspace(void* base, int n_v) {
     p += sizeof(Control);
     w.num_tiles = num_tiles_for(n_v);
     w.num_chunks = num_chunks_for(n_v);
-    w.tile_bm = (double*)p;
-    p += (size_t)w.num_tiles * sizeof(double);
-    w.vbm = (double*)p;
-    p += (size_t)n_v * sizeof(double);
-    w.chunk_off = (long long*)p;
-    p += ((size_t)w.num_chunks + 2) * sizeof(long long);
-    w.fin_part = (double*)p;
-    p += FT_FIN_MAX * sizeof(double);
-    w.fin_maxd = (double*)p;
-    p += FT_FIN_MAX * sizeof(double);
-    w.fin_cnt = (long long*)p;
-    p += FT_FIN_MAX * sizeof(long long);
-    w.fin_skel = (long long*)p;
-    p += FT_FIN_MAX * sizeof(long long);
-    w.tile_maxd = (double*)p;
-    p += (size_t)w.num_tiles * sizeof(double);
-    w.tile_cs = (int2*)p;
-    p += (size_t)w.num_tiles * sizeof(int2);
-    w.tile_gen = (int*)p;
-    p += (size_t)w.num_tiles * sizeof(int);
-    p = align16(p);
-    w.slow_mask = (unsigned int*)p;
-    p += (size_t)w.num_tiles * FT_WARPS * sizeof(unsigned int);
-    w.slow_list = (int*)p;
-    p += (4 * (size_t)n_v + FT_TPB) * sizeof(int);
+    const size_t ns = 4 * (size_t)w.num_tiles, nt = (size_t)w.num_tiles;
+    w.seg_bm = (double*)p;       p = align16(p + ns * 8);
+    w.seg_maxd = (double*)p;     p = align16(p + ns * 8);
+    w.seg_cs = (int2*)p;         p = align16(p + ns * 8);
+    w.gen_mask = (unsigned int*)p; p = align16(p + ns * 4);
+    w.slow_mask = (unsigned int*)p; p = align16(p + ns * 4);
+    w.gen_bm = (double*)p;       p = align16(p + nt * 8);
+    w.gen_maxd = (double*)p;     p = align16(p + nt * 8);
+    w.gen_cs = (int2*)p;         p = align16(p + nt * 8);
+    w.vbm = (double*)p;          p = align16(p + (size_t)n_v * 8);
+    w.slow_list = (int*)p;       p = align16(p + 3 * (size_t)n_v * 4);
+    w.chunk_off = (long long*)p; p = align16(p + ((size_t)w.num_chunks + 2) * 8);
+    w.fin_part = (double*)p;     p += FT_FIN_MAX * 8;
+    w.fin_maxd = (double*)p;     p += FT_FIN_MAX * 8;
+    w.fin_cnt = (long long*)p;   p += FT_FIN_MAX * 8;
+    w.fin_skel = (long long*)p;  p += FT_FIN_MAX * 8;
     return w;
+}
+
+// ---------------------------------------------------------------------------
+// hybrid field layout (ft_tiled, include/fieldtess_cuda.h)
+
+constexpr int kPair = FT_SIG_PAIR;
+
+__host__ __device__ __forceinline__ int sig_count(int s) {
+    return s >= 0 ? ((s & kPair) ? 2 : 1) : (s == FT_SIG_EMPTY ? 0 : -s);
+}
+
+// read-only view of a hybrid buffer
+struct HybIn {
+    const int* __restrict__ sig;
+    const int* __restrict__ aux;
+    const void* __restrict__ v0;
+    const void* __restrict__ v1;
+    const int* __restrict__ pidx;
+    const void* __restrict__ pval;
+};
+
+struct HybOut {
+    int* __restrict__ sig;
+    int* __restrict__ aux;
+    void* __restrict__ v0;
+    void* __restrict__ v1;
+    int* __restrict__ pidx;
+    void* __restrict__ pval;
+};
+
+inline HybIn hyb_in(const ft_tiled* t) { return HybIn{t->sig, t->aux, t->v0, t->v1, t->pool_idx, t->pool_val}; }
+inline HybOut hyb_out(ft_tiled* t) { return HybOut{t->sig, t->aux, t->v0, t->v1, t->pool_idx, t->pool_val}; }
+
+// entry k of column u whose signature is s and aux word a
+template <typename T>
+__device__ __forceinline__ int hyb_row(const HybIn& h, int s, int a, int k) {
+    if (s >= 0) return k == 0 ? (s & ~kPair) : a;
+    return __ldg(&h.pidx[a + k]);
+}
+template <typename T>
+__device__ __forceinline__ double hyb_val(const HybIn& h, int u, int s, int a, int k) {
+    if (s >= 0) return (double)__ldg(((const T*)(k == 0 ? h.v0 : h.v1)) + u);
+    return (double)__ldg(((const T*)h.pval) + a + k);
 }
 
 template <typename T>

@@ -7,7 +7,7 @@
 // column ranges needs, per step, only the one-ring halo of each range and
 // the global statistics of field.py:270-271 (max |delta|, base mass) for the
 // stop test of field.py:316-317.  These kernels move halo columns between a
-// rank's tiled buffer and a fixed-slot message (counts, rows, values) that
+// rank's hybrid buffer and a fixed-slot message (counts, rows, values) that
 // the host sends with ncclSend / ncclRecv, and fold the all-gathered per-rank
 // records into the global record in a fixed rank order.
 
@@ -19,16 +19,14 @@
 namespace ft {
 
 struct HaloParams {
-    int2* desc;
-    int* idx;
-    void* val;
-    int* sig;            // row signatures (tier-1 classification)
+    HybIn in;            // pack: the source buffer
+    HybOut out;          // unpack: the destination buffer
     const int* cols;
     int n, slots;
     int* m_cnt;          // message: counts[n]
     int* m_rows;         //          rows[n*slots]
     void* m_vals;        //          values[n*slots]
-    long long region;    // unpack: first entry of the halo region
+    long long region;    // unpack: first pool entry of the halo region
     ft_step_stats* record;
     int* need;
     Control* ctl;
@@ -42,20 +40,22 @@ __global__ void __launch_bounds__(256) halo_pack_kernel(const HaloParams h) {
         return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= h.n) return;
-    const int2 d = h.desc[h.cols[i]];
-    h.m_cnt[i] = d.y;
-    int c = d.y;
+    const int u = h.cols[i];
+    const int s = h.in.sig[u];
+    const int cnt = sig_count(s);
+    const int a = cnt >= 2 ? h.in.aux[u] : 0;
+    h.m_cnt[i] = cnt;
+    int c = cnt;
     if (c > h.slots) {
         atomicMax(h.need, c);
         h.record->status = FT_STATUS_HALO_OVERFLOW;   // same value from every writer
         c = h.slots;
     }
     const size_t o = (size_t)i * h.slots;
-    const T* v = (const T*)h.val;
     T* mv = (T*)h.m_vals;
     for (int t = 0; t < c; ++t) {
-        h.m_rows[o + t] = h.idx[d.x + t];
-        mv[o + t] = v[d.x + t];
+        h.m_rows[o + t] = hyb_row<T>(h.in, s, a, t);
+        mv[o + t] = (T)hyb_val<T>(h.in, u, s, a, t);
     }
 }
 
@@ -64,18 +64,34 @@ __global__ void __launch_bounds__(256) halo_unpack_kernel(const HaloParams h) {
     if (!h.force && *(volatile const int*)&h.ctl->done) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= h.n) return;
-    const int c = h.m_cnt[i];
-    const long long off = h.region + (long long)i * h.slots;
-    h.desc[h.cols[i]] = make_int2((int)off, c);
-    h.sig[h.cols[i]] = c == 1 ? h.m_rows[(size_t)i * h.slots] : (c == 0 ? -2 : -1);
+    const int c = min(h.m_cnt[i], h.slots);
+    const int u = h.cols[i];
     const size_t o = (size_t)i * h.slots;
-    T* v = (T*)h.val;
     const T* mv = (const T*)h.m_vals;
     bool nf = false;
-    for (int t = 0; t < c && t < h.slots; ++t) {
-        h.idx[off + t] = h.m_rows[o + t];
-        v[off + t] = mv[o + t];
-        nf |= !isfinite((double)mv[o + t]);
+    if (c == 0) {
+        h.out.sig[u] = FT_SIG_EMPTY;
+    } else if (c <= 2) {
+        ((T*)h.out.v0)[u] = mv[o];
+        nf |= !isfinite((double)mv[o]);
+        if (c == 1) {
+            h.out.sig[u] = h.m_rows[o];
+        } else {
+            h.out.sig[u] = h.m_rows[o] | kPair;
+            h.out.aux[u] = h.m_rows[o + 1];
+            ((T*)h.out.v1)[u] = mv[o + 1];
+            nf |= !isfinite((double)mv[o + 1]);
+        }
+    } else {
+        const long long off = h.region + (long long)i * h.slots;
+        h.out.sig[u] = -c;
+        h.out.aux[u] = (int)off;
+        T* v = (T*)h.out.pval;
+        for (int t = 0; t < c; ++t) {
+            h.out.pidx[off + t] = h.m_rows[o + t];
+            v[off + t] = mv[o + t];
+            nf |= !isfinite((double)mv[o + t]);
+        }
     }
     // a peer's non-finite value: this rank's next step checks its inputs
     if (nf) atomicOr(&h.ctl->nonfinite, 1u);
@@ -154,11 +170,13 @@ __global__ void control_kernel(Control* ctl, int set_steps, long long* out) {
     out[2] = ctl->needed;
 }
 
-static bool fill_halo(HaloParams& h, const ft_tiled* t, const int32_t* cols, int32_t n, int32_t slots,
+static bool fill_halo(HaloParams& h, ft_tiled* t, const int32_t* cols, int32_t n, int32_t slots,
                       int32_t dtype, const void* msg, void* workspace, int32_t flags) {
-    if (!t || !t->sig || !cols || !msg || !workspace || n < 0 || slots < 1) return false;
+    if (!t || !t->sig || !t->aux || !t->v0 || !t->v1 || !cols || !msg || !workspace || n < 0 || slots < 1)
+        return false;
     if (dtype != FT_F64 && dtype != FT_F32) return false;
-    h.desc = (int2*)t->desc; h.idx = t->row_idx; h.val = t->values; h.sig = t->sig;
+    h.in = hyb_in(t);
+    h.out = hyb_out(t);
     h.cols = cols; h.n = n; h.slots = slots;
     char* m = (char*)msg;
     h.m_cnt = (int*)m;
@@ -186,7 +204,7 @@ extern "C" int ft_halo_pack(const ft_tiled* src, const int32_t* cols, int32_t n,
                             void* msg, ft_step_stats* record, int32_t* need, void* workspace, int32_t flags,
                             void* stream) {
     ft::HaloParams h;
-    if (!record || !need || !ft::fill_halo(h, src, cols, n, slots, dtype, msg, workspace, flags)) return FT_ERR_ARG;
+    if (!record || !need || !ft::fill_halo(h, const_cast<ft_tiled*>(src), cols, n, slots, dtype, msg, workspace, flags)) return FT_ERR_ARG;
     h.record = record;
     h.need = need;
     if (n == 0) return FT_OK;

@@ -1,6 +1,6 @@
 // Fused explicit-Euler step of the layered field (sm_100a).
 //
-// One launch replaces the reference pipeline of field.step
+// One step replaces the reference pipeline of field.step
 // (reference pkg/src/fieldtess/field.py:198-286):
 //
 //   Lt = PHI L^T            spgemm_numeric      _kernels.py:26-62
@@ -10,25 +10,28 @@
 //   normalise + compact     column_sums_counts, normalize_compact
 //                                               _kernels.py:241-282
 //
-// Work split, three tiers over 128-column tiles (one thread per vertex
-// column):
-//   tier 1    step_kernel6: classification from the neighbours'
-//             descriptors; a single-row neighbourhood (a cell interior,
+// Between steps PHI is kept in the hybrid layout of ft_tiled: a column
+// with at most two entries (~99% at C3) lives in four dense per-column
+// arrays (signature, second row, two values), a wider one in a pool.  Every
+// kernel reads a neighbour's entries directly (no descriptor indirection)
+// and writes its own column at a fixed address (no placement scan, no
+// inter-CTA wait).  Work split over 128-column tiles, one thread per vertex
+// column:
+//   tier 1    tier1_kernel: classification from the neighbours' row
+//             signatures; a single-row neighbourhood (a cell interior,
 //             ~82% of the columns at C3) takes the exact closed form
-//             v' = v * (1 / (0 + v)); the others are listed per tile;
-//   tier 1.5  gen_kernel, one warp per tile: columns with at most two
-//             rows and two entries per neighbour, the update in one pass
+//             v' = v * (1 / (0 + v)); the others are flagged per 32-column
+//             segment (bit masks, no atomics);
+//   tier 1.5  gen_kernel, one warp per tile: columns with at most two rows
+//             and at most two entries per neighbour, the update in one pass
 //             (rows = min / max of the candidates, Lt accumulated in
 //             ascending-u order -- exactly the reference accumulator order;
 //             PHI(r, j) arrives through the diagonal u == j);
-//   tier 2/3  wide_kernel / deep_kernel: wider columns, ascending-row
-//             windows of up to 8 rows / no limit.
-//
-// Output: tiles write to their fixed slot of the tiled work buffer
-// (FT_SLOT entries; tier 1.5 appends to it) or, when they do not fit, to a
-// pool range taken with one atomic; column j is described by (start,
-// count).  No CTA waits for another and no queue takes a same-address
-// atomic per warp.  Canonical CSC comes from ft_compact.
+//   tier 2/3  wide3_kernel / wide_kernel / deep_kernel: wider columns,
+//             register windows of 3 / 8 rows, then no limit.
+// Statistics go to per-segment / per-tile slots that finalize_kernel
+// reduces in a fixed order (deterministic base mass).  Canonical CSC comes
+// from ft_compact.
 //
 // EXACT mode (double storage) replays the reference arithmetic operation by
 // operation; the library is compiled with -fmad=false (no FMA contraction)
@@ -57,21 +60,14 @@ struct StepParams {
     const int* __restrict__ lap_idx;
     const void* __restrict__ lap_val;
     const int4* __restrict__ lap_pack;  // FT_LAP_PACKED: int16 deltas u - j, 8 per column
-    const int* __restrict__ in_ptr;     // canonical input (IN_CANON)
-    const int2* __restrict__ in_desc;   // tiled input
-    const int* __restrict__ in_idx;
-    const void* __restrict__ in_val;
-    const int* __restrict__ in_sig;     // tiled input: row signature per column
-    int2* __restrict__ out_desc;
-    int* __restrict__ out_idx;
-    void* __restrict__ out_val;
-    int* __restrict__ out_sig;
-    long long cap;
+    HybIn in;
+    HybOut out;
+    long long cap;       // pool entries the step may use
     double w, a, e, eb, mu, dt;
     Workspace ws;
     int check_done;
     int finite;          // all couplings finite: enables the single-row closed form
-    int force_check;     // FT_LAP_CHECK_FINITE: check tiled input values for NaN / Inf
+    int force_check;     // FT_LAP_CHECK_FINITE: check input values for NaN / Inf
     const int* report_ids;  // nullable: caller ids of the owned columns (error reports)
 };
 
@@ -86,15 +82,8 @@ struct FinalizeParams {
     double base_threshold;
 };
 
-template <bool IN_CANON>
-__device__ __forceinline__ int2 load_desc(const StepParams& p, int u) {
-    if (IN_CANON) {
-        const int a = __ldg(&p.in_ptr[u]);
-        const int b = __ldg(&p.in_ptr[u + 1]);
-        return make_int2(a, b - a);
-    }
-    return __ldg(&p.in_desc[u]);
-}
+// ---------------------------------------------------------------------------
+// register window of layer rows for one vertex column
 
 // ---------------------------------------------------------------------------
 // register window of layer rows for one vertex column
@@ -146,32 +135,6 @@ __device__ __forceinline__ void win_insert(Win<K>& w, int r, double prod, bool d
 template <typename T>
 __device__ __forceinline__ double ldv(const void* p, long long i) {
     return (double)__ldg(((const T*)p) + i);
-}
-
-// Gather rows r > lo of the union of PHI(:, u), u in L^T(:, j), with the
-// Lt accumulation, into the window (the K smallest such rows).  Global
-// memory version (fallback tiles and the windowed slow path).
-template <typename T, int K, bool UNIFORM, bool IN_CANON>
-__device__ __forceinline__ void gather(Win<K>& w, int j, int lo, const StepParams& p) {
-    w.m = 0;
-    w.more = false;
-    const int q0 = __ldg(&p.lap_ptr[j - p.j_base]);   // L rows are local to the domain
-    const int q1 = __ldg(&p.lap_ptr[j - p.j_base + 1]);
-    const double invdeg = UNIFORM ? 1.0 / (double)(q1 - q0 - 1) : 0.0;
-    for (int q = q0; q < q1; ++q) {
-        const int u = __ldg(&p.lap_idx[q]);
-        const bool diag = (u == j);
-        double l;
-        if (UNIFORM) l = diag ? -1.0 : invdeg;
-        else l = ldv<T>(p.lap_val, q);
-        const int2 d = load_desc<IN_CANON>(p, u);
-        for (int c = d.x; c < d.x + d.y; ++c) {
-            const int r = __ldg(&p.in_idx[c]);
-            if (r <= lo) continue;
-            const double ph = ldv<T>(p.in_val, c);
-            win_insert<K>(w, r, ph * l, diag, ph);
-        }
-    }
 }
 
 // row signature of an output column: its row if it holds one entry, -1 if
@@ -497,50 +460,146 @@ __device__ __forceinline__ void report_flags(const VRes& res, int j, const StepP
         atomicMax(&p.ws.ctl->bad_lt_key, ~(((unsigned long long)j << 32) | (unsigned int)res.bad_lt_row));
 }
 
-// writes the flagged window slots; a non-finite output value raises the
-// sticky nonfinite flag (tier 1 then checks its inputs' values)
+// ---------------------------------------------------------------------------
+// output: a column with at most two entries goes to the dense arrays, a
+// wider one to the pool (offset from pool_place)
+
+template <typename T>
+__device__ __forceinline__ void put_dense(const StepParams& p, int j, int cnt, int r0, double x0, int r1,
+                                          double x1) {
+    if (cnt == 0) {
+        p.out.sig[j] = FT_SIG_EMPTY;
+        return;
+    }
+    ((T*)p.out.v0)[j] = (T)x0;
+    bool nf = !isfinite(x0);
+    if (cnt == 1) {
+        p.out.sig[j] = r0;
+    } else {
+        p.out.sig[j] = r0 | kPair;
+        p.out.aux[j] = r1;
+        ((T*)p.out.v1)[j] = (T)x1;
+        nf |= !isfinite(x1);
+    }
+    if (nf) atomicOr(&p.ws.ctl->nonfinite, 1u);
+}
+
+// the flagged window slots (ascending rows) as column j
 template <typename T, int K>
-__device__ __forceinline__ void emit_window(const Win<K>& w, unsigned int out_mask, long long off,
+__device__ __forceinline__ void emit_window(const Win<K>& w, unsigned int out_mask, int j, long long poff,
                                             const StepParams& p) {
-    T* ov = (T*)p.out_val;
+    const int cnt = __popc(out_mask);
+    if (cnt <= 2) {
+        int r0 = 0, r1 = 0, k = 0;
+        double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            if (out_mask & (1u << i)) {
+                if (k == 0) { r0 = w.rows[i]; x0 = w.lam[i]; }
+                else { r1 = w.rows[i]; x1 = w.lam[i]; }
+                ++k;
+            }
+        }
+        put_dense<T>(p, j, cnt, r0, x0, r1, x1);
+        return;
+    }
+    p.out.sig[j] = -cnt;
+    p.out.aux[j] = (int)poff;
+    T* ov = (T*)p.out.pval;
     bool nf = false;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         if (out_mask & (1u << i)) {
-            p.out_idx[off] = w.rows[i];
-            ov[off] = (T)w.lam[i];
+            p.out.pidx[poff] = w.rows[i];
+            ov[poff] = (T)w.lam[i];
             nf |= !isfinite(w.lam[i]);
-            ++off;
+            ++poff;
         }
     }
     if (nf) atomicOr(&p.ws.ctl->nonfinite, 1u);
 }
 
-// --- slow path: union larger than K, processed in ascending row windows ----
+// Gather rows r > lo of the union of PHI(:, u), u in L^T(:, j), with the
+// Lt accumulation, into the window (the K smallest such rows).  L from the
+// CSR (tier 3, any degree).
+template <typename T, int K, bool UNIFORM>
+__device__ __forceinline__ void gather(Win<K>& w, int j, int lo, const StepParams& p) {
+    w.m = 0;
+    w.more = false;
+    const int q0 = __ldg(&p.lap_ptr[j - p.j_base]);   // L rows are local to the domain
+    const int q1 = __ldg(&p.lap_ptr[j - p.j_base + 1]);
+    const double invdeg = UNIFORM ? 1.0 / (double)(q1 - q0 - 1) : 0.0;
+    for (int q = q0; q < q1; ++q) {
+        const int u = __ldg(&p.lap_idx[q]);
+        const bool diag = (u == j);
+        double l;
+        if (UNIFORM) l = diag ? -1.0 : invdeg;
+        else l = ldv<T>(p.lap_val, q);
+        const int s = __ldg(&p.in.sig[u]);
+        const int cnt = sig_count(s);
+        const int a = cnt >= 2 ? __ldg(&p.in.aux[u]) : 0;
+        for (int c = 0; c < cnt; ++c) {
+            const int r = hyb_row<T>(p.in, s, a, c);
+            if (r <= lo) continue;
+            const double ph = hyb_val<T>(p.in, u, s, a, c);
+            win_insert<K>(w, r, ph * l, diag, ph);
+        }
+    }
+}
 
-template <typename T, int K, bool UNIFORM, bool IN_CANON>
-__device__ __noinline__ void vertex_slow(int j, const StepParams& p, VRes& res, long long emit_off,
-                                         bool emit) {
+// entries of a tier-3 column, emitted in ascending row order
+struct Sink {
+    int k, cnt;
+    int r0, r1;
+    double x0, x1;
+    long long off;
+};
+
+template <typename T>
+__device__ __forceinline__ void sink_put(Sink& s, int r, double x, const StepParams& p) {
+    if (s.cnt <= 2) {
+        if (s.k == 0) { s.r0 = r; s.x0 = x; }
+        else { s.r1 = r; s.x1 = x; }
+    } else {
+        p.out.pidx[s.off + s.k] = r;
+        ((T*)p.out.pval)[s.off + s.k] = (T)x;
+        if (!isfinite(x)) atomicOr(&p.ws.ctl->nonfinite, 1u);
+    }
+    ++s.k;
+}
+
+// --- slow path: union larger than K, processed in ascending row windows ----
+// emit == false: statistics only (res.cnt = output entries); emit == true:
+// writes column j (the pool range at poff when res.cnt > 2)
+
+template <typename T, int K, bool UNIFORM>
+__device__ __noinline__ void vertex_slow(int j, const StepParams& p, VRes& res, long long poff, bool emit) {
     Win<K> w;
     Agg g;
     agg_init(g);
     int lo = -1;
     do {
-        gather<T, K, UNIFORM, IN_CANON>(w, j, lo, p);
+        gather<T, K, UNIFORM>(w, j, lo, p);
         pass_aggregate<K>(w, g);
         if (w.m > 0) lo = w.rows[w.m - 1];
     } while (w.more);
+    const int cnt_known = res.cnt;
     res.nskel = g.n;
     res.bad_phi_row = g.bad_phi_row;
     res.bad_lt_row = g.bad_lt_row;
     res.nan = false;
     res.cnt = 0; res.bm = 0.0; res.maxd = 0.0;
-    if (g.n == 0) return;
+    Sink sk;
+    sk.k = 0; sk.cnt = cnt_known; sk.r0 = 0; sk.r1 = 0; sk.x0 = 0.0; sk.x1 = 0.0; sk.off = poff;
+    if (g.n == 0) {
+        if (emit) p.out.sig[j] = FT_SIG_EMPTY;
+        return;
+    }
     const Coef c = make_coef(g, p, nullptr);
     double s = 0.0;
     lo = -1;
     do {
-        gather<T, K, UNIFORM, IN_CANON>(w, j, lo, p);
+        gather<T, K, UNIFORM>(w, j, lo, p);
         for (int i = 0; i < w.m; ++i) {
             const double ph = w.phi[i], lm = w.lam[i];
             if (!in_skeleton(ph, lm)) continue;
@@ -551,22 +610,16 @@ __device__ __noinline__ void vertex_slow(int j, const StepParams& p, VRes& res, 
     const bool spos = s > 0.0;
     const double inv = spos ? 1.0 / s : 0.0;
     bool dummy = false;
-    T* ov = (T*)p.out_val;
     lo = -1;
     do {
-        gather<T, K, UNIFORM, IN_CANON>(w, j, lo, p);
+        gather<T, K, UNIFORM>(w, j, lo, p);
         for (int i = 0; i < w.m; ++i) {
             const double ph = w.phi[i], lm = w.lam[i];
             if (!in_skeleton(ph, lm)) continue;
             const double v = update_entry(w.rows[i], ph, (lm != 0.0) ? lm : 0.0, c, p, dummy);
             const double nv = spos ? v * inv : v;
             if (nv != 0.0) {
-                if (emit) {
-                    p.out_idx[emit_off] = w.rows[i];
-                    ov[emit_off] = (T)nv;
-                    ++emit_off;
-                    if (!isfinite(nv)) atomicOr(&p.ws.ctl->nonfinite, 1u);
-                }
+                if (emit) sink_put<T>(sk, w.rows[i], nv, p);
                 res.cnt++;
                 if (w.rows[i] == 0) res.bm = res.bm + nv;
             }
@@ -575,73 +628,14 @@ __device__ __noinline__ void vertex_slow(int j, const StepParams& p, VRes& res, 
         }
         if (w.m > 0) lo = w.rows[w.m - 1];
     } while (w.more);
-}
-
-// ---------------------------------------------------------------------------
-// output placement
-
-// Tile epilogue: block scan of the output counts,
-// placement (tile slot, or a pool range), per-tile statistics.
-struct TileOut {
-    int local_off;
-    long long base;   // -1: overflow, nothing is written
-};
-
-template <bool POOL_ONLY>
-__device__ __forceinline__ TileOut tile_epilogue(int cnt, int nskel, double bmv, double maxd, int tile,
-                                                 double* bm_slot, const StepParams& p, int* s_scan,
-                                                 double* s_wbm, double* s_wmax, int* s_wskel,
-                                                 long long* s_base) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    int tile_total;
-    TileOut o;
-    o.local_off = block_excl_scan<FT_TPB>(cnt, s_scan, &tile_total);
-    const int skel = warp_sum(nskel);
-    const double bm = warp_sum(bmv);
-    double mx = maxd;
-#pragma unroll
-    for (int k = 16; k > 0; k >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, k));
-    if (lane == 0) { s_wskel[warp] = skel; s_wbm[warp] = bm; s_wmax[warp] = mx; }
-    __syncthreads();
-    if (tid == 0) {
-        long long base = POOL_ONLY ? -1 : (long long)tile * FT_SLOT;
-        if (tile_total > 0 && (POOL_ONLY || tile_total > FT_SLOT)) {
-            const unsigned long long q = atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)tile_total);
-            base = (long long)p.num_tiles * FT_SLOT + (long long)q;
-        }
-        if (base + tile_total > p.cap) {
-            atomicExch(&p.ws.ctl->overflow, 1);
-            base = -1;
-        }
-        if (tile_total == 0 && POOL_ONLY) base = 0;
-        *s_base = base;
-        double tbm = 0.0, tmx = 0.0;
-        int tsk = 0;
-#pragma unroll
-        for (int k = 0; k < FT_WARPS; ++k) { tbm = tbm + s_wbm[k]; tmx = fmax(tmx, s_wmax[k]); tsk += s_wskel[k]; }
-        *bm_slot = tbm;
-        if (POOL_ONLY) {
-            // fixup path (rare): fold into the global accumulators
-            if (tmx > 0.0) atomicMax(&p.ws.ctl->maxdelta_bits, (unsigned long long)__double_as_longlong(tmx));
-            if (tsk) atomicAdd(&p.ws.ctl->skel_total, (unsigned long long)tsk);
-            if (tile_total) atomicAdd(&p.ws.ctl->nnz_total, (unsigned long long)tile_total);
-        } else {
-            // fast path: per-tile slots, reduced by finalize_kernel (no
-            // same-address atomics across the ~10^5 tiles of a step)
-            p.ws.tile_maxd[tile] = tmx;
-            p.ws.tile_cs[tile] = make_int2(tile_total, tsk);
-        }
+    if (emit) {
+        if (res.cnt <= 2) put_dense<T>(p, j, res.cnt, sk.r0, sk.x0, sk.r1, sk.x1);
+        else { p.out.sig[j] = -res.cnt; p.out.aux[j] = (int)poff; }
     }
-    __syncthreads();
-    o.base = *s_base;
-    return o;
 }
 
 // ---------------------------------------------------------------------------
-// tier 1 (see step_kernel6 below for the default split variant and
-// step_kernel3 for the in-place one): one thread per vertex column,
-// 128-column CTAs, the L row, the neighbours' descriptors and entries in
-// registers, no barrier before the tile epilogue.
+// the L^T column of a vertex
 
 constexpr int kMD = 8;
 constexpr int kPackEmpty = -32768;
@@ -682,33 +676,34 @@ __device__ __forceinline__ int load_lrow(const StepParams& p, int jl, int j, boo
     return n;
 }
 
+template <typename T, bool UNIFORM>
+__device__ __forceinline__ double lap_value(const StepParams& p, int k, int kd, int q0, double invdeg) {
+    return UNIFORM ? ((k == kd) ? -1.0 : invdeg) : ldv<T>(p.lap_val, q0 + k);
+}
+
+__device__ __forceinline__ double recip_deg(int n) { return n - 1 <= 32 ? c_recip[n - 1] : 1.0 / (double)(n - 1); }
+
 // ---------------------------------------------------------------------------
-// tier 1, split (default): classification and the closed form only.
+// tier 1: classification and the closed form.
 //
 // A column whose neighbourhood is one layer row (every non-empty neighbour
 // holds one entry, of the column's own row; its phi > 0) is finished here
-// with the exact single-row closed form.  Everything else is queued: up to
-// two entries per neighbour for tier 1.5 (gen_kernel, the one-pass two-row
-// update on dense warps), more for tier 2.  So no warp runs the general
-// update for a few of its lanes.  The neighbours' VALUES are not read: the
+// with the exact single-row closed form.  The others are flagged in their
+// segment's masks: at most two entries per neighbour -> tier 1.5, more (or
+// no packable L row) -> tier 2.  The neighbours' VALUES are not read: the
 // closed form needs them only through the finiteness of Lt, and values this
 // library wrote are finite unless a kernel raised the sticky nonfinite flag
-// (the canonical input, FT_LAP_CHECK_FINITE and a raised flag switch the
-// check on).
+// (ft_tiled_from_csc raises it for non-finite input; FT_LAP_CHECK_FINITE and
+// a raised flag switch the check on).  One warp = one 32-column segment:
+// statistics and masks go to the segment's slots, no CTA barrier.
 
-template <typename T, bool UNIFORM, bool IN_CANON, bool PACKED>
-__global__ void __launch_bounds__(FT_TPB, 8) step_kernel6(const StepParams p) {
-    __shared__ double s_wbm[FT_WARPS];
-    __shared__ double s_wmax[FT_WARPS];
-    __shared__ int s_wskel[FT_WARPS];
-    __shared__ int s_scan[FT_WARPS];
-    __shared__ long long s_base;
-
+template <typename T, bool UNIFORM, bool PACKED>
+__global__ void __launch_bounds__(FT_TPB, 8) tier1_kernel(const StepParams p) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
-    const bool chk = IN_CANON || p.force_check || *(volatile unsigned int*)&p.ws.ctl->nonfinite;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool chk = p.force_check || *(volatile unsigned int*)&p.ws.ctl->nonfinite;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tile = blockIdx.x;
-    const int jl = tile * FT_TPB + tid;
+    const int jl = tile * FT_TPB + threadIdx.x;
     const int j = p.j_base + jl;
     const bool active = jl < p.n_v;
 
@@ -721,194 +716,89 @@ __global__ void __launch_bounds__(FT_TPB, 8) step_kernel6(const StepParams p) {
     for (int k = 0; k < kMD; ++k)
         if (u[k] == j) kd = k;
     if (active && kd < 0) wide = true;
-    int rs = INT_MAX;
-    double phs = 0.0;
-    bool cand;
-    if (IN_CANON) {
-        // canonical input: descriptors from col_ptr, rows by loads
-        int2 d[kMD];
+    int sg[kMD];
 #pragma unroll
-        for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<true>(p, u[k]) : make_int2(0, 0);
-        bool multi = false;
-        int2 dself = make_int2(0, 0);
+    for (int k = 0; k < kMD; ++k) sg[k] = (k < n) ? __ldg(&p.in.sig[u[k]]) : FT_SIG_EMPTY;
+    const double phs = active ? ldv<T>(p.in.v0, j) : 0.0;
+    int rs = FT_SIG_EMPTY;
 #pragma unroll
-        for (int k = 0; k < kMD; ++k) {
-            if (k == kd) dself = d[k];
-            multi |= d[k].y > 1;
-        }
-        cand = active && !wide && !multi && p.finite && dself.y == 1;
-        if (cand) {
-            rs = __ldg(&p.in_idx[dself.x]);
-            phs = ldv<T>(p.in_val, dself.x);
-        }
-        bool same = true;
+    for (int k = 0; k < kMD; ++k)
+        if (k == kd) rs = sg[k];
+    bool same = true, big = false;
 #pragma unroll
-        for (int k = 0; k < kMD; ++k)
-            if (cand && d[k].y == 1 && k != kd) same &= __ldg(&p.in_idx[d[k].x]) == rs;
-        cand = cand && same && phs > 0.0;
-    } else {
-        // tiled input: the neighbours' row signatures (their own descriptors
-        // are not needed), the column's value through its descriptor
-        int sg[kMD];
-#pragma unroll
-        for (int k = 0; k < kMD; ++k) sg[k] = (k < n) ? __ldg(&p.in_sig[u[k]]) : -2;
-        const int2 dself = active ? __ldg(&p.in_desc[j]) : make_int2(0, 0);
-#pragma unroll
-        for (int k = 0; k < kMD; ++k)
-            if (k == kd) rs = sg[k];
-        cand = active && !wide && p.finite && rs >= 0;
-        bool same = true;
-#pragma unroll
-        for (int k = 0; k < kMD; ++k) same &= (sg[k] == -2) || (sg[k] == rs);
-        if (cand) phs = ldv<T>(p.in_val, dself.x);
-        cand = cand && same && phs > 0.0;
+    for (int k = 0; k < kMD; ++k) {
+        same &= (sg[k] == FT_SIG_EMPTY) || (sg[k] == rs);
+        big |= sg[k] <= -3;
     }
+    bool cand = active && !wide && p.finite && rs >= 0 && rs < kPair && same && phs > 0.0;
     if (chk && cand) {
         // Lt(rs, j) must be finite for the closed form: read the values
         bool fin = true;
         double lam = 0.0;
-        const double invdeg = UNIFORM ? (n - 1 <= 32 ? c_recip[n - 1] : 1.0 / (double)(n - 1)) : 0.0;
+        const double invdeg = UNIFORM ? recip_deg(n) : 0.0;
 #pragma unroll
         for (int k = 0; k < kMD; ++k) {
-            const int2 dk = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
-            if (dk.y == 1) {
-                const double v = ldv<T>(p.in_val, dk.x);
+            if (k < n && sg[k] == rs) {
+                const double v = ldv<T>(p.in.v0, u[k]);
                 fin &= isfinite(v);
-                const double l = UNIFORM ? ((k == kd) ? -1.0 : invdeg) : ldv<T>(p.lap_val, q0 + k);
-                lam = lam + v * l;
+                lam = lam + v * lap_value<T, UNIFORM>(p, k, kd, q0, invdeg);
             }
         }
         cand = fin && isfinite(lam);
     }
     const bool fast = cand;
-    const bool gen = active && !wide && !fast;
+    const bool slow = active && !fast && (wide || big);
+    const bool gen = active && !fast && !slow;
 
-    VRes res;
-    vres_init(res);
-    double nv = 0.0;
+    double bm = 0.0, md = 0.0;
+    int cnt = 0;
     if (fast) {
         double v = phs;
         if (v > 1.0) v = 1.0;
         const double s = 0.0 + v;
-        nv = v * (1.0 / s);
-        res.nskel = 1;
+        const double nv = v * (1.0 / s);
         if (nv != 0.0) {
-            res.cnt = 1;
-            if (rs == 0) res.bm = nv;
+            cnt = 1;
+            if (rs == 0) bm = nv;
         }
-        res.maxd = fabs(nv - phs);
-    }
-    // queues without hot atomics: tier 1.5 (gen) columns into this tile's
-    // list (slow_list + 2 n_v + 128 tile, count tile_gen[tile]); tier 2
-    // (wide) columns into the global queue with one atomic per CTA
-    __shared__ int s_gq[FT_WARPS], s_wq[FT_WARPS + 1];
-    const unsigned int gbits = __ballot_sync(0xffffffffu, gen);
-    const unsigned int wbits = __ballot_sync(0xffffffffu, wide && active);
-    if (lane == 0) { s_gq[warp] = __popc(gbits); s_wq[warp] = __popc(wbits); }
-    __syncthreads();
-    int gpre = 0, wpre = 0, gtot = 0, wtot = 0;
-#pragma unroll
-    for (int q = 0; q < FT_WARPS; ++q) {
-        if (q < warp) { gpre += s_gq[q]; wpre += s_wq[q]; }
-        gtot += s_gq[q];
-        wtot += s_wq[q];
-    }
-    if (tid == 0) {
-        p.ws.tile_gen[tile] = gtot;
-        s_wq[FT_WARPS] = wtot ? atomicAdd(&p.ws.ctl->slow_count, wtot) : 0;
-    }
-    if (gen)
-        p.ws.slow_list[2 * p.n_v + tile * FT_TPB + gpre + __popc(gbits & ((1u << lane) - 1u))] = j;
-    __syncthreads();
-    if (wide && active) p.ws.slow_list[s_wq[FT_WARPS] + wpre + __popc(wbits & ((1u << lane) - 1u))] = j;
-    // tier-2 columns report their base mass through vbm (finalize, by mask);
-    // tier 1.5 adds its columns' base mass to tile_bm in a fixed order
-    if (lane == 0) p.ws.slow_mask[(size_t)tile * FT_WARPS + warp] = wbits;
-    const TileOut o = tile_epilogue<false>(res.cnt, res.nskel, res.bm, res.maxd, tile, &p.ws.tile_bm[tile], p,
-                                           s_scan, s_wbm, s_wmax, s_wskel, &s_base);
-    if (!fast || o.base < 0) return;
-    const long long off = o.base + o.local_off;
-    p.out_desc[j] = make_int2((int)off, res.cnt);
-    p.out_sig[j] = sig_of(res.cnt, rs);
-    if (res.cnt) {
-        p.out_idx[off] = rs;
-        ((T*)p.out_val)[off] = (T)nv;
+        md = fabs(nv - phs);
+        p.out.sig[j] = cnt ? rs : FT_SIG_EMPTY;
+        ((T*)p.out.v0)[j] = (T)nv;
         if (!isfinite(nv)) atomicOr(&p.ws.ctl->nonfinite, 1u);
     }
-}
-
-// ---------------------------------------------------------------------------
-// tier 2: the queued wide columns, one thread each over the compacted list
-// (full warps), with the exact windowed global-memory algorithm
-// (vertex_slow: no width limit).  Output space comes from the pool (one
-// atomic per warp); the column's base mass goes to vbm[j] so the finalize
-// reduction can add it in a fixed order.
-
-// Gather for tier 2: up to kMD L entries (descriptors in registers), any
-// number of entries per neighbour column (re-read from L1 in every row
-// pass), up to K rows.  Returns false when the column exceeds kMD or K (the
-// caller then uses vertex_slow).
-template <typename T, int K, bool UNIFORM, bool IN_CANON>
-__device__ __forceinline__ bool gather_wide(int j, const StepParams& p, Win<K>& w) {
-    const int q0 = __ldg(&p.lap_ptr[j - p.j_base]);
-    const int n = __ldg(&p.lap_ptr[j - p.j_base + 1]) - q0;
-    if (n > kMD || n < 1) return false;
-    int u[kMD];
+    const unsigned int fb = __ballot_sync(0xffffffffu, fast);
+    const unsigned int gb = __ballot_sync(0xffffffffu, gen);
+    const unsigned int wb = __ballot_sync(0xffffffffu, slow);
+    bm = warp_sum(bm);      // fixed shuffle tree: deterministic
+    cnt = warp_sum(cnt);
 #pragma unroll
-    for (int k = 0; k < kMD; ++k) u[k] = (k < n) ? __ldg(&p.lap_idx[q0 + k]) : -1;
-    int2 d[kMD];
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
-    int kd = -1;
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) if (u[k] == j) kd = k;
-    if (kd < 0) return false;
-    const int* __restrict__ gi = p.in_idx;
-    const T* __restrict__ gv = (const T*)p.in_val;
-    const double invdeg = UNIFORM ? (n - 1 <= 32 ? c_recip[n - 1] : 1.0 / (double)(n - 1)) : 0.0;
-    int lo = -1;
-    w.m = 0;
-#pragma unroll
-    for (int i = 0; i <= K; ++i) {
-        int rr = INT_MAX;
-#pragma unroll
-        for (int k = 0; k < kMD; ++k) {
-            for (int t = 0; t < d[k].y; ++t) {
-                const int x = __ldg(&gi[d[k].x + t]);
-                if (x > lo) { if (x < rr) rr = x; break; }   // rows ascend in a column
-            }
-        }
-        if (i == K) return rr == INT_MAX;     // more than K rows?
-        double lam = 0.0, ph = 0.0;
-        if (rr != INT_MAX) {
-#pragma unroll
-            for (int k = 0; k < kMD; ++k) {
-                const double l = UNIFORM ? ((k == kd) ? -1.0 : invdeg) : ldv<T>(p.lap_val, q0 + k);
-                for (int t = 0; t < d[k].y; ++t) {
-                    const int x = __ldg(&gi[d[k].x + t]);
-                    if (x == rr) {
-                        const double vv = (double)__ldg(&gv[d[k].x + t]);
-                        lam = lam + vv * l;
-                        if (k == kd) ph = vv;
-                    }
-                    if (x >= rr) break;
-                }
-            }
-            w.m = i + 1;
-            lo = rr;
-        }
-        w.rows[i] = rr;
-        w.lam[i] = lam;
-        w.phi[i] = ph;
+    for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_down_sync(0xffffffffu, md, o));
+    if (lane == 0) {
+        const int seg = tile * FT_WARPS + warp;
+        p.ws.seg_bm[seg] = bm;
+        p.ws.seg_maxd[seg] = md;
+        p.ws.seg_cs[seg] = make_int2(cnt, __popc(fb));
+        p.ws.gen_mask[seg] = gb;
+        p.ws.slow_mask[seg] = wb;
     }
-    return true;
 }
 
-// warp-aggregated pool allocation + statistics for one batch of columns
-template <typename T, int K>
-__device__ __forceinline__ long long pool_place(int cnt, const VRes& res, const StepParams& p, int lane,
-                                                bool& fits, int& excl) {
-    int incl = cnt;
+// the r-th (0-based) set bit of m
+__device__ __forceinline__ int nth_bit(unsigned int m, int r) {
+    int pos = 0;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const int c = __popc(m & ((1u << s) - 1u));
+        if (r >= c) { r -= c; m >>= s; pos += s; }
+    }
+    return pos;
+}
+
+// warp-aggregated pool allocation (need entries per lane) + the global
+// statistics of tiers 2/3 (few columns: one atomic per warp)
+__device__ __forceinline__ long long pool_place(int need, const VRes& res, const StepParams& p, int lane,
+                                                bool& fits) {
+    int incl = need;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -916,90 +806,101 @@ __device__ __forceinline__ long long pool_place(int cnt, const VRes& res, const 
     }
     const int wtot = __shfl_sync(0xffffffffu, incl, 31);
     long long base = 0;
-    if (lane == 31 && wtot > 0)
-        base = (long long)p.num_tiles * FT_SLOT +
-               (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)wtot);
+    if (lane == 31 && wtot > 0) base = (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)wtot);
     base = __shfl_sync(0xffffffffu, base, 31);
     fits = base + wtot <= p.cap;
     if (lane == 31 && !fits) atomicExch(&p.ws.ctl->overflow, 1);
     const int skel = warp_sum(res.nskel);
+    const int nnz = warp_sum(res.cnt);
     double mx = res.maxd;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
     if (lane == 0) {
         if (mx > 0.0) atomicMax(&p.ws.ctl->maxdelta_bits, (unsigned long long)__double_as_longlong(mx));
         if (skel) atomicAdd(&p.ws.ctl->skel_total, (unsigned long long)skel);
-        if (wtot) atomicAdd(&p.ws.ctl->nnz_total, (unsigned long long)wtot);
+        if (nnz) atomicAdd(&p.ws.ctl->nnz_total, (unsigned long long)nnz);
     }
-    excl = incl - cnt;
-    return base;
+    return base + incl - need;
 }
 
-// tier 1.5: the general columns (at most two entries per neighbour) that
-// tier 1 listed per tile, one warp per tile with the columns on its lanes:
-// the one-pass two-row update.  More than two rows -> tier 2.  Outputs go
-// right after the tile's tier-1 entries in its slot (the pool if they do
-// not fit), statistics into the tile's slots and vbm -- no hot atomics.
-template <typename T, bool UNIFORM, bool IN_CANON, bool PACKED>
-__global__ void __launch_bounds__(FT_TPB, 10) gen_kernel(const StepParams p) {
+// ---------------------------------------------------------------------------
+// tier 1.5: the flagged columns with at most two entries per neighbour, one
+// warp per tile with the columns on its lanes: the one-pass two-row update.
+// More than two rows -> tier 2 (added to the tile's slow mask).  The warp
+// then queues the tile's tier-2 columns with one atomic.  Statistics into
+// the tile's slots, base mass in lane order (fixed): no hot atomics.
+
+template <typename T, bool UNIFORM, bool PACKED>
+__global__ void __launch_bounds__(FT_TPB, 8) gen_kernel(const StepParams p) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
+    __shared__ int s_list[FT_WARPS][FT_TPB];
     const int lane = threadIdx.x & 31;
+    int* list = s_list[threadIdx.x >> 5];
     const int nwarps = gridDim.x * FT_WARPS;
     for (int t = (blockIdx.x * FT_TPB + threadIdx.x) >> 5; t < p.num_tiles; t += nwarps) {
-        const int ng = p.ws.tile_gen[t];
-        if (ng == 0) continue;
-        const int2 cs = p.ws.tile_cs[t];
-        const bool in_slot = cs.x <= FT_SLOT;     // tier 1 placed the tile in its slot
-        int used = cs.x;
-        double tmx = 0.0, tbm = 0.0;
+        const uint4 g4 = *reinterpret_cast<const uint4*>(&p.ws.gen_mask[(size_t)FT_WARPS * t]);
+        const uint4 w4 = *reinterpret_cast<const uint4*>(&p.ws.slow_mask[(size_t)FT_WARPS * t]);
+        const unsigned int gm[4] = {g4.x, g4.y, g4.z, g4.w};
+        const unsigned int wm[4] = {w4.x, w4.y, w4.z, w4.w};
+        int ng = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if ((gm[q] >> lane) & 1u) list[ng + __popc(gm[q] & ((1u << lane) - 1u))] = t * FT_TPB + q * 32 + lane;
+            ng += __popc(gm[q]);
+        }
+        if (ng == 0 && (wm[0] | wm[1] | wm[2] | wm[3]) == 0) continue;
+        __syncwarp();
+        double tbm = 0.0, tmx = 0.0;
         int tcnt = 0, tskel = 0;
+        unsigned int df[4] = {0u, 0u, 0u, 0u};
         for (int c0 = 0; c0 < ng; c0 += 32) {
             const bool mine = c0 + lane < ng;
-            const int j = mine ? p.ws.slow_list[2 * p.n_v + t * FT_TPB + c0 + lane] : p.j_base;
-            const int jl = j - p.j_base;
+            const int jl = mine ? list[c0 + lane] : 0;
+            const int j = p.j_base + jl;
             int q0 = 0;
             int u[kMD];
             const int n = load_lrow<PACKED>(p, jl, j, mine, u, q0);
-            int2 d[kMD];
+            int sg[kMD], ax[kMD];
 #pragma unroll
-            for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
+            for (int k = 0; k < kMD; ++k) {
+                const bool h = k < n;
+                sg[k] = h ? __ldg(&p.in.sig[u[k]]) : FT_SIG_EMPTY;
+                ax[k] = h ? __ldg(&p.in.aux[u[k]]) : 0;
+            }
             int kd = -1;
-            bool big = false;          // a neighbour with more than two entries
-#pragma unroll
-            for (int k = 0; k < kMD; ++k) {
-                if (u[k] == j) kd = k;
-                big |= d[k].y > 2;
-            }
-            // rows in registers; values loaded in the accumulation pass
-            int r0[kMD], r1[kMD];
-#pragma unroll
-            for (int k = 0; k < kMD; ++k) {
-                r0[k] = (d[k].y > 0) ? __ldg(&p.in_idx[d[k].x]) : INT_MAX;
-                r1[k] = (d[k].y > 1) ? __ldg(&p.in_idx[d[k].x + 1]) : INT_MAX;
-            }
+            bool big = false;
             int rlo = INT_MAX, rhi = -1;
 #pragma unroll
             for (int k = 0; k < kMD; ++k) {
-                if (r0[k] != INT_MAX) { rlo = min(rlo, r0[k]); rhi = max(rhi, r0[k]); }
-                if (r1[k] != INT_MAX) { rlo = min(rlo, r1[k]); rhi = max(rhi, r1[k]); }
+                if (u[k] == j) kd = k;
+                big |= sg[k] <= -3;
+                if (sg[k] >= 0) {
+                    const int x = sg[k] & ~kPair;
+                    rlo = min(rlo, x); rhi = max(rhi, x);
+                    if (sg[k] & kPair) { rlo = min(rlo, ax[k]); rhi = max(rhi, ax[k]); }
+                }
             }
-            const double invdeg = UNIFORM ? (n - 1 <= 32 ? c_recip[n - 1] : 1.0 / (double)(n - 1)) : 0.0;
+            // values loaded in the accumulation pass (registers)
+            const double invdeg = UNIFORM ? recip_deg(n) : 0.0;
             double l0 = 0.0, l1 = 0.0, p0 = 0.0, p1 = 0.0;
             bool more = false;
 #pragma unroll
             for (int k = 0; k < kMD; ++k) {
-                const double l = UNIFORM ? ((k == kd) ? -1.0 : invdeg)
-                                         : ((k < n) ? ldv<T>(p.lap_val, q0 + k) : 0.0);
-                const double a0 = (r0[k] != INT_MAX) ? ldv<T>(p.in_val, d[k].x) : 0.0;
-                const double a1 = (r1[k] != INT_MAX) ? ldv<T>(p.in_val, d[k].x + 1) : 0.0;
-                if (r0[k] == rlo) { l0 = l0 + a0 * l; if (k == kd) p0 = a0; }
-                else if (r0[k] == rhi) { l1 = l1 + a0 * l; if (k == kd) p1 = a0; }
-                else if (r0[k] != INT_MAX) more = true;
-                if (r1[k] == rlo) { l0 = l0 + a1 * l; if (k == kd) p0 = a1; }
-                else if (r1[k] == rhi) { l1 = l1 + a1 * l; if (k == kd) p1 = a1; }
-                else if (r1[k] != INT_MAX) more = true;
+                if (sg[k] < 0) continue;
+                const double l = lap_value<T, UNIFORM>(p, k, kd, q0, invdeg);
+                const int x0 = sg[k] & ~kPair;
+                const double a0 = ldv<T>(p.in.v0, u[k]);
+                if (x0 == rlo) { l0 = l0 + a0 * l; if (k == kd) p0 = a0; }
+                else if (x0 == rhi) { l1 = l1 + a0 * l; if (k == kd) p1 = a0; }
+                else more = true;
+                if (sg[k] & kPair) {
+                    const double a1 = ldv<T>(p.in.v1, u[k]);
+                    if (ax[k] == rlo) { l0 = l0 + a1 * l; if (k == kd) p0 = a1; }
+                    else if (ax[k] == rhi) { l1 = l1 + a1 * l; if (k == kd) p1 = a1; }
+                    else more = true;
+                }
             }
-            const bool wide = mine && (more || big || rlo == INT_MAX);
+            const bool defer = mine && (more || big || rlo == INT_MAX || kd < 0 || n == 0);
             Win<2> w;
             w.rows[0] = rlo; w.lam[0] = l0; w.phi[0] = p0;
             w.rows[1] = rhi; w.lam[1] = l1; w.phi[1] = p1;
@@ -1008,105 +909,92 @@ __global__ void __launch_bounds__(FT_TPB, 10) gen_kernel(const StepParams p) {
             VRes res;
             vres_init(res);
             unsigned int out_mask = 0;
-            if (mine && !wide) {
+            const bool run = mine && !defer;
+            if (run) {
                 process_two(w, p, res, out_mask);
                 report_flags(res, j, p);
+                emit_window<T, 2>(w, out_mask, j, 0, p);
             }
-            const unsigned int wb = __ballot_sync(0xffffffffu, wide);
-            if (wb) {
-                int qb = 0;
-                if (lane == 0) qb = atomicAdd(&p.ws.ctl->slow_count, __popc(wb));
-                qb = __shfl_sync(0xffffffffu, qb, 0);
-                if (wide) {
-                    p.ws.slow_list[qb + __popc(wb & ((1u << lane) - 1u))] = j;
-                    // tier 2 reports this column's base mass through vbm
-                    const int lt = jl - t * FT_TPB;
-                    atomicOr(&p.ws.slow_mask[(size_t)t * FT_WARPS + (lt >> 5)], 1u << (lt & 31));
-                }
-            }
-            // placement: the tile slot after its entries, else the pool
-            const int cnt = (mine && !wide) ? res.cnt : 0;
-            int incl = cnt;
+            if (defer) {
+                const int lt = jl - t * FT_TPB;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
+                for (int q = 0; q < 4; ++q)
+                    if ((lt >> 5) == q) df[q] |= 1u << (lt & 31);
             }
-            const int wsum = __shfl_sync(0xffffffffu, incl, 31);
-            long long base;
-            if (in_slot && used + wsum <= FT_SLOT) {
-                base = (long long)t * FT_SLOT + used;
-                used += wsum;
-            } else {
-                base = 0;
-                if (lane == 31 && wsum > 0)
-                    base = (long long)p.num_tiles * FT_SLOT +
-                           (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)wsum);
-                base = __shfl_sync(0xffffffffu, base, 31);
-                if (base + wsum > p.cap) {
-                    if (lane == 0) atomicExch(&p.ws.ctl->overflow, 1);
-                    base = -1;
-                }
-            }
-            // base mass of the chunk, lane order (the tile's gen list is in
-            // vertex order): a fixed order, so the total is deterministic
-            double cbm = (mine && !wide) ? res.bm : 0.0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double y = __shfl_down_sync(0xffffffffu, cbm, o);
-                if ((lane & (2 * o - 1)) == 0) cbm = cbm + y;
-            }
+            // base mass of the chunk in lane order (the list is in vertex
+            // order): a fixed order, so the total is deterministic
+            double cbm = run ? res.bm : 0.0;
+            cbm = warp_sum(cbm);
             tbm = tbm + __shfl_sync(0xffffffffu, cbm, 0);
-            if (mine && !wide) {
-                if (base >= 0) {
-                    const long long off = base + incl - cnt;
-                    p.out_desc[j] = make_int2((int)off, res.cnt);
-                    p.out_sig[j] = sig_of(res.cnt, window_row1<2>(w.rows, out_mask));
-                    if (out_mask) emit_window<T, 2>(w, out_mask, off, p);
-                }
-            }
             tmx = fmax(tmx, res.maxd);
-            tcnt += cnt;
-            tskel += (mine && !wide) ? res.nskel : 0;
+            tcnt += run ? res.cnt : 0;
+            tskel += run ? res.nskel : 0;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) tmx = fmax(tmx, __shfl_down_sync(0xffffffffu, tmx, o));
         tcnt = warp_sum(tcnt);
         tskel = warp_sum(tskel);
-        if (lane == 0) {
-            p.ws.tile_maxd[t] = fmax(p.ws.tile_maxd[t], tmx);
-            p.ws.tile_cs[t] = make_int2(cs.x + tcnt, cs.y + tskel);
-            p.ws.tile_bm[t] = p.ws.tile_bm[t] + tbm;
+        if (lane == 0 && ng > 0) {
+            p.ws.gen_bm[t] = tbm;
+            p.ws.gen_maxd[t] = tmx;
+            p.ws.gen_cs[t] = make_int2(tcnt, tskel);
         }
+        // tier-2 queue: tier 1's slow columns and the deferred ones
+        unsigned int all[4];
+        int nq = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const unsigned int d = __reduce_or_sync(0xffffffffu, df[q]);
+            all[q] = wm[q] | d;
+            if (d && lane == 0) p.ws.slow_mask[(size_t)FT_WARPS * t + q] = all[q];
+            nq += __popc(all[q]);
+        }
+        if (nq) {
+            int qb = 0;
+            if (lane == 0) qb = atomicAdd(&p.ws.ctl->slow_count, nq);
+            qb = __shfl_sync(0xffffffffu, qb, 0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if ((all[q] >> lane) & 1u)
+                    p.ws.slow_list[qb + __popc(all[q] & ((1u << lane) - 1u))] = p.j_base + t * FT_TPB + q * 32 + lane;
+                qb += __popc(all[q]);
+            }
+        }
+        __syncwarp();
     }
 }
 
-// tier 2a: the queued wide columns with at most three rows and at most
-// three entries per neighbour (~90% of them at C3): rows = min, max and the
-// one other candidate; the three Lt sums in one (u, t) pass.  Others go on
-// to tier 2b (the 8-row window) through slow_list + 3 n_v + FT_TPB.
-template <typename T, bool UNIFORM, bool IN_CANON, bool PACKED>
+// ---------------------------------------------------------------------------
+// tier 2a: the queued columns with at most three rows and at most three
+// entries per neighbour: rows = min, max and the one other candidate; the
+// three Lt sums in one (u, t) pass.  Others go on to tier 2b through
+// slow_list + 2 n_v.
+
+template <typename T, bool UNIFORM, bool PACKED>
 __device__ __forceinline__ bool wide3(int j, const StepParams& p, Win<3>& w) {
     int q0 = 0;
     int u[kMD];
     const int n = load_lrow<PACKED>(p, j - p.j_base, j, true, u, q0);
     if (n == 0) return false;
-    int2 d[kMD];
+    int sg[kMD], ax[kMD];
 #pragma unroll
-    for (int k = 0; k < kMD; ++k) d[k] = (k < n) ? load_desc<IN_CANON>(p, u[k]) : make_int2(0, 0);
+    for (int k = 0; k < kMD; ++k) {
+        sg[k] = (k < n) ? __ldg(&p.in.sig[u[k]]) : FT_SIG_EMPTY;
+        ax[k] = (k < n) ? __ldg(&p.in.aux[u[k]]) : 0;
+    }
     int kd = -1;
     bool big = false;
 #pragma unroll
     for (int k = 0; k < kMD; ++k) {
         if (u[k] == j) kd = k;
-        big |= d[k].y > 3;
+        big |= sig_count(sg[k]) > 3;
     }
     if (kd < 0 || big) return false;
     int rr[kMD][3];
 #pragma unroll
     for (int k = 0; k < kMD; ++k)
 #pragma unroll
-        for (int t = 0; t < 3; ++t) rr[k][t] = (t < d[k].y) ? __ldg(&p.in_idx[d[k].x + t]) : INT_MAX;
+        for (int t = 0; t < 3; ++t) rr[k][t] = (t < sig_count(sg[k])) ? hyb_row<T>(p.in, sg[k], ax[k], t) : INT_MAX;
     int rlo = INT_MAX, rhi = -1;
 #pragma unroll
     for (int k = 0; k < kMD; ++k)
@@ -1114,18 +1002,18 @@ __device__ __forceinline__ bool wide3(int j, const StepParams& p, Win<3>& w) {
         for (int t = 0; t < 3; ++t)
             if (rr[k][t] != INT_MAX) { rlo = min(rlo, rr[k][t]); rhi = max(rhi, rr[k][t]); }
     if (rlo == INT_MAX) return false;
-    const double invdeg = UNIFORM ? (n - 1 <= 32 ? c_recip[n - 1] : 1.0 / (double)(n - 1)) : 0.0;
+    const double invdeg = UNIFORM ? recip_deg(n) : 0.0;
     double l0 = 0.0, l1 = 0.0, l2 = 0.0, p0 = 0.0, p1 = 0.0, p2 = 0.0;
     int rmid = INT_MAX;
     bool more = false;
 #pragma unroll
     for (int k = 0; k < kMD; ++k) {
-        const double l = UNIFORM ? ((k == kd) ? -1.0 : invdeg) : ((k < n) ? ldv<T>(p.lap_val, q0 + k) : 0.0);
+        const double l = (k < n) ? lap_value<T, UNIFORM>(p, k, kd, q0, invdeg) : 0.0;
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
             const int r = rr[k][t];
             if (r == INT_MAX) continue;
-            const double a = ldv<T>(p.in_val, d[k].x + t);
+            const double a = hyb_val<T>(p.in, u[k], sg[k], ax[k], t);
             if (r == rlo) { l0 = l0 + a * l; if (k == kd) p0 = a; }
             else if (r == rhi) { l2 = l2 + a * l; if (k == kd) p2 = a; }
             else {
@@ -1152,7 +1040,7 @@ __device__ __forceinline__ bool wide3(int j, const StepParams& p, Win<3>& w) {
     return true;
 }
 
-template <typename T, bool UNIFORM, bool IN_CANON, bool PACKED>
+template <typename T, bool UNIFORM, bool PACKED>
 __global__ void __launch_bounds__(FT_TPB, 4) wide3_kernel(const StepParams p) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     const int n_wide = *(volatile int*)&p.ws.ctl->slow_count;
@@ -1170,7 +1058,7 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide3_kernel(const StepParams p) {
         unsigned int out_mask = 0;
         bool on = false;
         if (mine) {
-            on = !wide3<T, UNIFORM, IN_CANON, PACKED>(j, p, w);
+            on = !wide3<T, UNIFORM, PACKED>(j, p, w);
             if (!on) {
                 process_window<3>(w, p, res, out_mask, c_recip);
                 report_flags(res, j, p);
@@ -1182,26 +1070,83 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide3_kernel(const StepParams p) {
             if (lane == 0) qb = atomicAdd(&p.ws.ctl->wide8_count, __popc(ob));
             qb = __shfl_sync(0xffffffffu, qb, 0);
             if (on) {
-                p.ws.slow_list[3 * p.n_v + FT_TPB + qb + __popc(ob & ((1u << lane) - 1u))] = j;
+                p.ws.slow_list[2 * p.n_v + qb + __popc(ob & ((1u << lane) - 1u))] = j;
                 vres_init(res);
             }
         }
         bool fits;
-        int excl;
-        const long long base = pool_place<T, 3>(on ? 0 : res.cnt, res, p, lane, fits, excl);
+        const int need = (mine && !on && res.cnt > 2) ? res.cnt : 0;
+        const long long off = pool_place(need, res, p, lane, fits);
         if (mine && !on) {
             p.ws.vbm[j - p.j_base] = res.bm;
-            if (fits) {
-                const long long off = base + excl;
-                p.out_desc[j] = make_int2((int)off, res.cnt);
-                p.out_sig[j] = sig_of(res.cnt, window_row1<3>(w.rows, out_mask));
-                if (out_mask) emit_window<T, 3>(w, out_mask, off, p);
-            }
+            if (need == 0 || fits) emit_window<T, 3>(w, out_mask, j, off, p);
         }
     }
 }
 
-template <typename T, bool UNIFORM, bool IN_CANON>
+// Gather for tier 2b: up to kMD L entries (signatures in registers), any
+// number of entries per neighbour column (re-read from L1 in every row
+// pass), up to K rows.  Returns false when the column exceeds kMD or K (the
+// caller then uses vertex_slow).
+template <typename T, int K, bool UNIFORM>
+__device__ __forceinline__ bool gather_wide(int j, const StepParams& p, Win<K>& w) {
+    const int q0 = __ldg(&p.lap_ptr[j - p.j_base]);
+    const int n = __ldg(&p.lap_ptr[j - p.j_base + 1]) - q0;
+    if (n > kMD || n < 1) return false;
+    int u[kMD];
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) u[k] = (k < n) ? __ldg(&p.lap_idx[q0 + k]) : -1;
+    int sg[kMD], ax[kMD], cn[kMD];
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) {
+        sg[k] = (k < n) ? __ldg(&p.in.sig[u[k]]) : FT_SIG_EMPTY;
+        ax[k] = (k < n) ? __ldg(&p.in.aux[u[k]]) : 0;
+        cn[k] = sig_count(sg[k]);
+    }
+    int kd = -1;
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) if (u[k] == j) kd = k;
+    if (kd < 0) return false;
+    const double invdeg = UNIFORM ? recip_deg(n) : 0.0;
+    int lo = -1;
+    w.m = 0;
+#pragma unroll
+    for (int i = 0; i <= K; ++i) {
+        int rr = INT_MAX;
+#pragma unroll
+        for (int k = 0; k < kMD; ++k) {
+            for (int t = 0; t < cn[k]; ++t) {
+                const int x = hyb_row<T>(p.in, sg[k], ax[k], t);
+                if (x > lo) { if (x < rr) rr = x; break; }   // rows ascend in a column
+            }
+        }
+        if (i == K) return rr == INT_MAX;     // more than K rows?
+        double lam = 0.0, ph = 0.0;
+        if (rr != INT_MAX) {
+#pragma unroll
+            for (int k = 0; k < kMD; ++k) {
+                const double l = (k < n) ? lap_value<T, UNIFORM>(p, k, kd, q0, invdeg) : 0.0;
+                for (int t = 0; t < cn[k]; ++t) {
+                    const int x = hyb_row<T>(p.in, sg[k], ax[k], t);
+                    if (x == rr) {
+                        const double vv = hyb_val<T>(p.in, u[k], sg[k], ax[k], t);
+                        lam = lam + vv * l;
+                        if (k == kd) ph = vv;
+                    }
+                    if (x >= rr) break;
+                }
+            }
+            w.m = i + 1;
+            lo = rr;
+        }
+        w.rows[i] = rr;
+        w.lam[i] = lam;
+        w.phi[i] = ph;
+    }
+    return true;
+}
+
+template <typename T, bool UNIFORM>
 __global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p) {
     constexpr int KW = 8;      // wider unions go to tier 3
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
@@ -1212,20 +1157,20 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p) {
     for (int rnd = 0; rnd < rounds; ++rnd) {
         const int i = rnd * stride + blockIdx.x * FT_TPB + threadIdx.x;
         const bool mine = i < n_wide;
-        const int j = mine ? p.ws.slow_list[3 * p.n_v + FT_TPB + i] : 0;
+        const int j = mine ? p.ws.slow_list[2 * p.n_v + i] : 0;
         VRes res;
         vres_init(res);
         Win<KW> w;
         unsigned int out_mask = 0;
         bool deep = false;
         if (mine) {
-            deep = !gather_wide<T, KW, UNIFORM, IN_CANON>(j, p, w);
+            deep = !gather_wide<T, KW, UNIFORM>(j, p, w);
             if (!deep) {
                 process_window<KW>(w, p, res, out_mask, c_recip);
                 report_flags(res, j, p);
             }
         }
-        // tier 3: beyond the tier-2 window (queued at the tail of slow_list)
+        // tier 3: beyond the tier-2 window (queued at slow_list + n_v)
         const unsigned int db = __ballot_sync(0xffffffffu, deep);
         if (db) {
             int qb = 0;
@@ -1237,22 +1182,17 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p) {
             }
         }
         bool fits;
-        int excl;
-        const long long base = pool_place<T, KW>(deep ? 0 : res.cnt, res, p, lane, fits, excl);
+        const int need = (mine && !deep && res.cnt > 2) ? res.cnt : 0;
+        const long long off = pool_place(need, res, p, lane, fits);
         if (mine && !deep) {
             p.ws.vbm[j - p.j_base] = res.bm;
-            if (fits) {
-                const long long off = base + excl;
-                p.out_desc[j] = make_int2((int)off, res.cnt);
-                p.out_sig[j] = sig_of(res.cnt, window_row1<KW>(w.rows, out_mask));
-                if (out_mask) emit_window<T, KW>(w, out_mask, off, p);
-            }
+            if (need == 0 || fits) emit_window<T, KW>(w, out_mask, j, off, p);
         }
     }
 }
 
 // tier 3: exact windowed global-memory algorithm (no width limit)
-template <typename T, bool UNIFORM, bool IN_CANON>
+template <typename T, bool UNIFORM>
 __global__ void __launch_bounds__(FT_TPB) deep_kernel(const StepParams p) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     const int n_deep = *(volatile int*)&p.ws.ctl->deep_count;
@@ -1266,20 +1206,17 @@ __global__ void __launch_bounds__(FT_TPB) deep_kernel(const StepParams p) {
         VRes res;
         vres_init(res);
         if (mine) {
-            vertex_slow<T, 8, UNIFORM, IN_CANON>(j, p, res, 0, false);
+            vertex_slow<T, 8, UNIFORM>(j, p, res, 0, false);
             report_flags(res, j, p);
         }
         bool fits;
-        int excl;
-        const long long base = pool_place<T, 8>(res.cnt, res, p, lane, fits, excl);
+        const int need = (mine && res.cnt > 2) ? res.cnt : 0;
+        const long long off = pool_place(need, res, p, lane, fits);
         if (mine) {
             p.ws.vbm[j - p.j_base] = res.bm;
-            if (fits) {
-                const long long off = base + excl;
-                p.out_desc[j] = make_int2((int)off, res.cnt);
-                const int total = res.cnt;
-                if (total) vertex_slow<T, 8, UNIFORM, IN_CANON>(j, p, res, off, true);
-                p.out_sig[j] = sig_of(total, total == 1 ? p.out_idx[off] : 0);
+            if (need == 0 || fits) {
+                VRes r2 = res;
+                vertex_slow<T, 8, UNIFORM>(j, p, r2, off, true);
             }
         }
     }
@@ -1287,7 +1224,7 @@ __global__ void __launch_bounds__(FT_TPB) deep_kernel(const StepParams p) {
 
 // ---------------------------------------------------------------------------
 // per-step finalisation: deterministic two-level base-mass reduction (fixed
-// per-CTA ranges, then the last CTA sums the partials in order), stats
+// per-CTA tile ranges, then the last CTA sums the partials in order), stats
 // record, error / convergence flags, accumulator reset.
 
 #define FT_FIN_TPB 128
@@ -1304,23 +1241,36 @@ __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizePara
     double acc = 0.0, amx = 0.0;
     long long acnt = 0, askel = 0;
     for (int t = t0 + tid; t < t1; t += FT_FIN_TPB) {
-        double tb = f.ws.tile_bm[t];
-        const uint4 mk = *reinterpret_cast<const uint4*>(&f.ws.slow_mask[(size_t)t * FT_WARPS]);
-        const unsigned int mw[4] = {mk.x, mk.y, mk.z, mk.w};
+        const uint4 g4 = *reinterpret_cast<const uint4*>(&f.ws.gen_mask[(size_t)t * FT_WARPS]);
+        const uint4 m4 = *reinterpret_cast<const uint4*>(&f.ws.slow_mask[(size_t)t * FT_WARPS]);
+        const unsigned int mw[4] = {m4.x, m4.y, m4.z, m4.w};
+        double tb = 0.0;
+#pragma unroll
+        for (int k = 0; k < FT_WARPS; ++k) {
+            const int s = t * FT_WARPS + k;
+            tb = tb + f.ws.seg_bm[s];
+            amx = fmax(amx, f.ws.seg_maxd[s]);
+            const int2 cs = f.ws.seg_cs[s];
+            acnt += cs.x;
+            askel += cs.y;
+        }
+        if (g4.x | g4.y | g4.z | g4.w) {
+            tb = tb + f.ws.gen_bm[t];
+            amx = fmax(amx, f.ws.gen_maxd[t]);
+            const int2 cs = f.ws.gen_cs[t];
+            acnt += cs.x;
+            askel += cs.y;
+        }
 #pragma unroll
         for (int k = 0; k < FT_WARPS; ++k) {
             unsigned int m = mw[k];
-            while (m) {   // wide columns of the tile, in vertex order
+            while (m) {   // tier-2/3 columns of the tile, in vertex order
                 const int b = __ffs(m) - 1;
                 m &= m - 1;
                 tb = tb + f.ws.vbm[(size_t)t * FT_TPB + k * 32 + b];
             }
         }
         acc = acc + tb;
-        amx = fmax(amx, f.ws.tile_maxd[t]);
-        const int2 cs = f.ws.tile_cs[t];
-        acnt += cs.x;
-        askel += cs.y;
     }
     acc = warp_sum(acc);
     acnt = warp_sum(acnt);
@@ -1390,7 +1340,8 @@ __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizePara
     else if (ctl->overflow) status = FT_STATUS_OVERFLOW;
     const int stepno = ctl->steps_done + 1;
     st.step = stepno;
-    st.needed = (long long)f.ws.num_tiles * FT_SLOT + (long long)ctl->pool_next;
+    st.needed = (long long)ctl->pool_next;
+    if (ctl->conv_next > st.needed) st.needed = ctl->conv_next;
     if (st.needed < f.tiled_cap) st.needed = f.tiled_cap;
     bool converged = false;
     if (status == FT_STATUS_OK && f.evolve)
@@ -1404,6 +1355,7 @@ __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizePara
     ctl->skel_total = 0ULL;
     ctl->nnz_total = 0ULL;
     ctl->pool_next = 0ULL;
+    ctl->conv_next = 0;
     ctl->nan_key = 0u;
     ctl->overflow = 0;
     ctl->slow_count = 0;
@@ -1424,13 +1376,79 @@ __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizePara
 }
 
 // ---------------------------------------------------------------------------
-// compaction: tiled -> canonical CSC
+// canonical CSC -> hybrid layout
+
+template <typename T>
+__global__ void __launch_bounds__(256) convert_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
+                                                      const T* __restrict__ val, int n, HybOut o, long long cap,
+                                                      Control* ctl) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool active = j < n;
+    int c0 = 0, cnt = 0;
+    if (active) {
+        c0 = __ldg(&ptr[j]);
+        cnt = __ldg(&ptr[j + 1]) - c0;
+    }
+    const int need = cnt > 2 ? cnt : 0;
+    int incl = need;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, s);
+        if (lane >= s) incl += y;
+    }
+    const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+    long long base = 0;
+    if (lane == 31 && wtot > 0) base = (long long)atomicAdd((unsigned long long*)&ctl->conv_next, (unsigned long long)wtot);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    const bool fits = base + wtot <= cap;
+    if (lane == 31 && !fits) atomicExch(&ctl->overflow, 1);
+    if (!active) return;
+    bool nf = false;
+    if (cnt == 0) {
+        o.sig[j] = FT_SIG_EMPTY;
+    } else if (cnt <= 2) {
+        const T x0 = val[c0];
+        ((T*)o.v0)[j] = x0;
+        nf |= !isfinite((double)x0);
+        if (cnt == 1) {
+            o.sig[j] = idx[c0];
+        } else {
+            const T x1 = val[c0 + 1];
+            o.sig[j] = idx[c0] | kPair;
+            o.aux[j] = idx[c0 + 1];
+            ((T*)o.v1)[j] = x1;
+            nf |= !isfinite((double)x1);
+        }
+    } else if (fits) {
+        const long long off = base + incl - need;
+        o.sig[j] = -cnt;
+        o.aux[j] = (int)off;
+        for (int t = 0; t < cnt; ++t) {
+            o.pidx[off + t] = idx[c0 + t];
+            const T x = val[c0 + t];
+            ((T*)o.pval)[off + t] = x;
+            nf |= !isfinite((double)x);
+        }
+    } else {
+        o.sig[j] = FT_SIG_EMPTY;   // the step that follows reports the overflow
+    }
+    if (nf) atomicOr(&ctl->nonfinite, 1u);
+}
+
+__global__ void convert_report_kernel(Control* ctl, ft_step_stats* st, long long cap) {
+    st->status = ctl->overflow ? FT_STATUS_OVERFLOW : FT_STATUS_OK;
+    st->needed = ctl->conv_next > cap ? ctl->conv_next : cap;
+    ctl->overflow = 0;
+    ctl->conv_next = 0;
+}
+
+// ---------------------------------------------------------------------------
+// compaction: hybrid -> canonical CSC
 
 struct CompactParams {
     int n_v;
-    const int2* desc[2];
-    const int* idx[2];
-    const void* val[2];
+    HybIn src[2];
     int sel;               // 0/1: source buffer; -1: pick by evolve parity
     int* out_ptr;
     int* out_idx;
@@ -1455,12 +1473,12 @@ __global__ void __launch_bounds__(FT_CTPB) compact_count_kernel(const CompactPar
     __shared__ int s_scan[FT_CTPB / 32];
     const int src = compact_source(c);
     if (src < 0) return;
-    const int2* desc = c.desc[src];
+    const int* sig = c.src[src].sig;
     const int j0 = blockIdx.x * FT_CCH + threadIdx.x * kCPT;
     int sum = 0;
 #pragma unroll
     for (int k = 0; k < kCPT; ++k)
-        if (j0 + k < c.n_v) sum += __ldg(&desc[j0 + k]).y;
+        if (j0 + k < c.n_v) sum += sig_count(__ldg(&sig[j0 + k]));
     int tot;
     block_excl_scan<FT_CTPB>(sum, s_scan, &tot);
     if (threadIdx.x == 0) c.ws.chunk_off[blockIdx.x] = tot;
@@ -1523,17 +1541,15 @@ __global__ void __launch_bounds__(FT_CTPB) compact_copy_kernel(const CompactPara
     const int src = compact_source(c);
     if (src < 0) return;
     if (c.ws.chunk_off[c.ws.num_chunks + 1] == 0) return;  // does not fit
-    const int2* desc = c.desc[src];
-    const int* sidx = c.idx[src];
-    const T* sval = (const T*)c.val[src];
+    const HybIn h = c.src[src];
     T* oval = (T*)c.out_val;
     const int j0 = blockIdx.x * FT_CCH + threadIdx.x * kCPT;
-    int2 d[kCPT];
+    int sg[kCPT];
     int sum = 0;
 #pragma unroll
     for (int k = 0; k < kCPT; ++k) {
-        d[k] = (j0 + k < c.n_v) ? __ldg(&desc[j0 + k]) : make_int2(0, 0);
-        sum += d[k].y;
+        sg[k] = (j0 + k < c.n_v) ? __ldg(&h.sig[j0 + k]) : FT_SIG_EMPTY;
+        sum += sig_count(sg[k]);
     }
     int tot;
     const int pre = block_excl_scan<FT_CTPB>(sum, s_scan, &tot);
@@ -1541,18 +1557,21 @@ __global__ void __launch_bounds__(FT_CTPB) compact_copy_kernel(const CompactPara
 #pragma unroll
     for (int k = 0; k < kCPT; ++k) {
         if (j0 + k < c.n_v) {
-            c.out_ptr[j0 + k] = (int)o;
-            for (int t = 0; t < d[k].y; ++t) {
-                c.out_idx[o + t] = __ldg(&sidx[d[k].x + t]);
-                oval[o + t] = __ldg(&sval[d[k].x + t]);
+            const int u = j0 + k;
+            c.out_ptr[u] = (int)o;
+            const int cnt = sig_count(sg[k]);
+            const int a = cnt >= 2 ? __ldg(&h.aux[u]) : 0;
+            for (int t = 0; t < cnt; ++t) {
+                c.out_idx[o + t] = hyb_row<T>(h, sg[k], a, t);
+                oval[o + t] = (T)hyb_val<T>(h, u, sg[k], a, t);
             }
-            o += d[k].y;
+            o += cnt;
         }
     }
 }
 
 __global__ void evolve_reset_kernel(Control* ctl) {
-    ctl->nonfinite = 0u;    // step 0 reads the canonical input with full checks
+    ctl->nonfinite = 0u;    // ft_tiled_from_csc raises it again for non-finite input
     ctl->done = 0;
     ctl->steps_done = 0;
     ctl->status = FT_STATUS_OK;
@@ -1565,62 +1584,20 @@ __global__ void evolve_report_kernel(const Control* ctl, long long* control) {
     control[2] = ctl->needed;
 }
 
+__global__ void nonfinite_reset_kernel(Control* ctl) { ctl->nonfinite = 0u; }
+
 // ---------------------------------------------------------------------------
 // host side
 
 typedef void (*StepKernelFn)(const StepParams);
 
-static StepKernelFn pick_step_v6(int dtype, bool uniform, bool in_canon, bool packed) {
-    if (dtype == FT_F64) {
-        if (uniform && packed) return in_canon ? step_kernel6<double, true, true, true> : step_kernel6<double, true, false, true>;
-        if (uniform) return in_canon ? step_kernel6<double, true, true, false> : step_kernel6<double, true, false, false>;
-        return in_canon ? step_kernel6<double, false, true, false> : step_kernel6<double, false, false, false>;
-    }
-    if (uniform && packed) return in_canon ? step_kernel6<float, true, true, true> : step_kernel6<float, true, false, true>;
-    if (uniform) return in_canon ? step_kernel6<float, true, true, false> : step_kernel6<float, true, false, false>;
-    return in_canon ? step_kernel6<float, false, true, false> : step_kernel6<float, false, false, false>;
-}
-
-static StepKernelFn pick_gen(int dtype, bool uniform, bool in_canon, bool packed) {
-    if (dtype == FT_F64) {
-        if (uniform && packed) return in_canon ? gen_kernel<double, true, true, true> : gen_kernel<double, true, false, true>;
-        if (uniform) return in_canon ? gen_kernel<double, true, true, false> : gen_kernel<double, true, false, false>;
-        return in_canon ? gen_kernel<double, false, true, false> : gen_kernel<double, false, false, false>;
-    }
-    if (uniform && packed) return in_canon ? gen_kernel<float, true, true, true> : gen_kernel<float, true, false, true>;
-    if (uniform) return in_canon ? gen_kernel<float, true, true, false> : gen_kernel<float, true, false, false>;
-    return in_canon ? gen_kernel<float, false, true, false> : gen_kernel<float, false, false, false>;
-}
-
-
-static StepKernelFn pick_deep(int dtype, bool uniform, bool in_canon) {
-    if (dtype == FT_F64) {
-        if (uniform) return in_canon ? deep_kernel<double, true, true> : deep_kernel<double, true, false>;
-        return in_canon ? deep_kernel<double, false, true> : deep_kernel<double, false, false>;
-    }
-    if (uniform) return in_canon ? deep_kernel<float, true, true> : deep_kernel<float, true, false>;
-    return in_canon ? deep_kernel<float, false, true> : deep_kernel<float, false, false>;
-}
-
-static StepKernelFn pick_wide3(int dtype, bool uniform, bool in_canon, bool packed) {
-    if (dtype == FT_F64) {
-        if (uniform && packed) return in_canon ? wide3_kernel<double, true, true, true> : wide3_kernel<double, true, false, true>;
-        if (uniform) return in_canon ? wide3_kernel<double, true, true, false> : wide3_kernel<double, true, false, false>;
-        return in_canon ? wide3_kernel<double, false, true, false> : wide3_kernel<double, false, false, false>;
-    }
-    if (uniform && packed) return in_canon ? wide3_kernel<float, true, true, true> : wide3_kernel<float, true, false, true>;
-    if (uniform) return in_canon ? wide3_kernel<float, true, true, false> : wide3_kernel<float, true, false, false>;
-    return in_canon ? wide3_kernel<float, false, true, false> : wide3_kernel<float, false, false, false>;
-}
-
-static StepKernelFn pick_wide(int dtype, bool uniform, bool in_canon) {
-    if (dtype == FT_F64) {
-        if (uniform) return in_canon ? wide_kernel<double, true, true> : wide_kernel<double, true, false>;
-        return in_canon ? wide_kernel<double, false, true> : wide_kernel<double, false, false>;
-    }
-    if (uniform) return in_canon ? wide_kernel<float, true, true> : wide_kernel<float, true, false>;
-    return in_canon ? wide_kernel<float, false, true> : wide_kernel<float, false, false>;
-}
+#define FT_PICK3(K, dtype, uni, packed)                                               \
+    ((dtype) == FT_F64 ? ((uni) ? ((packed) ? K<double, true, true> : K<double, true, false>) \
+                                : K<double, false, false>)                             \
+                       : ((uni) ? ((packed) ? K<float, true, true> : K<float, true, false>)   \
+                                : K<float, false, false>))
+#define FT_PICK2(K, dtype, uni)                                                              \
+    ((dtype) == FT_F64 ? ((uni) ? K<double, true> : K<double, false>) : ((uni) ? K<float, true> : K<float, false>))
 
 }  // namespace ft
 
@@ -1656,66 +1633,61 @@ extern "C" int ft_workspace_init(void* workspace, size_t bytes, void* stream) {
     return cuda_check("ft_workspace_init");
 }
 
-extern "C" int64_t ft_tile_slot_entries(void) { return FT_SLOT; }
+extern "C" int64_t ft_tile_slot_entries(void) { return 0; }
 
 extern "C" int64_t ft_tiled_min_capacity(int32_t n_vertices) {
-    return (int64_t)ft::num_tiles_for(n_vertices < 0 ? 0 : n_vertices) * FT_SLOT;
+    (void)n_vertices;
+    return 0;
 }
 
-static int check_tiled(const ft_tiled* t, int n_rows, int n_cols, int n_own) {
-    if (!t || !t->desc || !t->row_idx || !t->values || !t->sig) return set_err(FT_ERR_ARG, "null tiled buffer");
-    if (t->n_rows != n_rows || t->n_cols != n_cols) return set_err(FT_ERR_SHAPE, "tiled buffer has wrong shape");
-    if (t->capacity < ft_tiled_min_capacity(n_own) || t->capacity > (int64_t)INT_MAX)
-        return set_err(FT_ERR_ARG, "tiled capacity out of range");
-    if (((uintptr_t)t->desc) & 7) return set_err(FT_ERR_ARG, "tiled desc must be 8-byte aligned");
+static int check_tiled(const ft_tiled* t, int n_rows, int n_cols) {
+    if (!t || !t->sig || !t->aux || !t->v0 || !t->v1) return set_err(FT_ERR_ARG, "null hybrid buffer");
+    if (t->capacity < 0 || t->capacity > (int64_t)INT_MAX) return set_err(FT_ERR_ARG, "pool capacity out of range");
+    if (t->capacity > 0 && (!t->pool_idx || !t->pool_val)) return set_err(FT_ERR_ARG, "null pool");
+    if (t->n_rows != n_rows || t->n_cols != n_cols) return set_err(FT_ERR_SHAPE, "hybrid buffer has wrong shape");
     return FT_OK;
 }
 
-static int g_window = 0;
+static int g_init = 0;
 static int g_fixup_grid = 4 * 148;
 static int g_fin_ctas = 4 * 148;   // finalize: ~one tile per thread at C3, <= FT_FIN_MAX
 
-static int window_size() {
-    if (g_window == 0) {
-        double h[33];
-        h[0] = 0.0;
-        for (int n = 1; n <= 32; ++n) h[n] = 1.0 / (double)n;
-        cudaMemcpyToSymbol(ft::c_recip, h, sizeof(h));
-        g_window = 2;
-        int dev = 0, sms = 148;
-        if (cudaGetDevice(&dev) == cudaSuccess &&
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
-            g_fixup_grid = 4 * sms;
-        g_fin_ctas = 4 * sms < FT_FIN_MAX ? 4 * sms : FT_FIN_MAX;
-    }
-    return g_window;
+static void lib_init() {
+    if (g_init) return;
+    double h[33];
+    h[0] = 0.0;
+    for (int n = 1; n <= 32; ++n) h[n] = 1.0 / (double)n;
+    cudaMemcpyToSymbol(ft::c_recip, h, sizeof(h));
+    g_init = 1;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+        g_fixup_grid = 4 * sms;
+    g_fin_ctas = 4 * sms < FT_FIN_MAX ? 4 * sms : FT_FIN_MAX;
 }
 
-// which = 1: fused kernel, 2: fixup kernel, 3: both
+// which = 1: tier 1, 2: tiers 1.5-3, 3: both
 // dom == nullptr: the whole field; otherwise the owned column range of a
 // partitioned field (lap_t then holds the owned columns of L^T only and the
 // workspace is sized for the owned columns)
-static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_canon,
-                       const ft_tiled* in_tiled, ft_tiled* out, int32_t dtype,
-                       const ft_params* prm, void* workspace, size_t ws_bytes, int check_done,
+static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* in, ft_tiled* out,
+                       int32_t dtype, const ft_params* prm, void* workspace, size_t ws_bytes, int check_done,
                        cudaStream_t s, int which = 3, const ft_domain* dom = nullptr) {
-    if (!lap_t || !out || !prm || !workspace) return set_err(FT_ERR_ARG, "null argument");
+    if (!lap_t || !out || !in || !prm || !workspace) return set_err(FT_ERR_ARG, "null argument");
     if (dtype != FT_F64 && dtype != FT_F32) return set_err(FT_ERR_ARG, "bad dtype");
-    const int n_rows = in_canon ? in_canon->n_rows : (in_tiled ? in_tiled->n_rows : -1);
-    const int n_v = in_canon ? in_canon->n_cols : (in_tiled ? in_tiled->n_cols : -1);
-    if (n_v < 0) return set_err(FT_ERR_ARG, "no input");
-    if (n_v == 0) return set_err(FT_ERR_SHAPE, "empty field");
+    const int n_rows = in->n_rows, n_v = in->n_cols;
+    if (n_v <= 0) return set_err(FT_ERR_SHAPE, "empty field");
     const int j_base = dom ? dom->col_begin : 0;
     const int n_own = dom ? dom->col_count : n_v;
     if (dom && (j_base < 0 || n_own < 1 || (long long)j_base + n_own > n_v))
         return set_err(FT_ERR_SHAPE, "domain outside the field");
     if (lap_t->n_rows != n_v || lap_t->n_cols != n_own)
         return set_err(FT_ERR_SHAPE, "Laplacian size does not match field");
-    int rc = check_tiled(out, n_rows, n_v, dom ? n_own : n_v);
+    int rc = check_tiled(in, n_rows, n_v);
+    if (rc == FT_OK) rc = check_tiled(out, n_rows, n_v);
     if (rc != FT_OK) return rc;
     const long long step_cap = dom ? dom->step_capacity : out->capacity;
-    if (step_cap < ft_tiled_min_capacity(n_own) || step_cap > out->capacity)
-        return set_err(FT_ERR_ARG, "domain step capacity out of range");
+    if (step_cap < 0 || step_cap > out->capacity) return set_err(FT_ERR_ARG, "domain step capacity out of range");
     if (ws_bytes < ft::workspace_bytes(n_own)) return set_err(FT_ERR_ARG, "workspace too small");
     ft::StepParams p;
     p.n_v = n_own;
@@ -1724,16 +1696,8 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_
     p.lap_ptr = lap_t->col_ptr;
     p.lap_idx = lap_t->row_idx;
     p.lap_val = lap_t->values;
-    p.in_ptr = in_canon ? in_canon->col_ptr : nullptr;
-    p.in_desc = in_canon ? nullptr : (const int2*)in_tiled->desc;
-    p.in_idx = in_canon ? in_canon->row_idx : in_tiled->row_idx;
-    p.in_val = in_canon ? in_canon->values : in_tiled->values;
-    p.in_sig = in_canon ? nullptr : in_tiled->sig;
-    if (!in_canon && !in_tiled->sig) return set_err(FT_ERR_ARG, "null tiled buffer");
-    p.out_desc = (int2*)out->desc;
-    p.out_idx = out->row_idx;
-    p.out_val = out->values;
-    p.out_sig = out->sig;
+    p.in = ft::hyb_in(in);
+    p.out = ft::hyb_out(out);
     p.cap = step_cap;
     p.w = prm->w; p.a = prm->a; p.e = prm->e; p.eb = prm->e_base; p.mu = prm->mu; p.dt = prm->dt;
     p.ws = ft::carve_workspace(workspace, n_own);
@@ -1743,18 +1707,16 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_
     const bool uni = (lap_flags & FT_LAP_UNIFORM) != 0;
     const bool packed = uni && (lap_flags & FT_LAP_PACKED) != 0;
     p.lap_pack = packed ? (const int4*)lap_t->values : nullptr;
-    const bool ic = in_canon != nullptr;
-    window_size();
+    lib_init();
     p.force_check = (lap_flags & FT_LAP_CHECK_FINITE) != 0;
     p.report_ids = dom ? dom->report_ids : nullptr;
-    const ft::StepKernelFn k = ft::pick_step_v6(dtype, uni, ic, packed);
-    if (which & 1) k<<<p.num_tiles, FT_TPB, 0, s>>>(p);
+    if (which & 1) FT_PICK3(ft::tier1_kernel, dtype, uni, packed)<<<p.num_tiles, FT_TPB, 0, s>>>(p);
     if (which & 2) {
         // tier 1.5, one warp per tile
-        ft::pick_gen(dtype, uni, ic, packed)<<<(p.num_tiles + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
-        ft::pick_wide3(dtype, uni, ic, packed)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
-        ft::pick_wide(dtype, uni, ic)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
-        ft::pick_deep(dtype, uni, ic)<<<g_fixup_grid / 4, FT_TPB, 0, s>>>(p);
+        FT_PICK3(ft::gen_kernel, dtype, uni, packed)<<<(p.num_tiles + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
+        FT_PICK3(ft::wide3_kernel, dtype, uni, packed)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
+        FT_PICK2(ft::wide_kernel, dtype, uni)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
+        FT_PICK2(ft::deep_kernel, dtype, uni)<<<g_fixup_grid / 4, FT_TPB, 0, s>>>(p);
     }
     return cuda_check("step kernel");
 }
@@ -1764,8 +1726,26 @@ static void launch_finalize(const ft::Workspace& ws, ft_step_stats* trace, long 
     ft::FinalizeParams f;
     f.ws = ws; f.trace = trace; f.tiled_cap = tiled_cap; f.fixed_slot = evolve ? 0 : 1;
     f.evolve = evolve; f.max_steps = max_steps; f.tol = tol; f.base_threshold = thr;
-    window_size();
+    lib_init();
     ft::finalize_kernel<<<g_fin_ctas, FT_FIN_TPB, 0, s>>>(f);
+}
+
+static int launch_convert(const ft_csc* src, ft_tiled* dst, int32_t dtype, const ft::Workspace& ws,
+                          cudaStream_t s) {
+    if (!src || !src->col_ptr || (!src->row_idx && src->capacity > 0)) return set_err(FT_ERR_ARG, "null argument");
+    if (dtype != FT_F64 && dtype != FT_F32) return set_err(FT_ERR_ARG, "bad dtype");
+    int rc = check_tiled(dst, src->n_rows, src->n_cols);
+    if (rc != FT_OK) return rc;
+    const int n = src->n_cols;
+    if (n <= 0) return set_err(FT_ERR_SHAPE, "empty field");
+    const int grid = (n + 255) / 256;
+    if (dtype == FT_F64)
+        ft::convert_kernel<double><<<grid, 256, 0, s>>>(src->col_ptr, src->row_idx, (const double*)src->values, n,
+                                                       ft::hyb_out(dst), dst->capacity, ws.ctl);
+    else
+        ft::convert_kernel<float><<<grid, 256, 0, s>>>(src->col_ptr, src->row_idx, (const float*)src->values, n,
+                                                      ft::hyb_out(dst), dst->capacity, ws.ctl);
+    return cuda_check("ft_tiled_from_csc");
 }
 
 static int launch_compact(ft::CompactParams& c, int dtype, cudaStream_t s) {
@@ -1777,20 +1757,28 @@ static int launch_compact(ft::CompactParams& c, int dtype, cudaStream_t s) {
     return cuda_check("compact");
 }
 
-extern "C" int ft_step_kernel(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_canon,
-                              const ft_tiled* in_tiled, ft_tiled* out, int32_t dtype,
-                              const ft_params* params, void* workspace, size_t ws_bytes,
-                              void* stream) {
-    return launch_step(lap_t, lap_flags, in_canon, in_tiled, out, dtype, params, workspace, ws_bytes,
-                       0, (cudaStream_t)stream, 1);
+extern "C" int ft_tiled_from_csc(const ft_csc* src, ft_tiled* dst, int32_t dtype, void* workspace,
+                                 size_t ws_bytes, ft_step_stats* stats, void* stream) {
+    if (!src || !dst || !workspace || !stats) return set_err(FT_ERR_ARG, "null argument");
+    if (ws_bytes < ft::workspace_bytes(src->n_cols)) return set_err(FT_ERR_ARG, "workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    const ft::Workspace ws = ft::carve_workspace(workspace, src->n_cols);
+    const int rc = launch_convert(src, dst, dtype, ws, s);
+    if (rc != FT_OK) return rc;
+    ft::convert_report_kernel<<<1, 1, 0, s>>>(ws.ctl, stats, dst->capacity);
+    return cuda_check("ft_tiled_from_csc");
 }
 
-extern "C" int ft_step_fixup(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* in_canon,
-                             const ft_tiled* in_tiled, ft_tiled* out, int32_t dtype,
-                             const ft_params* params, void* workspace, size_t ws_bytes,
+extern "C" int ft_step_kernel(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* in, ft_tiled* out,
+                              int32_t dtype, const ft_params* params, void* workspace, size_t ws_bytes,
+                              void* stream) {
+    return launch_step(lap_t, lap_flags, in, out, dtype, params, workspace, ws_bytes, 0, (cudaStream_t)stream, 1);
+}
+
+extern "C" int ft_step_fixup(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* in, ft_tiled* out,
+                             int32_t dtype, const ft_params* params, void* workspace, size_t ws_bytes,
                              void* stream) {
-    return launch_step(lap_t, lap_flags, in_canon, in_tiled, out, dtype, params, workspace, ws_bytes,
-                       0, (cudaStream_t)stream, 2);
+    return launch_step(lap_t, lap_flags, in, out, dtype, params, workspace, ws_bytes, 0, (cudaStream_t)stream, 2);
 }
 
 extern "C" int ft_step_finalize(void* workspace, size_t ws_bytes, int32_t n_vertices,
@@ -1802,12 +1790,11 @@ extern "C" int ft_step_finalize(void* workspace, size_t ws_bytes, int32_t n_vert
     return cuda_check("ft_step_finalize");
 }
 
-static void fill_compact(ft::CompactParams& c, const ft_tiled* a, const ft_tiled* b, int sel,
-                         ft_csc* dst, void* workspace) {
+static void fill_compact(ft::CompactParams& c, const ft_tiled* a, const ft_tiled* b, int sel, ft_csc* dst,
+                         void* workspace) {
     c.n_v = dst->n_cols;
-    c.desc[0] = (const int2*)a->desc; c.idx[0] = a->row_idx; c.val[0] = a->values;
-    const ft_tiled* bb = b ? b : a;
-    c.desc[1] = (const int2*)bb->desc; c.idx[1] = bb->row_idx; c.val[1] = bb->values;
+    c.src[0] = ft::hyb_in(a);
+    c.src[1] = ft::hyb_in(b ? b : a);
     c.sel = sel;
     c.out_ptr = dst->col_ptr; c.out_idx = dst->row_idx; c.out_val = dst->values; c.cap = dst->capacity;
     c.ws = ft::carve_workspace(workspace, dst->n_cols);
@@ -1816,8 +1803,8 @@ static void fill_compact(ft::CompactParams& c, const ft_tiled* a, const ft_tiled
     c.check_status = 0;
 }
 
-extern "C" int ft_compact(const ft_tiled* src, ft_csc* dst, int32_t dtype, void* workspace,
-                          size_t ws_bytes, ft_step_stats* stats, void* stream) {
+extern "C" int ft_compact(const ft_tiled* src, ft_csc* dst, int32_t dtype, void* workspace, size_t ws_bytes,
+                          ft_step_stats* stats, void* stream) {
     if (!src || !dst || !workspace || !stats) return set_err(FT_ERR_ARG, "null argument");
     if (src->n_cols != dst->n_cols || src->n_rows != dst->n_rows) return set_err(FT_ERR_SHAPE, "shape mismatch");
     if (ws_bytes < ft::workspace_bytes(dst->n_cols)) return set_err(FT_ERR_ARG, "workspace too small");
@@ -1828,20 +1815,25 @@ extern "C" int ft_compact(const ft_tiled* src, ft_csc* dst, int32_t dtype, void*
     return launch_compact(c, dtype, (cudaStream_t)stream);
 }
 
-extern "C" int ft_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
-                       ft_tiled* scratch, ft_csc* phi_out, int32_t dtype, const ft_params* params,
+extern "C" int ft_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in, ft_tiled* scratch_in,
+                       ft_tiled* scratch_out, ft_csc* phi_out, int32_t dtype, const ft_params* params,
                        void* workspace, size_t ws_bytes, ft_step_stats* stats, void* stream) {
-    if (!phi_in || !phi_out || !stats || !scratch) return set_err(FT_ERR_ARG, "null argument");
+    if (!phi_in || !phi_out || !stats || !scratch_in || !scratch_out) return set_err(FT_ERR_ARG, "null argument");
     if (phi_out->n_cols != phi_in->n_cols || phi_out->n_rows != phi_in->n_rows)
         return set_err(FT_ERR_SHAPE, "output buffer has wrong shape");
+    if (ws_bytes < ft::workspace_bytes(phi_in->n_cols)) return set_err(FT_ERR_ARG, "workspace too small");
     cudaStream_t s = (cudaStream_t)stream;
-    int rc = launch_step(lap_t, lap_flags, phi_in, nullptr, scratch, dtype, params, workspace, ws_bytes, 0, s);
-    if (rc != FT_OK) return rc;
     ft::Workspace ws = ft::carve_workspace(workspace, phi_in->n_cols);
-    launch_finalize(ws, stats, scratch->capacity, 0, 1, 0.0, 0.0, s);
+    ft::nonfinite_reset_kernel<<<1, 1, 0, s>>>(ws.ctl);
+    int rc = launch_convert(phi_in, scratch_in, dtype, ws, s);
+    if (rc != FT_OK) return rc;
+    rc = launch_step(lap_t, lap_flags, scratch_in, scratch_out, dtype, params, workspace, ws_bytes, 0, s);
+    if (rc != FT_OK) return rc;
+    const long long cap = scratch_out->capacity < scratch_in->capacity ? scratch_out->capacity : scratch_in->capacity;
+    launch_finalize(ws, stats, cap, 0, 1, 0.0, 0.0, s);
     // the compaction always runs; the host ignores it if the step failed
     ft::CompactParams c;
-    fill_compact(c, scratch, nullptr, 0, phi_out, workspace);
+    fill_compact(c, scratch_out, nullptr, 0, phi_out, workspace);
     c.stats = stats;
     c.check_status = 1;
     return launch_compact(c, dtype, s);
@@ -1855,7 +1847,7 @@ extern "C" int ft_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi
 constexpr int kGraphSteps = 16;
 
 struct GraphKey {
-    const void* ptrs[14];
+    const void* ptrs[18];
     long long caps[3];
     double prm[8];
     int ints[5];
@@ -1903,32 +1895,32 @@ static void graph_store(const GraphKey& k, cudaGraphExec_t exec) {
     e.used = true;
 }
 
-extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
-                         ft_tiled* work_a, ft_tiled* work_b, ft_csc* phi_out, int32_t dtype,
-                         const ft_params* params, int32_t max_steps, double tol,
-                         double base_threshold, void* workspace, size_t ws_bytes,
-                         ft_step_stats* trace, int64_t* control, void* stream) {
+extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in, ft_tiled* work_a,
+                         ft_tiled* work_b, ft_csc* phi_out, int32_t dtype, const ft_params* params,
+                         int32_t max_steps, double tol, double base_threshold, void* workspace,
+                         size_t ws_bytes, ft_step_stats* trace, int64_t* control, void* stream) {
     if (!phi_in || !phi_out || !work_a || !work_b || !trace || !control)
         return set_err(FT_ERR_ARG, "null argument");
     if (max_steps < 1) return set_err(FT_ERR_SHAPE, "max_steps must be >= 1");
     if (phi_out->n_cols != phi_in->n_cols || phi_out->n_rows != phi_in->n_rows)
         return set_err(FT_ERR_SHAPE, "output buffer has wrong shape");
-    int rc = check_tiled(work_b, phi_in->n_rows, phi_in->n_cols, phi_in->n_cols);
-    if (rc != FT_OK) return rc;
     if (ws_bytes < ft::workspace_bytes(phi_in->n_cols)) return set_err(FT_ERR_ARG, "workspace too small");
     cudaStream_t s = (cudaStream_t)stream;
     ft::Workspace ws = ft::carve_workspace(workspace, phi_in->n_cols);
     ft::evolve_reset_kernel<<<1, 1, 0, s>>>(ws.ctl);
-    // step 0: canonical input -> a
-    rc = launch_step(lap_t, lap_flags, phi_in, nullptr, work_a, dtype, params, workspace, ws_bytes, 1, s);
+    // canonical input -> b, step 1: b -> a
+    int rc = launch_convert(phi_in, work_b, dtype, ws, s);
     if (rc != FT_OK) return rc;
-    launch_finalize(ws, trace, work_a->capacity, 1, max_steps, tol, base_threshold, s);
+    rc = launch_step(lap_t, lap_flags, work_b, work_a, dtype, params, workspace, ws_bytes, 1, s);
+    if (rc != FT_OK) return rc;
+    const long long cap0 = work_a->capacity < work_b->capacity ? work_a->capacity : work_b->capacity;
+    launch_finalize(ws, trace, cap0, 1, max_steps, tol, base_threshold, s);
     const int rest = max_steps - 1;
     if (rest > 0 && rest < kGraphSteps) {
         for (int i = 1; i < max_steps; ++i) {
             ft_tiled* out = (i & 1) ? work_b : work_a;
             const ft_tiled* in_t = (i & 1) ? work_a : work_b;
-            rc = launch_step(lap_t, lap_flags, nullptr, in_t, out, dtype, params, workspace, ws_bytes, 1, s);
+            rc = launch_step(lap_t, lap_flags, in_t, out, dtype, params, workspace, ws_bytes, 1, s);
             if (rc != FT_OK) return rc;
             launch_finalize(ws, trace, out->capacity, 1, max_steps, tol, base_threshold, s);
         }
@@ -1937,9 +1929,10 @@ extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* p
         memset(&k, 0, sizeof(k));
         if (graph_stream_init() != FT_OK) return cuda_check("ft_evolve(graph stream)");
         cudaStream_t gs = g_gstream;
-        const void* ptrs[14] = {lap_t->col_ptr, lap_t->row_idx, lap_t->values, work_a->desc, work_a->row_idx,
-                                work_a->values, work_b->desc, work_b->row_idx, work_b->values, workspace,
-                                trace, work_a->sig, work_b->sig, nullptr};
+        const void* ptrs[18] = {lap_t->col_ptr, lap_t->row_idx, lap_t->values, work_a->sig, work_a->aux,
+                                work_a->v0, work_a->v1, work_a->pool_idx, work_a->pool_val, work_b->sig,
+                                work_b->aux, work_b->v0, work_b->v1, work_b->pool_idx, work_b->pool_val,
+                                workspace, trace, nullptr};
         memcpy(k.ptrs, ptrs, sizeof(ptrs));
         k.caps[0] = work_a->capacity; k.caps[1] = work_b->capacity; k.caps[2] = (long long)ws_bytes;
         const double prm[8] = {params->w, params->a, params->e, params->e_base, params->mu, params->dt, tol,
@@ -1955,14 +1948,12 @@ extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* p
             for (int i = 1; i <= kGraphSteps; ++i) {
                 ft_tiled* out = (i & 1) ? work_b : work_a;
                 const ft_tiled* in_t = (i & 1) ? work_a : work_b;
-                const int r2 = launch_step(lap_t, lap_flags, nullptr, in_t, out, dtype, params, workspace,
-                                           ws_bytes, 1, gs);
+                const int r2 = launch_step(lap_t, lap_flags, in_t, out, dtype, params, workspace, ws_bytes, 1, gs);
                 if (r2 != FT_OK) rc = r2;
                 launch_finalize(ws, trace, out->capacity, 1, max_steps, tol, base_threshold, gs);
             }
             const cudaError_t ec = cudaStreamEndCapture(gs, &graph);
-            if (ec != cudaSuccess || rc != FT_OK)
-                return rc != FT_OK ? rc : cuda_check("ft_evolve(end capture)");
+            if (ec != cudaSuccess || rc != FT_OK) return rc != FT_OK ? rc : cuda_check("ft_evolve(end capture)");
             if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
                 cudaGraphDestroy(graph);
                 return cuda_check("ft_evolve(instantiate)");
@@ -1987,17 +1978,14 @@ extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* p
 // partitioned field: one step of the owned columns (the halo kernels and the
 // combine live in ft_domain.cu)
 
-extern "C" int ft_domain_step(const ft_csc* lap_rows, int32_t lap_flags, const ft_tiled* in,
-                              ft_tiled* out, int32_t dtype, const ft_params* params,
-                              const ft_domain* dom, void* workspace, size_t ws_bytes,
-                              ft_step_stats* record, void* stream) {
+extern "C" int ft_domain_step(const ft_csc* lap_rows, int32_t lap_flags, const ft_tiled* in, ft_tiled* out,
+                              int32_t dtype, const ft_params* params, const ft_domain* dom, void* workspace,
+                              size_t ws_bytes, ft_step_stats* record, void* stream) {
     if (!in || !dom || !record) return set_err(FT_ERR_ARG, "null argument");
     cudaStream_t s = (cudaStream_t)stream;
-    const int rc = launch_step(lap_rows, lap_flags, nullptr, in, out, dtype, params, workspace, ws_bytes, 1, s,
-                               3, dom);
+    const int rc = launch_step(lap_rows, lap_flags, in, out, dtype, params, workspace, ws_bytes, 1, s, 3, dom);
     if (rc != FT_OK) return rc;
-    launch_finalize(ft::carve_workspace(workspace, dom->col_count), record, dom->step_capacity, 0, 1, 0.0, 0.0,
-                    s);
+    launch_finalize(ft::carve_workspace(workspace, dom->col_count), record, dom->step_capacity, 0, 1, 0.0, 0.0, s);
     return cuda_check("ft_domain_step");
 }
 

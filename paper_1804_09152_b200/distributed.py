@@ -36,7 +36,7 @@ from .errors import BackendError, ShapeError
 from .field import (BASE_EXHAUSTION_PER_VERTEX, POOL_FRACTION, POOL_MIN, StepStats, _check,
                     _ft_dtype, _raise_step_error, _stats_from_bytes, _stream_handle,
                     _value_dtype)
-from .sparse import INDEX, GROWTH, DeviceCSC, DeviceTiled, SparseMat
+from .sparse import INDEX, GROWTH, DeviceCSC, DeviceTiled, SparseMat, hybrid_columns
 
 DEFAULT_SLOTS = 7      # halo message entries per column (grows on demand)
 
@@ -460,7 +460,7 @@ class DomainRank:
         self.n_halo = off
         own_mask = (problem.cols >= self.col_begin) & (problem.cols < e)
         own_nnz = int(np.sum(np.diff(problem.col_ptr)[own_mask]))
-        self.step_cap = int(self.lib.ft_tiled_min_capacity(self.n_own)) + max(
+        self.step_cap = int(self.lib.ft_tiled_min_capacity(self.n_v)) + max(
             int(own_nnz * POOL_FRACTION), POOL_MIN)
         self.slots = int(slots)
         self.bufs = [None, None]
@@ -494,32 +494,27 @@ class DomainRank:
                 capacity = max(capacity, int(old.capacity * GROWTH))
             buf = DeviceTiled(self.n_rows, self.n_v, capacity, self.vdtype, self.device)
             if old is not None:
-                buf.desc.copy_(old.desc)
-                buf.sig.copy_(old.sig)
-                buf.row_idx[:old.capacity].copy_(old.row_idx)
-                buf.values[:old.capacity].copy_(old.values)
+                for name in ("sig", "aux", "v0", "v1"):
+                    getattr(buf, name).copy_(getattr(old, name))
+                buf.pool_idx[:old.capacity].copy_(old.pool_idx)
+                buf.pool_val[:old.capacity].copy_(old.pool_val)
             self.bufs[k] = buf
         return buf
 
     def _upload(self, problem):
         torch = _torch()
-        nnz = int(problem.col_ptr[-1])
-        buf = self._buffer(0, max(self._need_capacity(), nnz, 1))
+        sig, aux, v0, v1, pidx, pval = hybrid_columns(problem.col_ptr, problem.row_idx,
+                                                      problem.values.astype(np.float64))
+        buf = self._buffer(0, max(self._need_capacity(), pidx.size, 1))
         cols = torch.from_numpy(problem.cols).to(self.device)
-        desc = buf.desc.view(-1, 2)
-        starts = torch.from_numpy(problem.col_ptr[:-1].astype(np.int32)).to(self.device)
-        counts = torch.from_numpy(np.diff(problem.col_ptr).astype(np.int32)).to(self.device)
-        desc[cols, 0] = starts
-        desc[cols, 1] = counts
-        # row signatures (tier-1 classification): row of a single entry, -1 more, -2 none
-        cnt_h = np.diff(problem.col_ptr)
-        first = problem.row_idx[np.minimum(problem.col_ptr[:-1], max(nnz - 1, 0))] if nnz else np.zeros(cnt_h.size)
-        sig = np.where(cnt_h == 1, first, np.where(cnt_h == 0, -2, -1)).astype(np.int32)
-        buf.sig[cols] = torch.from_numpy(sig).to(self.device)
-        if nnz:
-            buf.row_idx[:nnz].copy_(torch.from_numpy(problem.row_idx[:nnz]).to(self.device))
-            buf.values[:nnz].copy_(torch.from_numpy(problem.values[:nnz]).to(self.device,
-                                                                               self.vdtype))
+        dev = self.device
+        buf.sig[cols] = torch.from_numpy(sig).to(dev)
+        buf.aux[cols] = torch.from_numpy(aux).to(dev)
+        buf.v0[cols] = torch.from_numpy(v0).to(dev, self.vdtype)
+        buf.v1[cols] = torch.from_numpy(v1).to(dev, self.vdtype)
+        if pidx.size:
+            buf.pool_idx[:pidx.size].copy_(torch.from_numpy(pidx).to(dev))
+            buf.pool_val[:pidx.size].copy_(torch.from_numpy(pval).to(dev, self.vdtype))
         self.meta[0] = (buf.ft_tiled(), 0, self.slots)
         # values of unknown origin: the first step checks them unless finite
         self.first_check = not bool(np.all(np.isfinite(problem.values)))
@@ -638,13 +633,11 @@ class DomainRank:
         """The owned columns after ``steps_done`` steps as a DeviceCSC
         (n_rows x n_own), compacted from the tiled buffer."""
         torch = _torch()
-        tiled_t = self.meta[steps_done % 2][0]
         buf = self.bufs[steps_done % 2]
-        src = _lib.FtTiled(self.n_rows, self.n_own,
-                           buf.desc.data_ptr() + 8 * self.col_begin, buf.row_idx.data_ptr(),
-                           buf.values.data_ptr(), tiled_t.capacity)
-        cap = max(1, int(buf.desc.view(-1, 2)[self.col_begin:self.col_begin + self.n_own, 1]
-                         .sum().item()))
+        src = buf.ft_tiled(self.col_begin, self.n_own)
+        sg = buf.sig[self.col_begin:self.col_begin + self.n_own]
+        counts = torch.where(sg >= (1 << 30), 2, torch.where(sg >= 0, 1, torch.where(sg == -1, 0, -sg)))
+        cap = max(1, int(counts.sum().item()))
         out = DeviceCSC.allocate(self.n_rows, self.n_own, cap, self.vdtype, self.device)
         o_c = out.ft_csc()
         rec = torch.zeros(_lib.STATS_BYTES, dtype=torch.uint8, device=self.device)

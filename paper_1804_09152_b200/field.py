@@ -366,7 +366,7 @@ def device_laplacian(lap, precision):
     return dl
 
 
-POOL_FRACTION = 0.5     # overflow pool of a tiled buffer, relative to nnz
+POOL_FRACTION = 0.25    # pool of a hybrid buffer (columns with > 2 entries), relative to nnz
 PACK_LAPLACIAN = True   # uniform Laplacians: packed neighbour table for tier 1
 POOL_MIN = 4096
 
@@ -374,7 +374,7 @@ POOL_MIN = 4096
 class StepWorkspace:
     """Reusable device buffers for the step pipeline (field.py:169-189): the
     workspace (per-tile partial sums, compaction scan, control block), the
-    statistics record, two tiled work buffers and a spare canonical output.
+    statistics record, two hybrid work buffers and a spare canonical output.
     With a shared workspace the input field's storage is recycled as a later
     output, so only the newest field stays valid (as in the reference)."""
 
@@ -460,8 +460,9 @@ def _compact(tiled, out, precision, ws, stream):
 
 def step(field, lap, params, workspace=None):
     """One explicit Euler step; returns ``(new_field, StepStats)``
-    (field.py:198-286).  Runs the fused kernel into a tiled work buffer and
-    compacts the result into a canonical CSC (ft_step)."""
+    (field.py:198-286).  Converts the input into a hybrid work buffer, runs
+    the fused step kernels into a second one and compacts the result into a
+    canonical CSC (ft_step)."""
     torch = _torch()
     params.validate()
     ws = workspace if workspace is not None else StepWorkspace()
@@ -472,6 +473,7 @@ def step(field, lap, params, workspace=None):
     device = dphi.values.device
     dl = device_laplacian(lap, field.precision)
     ws.prepare(n_v, device)
+    scratch_in = ws.tiled_buffer("b", dphi, dphi.nnz)
     scratch = ws.tiled_buffer("a", dphi, dphi.nnz)
     out = ws.take_output(dphi, _initial_capacity(dphi))
     reallocs = ws.realloc_count
@@ -484,10 +486,10 @@ def step(field, lap, params, workspace=None):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     while True:
-        in_c, sc_c, out_c = dphi.ft_csc(), scratch.ft_tiled(), out.ft_csc()
+        in_c, si_c, sc_c, out_c = dphi.ft_csc(), scratch_in.ft_tiled(), scratch.ft_tiled(), out.ft_csc()
         ev0.record()
-        rc = lib.ft_step(ctypes.byref(lap_c), dl.launch_flags(), ctypes.byref(in_c), ctypes.byref(sc_c),
-                         ctypes.byref(out_c), _ft_dtype(field.precision), ctypes.byref(prm),
+        rc = lib.ft_step(ctypes.byref(lap_c), dl.launch_flags(), ctypes.byref(in_c), ctypes.byref(si_c),
+                         ctypes.byref(sc_c), ctypes.byref(out_c), _ft_dtype(field.precision), ctypes.byref(prm),
                          wp, wn, ctypes.c_void_p(ws.stats.data_ptr()), stream)
         ev1.record()
         _check(rc, "ft_step")
@@ -495,6 +497,7 @@ def step(field, lap, params, workspace=None):
         status = int(rec["status"])
         if status == _lib.FT_STATUS_OVERFLOW:
             scratch.grow(int(rec["needed"]) + int(rec["needed"]) // 5)
+            scratch_in.grow(int(rec["needed"]) + int(rec["needed"]) // 5)
             reallocs += 1
             continue
         if status == _lib.FT_STATUS_OUT_OVERFLOW:

@@ -301,36 +301,84 @@ class DeviceCSC:
 
 
 class DeviceTiled:
-    """Tiled working storage of a field on the GPU (``ft_tiled`` in
-    include/fieldtess_cuda.h): per-column (start, count) descriptors, entries
-    in per-tile slots plus an overflow pool.  Used between Euler steps."""
+    """Working storage of a field on the GPU between Euler steps (``ft_tiled``
+    in include/fieldtess_cuda.h), the hybrid layout: a column with at most
+    two entries in the dense per-column arrays ``sig`` (row signature),
+    ``aux`` (second row), ``v0`` / ``v1`` (values); a wider column in the
+    pool (``pool_idx`` / ``pool_val``, offset in ``aux``)."""
 
-    __slots__ = ("n_rows", "n_cols", "desc", "row_idx", "values", "sig")
+    __slots__ = ("n_rows", "n_cols", "sig", "aux", "v0", "v1", "pool_idx", "pool_val")
 
     def __init__(self, n_rows, n_cols, capacity, dtype, device):
         torch = _torch()
         self.n_rows = int(n_rows)
         self.n_cols = int(n_cols)
-        self.desc = torch.zeros(2 * max(n_cols, 1), dtype=torch.int32, device=device)
-        self.row_idx = torch.empty(int(capacity), dtype=torch.int32, device=device)
-        self.values = torch.empty(int(capacity), dtype=dtype, device=device)
-        # row signature per column (row of a single entry, -1 more, -2 none)
-        self.sig = torch.full((max(n_cols, 1),), -2, dtype=torch.int32, device=device)
+        n = max(self.n_cols, 1)
+        self.sig = torch.full((n,), -1, dtype=torch.int32, device=device)   # all columns empty
+        self.aux = torch.zeros(n, dtype=torch.int32, device=device)
+        self.v0 = torch.zeros(n, dtype=dtype, device=device)
+        self.v1 = torch.zeros(n, dtype=dtype, device=device)
+        cap = max(int(capacity), 1)
+        self.pool_idx = torch.empty(cap, dtype=torch.int32, device=device)
+        self.pool_val = torch.empty(cap, dtype=dtype, device=device)
 
     @property
     def capacity(self):
-        return int(self.row_idx.numel())
+        return int(self.pool_idx.numel())
 
-    def grow(self, needed):
+    @property
+    def values(self):
+        return self.v0
+
+    def grow(self, needed, keep=False):
+        """Pool of at least ``needed`` entries (>= GROWTH x); ``keep`` copies
+        the old pool (the dense arrays are never reallocated)."""
         torch = _torch()
         if self.capacity >= needed:
             return False
         new_cap = max(int(needed), int(math.ceil(self.capacity * GROWTH)))
-        self.row_idx = torch.empty(new_cap, dtype=torch.int32, device=self.row_idx.device)
-        self.values = torch.empty(new_cap, dtype=self.values.dtype, device=self.values.device)
+        old_i, old_v = self.pool_idx, self.pool_val
+        self.pool_idx = torch.empty(new_cap, dtype=torch.int32, device=old_i.device)
+        self.pool_val = torch.empty(new_cap, dtype=old_v.dtype, device=old_v.device)
+        if keep:
+            self.pool_idx[:old_i.numel()].copy_(old_i)
+            self.pool_val[:old_v.numel()].copy_(old_v)
         return True
 
-    def ft_tiled(self):
+    def ft_tiled(self, col_begin=0, n_cols=None):
+        """The ``ft_tiled`` struct, or a view of columns [col_begin,
+        col_begin + n_cols)."""
         from ._lib import FtTiled
-        return FtTiled(self.n_rows, self.n_cols, self.desc.data_ptr(), self.row_idx.data_ptr(),
-                       self.values.data_ptr(), self.capacity, self.sig.data_ptr())
+        n = self.n_cols if n_cols is None else int(n_cols)
+        vs = self.v0.element_size()
+        return FtTiled(self.n_rows, n, self.sig.data_ptr() + 4 * col_begin,
+                       self.aux.data_ptr() + 4 * col_begin, self.v0.data_ptr() + vs * col_begin,
+                       self.v1.data_ptr() + vs * col_begin, self.pool_idx.data_ptr(),
+                       self.pool_val.data_ptr(), self.capacity)
+
+
+def hybrid_columns(col_ptr, row_idx, values, pool_base=0):
+    """Host arrays of the hybrid layout for the CSC columns (col_ptr,
+    row_idx, values): (sig, aux, v0, v1, pool_idx, pool_val); wide columns
+    take consecutive pool entries from ``pool_base`` in column order."""
+    col_ptr = np.asarray(col_ptr, dtype=np.int64)
+    cnt = np.diff(col_ptr)
+    n = cnt.size
+    start = col_ptr[:-1]
+    nnz = int(col_ptr[-1]) if n else 0
+    first = np.minimum(start, max(nnz - 1, 0))
+    second = np.minimum(start + 1, max(nnz - 1, 0))
+    r0 = row_idx[first] if nnz else np.zeros(n, dtype=np.int32)
+    r1 = row_idx[second] if nnz else np.zeros(n, dtype=np.int32)
+    x0 = values[first] if nnz else np.zeros(n, dtype=values.dtype)
+    x1 = values[second] if nnz else np.zeros(n, dtype=values.dtype)
+    wide = cnt > 2
+    wcnt = np.where(wide, cnt, 0)
+    woff = pool_base + np.cumsum(wcnt) - wcnt
+    sig = np.where(cnt == 0, -1, np.where(cnt == 1, r0, np.where(cnt == 2, r0 | (1 << 30), -cnt)))
+    aux = np.where(cnt == 2, r1, np.where(wide, woff, 0))
+    sel = np.repeat(wide, cnt)
+    pidx = row_idx[:nnz][sel]
+    pval = values[:nnz][sel]
+    return (sig.astype(np.int32), aux.astype(np.int32), np.where(cnt >= 1, x0, 0).astype(values.dtype),
+            np.where(cnt == 2, x1, 0).astype(values.dtype), pidx.astype(np.int32), pval)

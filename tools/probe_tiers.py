@@ -1,7 +1,7 @@
 """Per-tier timing and tier populations of the C3 step in steady state.
 
 usage: python tools/probe_tiers.py [nx ny seeds warm]
-Times tier 1 (ft_step_kernel), tiers 2+3 (ft_step_fixup) and the finalize
+Times tier 1 (ft_step_kernel), tiers 1.5-3 (ft_step_fixup) and the finalize
 separately with CUDA events (on the launching stream) and reads the queue
 counts of the control block before the finalize resets them.
 """
@@ -28,7 +28,7 @@ cur, _ = ft.evolve(fld, lap, ft.CouplingParams(), max_steps=warm, tol=0.0)
 dphi = cur.device_phi()
 ws = ft.StepWorkspace()
 ws.prepare(n_v, dphi.values.device)
-cap = int(lib.ft_tiled_min_capacity(n_v)) + 2 * dphi.nnz
+cap = int(lib.ft_tiled_min_capacity(n_v)) + dphi.nnz
 ta = ft.DeviceTiled(dphi.n_rows, n_v, cap, dphi.values.dtype, dphi.values.device)
 tb = ft.DeviceTiled(dphi.n_rows, n_v, cap, dphi.values.dtype, dphi.values.device)
 dl = F.device_laplacian(lap, "exact")
@@ -39,18 +39,20 @@ st = F._stream_handle()
 wp, wn = ws.ws_args()
 src = dphi.ft_csc()
 rows = []
+tb_c = tb.ft_tiled()
+assert lib.ft_tiled_from_csc(ctypes.byref(src), ctypes.byref(tb_c), 0, wp, wn, ctypes.c_void_p(ws.stats.data_ptr()),
+                             st) == 0
 for i in range(41):
     out = ta if i % 2 == 0 else tb
     inp = tb if i % 2 == 0 else ta
     oc, ic = out.ft_tiled(), inp.ft_tiled()
-    canon = ctypes.byref(src) if i == 0 else None
-    tiled = None if i == 0 else ctypes.byref(ic)
+    tiled = ctypes.byref(ic)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     ev[0].record()
-    assert lib.ft_step_kernel(ctypes.byref(lc), fl, canon, tiled, ctypes.byref(oc), 0, ctypes.byref(prm), wp, wn,
+    assert lib.ft_step_kernel(ctypes.byref(lc), fl, tiled, ctypes.byref(oc), 0, ctypes.byref(prm), wp, wn,
                               st) == 0
     ev[1].record()
-    assert lib.ft_step_fixup(ctypes.byref(lc), fl, canon, tiled, ctypes.byref(oc), 0, ctypes.byref(prm), wp, wn,
+    assert lib.ft_step_fixup(ctypes.byref(lc), fl, tiled, ctypes.byref(oc), 0, ctypes.byref(prm), wp, wn,
                              st) == 0
     ev[2].record()
     torch.cuda.synchronize()
