@@ -377,8 +377,10 @@ __device__ __forceinline__ void process_window(Win<K>& w, const StepParams& p, V
 }
 
 // process_window<2> as straight-line code for a window of one or two rows
-// (the tier-1 general path): the same operations in the same order, so the
-// result is bitwise identical; no loops, masks or warp votes.
+// (tier 1.5): the same operations in the same order, so the result is
+// bitwise identical; no loops, masks or warp votes.  A single skeleton row
+// takes the general arithmetic too: with finite inputs every term cancels
+// exactly (the closed form of tier 1), so no divergent shortcut is needed.
 __device__ __forceinline__ void process_two(Win<2>& w, const StepParams& p, VRes& res, unsigned int& out_mask) {
     const bool h1 = w.m > 1;
     const double ph0 = w.phi[0], lm0 = w.lam[0];
@@ -395,26 +397,6 @@ __device__ __forceinline__ void process_two(Win<2>& w, const StepParams& p, VRes
     res.nskel = n;
     out_mask = 0;
     if (n == 0) return;
-    if (n == 1) {
-        const double ph = in0 ? ph0 : ph1, lm = in0 ? lm0 : lm1;
-        if (p.finite && isfinite(ph) && isfinite(lm)) {      // single-row closed form
-            double v = ph;
-            if (v > 1.0) v = 1.0;
-            else if (v <= 0.0) v = 0.0;
-            const double s = 0.0 + v;
-            const double nv = s > 0.0 ? v * (1.0 / s) : v;
-            const int slot = in0 ? 0 : 1;
-            if (nv != 0.0) {
-                res.cnt = 1;
-                out_mask = 1u << slot;
-                if (w.rows[slot] == 0) res.bm = nv;
-            }
-            const double dd = fabs(nv - ph);
-            if (dd > res.maxd) res.maxd = dd;
-            w.lam[slot] = nv;
-            return;
-        }
-    }
     // aggregates over the skeleton rows in row order (Appendix A)
     const double sq0 = in0 ? sqrt(ph0) : 0.0;
     const double sq1 = in1 ? sqrt(ph1) : 0.0;
@@ -831,7 +813,7 @@ __device__ __forceinline__ long long pool_place(int need, const VRes& res, const
 // the tile's slots, base mass in lane order (fixed): no hot atomics.
 
 template <typename T, bool UNIFORM, bool PACKED>
-__global__ void __launch_bounds__(FT_TPB, 8) gen_kernel(const StepParams p) {
+__global__ void __launch_bounds__(FT_TPB, 6) gen_kernel(const StepParams p) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     __shared__ int s_list[FT_WARPS][FT_TPB];
     const int lane = threadIdx.x & 31;
@@ -872,33 +854,39 @@ __global__ void __launch_bounds__(FT_TPB, 8) gen_kernel(const StepParams p) {
             int rlo = INT_MAX, rhi = -1;
 #pragma unroll
             for (int k = 0; k < kMD; ++k) {
-                if (u[k] == j) kd = k;
+                kd = (u[k] == j) ? k : kd;
                 big |= sg[k] <= -3;
-                if (sg[k] >= 0) {
-                    const int x = sg[k] & ~kPair;
-                    rlo = min(rlo, x); rhi = max(rhi, x);
-                    if (sg[k] & kPair) { rlo = min(rlo, ax[k]); rhi = max(rhi, ax[k]); }
-                }
+                const bool h = sg[k] >= 0, pr = h && (sg[k] & kPair);
+                const int x0 = h ? (sg[k] & ~kPair) : INT_MAX;
+                rlo = min(rlo, x0);
+                rhi = max(rhi, h ? x0 : -1);
+                rlo = min(rlo, pr ? ax[k] : INT_MAX);
+                rhi = max(rhi, pr ? ax[k] : -1);
             }
-            // values loaded in the accumulation pass (registers)
+            // values loaded in the accumulation pass; branch-free: a term of
+            // another row adds +0.0, which changes at most the sign of an
+            // exact-zero sum (irrelevant: DESIGN.md section 4)
             const double invdeg = UNIFORM ? recip_deg(n) : 0.0;
             double l0 = 0.0, l1 = 0.0, p0 = 0.0, p1 = 0.0;
             bool more = false;
 #pragma unroll
             for (int k = 0; k < kMD; ++k) {
-                if (sg[k] < 0) continue;
-                const double l = lap_value<T, UNIFORM>(p, k, kd, q0, invdeg);
+                const bool h = sg[k] >= 0, pr = h && (sg[k] & kPair);
+                const double l = (k < n) ? lap_value<T, UNIFORM>(p, k, kd, q0, invdeg) : 0.0;
                 const int x0 = sg[k] & ~kPair;
-                const double a0 = ldv<T>(p.in.v0, u[k]);
-                if (x0 == rlo) { l0 = l0 + a0 * l; if (k == kd) p0 = a0; }
-                else if (x0 == rhi) { l1 = l1 + a0 * l; if (k == kd) p1 = a0; }
-                else more = true;
-                if (sg[k] & kPair) {
-                    const double a1 = ldv<T>(p.in.v1, u[k]);
-                    if (ax[k] == rlo) { l0 = l0 + a1 * l; if (k == kd) p0 = a1; }
-                    else if (ax[k] == rhi) { l1 = l1 + a1 * l; if (k == kd) p1 = a1; }
-                    else more = true;
-                }
+                const double a0 = h ? ldv<T>(p.in.v0, u[k]) : 0.0;
+                const double a1 = pr ? ldv<T>(p.in.v1, u[k]) : 0.0;
+                const bool e00 = h && x0 == rlo, e01 = h && x0 != rlo && x0 == rhi;
+                const bool e10 = pr && ax[k] == rlo, e11 = pr && ax[k] != rlo && ax[k] == rhi;
+                more |= (h && x0 != rlo && x0 != rhi) || (pr && ax[k] != rlo && ax[k] != rhi);
+                const double t0 = a0 * l, t1 = a1 * l;
+                l0 = l0 + (e00 ? t0 : 0.0);
+                l0 = l0 + (e10 ? t1 : 0.0);
+                l1 = l1 + (e01 ? t0 : 0.0);
+                l1 = l1 + (e11 ? t1 : 0.0);
+                const bool dg = k == kd;
+                p0 = (dg && e00) ? a0 : ((dg && e10) ? a1 : p0);
+                p1 = (dg && e01) ? a0 : ((dg && e11) ? a1 : p1);
             }
             const bool defer = mine && (more || big || rlo == INT_MAX || kd < 0 || n == 0);
             Win<2> w;
@@ -1712,11 +1700,16 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
     p.report_ids = dom ? dom->report_ids : nullptr;
     if (which & 1) FT_PICK3(ft::tier1_kernel, dtype, uni, packed)<<<p.num_tiles, FT_TPB, 0, s>>>(p);
     if (which & 2) {
+        // FT_PROBE_FIXUP (timing probes only, results invalid): bit mask of
+        // the tier-1.5 / 2a / 2b / 3 launches
+        static const char* probe = getenv("FT_PROBE_FIXUP");
+        const int m = probe ? atoi(probe) : 15;
         // tier 1.5, one warp per tile
-        FT_PICK3(ft::gen_kernel, dtype, uni, packed)<<<(p.num_tiles + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
-        FT_PICK3(ft::wide3_kernel, dtype, uni, packed)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
-        FT_PICK2(ft::wide_kernel, dtype, uni)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
-        FT_PICK2(ft::deep_kernel, dtype, uni)<<<g_fixup_grid / 4, FT_TPB, 0, s>>>(p);
+        if (m & 1)
+            FT_PICK3(ft::gen_kernel, dtype, uni, packed)<<<(p.num_tiles + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
+        if (m & 2) FT_PICK3(ft::wide3_kernel, dtype, uni, packed)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
+        if (m & 4) FT_PICK2(ft::wide_kernel, dtype, uni)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
+        if (m & 8) FT_PICK2(ft::deep_kernel, dtype, uni)<<<g_fixup_grid / 4, FT_TPB, 0, s>>>(p);
     }
     return cuda_check("step kernel");
 }
