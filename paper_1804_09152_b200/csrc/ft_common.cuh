@@ -24,19 +24,21 @@ struct Control {
     unsigned long long pool_next;      // pool bump pointer of the step's output
     unsigned int       nan_key;        // atomicMax(INT_MAX - col) -> min col
     int                overflow;       // the output pool is too small
-    int                slow_count;     // wide columns queued for tier 2
+    int                slow_count;     // queue A: tier-1 columns for tier 2
     unsigned int       fin_count;      // finalize: CTAs done (last-block pattern)
-    int                deep_count;     // tier-3 columns (slow_list + n_v)
-    int                gen_count;      // tier-1.5 columns (slow_list + 2 n_v)
+    int                deep_count;     // tier-3 columns of queue A
+    int                gen_count;      // queue B: tier-1.5 columns deferred to tier 2
     int                done;           // evolve: stop flag (finalize sets it)
     int                steps_done;     // evolve: completed steps
     int                status;         // evolve: final status
     unsigned int       nonfinite;      // sticky: a kernel wrote a non-finite value
     long long          needed;         // capacity needed on overflow
-    int                wide8_count;    // tier-2b columns (slow_list + 3 n_v + FT_TPB)
-    int                pad2;
+    int                wide8_count;    // tier-2b columns of queue A
+    int                wide8b_count;   // tier-2b columns of queue B
     long long          conv_next;      // pool bump pointer of ft_tiled_from_csc
-    long long          pad1[2];
+    int                deepb_count;    // tier-3 columns of queue B
+    int                pad3;
+    long long          pad1;
 };
 static_assert(sizeof(Control) % 16 == 0, "Control must stay 16B aligned");
 
@@ -57,7 +59,8 @@ struct Workspace {
     double*       gen_maxd;     // [num_tiles]
     int2*         gen_cs;       // [num_tiles]
     double*       vbm;          // [n_v] base mass of tier-2/3 columns
-    int*          slow_list;    // tier-2 queue [0, n_v), tier-3 at +n_v, tier-2b at +2 n_v
+    int*          slow_list;    // [3 n_v] tier-2 / 2b / 3 lists of queues A (growing up from
+                                //   0, n_v, 2 n_v) and B (growing down from n_v - 1, ...)
     long long*    chunk_off;    // [num_chunks + 2] compaction chunk offsets
     double*       fin_part;     // [FT_FIN_MAX] finalize partial sums (base mass)
     double*       fin_maxd;     // [FT_FIN_MAX] finalize partial maxima

@@ -82,6 +82,17 @@ struct FinalizeParams {
     double base_threshold;
 };
 
+// One tier-2/3 pipeline: its input queue and the tier-2b / tier-3 lists it
+// feeds.  Queue A holds tier 1's wide columns and runs on a side stream
+// concurrently with tier 1.5; queue B holds the columns tier 1.5 defers.
+// Entry i of a list is base[dir * i] (A grows up, B down: disjoint).
+struct Queues {
+    int* q;  int* q_n;
+    int* w8; int* w8_n;
+    int* dp; int* dp_n;
+    int dir;
+};
+
 // ---------------------------------------------------------------------------
 // register window of layer rows for one vertex column
 
@@ -813,7 +824,7 @@ __device__ __forceinline__ long long pool_place(int need, const VRes& res, const
 // the tile's slots, base mass in lane order (fixed): no hot atomics.
 
 template <typename T, bool UNIFORM, bool PACKED>
-__global__ void __launch_bounds__(FT_TPB, 6) gen_kernel(const StepParams p) {
+__global__ void __launch_bounds__(FT_TPB, 8) gen_kernel(const StepParams p) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     __shared__ int s_list[FT_WARPS][FT_TPB];
     const int lane = threadIdx.x & 31;
@@ -821,20 +832,17 @@ __global__ void __launch_bounds__(FT_TPB, 6) gen_kernel(const StepParams p) {
     const int nwarps = gridDim.x * FT_WARPS;
     for (int t = (blockIdx.x * FT_TPB + threadIdx.x) >> 5; t < p.num_tiles; t += nwarps) {
         const uint4 g4 = *reinterpret_cast<const uint4*>(&p.ws.gen_mask[(size_t)FT_WARPS * t]);
-        const uint4 w4 = *reinterpret_cast<const uint4*>(&p.ws.slow_mask[(size_t)FT_WARPS * t]);
         const unsigned int gm[4] = {g4.x, g4.y, g4.z, g4.w};
-        const unsigned int wm[4] = {w4.x, w4.y, w4.z, w4.w};
         int ng = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             if ((gm[q] >> lane) & 1u) list[ng + __popc(gm[q] & ((1u << lane) - 1u))] = t * FT_TPB + q * 32 + lane;
             ng += __popc(gm[q]);
         }
-        if (ng == 0 && (wm[0] | wm[1] | wm[2] | wm[3]) == 0) continue;
+        if (ng == 0) continue;
         __syncwarp();
         double tbm = 0.0, tmx = 0.0;
         int tcnt = 0, tskel = 0;
-        unsigned int df[4] = {0u, 0u, 0u, 0u};
         for (int c0 = 0; c0 < ng; c0 += 32) {
             const bool mine = c0 + lane < ng;
             const int jl = mine ? list[c0 + lane] : 0;
@@ -849,6 +857,8 @@ __global__ void __launch_bounds__(FT_TPB, 6) gen_kernel(const StepParams p) {
                 sg[k] = h ? __ldg(&p.in.sig[u[k]]) : FT_SIG_EMPTY;
                 ax[k] = h ? __ldg(&p.in.aux[u[k]]) : 0;
             }
+            const double vj0 = mine ? ldv<T>(p.in.v0, j) : 0.0;
+            const double vj1 = mine ? ldv<T>(p.in.v1, j) : 0.0;
             int kd = -1;
             bool big = false;
             int rlo = INT_MAX, rhi = -1;
@@ -863,11 +873,22 @@ __global__ void __launch_bounds__(FT_TPB, 6) gen_kernel(const StepParams p) {
                 rlo = min(rlo, pr ? ax[k] : INT_MAX);
                 rhi = max(rhi, pr ? ax[k] : -1);
             }
-            // values loaded in the accumulation pass; branch-free: a term of
-            // another row adds +0.0, which changes at most the sign of an
-            // exact-zero sum (irrelevant: DESIGN.md section 4)
+            // PHI(r, j) from the column's own entries (sg[kd], aux[kd])
+            int sgj = FT_SIG_EMPTY, axj = 0;
+#pragma unroll
+            for (int k = 0; k < kMD; ++k) {
+                sgj = (k == kd) ? sg[k] : sgj;
+                axj = (k == kd) ? ax[k] : axj;
+            }
+            const bool hj = sgj >= 0, prj = hj && (sgj & kPair);
+            const int xj = sgj & ~kPair;
+            const double p0 = (hj && xj == rlo) ? vj0 : 0.0;
+            const double p1 = (hj && xj == rhi) ? vj0 : ((prj && axj == rhi) ? vj1 : 0.0);
+            // Lt(rlo, j), Lt(rhi, j) in L order; an entry of a neighbour
+            // holding rows x0 < x1 goes to its row's sum (x1 == rlo and
+            // x0 == rhi are impossible: rlo / rhi are the min / max)
             const double invdeg = UNIFORM ? recip_deg(n) : 0.0;
-            double l0 = 0.0, l1 = 0.0, p0 = 0.0, p1 = 0.0;
+            double l0 = 0.0, l1 = 0.0;
             bool more = false;
 #pragma unroll
             for (int k = 0; k < kMD; ++k) {
@@ -876,17 +897,12 @@ __global__ void __launch_bounds__(FT_TPB, 6) gen_kernel(const StepParams p) {
                 const int x0 = sg[k] & ~kPair;
                 const double a0 = h ? ldv<T>(p.in.v0, u[k]) : 0.0;
                 const double a1 = pr ? ldv<T>(p.in.v1, u[k]) : 0.0;
-                const bool e00 = h && x0 == rlo, e01 = h && x0 != rlo && x0 == rhi;
-                const bool e10 = pr && ax[k] == rlo, e11 = pr && ax[k] != rlo && ax[k] == rhi;
-                more |= (h && x0 != rlo && x0 != rhi) || (pr && ax[k] != rlo && ax[k] != rhi);
-                const double t0 = a0 * l, t1 = a1 * l;
-                l0 = l0 + (e00 ? t0 : 0.0);
-                l0 = l0 + (e10 ? t1 : 0.0);
-                l1 = l1 + (e01 ? t0 : 0.0);
-                l1 = l1 + (e11 ? t1 : 0.0);
-                const bool dg = k == kd;
-                p0 = (dg && e00) ? a0 : ((dg && e10) ? a1 : p0);
-                p1 = (dg && e01) ? a0 : ((dg && e11) ? a1 : p1);
+                const bool m0 = h && x0 == rlo;
+                const bool m1a = h && x0 != rlo && x0 == rhi, m1b = pr && ax[k] == rhi;
+                more |= (h && x0 != rlo && x0 != rhi) || (pr && ax[k] != rhi);
+                l0 = m0 ? l0 + a0 * l : l0;
+                const double c1 = m1a ? a0 : a1;
+                l1 = (m1a || m1b) ? l1 + c1 * l : l1;
             }
             const bool defer = mine && (more || big || rlo == INT_MAX || kd < 0 || n == 0);
             Win<2> w;
@@ -903,21 +919,26 @@ __global__ void __launch_bounds__(FT_TPB, 6) gen_kernel(const StepParams p) {
                 report_flags(res, j, p);
                 emit_window<T, 2>(w, out_mask, j, 0, p);
             }
-            if (defer) {
-                const int lt = jl - t * FT_TPB;
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if ((lt >> 5) == q) df[q] |= 1u << (lt & 31);
+            // three or more rows (rare): queue B, one atomic per chunk
+            const unsigned int db = __ballot_sync(0xffffffffu, defer);
+            if (db) {
+                if (defer) {
+                    const int lt = jl - t * FT_TPB;
+                    atomicOr(&p.ws.slow_mask[(size_t)FT_WARPS * t + (lt >> 5)], 1u << (lt & 31));
+                }
+                int qb = 0;
+                if (lane == 0) qb = atomicAdd(&p.ws.ctl->gen_count, __popc(db));
+                qb = __shfl_sync(0xffffffffu, qb, 0);
+                if (defer) p.ws.slow_list[(p.n_v - 1) - (qb + __popc(db & ((1u << lane) - 1u)))] = j;
             }
-            // base mass of the chunk in lane order (the list is in vertex
-            // order): a fixed order, so the total is deterministic
-            double cbm = run ? res.bm : 0.0;
-            cbm = warp_sum(cbm);
-            tbm = tbm + __shfl_sync(0xffffffffu, cbm, 0);
+            // per-lane partials (lane l: list entries l, l + 32, ...), then
+            // one fixed shuffle tree: the base mass is deterministic
+            if (run) tbm = tbm + res.bm;
             tmx = fmax(tmx, res.maxd);
             tcnt += run ? res.cnt : 0;
             tskel += run ? res.nskel : 0;
         }
+        tbm = warp_sum(tbm);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) tmx = fmax(tmx, __shfl_down_sync(0xffffffffu, tmx, o));
         tcnt = warp_sum(tcnt);
@@ -927,28 +948,34 @@ __global__ void __launch_bounds__(FT_TPB, 6) gen_kernel(const StepParams p) {
             p.ws.gen_maxd[t] = tmx;
             p.ws.gen_cs[t] = make_int2(tcnt, tskel);
         }
-        // tier-2 queue: tier 1's slow columns and the deferred ones
-        unsigned int all[4];
-        int nq = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const unsigned int d = __reduce_or_sync(0xffffffffu, df[q]);
-            all[q] = wm[q] | d;
-            if (d && lane == 0) p.ws.slow_mask[(size_t)FT_WARPS * t + q] = all[q];
-            nq += __popc(all[q]);
-        }
-        if (nq) {
-            int qb = 0;
-            if (lane == 0) qb = atomicAdd(&p.ws.ctl->slow_count, nq);
-            qb = __shfl_sync(0xffffffffu, qb, 0);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if ((all[q] >> lane) & 1u)
-                    p.ws.slow_list[qb + __popc(all[q] & ((1u << lane) - 1u))] = p.j_base + t * FT_TPB + q * 32 + lane;
-                qb += __popc(all[q]);
-            }
-        }
         __syncwarp();
+    }
+}
+
+// tier-1 wide columns (segment slow masks) -> queue A, one thread per
+// segment, one atomic per warp
+__global__ void __launch_bounds__(256) queue_kernel(const StepParams p) {
+    if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
+    const int seg = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const unsigned int m = seg < FT_WARPS * p.num_tiles ? p.ws.slow_mask[seg] : 0u;
+    const int c = __popc(m);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (tot == 0) return;
+    int qb = 0;
+    if (lane == 31) qb = atomicAdd(&p.ws.ctl->slow_count, tot);
+    qb = __shfl_sync(0xffffffffu, qb, 31) + incl - c;
+    unsigned int mm = m;
+    while (mm) {
+        const int b = __ffs(mm) - 1;
+        mm &= mm - 1;
+        p.ws.slow_list[qb++] = p.j_base + seg * 32 + b;
     }
 }
 
@@ -1029,16 +1056,16 @@ __device__ __forceinline__ bool wide3(int j, const StepParams& p, Win<3>& w) {
 }
 
 template <typename T, bool UNIFORM, bool PACKED>
-__global__ void __launch_bounds__(FT_TPB, 4) wide3_kernel(const StepParams p) {
+__global__ void __launch_bounds__(FT_TPB, 4) wide3_kernel(const StepParams p, const Queues qs) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
-    const int n_wide = *(volatile int*)&p.ws.ctl->slow_count;
+    const int n_wide = *(volatile int*)qs.q_n;
     const int lane = threadIdx.x & 31;
     const int stride = gridDim.x * FT_TPB;
     const int rounds = (n_wide + stride - 1) / stride;
     for (int rnd = 0; rnd < rounds; ++rnd) {
         const int i = rnd * stride + blockIdx.x * FT_TPB + threadIdx.x;
         const bool mine = i < n_wide;
-        const int j = mine ? p.ws.slow_list[i] : 0;
+        const int j = mine ? qs.q[qs.dir * i] : 0;
         VRes res;
         vres_init(res);
         Win<3> w;
@@ -1055,10 +1082,10 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide3_kernel(const StepParams p) {
         const unsigned int ob = __ballot_sync(0xffffffffu, on);
         if (ob) {
             int qb = 0;
-            if (lane == 0) qb = atomicAdd(&p.ws.ctl->wide8_count, __popc(ob));
+            if (lane == 0) qb = atomicAdd(qs.w8_n, __popc(ob));
             qb = __shfl_sync(0xffffffffu, qb, 0);
             if (on) {
-                p.ws.slow_list[2 * p.n_v + qb + __popc(ob & ((1u << lane) - 1u))] = j;
+                qs.w8[qs.dir * (qb + __popc(ob & ((1u << lane) - 1u)))] = j;
                 vres_init(res);
             }
         }
@@ -1135,17 +1162,17 @@ __device__ __forceinline__ bool gather_wide(int j, const StepParams& p, Win<K>& 
 }
 
 template <typename T, bool UNIFORM>
-__global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p) {
+__global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p, const Queues qs) {
     constexpr int KW = 8;      // wider unions go to tier 3
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
-    const int n_wide = *(volatile int*)&p.ws.ctl->wide8_count;   // tier-2a leftovers
+    const int n_wide = *(volatile int*)qs.w8_n;   // tier-2a leftovers
     const int lane = threadIdx.x & 31;
     const int stride = gridDim.x * FT_TPB;
     const int rounds = (n_wide + stride - 1) / stride;
     for (int rnd = 0; rnd < rounds; ++rnd) {
         const int i = rnd * stride + blockIdx.x * FT_TPB + threadIdx.x;
         const bool mine = i < n_wide;
-        const int j = mine ? p.ws.slow_list[2 * p.n_v + i] : 0;
+        const int j = mine ? qs.w8[qs.dir * i] : 0;
         VRes res;
         vres_init(res);
         Win<KW> w;
@@ -1158,14 +1185,14 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p) {
                 report_flags(res, j, p);
             }
         }
-        // tier 3: beyond the tier-2 window (queued at slow_list + n_v)
+        // tier 3: beyond the tier-2 window
         const unsigned int db = __ballot_sync(0xffffffffu, deep);
         if (db) {
             int qb = 0;
-            if (lane == 0) qb = atomicAdd(&p.ws.ctl->deep_count, __popc(db));
+            if (lane == 0) qb = atomicAdd(qs.dp_n, __popc(db));
             qb = __shfl_sync(0xffffffffu, qb, 0);
             if (deep) {
-                p.ws.slow_list[p.n_v + qb + __popc(db & ((1u << lane) - 1u))] = j;
+                qs.dp[qs.dir * (qb + __popc(db & ((1u << lane) - 1u)))] = j;
                 vres_init(res);    // only the columns handed to tier 3
             }
         }
@@ -1179,18 +1206,278 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// warp-cooperative column (the wide tail: tier-2a leftovers, tier-1.5
+// deferrals).  One warp per column: lane e holds entry e of the
+// neighbourhood (neighbours in L order, rows ascending within one), lanes
+// with equal rows are grouped with __match_any_sync, and every sum is taken
+// in the reference's order -- Lt(r, j) over the entries in L order
+// (_kernels.py:36-50), the skeleton aggregates and the normaliser in
+// ascending row order (_kernels.py:179-282) -- by shuffles, so the result is
+// bitwise that of process_window / vertex_slow.  Neighbourhoods of more
+// than 32 entries (or 32 L entries) take vertex_slow in lane 0.
+
+struct WarpStats {
+    double maxd;
+    long long cnt, skel;
+};
+
+template <typename T, bool UNIFORM>
+__device__ __forceinline__ void warp_column(int j, const StepParams& p, int lane, WarpStats& ws) {
+    const unsigned int full = 0xffffffffu;
+    const int jl = j - p.j_base;
+    const int q0 = __ldg(&p.lap_ptr[jl]);
+    const int n = __ldg(&p.lap_ptr[jl + 1]) - q0;
+    int u = -1, sgk = FT_SIG_EMPTY, axk = 0, ck = 0;
+    double lk = 0.0;
+    if (lane < n && n <= 32) {
+        u = __ldg(&p.lap_idx[q0 + lane]);
+        sgk = __ldg(&p.in.sig[u]);
+        ck = sig_count(sgk);
+        axk = ck >= 2 ? __ldg(&p.in.aux[u]) : 0;
+    }
+    const unsigned int dmask = __ballot_sync(full, lane < n && u == j);
+    const int kd = dmask ? __ffs(dmask) - 1 : -1;
+    if (lane < n && n <= 32) {
+        if (UNIFORM) lk = (lane == kd) ? -1.0 : 1.0 / (double)(n - 1);
+        else lk = ldv<T>(p.lap_val, q0 + lane);
+    }
+    // entry offsets: exclusive scan of the counts over the L entries
+    int incl = ck;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(full, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int E = __shfl_sync(full, incl, 31);
+    if (n > 32 || n < 1 || kd < 0 || E > 32) {
+        // general fallback in lane 0 (statistics through the atomics)
+        if (lane == 0) {
+            VRes res;
+            vres_init(res);
+            vertex_slow<T, 8, UNIFORM>(j, p, res, 0, false);
+            report_flags(res, j, p);
+            long long off = 0;
+            bool ok = true;
+            if (res.cnt > 2) {
+                off = (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)res.cnt);
+                if (off + res.cnt > p.cap) { atomicExch(&p.ws.ctl->overflow, 1); ok = false; }
+            }
+            p.ws.vbm[jl] = res.bm;
+            if (ok) { VRes r2 = res; vertex_slow<T, 8, UNIFORM>(j, p, r2, off, true); }
+            ws.maxd = fmax(ws.maxd, res.maxd);
+            ws.cnt += res.cnt;
+            ws.skel += res.nskel;
+        }
+        return;
+    }
+    const int e0k = incl - ck;
+    // this lane's entry: owner neighbour k (entries are k-major) and index t
+    int myk = 0, t = 0;
+    for (int k = 0; k < n; ++k) {
+        const int a = __shfl_sync(full, e0k, k), c = __shfl_sync(full, ck, k);
+        if (lane >= a && lane < a + c) { myk = k; t = lane - a; }
+    }
+    const int su = __shfl_sync(full, u, myk), ss = __shfl_sync(full, sgk, myk), sa = __shfl_sync(full, axk, myk);
+    const double sl = __shfl_sync(full, lk, myk);
+    const bool valid = lane < E;
+    int r = -1 - lane;                // unique key for lanes without an entry
+    double v = 0.0;
+    if (valid) {
+        r = hyb_row<T>(p.in, ss, sa, t);
+        v = hyb_val<T>(p.in, su, ss, sa, t);
+    }
+    const double prod = v * sl;       // PHI(r, u) * L(j, u)
+    const bool dg = valid && myk == kd;
+    const unsigned int grp = __match_any_sync(full, r);
+    const bool leader = valid && (__ffs(grp) - 1) == lane;
+    // Lt(r, j) in L order, PHI(r, j) from the diagonal neighbour, and the
+    // row rank among the distinct rows
+    double lam = 0.0, ph = 0.0;
+    int rank = 0;
+    for (int src = 0; src < E; ++src) {
+        const double pv = __shfl_sync(full, prod, src);
+        const double vv = __shfl_sync(full, v, src);
+        const int rr = __shfl_sync(full, r, src);
+        const bool ds = __shfl_sync(full, dg, src);
+        const bool ls = __shfl_sync(full, leader, src);
+        if ((grp >> src) & 1u) {
+            lam = lam + pv;
+            if (ds) ph = vv;
+        }
+        if (ls && rr < r) ++rank;
+    }
+    const int m = __popc(__ballot_sync(full, leader));
+    const bool in = leader && in_skeleton(ph, lam);
+    int bad_phi = (leader && ph != 0.0 && !in) ? r : -1;
+    int bad_lt = (leader && lam != 0.0 && !in) ? r : -1;
+    const double lh = (lam != 0.0) ? lam : 0.0;
+    const double sq = in ? sqrt(ph) : 0.0;
+    // aggregates over the skeleton rows in ascending row order
+    Agg g;
+    agg_init(g);
+    for (int q = 0; q < m; ++q) {
+        const int lq = __ffs(__ballot_sync(full, leader && rank == q)) - 1;
+        const bool iq = __shfl_sync(full, in, lq);
+        const double phq = __shfl_sync(full, ph, lq), lhq = __shfl_sync(full, lh, lq), sqq = __shfl_sync(full, sq, lq);
+        const int rq = __shfl_sync(full, r, lq);
+        if (iq) {
+            if (g.n == 0) { g.first_row = rq; g.phi0 = phq; }
+            g.n++;
+            g.sl = g.sl + lhq;
+            g.sp = g.sp + phq;
+            g.sr = g.sr + sqq;
+        }
+    }
+    bool nan = false;
+    double vn = 0.0;
+    double s = 0.0;
+    if (g.n > 0) {
+        const Coef c = make_coef(g, p, c_recip);
+        if (in) vn = update_entry_sq(r, ph, lh, sq, c, p, nan);
+        for (int q = 0; q < m; ++q) {
+            const int lq = __ffs(__ballot_sync(full, leader && rank == q)) - 1;
+            const bool iq = __shfl_sync(full, in, lq);
+            const double vq = __shfl_sync(full, vn, lq);
+            if (iq) s = s + vq;
+        }
+    }
+    const bool spos = s > 0.0;
+    const double inv = spos ? 1.0 / s : 0.0;
+    const double nv = spos ? vn * inv : vn;
+    const bool out = in && nv != 0.0;
+    const unsigned int ob = __ballot_sync(full, out);
+    const int cnt = __popc(ob);
+    int pos = 0;       // rank among the output rows
+    for (int src = 0; src < E; ++src) {
+        const bool os = __shfl_sync(full, out, src);
+        const int rk = __shfl_sync(full, rank, src);
+        if (os && rk < rank) ++pos;
+    }
+    // statistics and error reports of the column
+    double bm = (out && r == 0) ? nv : 0.0;
+    double dd = in ? fabs(nv - ph) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        bm = bm + __shfl_xor_sync(full, bm, o);   // at most one nonzero term: exact
+        dd = fmax(dd, __shfl_xor_sync(full, dd, o));
+        bad_phi = max(bad_phi, __shfl_xor_sync(full, bad_phi, o));
+        bad_lt = max(bad_lt, __shfl_xor_sync(full, bad_lt, o));
+    }
+    const bool anynan = __any_sync(full, nan);
+    const int nskel = __popc(__ballot_sync(full, in));
+    if (lane == 0) {
+        VRes res;
+        vres_init(res);
+        res.nan = anynan; res.bad_phi_row = bad_phi; res.bad_lt_row = bad_lt;
+        report_flags(res, j, p);
+        p.ws.vbm[jl] = bm;
+        ws.maxd = fmax(ws.maxd, dd);
+        ws.cnt += cnt;
+        ws.skel += nskel;
+    }
+    // output: dense for at most two rows, else a pool range
+    if (cnt <= 2) {
+        if (cnt == 0) {
+            if (lane == 0) p.out.sig[j] = FT_SIG_EMPTY;
+        } else if (out) {
+            if (pos == 0) {
+                p.out.sig[j] = cnt == 2 ? (r | kPair) : r;
+                ((T*)p.out.v0)[j] = (T)nv;
+            } else {
+                p.out.aux[j] = r;
+                ((T*)p.out.v1)[j] = (T)nv;
+            }
+            if (!isfinite(nv)) atomicOr(&p.ws.ctl->nonfinite, 1u);
+        }
+        return;
+    }
+    long long off = 0;
+    if (lane == 0) off = (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)cnt);
+    off = __shfl_sync(full, off, 0);
+    if (off + cnt > p.cap) {
+        if (lane == 0) atomicExch(&p.ws.ctl->overflow, 1);
+        return;
+    }
+    if (lane == 0) { p.out.sig[j] = -cnt; p.out.aux[j] = (int)off; }
+    if (out) {
+        p.out.pidx[off + pos] = r;
+        ((T*)p.out.pval)[off + pos] = (T)nv;
+        if (!isfinite(nv)) atomicOr(&p.ws.ctl->nonfinite, 1u);
+    }
+}
+
+// one warp per listed column (grid-stride); the warp's statistics go to
+// the global accumulators once
+template <typename T, bool UNIFORM>
+__global__ void __launch_bounds__(FT_TPB, 4) warp_kernel(const StepParams p, const int* list, const int* count, int dir) {
+    if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
+    const int nc = *(volatile const int*)count;
+    const int lane = threadIdx.x & 31;
+    const int nw = gridDim.x * FT_WARPS;
+    WarpStats ws;
+    ws.maxd = 0.0; ws.cnt = 0; ws.skel = 0;
+    for (int i = (blockIdx.x * FT_TPB + threadIdx.x) >> 5; i < nc; i += nw)
+        warp_column<T, UNIFORM>(__ldg(&list[dir * i]), p, lane, ws);
+    if (lane == 0 && (ws.maxd > 0.0 || ws.cnt || ws.skel)) {
+        if (ws.maxd > 0.0) atomicMax(&p.ws.ctl->maxdelta_bits, (unsigned long long)__double_as_longlong(ws.maxd));
+        if (ws.skel) atomicAdd(&p.ws.ctl->skel_total, (unsigned long long)ws.skel);
+        if (ws.cnt) atomicAdd(&p.ws.ctl->nnz_total, (unsigned long long)ws.cnt);
+    }
+}
+
+// queue B (the few columns tier 1.5 defers) in ONE launch after tier 1.5:
+// the tier-2a register path, else the general windowed algorithm in the
+// same lane (no further queues, so no chain of dependent tail launches)
+template <typename T, bool UNIFORM, bool PACKED>
+__global__ void __launch_bounds__(FT_TPB) tail_kernel(const StepParams p, const Queues qs) {
+    if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
+    const int n_q = *(volatile int*)qs.q_n;
+    const int lane = threadIdx.x & 31;
+    const int stride = gridDim.x * FT_TPB;
+    const int rounds = (n_q + stride - 1) / stride;
+    for (int rnd = 0; rnd < rounds; ++rnd) {
+        const int i = rnd * stride + blockIdx.x * FT_TPB + threadIdx.x;
+        const bool mine = i < n_q;
+        const int j = mine ? qs.q[qs.dir * i] : 0;
+        VRes res;
+        vres_init(res);
+        Win<3> w;
+        w.m = 0;
+        unsigned int out_mask = 0;
+        bool slow = false;
+        if (mine) {
+            slow = !wide3<T, UNIFORM, PACKED>(j, p, w);
+            if (!slow) process_window<3>(w, p, res, out_mask, c_recip);
+            else vertex_slow<T, 8, UNIFORM>(j, p, res, 0, false);
+            report_flags(res, j, p);
+        }
+        bool fits;
+        const int need = (mine && res.cnt > 2) ? res.cnt : 0;
+        const long long off = pool_place(need, res, p, lane, fits);
+        if (mine) {
+            p.ws.vbm[j - p.j_base] = res.bm;
+            if (need == 0 || fits) {
+                if (!slow) emit_window<T, 3>(w, out_mask, j, off, p);
+                else { VRes r2 = res; vertex_slow<T, 8, UNIFORM>(j, p, r2, off, true); }
+            }
+        }
+    }
+}
+
 // tier 3: exact windowed global-memory algorithm (no width limit)
 template <typename T, bool UNIFORM>
-__global__ void __launch_bounds__(FT_TPB) deep_kernel(const StepParams p) {
+__global__ void __launch_bounds__(FT_TPB) deep_kernel(const StepParams p, const Queues qs) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
-    const int n_deep = *(volatile int*)&p.ws.ctl->deep_count;
+    const int n_deep = *(volatile int*)qs.dp_n;
     const int lane = threadIdx.x & 31;
     const int stride = gridDim.x * FT_TPB;
     const int rounds = (n_deep + stride - 1) / stride;
     for (int rnd = 0; rnd < rounds; ++rnd) {
         const int i = rnd * stride + blockIdx.x * FT_TPB + threadIdx.x;
         const bool mine = i < n_deep;
-        const int j = mine ? p.ws.slow_list[p.n_v + i] : 0;
+        const int j = mine ? qs.dp[qs.dir * i] : 0;
         VRes res;
         vres_init(res);
         if (mine) {
@@ -1350,6 +1637,8 @@ __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizePara
     ctl->deep_count = 0;
     ctl->gen_count = 0;
     ctl->wide8_count = 0;
+    ctl->wide8b_count = 0;
+    ctl->deepb_count = 0;
     if (f.evolve) {
         if (status != FT_STATUS_OK) {
             ctl->done = 1;
@@ -1579,6 +1868,21 @@ __global__ void nonfinite_reset_kernel(Control* ctl) { ctl->nonfinite = 0u; }
 
 typedef void (*StepKernelFn)(const StepParams);
 
+static Queues queues(const StepParams& p, int which) {
+    Queues q;
+    int* L = p.ws.slow_list;
+    Control* c = p.ws.ctl;
+    const int n = p.n_v;
+    if (which == 0) {
+        q.q = L; q.w8 = L + n; q.dp = L + 2 * n; q.dir = 1;
+        q.q_n = &c->slow_count; q.w8_n = &c->wide8_count; q.dp_n = &c->deep_count;
+    } else {
+        q.q = L + n - 1; q.w8 = L + 2 * n - 1; q.dp = L + 3 * n - 1; q.dir = -1;
+        q.q_n = &c->gen_count; q.w8_n = &c->wide8b_count; q.dp_n = &c->deepb_count;
+    }
+    return q;
+}
+
 #define FT_PICK3(K, dtype, uni, packed)                                               \
     ((dtype) == FT_F64 ? ((uni) ? ((packed) ? K<double, true, true> : K<double, true, false>) \
                                 : K<double, false, false>)                             \
@@ -1637,6 +1941,50 @@ static int check_tiled(const ft_tiled* t, int n_rows, int n_cols) {
 }
 
 static int g_init = 0;
+
+// side stream (highest priority) for the tier-2 pipeline of queue A, and its
+// fork / join events (captured into the evolve graph like any stream work)
+static cudaStream_t g_side = nullptr;
+static cudaEvent_t g_fork, g_join;
+
+// FT_PROBE_EVENTS=1 (timing probes only): events at the stage boundaries of
+// the last launch_step, read with ft_probe_timeline (debug export)
+static cudaEvent_t g_pev[8];
+static int g_pev_on = -1;
+
+static void pev(int i, cudaStream_t st) {
+    if (g_pev_on < 0) {
+        const char* e = getenv("FT_PROBE_EVENTS");
+        g_pev_on = e && atoi(e) ? 1 : 0;
+        if (g_pev_on)
+            for (auto& ev : g_pev) cudaEventCreate(&ev);
+    }
+    if (g_pev_on) cudaEventRecord(g_pev[i], st);
+}
+
+extern "C" int ft_probe_timeline(float* ms, int n) {
+    if (g_pev_on != 1) return FT_ERR_ARG;
+    cudaDeviceSynchronize();
+    for (int i = 0; i < n && i < 8; ++i) ms[i] = -1.0f;
+    for (int i = 1; i < n && i < 8; ++i)
+        if (cudaEventElapsedTime(&ms[i], g_pev[0], g_pev[i]) != cudaSuccess) ms[i] = -1.0f;
+    ms[0] = 0.0f;
+    cudaGetLastError();
+    return FT_OK;
+}
+
+static int side_init() {
+    if (g_side) return FT_OK;
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&g_side, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_join, cudaEventDisableTiming) != cudaSuccess) {
+        g_side = nullptr;
+        return FT_ERR_CUDA;
+    }
+    return FT_OK;
+}
 static int g_fixup_grid = 4 * 148;
 static int g_fin_ctas = 4 * 148;   // finalize: ~one tile per thread at C3, <= FT_FIN_MAX
 
@@ -1698,18 +2046,39 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
     lib_init();
     p.force_check = (lap_flags & FT_LAP_CHECK_FINITE) != 0;
     p.report_ids = dom ? dom->report_ids : nullptr;
-    if (which & 1) FT_PICK3(ft::tier1_kernel, dtype, uni, packed)<<<p.num_tiles, FT_TPB, 0, s>>>(p);
+    if (which & 1) {
+        pev(0, s);
+        FT_PICK3(ft::tier1_kernel, dtype, uni, packed)<<<p.num_tiles, FT_TPB, 0, s>>>(p);
+    }
     if (which & 2) {
         // FT_PROBE_FIXUP (timing probes only, results invalid): bit mask of
-        // the tier-1.5 / 2a / 2b / 3 launches
+        // the tier-1.5 / 2a / 2b / 3 launches; 32 skips queue A
         static const char* probe = getenv("FT_PROBE_FIXUP");
         const int m = probe ? atoi(probe) : 15;
+        // queue A (tier 1's wide columns) on the high-priority side stream,
+        // concurrently with tier 1.5
+        if (side_init() != FT_OK) return cuda_check("side stream");
+        const ft::Queues qa = ft::queues(p, 0), qb = ft::queues(p, 1);
+        cudaEventRecord(g_fork, s);
+        cudaStreamWaitEvent(g_side, g_fork, 0);
+        const bool pa = !(m & 32);   // probe: skip queue A
+        ft::queue_kernel<<<(FT_WARPS * p.num_tiles + 255) / 256, 256, 0, g_side>>>(p);
+        if ((m & 2) && pa) FT_PICK3(ft::wide3_kernel, dtype, uni, packed)<<<g_fixup_grid, FT_TPB, 0, g_side>>>(p, qa);
+        pev(3, g_side);
+        if ((m & 4) && pa) FT_PICK2(ft::wide_kernel, dtype, uni)<<<g_fixup_grid, FT_TPB, 0, g_side>>>(p, qa);
+        if ((m & 8) && pa) FT_PICK2(ft::deep_kernel, dtype, uni)<<<g_fixup_grid / 4, FT_TPB, 0, g_side>>>(p, qa);
+        pev(4, g_side);
+        cudaEventRecord(g_join, g_side);
         // tier 1.5, one warp per tile
         if (m & 1)
             FT_PICK3(ft::gen_kernel, dtype, uni, packed)<<<(p.num_tiles + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
-        if (m & 2) FT_PICK3(ft::wide3_kernel, dtype, uni, packed)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
-        if (m & 4) FT_PICK2(ft::wide_kernel, dtype, uni)<<<g_fixup_grid, FT_TPB, 0, s>>>(p);
-        if (m & 8) FT_PICK2(ft::deep_kernel, dtype, uni)<<<g_fixup_grid / 4, FT_TPB, 0, s>>>(p);
+        pev(5, s);
+        // queue B: what tier 1.5 defers (unions of three or more rows), one
+        // warp per column
+        if (m & 2) FT_PICK2(ft::warp_kernel, dtype, uni)<<<g_fixup_grid * 4, FT_TPB, 0, s>>>(p, qb.q, qb.q_n, qb.dir);
+        pev(6, s);
+        cudaStreamWaitEvent(s, g_join, 0);
+        pev(7, s);
     }
     return cuda_check("step kernel");
 }

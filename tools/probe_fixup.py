@@ -47,3 +47,25 @@ for i in range(30):
         t.append([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])])
 t = np.median(np.array(t), axis=0) * 1e3
 print(f"mask {os.environ.get('FT_PROBE_FIXUP', '15')}: tier1 {t[0]:.1f} us  fixup {t[1]:.1f} us  finalize {t[2]:.1f} us")
+
+# tier populations of this state: masks after tier 1, queue after tier 1.5
+def al(x):
+    return (x + 15) & ~15
+nt = (n_v + 127) // 128
+ns = 4 * nt
+off = 128
+off_gen = al(al(al(off + ns * 8) + ns * 8) + ns * 8)
+off_slow = al(off_gen + ns * 4)
+os.environ["FT_PROBE_FIXUP"] = "0"
+assert lib.ft_step_kernel(ctypes.byref(lc), fl, ctypes.byref(bc), ctypes.byref(ac), 0, ctypes.byref(prm), wp, wn, st) == 0
+torch.cuda.synchronize()
+raw = ws.ws.cpu().numpy()
+gm = raw[off_gen:off_gen + ns * 4].view(np.uint32)
+sm = raw[off_slow:off_slow + ns * 4].view(np.uint32)
+pc = lambda a: int(np.unpackbits(a.view(np.uint8)).sum())
+print(f"tier-1.5 columns {pc(gm)}  tier-1 slow columns {pc(sm)}  tiles with gen {int((gm.reshape(-1, 4).any(1)).sum())} of {nt}")
+assert lib.ft_step_fixup(ctypes.byref(lc), fl, ctypes.byref(bc), ctypes.byref(ac), 0, ctypes.byref(prm), wp, wn, st) == 0
+torch.cuda.synchronize()
+c = ws.ws[:128].cpu().numpy()
+i32 = lambda o: int(c[o:o + 4].view(np.int32)[0])
+print(f"tier-2 queue A {i32(56)} B (tier-1.5 deferred) {i32(68)}  tier-2b {i32(96)}  tier-3 {i32(64)}  pool {int(c[40:48].view(np.int64)[0])}")
