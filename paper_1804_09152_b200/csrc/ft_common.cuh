@@ -42,7 +42,7 @@ struct Control {
 };
 static_assert(sizeof(Control) % 16 == 0, "Control must stay 16B aligned");
 
-#define FT_FIN_MAX 1024   // finalize CTAs at most (partials in the workspace)
+#define FT_FIN_MAX 4096   // finalize CTAs at most (partials in the workspace)
 
 // Statistics are kept per 32-column segment (one warp of tier 1) and per
 // 128-column tile (one warp of tier 1.5), so no kernel needs a CTA barrier

@@ -762,10 +762,13 @@ __global__ void __launch_bounds__(FT_TPB, 8) tier1_kernel(const StepParams p) {
     const unsigned int fb = __ballot_sync(0xffffffffu, fast);
     const unsigned int gb = __ballot_sync(0xffffffffu, gen);
     const unsigned int wb = __ballot_sync(0xffffffffu, slow);
-    bm = warp_sum(bm);      // fixed shuffle tree: deterministic
-    cnt = warp_sum(cnt);
+    cnt = __popc(__ballot_sync(0xffffffffu, cnt != 0));
+    // cell interiors at rest give bm = md = 0: skip the shuffle trees then
+    if (__any_sync(0xffffffffu, bm != 0.0)) bm = warp_sum(bm);      // fixed tree: deterministic
+    if (__any_sync(0xffffffffu, md != 0.0)) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_down_sync(0xffffffffu, md, o));
+        for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_down_sync(0xffffffffu, md, o));
+    }
     if (lane == 0) {
         const int seg = tile * FT_WARPS + warp;
         p.ws.seg_bm[seg] = bm;
@@ -1510,39 +1513,35 @@ __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizePara
     __shared__ double s_part[FT_FIN_TPB / 32];
     __shared__ int s_last;
     const int tid = threadIdx.x;
-    const int nt = f.ws.num_tiles;
-    const int per = (nt + gridDim.x - 1) / gridDim.x;
-    const int t0 = blockIdx.x * per, t1 = min(nt, t0 + per);
+    // one thread per 32-column segment, a fixed range of segments per CTA;
+    // the segment's value: its tier-1 sum, its tier-2/3 columns in vertex
+    // order, and (first segment of a tile) the tile's tier-1.5 sum
+    const int ns = FT_WARPS * f.ws.num_tiles;
+    const int per = ((ns + gridDim.x - 1) / gridDim.x + FT_FIN_TPB - 1) / FT_FIN_TPB * FT_FIN_TPB;
+    const int s0 = blockIdx.x * per, s1 = min(ns, s0 + per);
     double acc = 0.0, amx = 0.0;
     long long acnt = 0, askel = 0;
-    for (int t = t0 + tid; t < t1; t += FT_FIN_TPB) {
-        const uint4 g4 = *reinterpret_cast<const uint4*>(&f.ws.gen_mask[(size_t)t * FT_WARPS]);
-        const uint4 m4 = *reinterpret_cast<const uint4*>(&f.ws.slow_mask[(size_t)t * FT_WARPS]);
-        const unsigned int mw[4] = {m4.x, m4.y, m4.z, m4.w};
-        double tb = 0.0;
-#pragma unroll
-        for (int k = 0; k < FT_WARPS; ++k) {
-            const int s = t * FT_WARPS + k;
-            tb = tb + f.ws.seg_bm[s];
-            amx = fmax(amx, f.ws.seg_maxd[s]);
-            const int2 cs = f.ws.seg_cs[s];
-            acnt += cs.x;
-            askel += cs.y;
+    for (int sg = s0 + tid; sg < s1; sg += FT_FIN_TPB) {
+        double tb = f.ws.seg_bm[sg];
+        amx = fmax(amx, f.ws.seg_maxd[sg]);
+        const int2 cs = f.ws.seg_cs[sg];
+        acnt += cs.x;
+        askel += cs.y;
+        unsigned int m = f.ws.slow_mask[sg];
+        while (m) {   // tier-2/3 columns of the segment, in vertex order
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            tb = tb + f.ws.vbm[(size_t)sg * 32 + b];
         }
-        if (g4.x | g4.y | g4.z | g4.w) {
-            tb = tb + f.ws.gen_bm[t];
-            amx = fmax(amx, f.ws.gen_maxd[t]);
-            const int2 cs = f.ws.gen_cs[t];
-            acnt += cs.x;
-            askel += cs.y;
-        }
-#pragma unroll
-        for (int k = 0; k < FT_WARPS; ++k) {
-            unsigned int m = mw[k];
-            while (m) {   // tier-2/3 columns of the tile, in vertex order
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                tb = tb + f.ws.vbm[(size_t)t * FT_TPB + k * 32 + b];
+        if ((sg & (FT_WARPS - 1)) == 0) {
+            const int t = sg / FT_WARPS;
+            const uint4 g4 = *reinterpret_cast<const uint4*>(&f.ws.gen_mask[(size_t)t * FT_WARPS]);
+            if (g4.x | g4.y | g4.z | g4.w) {
+                tb = tb + f.ws.gen_bm[t];
+                amx = fmax(amx, f.ws.gen_maxd[t]);
+                const int2 gc = f.ws.gen_cs[t];
+                acnt += gc.x;
+                askel += gc.y;
             }
         }
         acc = acc + tb;
@@ -1986,7 +1985,6 @@ static int side_init() {
     return FT_OK;
 }
 static int g_fixup_grid = 4 * 148;
-static int g_fin_ctas = 4 * 148;   // finalize: ~one tile per thread at C3, <= FT_FIN_MAX
 
 static void lib_init() {
     if (g_init) return;
@@ -1999,7 +1997,6 @@ static void lib_init() {
     if (cudaGetDevice(&dev) == cudaSuccess &&
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
         g_fixup_grid = 4 * sms;
-    g_fin_ctas = 4 * sms < FT_FIN_MAX ? 4 * sms : FT_FIN_MAX;
 }
 
 // which = 1: tier 1, 2: tiers 1.5-3, 3: both
@@ -2089,7 +2086,10 @@ static void launch_finalize(const ft::Workspace& ws, ft_step_stats* trace, long 
     f.ws = ws; f.trace = trace; f.tiled_cap = tiled_cap; f.fixed_slot = evolve ? 0 : 1;
     f.evolve = evolve; f.max_steps = max_steps; f.tol = tol; f.base_threshold = thr;
     lib_init();
-    ft::finalize_kernel<<<g_fin_ctas, FT_FIN_TPB, 0, s>>>(f);
+    // about one 32-column segment per thread
+    int ctas = (FT_WARPS * ws.num_tiles + FT_FIN_TPB - 1) / FT_FIN_TPB;
+    ctas = ctas < 1 ? 1 : (ctas > FT_FIN_MAX ? FT_FIN_MAX : ctas);
+    ft::finalize_kernel<<<ctas, FT_FIN_TPB, 0, s>>>(f);
 }
 
 static int launch_convert(const ft_csc* src, ft_tiled* dst, int32_t dtype, const ft::Workspace& ws,
