@@ -669,6 +669,37 @@ __device__ __forceinline__ int load_lrow(const StepParams& p, int jl, int j, boo
     return n;
 }
 
+// load_lrow with the packed row already loaded (PACKED), else the CSR
+template <bool PACKED>
+__device__ __forceinline__ int unpack_lrow(const StepParams& p, int4 pk, int jl, int j, bool active, int (&u)[kMD],
+                                           int& q0) {
+    int n = 0;
+    q0 = 0;
+    bool csr = !PACKED;
+    if (PACKED) {
+        const int w4[4] = {pk.x, pk.y, pk.z, pk.w};
+#pragma unroll
+        for (int k = 0; k < kMD; ++k) {
+            const int s = (k & 1) ? (w4[k >> 1] >> 16) : ((int)(w4[k >> 1] << 16) >> 16);
+            const bool valid = active && s != kPackEmpty;
+            u[k] = valid ? j + s : -1;
+            n += valid ? 1 : 0;
+        }
+        csr = active && n == 0;
+    }
+    if (csr && active) {
+        q0 = __ldg(&p.lap_ptr[jl]);
+        n = __ldg(&p.lap_ptr[jl + 1]) - q0;
+        if (n > kMD || n < 1) n = 0;
+#pragma unroll
+        for (int k = 0; k < kMD; ++k) u[k] = (k < n) ? __ldg(&p.lap_idx[q0 + k]) : -1;
+    } else if (!PACKED) {
+#pragma unroll
+        for (int k = 0; k < kMD; ++k) u[k] = -1;
+    }
+    return n;
+}
+
 template <typename T, bool UNIFORM>
 __device__ __forceinline__ double lap_value(const StepParams& p, int k, int kd, int q0, double invdeg) {
     return UNIFORM ? ((k == kd) ? -1.0 : invdeg) : ldv<T>(p.lap_val, q0 + k);
@@ -690,19 +721,18 @@ __device__ __forceinline__ double recip_deg(int n) { return n - 1 <= 32 ? c_reci
 // a raised flag switch the check on).  One warp = one 32-column segment:
 // statistics and masks go to the segment's slots, no CTA barrier.
 
+// one 32-column segment (one warp), the packed L row and the column's value
+// already loaded (prefetched by the caller)
 template <typename T, bool UNIFORM, bool PACKED>
-__global__ void __launch_bounds__(FT_TPB, 8) tier1_kernel(const StepParams p) {
-    if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
-    const bool chk = p.force_check || *(volatile unsigned int*)&p.ws.ctl->nonfinite;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tile = blockIdx.x;
-    const int jl = tile * FT_TPB + threadIdx.x;
+__device__ __forceinline__ void tier1_segment(const StepParams& p, int seg, int lane, bool chk, int4 pk,
+                                              double phs) {
+    const int jl = seg * 32 + lane;
     const int j = p.j_base + jl;
     const bool active = jl < p.n_v;
 
     int q0 = 0;
     int u[kMD];
-    const int n = load_lrow<PACKED>(p, jl, j, active, u, q0);
+    const int n = unpack_lrow<PACKED>(p, pk, jl, j, active, u, q0);
     bool wide = active && n == 0;
     int kd = -1;
 #pragma unroll
@@ -712,7 +742,6 @@ __global__ void __launch_bounds__(FT_TPB, 8) tier1_kernel(const StepParams p) {
     int sg[kMD];
 #pragma unroll
     for (int k = 0; k < kMD; ++k) sg[k] = (k < n) ? __ldg(&p.in.sig[u[k]]) : FT_SIG_EMPTY;
-    const double phs = active ? ldv<T>(p.in.v0, j) : 0.0;
     int rs = FT_SIG_EMPTY;
 #pragma unroll
     for (int k = 0; k < kMD; ++k)
@@ -770,12 +799,45 @@ __global__ void __launch_bounds__(FT_TPB, 8) tier1_kernel(const StepParams p) {
         for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_down_sync(0xffffffffu, md, o));
     }
     if (lane == 0) {
-        const int seg = tile * FT_WARPS + warp;
         p.ws.seg_bm[seg] = bm;
         p.ws.seg_maxd[seg] = md;
         p.ws.seg_cs[seg] = make_int2(cnt, __popc(fb));
         p.ws.gen_mask[seg] = gb;
         p.ws.slow_mask[seg] = wb;
+    }
+}
+
+// persistent: each warp walks segments seg, seg + (warps in the grid), ...,
+// loading the next segment's packed L row and value while it classifies
+// the current one (two segments of loads in flight per warp)
+template <typename T, bool UNIFORM, bool PACKED>
+__global__ void __launch_bounds__(FT_TPB, 8) tier1_kernel(const StepParams p) {
+    if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
+    const bool chk = p.force_check || *(volatile unsigned int*)&p.ws.ctl->nonfinite;
+    const int lane = threadIdx.x & 31;
+    const int nseg = FT_WARPS * p.num_tiles;
+    const int nw = gridDim.x * FT_WARPS;
+    int seg = (blockIdx.x * FT_TPB + threadIdx.x) >> 5;
+    int4 pk = make_int4(0, 0, 0, 0);
+    double phs = 0.0;
+    {
+        const int jl = seg * 32 + lane;
+        if (seg < nseg && jl < p.n_v) {
+            if (PACKED) pk = __ldg(&p.lap_pack[jl]);
+            phs = ldv<T>(p.in.v0, p.j_base + jl);
+        }
+    }
+    for (; seg < nseg; seg += nw) {
+        int4 pk2 = make_int4(0, 0, 0, 0);
+        double ph2 = 0.0;
+        const int jl2 = (seg + nw) * 32 + lane;
+        if (seg + nw < nseg && jl2 < p.n_v) {
+            if (PACKED) pk2 = __ldg(&p.lap_pack[jl2]);
+            ph2 = ldv<T>(p.in.v0, p.j_base + jl2);
+        }
+        tier1_segment<T, UNIFORM, PACKED>(p, seg, lane, chk, pk, phs);
+        pk = pk2;
+        phs = ph2;
     }
 }
 
@@ -817,6 +879,207 @@ __device__ __forceinline__ long long pool_place(int need, const VRes& res, const
         if (nnz) atomicAdd(&p.ws.ctl->nnz_total, (unsigned long long)nnz);
     }
     return base + incl - need;
+}
+
+// ---------------------------------------------------------------------------
+// warp-cooperative column (the wide tail: tier-2a leftovers, tier-1.5
+// deferrals).  One warp per column: lane e holds entry e of the
+// neighbourhood (neighbours in L order, rows ascending within one), lanes
+// with equal rows are grouped with __match_any_sync, and every sum is taken
+// in the reference's order -- Lt(r, j) over the entries in L order
+// (_kernels.py:36-50), the skeleton aggregates and the normaliser in
+// ascending row order (_kernels.py:179-282) -- by shuffles, so the result is
+// bitwise that of process_window / vertex_slow.  Neighbourhoods of more
+// than 32 entries (or 32 L entries) take vertex_slow in lane 0.
+
+struct WarpStats {
+    double maxd;
+    long long cnt, skel;
+};
+
+template <typename T, bool UNIFORM>
+__device__ __forceinline__ void warp_column(int j, const StepParams& p, int lane, WarpStats& ws) {
+    const unsigned int full = 0xffffffffu;
+    const int jl = j - p.j_base;
+    const int q0 = __ldg(&p.lap_ptr[jl]);
+    const int n = __ldg(&p.lap_ptr[jl + 1]) - q0;
+    int u = -1, sgk = FT_SIG_EMPTY, axk = 0, ck = 0;
+    double lk = 0.0;
+    if (lane < n && n <= 32) {
+        u = __ldg(&p.lap_idx[q0 + lane]);
+        sgk = __ldg(&p.in.sig[u]);
+        ck = sig_count(sgk);
+        axk = ck >= 2 ? __ldg(&p.in.aux[u]) : 0;
+    }
+    const unsigned int dmask = __ballot_sync(full, lane < n && u == j);
+    const int kd = dmask ? __ffs(dmask) - 1 : -1;
+    if (lane < n && n <= 32) {
+        if (UNIFORM) lk = (lane == kd) ? -1.0 : 1.0 / (double)(n - 1);
+        else lk = ldv<T>(p.lap_val, q0 + lane);
+    }
+    // entry offsets: exclusive scan of the counts over the L entries
+    int incl = ck;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(full, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int E = __shfl_sync(full, incl, 31);
+    if (n > 32 || n < 1 || kd < 0 || E > 32) {
+        // general fallback in lane 0 (statistics through the atomics)
+        if (lane == 0) {
+            VRes res;
+            vres_init(res);
+            vertex_slow<T, 8, UNIFORM>(j, p, res, 0, false);
+            report_flags(res, j, p);
+            long long off = 0;
+            bool ok = true;
+            if (res.cnt > 2) {
+                off = (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)res.cnt);
+                if (off + res.cnt > p.cap) { atomicExch(&p.ws.ctl->overflow, 1); ok = false; }
+            }
+            p.ws.vbm[jl] = res.bm;
+            if (ok) { VRes r2 = res; vertex_slow<T, 8, UNIFORM>(j, p, r2, off, true); }
+            ws.maxd = fmax(ws.maxd, res.maxd);
+            ws.cnt += res.cnt;
+            ws.skel += res.nskel;
+        }
+        return;
+    }
+    const int e0k = incl - ck;
+    // this lane's entry: owner neighbour k (entries are k-major) and index t
+    int myk = 0, t = 0;
+    for (int k = 0; k < n; ++k) {
+        const int a = __shfl_sync(full, e0k, k), c = __shfl_sync(full, ck, k);
+        if (lane >= a && lane < a + c) { myk = k; t = lane - a; }
+    }
+    const int su = __shfl_sync(full, u, myk), ss = __shfl_sync(full, sgk, myk), sa = __shfl_sync(full, axk, myk);
+    const double sl = __shfl_sync(full, lk, myk);
+    const bool valid = lane < E;
+    int r = -1 - lane;                // unique key for lanes without an entry
+    double v = 0.0;
+    if (valid) {
+        r = hyb_row<T>(p.in, ss, sa, t);
+        v = hyb_val<T>(p.in, su, ss, sa, t);
+    }
+    const double prod = v * sl;       // PHI(r, u) * L(j, u)
+    const bool dg = valid && myk == kd;
+    const unsigned int grp = __match_any_sync(full, r);
+    const bool leader = valid && (__ffs(grp) - 1) == lane;
+    // Lt(r, j) in L order, PHI(r, j) from the diagonal neighbour, and the
+    // row rank among the distinct rows
+    double lam = 0.0, ph = 0.0;
+    int rank = 0;
+    for (int src = 0; src < E; ++src) {
+        const double pv = __shfl_sync(full, prod, src);
+        const double vv = __shfl_sync(full, v, src);
+        const int rr = __shfl_sync(full, r, src);
+        const bool ds = __shfl_sync(full, dg, src);
+        const bool ls = __shfl_sync(full, leader, src);
+        if ((grp >> src) & 1u) {
+            lam = lam + pv;
+            if (ds) ph = vv;
+        }
+        if (ls && rr < r) ++rank;
+    }
+    const int m = __popc(__ballot_sync(full, leader));
+    const bool in = leader && in_skeleton(ph, lam);
+    int bad_phi = (leader && ph != 0.0 && !in) ? r : -1;
+    int bad_lt = (leader && lam != 0.0 && !in) ? r : -1;
+    const double lh = (lam != 0.0) ? lam : 0.0;
+    const double sq = in ? sqrt(ph) : 0.0;
+    // aggregates over the skeleton rows in ascending row order
+    Agg g;
+    agg_init(g);
+    for (int q = 0; q < m; ++q) {
+        const int lq = __ffs(__ballot_sync(full, leader && rank == q)) - 1;
+        const bool iq = __shfl_sync(full, in, lq);
+        const double phq = __shfl_sync(full, ph, lq), lhq = __shfl_sync(full, lh, lq), sqq = __shfl_sync(full, sq, lq);
+        const int rq = __shfl_sync(full, r, lq);
+        if (iq) {
+            if (g.n == 0) { g.first_row = rq; g.phi0 = phq; }
+            g.n++;
+            g.sl = g.sl + lhq;
+            g.sp = g.sp + phq;
+            g.sr = g.sr + sqq;
+        }
+    }
+    bool nan = false;
+    double vn = 0.0;
+    double s = 0.0;
+    if (g.n > 0) {
+        const Coef c = make_coef(g, p, c_recip);
+        if (in) vn = update_entry_sq(r, ph, lh, sq, c, p, nan);
+        for (int q = 0; q < m; ++q) {
+            const int lq = __ffs(__ballot_sync(full, leader && rank == q)) - 1;
+            const bool iq = __shfl_sync(full, in, lq);
+            const double vq = __shfl_sync(full, vn, lq);
+            if (iq) s = s + vq;
+        }
+    }
+    const bool spos = s > 0.0;
+    const double inv = spos ? 1.0 / s : 0.0;
+    const double nv = spos ? vn * inv : vn;
+    const bool out = in && nv != 0.0;
+    const unsigned int ob = __ballot_sync(full, out);
+    const int cnt = __popc(ob);
+    int pos = 0;       // rank among the output rows
+    for (int src = 0; src < E; ++src) {
+        const bool os = __shfl_sync(full, out, src);
+        const int rk = __shfl_sync(full, rank, src);
+        if (os && rk < rank) ++pos;
+    }
+    // statistics and error reports of the column
+    double bm = (out && r == 0) ? nv : 0.0;
+    double dd = in ? fabs(nv - ph) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        bm = bm + __shfl_xor_sync(full, bm, o);   // at most one nonzero term: exact
+        dd = fmax(dd, __shfl_xor_sync(full, dd, o));
+        bad_phi = max(bad_phi, __shfl_xor_sync(full, bad_phi, o));
+        bad_lt = max(bad_lt, __shfl_xor_sync(full, bad_lt, o));
+    }
+    const bool anynan = __any_sync(full, nan);
+    const int nskel = __popc(__ballot_sync(full, in));
+    if (lane == 0) {
+        VRes res;
+        vres_init(res);
+        res.nan = anynan; res.bad_phi_row = bad_phi; res.bad_lt_row = bad_lt;
+        report_flags(res, j, p);
+        p.ws.vbm[jl] = bm;
+        ws.maxd = fmax(ws.maxd, dd);
+        ws.cnt += cnt;
+        ws.skel += nskel;
+    }
+    // output: dense for at most two rows, else a pool range
+    if (cnt <= 2) {
+        if (cnt == 0) {
+            if (lane == 0) p.out.sig[j] = FT_SIG_EMPTY;
+        } else if (out) {
+            if (pos == 0) {
+                p.out.sig[j] = cnt == 2 ? (r | kPair) : r;
+                ((T*)p.out.v0)[j] = (T)nv;
+            } else {
+                p.out.aux[j] = r;
+                ((T*)p.out.v1)[j] = (T)nv;
+            }
+            if (!isfinite(nv)) atomicOr(&p.ws.ctl->nonfinite, 1u);
+        }
+        return;
+    }
+    long long off = 0;
+    if (lane == 0) off = (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)cnt);
+    off = __shfl_sync(full, off, 0);
+    if (off + cnt > p.cap) {
+        if (lane == 0) atomicExch(&p.ws.ctl->overflow, 1);
+        return;
+    }
+    if (lane == 0) { p.out.sig[j] = -cnt; p.out.aux[j] = (int)off; }
+    if (out) {
+        p.out.pidx[off + pos] = r;
+        ((T*)p.out.pval)[off + pos] = (T)nv;
+        if (!isfinite(nv)) atomicOr(&p.ws.ctl->nonfinite, 1u);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1209,207 +1472,6 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p, con
     }
 }
 
-
-// ---------------------------------------------------------------------------
-// warp-cooperative column (the wide tail: tier-2a leftovers, tier-1.5
-// deferrals).  One warp per column: lane e holds entry e of the
-// neighbourhood (neighbours in L order, rows ascending within one), lanes
-// with equal rows are grouped with __match_any_sync, and every sum is taken
-// in the reference's order -- Lt(r, j) over the entries in L order
-// (_kernels.py:36-50), the skeleton aggregates and the normaliser in
-// ascending row order (_kernels.py:179-282) -- by shuffles, so the result is
-// bitwise that of process_window / vertex_slow.  Neighbourhoods of more
-// than 32 entries (or 32 L entries) take vertex_slow in lane 0.
-
-struct WarpStats {
-    double maxd;
-    long long cnt, skel;
-};
-
-template <typename T, bool UNIFORM>
-__device__ __forceinline__ void warp_column(int j, const StepParams& p, int lane, WarpStats& ws) {
-    const unsigned int full = 0xffffffffu;
-    const int jl = j - p.j_base;
-    const int q0 = __ldg(&p.lap_ptr[jl]);
-    const int n = __ldg(&p.lap_ptr[jl + 1]) - q0;
-    int u = -1, sgk = FT_SIG_EMPTY, axk = 0, ck = 0;
-    double lk = 0.0;
-    if (lane < n && n <= 32) {
-        u = __ldg(&p.lap_idx[q0 + lane]);
-        sgk = __ldg(&p.in.sig[u]);
-        ck = sig_count(sgk);
-        axk = ck >= 2 ? __ldg(&p.in.aux[u]) : 0;
-    }
-    const unsigned int dmask = __ballot_sync(full, lane < n && u == j);
-    const int kd = dmask ? __ffs(dmask) - 1 : -1;
-    if (lane < n && n <= 32) {
-        if (UNIFORM) lk = (lane == kd) ? -1.0 : 1.0 / (double)(n - 1);
-        else lk = ldv<T>(p.lap_val, q0 + lane);
-    }
-    // entry offsets: exclusive scan of the counts over the L entries
-    int incl = ck;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(full, incl, o);
-        if (lane >= o) incl += y;
-    }
-    const int E = __shfl_sync(full, incl, 31);
-    if (n > 32 || n < 1 || kd < 0 || E > 32) {
-        // general fallback in lane 0 (statistics through the atomics)
-        if (lane == 0) {
-            VRes res;
-            vres_init(res);
-            vertex_slow<T, 8, UNIFORM>(j, p, res, 0, false);
-            report_flags(res, j, p);
-            long long off = 0;
-            bool ok = true;
-            if (res.cnt > 2) {
-                off = (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)res.cnt);
-                if (off + res.cnt > p.cap) { atomicExch(&p.ws.ctl->overflow, 1); ok = false; }
-            }
-            p.ws.vbm[jl] = res.bm;
-            if (ok) { VRes r2 = res; vertex_slow<T, 8, UNIFORM>(j, p, r2, off, true); }
-            ws.maxd = fmax(ws.maxd, res.maxd);
-            ws.cnt += res.cnt;
-            ws.skel += res.nskel;
-        }
-        return;
-    }
-    const int e0k = incl - ck;
-    // this lane's entry: owner neighbour k (entries are k-major) and index t
-    int myk = 0, t = 0;
-    for (int k = 0; k < n; ++k) {
-        const int a = __shfl_sync(full, e0k, k), c = __shfl_sync(full, ck, k);
-        if (lane >= a && lane < a + c) { myk = k; t = lane - a; }
-    }
-    const int su = __shfl_sync(full, u, myk), ss = __shfl_sync(full, sgk, myk), sa = __shfl_sync(full, axk, myk);
-    const double sl = __shfl_sync(full, lk, myk);
-    const bool valid = lane < E;
-    int r = -1 - lane;                // unique key for lanes without an entry
-    double v = 0.0;
-    if (valid) {
-        r = hyb_row<T>(p.in, ss, sa, t);
-        v = hyb_val<T>(p.in, su, ss, sa, t);
-    }
-    const double prod = v * sl;       // PHI(r, u) * L(j, u)
-    const bool dg = valid && myk == kd;
-    const unsigned int grp = __match_any_sync(full, r);
-    const bool leader = valid && (__ffs(grp) - 1) == lane;
-    // Lt(r, j) in L order, PHI(r, j) from the diagonal neighbour, and the
-    // row rank among the distinct rows
-    double lam = 0.0, ph = 0.0;
-    int rank = 0;
-    for (int src = 0; src < E; ++src) {
-        const double pv = __shfl_sync(full, prod, src);
-        const double vv = __shfl_sync(full, v, src);
-        const int rr = __shfl_sync(full, r, src);
-        const bool ds = __shfl_sync(full, dg, src);
-        const bool ls = __shfl_sync(full, leader, src);
-        if ((grp >> src) & 1u) {
-            lam = lam + pv;
-            if (ds) ph = vv;
-        }
-        if (ls && rr < r) ++rank;
-    }
-    const int m = __popc(__ballot_sync(full, leader));
-    const bool in = leader && in_skeleton(ph, lam);
-    int bad_phi = (leader && ph != 0.0 && !in) ? r : -1;
-    int bad_lt = (leader && lam != 0.0 && !in) ? r : -1;
-    const double lh = (lam != 0.0) ? lam : 0.0;
-    const double sq = in ? sqrt(ph) : 0.0;
-    // aggregates over the skeleton rows in ascending row order
-    Agg g;
-    agg_init(g);
-    for (int q = 0; q < m; ++q) {
-        const int lq = __ffs(__ballot_sync(full, leader && rank == q)) - 1;
-        const bool iq = __shfl_sync(full, in, lq);
-        const double phq = __shfl_sync(full, ph, lq), lhq = __shfl_sync(full, lh, lq), sqq = __shfl_sync(full, sq, lq);
-        const int rq = __shfl_sync(full, r, lq);
-        if (iq) {
-            if (g.n == 0) { g.first_row = rq; g.phi0 = phq; }
-            g.n++;
-            g.sl = g.sl + lhq;
-            g.sp = g.sp + phq;
-            g.sr = g.sr + sqq;
-        }
-    }
-    bool nan = false;
-    double vn = 0.0;
-    double s = 0.0;
-    if (g.n > 0) {
-        const Coef c = make_coef(g, p, c_recip);
-        if (in) vn = update_entry_sq(r, ph, lh, sq, c, p, nan);
-        for (int q = 0; q < m; ++q) {
-            const int lq = __ffs(__ballot_sync(full, leader && rank == q)) - 1;
-            const bool iq = __shfl_sync(full, in, lq);
-            const double vq = __shfl_sync(full, vn, lq);
-            if (iq) s = s + vq;
-        }
-    }
-    const bool spos = s > 0.0;
-    const double inv = spos ? 1.0 / s : 0.0;
-    const double nv = spos ? vn * inv : vn;
-    const bool out = in && nv != 0.0;
-    const unsigned int ob = __ballot_sync(full, out);
-    const int cnt = __popc(ob);
-    int pos = 0;       // rank among the output rows
-    for (int src = 0; src < E; ++src) {
-        const bool os = __shfl_sync(full, out, src);
-        const int rk = __shfl_sync(full, rank, src);
-        if (os && rk < rank) ++pos;
-    }
-    // statistics and error reports of the column
-    double bm = (out && r == 0) ? nv : 0.0;
-    double dd = in ? fabs(nv - ph) : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        bm = bm + __shfl_xor_sync(full, bm, o);   // at most one nonzero term: exact
-        dd = fmax(dd, __shfl_xor_sync(full, dd, o));
-        bad_phi = max(bad_phi, __shfl_xor_sync(full, bad_phi, o));
-        bad_lt = max(bad_lt, __shfl_xor_sync(full, bad_lt, o));
-    }
-    const bool anynan = __any_sync(full, nan);
-    const int nskel = __popc(__ballot_sync(full, in));
-    if (lane == 0) {
-        VRes res;
-        vres_init(res);
-        res.nan = anynan; res.bad_phi_row = bad_phi; res.bad_lt_row = bad_lt;
-        report_flags(res, j, p);
-        p.ws.vbm[jl] = bm;
-        ws.maxd = fmax(ws.maxd, dd);
-        ws.cnt += cnt;
-        ws.skel += nskel;
-    }
-    // output: dense for at most two rows, else a pool range
-    if (cnt <= 2) {
-        if (cnt == 0) {
-            if (lane == 0) p.out.sig[j] = FT_SIG_EMPTY;
-        } else if (out) {
-            if (pos == 0) {
-                p.out.sig[j] = cnt == 2 ? (r | kPair) : r;
-                ((T*)p.out.v0)[j] = (T)nv;
-            } else {
-                p.out.aux[j] = r;
-                ((T*)p.out.v1)[j] = (T)nv;
-            }
-            if (!isfinite(nv)) atomicOr(&p.ws.ctl->nonfinite, 1u);
-        }
-        return;
-    }
-    long long off = 0;
-    if (lane == 0) off = (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)cnt);
-    off = __shfl_sync(full, off, 0);
-    if (off + cnt > p.cap) {
-        if (lane == 0) atomicExch(&p.ws.ctl->overflow, 1);
-        return;
-    }
-    if (lane == 0) { p.out.sig[j] = -cnt; p.out.aux[j] = (int)off; }
-    if (out) {
-        p.out.pidx[off + pos] = r;
-        ((T*)p.out.pval)[off + pos] = (T)nv;
-        if (!isfinite(nv)) atomicOr(&p.ws.ctl->nonfinite, 1u);
-    }
-}
 
 // one warp per listed column (grid-stride); the warp's statistics go to
 // the global accumulators once
@@ -1985,6 +2047,7 @@ static int side_init() {
     return FT_OK;
 }
 static int g_fixup_grid = 4 * 148;
+static int g_sms = 148;
 
 static void lib_init() {
     if (g_init) return;
@@ -1995,8 +2058,10 @@ static void lib_init() {
     g_init = 1;
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess &&
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) {
         g_fixup_grid = 4 * sms;
+        g_sms = sms;
+    }
 }
 
 // which = 1: tier 1, 2: tiers 1.5-3, 3: both
@@ -2045,7 +2110,13 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
     p.report_ids = dom ? dom->report_ids : nullptr;
     if (which & 1) {
         pev(0, s);
-        FT_PICK3(ft::tier1_kernel, dtype, uni, packed)<<<p.num_tiles, FT_TPB, 0, s>>>(p);
+        const ft::StepKernelFn k1 = FT_PICK3(ft::tier1_kernel, dtype, uni, packed);
+        static int t1_ctas[2][2][2] = {};
+        int& per_sm = t1_ctas[dtype == FT_F64][uni][packed];
+        if (!per_sm && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, FT_TPB, 0) != cudaSuccess)
+            per_sm = 8;
+        const int grid = per_sm * g_sms < p.num_tiles ? per_sm * g_sms : p.num_tiles;
+        k1<<<grid, FT_TPB, 0, s>>>(p);
     }
     if (which & 2) {
         // FT_PROBE_FIXUP (timing probes only, results invalid): bit mask of

@@ -1,6 +1,6 @@
 """Per-source-line instruction counts / stall samples for one kernel.
 
-usage: python tools/sass_lines.py <report.ncu-rep> <lib-or-object> <mangled-kernel-substring> [top]
+usage: python tools/sass_lines.py <report.ncu-rep> <lib-or-object> <mangled-kernel-substring> [top] [demangled-substring]
 Joins ncu's SASS page (executed instructions, stall samples per SASS
 address) with nvdisasm -g line info of the same cubin.
 """
@@ -18,7 +18,9 @@ for r in rows:
         blocks.append(cur)
     elif cur is not None:
         cur["rows"].append(r)
-blk = next(b for b in blocks if kern in b["name"] or True)
+# the report block: 4th argument (a substring of the demangled name), else the first
+pick = sys.argv[5] if len(sys.argv) > 5 else None
+blk = next(b for b in blocks if (pick is None or pick in b["name"]))
 hdr = blk["rows"][0]
 idx = {k: i for i, k in enumerate(hdr)}
 data = blk["rows"][1:]
