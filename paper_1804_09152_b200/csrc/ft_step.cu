@@ -897,16 +897,29 @@ struct WarpStats {
     long long cnt, skel;
 };
 
-template <typename T, bool UNIFORM>
+template <typename T, bool UNIFORM, bool PACKED>
 __device__ __forceinline__ void warp_column(int j, const StepParams& p, int lane, WarpStats& ws) {
     const unsigned int full = 0xffffffffu;
     const int jl = j - p.j_base;
-    const int q0 = __ldg(&p.lap_ptr[jl]);
-    const int n = __ldg(&p.lap_ptr[jl + 1]) - q0;
+    int q0 = 0, n = 0, pu = -1;
+    if (PACKED) {
+        // lane k < 8 takes delta k of the packed row (one 16-byte load)
+        const int4 pk = __ldg(&p.lap_pack[jl]);
+        const int w = (lane >> 1) == 0 ? pk.x : ((lane >> 1) == 1 ? pk.y : ((lane >> 1) == 2 ? pk.z : pk.w));
+        const int d = (lane & 1) ? (w >> 16) : ((int)(w << 16) >> 16);
+        const bool valid = lane < kMD && d != kPackEmpty;
+        pu = valid ? j + d : -1;
+        n = __popc(__ballot_sync(full, valid));      // stored in order: valid slots lead
+    }
+    if (n == 0) {
+        q0 = __ldg(&p.lap_ptr[jl]);
+        n = __ldg(&p.lap_ptr[jl + 1]) - q0;
+        pu = -1;
+    }
     int u = -1, sgk = FT_SIG_EMPTY, axk = 0, ck = 0;
     double lk = 0.0;
     if (lane < n && n <= 32) {
-        u = __ldg(&p.lap_idx[q0 + lane]);
+        u = pu >= 0 ? pu : __ldg(&p.lap_idx[q0 + lane]);
         sgk = __ldg(&p.in.sig[u]);
         ck = sig_count(sgk);
         axk = ck >= 2 ? __ldg(&p.in.aux[u]) : 0;
@@ -915,7 +928,7 @@ __device__ __forceinline__ void warp_column(int j, const StepParams& p, int lane
     const int kd = dmask ? __ffs(dmask) - 1 : -1;
     if (lane < n && n <= 32) {
         if (UNIFORM) lk = (lane == kd) ? -1.0 : 1.0 / (double)(n - 1);
-        else lk = ldv<T>(p.lap_val, q0 + lane);
+        else lk = ldv<T>(p.lap_val, q0 + lane);     // (PACKED implies UNIFORM)
     }
     // entry offsets: exclusive scan of the counts over the L entries
     int incl = ck;
@@ -1475,7 +1488,7 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p, con
 
 // one warp per listed column (grid-stride); the warp's statistics go to
 // the global accumulators once
-template <typename T, bool UNIFORM>
+template <typename T, bool UNIFORM, bool PACKED>
 __global__ void __launch_bounds__(FT_TPB, 4) warp_kernel(const StepParams p, const int* list, const int* count, int dir) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     const int nc = *(volatile const int*)count;
@@ -1484,7 +1497,7 @@ __global__ void __launch_bounds__(FT_TPB, 4) warp_kernel(const StepParams p, con
     WarpStats ws;
     ws.maxd = 0.0; ws.cnt = 0; ws.skel = 0;
     for (int i = (blockIdx.x * FT_TPB + threadIdx.x) >> 5; i < nc; i += nw)
-        warp_column<T, UNIFORM>(__ldg(&list[dir * i]), p, lane, ws);
+        warp_column<T, UNIFORM, PACKED>(__ldg(&list[dir * i]), p, lane, ws);
     if (lane == 0 && (ws.maxd > 0.0 || ws.cnt || ws.skel)) {
         if (ws.maxd > 0.0) atomicMax(&p.ws.ctl->maxdelta_bits, (unsigned long long)__double_as_longlong(ws.maxd));
         if (ws.skel) atomicAdd(&p.ws.ctl->skel_total, (unsigned long long)ws.skel);
@@ -2143,7 +2156,7 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
         pev(5, s);
         // queue B: what tier 1.5 defers (unions of three or more rows), one
         // warp per column
-        if (m & 2) FT_PICK2(ft::warp_kernel, dtype, uni)<<<g_fixup_grid * 4, FT_TPB, 0, s>>>(p, qb.q, qb.q_n, qb.dir);
+        if (m & 2) FT_PICK3(ft::warp_kernel, dtype, uni, packed)<<<g_fixup_grid * 4, FT_TPB, 0, s>>>(p, qb.q, qb.q_n, qb.dir);
         pev(6, s);
         cudaStreamWaitEvent(s, g_join, 0);
         pev(7, s);
