@@ -890,7 +890,7 @@ __device__ __forceinline__ long long pool_place(int need, const VRes& res, const
 // (_kernels.py:36-50), the skeleton aggregates and the normaliser in
 // ascending row order (_kernels.py:179-282) -- by shuffles, so the result is
 // bitwise that of process_window / vertex_slow.  Neighbourhoods of more
-// than 32 entries (or 32 L entries) take vertex_slow in lane 0.
+// than 32 entries (or 32 L entries) go to the queue's tier-3 list.
 
 struct WarpStats {
     double maxd;
@@ -898,7 +898,7 @@ struct WarpStats {
 };
 
 template <typename T, bool UNIFORM, bool PACKED>
-__device__ __forceinline__ void warp_column(int j, const StepParams& p, int lane, WarpStats& ws) {
+__device__ __forceinline__ void warp_column(int j, const StepParams& p, const Queues& qs, int lane, WarpStats& ws) {
     const unsigned int full = 0xffffffffu;
     const int jl = j - p.j_base;
     int q0 = 0, n = 0, pu = -1;
@@ -939,23 +939,10 @@ __device__ __forceinline__ void warp_column(int j, const StepParams& p, int lane
     }
     const int E = __shfl_sync(full, incl, 31);
     if (n > 32 || n < 1 || kd < 0 || E > 32) {
-        // general fallback in lane 0 (statistics through the atomics)
+        // beyond one warp (or no diagonal): the queue's tier-3 list
         if (lane == 0) {
-            VRes res;
-            vres_init(res);
-            vertex_slow<T, 8, UNIFORM>(j, p, res, 0, false);
-            report_flags(res, j, p);
-            long long off = 0;
-            bool ok = true;
-            if (res.cnt > 2) {
-                off = (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)res.cnt);
-                if (off + res.cnt > p.cap) { atomicExch(&p.ws.ctl->overflow, 1); ok = false; }
-            }
-            p.ws.vbm[jl] = res.bm;
-            if (ok) { VRes r2 = res; vertex_slow<T, 8, UNIFORM>(j, p, r2, off, true); }
-            ws.maxd = fmax(ws.maxd, res.maxd);
-            ws.cnt += res.cnt;
-            ws.skel += res.nskel;
+            const int q = atomicAdd(qs.dp_n, 1);
+            qs.dp[qs.dir * q] = j;
         }
         return;
     }
@@ -1489,15 +1476,15 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p, con
 // one warp per listed column (grid-stride); the warp's statistics go to
 // the global accumulators once
 template <typename T, bool UNIFORM, bool PACKED>
-__global__ void __launch_bounds__(FT_TPB, 4) warp_kernel(const StepParams p, const int* list, const int* count, int dir) {
+__global__ void __launch_bounds__(FT_TPB, 4) warp_kernel(const StepParams p, const Queues qs) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
-    const int nc = *(volatile const int*)count;
+    const int nc = *(volatile const int*)qs.q_n;
     const int lane = threadIdx.x & 31;
     const int nw = gridDim.x * FT_WARPS;
     WarpStats ws;
     ws.maxd = 0.0; ws.cnt = 0; ws.skel = 0;
     for (int i = (blockIdx.x * FT_TPB + threadIdx.x) >> 5; i < nc; i += nw)
-        warp_column<T, UNIFORM, PACKED>(__ldg(&list[dir * i]), p, lane, ws);
+        warp_column<T, UNIFORM, PACKED>(__ldg(&qs.q[qs.dir * i]), p, qs, lane, ws);
     if (lane == 0 && (ws.maxd > 0.0 || ws.cnt || ws.skel)) {
         if (ws.maxd > 0.0) atomicMax(&p.ws.ctl->maxdelta_bits, (unsigned long long)__double_as_longlong(ws.maxd));
         if (ws.skel) atomicAdd(&p.ws.ctl->skel_total, (unsigned long long)ws.skel);
@@ -2156,7 +2143,9 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
         pev(5, s);
         // queue B: what tier 1.5 defers (unions of three or more rows), one
         // warp per column
-        if (m & 2) FT_PICK3(ft::warp_kernel, dtype, uni, packed)<<<g_fixup_grid * 4, FT_TPB, 0, s>>>(p, qb.q, qb.q_n, qb.dir);
+        if (m & 2) FT_PICK3(ft::warp_kernel, dtype, uni, packed)<<<g_fixup_grid * 4, FT_TPB, 0, s>>>(p, qb);
+        // (its tier-3 list is empty unless a column exceeds one warp)
+        if (m & 8) FT_PICK2(ft::deep_kernel, dtype, uni)<<<g_fixup_grid / 8, FT_TPB, 0, s>>>(p, qb);
         pev(6, s);
         cudaStreamWaitEvent(s, g_join, 0);
         pev(7, s);
