@@ -440,8 +440,9 @@ def run_ours(args):
             "e2e": e2e,
             "clocks": clk,
             # per step: tier 1, queue A, tiers 2a/2b/3 of queue A (side stream),
-            # tier 1.5, the warp tail of queue B, finalize; conversion + compaction
-            "gpu_launches": 8 * K + 4,
+            # tier 1.5, queue B (warp kernel + its tier-3 list), finalize;
+            # conversion + compaction
+            "gpu_launches": 9 * K + 4,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -575,10 +576,10 @@ def run_partitioned(args, world, rank, local, emulate=0):
             "cpu_baseline": None,
             "e2e": e2e,
             "clocks": clk,
-            # per step and rank: the 8 launches of ft_domain_step, one pack per peer
+            # per step and rank: the 9 launches of ft_domain_step, one pack per peer
             # sent to, the combine, one unpack per peer received from; one control
             # snapshot per 16-step chunk
-            "gpu_launches": (9 + len(r0.send_msg) + len(r0.recv_msg)) * K + -(-K // 16),
+            "gpu_launches": (10 + len(r0.send_msg) + len(r0.recv_msg)) * K + -(-K // 16),
         }
         if emulate:
             line["emulated"] = True

@@ -966,21 +966,27 @@ __device__ __forceinline__ void warp_column(int j, const StepParams& p, const Qu
     const bool dg = valid && myk == kd;
     const unsigned int grp = __match_any_sync(full, r);
     const bool leader = valid && (__ffs(grp) - 1) == lane;
-    // Lt(r, j) in L order, PHI(r, j) from the diagonal neighbour, and the
-    // row rank among the distinct rows
-    double lam = 0.0, ph = 0.0;
-    int rank = 0;
-    for (int src = 0; src < E; ++src) {
+    // Lt(r, j): the group's products added in lane (= L) order, walking the
+    // group's members; PHI(r, j) from the group's diagonal entry; the row
+    // rank among the distinct rows (over the group leaders)
+    const int gsz = __popc(grp);
+    const int gmax = __reduce_max_sync(full, (unsigned int)gsz);
+    double lam = 0.0;
+    unsigned int rest = grp;
+    for (int it = 0; it < gmax; ++it) {
+        const int src = rest ? __ffs(rest) - 1 : lane;
+        rest = rest ? (rest & (rest - 1)) : 0u;
         const double pv = __shfl_sync(full, prod, src);
-        const double vv = __shfl_sync(full, v, src);
-        const int rr = __shfl_sync(full, r, src);
-        const bool ds = __shfl_sync(full, dg, src);
-        const bool ls = __shfl_sync(full, leader, src);
-        if ((grp >> src) & 1u) {
-            lam = lam + pv;
-            if (ds) ph = vv;
-        }
-        if (ls && rr < r) ++rank;
+        if (it < gsz) lam = lam + pv;
+    }
+    const unsigned int dgm = grp & __ballot_sync(full, dg);
+    const double vd = __shfl_sync(full, v, dgm ? __ffs(dgm) - 1 : lane);
+    const double ph = dgm ? vd : 0.0;
+    const unsigned int lmask = __ballot_sync(full, leader);
+    int rank = 0;
+    for (unsigned int mm = lmask; mm; mm &= mm - 1) {
+        const int rr = __shfl_sync(full, r, __ffs(mm) - 1);
+        rank += rr < r ? 1 : 0;
     }
     const int m = __popc(__ballot_sync(full, leader));
     const bool in = leader && in_skeleton(ph, lam);
@@ -1024,10 +1030,9 @@ __device__ __forceinline__ void warp_column(int j, const StepParams& p, const Qu
     const unsigned int ob = __ballot_sync(full, out);
     const int cnt = __popc(ob);
     int pos = 0;       // rank among the output rows
-    for (int src = 0; src < E; ++src) {
-        const bool os = __shfl_sync(full, out, src);
-        const int rk = __shfl_sync(full, rank, src);
-        if (os && rk < rank) ++pos;
+    for (unsigned int mm = ob; mm; mm &= mm - 1) {
+        const int rk = __shfl_sync(full, rank, __ffs(mm) - 1);
+        pos += rk < rank ? 1 : 0;
     }
     // statistics and error reports of the column
     double bm = (out && r == 0) ? nv : 0.0;
@@ -1489,45 +1494,6 @@ __global__ void __launch_bounds__(FT_TPB, 4) warp_kernel(const StepParams p, con
         if (ws.maxd > 0.0) atomicMax(&p.ws.ctl->maxdelta_bits, (unsigned long long)__double_as_longlong(ws.maxd));
         if (ws.skel) atomicAdd(&p.ws.ctl->skel_total, (unsigned long long)ws.skel);
         if (ws.cnt) atomicAdd(&p.ws.ctl->nnz_total, (unsigned long long)ws.cnt);
-    }
-}
-
-// queue B (the few columns tier 1.5 defers) in ONE launch after tier 1.5:
-// the tier-2a register path, else the general windowed algorithm in the
-// same lane (no further queues, so no chain of dependent tail launches)
-template <typename T, bool UNIFORM, bool PACKED>
-__global__ void __launch_bounds__(FT_TPB) tail_kernel(const StepParams p, const Queues qs) {
-    if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
-    const int n_q = *(volatile int*)qs.q_n;
-    const int lane = threadIdx.x & 31;
-    const int stride = gridDim.x * FT_TPB;
-    const int rounds = (n_q + stride - 1) / stride;
-    for (int rnd = 0; rnd < rounds; ++rnd) {
-        const int i = rnd * stride + blockIdx.x * FT_TPB + threadIdx.x;
-        const bool mine = i < n_q;
-        const int j = mine ? qs.q[qs.dir * i] : 0;
-        VRes res;
-        vres_init(res);
-        Win<3> w;
-        w.m = 0;
-        unsigned int out_mask = 0;
-        bool slow = false;
-        if (mine) {
-            slow = !wide3<T, UNIFORM, PACKED>(j, p, w);
-            if (!slow) process_window<3>(w, p, res, out_mask, c_recip);
-            else vertex_slow<T, 8, UNIFORM>(j, p, res, 0, false);
-            report_flags(res, j, p);
-        }
-        bool fits;
-        const int need = (mine && res.cnt > 2) ? res.cnt : 0;
-        const long long off = pool_place(need, res, p, lane, fits);
-        if (mine) {
-            p.ws.vbm[j - p.j_base] = res.bm;
-            if (need == 0 || fits) {
-                if (!slow) emit_window<T, 3>(w, out_mask, j, off, p);
-                else { VRes r2 = res; vertex_slow<T, 8, UNIFORM>(j, p, r2, off, true); }
-            }
-        }
     }
 }
 
@@ -2119,33 +2085,27 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
         k1<<<grid, FT_TPB, 0, s>>>(p);
     }
     if (which & 2) {
-        // FT_PROBE_FIXUP (timing probes only, results invalid): bit mask of
-        // the tier-1.5 / 2a / 2b / 3 launches; 32 skips queue A
-        static const char* probe = getenv("FT_PROBE_FIXUP");
-        const int m = probe ? atoi(probe) : 15;
         // queue A (tier 1's wide columns) on the high-priority side stream,
         // concurrently with tier 1.5
         if (side_init() != FT_OK) return cuda_check("side stream");
         const ft::Queues qa = ft::queues(p, 0), qb = ft::queues(p, 1);
         cudaEventRecord(g_fork, s);
         cudaStreamWaitEvent(g_side, g_fork, 0);
-        const bool pa = !(m & 32);   // probe: skip queue A
         ft::queue_kernel<<<(FT_WARPS * p.num_tiles + 255) / 256, 256, 0, g_side>>>(p);
-        if ((m & 2) && pa) FT_PICK3(ft::wide3_kernel, dtype, uni, packed)<<<g_fixup_grid, FT_TPB, 0, g_side>>>(p, qa);
+        FT_PICK3(ft::wide3_kernel, dtype, uni, packed)<<<g_fixup_grid, FT_TPB, 0, g_side>>>(p, qa);
         pev(3, g_side);
-        if ((m & 4) && pa) FT_PICK2(ft::wide_kernel, dtype, uni)<<<g_fixup_grid, FT_TPB, 0, g_side>>>(p, qa);
-        if ((m & 8) && pa) FT_PICK2(ft::deep_kernel, dtype, uni)<<<g_fixup_grid / 4, FT_TPB, 0, g_side>>>(p, qa);
+        FT_PICK2(ft::wide_kernel, dtype, uni)<<<g_fixup_grid, FT_TPB, 0, g_side>>>(p, qa);
+        FT_PICK2(ft::deep_kernel, dtype, uni)<<<g_fixup_grid / 4, FT_TPB, 0, g_side>>>(p, qa);
         pev(4, g_side);
         cudaEventRecord(g_join, g_side);
         // tier 1.5, one warp per tile
-        if (m & 1)
-            FT_PICK3(ft::gen_kernel, dtype, uni, packed)<<<(p.num_tiles + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
+        FT_PICK3(ft::gen_kernel, dtype, uni, packed)<<<(p.num_tiles + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
         pev(5, s);
         // queue B: what tier 1.5 defers (unions of three or more rows), one
         // warp per column
-        if (m & 2) FT_PICK3(ft::warp_kernel, dtype, uni, packed)<<<g_fixup_grid * 4, FT_TPB, 0, s>>>(p, qb);
+        FT_PICK3(ft::warp_kernel, dtype, uni, packed)<<<g_fixup_grid * 4, FT_TPB, 0, s>>>(p, qb);
         // (its tier-3 list is empty unless a column exceeds one warp)
-        if (m & 8) FT_PICK2(ft::deep_kernel, dtype, uni)<<<g_fixup_grid / 8, FT_TPB, 0, s>>>(p, qb);
+        FT_PICK2(ft::deep_kernel, dtype, uni)<<<g_fixup_grid / 8, FT_TPB, 0, s>>>(p, qb);
         pev(6, s);
         cudaStreamWaitEvent(s, g_join, 0);
         pev(7, s);

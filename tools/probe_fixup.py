@@ -1,8 +1,8 @@
-"""Warm per-kernel times of the C3 step from ONE fixed input state (the
-same step repeated: tb -> ta), with FT_PROBE_FIXUP selecting the fixup
-launches (results are only valid with all of them; this is a timing probe).
+"""Warm times of tier 1 / the fixup launches / the finalize of the C3 step
+from ONE fixed input state (the same step repeated: tb -> ta), and the tier
+populations of that state.  (tools/probe_timeline.py splits the fixup.)
 
-usage: FT_PROBE_FIXUP=<mask> python tools/probe_fixup.py [nx ny seeds warm]
+usage: python tools/probe_fixup.py [nx ny seeds warm]
 """
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -46,7 +46,7 @@ for i in range(30):
     if i >= 5:
         t.append([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])])
 t = np.median(np.array(t), axis=0) * 1e3
-print(f"mask {os.environ.get('FT_PROBE_FIXUP', '15')}: tier1 {t[0]:.1f} us  fixup {t[1]:.1f} us  finalize {t[2]:.1f} us")
+print(f"tier1 {t[0]:.1f} us  fixup {t[1]:.1f} us  finalize {t[2]:.1f} us")
 
 # tier populations of this state: masks after tier 1, queue after tier 1.5
 def al(x):
@@ -56,7 +56,6 @@ ns = 4 * nt
 off = 128
 off_gen = al(al(al(off + ns * 8) + ns * 8) + ns * 8)
 off_slow = al(off_gen + ns * 4)
-os.environ["FT_PROBE_FIXUP"] = "0"
 assert lib.ft_step_kernel(ctypes.byref(lc), fl, ctypes.byref(bc), ctypes.byref(ac), 0, ctypes.byref(prm), wp, wn, st) == 0
 torch.cuda.synchronize()
 raw = ws.ws.cpu().numpy()
