@@ -774,11 +774,14 @@ __device__ __forceinline__ void tier1_segment(const StepParams& p, int seg, int 
 
     double bm = 0.0, md = 0.0;
     int cnt = 0;
+    // a cell interior at rest holds exactly 1.0, and 1.0 * (1 / (0 + 1.0))
+    // == 1.0: a warp whose fast lanes all hold 1.0 skips the division
+    const bool ones = __all_sync(0xffffffffu, !fast || phs == 1.0);
     if (fast) {
         double v = phs;
         if (v > 1.0) v = 1.0;
         const double s = 0.0 + v;
-        const double nv = v * (1.0 / s);
+        const double nv = ones ? 1.0 : v * (1.0 / s);
         if (nv != 0.0) {
             cnt = 1;
             if (rs == 0) bm = nv;
