@@ -8,6 +8,7 @@
 #define FT_TPB 128              // threads (= vertex columns) per CTA tile
 #define FT_WARPS (FT_TPB / 32)
 #define FT_CCH 2048             // columns per compaction chunk
+#define FT_GEN_TILES 3          // tiles per tier-1.5 warp (~63 flagged columns: two full chunks)
 #define FT_CTPB 256             // threads of the compaction kernels
 
 namespace ft {
@@ -55,7 +56,7 @@ struct Workspace {
     int2*         seg_cs;       // [4 num_tiles] tier-1 (nnz, skeleton nnz) per segment
     unsigned int* gen_mask;     // [4 num_tiles] tier-1.5 columns of each segment
     unsigned int* slow_mask;    // [4 num_tiles] tier-2 columns of each segment
-    double*       gen_bm;       // [num_tiles] tier-1.5 base mass per tile
+    double*       gen_bm;       // [num_tiles] tier-1.5 base mass per tile group (FT_GEN_TILES tiles)
     double*       gen_maxd;     // [num_tiles]
     int2*         gen_cs;       // [num_tiles]
     double*       vbm;          // [n_v] base mass of tier-2/3 columns

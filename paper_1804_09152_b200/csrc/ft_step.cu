@@ -1092,26 +1092,34 @@ __device__ __forceinline__ void warp_column(int j, const StepParams& p, const Qu
 
 // ---------------------------------------------------------------------------
 // tier 1.5: the flagged columns with at most two entries per neighbour, one
-// warp per tile with the columns on its lanes: the one-pass two-row update.
-// More than two rows -> tier 2 (added to the tile's slow mask).  The warp
-// then queues the tile's tier-2 columns with one atomic.  Statistics into
-// the tile's slots, base mass in lane order (fixed): no hot atomics.
+// warp per group of FT_GEN_TILES tiles (~63 columns at C3: two nearly full
+// chunks) with the columns on its lanes: the one-pass two-row update.  More
+// than two rows -> queue B (and the tile's slow mask).  Statistics into the
+// group's slots, base mass in lane order (fixed): no hot atomics.
 
 template <typename T, bool UNIFORM, bool PACKED>
 __global__ void __launch_bounds__(FT_TPB, 8) gen_kernel(const StepParams p) {
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
-    __shared__ int s_list[FT_WARPS][FT_TPB];
+    __shared__ int s_list[FT_WARPS][FT_GEN_TILES * FT_TPB];
     const int lane = threadIdx.x & 31;
     int* list = s_list[threadIdx.x >> 5];
     const int nwarps = gridDim.x * FT_WARPS;
-    for (int t = (blockIdx.x * FT_TPB + threadIdx.x) >> 5; t < p.num_tiles; t += nwarps) {
-        const uint4 g4 = *reinterpret_cast<const uint4*>(&p.ws.gen_mask[(size_t)FT_WARPS * t]);
-        const unsigned int gm[4] = {g4.x, g4.y, g4.z, g4.w};
+    const int ngroups = (p.num_tiles + FT_GEN_TILES - 1) / FT_GEN_TILES;
+    for (int t = (blockIdx.x * FT_TPB + threadIdx.x) >> 5; t < ngroups; t += nwarps) {
+        // the flagged columns of the group's tiles, in vertex order
         int ng = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if ((gm[q] >> lane) & 1u) list[ng + __popc(gm[q] & ((1u << lane) - 1u))] = t * FT_TPB + q * 32 + lane;
-            ng += __popc(gm[q]);
+        for (int tt = 0; tt < FT_GEN_TILES; ++tt) {
+            const int tile = t * FT_GEN_TILES + tt;
+            if (tile >= p.num_tiles) break;
+            const uint4 g4 = *reinterpret_cast<const uint4*>(&p.ws.gen_mask[(size_t)FT_WARPS * tile]);
+            const unsigned int gm[4] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if ((gm[q] >> lane) & 1u)
+                    list[ng + __popc(gm[q] & ((1u << lane) - 1u))] = tile * FT_TPB + q * 32 + lane;
+                ng += __popc(gm[q]);
+            }
         }
         if (ng == 0) continue;
         __syncwarp();
@@ -1196,10 +1204,7 @@ __global__ void __launch_bounds__(FT_TPB, 8) gen_kernel(const StepParams p) {
             // three or more rows (rare): queue B, one atomic per chunk
             const unsigned int db = __ballot_sync(0xffffffffu, defer);
             if (db) {
-                if (defer) {
-                    const int lt = jl - t * FT_TPB;
-                    atomicOr(&p.ws.slow_mask[(size_t)FT_WARPS * t + (lt >> 5)], 1u << (lt & 31));
-                }
+                if (defer) atomicOr(&p.ws.slow_mask[jl >> 5], 1u << (jl & 31));
                 int qb = 0;
                 if (lane == 0) qb = atomicAdd(&p.ws.ctl->gen_count, __popc(db));
                 qb = __shfl_sync(0xffffffffu, qb, 0);
@@ -1564,13 +1569,15 @@ __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizePara
             m &= m - 1;
             tb = tb + f.ws.vbm[(size_t)sg * 32 + b];
         }
-        if ((sg & (FT_WARPS - 1)) == 0) {
-            const int t = sg / FT_WARPS;
-            const uint4 g4 = *reinterpret_cast<const uint4*>(&f.ws.gen_mask[(size_t)t * FT_WARPS]);
-            if (g4.x | g4.y | g4.z | g4.w) {
-                tb = tb + f.ws.gen_bm[t];
-                amx = fmax(amx, f.ws.gen_maxd[t]);
-                const int2 gc = f.ws.gen_cs[t];
+        if (sg % (FT_WARPS * FT_GEN_TILES) == 0) {
+            // first segment of a tier-1.5 tile group: the group's slots
+            const int g = sg / (FT_WARPS * FT_GEN_TILES);
+            unsigned int any = 0u;
+            for (int k = sg; k < sg + FT_WARPS * FT_GEN_TILES && k < ns; ++k) any |= f.ws.gen_mask[k];
+            if (any) {
+                tb = tb + f.ws.gen_bm[g];
+                amx = fmax(amx, f.ws.gen_maxd[g]);
+                const int2 gc = f.ws.gen_cs[g];
                 acnt += gc.x;
                 askel += gc.y;
             }
@@ -2102,7 +2109,8 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
         pev(4, g_side);
         cudaEventRecord(g_join, g_side);
         // tier 1.5, one warp per tile
-        FT_PICK3(ft::gen_kernel, dtype, uni, packed)<<<(p.num_tiles + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
+        const int ngroups = (p.num_tiles + FT_GEN_TILES - 1) / FT_GEN_TILES;
+        FT_PICK3(ft::gen_kernel, dtype, uni, packed)<<<(ngroups + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
         pev(5, s);
         // queue B: what tier 1.5 defers (unions of three or more rows), one
         // warp per column
