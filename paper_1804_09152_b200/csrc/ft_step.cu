@@ -1415,6 +1415,7 @@ __device__ __forceinline__ bool gather_wide(int j, const StepParams& p, Win<K>& 
             }
         }
         if (i == K) return rr == INT_MAX;     // more than K rows?
+        if (rr == INT_MAX) return true;       // all rows found (w.m of them)
         double lam = 0.0, ph = 0.0;
         if (rr != INT_MAX) {
 #pragma unroll
