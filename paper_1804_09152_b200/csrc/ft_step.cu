@@ -1574,7 +1574,9 @@ __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizePara
             // first segment of a tier-1.5 tile group: the group's slots
             const int g = sg / (FT_WARPS * FT_GEN_TILES);
             unsigned int any = 0u;
-            for (int k = sg; k < sg + FT_WARPS * FT_GEN_TILES && k < ns; ++k) any |= f.ws.gen_mask[k];
+#pragma unroll
+            for (int k = 0; k < FT_WARPS * FT_GEN_TILES; ++k)
+                if (sg + k < ns) any |= f.ws.gen_mask[sg + k];
             if (any) {
                 tb = tb + f.ws.gen_bm[g];
                 amx = fmax(amx, f.ws.gen_maxd[g]);
@@ -1612,11 +1614,27 @@ __global__ void __launch_bounds__(FT_FIN_TPB) finalize_kernel(const FinalizePara
     // t + FT_FIN_TPB, ... (fixed order), then fixed shuffle / warp trees
     double pb = 0.0, pm = 0.0;
     long long pc = 0, pk = 0;
-    for (int q = tid; q < (int)gridDim.x; q += FT_FIN_TPB) {
-        pb = pb + __ldcg(&f.ws.fin_part[q]);
-        pm = fmax(pm, __ldcg(&f.ws.fin_maxd[q]));
-        pc += __ldcg(&f.ws.fin_cnt[q]);
-        pk += __ldcg(&f.ws.fin_skel[q]);
+    const int G = (int)gridDim.x;
+    for (int q0 = tid; q0 < G; q0 += 4 * FT_FIN_TPB) {
+        // four partials' loads in flight, added in the same order
+        double b4[4], m4[4];
+        long long c4[4], k4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int q = q0 + k * FT_FIN_TPB;
+            const bool h = q < G;
+            b4[k] = h ? __ldcg(&f.ws.fin_part[q]) : 0.0;
+            m4[k] = h ? __ldcg(&f.ws.fin_maxd[q]) : 0.0;
+            c4[k] = h ? __ldcg(&f.ws.fin_cnt[q]) : 0;
+            k4[k] = h ? __ldcg(&f.ws.fin_skel[q]) : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (q0 + k * FT_FIN_TPB < G) pb = pb + b4[k];
+            pm = fmax(pm, m4[k]);
+            pc += c4[k];
+            pk += k4[k];
+        }
     }
     pb = warp_sum(pb);
     pc = warp_sum(pc);
