@@ -885,127 +885,134 @@ __device__ __forceinline__ long long pool_place(int need, const VRes& res, const
 }
 
 // ---------------------------------------------------------------------------
-// warp-cooperative column (the wide tail: tier-2a leftovers, tier-1.5
-// deferrals).  One warp per column: lane e holds entry e of the
-// neighbourhood (neighbours in L order, rows ascending within one), lanes
+// lane-cooperative column (queue B: the tier-1.5 deferrals).  Sixteen
+// lanes per column: lane e holds entry e of the neighbourhood (neighbours in L order, rows ascending within one), lanes
 // with equal rows are grouped with __match_any_sync, and every sum is taken
 // in the reference's order -- Lt(r, j) over the entries in L order
 // (_kernels.py:36-50), the skeleton aggregates and the normaliser in
 // ascending row order (_kernels.py:179-282) -- by shuffles, so the result is
 // bitwise that of process_window / vertex_slow.  Neighbourhoods of more
-// than 32 entries (or 32 L entries) go to the queue's tier-3 list.
+// than 16 entries (or 16 L entries) go to the queue's tier-3 list.
 
 struct WarpStats {
     double maxd;
     long long cnt, skel;
 };
 
+// Two columns per warp: lanes 0-15 and 16-31 each hold one column's
+// neighbourhood (queue B: at most two entries per neighbour and at most 8
+// neighbours, so at most 16 entries).  Every loop has a warp-uniform trip
+// count, so the full-mask shuffles never diverge between the halves.
 template <typename T, bool UNIFORM, bool PACKED>
-__device__ __forceinline__ void warp_column(int j, const StepParams& p, const Queues& qs, int lane, WarpStats& ws) {
+__device__ __forceinline__ void half_column(int j, bool have, const StepParams& p, const Queues& qs, int lane,
+                                            WarpStats& ws) {
+    constexpr int W = 16;
     const unsigned int full = 0xffffffffu;
+    const int sl = lane & (W - 1);               // lane within the half
+    const int gb = lane & W;                     // 0 or 16
+    auto half_bits = [&](unsigned int b) { return (b >> gb) & 0xffffu; };
     const int jl = j - p.j_base;
     int q0 = 0, n = 0, pu = -1;
     if (PACKED) {
-        // lane k < 8 takes delta k of the packed row (one 16-byte load)
-        const int4 pk = __ldg(&p.lap_pack[jl]);
-        const int w = (lane >> 1) == 0 ? pk.x : ((lane >> 1) == 1 ? pk.y : ((lane >> 1) == 2 ? pk.z : pk.w));
-        const int d = (lane & 1) ? (w >> 16) : ((int)(w << 16) >> 16);
-        const bool valid = lane < kMD && d != kPackEmpty;
+        int4 pk = make_int4(0, 0, 0, 0);
+        if (have) pk = __ldg(&p.lap_pack[jl]);
+        const int w = (sl >> 1) == 0 ? pk.x : ((sl >> 1) == 1 ? pk.y : ((sl >> 1) == 2 ? pk.z : pk.w));
+        const int d = (sl & 1) ? (w >> 16) : ((int)(w << 16) >> 16);
+        const bool valid = have && sl < kMD && d != kPackEmpty;
         pu = valid ? j + d : -1;
-        n = __popc(__ballot_sync(full, valid));      // stored in order: valid slots lead
+        n = __popc(half_bits(__ballot_sync(full, valid)));   // valid slots lead
     }
-    if (n == 0) {
+    if (have && n == 0) {
         q0 = __ldg(&p.lap_ptr[jl]);
         n = __ldg(&p.lap_ptr[jl + 1]) - q0;
         pu = -1;
     }
     int u = -1, sgk = FT_SIG_EMPTY, axk = 0, ck = 0;
     double lk = 0.0;
-    if (lane < n && n <= 32) {
-        u = pu >= 0 ? pu : __ldg(&p.lap_idx[q0 + lane]);
+    const bool lv = have && sl < n && n <= W;
+    if (lv) {
+        u = pu >= 0 ? pu : __ldg(&p.lap_idx[q0 + sl]);
         sgk = __ldg(&p.in.sig[u]);
         ck = sig_count(sgk);
         axk = ck >= 2 ? __ldg(&p.in.aux[u]) : 0;
     }
-    const unsigned int dmask = __ballot_sync(full, lane < n && u == j);
+    const unsigned int dmask = half_bits(__ballot_sync(full, lv && u == j));
     const int kd = dmask ? __ffs(dmask) - 1 : -1;
-    if (lane < n && n <= 32) {
-        if (UNIFORM) lk = (lane == kd) ? -1.0 : 1.0 / (double)(n - 1);
-        else lk = ldv<T>(p.lap_val, q0 + lane);     // (PACKED implies UNIFORM)
+    if (lv) {
+        if (UNIFORM) lk = (sl == kd) ? -1.0 : 1.0 / (double)(n - 1);
+        else lk = ldv<T>(p.lap_val, q0 + sl);
     }
-    // entry offsets: exclusive scan of the counts over the L entries
-    int incl = ck;
+    int incl = ck;                               // entry offsets within the half
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(full, incl, o);
-        if (lane >= o) incl += y;
+    for (int o = 1; o < W; o <<= 1) {
+        const int y = __shfl_up_sync(full, incl, o, W);
+        if (sl >= o) incl += y;
     }
-    const int E = __shfl_sync(full, incl, 31);
-    if (n > 32 || n < 1 || kd < 0 || E > 32) {
-        // beyond one warp (or no diagonal): the queue's tier-3 list
-        if (lane == 0) {
-            const int q = atomicAdd(qs.dp_n, 1);
-            qs.dp[qs.dir * q] = j;
-        }
-        return;
+    const int E = __shfl_sync(full, incl, W - 1, W);
+    const bool fb = have && (n > W || n < 1 || kd < 0 || E > W);   // to the tier-3 list
+    if (fb && sl == 0) {
+        const int q = atomicAdd(qs.dp_n, 1);
+        qs.dp[qs.dir * q] = j;
     }
+    const bool act = have && !fb;
     const int e0k = incl - ck;
-    // this lane's entry: owner neighbour k (entries are k-major) and index t
     int myk = 0, t = 0;
-    for (int k = 0; k < n; ++k) {
-        const int a = __shfl_sync(full, e0k, k), c = __shfl_sync(full, ck, k);
-        if (lane >= a && lane < a + c) { myk = k; t = lane - a; }
+    for (int k = 0; k < W; ++k) {
+        const int a = __shfl_sync(full, e0k, k, W), c = __shfl_sync(full, ck, k, W);
+        if (sl >= a && sl < a + c) { myk = k; t = sl - a; }
     }
-    const int su = __shfl_sync(full, u, myk), ss = __shfl_sync(full, sgk, myk), sa = __shfl_sync(full, axk, myk);
-    const double sl = __shfl_sync(full, lk, myk);
-    const bool valid = lane < E;
-    int r = -1 - lane;                // unique key for lanes without an entry
+    const int su = __shfl_sync(full, u, myk, W), ss = __shfl_sync(full, sgk, myk, W);
+    const int sa = __shfl_sync(full, axk, myk, W);
+    const double slk = __shfl_sync(full, lk, myk, W);
+    const bool valid = act && sl < E;
+    int r = -1 - lane;                           // unique key for lanes without an entry
     double v = 0.0;
     if (valid) {
         r = hyb_row<T>(p.in, ss, sa, t);
         v = hyb_val<T>(p.in, su, ss, sa, t);
     }
-    const double prod = v * sl;       // PHI(r, u) * L(j, u)
+    const double prod = v * slk;                 // PHI(r, u) * L(j, u)
     const bool dg = valid && myk == kd;
-    const unsigned int grp = __match_any_sync(full, r);
-    const bool leader = valid && (__ffs(grp) - 1) == lane;
-    // Lt(r, j): the group's products added in lane (= L) order, walking the
-    // group's members; PHI(r, j) from the group's diagonal entry; the row
-    // rank among the distinct rows (over the group leaders)
+    // group equal rows within the half: key = row and half
+    const unsigned int grpw = __match_any_sync(full, valid ? ((r << 1) | (gb >> 4)) : r);
+    const unsigned int grp = half_bits(grpw);
+    const bool leader = valid && (__ffs(grp) - 1) == sl;
     const int gsz = __popc(grp);
     const int gmax = __reduce_max_sync(full, (unsigned int)gsz);
     double lam = 0.0;
     unsigned int rest = grp;
-    for (int it = 0; it < gmax; ++it) {
-        const int src = rest ? __ffs(rest) - 1 : lane;
+    for (int it = 0; it < gmax; ++it) {          // Lt(r, j) in L order
+        const int src = rest ? __ffs(rest) - 1 : sl;
         rest = rest ? (rest & (rest - 1)) : 0u;
-        const double pv = __shfl_sync(full, prod, src);
+        const double pv = __shfl_sync(full, prod, src, W);
         if (it < gsz) lam = lam + pv;
     }
-    const unsigned int dgm = grp & __ballot_sync(full, dg);
-    const double vd = __shfl_sync(full, v, dgm ? __ffs(dgm) - 1 : lane);
+    const unsigned int dgm = grp & half_bits(__ballot_sync(full, dg));
+    const double vd = __shfl_sync(full, v, dgm ? __ffs(dgm) - 1 : sl, W);
     const double ph = dgm ? vd : 0.0;
-    const unsigned int lmask = __ballot_sync(full, leader);
     int rank = 0;
-    for (unsigned int mm = lmask; mm; mm &= mm - 1) {
-        const int rr = __shfl_sync(full, r, __ffs(mm) - 1);
-        rank += rr < r ? 1 : 0;
+    for (int s2 = 0; s2 < W; ++s2) {
+        const int rr = __shfl_sync(full, r, s2, W);
+        const bool ls = __shfl_sync(full, leader, s2, W);
+        rank += (ls && rr < r) ? 1 : 0;
     }
-    const int m = __popc(__ballot_sync(full, leader));
+    const int m = __popc(half_bits(__ballot_sync(full, leader)));
+    const int mmax = __reduce_max_sync(full, (unsigned int)m);
     const bool in = leader && in_skeleton(ph, lam);
     int bad_phi = (leader && ph != 0.0 && !in) ? r : -1;
     int bad_lt = (leader && lam != 0.0 && !in) ? r : -1;
     const double lh = (lam != 0.0) ? lam : 0.0;
     const double sq = in ? sqrt(ph) : 0.0;
-    // aggregates over the skeleton rows in ascending row order
-    Agg g;
+    Agg g;                                       // ascending row order
     agg_init(g);
-    for (int q = 0; q < m; ++q) {
-        const int lq = __ffs(__ballot_sync(full, leader && rank == q)) - 1;
-        const bool iq = __shfl_sync(full, in, lq);
-        const double phq = __shfl_sync(full, ph, lq), lhq = __shfl_sync(full, lh, lq), sqq = __shfl_sync(full, sq, lq);
-        const int rq = __shfl_sync(full, r, lq);
-        if (iq) {
+    for (int q = 0; q < mmax; ++q) {
+        const unsigned int hb = half_bits(__ballot_sync(full, leader && rank == q));
+        const int lq = hb ? __ffs(hb) - 1 : 0;
+        const bool iq = __shfl_sync(full, in, lq, W);
+        const double phq = __shfl_sync(full, ph, lq, W), lhq = __shfl_sync(full, lh, lq, W);
+        const double sqq = __shfl_sync(full, sq, lq, W);
+        const int rq = __shfl_sync(full, r, lq, W);
+        if (hb && iq) {
             if (g.n == 0) { g.first_row = rq; g.phi0 = phq; }
             g.n++;
             g.sl = g.sl + lhq;
@@ -1014,42 +1021,40 @@ __device__ __forceinline__ void warp_column(int j, const StepParams& p, const Qu
         }
     }
     bool nan = false;
-    double vn = 0.0;
-    double s = 0.0;
-    if (g.n > 0) {
-        const Coef c = make_coef(g, p, c_recip);
-        if (in) vn = update_entry_sq(r, ph, lh, sq, c, p, nan);
-        for (int q = 0; q < m; ++q) {
-            const int lq = __ffs(__ballot_sync(full, leader && rank == q)) - 1;
-            const bool iq = __shfl_sync(full, in, lq);
-            const double vq = __shfl_sync(full, vn, lq);
-            if (iq) s = s + vq;
-        }
+    double vn = 0.0, s = 0.0;
+    Coef c;
+    if (g.n > 0) c = make_coef(g, p, c_recip);
+    if (g.n > 0 && in) vn = update_entry_sq(r, ph, lh, sq, c, p, nan);
+    for (int q = 0; q < mmax; ++q) {
+        const unsigned int hb = half_bits(__ballot_sync(full, leader && rank == q));
+        const int lq = hb ? __ffs(hb) - 1 : 0;
+        const bool iq = __shfl_sync(full, in, lq, W);
+        const double vq = __shfl_sync(full, vn, lq, W);
+        if (g.n > 0 && hb && iq) s = s + vq;
     }
     const bool spos = s > 0.0;
     const double inv = spos ? 1.0 / s : 0.0;
     const double nv = spos ? vn * inv : vn;
     const bool out = in && nv != 0.0;
-    const unsigned int ob = __ballot_sync(full, out);
-    const int cnt = __popc(ob);
-    int pos = 0;       // rank among the output rows
-    for (unsigned int mm = ob; mm; mm &= mm - 1) {
-        const int rk = __shfl_sync(full, rank, __ffs(mm) - 1);
-        pos += rk < rank ? 1 : 0;
+    const int cnt = __popc(half_bits(__ballot_sync(full, out)));
+    int pos = 0;                                 // rank among the output rows
+    for (int s2 = 0; s2 < W; ++s2) {
+        const bool os = __shfl_sync(full, out, s2, W);
+        const int rk = __shfl_sync(full, rank, s2, W);
+        pos += (os && rk < rank) ? 1 : 0;
     }
-    // statistics and error reports of the column
     double bm = (out && r == 0) ? nv : 0.0;
     double dd = in ? fabs(nv - ph) : 0.0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        bm = bm + __shfl_xor_sync(full, bm, o);   // at most one nonzero term: exact
-        dd = fmax(dd, __shfl_xor_sync(full, dd, o));
-        bad_phi = max(bad_phi, __shfl_xor_sync(full, bad_phi, o));
-        bad_lt = max(bad_lt, __shfl_xor_sync(full, bad_lt, o));
+    for (int o = W / 2; o > 0; o >>= 1) {
+        bm = bm + __shfl_xor_sync(full, bm, o, W);   // at most one nonzero term: exact
+        dd = fmax(dd, __shfl_xor_sync(full, dd, o, W));
+        bad_phi = max(bad_phi, __shfl_xor_sync(full, bad_phi, o, W));
+        bad_lt = max(bad_lt, __shfl_xor_sync(full, bad_lt, o, W));
     }
-    const bool anynan = __any_sync(full, nan);
-    const int nskel = __popc(__ballot_sync(full, in));
-    if (lane == 0) {
+    const bool anynan = half_bits(__ballot_sync(full, nan)) != 0;
+    const int nskel = __popc(half_bits(__ballot_sync(full, in)));
+    if (act && sl == 0) {
         VRes res;
         vres_init(res);
         res.nan = anynan; res.bad_phi_row = bad_phi; res.bad_lt_row = bad_lt;
@@ -1060,9 +1065,13 @@ __device__ __forceinline__ void warp_column(int j, const StepParams& p, const Qu
         ws.skel += nskel;
     }
     // output: dense for at most two rows, else a pool range
+    long long off = 0;
+    if (act && cnt > 2 && sl == 0) off = (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)cnt);
+    off = __shfl_sync(full, off, 0, W);
+    if (!act) return;
     if (cnt <= 2) {
         if (cnt == 0) {
-            if (lane == 0) p.out.sig[j] = FT_SIG_EMPTY;
+            if (sl == 0) p.out.sig[j] = FT_SIG_EMPTY;
         } else if (out) {
             if (pos == 0) {
                 p.out.sig[j] = cnt == 2 ? (r | kPair) : r;
@@ -1075,14 +1084,11 @@ __device__ __forceinline__ void warp_column(int j, const StepParams& p, const Qu
         }
         return;
     }
-    long long off = 0;
-    if (lane == 0) off = (long long)atomicAdd(&p.ws.ctl->pool_next, (unsigned long long)cnt);
-    off = __shfl_sync(full, off, 0);
     if (off + cnt > p.cap) {
-        if (lane == 0) atomicExch(&p.ws.ctl->overflow, 1);
+        if (sl == 0) atomicExch(&p.ws.ctl->overflow, 1);
         return;
     }
-    if (lane == 0) { p.out.sig[j] = -cnt; p.out.aux[j] = (int)off; }
+    if (sl == 0) { p.out.sig[j] = -cnt; p.out.aux[j] = (int)off; }
     if (out) {
         p.out.pidx[off + pos] = r;
         ((T*)p.out.pval)[off + pos] = (T)nv;
@@ -1497,8 +1503,16 @@ __global__ void __launch_bounds__(FT_TPB, 4) warp_kernel(const StepParams p, con
     const int nw = gridDim.x * FT_WARPS;
     WarpStats ws;
     ws.maxd = 0.0; ws.cnt = 0; ws.skel = 0;
-    for (int i = (blockIdx.x * FT_TPB + threadIdx.x) >> 5; i < nc; i += nw)
-        warp_column<T, UNIFORM, PACKED>(__ldg(&qs.q[qs.dir * i]), p, qs, lane, ws);
+    // two columns per warp and pass (uniform trip count over the warp)
+    for (int i0 = 2 * ((blockIdx.x * FT_TPB + threadIdx.x) >> 5); i0 < nc; i0 += 2 * nw) {
+        const int i = i0 + (lane >> 4);
+        const bool have = i < nc;
+        half_column<T, UNIFORM, PACKED>(have ? __ldg(&qs.q[qs.dir * i]) : p.j_base, have, p, qs, lane, ws);
+    }
+    // lanes 0 and 16 hold the halves' statistics
+    ws.maxd = fmax(ws.maxd, __shfl_down_sync(0xffffffffu, ws.maxd, 16));
+    ws.cnt += __shfl_down_sync(0xffffffffu, ws.cnt, 16);
+    ws.skel += __shfl_down_sync(0xffffffffu, ws.skel, 16);
     if (lane == 0 && (ws.maxd > 0.0 || ws.cnt || ws.skel)) {
         if (ws.maxd > 0.0) atomicMax(&p.ws.ctl->maxdelta_bits, (unsigned long long)__double_as_longlong(ws.maxd));
         if (ws.skel) atomicAdd(&p.ws.ctl->skel_total, (unsigned long long)ws.skel);
