@@ -2010,15 +2010,37 @@ static int check_tiled(const ft_tiled* t, int n_rows, int n_cols) {
     return FT_OK;
 }
 
-static int g_init = 0;
+// Per-device state (a process may drive several GPUs): whether c_recip is
+// set on the device, grid sizes, the side stream with its fork / join events
+// and the evolve-graph stream.  Indexed by the current device ordinal.
+struct DevState {
+    int init;
+    int fixup_grid, sms;
+    cudaStream_t side;
+    cudaEvent_t fork, join;
+    cudaStream_t gstream;
+    cudaEvent_t gev[2];
+};
+static DevState g_dev[64];
 
-// side stream (highest priority) for the tier-2 pipeline of queue A, and its
-// fork / join events (captured into the evolve graph like any stream work)
-static cudaStream_t g_side = nullptr;
-static cudaEvent_t g_fork, g_join;
+static DevState& dev_state() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return g_dev[d & 63];
+}
+
+#define g_init (dev_state().init)
+#define g_fixup_grid (dev_state().fixup_grid)
+#define g_sms (dev_state().sms)
+#define g_side (dev_state().side)
+#define g_fork (dev_state().fork)
+#define g_join (dev_state().join)
+#define g_gstream (dev_state().gstream)
+#define g_gev (dev_state().gev)
 
 // FT_PROBE_EVENTS=1 (timing probes only): events at the stage boundaries of
-// the last launch_step, read with ft_probe_timeline (debug export)
+// the last launch_step, read with ft_probe_timeline (debug export; first
+// device only)
 static cudaEvent_t g_pev[8];
 static int g_pev_on = -1;
 
@@ -2044,33 +2066,33 @@ extern "C" int ft_probe_timeline(float* ms, int n) {
 }
 
 static int side_init() {
-    if (g_side) return FT_OK;
+    DevState& d = dev_state();
+    if (d.side) return FT_OK;
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    if (cudaStreamCreateWithPriority(&g_side, cudaStreamNonBlocking, hi) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g_join, cudaEventDisableTiming) != cudaSuccess) {
-        g_side = nullptr;
+    if (cudaStreamCreateWithPriority(&d.side, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.join, cudaEventDisableTiming) != cudaSuccess) {
+        d.side = nullptr;
         return FT_ERR_CUDA;
     }
     return FT_OK;
 }
-static int g_fixup_grid = 4 * 148;
-static int g_sms = 148;
 
 static void lib_init() {
-    if (g_init) return;
+    DevState& d = dev_state();
+    if (d.init) return;
     double h[33];
     h[0] = 0.0;
     for (int n = 1; n <= 32; ++n) h[n] = 1.0 / (double)n;
     cudaMemcpyToSymbol(ft::c_recip, h, sizeof(h));
-    g_init = 1;
     int dev = 0, sms = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess &&
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) {
-        g_fixup_grid = 4 * sms;
-        g_sms = sms;
-    }
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        sms = 148;
+    d.fixup_grid = 4 * sms;
+    d.sms = sms;
+    d.init = 1;
 }
 
 // which = 1: tier 1, 2: tiers 1.5-3, 3: both
@@ -2305,15 +2327,13 @@ static int g_graph_next = 0;
 // private non-blocking stream for capture and replay (the caller's stream may
 // be the legacy default stream, which cannot be captured); ordered against the
 // caller's stream with events
-static cudaStream_t g_gstream = nullptr;
-static cudaEvent_t g_gev[2];
-
 static int graph_stream_init() {
-    if (g_gstream) return FT_OK;
-    if (cudaStreamCreateWithFlags(&g_gstream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g_gev[0], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g_gev[1], cudaEventDisableTiming) != cudaSuccess) {
-        g_gstream = nullptr;
+    DevState& d = dev_state();
+    if (d.gstream) return FT_OK;
+    if (cudaStreamCreateWithFlags(&d.gstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.gev[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.gev[1], cudaEventDisableTiming) != cudaSuccess) {
+        d.gstream = nullptr;
         return FT_ERR_CUDA;
     }
     return FT_OK;
