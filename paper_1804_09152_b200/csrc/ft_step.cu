@@ -821,26 +821,31 @@ __global__ void __launch_bounds__(FT_TPB, 8) tier1_kernel(const StepParams p) {
     const int nseg = FT_WARPS * p.num_tiles;
     const int nw = gridDim.x * FT_WARPS;
     int seg = (blockIdx.x * FT_TPB + threadIdx.x) >> 5;
-    int4 pk = make_int4(0, 0, 0, 0);
-    double phs = 0.0;
+    // two segments of loads in flight ahead of the one being classified
+    int4 pk = make_int4(0, 0, 0, 0), pk1 = make_int4(0, 0, 0, 0);
+    double phs = 0.0, ph1 = 0.0;
     {
-        const int jl = seg * 32 + lane;
+        const int jl = seg * 32 + lane, jl1 = (seg + nw) * 32 + lane;
         if (seg < nseg && jl < p.n_v) {
             if (PACKED) pk = __ldg(&p.lap_pack[jl]);
             phs = ldv<T>(p.in.v0, p.j_base + jl);
+        }
+        if (seg + nw < nseg && jl1 < p.n_v) {
+            if (PACKED) pk1 = __ldg(&p.lap_pack[jl1]);
+            ph1 = ldv<T>(p.in.v0, p.j_base + jl1);
         }
     }
     for (; seg < nseg; seg += nw) {
         int4 pk2 = make_int4(0, 0, 0, 0);
         double ph2 = 0.0;
-        const int jl2 = (seg + nw) * 32 + lane;
-        if (seg + nw < nseg && jl2 < p.n_v) {
+        const int jl2 = (seg + 2 * nw) * 32 + lane;
+        if (seg + 2 * nw < nseg && jl2 < p.n_v) {
             if (PACKED) pk2 = __ldg(&p.lap_pack[jl2]);
             ph2 = ldv<T>(p.in.v0, p.j_base + jl2);
         }
         tier1_segment<T, UNIFORM, PACKED>(p, seg, lane, chk, pk, phs);
-        pk = pk2;
-        phs = ph2;
+        pk = pk1; phs = ph1;
+        pk1 = pk2; ph1 = ph2;
     }
 }
 
