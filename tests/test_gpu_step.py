@@ -244,3 +244,78 @@ def test_four_symmetric_seeds_exhaust_base():
     seeds = [50 * 12 + 12, 50 * 12 + 37, 50 * 37 + 12, 50 * 37 + 37]
     out, trace = ft.evolve(ft.init_field(mesh, seeds), lap, DEFAULT, max_steps=2500)
     assert trace[-1].converged and trace[-1].base_mass < 1e-9 * mesh.n_vertices
+
+
+def _random_field(rng, n_v, n_rows, max_cnt, row_pool):
+    """A field whose columns hold 0..max_cnt random rows out of ``row_pool``
+    (sorted, values in (0, 1], columns normalised like the reference's)."""
+    cols = []
+    for _ in range(n_v):
+        c = int(rng.integers(1 if max_cnt == 1 else 0, max_cnt + 1))
+        rows = np.sort(rng.choice(row_pool, size=min(c, len(row_pool)), replace=False))
+        vals = rng.random(rows.size) + 0.05
+        vals = vals / vals.sum() if rows.size else vals
+        cols.append((rows.astype(np.int32), vals))
+    cnt = np.array([r.size for r, _ in cols])
+    cp = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int32)
+    ri = np.concatenate([r for r, _ in cols]).astype(np.int32) if cp[-1] else np.zeros(0, np.int32)
+    va = np.concatenate([v for _, v in cols]) if cp[-1] else np.zeros(0)
+    return ft.SparseMat(n_rows, n_v, cp, ri, va, check=False)
+
+
+def _tier_counts(phi, lap):
+    """Queue counters of the control block after the fixup launches of one
+    step (read before the finalize resets them)."""
+    import ctypes
+    import torch
+    from paper_1804_09152_b200 import _lib
+    from paper_1804_09152_b200 import field as F
+    lib = _lib.lib()
+    d = ft.DeviceCSC.from_host(phi, torch.float64, torch.device("cuda"))
+    ws = ft.StepWorkspace()
+    ws.prepare(phi.n_cols, d.values.device)
+    a = ft.DeviceTiled(phi.n_rows, phi.n_cols, 4 * phi.nnz + 64, torch.float64, d.values.device)
+    b = ft.DeviceTiled(phi.n_rows, phi.n_cols, 4 * phi.nnz + 64, torch.float64, d.values.device)
+    dl = F.device_laplacian(lap, "exact")
+    lc, prm, st = dl.ft_csc("exact"), DEFAULT.ft_params(), F._stream_handle()
+    wp, wn = ws.ws_args()
+    s_c, a_c, b_c = d.ft_csc(), a.ft_tiled(), b.ft_tiled()
+    rec = ctypes.c_void_p(ws.stats.data_ptr())
+    assert lib.ft_tiled_from_csc(ctypes.byref(s_c), ctypes.byref(b_c), 0, wp, wn, rec, st) == 0
+    assert lib.ft_step_kernel(ctypes.byref(lc), dl.launch_flags(), ctypes.byref(b_c), ctypes.byref(a_c), 0,
+                              ctypes.byref(prm), wp, wn, st) == 0
+    assert lib.ft_step_fixup(ctypes.byref(lc), dl.launch_flags(), ctypes.byref(b_c), ctypes.byref(a_c), 0,
+                             ctypes.byref(prm), wp, wn, st) == 0
+    c = ws.ws[:128].cpu().numpy()
+    i32 = lambda o: int(c[o:o + 4].view(np.int32)[0])
+    counts = {"queue_a": i32(56), "queue_b": i32(68), "tier2b": i32(96), "tier3": i32(64) + i32(112)}
+    assert lib.ft_step_finalize(wp, wn, phi.n_cols, a.capacity, rec, st) == 0
+    return counts
+
+
+@pytest.mark.parametrize("max_cnt,n_pool,seed,tier", [
+    (2, 6, 1, "queue_b"),   # two entries per column at most: tier 1.5 and its deferrals
+    (3, 8, 2, "queue_a"),   # pool columns: queue A (tiers 2a / 2b)
+    (4, 12, 3, "tier2b"),   # wider unions: tier 2b
+    (9, 16, 4, "tier3"),    # beyond the 8-row window / 16 entries: tier 3
+])
+def test_random_fields_every_tier(max_cnt, n_pool, seed, tier):
+    """Random fields on a small torus drive every tier (1, 1.5, queue B's
+    16-lane groups, 2a, 2b, 3); one step and a 5-step evolve are bitwise
+    equal to the C oracle."""
+    rng = np.random.default_rng(seed)
+    mesh = ft.gen_periodic_grid(24, 20)
+    lap = ft.build_laplacian(mesh)
+    n_rows = 17
+    phi = _random_field(rng, mesh.n_vertices, n_rows, max_cnt, np.arange(n_rows)[:n_pool])
+    fld = ft.LayeredField(phi, np.arange(n_rows - 1))
+    assert _tier_counts(phi, lap)[tier] > 0          # the case reaches the tier it names
+    lt = po.Csc.of(ft.field._with_diagonal(lap.mat_t))
+    out, st = ft.step(fld, lap, DEFAULT)
+    ref1, rst = po.step_c(po.Csc.of(phi), lt, DEFAULT)
+    assert_csc_equal(out.phi, ref1)
+    assert st.max_delta == rst["max_delta"] and st.nnz_skel == rst["nnz_skel"]
+    out5, trace = ft.evolve(fld, lap, DEFAULT, max_steps=5, tol=0.0)
+    ref5, rtrace = po.evolve_c(po.Csc.of(phi), lt, DEFAULT, 5)
+    assert_csc_equal(out5.phi, ref5)
+    assert [s.max_delta for s in trace] == [s["max_delta"] for s in rtrace]
