@@ -2174,7 +2174,7 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
         pev(5, s);
         // queue B: what tier 1.5 defers (unions of three or more rows), one
         // warp per column
-        FT_PICK3(ft::warp_kernel, dtype, uni, packed)<<<g_fixup_grid * 4, FT_TPB, 0, s>>>(p, qb);
+        FT_PICK3(ft::warp_kernel, dtype, uni, packed)<<<g_fixup_grid * 2, FT_TPB, 0, s>>>(p, qb);
         // (its tier-3 list is empty unless a column exceeds one warp)
         FT_PICK2(ft::deep_kernel, dtype, uni)<<<g_fixup_grid / 8, FT_TPB, 0, s>>>(p, qb);
         pev(6, s);
