@@ -69,15 +69,18 @@ struct Workspace {
     long long*    fin_skel;     // [FT_FIN_MAX] finalize partial skeleton nnz
     int           num_tiles;
     int           num_chunks;
+    size_t        par_off;      // bytes between the parity-0 and parity-1 segment slots
 };
 
 __host__ __device__ inline int num_tiles_for(int n_v) { return (n_v + FT_TPB - 1) / FT_TPB; }
 __host__ __device__ inline int num_chunks_for(int n_v) { return (n_v + FT_CCH - 1) / FT_CCH; }
 
+// the per-segment slots written by tier 1 exist twice (step parity), so
+// that ft_evolve can finalize step k while tier 1 of step k + 1 runs
 inline size_t workspace_bytes(int n_v) {
     const size_t t = (size_t)num_tiles_for(n_v), c = (size_t)num_chunks_for(n_v), v = (size_t)n_v;
-    return sizeof(Control) + 4 * t * (8 + 8 + 8 + 4 + 4) + t * (8 + 8 + 8) + v * 8 + 3 * v * 4 +
-           (c + 2) * 8 + 4 * FT_FIN_MAX * 8 + 16 * 16;
+    return sizeof(Control) + 2 * 4 * t * (8 + 8 + 8 + 4 + 4) + t * (8 + 8 + 8) + v * 8 + 3 * v * 4 +
+           (c + 2) * 8 + 4 * FT_FIN_MAX * 8 + 24 * 16;
 }
 
 static_assert(FT_WARPS == 4, "segment masks are read as one uint4 per tile");
@@ -92,11 +95,15 @@ inline Workspace carve_workspace(void* base, int n_v) {
     w.num_tiles = num_tiles_for(n_v);
     w.num_chunks = num_chunks_for(n_v);
     const size_t ns = 4 * (size_t)w.num_tiles, nt = (size_t)w.num_tiles;
+    // parity 0 copies; parity 1 at par_off bytes further (ws_parity)
+    char* seg0 = p;
     w.seg_bm = (double*)p;       p = align16(p + ns * 8);
     w.seg_maxd = (double*)p;     p = align16(p + ns * 8);
     w.seg_cs = (int2*)p;         p = align16(p + ns * 8);
     w.gen_mask = (unsigned int*)p; p = align16(p + ns * 4);
     w.slow_mask = (unsigned int*)p; p = align16(p + ns * 4);
+    w.par_off = (size_t)(p - seg0);
+    p += w.par_off;
     w.gen_bm = (double*)p;       p = align16(p + nt * 8);
     w.gen_maxd = (double*)p;     p = align16(p + nt * 8);
     w.gen_cs = (int2*)p;         p = align16(p + nt * 8);
@@ -107,6 +114,18 @@ inline Workspace carve_workspace(void* base, int n_v) {
     w.fin_maxd = (double*)p;     p += FT_FIN_MAX * 8;
     w.fin_cnt = (long long*)p;   p += FT_FIN_MAX * 8;
     w.fin_skel = (long long*)p;  p += FT_FIN_MAX * 8;
+    return w;
+}
+
+// the workspace view of step parity `par` (its segment slots)
+inline Workspace ws_parity(Workspace w, int par) {
+    if (par & 1) {
+        w.seg_bm = (double*)((char*)w.seg_bm + w.par_off);
+        w.seg_maxd = (double*)((char*)w.seg_maxd + w.par_off);
+        w.seg_cs = (int2*)((char*)w.seg_cs + w.par_off);
+        w.gen_mask = (unsigned int*)((char*)w.gen_mask + w.par_off);
+        w.slow_mask = (unsigned int*)((char*)w.slow_mask + w.par_off);
+    }
     return w;
 }
 

@@ -2025,6 +2025,7 @@ struct DevState {
     cudaEvent_t fork, join;
     cudaStream_t gstream;
     cudaEvent_t gev[2];
+    cudaEvent_t bdone, fdone, sjoin;   // evolve: queue B done, finalize done, side joined
 };
 static DevState g_dev[64];
 
@@ -2077,7 +2078,10 @@ static int side_init() {
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     if (cudaStreamCreateWithPriority(&d.side, cudaStreamNonBlocking, hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&d.join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&d.join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.bdone, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.fdone, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.sjoin, cudaEventDisableTiming) != cudaSuccess) {
         d.side = nullptr;
         return FT_ERR_CUDA;
     }
@@ -2104,9 +2108,14 @@ static void lib_init() {
 // dom == nullptr: the whole field; otherwise the owned column range of a
 // partitioned field (lap_t then holds the owned columns of L^T only and the
 // workspace is sized for the owned columns)
+// parity: the step's segment-slot copy (ft_evolve alternates it); fin_wait
+// (nullable): the previous step's finalize, waited for before tier 1.5
+// touches the shared slots and accumulators; b_done (nullable): recorded
+// after queue B (the side-stream finalize of this step waits on it)
 static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* in, ft_tiled* out,
                        int32_t dtype, const ft_params* prm, void* workspace, size_t ws_bytes, int check_done,
-                       cudaStream_t s, int which = 3, const ft_domain* dom = nullptr) {
+                       cudaStream_t s, int which = 3, const ft_domain* dom = nullptr, int parity = 0,
+                       cudaEvent_t fin_wait = nullptr, cudaEvent_t b_done = nullptr) {
     if (!lap_t || !out || !in || !prm || !workspace) return set_err(FT_ERR_ARG, "null argument");
     if (dtype != FT_F64 && dtype != FT_F32) return set_err(FT_ERR_ARG, "bad dtype");
     const int n_rows = in->n_rows, n_v = in->n_cols;
@@ -2134,7 +2143,7 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
     p.out = ft::hyb_out(out);
     p.cap = step_cap;
     p.w = prm->w; p.a = prm->a; p.e = prm->e; p.eb = prm->e_base; p.mu = prm->mu; p.dt = prm->dt;
-    p.ws = ft::carve_workspace(workspace, n_own);
+    p.ws = ft::ws_parity(ft::carve_workspace(workspace, n_own), parity);
     p.check_done = check_done;
     p.finite = std::isfinite(p.w) && std::isfinite(p.a) && std::isfinite(p.e) && std::isfinite(p.eb) &&
                std::isfinite(p.mu) && std::isfinite(p.dt);
@@ -2159,6 +2168,7 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
         // concurrently with tier 1.5
         if (side_init() != FT_OK) return cuda_check("side stream");
         const ft::Queues qa = ft::queues(p, 0), qb = ft::queues(p, 1);
+        if (fin_wait) cudaStreamWaitEvent(s, fin_wait, 0);
         cudaEventRecord(g_fork, s);
         cudaStreamWaitEvent(g_side, g_fork, 0);
         ft::queue_kernel<<<(FT_WARPS * p.num_tiles + 255) / 256, 256, 0, g_side>>>(p);
@@ -2178,6 +2188,7 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
         // (its tier-3 list is empty unless a column exceeds one warp)
         FT_PICK2(ft::deep_kernel, dtype, uni)<<<g_fixup_grid / 8, FT_TPB, 0, s>>>(p, qb);
         pev(6, s);
+        if (b_done) cudaEventRecord(b_done, s);
         cudaStreamWaitEvent(s, g_join, 0);
         pev(7, s);
     }
@@ -2185,9 +2196,9 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
 }
 
 static void launch_finalize(const ft::Workspace& ws, ft_step_stats* trace, long long tiled_cap,
-                            int evolve, int max_steps, double tol, double thr, cudaStream_t s) {
+                            int evolve, int max_steps, double tol, double thr, cudaStream_t s, int parity = 0) {
     ft::FinalizeParams f;
-    f.ws = ws; f.trace = trace; f.tiled_cap = tiled_cap; f.fixed_slot = evolve ? 0 : 1;
+    f.ws = ft::ws_parity(ws, parity); f.trace = trace; f.tiled_cap = tiled_cap; f.fixed_slot = evolve ? 0 : 1;
     f.evolve = evolve; f.max_steps = max_steps; f.tol = tol; f.base_threshold = thr;
     lib_init();
     // about one 32-column segment per thread
@@ -2371,24 +2382,39 @@ extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* p
     if (ws_bytes < ft::workspace_bytes(phi_in->n_cols)) return set_err(FT_ERR_ARG, "workspace too small");
     cudaStream_t s = (cudaStream_t)stream;
     ft::Workspace ws = ft::carve_workspace(workspace, phi_in->n_cols);
+    if (side_init() != FT_OK) return cuda_check("ft_evolve(side stream)");
+    DevState& d = dev_state();
+    // Step i runs on the main stream (tier 1, 1.5, queue B) and the side
+    // stream (queue A); its finalize runs on the side stream once queue B is
+    // done, overlapping tier 1 of step i + 1 (which writes the other parity's
+    // segment slots); tier 1.5 of step i + 1 waits for that finalize.
+    auto step = [&](int i, const ft_tiled* in_t, ft_tiled* out, long long cap, cudaStream_t ms,
+                    bool wait_prev) -> int {
+        const int r = launch_step(lap_t, lap_flags, in_t, out, dtype, params, workspace, ws_bytes, 1, ms, 3,
+                                  nullptr, i & 1, wait_prev ? d.fdone : nullptr, d.bdone);
+        if (r != FT_OK) return r;
+        cudaStreamWaitEvent(d.side, d.bdone, 0);
+        launch_finalize(ws, trace, cap, 1, max_steps, tol, base_threshold, d.side, i & 1);
+        cudaEventRecord(d.fdone, d.side);
+        return FT_OK;
+    };
     ft::evolve_reset_kernel<<<1, 1, 0, s>>>(ws.ctl);
     // canonical input -> b, step 1: b -> a
     int rc = launch_convert(phi_in, work_b, dtype, ws, s);
     if (rc != FT_OK) return rc;
-    rc = launch_step(lap_t, lap_flags, work_b, work_a, dtype, params, workspace, ws_bytes, 1, s);
-    if (rc != FT_OK) return rc;
     const long long cap0 = work_a->capacity < work_b->capacity ? work_a->capacity : work_b->capacity;
-    launch_finalize(ws, trace, cap0, 1, max_steps, tol, base_threshold, s);
+    rc = step(0, work_b, work_a, cap0, s, false);
+    if (rc != FT_OK) return rc;
     const int rest = max_steps - 1;
-    if (rest > 0 && rest < kGraphSteps) {
+    if (rest < kGraphSteps) {
         for (int i = 1; i < max_steps; ++i) {
             ft_tiled* out = (i & 1) ? work_b : work_a;
             const ft_tiled* in_t = (i & 1) ? work_a : work_b;
-            rc = launch_step(lap_t, lap_flags, in_t, out, dtype, params, workspace, ws_bytes, 1, s);
+            rc = step(i, in_t, out, out->capacity, s, true);
             if (rc != FT_OK) return rc;
-            launch_finalize(ws, trace, out->capacity, 1, max_steps, tol, base_threshold, s);
         }
-    } else if (rest > 0) {
+        cudaStreamWaitEvent(s, d.fdone, 0);     // the last finalize
+    } else {
         GraphKey k;
         memset(&k, 0, sizeof(k));
         if (graph_stream_init() != FT_OK) return cuda_check("ft_evolve(graph stream)");
@@ -2404,6 +2430,11 @@ extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* p
         memcpy(k.prm, prm, sizeof(prm));
         const int ints[5] = {lap_flags, dtype, max_steps, phi_in->n_cols, phi_in->n_rows};
         memcpy(k.ints, ints, sizeof(ints));
+        // the graph's first step starts after the previous finalize (step 0's
+        // here, the previous replay's last one inside the graph's end join)
+        cudaEventRecord(g_gev[0], s);
+        cudaStreamWaitEvent(gs, g_gev[0], 0);
+        cudaStreamWaitEvent(gs, d.fdone, 0);
         cudaGraphExec_t exec = graph_lookup(k);
         if (!exec) {
             cudaGraph_t graph;
@@ -2412,10 +2443,11 @@ extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* p
             for (int i = 1; i <= kGraphSteps; ++i) {
                 ft_tiled* out = (i & 1) ? work_b : work_a;
                 const ft_tiled* in_t = (i & 1) ? work_a : work_b;
-                const int r2 = launch_step(lap_t, lap_flags, in_t, out, dtype, params, workspace, ws_bytes, 1, gs);
+                const int r2 = step(i, in_t, out, out->capacity, gs, i > 1);
                 if (r2 != FT_OK) rc = r2;
-                launch_finalize(ws, trace, out->capacity, 1, max_steps, tol, base_threshold, gs);
             }
+            cudaEventRecord(d.sjoin, d.side);   // the side stream rejoins the capture
+            cudaStreamWaitEvent(gs, d.sjoin, 0);
             const cudaError_t ec = cudaStreamEndCapture(gs, &graph);
             if (ec != cudaSuccess || rc != FT_OK) return rc != FT_OK ? rc : cuda_check("ft_evolve(end capture)");
             if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
@@ -2425,8 +2457,6 @@ extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* p
             cudaGraphDestroy(graph);
             graph_store(k, exec);
         }
-        cudaEventRecord(g_gev[0], s);
-        cudaStreamWaitEvent(gs, g_gev[0], 0);
         for (int done = 0; done < rest; done += kGraphSteps) cudaGraphLaunch(exec, gs);
         cudaEventRecord(g_gev[1], gs);
         cudaStreamWaitEvent(s, g_gev[1], 0);
