@@ -2450,7 +2450,8 @@ extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* p
             cudaStreamWaitEvent(gs, d.sjoin, 0);
             const cudaError_t ec = cudaStreamEndCapture(gs, &graph);
             if (ec != cudaSuccess || rc != FT_OK) return rc != FT_OK ? rc : cuda_check("ft_evolve(end capture)");
-            if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+            // node priorities: queue A keeps its side stream's high priority
+            if (cudaGraphInstantiateWithFlags(&exec, graph, cudaGraphInstantiateFlagUseNodePriority) != cudaSuccess) {
                 cudaGraphDestroy(graph);
                 return cuda_check("ft_evolve(instantiate)");
             }
