@@ -365,6 +365,35 @@ class TorchTransport:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return int(t.item())
 
+    def gather_owned(self, ranks, steps_done):
+        """Every rank's owned columns, in rank order, on every rank: (column
+        counts, rows, values) as host arrays per rank (all_gather of the
+        padded device arrays: NCCL over NVLink)."""
+        torch = _torch()
+        (r,) = ranks
+        f = r.owned_field(steps_done)
+        dev = f.values.device if self.nccl else "cpu"
+        cnt = (f.col_ptr[1:] - f.col_ptr[:-1]).to(torch.int32)
+        sizes = torch.tensor([r.n_own, f.nnz], dtype=torch.int64, device=dev)
+        all_sizes = [torch.zeros_like(sizes) for _ in range(self.world)]
+        self.dist.all_gather(all_sizes, sizes, group=self.group)
+        all_sizes = [tuple(int(x) for x in t.cpu()) for t in all_sizes]
+        mo = max(a for a, _ in all_sizes)
+        mn = max(max(b for _, b in all_sizes), 1)
+
+        def pad(t, n):
+            out = torch.zeros(n, dtype=t.dtype, device=dev)
+            out[:t.numel()] = t.to(dev)
+            return out
+
+        parts = []
+        for t, n in ((cnt, mo), (f.row_idx[:f.nnz], mn), (f.values[:f.nnz].double(), mn)):
+            mine = pad(t, n)
+            got = [torch.zeros_like(mine) for _ in range(self.world)]
+            self.dist.all_gather(got, mine, group=self.group)
+            parts.append([g.cpu().numpy() for g in got])
+        return [(parts[0][q][:a], parts[1][q][:b], parts[2][q][:b]) for q, (a, b) in enumerate(all_sizes)]
+
 
 class LoopbackTransport:
     """All ranks live in this process (one device): collectives are copies.
@@ -390,6 +419,15 @@ class LoopbackTransport:
 
     def max_int(self, values):
         return max(int(v) for v in values)
+
+    def gather_owned(self, ranks, steps_done):
+        out = []
+        for r in sorted(ranks, key=lambda x: x.col_begin):
+            h = r.owned_field(steps_done).to_host()
+            cp = np.asarray(h.col_ptr, dtype=np.int64)
+            out.append((np.diff(cp).astype(np.int32), np.asarray(h.row_idx[:cp[-1]]),
+                        np.asarray(h.values[:cp[-1]], dtype=np.float64)))
+        return out
 
 
 # ---------------------------------------------------------------------------
@@ -773,3 +811,55 @@ def gather_field(ranks, steps_done=None, n_rows=None, renumbering=None):
                     np.concatenate(idx) if idx else np.zeros(0, INDEX),
                     np.concatenate(vals) if vals else np.zeros(0), check=False)
     return out if renumbering is None else renumbering.restore(out)
+
+
+def assemble_owned(parts, n_rows, n_vertices, renumbering=None):
+    """Host SparseMat of the whole field from the ranks' owned parts (rank
+    order = column order), in the mesh's vertex ids."""
+    cnt = np.concatenate([c for c, _, _ in parts]).astype(np.int64)
+    cp = np.concatenate([[0], np.cumsum(cnt)])
+    out = SparseMat(n_rows, n_vertices, cp, np.concatenate([r for _, r, _ in parts]).astype(INDEX),
+                    np.concatenate([v for _, _, v in parts]), check=False)
+    return out if renumbering is None else renumbering.restore(out)
+
+
+def lloyd_iterate_partitioned(state, mesh, lap, params, n_iter, transport, partition, local_ranks,
+                              max_steps=1000, tol=1e-4, precision="exact", renumbering=None, device=None):
+    """:func:`lloyd.lloyd_iterate` (lloyd.py:198-229) with every evolve
+    partitioned over the ranks (vertex row partition, NCCL halo exchange)
+    and the reseed replicated on every rank: the owned fields are
+    all-gathered, then the single-GPU centroid / back-projection
+    kernels and the order-dependent collision pass run on the whole field,
+    identically everywhere.  The seeds and the history equal
+    ``lloyd_iterate``'s (the partitioned evolve is bitwise the single-GPU
+    one); ``local_ranks`` are the rank ids this process drives (one for a
+    TorchTransport, all for a LoopbackTransport)."""
+    from . import lloyd as LL
+    from .field import LayeredField, init_field
+    if n_iter < 1:
+        raise ShapeError("n_iter must be >= 1")
+
+    def run_evolve(seeds, fld=None):
+        fld = fld if fld is not None else init_field(mesh, seeds, precision=precision)
+        problems = [local_problem(fld.phi, lap, partition, q, renumbering=renumbering) for q in local_ranks]
+        plans = build_plans(problems, transport)
+        ranks = [DomainRank(pr, pl, precision=precision, device=device, renumbering=renumbering)
+                 for pr, pl in zip(problems, plans)]
+        steps, trace = evolve_partitioned(ranks, transport, params, max_steps=max_steps, tol=tol)
+        parts = transport.gather_owned(ranks, steps)
+        phi = assemble_owned(parts, fld.phi.n_rows, mesh.n_vertices, renumbering)
+        return LayeredField(phi, seeds, steps, precision=precision), trace
+
+    if state.field is None or state.field.step_count == 0:
+        state.field, trace = run_evolve(np.asarray(state.seeds), state.field)
+    else:
+        trace = []
+    if not state.history:
+        LL._record(state, mesh, trace, {"reseed_misses": 0, "seed_collisions": 0})
+    for _ in range(n_iter):
+        seeds, report = LL._reseed(state, mesh)
+        state.seeds = seeds
+        state.iteration += 1
+        state.field, trace = run_evolve(seeds)
+        LL._record(state, mesh, trace, report)
+    return state

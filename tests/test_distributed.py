@@ -187,6 +187,24 @@ def _gloo_worker(rank, world, port, n_steps, out_q):
             for q, cols in plan.recv.items():
                 _unpack(cols, host.recv_msg[q].numpy(), new, slots)
             held = new
+        # the owned fields, all-gathered through the transport (the partitioned
+        # Lloyd step's gather), reassemble the whole reference field
+        own = [held[c] for c in range(b, e)]
+
+        class _Owned:
+            pass
+
+        f = _Owned()
+        f.col_ptr = torch.from_numpy(np.concatenate([[0], np.cumsum([r.size for r, _ in own])]).astype(np.int32))
+        f.row_idx = torch.from_numpy(np.concatenate([r for r, _ in own]).astype(np.int32))
+        f.values = torch.from_numpy(np.concatenate([v for _, v in own]))
+        f.nnz = int(f.row_idx.numel())
+        host.n_own = e - b
+        host.owned_field = lambda steps: f
+        whole = D.assemble_owned(tr.gather_owned([host], n_steps), prob.n_rows, n_v)
+        assert np.array_equal(np.asarray(whole.col_ptr), np.asarray(ref.col_ptr))
+        assert np.array_equal(np.asarray(whole.row_idx[:whole.nnz]), np.asarray(ref.row_idx[:ref.nnz]))
+        assert np.array_equal(np.asarray(whole.values[:whole.nnz]), np.asarray(ref.values[:ref.nnz]))
         assert tr.max_int([rank + 5]) == world + 4
         out_q.put((rank, "ok"))
     except Exception as exc:                    # pragma: no cover - reported to the parent
@@ -376,3 +394,30 @@ def test_loopback_morton_renumbered_matches_single_gpu():
     with pytest.raises(ft.errors.NumericalBlowupError) as e2:
         D.evolve_partitioned(ranks, D.LoopbackTransport(), bad, max_steps=3, tol=0.0)
     assert str(e1.value) == str(e2.value)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,morton", [(2, False), (3, True)])
+def test_partitioned_lloyd_matches_single_gpu(world, morton):
+    """Lloyd relaxation with every evolve partitioned (loopback ranks) and
+    the reseed replicated on the all-gathered field: seeds and history equal
+    the single-GPU lloyd_iterate."""
+    mesh = ft.gen_icosphere(4)
+    lap = ft.build_laplacian(mesh)
+    seeds = ft.sample_seed_vertices(mesh, 48, 5)
+    ref = ft.lloyd_iterate(ft.LloydState(seeds=np.array(seeds)), mesh, lap, ft.CouplingParams(),
+                           n_iter=2, max_steps=60, tol=1e-4)
+    ren = D.Renumbering.morton(mesh) if morton else None
+    part = D.Partition.even(mesh.n_vertices, world)
+    got = D.lloyd_iterate_partitioned(ft.LloydState(seeds=np.array(seeds)), mesh, lap, ft.CouplingParams(),
+                                      2, D.LoopbackTransport(), part, list(range(world)),
+                                      max_steps=60, tol=1e-4, renumbering=ren)
+    assert np.array_equal(np.asarray(got.seeds), np.asarray(ref.seeds))
+    assert len(got.history) == len(ref.history)
+    for a, b in zip(got.history, ref.history):
+        for key in ("iteration", "seeds", "cell_areas", "steps", "reseed_misses", "seed_collisions"):
+            assert a[key] == b[key], key
+    a, b = got.field.phi, ref.field.phi
+    assert np.array_equal(np.asarray(a.col_ptr), np.asarray(b.col_ptr))
+    assert np.array_equal(np.asarray(a.row_idx[:a.nnz]), np.asarray(b.row_idx[:b.nnz]))
+    assert np.array_equal(np.asarray(a.values[:a.nnz]), np.asarray(b.values[:b.nnz]))
