@@ -823,6 +823,17 @@ def assemble_owned(parts, n_rows, n_vertices, renumbering=None):
     return out if renumbering is None else renumbering.restore(out)
 
 
+def gathered_field(ranks, transport, seeds, renumbering=None, precision="exact"):
+    """The whole field on every rank (the all-gathered owned columns) as a
+    LayeredField in the mesh's vertex ids: the input of the dual-mesh API
+    (dual.py) and of any other whole-field consumer."""
+    from .field import LayeredField
+    steps = ranks[0].steps_done
+    parts = transport.gather_owned(ranks, steps)
+    phi = assemble_owned(parts, ranks[0].n_rows, ranks[0].n_v, renumbering)
+    return LayeredField(phi, seeds, steps, precision=precision)
+
+
 def lloyd_iterate_partitioned(state, mesh, lap, params, n_iter, transport, partition, local_ranks,
                               max_steps=1000, tol=1e-4, precision="exact", renumbering=None, device=None):
     """:func:`lloyd.lloyd_iterate` (lloyd.py:198-229) with every evolve

@@ -67,3 +67,32 @@ def test_dual_c1_matches_reference():
 @pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "c2_dual.json")), reason="no C2 dual golden")
 def test_dual_c2_matches_reference():
     _check_case("c2_dual.json", "c2_traj.npz", 1000, ft.gen_icosphere(7))
+
+
+@pytest.mark.gpu
+def test_dual_from_partitioned_evolve_matches_reference():
+    """C1 evolved on 3 loopback ranks (Morton-renumbered partition), the owned
+    fields all-gathered (distributed.gathered_field), then the dual API: the
+    reference's C1 dual, exactly."""
+    from paper_1804_09152_b200 import distributed as D
+    mesh = ft.gen_icosphere(4)
+    lap = ft.build_laplacian(mesh)
+    f0 = _field("c1_traj.npz", 0)
+    ren = D.Renumbering.morton(mesh)
+    part = D.Partition.even(mesh.n_vertices, 3)
+    tr = D.LoopbackTransport()
+    probs = [D.local_problem(f0.phi, lap, part, r, renumbering=ren) for r in range(3)]
+    plans = D.build_plans(probs, tr)
+    ranks = [D.DomainRank(p, pl, renumbering=ren) for p, pl in zip(probs, plans)]
+    steps, _ = D.evolve_partitioned(ranks, tr, ft.CouplingParams(), max_steps=500, tol=0.0)
+    assert steps == 500
+    fld = D.gathered_field(ranks, tr, f0.seed_vertices, renumbering=ren)
+    ref_fld = _field("c1_traj.npz", 500)
+    assert np.array_equal(np.asarray(fld.phi.values[:fld.phi.nnz]), np.asarray(ref_fld.phi.values[:ref_fld.phi.nnz]))
+    ref = golden_json("c1_dual.json")
+    a_v = ft.vertex_adjacency(fld, 0.25)
+    a_t = ft.triangle_adjacency(fld, mesh, 0.25)
+    cur = ft.confirm_candidates(fld, mesh, a_v, a_t, 0.25)
+    assert sorted(map(list, cur.pairs())) == ref["curated"]
+    dm = ft.build_dual(cur, np.zeros((fld.n_cells, 3)))
+    assert sorted(map(sorted, dm.triangles.tolist())) == ref["triangles"]
