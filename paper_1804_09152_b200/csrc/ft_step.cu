@@ -15,21 +15,26 @@
 // arrays (signature, second row, two values), a wider one in a pool.  Every
 // kernel reads a neighbour's entries directly (no descriptor indirection)
 // and writes its own column at a fixed address (no placement scan, no
-// inter-CTA wait).  Work split over 128-column tiles, one thread per vertex
-// column:
-//   tier 1    tier1_kernel: classification from the neighbours' row
-//             signatures; a single-row neighbourhood (a cell interior,
-//             ~82% of the columns at C3) takes the exact closed form
-//             v' = v * (1 / (0 + v)); the others are flagged per 32-column
-//             segment (bit masks, no atomics);
-//   tier 1.5  gen_kernel, one warp per tile: columns with at most two rows
-//             and at most two entries per neighbour, the update in one pass
-//             (rows = min / max of the candidates, Lt accumulated in
+// inter-CTA wait).  Work split:
+//   tier 1    tier1_kernel (persistent, one warp per 32-column segment at a
+//             time, the next segments' L rows prefetched): classification
+//             from the neighbours' row signatures; a single-row
+//             neighbourhood (a cell interior, ~82% of the columns at C3)
+//             takes the exact closed form v' = v * (1 / (0 + v)); the others
+//             are flagged in the segment's bit masks (no atomics);
+//   tier 1.5  gen_kernel, one warp per three tiles: columns with at most two
+//             rows and at most two entries per neighbour, the update in one
+//             pass (rows = min / max of the candidates, Lt accumulated in
 //             ascending-u order -- exactly the reference accumulator order;
-//             PHI(r, j) arrives through the diagonal u == j);
-//   tier 2/3  wide3_kernel / wide_kernel / deep_kernel: wider columns,
-//             register windows of 3 / 8 rows, then no limit.
-// Statistics go to per-segment / per-tile slots that finalize_kernel
+//             PHI(r, j) arrives through the diagonal u == j); a union of
+//             three or more rows goes to queue B;
+//   queue A   tier 1's wide columns, on a high-priority side stream while
+//             tier 1.5 runs: queue_kernel, wide3_kernel (3-row window),
+//             wide_kernel (8-row window), deep_kernel (no limit);
+//   queue B   warp_kernel after tier 1.5: two columns per warp, 16 lanes
+//             holding a column's neighbourhood entries, sums by shuffles in
+//             the reference's order.
+// Statistics go to per-segment / per-group slots that finalize_kernel
 // reduces in a fixed order (deterministic base mass).  Canonical CSC comes
 // from ft_compact.
 //
