@@ -319,3 +319,21 @@ def test_random_fields_every_tier(max_cnt, n_pool, seed, tier):
     ref5, rtrace = po.evolve_c(po.Csc.of(phi), lt, DEFAULT, 5)
     assert_csc_equal(out5.phi, ref5)
     assert [s.max_delta for s in trace] == [s["max_delta"] for s in rtrace]
+
+
+@pytest.mark.parametrize("max_cnt,n_pool,seed", [(2, 6, 11), (3, 8, 12), (4, 12, 13), (9, 16, 14)])
+def test_random_fields_every_tier_fast(max_cnt, n_pool, seed):
+    """FAST (fp32 storage) through every tier on random fields: one step from
+    the fp32-rounded input within |d| <= 1e-5|ref| + 2e-7 of the oracle."""
+    rng = np.random.default_rng(seed)
+    mesh = ft.gen_periodic_grid(24, 20)
+    lap = ft.build_laplacian(mesh)
+    n_rows = 17
+    phi = _random_field(rng, mesh.n_vertices, n_rows, max_cnt, np.arange(n_rows)[:n_pool])
+    phi32 = ft.SparseMat(phi.n_rows, phi.n_cols, phi.col_ptr, phi.row_idx,
+                         np.asarray(phi.values[:phi.nnz], dtype=np.float32).astype(np.float64), check=False)
+    out, _ = ft.step(ft.LayeredField(phi32, np.arange(n_rows - 1), precision="fast"), lap, DEFAULT)
+    lt = po.Csc.of(ft.field._with_diagonal(lap.mat_t))
+    ref, _ = po.step_c(po.Csc.of(phi32), lt, DEFAULT)
+    got, want = out.phi.to_dense(), ref.to_dense()
+    assert np.all(np.abs(got - want) <= 1e-5 * np.abs(want) + 2e-7)
