@@ -109,7 +109,8 @@ typedef struct {
  *   sig[j] <= -3            -sig[j] entries at pool_idx / pool_val
  *                           [aux[j], aux[j] - sig[j])
  * The dense arrays have n_cols entries; pool offsets index pool_idx /
- * pool_val.  A view of a column range offsets the four dense pointers. */
+ * pool_val.  A view of a column range offsets the four dense pointers.
+ * At most 2^30 layer rows (FT_ERR_SHAPE otherwise). */
 typedef struct {
     int32_t  n_rows;
     int32_t  n_cols;

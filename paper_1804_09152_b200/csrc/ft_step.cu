@@ -2014,6 +2014,8 @@ extern "C" int64_t ft_tiled_min_capacity(int32_t n_vertices) {
 
 static int check_tiled(const ft_tiled* t, int n_rows, int n_cols) {
     if (!t || !t->sig || !t->aux || !t->v0 || !t->v1) return set_err(FT_ERR_ARG, "null hybrid buffer");
+    if (n_rows < 1 || n_rows > FT_SIG_PAIR)
+        return set_err(FT_ERR_SHAPE, "the hybrid layout holds at most 2^30 layer rows");
     if (t->capacity < 0 || t->capacity > (int64_t)INT_MAX) return set_err(FT_ERR_ARG, "pool capacity out of range");
     if (t->capacity > 0 && (!t->pool_idx || !t->pool_val)) return set_err(FT_ERR_ARG, "null pool");
     if (t->n_rows != n_rows || t->n_cols != n_cols) return set_err(FT_ERR_SHAPE, "hybrid buffer has wrong shape");
