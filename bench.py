@@ -477,10 +477,11 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk,
-            # timed ft_evolve: per step tier 1, queue A, tiers 2a/2b/3 of queue A
-            # (side stream), tier 1.5, queue B (warp kernel + its tier-3 list),
-            # finalize; reset, conversion, report, compaction (3)
-            "gpu_launches": 9 * K + 6,
+            # timed ft_evolve: per launched step tier 1, queue A, tiers 2a/2b/3 of
+            # queue A (side stream), tier 1.5, queue B (warp kernel + its tier-3
+            # list), finalize; step 1 plus whole 16-step graph chunks (the steps
+            # past K are device no-ops); reset, conversion, report, compaction (3)
+            "gpu_launches": 9 * (1 + (16 * -(-(K - 1) // 16) if K - 1 >= 16 else K - 1)) + 6,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
