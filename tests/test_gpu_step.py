@@ -337,3 +337,22 @@ def test_random_fields_every_tier_fast(max_cnt, n_pool, seed):
     ref, _ = po.step_c(po.Csc.of(phi32), lt, DEFAULT)
     got, want = out.phi.to_dense(), ref.to_dense()
     assert np.all(np.abs(got - want) <= 1e-5 * np.abs(want) + 2e-7)
+
+
+@pytest.mark.parametrize("max_steps", [1, 2, 3, 16, 17, 18, 33])
+def test_evolve_chunk_boundaries(max_steps):
+    """ft_evolve around its CUDA-graph chunking (step 1, then 16-step graph
+    replays whose steps past max_steps are device no-ops) with each step's
+    finalize on the side stream: field, trace length and per-step max |d|
+    equal the C oracle's."""
+    mesh = ft.gen_icosphere(3)
+    lap = ft.build_laplacian(mesh)
+    seeds = np.random.default_rng(7).choice(mesh.n_vertices, 40, replace=False)
+    fld = ft.init_field(mesh, seeds)
+    out, trace = ft.evolve(fld, lap, DEFAULT, max_steps=max_steps, tol=0.0)
+    lt = po.Csc.of(ft.field._with_diagonal(lap.mat_t))
+    ref, rtrace = po.evolve_c(po.Csc.of(fld.phi), lt, DEFAULT, max_steps)
+    assert len(trace) == max_steps and out.step_count == max_steps
+    assert_csc_equal(out.phi, ref)
+    assert [s.max_delta for s in trace] == [s["max_delta"] for s in rtrace]
+    assert [s.nnz_skel for s in trace] == [s["nnz_skel"] for s in rtrace]
