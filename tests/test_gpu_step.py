@@ -356,3 +356,21 @@ def test_evolve_chunk_boundaries(max_steps):
     assert_csc_equal(out.phi, ref)
     assert [s.max_delta for s in trace] == [s["max_delta"] for s in rtrace]
     assert [s.nnz_skel for s in trace] == [s["nnz_skel"] for s in rtrace]
+
+
+def test_evolve_step_evolve_with_shared_workspace():
+    """evolve -> step -> evolve with one StepWorkspace (cached graph, parity
+    slots, side-stream finalize state carried between calls) equals 40 + 1 +
+    25 oracle steps, bitwise."""
+    mesh = ft.gen_icosphere(3)
+    lap = ft.build_laplacian(mesh)
+    seeds = np.random.default_rng(8).choice(mesh.n_vertices, 30, replace=False)
+    fld = ft.init_field(mesh, seeds)
+    ws = ft.StepWorkspace()
+    a, _ = ft.evolve(fld, lap, DEFAULT, max_steps=40, tol=0.0, workspace=ws)
+    b, _ = ft.step(a, lap, DEFAULT, workspace=ws)
+    c, tr = ft.evolve(b, lap, DEFAULT, max_steps=25, tol=0.0, workspace=ws)
+    lt = po.Csc.of(ft.field._with_diagonal(lap.mat_t))
+    ref, _ = po.evolve_c(po.Csc.of(fld.phi), lt, DEFAULT, 66)
+    assert c.step_count == 66 and len(tr) == 25
+    assert_csc_equal(c.phi, ref)
