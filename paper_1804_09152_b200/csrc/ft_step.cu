@@ -49,6 +49,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <utility>
 
 #include "ft_common.cuh"
 
@@ -56,6 +57,12 @@ namespace ft {
 
 // exact 1.0 / n for n = 0..32 (host IEEE division; entry 0 unused)
 __constant__ double c_recip[33];
+
+// Programmatic dependent launch: a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start before its
+// predecessor in the stream has finished; it waits here, before touching
+// anything the predecessor writes.  A no-op for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 struct StepParams {
     int n_v;             // owned columns (the whole field outside domain mode)
@@ -820,6 +827,7 @@ __device__ __forceinline__ void tier1_segment(const StepParams& p, int seg, int 
 // the current one (two segments of loads in flight per warp)
 template <typename T, bool UNIFORM, bool PACKED>
 __global__ void __launch_bounds__(FT_TPB, 8) tier1_kernel(const StepParams p) {
+    pdl_wait();
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     const bool chk = p.force_check || *(volatile unsigned int*)&p.ws.ctl->nonfinite;
     const int lane = threadIdx.x & 31;
@@ -1115,6 +1123,7 @@ __device__ __forceinline__ void half_column(int j, bool have, const StepParams& 
 
 template <typename T, bool UNIFORM, bool PACKED>
 __global__ void __launch_bounds__(FT_TPB, 8) gen_kernel(const StepParams p) {
+    pdl_wait();
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     __shared__ int s_list[FT_WARPS][FT_GEN_TILES * FT_TPB];
     const int lane = threadIdx.x & 31;
@@ -1507,6 +1516,7 @@ __global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p, con
 // the global accumulators once
 template <typename T, bool UNIFORM, bool PACKED>
 __global__ void __launch_bounds__(FT_TPB, 4) warp_kernel(const StepParams p, const Queues qs) {
+    pdl_wait();
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     const int nc = *(volatile const int*)qs.q_n;
     const int lane = threadIdx.x & 31;
@@ -1533,6 +1543,7 @@ __global__ void __launch_bounds__(FT_TPB, 4) warp_kernel(const StepParams p, con
 // tier 3: exact windowed global-memory algorithm (no width limit)
 template <typename T, bool UNIFORM>
 __global__ void __launch_bounds__(FT_TPB) deep_kernel(const StepParams p, const Queues qs) {
+    pdl_wait();
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     const int n_deep = *(volatile int*)qs.dp_n;
     const int lane = threadIdx.x & 31;
@@ -2095,6 +2106,34 @@ static int side_init() {
     return FT_OK;
 }
 
+static int pdl_enabled() {
+    static const int on = [] {
+        const char* e = getenv("FT_PDL");
+        return e ? atoi(e) : 1;
+    }();
+    return on;
+}
+
+// launch k on s, programmatically dependent on the stream's previous kernel
+// (its launch and CTA ramp overlap the predecessor's tail; the kernel's
+// pdl_wait() orders the memory accesses)
+template <typename... KA, typename... AA>
+static void launch_dep(void (*k)(KA...), int grid, int block, cudaStream_t s, AA&&... args) {
+    if (!pdl_enabled()) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid); cfg.blockDim = dim3(block); cfg.stream = s;
+        cudaLaunchKernelEx(&cfg, k, std::forward<AA>(args)...);
+        return;
+    }
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid); cfg.blockDim = dim3(block); cfg.stream = s;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, std::forward<AA>(args)...);
+}
+
 static void lib_init() {
     DevState& d = dev_state();
     if (d.init) return;
@@ -2168,7 +2207,7 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
         if (!per_sm && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, FT_TPB, 0) != cudaSuccess)
             per_sm = 8;
         const int grid = per_sm * g_sms < p.num_tiles ? per_sm * g_sms : p.num_tiles;
-        k1<<<grid, FT_TPB, 0, s>>>(p);
+        launch_dep(k1, grid, FT_TPB, s, p);
     }
     if (which & 2) {
         // queue A (tier 1's wide columns) on the high-priority side stream,
@@ -2187,13 +2226,14 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
         cudaEventRecord(g_join, g_side);
         // tier 1.5, one warp per tile
         const int ngroups = (p.num_tiles + FT_GEN_TILES - 1) / FT_GEN_TILES;
-        FT_PICK3(ft::gen_kernel, dtype, uni, packed)<<<(ngroups + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
+        launch_dep(FT_PICK3(ft::gen_kernel, dtype, uni, packed), (ngroups + FT_WARPS - 1) / FT_WARPS, FT_TPB, s,
+                   p);
         pev(5, s);
         // queue B: what tier 1.5 defers (unions of three or more rows), one
         // warp per column
-        FT_PICK3(ft::warp_kernel, dtype, uni, packed)<<<g_fixup_grid * 2, FT_TPB, 0, s>>>(p, qb);
+        launch_dep(FT_PICK3(ft::warp_kernel, dtype, uni, packed), g_fixup_grid * 2, FT_TPB, s, p, qb);
         // (its tier-3 list is empty unless a column exceeds one warp)
-        FT_PICK2(ft::deep_kernel, dtype, uni)<<<g_fixup_grid / 8, FT_TPB, 0, s>>>(p, qb);
+        launch_dep(FT_PICK2(ft::deep_kernel, dtype, uni), g_fixup_grid / 8, FT_TPB, s, p, qb);
         pev(6, s);
         if (b_done) cudaEventRecord(b_done, s);
         cudaStreamWaitEvent(s, g_join, 0);
