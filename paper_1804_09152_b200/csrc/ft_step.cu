@@ -34,6 +34,10 @@
 //   queue B   warp_kernel after tier 1.5: two columns per warp, 16 lanes
 //             holding a column's neighbourhood entries, sums by shuffles in
 //             the reference's order.
+// The kernels of each stream's chain (main: tier 1 -> 1.5 -> queue B ->
+// tier 3; side: tier 2a -> 2b -> tier 3) are programmatic dependent
+// launches: each starts with pdl_wait(), so its launch overlaps the
+// predecessor's tail (FT_PDL=0 turns this off).
 // Statistics go to per-segment / per-group slots that finalize_kernel
 // reduces in a fixed order (deterministic base mass).  Canonical CSC comes
 // from ft_compact.
@@ -1361,6 +1365,7 @@ __device__ __forceinline__ bool wide3(int j, const StepParams& p, Win<3>& w) {
 
 template <typename T, bool UNIFORM, bool PACKED>
 __global__ void __launch_bounds__(FT_TPB, 4) wide3_kernel(const StepParams p, const Queues qs) {
+    pdl_wait();
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     const int n_wide = *(volatile int*)qs.q_n;
     const int lane = threadIdx.x & 31;
@@ -1468,6 +1473,7 @@ __device__ __forceinline__ bool gather_wide(int j, const StepParams& p, Win<K>& 
 
 template <typename T, bool UNIFORM>
 __global__ void __launch_bounds__(FT_TPB, 4) wide_kernel(const StepParams p, const Queues qs) {
+    pdl_wait();
     constexpr int KW = 8;      // wider unions go to tier 3
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     const int n_wide = *(volatile int*)qs.w8_n;   // tier-2a leftovers
@@ -2218,10 +2224,10 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
         cudaEventRecord(g_fork, s);
         cudaStreamWaitEvent(g_side, g_fork, 0);
         ft::queue_kernel<<<(FT_WARPS * p.num_tiles + 255) / 256, 256, 0, g_side>>>(p);
-        FT_PICK3(ft::wide3_kernel, dtype, uni, packed)<<<g_fixup_grid, FT_TPB, 0, g_side>>>(p, qa);
+        launch_dep(FT_PICK3(ft::wide3_kernel, dtype, uni, packed), g_fixup_grid, FT_TPB, g_side, p, qa);
         pev(3, g_side);
-        FT_PICK2(ft::wide_kernel, dtype, uni)<<<g_fixup_grid, FT_TPB, 0, g_side>>>(p, qa);
-        FT_PICK2(ft::deep_kernel, dtype, uni)<<<g_fixup_grid / 4, FT_TPB, 0, g_side>>>(p, qa);
+        launch_dep(FT_PICK2(ft::wide_kernel, dtype, uni), g_fixup_grid, FT_TPB, g_side, p, qa);
+        launch_dep(FT_PICK2(ft::deep_kernel, dtype, uni), g_fixup_grid / 4, FT_TPB, g_side, p, qa);
         pev(4, g_side);
         cudaEventRecord(g_join, g_side);
         // tier 1.5, one warp per tile
