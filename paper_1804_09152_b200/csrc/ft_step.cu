@@ -34,10 +34,12 @@
 //   queue B   warp_kernel after tier 1.5: two columns per warp, 16 lanes
 //             holding a column's neighbourhood entries, sums by shuffles in
 //             the reference's order.
-// The kernels of each stream's chain (main: tier 1 -> 1.5 -> queue B ->
-// tier 3; side: tier 2a -> 2b -> tier 3) are programmatic dependent
-// launches: each starts with pdl_wait(), so its launch overlaps the
-// predecessor's tail (FT_PDL=0 turns this off).
+// Within each stream's chain, a kernel that directly follows another kernel
+// (no event record or wait in between: queue B and its tier 3 after tier 1.5;
+// tier 2a, 2b and tier 3 on the side stream) is a programmatic dependent
+// launch: it starts with pdl_wait(), so its launch overlaps the
+// predecessor's tail; the predecessors never trigger early, so an event
+// recorded after them still means "finished" (FT_PDL=0 turns this off).
 // Statistics go to per-segment / per-group slots that finalize_kernel
 // reduces in a fixed order (deterministic base mass).  Canonical CSC comes
 // from ft_compact.
@@ -831,7 +833,6 @@ __device__ __forceinline__ void tier1_segment(const StepParams& p, int seg, int 
 // the current one (two segments of loads in flight per warp)
 template <typename T, bool UNIFORM, bool PACKED>
 __global__ void __launch_bounds__(FT_TPB, 8) tier1_kernel(const StepParams p) {
-    pdl_wait();
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     const bool chk = p.force_check || *(volatile unsigned int*)&p.ws.ctl->nonfinite;
     const int lane = threadIdx.x & 31;
@@ -1127,7 +1128,6 @@ __device__ __forceinline__ void half_column(int j, bool have, const StepParams& 
 
 template <typename T, bool UNIFORM, bool PACKED>
 __global__ void __launch_bounds__(FT_TPB, 8) gen_kernel(const StepParams p) {
-    pdl_wait();
     if (p.check_done && *(volatile int*)&p.ws.ctl->done) return;
     __shared__ int s_list[FT_WARPS][FT_GEN_TILES * FT_TPB];
     const int lane = threadIdx.x & 31;
@@ -2125,7 +2125,7 @@ static int pdl_enabled() {
 // pdl_wait() orders the memory accesses)
 template <typename... KA, typename... AA>
 static void launch_dep(void (*k)(KA...), int grid, int block, cudaStream_t s, AA&&... args) {
-    if (!pdl_enabled()) {
+    if (!pdl_enabled() || g_pev_on == 1) {   // probe events sit between the kernels
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid); cfg.blockDim = dim3(block); cfg.stream = s;
         cudaLaunchKernelEx(&cfg, k, std::forward<AA>(args)...);
@@ -2213,7 +2213,7 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
         if (!per_sm && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, FT_TPB, 0) != cudaSuccess)
             per_sm = 8;
         const int grid = per_sm * g_sms < p.num_tiles ? per_sm * g_sms : p.num_tiles;
-        launch_dep(k1, grid, FT_TPB, s, p);
+        k1<<<grid, FT_TPB, 0, s>>>(p);
     }
     if (which & 2) {
         // queue A (tier 1's wide columns) on the high-priority side stream,
@@ -2232,8 +2232,8 @@ static int launch_step(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* i
         cudaEventRecord(g_join, g_side);
         // tier 1.5, one warp per tile
         const int ngroups = (p.num_tiles + FT_GEN_TILES - 1) / FT_GEN_TILES;
-        launch_dep(FT_PICK3(ft::gen_kernel, dtype, uni, packed), (ngroups + FT_WARPS - 1) / FT_WARPS, FT_TPB, s,
-                   p);
+        // (a normal launch: the fork event sits between tier 1 and tier 1.5)
+        FT_PICK3(ft::gen_kernel, dtype, uni, packed)<<<(ngroups + FT_WARPS - 1) / FT_WARPS, FT_TPB, 0, s>>>(p);
         pev(5, s);
         // queue B: what tier 1.5 defers (unions of three or more rows), one
         // warp per column
