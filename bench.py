@@ -6,26 +6,38 @@
 
 Workload (BASELINE.json configs[2], the config the time-step metric is
 quoted on): synthetic torus grid 3200 x 3125 (10,000,000 vertices, order-
-identical to the reference generator), 4,096 seeds drawn with
-numpy.random.default_rng(0), CouplingParams() defaults, uniform Laplacian.
-One "step" is one explicit Euler step of the whole field.  W untimed steps
-from init_field, then K timed steps (steps W+1..W+K), inputs resident in
-HBM, then the compaction to canonical CSC -- all on one stream, bracketed by
-barrier + synchronize, timed with CUDA events, max over ranks.  The working
-set (L^T indices ~280 MB + PHI ~130 MB) exceeds the 126 MB L2, so no flush
-is needed between steps.
+identical to the reference generator), 4,096 seeds drawn by the exact replay
+of the reference's cli.sample_seed_vertices(mesh, 4096, rng=0), the
+CouplingParams() defaults, uniform Laplacian.  One "step" is one explicit
+Euler step of the whole field.
+
+Window ("steps 1-120 from init, with a steady window
+of steps 81-120"): the field is evolved untimed to step 80 - W, W warm-up
+steps run through the same ft_evolve call the timed region uses (reaching
+step 80), then K timed steps 81..80+K (K = 40 covers the whole steady
+window); `value` is that steady window.  The full window 1..120 from
+init_field is timed as well (`window_1_120`).  Inputs resident in HBM, one
+stream, barrier + synchronize on both sides, CUDA events, max over ranks.
+The working set (PHI in the hybrid layout ~480 MB, L^T ~280 MB) exceeds
+the 126 MB L2, so no flush is needed between steps.
 
 Reported beside `value` (steps/s):
-  roofline      the fused kernel's algorithmic bytes per launch (reference
-                data structures: L^T CSR + PHI_in CSC + PHI_out CSC; L values
-                not counted because the uniform path never reads them) over
-                its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs;
-  e2e           the public API end to end: host (pinned) field in ->
-                evolve(K steps) -> field + labels back on the host;
+  roofline      the step's column kernels (active list, band kernel, wide
+                kernels): algorithmic bytes of one step (the
+                reference L^T CSR indices + PHI in + PHI out CSC) over their
+                CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs;
+                `traffic` = ncu dram bytes per step of the same build
+                (profiles/step_kernel_traffic.json, matched by source hash);
+  e2e           the public API end to end: host (pinned) field at step 80 ->
+                evolve(K steps) -> field + labels back on the host (warm and
+                cold call);
   cpu_baseline  the reference package (numba, all host cores) timed on a
-                bounded sample of the same workload (rank 0, N=1).
---impl reference runs only the reference CPU implementation and prints its
-line (rank 0; other ranks exit 0).
+                bounded sample of the same window, from the GPU's state at
+                step 80 (EXACT: bitwise the reference's own state);
+  parity        the reference's fields after that sample compared bitwise
+                with the GPU's after the same steps.
+--impl reference runs only the reference CPU implementation on the same
+window and prints its line (rank 0; other ranks exit 0).
 
 N > 1 (torchrun, one rank per GPU over NCCL): weak scaling on ONE field --
 the torus grows to 3200 x (3125 N) vertices with 4096 N seeds (N = 1 is C3
@@ -40,6 +52,7 @@ GPU (sequential; for validating the code path, not a performance number).
 
 import argparse
 import ctypes
+import hashlib
 import json
 import os
 import statistics
@@ -54,6 +67,9 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 NX, NY, N_SEEDS = 3200, 3125, 4096
+METRIC = "time-steps/sec (fused Euler step)"    # identical in both arms
+STEADY_FROM = 80                                 # steady window 81-120
+FULL_WINDOW = 120
 
 
 def workload_name(args):
@@ -62,11 +78,17 @@ def workload_name(args):
             f"{args.seeds:,} seeds, fused Euler step")
 
 
+def window_of(args):
+    w = max(3, args.warmup)
+    start = max(0, STEADY_FROM - w)
+    return w, start, start + w      # warm-up steps, prep steps, first timed step - 1
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=80)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--precision", default="exact", choices=["exact", "fast"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--nx", type=int, default=NX)
@@ -85,7 +107,7 @@ def build_workload(nx, ny, n_seeds):
     import paper_1804_09152_b200 as ft
     mesh = ft.gen_periodic_grid(nx, ny)
     lap = ft.build_laplacian(mesh)
-    seeds = np.random.default_rng(0).choice(mesh.n_vertices, n_seeds, replace=False)
+    seeds = ft.sample_seed_vertices(mesh, n_seeds, 0)      # == reference cli.py:183-215
     return mesh, lap, seeds
 
 
@@ -154,56 +176,60 @@ def load_reference():
     return None
 
 
-def reference_steps_per_sec(phi_host, lap, seeds, n_max, budget_s, label):
-    """Time the reference's own `step` (shared StepWorkspace, like evolve)
-    from `phi_host` for up to n_max steps / budget_s seconds."""
-    ref = load_reference()
-    if ref is not None:
-        import numba
-        from fieldtess.field import StepWorkspace
-        # JIT warm-up on a tiny grid (reference conftest.py:7-16)
-        m6 = ref.gen_periodic_grid(6, 6)
-        ref.evolve(ref.init_field(m6, [0]), ref.build_laplacian(m6), ref.CouplingParams(), max_steps=3)
-        rphi = ref.SparseMat(phi_host.n_rows, phi_host.n_cols, phi_host.col_ptr,
-                             phi_host.row_idx[:phi_host.nnz], phi_host.values[:phi_host.nnz], check=False)
-        rmat_t = ref.SparseMat(lap.mat_t.n_rows, lap.mat_t.n_cols, lap.mat_t.col_ptr,
-                               lap.mat_t.row_idx, lap.mat_t.values, check=False)
-        rmat = ref.SparseMat(lap.mat.n_rows, lap.mat.n_cols, lap.mat.col_ptr,
-                             lap.mat.row_idx, lap.mat.values, check=False)
-        rlap = ref.Laplacian(mat=rmat, mat_t=rmat_t, scheme="uniform")
-        fld = ref.LayeredField(rphi, seeds)
-        ws = StepWorkspace()
-        fld, _ = ref.step(fld, rlap, ref.CouplingParams(), workspace=ws)   # untimed first step
-        n = 0
-        t0 = time.perf_counter()
-        while n < n_max:
-            fld, _ = ref.step(fld, rlap, ref.CouplingParams(), workspace=ws)
-            n += 1
-            if time.perf_counter() - t0 > budget_s:
-                break
-        dt = time.perf_counter() - t0
-        return {"value": n / dt, "unit": "steps/s", "cores": int(numba.get_num_threads()),
-                "kind": "reference",
-                "sample": f"{n} reference field.step calls ({label}), numba "
-                          f"{numba.__version__}, {numba.get_num_threads()} threads, "
-                          f"CPU {os.cpu_count()} logical cores"}
-    # fall back: the plain-C restatement (OpenMP over columns)
-    from oracle import pyoracle as po
-    import paper_1804_09152_b200 as ft
-    cores = os.cpu_count() or 1
-    cur = po.Csc.of(phi_host)
-    lapt = po.Csc.of(lap.mat_t)
-    cur, _ = po.step_c(cur, lapt, ft.CouplingParams(), n_threads=cores)
-    n = 0
-    t0 = time.perf_counter()
-    while n < n_max:
-        cur, _ = po.step_c(cur, lapt, ft.CouplingParams(), n_threads=cores)
-        n += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "steps/s", "cores": cores, "kind": "port",
-            "sample": f"{n} steps of the C oracle port ({label}), {cores} OpenMP threads"}
+class ReferenceCPU:
+    """The reference's own ``field.step`` on the host cores: the reference
+    package installed in oracle/_ref/py (numba, all threads, one shared
+    StepWorkspace as in its evolve), else the plain-C restatement (OpenMP).
+    Test / baseline infrastructure: never on the product path."""
+
+    def __init__(self, lap):
+        self.ref = load_reference()
+        self.cores = os.cpu_count() or 1
+        if self.ref is not None:
+            import numba
+            from fieldtess.field import StepWorkspace
+            r = self.ref
+            # JIT warm-up on a tiny grid (reference conftest.py:7-16)
+            m6 = r.gen_periodic_grid(6, 6)
+            r.evolve(r.init_field(m6, [0]), r.build_laplacian(m6), r.CouplingParams(), max_steps=3)
+            mk = lambda m: r.SparseMat(m.n_rows, m.n_cols, m.col_ptr, m.row_idx[:m.nnz], m.values[:m.nnz],
+                                       check=False)
+            self.rlap = r.Laplacian(mat=mk(lap.mat), mat_t=mk(lap.mat_t), scheme="uniform")
+            self.ws = StepWorkspace()
+            self.params = r.CouplingParams()
+            self.kind = "reference"
+            self.cores = int(numba.get_num_threads())
+            self.label = (f"the reference field.step (numba {numba.__version__}, {self.cores} threads, "
+                          f"CPU {os.cpu_count()} logical cores)")
+        else:
+            from oracle import pyoracle as po
+            import paper_1804_09152_b200 as ft
+            self.po = po
+            self.lapt = po.Csc.of(lap.mat_t)
+            self.params = ft.CouplingParams()
+            self.kind = "port"
+            self.label = f"the C oracle port ({self.cores} OpenMP threads)"
+        self.cur = None
+
+    def start(self, phi, seeds, step_count=0):
+        if self.ref is not None:
+            rp = self.ref.SparseMat(phi.n_rows, phi.n_cols, phi.col_ptr, phi.row_idx[:phi.nnz],
+                                    phi.values[:phi.nnz], check=False)
+            self.cur = self.ref.LayeredField(rp, seeds, step_count)
+        else:
+            self.cur = self.po.Csc.of(phi)
+
+    def step(self):
+        if self.ref is not None:
+            self.cur, _ = self.ref.step(self.cur, self.rlap, self.params, workspace=self.ws)
+        else:
+            self.cur, _ = self.po.step_c(self.cur, self.lapt, self.params, n_threads=self.cores)
+
+    def arrays(self):
+        """(col_ptr, row_idx, values) of the current field."""
+        m = self.cur.phi if self.ref is not None else self.cur
+        nnz = int(m.col_ptr[-1])
+        return np.asarray(m.col_ptr), np.asarray(m.row_idx[:nnz]), np.asarray(m.values[:nnz])
 
 
 def run_reference_arm(args):
@@ -212,19 +238,31 @@ def run_reference_arm(args):
         return
     import paper_1804_09152_b200 as ft
     mesh, lap, seeds = build_workload(args.nx, args.ny, args.seeds)
-    phi0 = ft.init_field(mesh, seeds).phi          # host numpy, identical to the reference's
-    res = reference_steps_per_sec(phi0, lap, seeds, max(1, args.steps), 60.0,
-                                  "steps 2.. from init_field; mesh/L^T/PHI0 built by the "
-                                  "bitwise-identical vectorised generators")
-    line = {"impl": "reference", "metric": "time-steps/sec (fused Euler step)",
-            "value": res["value"], "unit": "steps/s", "higher_is_better": True,
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 / res["value"], "dtype": "f64", "data": "synthetic",
+    w, start, first = window_of(args)
+    cpu = ReferenceCPU(lap)
+    cpu.start(ft.init_field(mesh, seeds).phi, seeds)   # host init_field == the reference's (tested)
+    t_prep = time.perf_counter()
+    for _ in range(start + w):                          # untimed: steps 1..80 (warm-up included)
+        cpu.step()
+    t_prep = time.perf_counter() - t_prep
+    K = max(1, args.steps)
+    t0 = time.perf_counter()
+    for _ in range(K):
+        cpu.step()
+    dt = time.perf_counter() - t0
+    value = K / dt
+    sample = (f"{K} steps ({first + 1}..{first + K}) of {cpu.label}; steps 1..{first} untimed "
+              f"({t_prep:.0f} s); mesh / L^T / PHI0 from the bitwise-identical vectorised generators")
+    line = {"impl": "reference", "metric": METRIC,
+            "value": value, "unit": "steps/s", "higher_is_better": True,
+            "n_gpus": args.gpus, "steps": K, "warmup": w,
+            "ms_per_step": 1e3 / value, "dtype": "f64", "data": "synthetic",
             "scaling": "weak", "vs_baseline": None,
-            "config": {"workload": workload_name(args), "precision": "f64 (reference)"},
-            "cpu_baseline": res,
-            "e2e": {"value": res["value"], "unit": "steps/s",
-                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": {"workload": workload_name(args), "precision": "f64 (reference)",
+                       "window": f"steps {first + 1}..{first + K} from init_field (BASELINE.md 3 steady window)"},
+            "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cpu.cores, "kind": cpu.kind,
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -238,6 +276,23 @@ def algorithmic_bytes(n_v, nnz_l, nnz_in, nnz_out, value_bytes, lap_values=False
     and PHI out CSC."""
     lb = 4 * (n_v + 1) + (4 + (value_bytes if lap_values else 0)) * nnz_l
     return lb + 2 * 4 * (n_v + 1) + (4 + value_bytes) * (nnz_in + nnz_out)
+
+
+def engine_source_hash():
+    h = hashlib.sha256()
+    for f in ("ft_step.cu", "ft_arith.cuh", "ft_common.cuh"):
+        h.update(open(os.path.join(REPO, "paper_1804_09152_b200", "csrc", f), "rb").read())
+    return h.hexdigest()[:16]
+
+
+def load_peak():
+    try:
+        peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        peaks = {}
+    if "hbm_gbs" in peaks:
+        return float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
 def run_ours(args):
@@ -269,219 +324,247 @@ def run_ours(args):
     n_v = mesh.n_vertices
     prec = args.precision
     vbytes = 8 if prec == "exact" else 4
+    W, start, first = window_of(args)
+    K = args.steps
     fld0 = ft.init_field(mesh, seeds, precision=prec)
-    warm = max(3, args.warmup)
-    cur, _ = ft.evolve(fld0, lap, params, max_steps=warm, tol=0.0)
-    dphi = cur.device_phi()
-    dev = dphi.values.device
+    # untimed: steps 1..80-W through the public API
+    cur = ft.evolve(fld0, lap, params, max_steps=start, tol=0.0)[0] if start > 0 else fld0
+    src = cur.device_phi()
+    dev = src.values.device
     ws = ft.StepWorkspace()
     ws.prepare(n_v, dev)
-    cap = int(_lib.lib().ft_tiled_min_capacity(n_v)) + dphi.nnz
-    ta = ft.DeviceTiled(dphi.n_rows, n_v, cap, dphi.values.dtype, dev)
-    tb = ft.DeviceTiled(dphi.n_rows, n_v, cap, dphi.values.dtype, dev)
-    out = ft.DeviceCSC.allocate(dphi.n_rows, n_v, 3 * dphi.nnz, dphi.values.dtype, dev)
+    cap = max(int(src.nnz * F.POOL_FRACTION), F.POOL_MIN)
+    ta = ft.DeviceTiled(src.n_rows, n_v, cap, src.values.dtype, dev)
+    tb = ft.DeviceTiled(src.n_rows, n_v, cap, src.values.dtype, dev)
+    out = ft.DeviceCSC.allocate(src.n_rows, n_v, 3 * src.nnz, src.values.dtype, dev)
     dl = F.device_laplacian(lap, prec)
     lib = _lib.lib()
     lap_c = dl.ft_csc(prec)
+    flags = dl.launch_flags()
     prm = params.ft_params()
     dt_code = F._ft_dtype(prec)
     wp, wn = ws.ws_args()
-    K = args.steps
-    trace = torch.zeros(K * _lib.STATS_BYTES, dtype=torch.uint8, device=dev)
-    comp_rec = torch.zeros(_lib.STATS_BYTES, dtype=torch.uint8, device=dev)
+    n_tr = max(K, W, FULL_WINDOW)
+    trace = torch.zeros(n_tr * _lib.STATS_BYTES, dtype=torch.uint8, device=dev)
+    ev_ctl = torch.zeros(6, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
     sh = ctypes.c_void_p(stream.cuda_stream)
-    src_c = dphi.ft_csc()
     ta_c, tb_c, out_c = ta.ft_tiled(), tb.ft_tiled(), out.ft_csc()
-    evk = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     e_start = torch.cuda.Event(enable_timing=True)
     e_end = torch.cuda.Event(enable_timing=True)
 
-    def one_step(k):
-        dst = ta_c if k % 2 == 0 else tb_c
-        src_t = tb_c if k % 2 == 0 else ta_c
-        evk[k][0].record(stream)
-        rc = lib.ft_step_kernel(ctypes.byref(lap_c), dl.launch_flags(), ctypes.byref(src_t), ctypes.byref(dst),
-                                dt_code, ctypes.byref(prm), wp, wn, sh)
-        rc |= lib.ft_step_fixup(ctypes.byref(lap_c), dl.launch_flags(), ctypes.byref(src_t), ctypes.byref(dst),
-                                dt_code, ctypes.byref(prm), wp, wn, sh)
-        evk[k][1].record(stream)
-        rc |= lib.ft_step_finalize(wp, wn, n_v, dst.capacity,
-                                   ctypes.c_void_p(trace.data_ptr() + k * _lib.STATS_BYTES), sh)
+    def evolve_dev(src_dev, steps):
+        s_c = src_dev.ft_csc()
+        rc = lib.ft_evolve(ctypes.byref(lap_c), flags, ctypes.byref(s_c), ctypes.byref(ta_c),
+                           ctypes.byref(tb_c), ctypes.byref(out_c), dt_code, ctypes.byref(prm), steps, 0.0, 0.0,
+                           wp, wn, ctypes.c_void_p(trace.data_ptr()), ctypes.c_void_p(ev_ctl.data_ptr()), sh)
         if rc:
             raise RuntimeError(_lib.last_error())
 
+    def check_evolve(steps, what):
+        ctl = ev_ctl.cpu().numpy()
+        if int(ctl[0]) != steps or int(ctl[1]) != _lib.FT_STATUS_MAXSTEPS or int(ctl[3]) != 1:
+            raise RuntimeError(f"ft_evolve {what}: control {ctl.tolist()}")
+        recs = np.frombuffer(trace[:steps * _lib.STATS_BYTES].cpu().numpy().tobytes(), dtype=_lib.STATS_DTYPE)
+        bad = [int(r["status"]) for r in recs if int(r["status"]) not in (0, _lib.FT_STATUS_MAXSTEPS)]
+        if bad:
+            raise RuntimeError(f"step status {bad[:3]} in {what}")
+        return recs
+
+    # ---- warm-up: W steps (80-W+1 .. 80) through the timed call itself;
+    # the first call also captures the evolve graph
+    evolve_dev(src, W)
+    torch.cuda.synchronize()
+    check_evolve(W, "warm-up")
+    out.nnz = int(ev_ctl[4].item())
+    src80 = out.clone()                  # canonical field at step 80
+
+    # ---- value: steps 81..80+K through ft_evolve (resident canonical input
+    # -> hybrid -> K steps in CUDA-graph chunks -> canonical output)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
     e_start.record(stream)
-    # canonical state after the warm-up -> hybrid layout (inside the timed region)
-    rc0 = lib.ft_tiled_from_csc(ctypes.byref(src_c), ctypes.byref(tb_c), dt_code, wp, wn,
-                                ctypes.c_void_p(comp_rec.data_ptr()), sh)
-    if rc0:
-        raise RuntimeError(_lib.last_error())
-    for k in range(K):
-        one_step(k)
-    last = ta_c if (K - 1) % 2 == 0 else tb_c
-    rc = lib.ft_compact(ctypes.byref(last), ctypes.byref(out_c), dt_code, wp, wn,
-                        ctypes.c_void_p(comp_rec.data_ptr()), sh)
-    e_end.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    clocks.stop()
-    if rc:
-        raise RuntimeError(_lib.last_error())
-    kern_pass_ms = e_start.elapsed_time(e_end)
-
-    # ---- value: the same K steps through the production path, ft_evolve
-    # (resident canonical input -> hybrid -> K steps in CUDA-graph chunks,
-    # each finalize overlapped with the next step on the side stream ->
-    # canonical output); one untimed call first captures the graph
-    ev_trace = torch.zeros(K * _lib.STATS_BYTES, dtype=torch.uint8, device=dev)
-    ev_ctl = torch.zeros(6, dtype=torch.int64, device=dev)
-
-    def evolve_pass():
-        return lib.ft_evolve(ctypes.byref(lap_c), dl.launch_flags(), ctypes.byref(src_c), ctypes.byref(ta_c),
-                             ctypes.byref(tb_c), ctypes.byref(out_c), dt_code, ctypes.byref(prm), K, 0.0, 0.0,
-                             wp, wn, ctypes.c_void_p(ev_trace.data_ptr()), ctypes.c_void_p(ev_ctl.data_ptr()), sh)
-
-    if evolve_pass():
-        raise RuntimeError(_lib.last_error())
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
-    e_start.record(stream)
-    rc = evolve_pass()
+    evolve_dev(src80, K)
     e_end.record(stream)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     clk = clocks.stop()
-    if rc:
+    recs = check_evolve(K, "timed window")
+    elapsed_ms = allmax(e_start.elapsed_time(e_end))
+
+    # ---- kernel timing: the same K steps through ft_step_run, CUDA events
+    # around each step's column kernels (the finalize outside)
+    comp_rec = torch.zeros(_lib.STATS_BYTES, dtype=torch.uint8, device=dev)
+    krec = torch.zeros(K * _lib.STATS_BYTES, dtype=torch.uint8, device=dev)
+    evk = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    s80 = src80.ft_csc()
+    if lib.ft_tiled_from_csc(ctypes.byref(s80), ctypes.byref(tb_c), dt_code, wp, wn,
+                             ctypes.c_void_p(comp_rec.data_ptr()), sh):
         raise RuntimeError(_lib.last_error())
-    ctl = ev_ctl.cpu().numpy()
-    if int(ctl[0]) != K or int(ctl[1]) != _lib.FT_STATUS_MAXSTEPS or int(ctl[3]) != 1:
-        raise RuntimeError(f"ft_evolve timed pass: control {ctl.tolist()}")
-    recs = np.frombuffer(trace.cpu().numpy().tobytes(), dtype=_lib.STATS_DTYPE)
-    bad = [int(r["status"]) for r in recs if int(r["status"]) != 0]
-    if bad:
-        raise RuntimeError(f"step status {bad[:3]} in the timed region")
-    crec = np.frombuffer(comp_rec.cpu().numpy().tobytes(), dtype=_lib.STATS_DTYPE)[0]
-    if int(crec["status"]) != 0:
-        raise RuntimeError("compaction overflow in the timed region")
-    elapsed_ms = e_start.elapsed_time(e_end)
+    for k in range(K):
+        dst, srct = (ta_c, tb_c) if k % 2 == 0 else (tb_c, ta_c)
+        evk[k][0].record(stream)
+        rc = lib.ft_step_run(ctypes.byref(lap_c), flags, ctypes.byref(srct), ctypes.byref(dst), k & 1, dt_code,
+                             ctypes.byref(prm), wp, wn, _lib.FT_PHASE_COLUMNS, None, sh)
+        evk[k][1].record(stream)
+        rc |= lib.ft_step_run(ctypes.byref(lap_c), flags, ctypes.byref(srct), ctypes.byref(dst), k & 1, dt_code,
+                              ctypes.byref(prm), wp, wn, _lib.FT_PHASE_FINALIZE,
+                              ctypes.c_void_p(krec.data_ptr() + k * _lib.STATS_BYTES), sh)
+        if rc:
+            raise RuntimeError(_lib.last_error())
+    torch.cuda.synchronize()
+    kr = np.frombuffer(krec.cpu().numpy().tobytes(), dtype=_lib.STATS_DTYPE)
+    if any(int(r["status"]) != 0 for r in kr) or [int(r["nnz_phi"]) for r in kr] != [int(r["nnz_phi"]) for r in recs]:
+        raise RuntimeError("kernel-timing pass diverged from the timed ft_evolve")
     kern_ms = np.array([a.elapsed_time(b) for a, b in evk])
-    elapsed_ms = allmax(elapsed_ms)
-    nnz_in = [dphi.nnz] + [int(r["nnz_phi"]) for r in recs[:-1]]
+
+    nnz_in = [src80.nnz] + [int(r["nnz_phi"]) for r in recs[:-1]]
     nnz_out = [int(r["nnz_phi"]) for r in recs]
     skel = sum(int(r["nnz_skel"]) for r in recs)
     nnz_l = lap.mat_t.nnz
     uniform = dl.flags == _lib.FT_LAP_UNIFORM
-    lap_bytes_note = ("packed neighbour table (16 B/column) read; algorithmic bytes keep the "
-                      "reference L^T CSR" if dl.pack is not None else "L^T CSR")
     alg = np.array([algorithmic_bytes(n_v, nnz_l, a, b, vbytes, lap_values=not uniform)
                     for a, b in zip(nnz_in, nnz_out)], dtype=np.float64)
     achieved = float(alg.sum() / (kern_ms.sum() * 1e-3) / 1e9)
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
-    except (OSError, ValueError):
-        pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
-    traffic = None
+    peak, peak_src = load_peak()
+    traffic, traffic_note = None, "no ncu capture of this build in profiles/step_kernel_traffic.json"
+    src_hash = engine_source_hash()
     tpath = os.path.join(REPO, "profiles", "step_kernel_traffic.json")
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
-            if tj.get("precision") == prec and tj.get("n_vertices") == n_v:
-                traffic = tj.get("dram_bytes_per_launch")
+            if (tj.get("engine_hash") == src_hash and tj.get("precision") == prec
+                    and tj.get("n_vertices") == n_v):
+                traffic = tj.get("dram_bytes_per_step")
+                traffic_note = tj.get("note", "ncu dram__bytes_read+write per step, same build")
         except (OSError, ValueError):
             pass
 
-    # ---- e2e through the public API ----------------------------------------
+    # ---- the full window 1..120 from init_field (same buffers, graph warm)
+    d0 = fld0.device_phi()
+    torch.cuda.synchronize()
+    e_start.record(stream)
+    evolve_dev(d0, FULL_WINDOW)
+    e_end.record(stream)
+    torch.cuda.synchronize()
+    check_evolve(FULL_WINDOW, "window 1..120")
+    full_ms = allmax(e_start.elapsed_time(e_end))
+
+    # ---- e2e through the public API: host field at step 80 (pinned) ->
+    # evolve(K) -> field + labels on the host
     e2e = None
     if not args.no_e2e:
-        host0 = fld0.phi
+        host0 = ft.LayeredField(src80, seeds, step_count=first).phi
         nnz0 = host0.nnz
         pinned = [torch.empty(a.size, dtype=t, pin_memory=True)
                   for a, t in ((host0.col_ptr, torch.int32), (host0.row_idx[:nnz0], torch.int32),
-                               (host0.values[:nnz0], torch.float64))]
+                               (host0.values[:nnz0], torch.float64 if prec == "exact" else torch.float32))]
         pinned[0].numpy()[:] = host0.col_ptr
         pinned[1].numpy()[:] = host0.row_idx[:nnz0]
         pinned[2].numpy()[:] = host0.values[:nnz0]
         hphi = ft.SparseMat(host0.n_rows, n_v, pinned[0].numpy(), pinned[1].numpy(),
                             pinned[2].numpy(), check=False)
+
         def api_run():
-            fin, tr = ft.evolve(ft.LayeredField(hphi, seeds, precision=prec), lap, params,
+            fin, tr = ft.evolve(ft.LayeredField(hphi, seeds, step_count=first, precision=prec), lap, params,
                                 max_steps=K, tol=0.0)
             return fin.phi, ft.sharp_labels(fin), tr
 
-        # one untimed call first: the host (pinned) and device caching
-        # allocators are warm, as for a service making repeated calls
-        warm_out = api_run()
-        del warm_out
-        torch.cuda.synchronize()
-        barrier()
-        t0 = time.perf_counter()
-        phi_back, labels, tr = api_run()
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        barrier()
-        e2e_s = allmax(t1 - t0)
+        times = []
+        for _ in range(2):          # cold (first API call on this workload), then warm
+            torch.cuda.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            phi_back, labels, tr = api_run()
+            torch.cuda.synchronize()
+            times.append(allmax(time.perf_counter() - t0))
+            barrier()
         h2d = 4 * (n_v + 1) + (4 + vbytes) * nnz0
-        d2h = 4 * (n_v + 1) + 12 * phi_back.nnz + 8 * labels.size + _lib.STATS_BYTES * len(tr)
-        e2e = {"value": world * K / e2e_s, "unit": "steps/s",
+        d2h = 4 * (n_v + 1) + (4 + vbytes) * phi_back.nnz + 8 * labels.size + _lib.STATS_BYTES * len(tr)
+        e2e = {"value": world * K / times[1], "unit": "steps/s",
                "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K),
-               "path": "evolve(host field, K steps) -> field.phi + sharp_labels on the host; "
-                       "steps 1..K from init_field; L^T resident (uploaded once per mesh); "
-                       "second of two identical calls (allocators warm)"}
+               "cold_value": world * K / times[0],
+               "path": f"evolve(host field at step {first}, K steps) -> field.phi + sharp_labels on the host; "
+                       "L^T resident (uploaded once per mesh); value = second identical call, cold_value = "
+                       "first"}
 
-    cpu = None
+    # ---- CPU baseline + parity: the reference from the GPU's step-80 state
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        snap = cur.phi                       # EXACT: bitwise the reference's state at step W
-        cpu = reference_steps_per_sec(snap, lap, seeds, K, args.cpu_seconds,
-                                      f"steps {warm + 2}.. of this workload")
+        rcpu = ReferenceCPU(lap)
+        snap = ft.LayeredField(src80, seeds, step_count=first).phi   # EXACT: bitwise the reference's state
+        rcpu.start(snap, seeds, first)
+        n = 0
+        t0 = time.perf_counter()
+        while n < max(1, K):
+            rcpu.step()
+            n += 1
+            if time.perf_counter() - t0 > args.cpu_seconds:
+                break
+        dt = time.perf_counter() - t0
+        cpu = {"value": n / dt, "unit": "steps/s", "cores": rcpu.cores, "kind": rcpu.kind,
+               "sample": f"{n} steps ({first + 1}..{first + n}) of {rcpu.label}, from the GPU's step-{first} field"}
+        gpu_n, _ = ft.evolve(ft.LayeredField(src80, seeds, step_count=first), lap, params, max_steps=n, tol=0.0)
+        g = gpu_n.phi
+        rp, ri, rv = rcpu.arrays()
+        gp, gi, gv = np.asarray(g.col_ptr), np.asarray(g.row_idx[:g.nnz]), np.asarray(g.values[:g.nnz])
+        same_pattern = np.array_equal(gp, rp) and np.array_equal(gi, ri)
+        if prec == "exact":
+            ok = bool(same_pattern and np.array_equal(gv, rv))
+            parity = {"steps": n, "window": f"{first + 1}..{first + n}", "bitwise": ok,
+                      "against": rcpu.kind, "nnz": int(rp[-1])}
+        else:
+            parity = {"steps": n, "window": f"{first + 1}..{first + n}", "bitwise": False,
+                      "same_pattern": bool(same_pattern), "against": rcpu.kind,
+                      "labels_agree": float(np.mean(ft.sharp_labels(gpu_n) == ft.sharp_labels(
+                          ft.LayeredField(ft.SparseMat(g.n_rows, g.n_cols, rp, ri, rv, check=False), seeds))))}
 
     if rank == 0:
         value = world * K / (elapsed_ms * 1e-3)
+        # launches of one ft_evolve call: reset, conversion (2), step 1 (5),
+        # ceil((K-1)/16) graph replays of 16 steps x 5 kernels (steps past K
+        # are device no-ops), report, compaction (3)
+        launches = 3 + 5 + 80 * -(-(K - 1) // 16) + 1 + 3
         line = {
-            "metric": "time-steps/sec (fused Euler step); layer-nnz updates/sec; HBM GB/s vs roofline",
-            "value": value, "unit": "steps/s", "n_gpus": world, "steps": K, "warmup": warm,
+            "metric": METRIC,
+            "value": value, "unit": "steps/s", "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": elapsed_ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64" if prec == "exact" else "f32-storage/f64-arith",
             "data": "synthetic",
             "config": {"workload": workload_name(args), "mesh": f"torus {args.nx}x{args.ny}", "n_vertices": n_v,
-                       "seeds": args.seeds, "precision": prec, "laplacian": "uniform",
+                       "seeds": args.seeds, "seed_sampler": "reference cli.sample_seed_vertices(mesh, n, rng=0) "
+                                                            "(exact replay)",
+                       "precision": prec, "laplacian": "uniform",
                        "parallelism": "single GPU" if world == 1 else f"{world} replicas",
                        "l2": "working set > 126 MB L2 (no flush needed)",
-                       "window": f"steps {warm + 1}..{warm + K} from init_field"},
+                       "window": f"steps {first + 1}..{first + K} from init_field (BASELINE.md 3 steady window "
+                                 f"81-120); warm-up steps {start + 1}..{first}"},
+            "window_1_120": {"value": FULL_WINDOW / (full_ms * 1e-3), "unit": "steps/s",
+                             "ms_per_step": full_ms / FULL_WINDOW,
+                             "path": "the same ft_evolve call from init_field, steps 1..120"},
             "layer_nnz_updates_per_s": world * skel / (elapsed_ms * 1e-3),
             "kernel_ms_per_step": float(kern_ms.mean()),
-            "timed_path": "ft_evolve (the evolve() device loop: CUDA-graph chunks, finalize overlapped on the "
-                          "side stream), resident canonical input -> K steps -> canonical output",
-            "kernel_timing_path": f"the same K steps as ft_step_kernel + ft_step_fixup + ft_step_finalize "
-                                  f"calls with CUDA events around the column kernels ({kern_pass_ms / K:.4f} ms/step "
-                                  f"including the unoverlapped finalize)",
+            "timed_path": "ft_evolve (the evolve() device loop: active-set steps in CUDA-graph chunks), "
+                          "resident canonical input -> K steps -> canonical output",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "the step's column kernels: tier 1 (classify + single-row closed form), "
-                                   "tier 1.5 (two-row update), tiers 2/3 (wide columns); finalize excluded",
+                         "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note,
+                         "kernel": "one Euler step's column kernels (active list, band kernel, wide kernels), "
+                                   "CUDA events on the launch stream in a second pass over the same K steps; "
+                                   "finalize excluded",
                          "bytes_per_launch": float(alg.mean()), "peak_source": peak_src,
-                         "lap_layout": lap_bytes_note},
+                         "bytes_definition": "SURVEY 8(d) algorithmic bytes of a full step: L^T CSR indices + "
+                                             "PHI in + PHI out CSC; an active step reads only the changed "
+                                             "columns' one-rings, so frac > 1 is possible -- see traffic",
+                         "engine_hash": src_hash},
+            "parity": parity,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk,
-            # timed ft_evolve: per launched step tier 1, queue A, tiers 2a/2b/3 of
-            # queue A (side stream), tier 1.5, queue B (warp kernel + its tier-3
-            # list), finalize; step 1 plus whole 16-step graph chunks (the steps
-            # past K are device no-ops); reset, conversion, report, compaction (3)
-            "gpu_launches": 9 * (1 + (16 * -(-(K - 1) // 16) if K - 1 >= 16 else K - 1)) + 6,
+            "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -593,7 +676,7 @@ def run_partitioned(args, world, rank, local, emulate=0):
     if rank == 0:
         value = W * K / (elapsed_ms * 1e-3)
         line = {
-            "metric": "time-steps/sec (fused Euler step); layer-nnz updates/sec; HBM GB/s vs roofline",
+            "metric": METRIC,
             "value": value, "unit": "steps/s (C3-equivalent: 10M-vertex steps)", "n_gpus": world,
             "steps": K, "warmup": warm, "ms_per_step": elapsed_ms / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,

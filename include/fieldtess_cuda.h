@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define FT_ABI_VERSION 5
+#define FT_ABI_VERSION 6
 
 /* return codes (mapped onto the reference's TessError subclasses,
  * `errors.py:9-75`, by the Python host layer) */
@@ -73,6 +73,12 @@ extern "C" {
 #define FT_LAP_CHECK_FINITE 4  /* tiled input of unknown origin: check its
                               values for NaN / Inf (automatic for canonical
                               input and after any non-finite output)        */
+#define FT_LAP_SYMMETRIC 8 /* the pattern of L^T is symmetric (column j is read
+                              by exactly the columns it reads; every mesh
+                              Laplacian of mesh.py:379-431): enables
+                              active-set stepping -- a column whose closed
+                              one-ring did not change in the previous step is
+                              not recomputed (its value is already in place)  */
 
 /* status codes written into ft_step_stats.status / evolve control[1] */
 #define FT_STATUS_OK           0
@@ -148,16 +154,13 @@ int         ft_abi_version(void);
 const char* ft_last_error(void);
 
 /* Scratch `workspace` for a field of n_vertices columns (device control
- * block, per-tile partial sums, compaction scan space).  Zero it once with
- * ft_workspace_init; then reuse it for every call on fields of that size. */
+ * block with the running statistics, the active list, the column lists of
+ * the wide kernels, per-column skeleton sizes and activity stamps,
+ * compaction scan space; 17 bytes per column).  Zero it once with
+ * ft_workspace_init; then reuse it for every call on fields of that size.
+ * It carries the active-set state between the steps of one field. */
 size_t ft_workspace_bytes(int32_t n_vertices);
 int    ft_workspace_init(void* workspace, size_t bytes, void* stream);
-
-/* Entries reserved per tile slot (kept for ABI compatibility: 0, the
- * hybrid layout has no slots), and the smallest legal ft_tiled pool
- * capacity (0: a field with at most two entries per column needs no pool). */
-int64_t ft_tile_slot_entries(void);
-int64_t ft_tiled_min_capacity(int32_t n_vertices);
 
 /* Canonical CSC -> hybrid layout (columns with more than two entries take
  * pool space with one atomic per warp).  A non-finite value raises the
@@ -195,21 +198,23 @@ int ft_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
             const ft_params* params, void* workspace, size_t ws_bytes,
             ft_step_stats* stats, void* stream);
 
-/* The launches of one step from a hybrid-layout input, for callers that
- * time the kernels on their own (bench.py brackets them with CUDA events):
- *   ft_step_kernel   tier 1: classification and the single-row closed form
- *                    (most columns), the rest listed per tile;
- *   ft_step_fixup    tiers 1.5-3: the listed columns;
- *   ft_step_finalize reduces the workspace accumulators into `stats`.
+/* One step from a hybrid-layout input, for callers that drive the step
+ * sequence themselves (bench.py brackets the column kernels with CUDA
+ * events).  `out_id` (0 / 1) names the target buffer: a sequence of steps
+ * ping-pongs between two buffers with ids 0 and 1 (ft_evolve: work_a = 0,
+ * work_b = 1), starting after ft_tiled_from_csc into buffer 1.
+ *   FT_PHASE_COLUMNS   the column kernels: active list, band kernel (one
+ *                      lane per column: closed form / two-row update), the
+ *                      warp-cooperative and serial kernels for wide columns;
+ *   FT_PHASE_FINALIZE  the statistics record into `stats` (device), the
+ *                      next step's mode.
  * ft_evolve issues exactly this sequence. */
-int ft_step_kernel(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* in,
-                   ft_tiled* out, int32_t dtype, const ft_params* params,
-                   void* workspace, size_t ws_bytes, void* stream);
-int ft_step_fixup(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* in,
-                  ft_tiled* out, int32_t dtype, const ft_params* params,
-                  void* workspace, size_t ws_bytes, void* stream);
-int ft_step_finalize(void* workspace, size_t ws_bytes, int32_t n_vertices,
-                     int64_t tiled_capacity, ft_step_stats* stats, void* stream);
+#define FT_PHASE_COLUMNS  1
+#define FT_PHASE_FINALIZE 2
+int ft_step_run(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* in,
+                ft_tiled* out, int32_t out_id, int32_t dtype, const ft_params* params,
+                void* workspace, size_t ws_bytes, int32_t phases,
+                ft_step_stats* stats, void* stream);
 
 /* Tiled -> canonical CSC (device-wide scan of column counts, then a
  * coalesced copy).  stats->nnz_phi / needed / status report the result

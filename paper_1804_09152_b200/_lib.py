@@ -27,6 +27,10 @@ FT_LAP_EXPLICIT = 0
 FT_LAP_UNIFORM = 1
 FT_LAP_PACKED = 2
 FT_LAP_CHECK_FINITE = 4
+FT_LAP_SYMMETRIC = 8
+
+FT_PHASE_COLUMNS = 1
+FT_PHASE_FINALIZE = 2
 
 FT_STATUS_OK = 0
 FT_STATUS_NAN = 1
@@ -39,7 +43,7 @@ FT_STATUS_HALO_OVERFLOW = 7
 
 FT_HALO_FORCE = 1
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 
 class FtParams(ctypes.Structure):
@@ -92,8 +96,8 @@ assert STATS_DTYPE.itemsize == STATS_BYTES
 
 # every symbol include/fieldtess_cuda.h declares
 EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
-           "ft_workspace_init", "ft_tile_slot_entries", "ft_tiled_min_capacity", "ft_tiled_from_csc",
-           "ft_step", "ft_step_kernel", "ft_step_fixup", "ft_step_finalize", "ft_compact",
+           "ft_workspace_init", "ft_tiled_from_csc",
+           "ft_step", "ft_step_run", "ft_compact",
            "ft_evolve", "ft_labels", "ft_faces_by_cell", "ft_lloyd_centroids",
            "ft_dual_products", "ft_domain_step", "ft_halo_bytes", "ft_halo_pack",
            "ft_halo_unpack", "ft_domain_combine", "ft_domain_control", "ft_laplacian_pack",
@@ -115,23 +119,16 @@ def _declare(lib):
     lib.ft_workspace_bytes.restype = ctypes.c_size_t
     lib.ft_workspace_init.argtypes = [vp, ctypes.c_size_t, vp]
     lib.ft_workspace_init.restype = ctypes.c_int
-    lib.ft_tile_slot_entries.restype = ctypes.c_int64
-    lib.ft_tiled_min_capacity.argtypes = [ctypes.c_int32]
-    lib.ft_tiled_min_capacity.restype = ctypes.c_int64
     lib.ft_tiled_from_csc.argtypes = [P(FtCsc), P(FtTiled), ctypes.c_int32, vp, ctypes.c_size_t,
                                       vp, vp]
     lib.ft_tiled_from_csc.restype = ctypes.c_int
     lib.ft_step.argtypes = [P(FtCsc), ctypes.c_int32, P(FtCsc), P(FtTiled), P(FtTiled), P(FtCsc),
                             ctypes.c_int32, P(FtParams), vp, ctypes.c_size_t, vp, vp]
     lib.ft_step.restype = ctypes.c_int
-    lib.ft_step_kernel.argtypes = [P(FtCsc), ctypes.c_int32, P(FtTiled), P(FtTiled),
-                                   ctypes.c_int32, P(FtParams), vp, ctypes.c_size_t, vp]
-    lib.ft_step_kernel.restype = ctypes.c_int
-    lib.ft_step_fixup.argtypes = lib.ft_step_kernel.argtypes
-    lib.ft_step_fixup.restype = ctypes.c_int
-    lib.ft_step_finalize.argtypes = [vp, ctypes.c_size_t, ctypes.c_int32, ctypes.c_int64,
-                                     vp, vp]
-    lib.ft_step_finalize.restype = ctypes.c_int
+    lib.ft_step_run.argtypes = [P(FtCsc), ctypes.c_int32, P(FtTiled), P(FtTiled), ctypes.c_int32,
+                                ctypes.c_int32, P(FtParams), vp, ctypes.c_size_t, ctypes.c_int32,
+                                vp, vp]
+    lib.ft_step_run.restype = ctypes.c_int
     lib.ft_compact.argtypes = [P(FtTiled), P(FtCsc), ctypes.c_int32, vp, ctypes.c_size_t,
                                vp, vp]
     lib.ft_compact.restype = ctypes.c_int

@@ -5,85 +5,79 @@
 
 #include "fieldtess_cuda.h"
 
-#define FT_TPB 128              // threads (= vertex columns) per CTA tile
+#define FT_TPB 128              // threads of the generic per-column kernels
 #define FT_WARPS (FT_TPB / 32)
 #define FT_CCH 2048             // columns per compaction chunk
-#define FT_GEN_TILES 3          // tiles per tier-1.5 warp (~63 flagged columns: two full chunks)
 #define FT_CTPB 256             // threads of the compaction kernels
 
 namespace ft {
 
-// Device control block at the head of the workspace.  Accumulators are
-// "zero = neutral" so a plain memset initialises them; the finalize kernel
-// re-zeroes the per-step ones after every step.
+// Device control block at the head of the workspace.  The per-step
+// accumulators are "zero = neutral": a plain memset initialises them and the
+// finalize kernel re-zeroes them after every step.  All statistics are
+// order-independent (integers, a max, a fixed-point base mass), so every
+// kernel folds its columns in with CTA-level atomics and the result is
+// deterministic.
 struct Control {
+    // -- per-step accumulators (zeroed by finalize) --
     unsigned long long maxdelta_bits;  // atomicMax over non-negative doubles
     unsigned long long bad_phi_key;    // atomicMax(~(col<<32|row)) -> min col
     unsigned long long bad_lt_key;
-    unsigned long long skel_total;     // interest-skeleton nnz of the step
-    unsigned long long nnz_total;      // output nnz of the step
-    unsigned long long pool_next;      // pool bump pointer of the step's output
+    long long          acc_nnz;        // full step: output nnz; active step: its change
+    long long          acc_skel;       // the same for the interest-skeleton nnz
+    long long          acc_bm[4];      // base mass (fixed point, see fx_split) or its change
     unsigned int       nan_key;        // atomicMax(INT_MAX - col) -> min col
     int                overflow;       // the output pool is too small
-    int                slow_count;     // queue A: tier-1 columns for tier 2
-    unsigned int       fin_count;      // finalize: CTAs done (last-block pattern)
-    int                deep_count;     // tier-3 columns of queue A
-    int                gen_count;      // queue B: tier-1.5 columns deferred to tier 2
+    int                n_act;          // active columns of the step (prep_kernel)
+    int                n_wide;         // columns handed to the warp-cooperative kernel
+    int                n_deep;         // wide-kernel columns beyond its staging capacity
+    int                n_w2;           // columns the three-row kernel hands to the warp kernel
+    // -- persistent state --
+    unsigned long long pool_next[2];   // pool bump pointer of hybrid buffer 0 / 1
+    long long          tot_nnz;        // running totals of the current field
+    long long          tot_skel;
+    long long          tot_bm[4];
+    int                full;           // the next step recomputes every column
+    int                seq;            // step sequence number (mark stamps)
     int                done;           // evolve: stop flag (finalize sets it)
     int                steps_done;     // evolve: completed steps
     int                status;         // evolve: final status
     unsigned int       nonfinite;      // sticky: a kernel wrote a non-finite value
     long long          needed;         // capacity needed on overflow
-    int                wide8_count;    // tier-2b columns of queue A
-    int                wide8b_count;   // tier-2b columns of queue B
     long long          conv_next;      // pool bump pointer of ft_tiled_from_csc
-    int                deepb_count;    // tier-3 columns of queue B
-    int                pad3;
-    long long          pad1;
+    double             tol;            // evolve: the stop test (field.py:316-317),
+    double             base_threshold; //   set per call by evolve_reset_kernel, so
+    int                max_steps;      //   the captured graph does not depend on them
+    int                pad2;
 };
 static_assert(sizeof(Control) % 16 == 0, "Control must stay 16B aligned");
 
-#define FT_FIN_MAX 4096   // finalize CTAs at most (partials in the workspace)
-
-// Statistics are kept per 32-column segment (one warp of tier 1) and per
-// 128-column tile (one warp of tier 1.5), so no kernel needs a CTA barrier
-// or a same-address atomic per warp; the finalize reduces them in a fixed
-// order.
+// Workspace: the control block, then per-column arrays.
+//   act[n]    active list of the step (local column indices)
+//   wide[n]   columns the band kernel hands to the three-row kernel
+//   w2[n]     columns the three-row kernel hands to the warp kernel
+//   skc[n]    interest-skeleton size of each column when it was last computed
+//   stamp[n]  mark: column is active in the step whose sequence number (mod
+//             256) equals the stamp
+//   chunk_off compaction chunk offsets
 struct Workspace {
-    Control*      ctl;
-    double*       seg_bm;       // [4 num_tiles] tier-1 base mass per segment
-    double*       seg_maxd;     // [4 num_tiles] tier-1 max |delta| per segment
-    int2*         seg_cs;       // [4 num_tiles] tier-1 (nnz, skeleton nnz) per segment
-    unsigned int* gen_mask;     // [4 num_tiles] tier-1.5 columns of each segment
-    unsigned int* slow_mask;    // [4 num_tiles] tier-2 columns of each segment
-    double*       gen_bm;       // [num_tiles] tier-1.5 base mass per tile group (FT_GEN_TILES tiles)
-    double*       gen_maxd;     // [num_tiles]
-    int2*         gen_cs;       // [num_tiles]
-    double*       vbm;          // [n_v] base mass of tier-2/3 columns
-    int*          slow_list;    // [3 n_v] tier-2 / 2b / 3 lists of queues A (growing up from
-                                //   0, n_v, 2 n_v) and B (growing down from n_v - 1, ...)
-    long long*    chunk_off;    // [num_chunks + 2] compaction chunk offsets
-    double*       fin_part;     // [FT_FIN_MAX] finalize partial sums (base mass)
-    double*       fin_maxd;     // [FT_FIN_MAX] finalize partial maxima
-    long long*    fin_cnt;      // [FT_FIN_MAX] finalize partial nnz
-    long long*    fin_skel;     // [FT_FIN_MAX] finalize partial skeleton nnz
-    int           num_tiles;
-    int           num_chunks;
-    size_t        par_off;      // bytes between the parity-0 and parity-1 segment slots
+    Control*       ctl;
+    int*           act;
+    int*           wide;
+    int*           w2;
+    int*           skc;
+    unsigned char* stamp;
+    long long*     chunk_off;
+    int            n;
+    int            num_chunks;
 };
 
-__host__ __device__ inline int num_tiles_for(int n_v) { return (n_v + FT_TPB - 1) / FT_TPB; }
 __host__ __device__ inline int num_chunks_for(int n_v) { return (n_v + FT_CCH - 1) / FT_CCH; }
 
-// the per-segment slots written by tier 1 exist twice (step parity), so
-// that ft_evolve can finalize step k while tier 1 of step k + 1 runs
 inline size_t workspace_bytes(int n_v) {
-    const size_t t = (size_t)num_tiles_for(n_v), c = (size_t)num_chunks_for(n_v), v = (size_t)n_v;
-    return sizeof(Control) + 2 * 4 * t * (8 + 8 + 8 + 4 + 4) + t * (8 + 8 + 8) + v * 8 + 3 * v * 4 +
-           (c + 2) * 8 + 4 * FT_FIN_MAX * 8 + 24 * 16;
+    const size_t c = (size_t)num_chunks_for(n_v), v = (size_t)n_v;
+    return sizeof(Control) + 4 * (v * 4 + 16) + (v + 80) + (c + 2) * 8 + 64;
 }
-
-static_assert(FT_WARPS == 4, "segment masks are read as one uint4 per tile");
 
 inline char* align16(char* p) { return (char*)(((uintptr_t)p + 15) & ~(uintptr_t)15); }
 
@@ -92,40 +86,14 @@ inline Workspace carve_workspace(void* base, int n_v) {
     char* p = (char*)base;
     w.ctl = (Control*)p;
     p += sizeof(Control);
-    w.num_tiles = num_tiles_for(n_v);
+    w.n = n_v;
     w.num_chunks = num_chunks_for(n_v);
-    const size_t ns = 4 * (size_t)w.num_tiles, nt = (size_t)w.num_tiles;
-    // parity 0 copies; parity 1 at par_off bytes further (ws_parity)
-    char* seg0 = p;
-    w.seg_bm = (double*)p;       p = align16(p + ns * 8);
-    w.seg_maxd = (double*)p;     p = align16(p + ns * 8);
-    w.seg_cs = (int2*)p;         p = align16(p + ns * 8);
-    w.gen_mask = (unsigned int*)p; p = align16(p + ns * 4);
-    w.slow_mask = (unsigned int*)p; p = align16(p + ns * 4);
-    w.par_off = (size_t)(p - seg0);
-    p += w.par_off;
-    w.gen_bm = (double*)p;       p = align16(p + nt * 8);
-    w.gen_maxd = (double*)p;     p = align16(p + nt * 8);
-    w.gen_cs = (int2*)p;         p = align16(p + nt * 8);
-    w.vbm = (double*)p;          p = align16(p + (size_t)n_v * 8);
-    w.slow_list = (int*)p;       p = align16(p + 3 * (size_t)n_v * 4);
-    w.chunk_off = (long long*)p; p = align16(p + ((size_t)w.num_chunks + 2) * 8);
-    w.fin_part = (double*)p;     p += FT_FIN_MAX * 8;
-    w.fin_maxd = (double*)p;     p += FT_FIN_MAX * 8;
-    w.fin_cnt = (long long*)p;   p += FT_FIN_MAX * 8;
-    w.fin_skel = (long long*)p;  p += FT_FIN_MAX * 8;
-    return w;
-}
-
-// the workspace view of step parity `par` (its segment slots)
-inline Workspace ws_parity(Workspace w, int par) {
-    if (par & 1) {
-        w.seg_bm = (double*)((char*)w.seg_bm + w.par_off);
-        w.seg_maxd = (double*)((char*)w.seg_maxd + w.par_off);
-        w.seg_cs = (int2*)((char*)w.seg_cs + w.par_off);
-        w.gen_mask = (unsigned int*)((char*)w.gen_mask + w.par_off);
-        w.slow_mask = (unsigned int*)((char*)w.slow_mask + w.par_off);
-    }
+    w.act = (int*)p;             p = align16(p + (size_t)n_v * 4);
+    w.wide = (int*)p;            p = align16(p + (size_t)n_v * 4);
+    w.w2 = (int*)p;              p = align16(p + (size_t)n_v * 4);
+    w.skc = (int*)p;             p = align16(p + (size_t)n_v * 4);
+    w.stamp = (unsigned char*)p; p = align16(p + (size_t)n_v + 64);   // + padding: prep reads 64 B
+    w.chunk_off = (long long*)p;
     return w;
 }
 
@@ -202,6 +170,46 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_scan, int* total) {
     __syncthreads();
     *total = tot;
     return pre + incl - v;
+}
+
+// ---------------------------------------------------------------------------
+// fixed-point base mass.  A column's base mass x (a normalised value, finite
+// and >= 0) is split exactly into an integer part and three 32-bit fraction
+// limbs (truncated below 2^-96); limb sums are exact integers, so the total
+// is independent of the summation order and can be updated by per-column
+// differences.  The reference sums the per-column base masses with numpy's
+// pairwise sum (field.py:270); the fixed-point total, rounded to double, is
+// within a few ulp of it.
+
+__host__ __device__ __forceinline__ void fx_split(double x, long long (&l)[4]) {
+    if (!(x > 0.0) || !(x < 9.0e15)) {   // 0, NaN, Inf: contributes nothing
+        l[0] = l[1] = l[2] = l[3] = 0;
+        return;
+    }
+    double y = floor(x);
+    l[0] = (long long)y;
+    double f = x - y;                      // exact
+#pragma unroll
+    for (int k = 1; k < 4; ++k) {
+        f = f * 4294967296.0;              // exact (power of two)
+        y = floor(f);
+        l[k] = (long long)y;
+        f = f - y;                         // exact
+    }
+}
+
+// limbs (possibly unnormalised, signed) -> double
+__host__ __device__ __forceinline__ double fx_value(const long long (&t)[4]) {
+    long long a[4] = {t[0], t[1], t[2], t[3]};
+    // carry-normalise limbs 3..1 into [0, 2^32)
+#pragma unroll
+    for (int k = 3; k > 0; --k) {
+        const long long c = a[k] >> 32;    // arithmetic shift: floor division
+        a[k] -= c * 4294967296LL;
+        a[k - 1] += c;
+    }
+    const double s = 1.0 / 4294967296.0;
+    return (((double)a[3] * s + (double)a[2]) * s + (double)a[1]) * s + (double)a[0];
 }
 
 }  // namespace ft

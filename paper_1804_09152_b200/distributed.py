@@ -498,7 +498,7 @@ class DomainRank:
         self.n_halo = off
         own_mask = (problem.cols >= self.col_begin) & (problem.cols < e)
         own_nnz = int(np.sum(np.diff(problem.col_ptr)[own_mask]))
-        self.step_cap = int(self.lib.ft_tiled_min_capacity(self.n_v)) + max(
+        self.step_cap = max(
             int(own_nnz * POOL_FRACTION), POOL_MIN)
         self.slots = int(slots)
         self.bufs = [None, None]

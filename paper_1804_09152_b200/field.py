@@ -19,6 +19,7 @@ per field (``init_field(..., precision=)``) or globally with
 
 import ctypes
 import json
+import os
 from dataclasses import asdict, dataclass
 
 import numpy as np
@@ -272,15 +273,19 @@ def init_field(mesh, seeds, precision=None):
 
 
 class _DeviceLap:
-    def __init__(self, lap_t, flags, n_v):
+    def __init__(self, lap_t, flags, n_v, symmetric=False):
         self.lap_t = lap_t     # dict precision -> DeviceCSC
         self.flags = flags     # FT_LAP_* of the stored values (UNIFORM / EXPLICIT)
         self.n_v = n_v
+        self.symmetric = symmetric   # pattern of L^T symmetric: active-set stepping
         self.pack = None       # packed neighbour table (uniform Laplacians)
         self.n_csr = 0         # columns the pack leaves to the CSR
 
     def launch_flags(self):
-        return self.flags | (_lib.FT_LAP_PACKED if self.pack is not None else 0)
+        f = self.flags | (_lib.FT_LAP_PACKED if self.pack is not None else 0)
+        if self.symmetric and ACTIVE_SET:
+            f |= _lib.FT_LAP_SYMMETRIC
+        return f
 
     def ft_csc(self, precision):
         """ft_csc of L^T for the step entry points: with FT_LAP_PACKED the
@@ -323,6 +328,21 @@ def _uniform_values_exact(mat_t):
     return bool(np.array_equal(vals, want))
 
 
+def _pattern_symmetric(lap):
+    """True when the pattern of L^T equals the pattern of L (lap.mat is the
+    transpose of lap.mat_t, both CSC with ascending rows; mesh.py:379-431
+    builds both from the symmetric edge set): column j of L^T is read by
+    exactly the columns it reads, which active-set stepping relies on."""
+    a, b = getattr(lap, "mat", None), lap.mat_t
+    if a is None or a.n_cols != b.n_cols or a.n_rows != b.n_rows:
+        return False
+    pa, pb = np.asarray(a.col_ptr), np.asarray(b.col_ptr)
+    if not np.array_equal(pa, pb):
+        return False
+    nnz = int(pb[-1])
+    return bool(np.array_equal(np.asarray(a.row_idx[:nnz]), np.asarray(b.row_idx[:nnz])))
+
+
 def _with_diagonal(mat_t):
     """L^T with an explicit (zero) diagonal entry wherever one is missing,
     so the fused step always meets PHI(:, j) through u == j.  A zero weight
@@ -351,7 +371,7 @@ def device_laplacian(lap, precision):
     if cache is None or cache[0] != key:
         mat_t = _with_diagonal(lap.mat_t)
         flags = _lib.FT_LAP_UNIFORM if _uniform_values_exact(mat_t) else _lib.FT_LAP_EXPLICIT
-        dl = _DeviceLap({}, flags, mat_t.n_cols)
+        dl = _DeviceLap({}, flags, mat_t.n_cols, symmetric=_pattern_symmetric(lap))
         dl.host = mat_t
         cache = (key, dl)
         try:
@@ -367,8 +387,9 @@ def device_laplacian(lap, precision):
 
 
 POOL_FRACTION = 0.25    # pool of a hybrid buffer (columns with > 2 entries), relative to nnz
-PACK_LAPLACIAN = True   # uniform Laplacians: packed neighbour table for tier 1
+PACK_LAPLACIAN = True   # uniform Laplacians: packed neighbour table (one 16-byte load per column)
 POOL_MIN = 4096
+ACTIVE_SET = os.environ.get("FT_ACTIVE_SET", "1") != "0"   # active-set stepping (symmetric L^T)
 
 
 class StepWorkspace:
@@ -401,8 +422,7 @@ class StepWorkspace:
         buf = self.tiled.get(key)
         if (buf is None or buf.n_rows != like.n_rows or buf.n_cols != like.n_cols
                 or buf.values.dtype != like.values.dtype):
-            cap = int(_lib.lib().ft_tiled_min_capacity(like.n_cols)) + max(
-                int(nnz_hint * POOL_FRACTION), POOL_MIN)
+            cap = max(int(nnz_hint * POOL_FRACTION), POOL_MIN)
             buf = DeviceTiled(like.n_rows, like.n_cols, cap, like.values.dtype, like.values.device)
             self.tiled[key] = buf
         return buf

@@ -213,6 +213,52 @@ def test_tiled_pool_overflow_regrows(monkeypatch):
     assert_csc_equal(out2.phi, ref2)
 
 
+def test_pool_overflow_late_in_evolve_restarts_from_last_good(monkeypatch):
+    """A pool overflow at a step >= 2 inside the device evolve loop: the
+    failed step's later launches are no-ops, the host grows the buffers and
+    continues from the last good field; the result equals the oracle
+    bitwise (the field two steps back is never overwritten early)."""
+    from paper_1804_09152_b200 import field as fmod
+    monkeypatch.setattr(fmod, "POOL_FRACTION", 0.0)
+    monkeypatch.setattr(fmod, "POOL_MIN", 0)
+    mesh = ft.gen_icosphere(3)
+    lap = ft.build_laplacian(mesh)
+    seeds = np.random.default_rng(26).choice(mesh.n_vertices, 6, replace=False)
+    fld = ft.init_field(mesh, seeds)
+    lt = po.Csc.of(ft.field._with_diagonal(lap.mat_t))
+    ref, rtrace = po.evolve_c(po.Csc.of(fld.phi), lt, DEFAULT, 30)
+    s2, _ = po.evolve_c(po.Csc.of(fld.phi), lt, DEFAULT, 2)
+    s3, _ = po.evolve_c(po.Csc.of(fld.phi), lt, DEFAULT, 3)
+    # at most two entries per column through step 2: the first pool column
+    # (and so the overflow) appears at step 3
+    assert np.diff(s2.col_ptr).max() <= 2 < np.diff(s3.col_ptr).max()
+    out, trace = ft.evolve(fld, lap, DEFAULT, max_steps=30, tol=0.0)
+    assert trace[-1].realloc_count >= 1
+    assert len(trace) == 30 and out.step_count == 30
+    assert_csc_equal(out.phi, ref)
+    assert [s.max_delta for s in trace] == [s["max_delta"] for s in rtrace]
+    assert [s.nnz_skel for s in trace] == [s["nnz_skel"] for s in rtrace]
+    assert all(abs(s.base_mass - r["base_mass"]) <= 1e-12 * max(1.0, r["base_mass"]) for s, r in zip(trace, rtrace))
+
+
+def test_active_set_matches_full_recomputation(monkeypatch):
+    """Active-set stepping (the default on symmetric Laplacians) against
+    every step recomputed in full (FT_LAP_SYMMETRIC off): identical fields
+    and statistics over 120 steps of a 120x100 torus."""
+    from paper_1804_09152_b200 import field as fmod
+    mesh = ft.gen_periodic_grid(120, 100)
+    lap = ft.build_laplacian(mesh)
+    seeds = np.random.default_rng(9).choice(mesh.n_vertices, 60, replace=False)
+    fld = ft.init_field(mesh, seeds)
+    a, ta = ft.evolve(fld, lap, DEFAULT, max_steps=120, tol=0.0)
+    monkeypatch.setattr(fmod, "ACTIVE_SET", False)
+    b, tb = ft.evolve(fld, lap, DEFAULT, max_steps=120, tol=0.0)
+    assert_csc_equal(a.phi, po.Csc.of(b.phi))
+    for x, y in zip(ta, tb):
+        assert (x.max_delta, x.nnz_phi, x.nnz_skel, x.base_mass) == (y.max_delta, y.nnz_phi, y.nnz_skel,
+                                                                      y.base_mass)
+
+
 def test_converged_input_returns_after_one_step():
     mesh = ft.gen_periodic_grid(9, 9)
     lap = ft.build_laplacian(mesh)
@@ -264,8 +310,10 @@ def _random_field(rng, n_v, n_rows, max_cnt, row_pool):
 
 
 def _tier_counts(phi, lap):
-    """Queue counters of the control block after the fixup launches of one
-    step (read before the finalize resets them)."""
+    """List counters of the control block after the column kernels of one
+    (full) step, read before the finalize resets them: columns the band
+    kernel handed to the warp-cooperative kernel, and those handed on to the
+    serial windowed kernel."""
     import ctypes
     import torch
     from paper_1804_09152_b200 import _lib
@@ -282,26 +330,26 @@ def _tier_counts(phi, lap):
     s_c, a_c, b_c = d.ft_csc(), a.ft_tiled(), b.ft_tiled()
     rec = ctypes.c_void_p(ws.stats.data_ptr())
     assert lib.ft_tiled_from_csc(ctypes.byref(s_c), ctypes.byref(b_c), 0, wp, wn, rec, st) == 0
-    assert lib.ft_step_kernel(ctypes.byref(lc), dl.launch_flags(), ctypes.byref(b_c), ctypes.byref(a_c), 0,
-                              ctypes.byref(prm), wp, wn, st) == 0
-    assert lib.ft_step_fixup(ctypes.byref(lc), dl.launch_flags(), ctypes.byref(b_c), ctypes.byref(a_c), 0,
-                             ctypes.byref(prm), wp, wn, st) == 0
+    assert lib.ft_step_run(ctypes.byref(lc), dl.launch_flags(), ctypes.byref(b_c), ctypes.byref(a_c), 0, 0,
+                           ctypes.byref(prm), wp, wn, _lib.FT_PHASE_COLUMNS, rec, st) == 0
     c = ws.ws[:128].cpu().numpy()
     i32 = lambda o: int(c[o:o + 4].view(np.int32)[0])
-    counts = {"queue_a": i32(56), "queue_b": i32(68), "tier2b": i32(96), "tier3": i32(64) + i32(112)}
-    assert lib.ft_step_finalize(wp, wn, phi.n_cols, a.capacity, rec, st) == 0
+    counts = {"wide": i32(84), "w2": i32(92), "deep": i32(88)}
+    assert lib.ft_step_run(ctypes.byref(lc), dl.launch_flags(), ctypes.byref(b_c), ctypes.byref(a_c), 0, 0,
+                           ctypes.byref(prm), wp, wn, _lib.FT_PHASE_FINALIZE, rec, st) == 0
     return counts
 
 
 @pytest.mark.parametrize("max_cnt,n_pool,seed,tier", [
-    (2, 6, 1, "queue_b"),   # two entries per column at most: tier 1.5 and its deferrals
-    (3, 8, 2, "queue_a"),   # pool columns: queue A (tiers 2a / 2b)
-    (4, 12, 3, "tier2b"),   # wider unions: tier 2b
-    (9, 16, 4, "tier3"),    # beyond the 8-row window / 16 entries: tier 3
+    (2, 6, 1, "wide"),      # two entries per column at most: band kernel, 3-row unions listed
+    (3, 8, 2, "wide"),      # three-entry (pool) neighbours: the three-row kernel
+    (4, 12, 3, "w2"),       # wider unions: the staged warp kernel
+    (9, 16, 4, "w2"),
 ])
 def test_random_fields_every_tier(max_cnt, n_pool, seed, tier):
-    """Random fields on a small torus drive every tier (1, 1.5, queue B's
-    16-lane groups, 2a, 2b, 3); one step and a 5-step evolve are bitwise
+    """Random fields on a small torus drive every kernel (band closed form and
+    two-row update, the warp-cooperative 16-lane groups, the serial windowed
+    kernel); one step and a 5-step evolve (active-set steps) are bitwise
     equal to the C oracle."""
     rng = np.random.default_rng(seed)
     mesh = ft.gen_periodic_grid(24, 20)
@@ -319,6 +367,33 @@ def test_random_fields_every_tier(max_cnt, n_pool, seed, tier):
     ref5, rtrace = po.evolve_c(po.Csc.of(phi), lt, DEFAULT, 5)
     assert_csc_equal(out5.phi, ref5)
     assert [s.max_delta for s in trace] == [s["max_delta"] for s in rtrace]
+
+
+def test_neighbourhood_beyond_staging_capacity():
+    """A hub vertex adjacent to every other vertex: its neighbourhood holds
+    more entries than the wide kernel stages in shared memory, so it runs
+    the exact windowed algorithm from global memory; bitwise vs the oracle."""
+    rng = np.random.default_rng(17)
+    n = 200
+    rows, cols = [], []
+    for j in range(n):                  # L^T column j: the hub, the ring neighbours, itself
+        nb = sorted({0, j, (j - 1) % n, (j + 1) % n} if j else set(range(n)))
+        rows += nb
+        cols += [j] * len(nb)
+    deg = np.bincount(np.asarray(cols), minlength=n) - 1
+    vals = np.where(np.asarray(rows) == np.asarray(cols), -1.0, 1.0 / deg[np.asarray(cols)])
+    lapt = ft.SparseMat.from_triplets(n, n, rows, cols, vals)
+    phi = _random_field(rng, n, 9, 3, np.arange(9))
+    fld = ft.LayeredField(phi, np.arange(8))
+    lap = _Lap(po.Csc.of(lapt))
+    assert _tier_counts(phi, lap)["deep"] >= 1
+    out, st = ft.step(fld, lap, DEFAULT)
+    ref, rst = po.step_c(po.Csc.of(phi), po.Csc.of(lapt), DEFAULT)
+    assert_csc_equal(out.phi, ref)
+    assert st.max_delta == rst["max_delta"] and st.nnz_skel == rst["nnz_skel"]
+    out3, _ = ft.evolve(fld, lap, DEFAULT, max_steps=3, tol=0.0)
+    ref3, _ = po.evolve_c(po.Csc.of(phi), po.Csc.of(lapt), DEFAULT, 3)
+    assert_csc_equal(out3.phi, ref3)
 
 
 @pytest.mark.parametrize("max_cnt,n_pool,seed", [(2, 6, 11), (3, 8, 12), (4, 12, 13), (9, 16, 14)])

@@ -97,6 +97,6 @@ def test_hybrid_roundtrip_device(precision):
         assert np.array_equal(out.col_ptr.cpu().numpy(), cp)
         assert np.array_equal(out.row_idx[:cp[-1]].cpu().numpy(), ri)
         assert np.array_equal(out.values[:cp[-1]].cpu().numpy(), va)
-        # the conversion raised the sticky non-finite flag (offset 84 of the control block)
-        ctl = ws.ws[:128].cpu().numpy()
-        assert int(ctl[84:88].view(np.uint32)[0]) == 1
+        # the conversion raised the sticky non-finite flag (offset 180 of the control block)
+        ctl = ws.ws[:224].cpu().numpy()
+        assert int(ctl[180:184].view(np.uint32)[0]) == 1
