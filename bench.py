@@ -475,7 +475,8 @@ def run_ours(args):
             return fin.phi, ft.sharp_labels(fin), tr
 
         times = []
-        for _ in range(2):          # cold (first API call on this workload), then warm
+        held = []
+        for _ in range(5):          # cold (first API call on this workload), then steady calls
             torch.cuda.synchronize()
             barrier()
             t0 = time.perf_counter()
@@ -483,14 +484,18 @@ def run_ours(args):
             torch.cuda.synchronize()
             times.append(allmax(time.perf_counter() - t0))
             barrier()
+            held = [phi_back, labels]   # a caller holds the latest result while making the next call
         h2d = 4 * (n_v + 1) + (4 + vbytes) * nnz0
         d2h = 4 * (n_v + 1) + (4 + vbytes) * phi_back.nnz + 8 * labels.size + _lib.STATS_BYTES * len(tr)
-        e2e = {"value": world * K / times[1], "unit": "steps/s",
+        steady = statistics.median(times[2:])
+        e2e = {"value": world * K / steady, "unit": "steps/s",
                "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K),
-               "cold_value": world * K / times[0],
+               "cold_value": world * K / times[0], "second_call_value": world * K / times[1],
                "path": f"evolve(host field at step {first}, K steps) -> field.phi + sharp_labels on the host; "
-                       "L^T resident (uploaded once per mesh); value = second identical call, cold_value = "
-                       "first"}
+                       "L^T resident (uploaded once per mesh); value = median of calls 3-5 of a caller that "
+                       "keeps its latest result (steady service: the pinned host allocator recycles the "
+                       "result two calls back), cold_value = the first call on this workload"}
+        del held
 
     # ---- CPU baseline + parity: the reference from the GPU's step-80 state
     cpu, parity = None, None

@@ -349,44 +349,43 @@ template <typename T, bool UNIFORM, bool PACKED>
 __device__ __forceinline__ void band_column(const StepParams& p, int jl, bool have, bool full, bool chk,
                                             unsigned char nxt, int lane, Acc& acc, long long* s_bm) {
     const int j = p.j_base + jl;
+    // stage 1: the packed L^T row; the column's own signature and value
     int4 pk = make_int4(0, 0, 0, 0);
     if (PACKED && have) pk = __ldg(&p.lap_pack[jl]);
     const double phs = have ? ldv<T>(p.in.v0, j) : 0.0;
+    const int sgj = have ? __ldg(&p.in.sig[j]) : FT_SIG_EMPTY;
     int q0 = 0;
     int u[kMD];
-    const int n = unpack_lrow<PACKED>(p, pk, jl, j, have, u, q0);
+    const int n = unpack_lrow<PACKED>(p, pk, jl, j, have, u, q0);   // u[k] = -1 beyond n
+    // stage 2: the neighbours' signatures
     int sg[kMD];
 #pragma unroll
-    for (int k = 0; k < kMD; ++k) sg[k] = (k < n) ? __ldg(&p.in.sig[u[k]]) : FT_SIG_EMPTY;
-    int kd = -1;
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) kd = (k < n && u[k] == j) ? k : kd;
-    int sgj = FT_SIG_EMPTY;
-#pragma unroll
-    for (int k = 0; k < kMD; ++k) sgj = (k == kd) ? sg[k] : sgj;
-    bool same = true, big = false;
+    for (int k = 0; k < kMD; ++k) sg[k] = (u[k] >= 0) ? __ldg(&p.in.sig[u[k]]) : FT_SIG_EMPTY;
+    bool same = true, big = false, hasd = false;
 #pragma unroll
     for (int k = 0; k < kMD; ++k) {
         same &= (sg[k] == FT_SIG_EMPTY) || (sg[k] == sgj);
         big |= sg[k] <= -3;
+        hasd |= u[k] == j;
     }
-    bool fast = have && kd >= 0 && p.cp.finite && sgj >= 0 && sgj < kPair && same && phs > 0.0;
+    const double invdeg = UNIFORM ? recip_deg(n) : 0.0;
+    bool fast = have && hasd && p.cp.finite && sgj >= 0 && sgj < kPair && same && phs > 0.0;
     if (chk && fast) {
         // Lt(sgj, j) and the values must be finite for the closed form
         bool fin = true;
         double lam = 0.0;
-        const double invdeg = UNIFORM ? recip_deg(n) : 0.0;
 #pragma unroll
         for (int k = 0; k < kMD; ++k) {
             if (k < n && sg[k] == sgj) {
                 const double v = ldv<T>(p.in.v0, u[k]);
                 fin &= isfinite(v);
-                lam = lam + v * lap_value<T, UNIFORM>(p, k, kd, q0, invdeg);
+                const double l = UNIFORM ? (u[k] == j ? -1.0 : invdeg) : ldv<T>(p.lap_val, q0 + k);
+                lam = lam + v * l;
             }
         }
         fast = fin && isfinite(lam);
     }
-    const bool wide = have && !fast && (kd < 0 || big);
+    const bool wide = have && !fast && (!hasd || big);
     const bool gen = have && !fast && !wide;
     const int skc_old = (have && !full) ? __ldg(&p.ws.skc[jl]) : 0;
 
@@ -417,67 +416,72 @@ __device__ __forceinline__ void band_column(const StepParams& p, int jl, bool ha
     }
     bool more = false;
     if (gen) {
-        int ax[kMD];
-#pragma unroll
-        for (int k = 0; k < kMD; ++k) ax[k] = (sg[k] >= kPair) ? __ldg(&p.in.aux[u[k]]) : 0;
-        int rlo = INT_MAX, rhi = -1;
+        // stage 3: second rows and values.  x = a neighbour's first row, ax
+        // its second (-1 when absent)
+        int x[kMD], ax[kMD];
 #pragma unroll
         for (int k = 0; k < kMD; ++k) {
-            const bool h = sg[k] >= 0, pr = sg[k] >= kPair;
-            const int x0 = sg[k] & ~kPair;
-            rlo = min(rlo, h ? x0 : INT_MAX);
-            rhi = max(rhi, h ? x0 : -1);
-            rlo = min(rlo, pr ? ax[k] : INT_MAX);
-            rhi = max(rhi, pr ? ax[k] : -1);
+            x[k] = sg[k] >= 0 ? (sg[k] & ~kPair) : -1;
+            ax[k] = sg[k] >= kPair ? __ldg(&p.in.aux[u[k]]) : -1;
         }
-        // Lt(rlo, j), Lt(rhi, j) in L order; PHI(r, j) through u == j
-        const double invdeg = UNIFORM ? recip_deg(n) : 0.0;
-        double l0 = 0.0, l1 = 0.0, vj0 = 0.0, vj1 = 0.0;
-        int axj = 0;
+        const bool prj = sgj >= kPair;
+        const int xj = sgj & ~kPair;
+        const int axj = prj ? __ldg(&p.in.aux[j]) : -1;
+        const double vj1 = prj ? ldv<T>(p.in.v1, j) : 0.0;
+        unsigned int rlo = 0xffffffffu;   // -1 (absent) is the largest unsigned value
+        int rhi = -1;
 #pragma unroll
         for (int k = 0; k < kMD; ++k) {
-            const bool h = sg[k] >= 0, pr = sg[k] >= kPair;
-            const double l = (k < n) ? lap_value<T, UNIFORM>(p, k, kd, q0, invdeg) : 0.0;
-            const int x0 = sg[k] & ~kPair;
-            const double a0 = h ? ldv<T>(p.in.v0, u[k]) : 0.0;
-            const double a1 = pr ? ldv<T>(p.in.v1, u[k]) : 0.0;
-            if (k == kd) { vj0 = a0; vj1 = a1; axj = ax[k]; }
-            const bool m0 = h && x0 == rlo;
-            const bool m1a = h && x0 != rlo && x0 == rhi, m1b = pr && ax[k] == rhi;
-            more |= (h && x0 != rlo && x0 != rhi) || (pr && ax[k] != rhi);
-            l0 = m0 ? l0 + a0 * l : l0;
-            const double c1 = m1a ? a0 : a1;
-            l1 = (m1a || m1b) ? l1 + c1 * l : l1;
+            rlo = min(rlo, min((unsigned int)x[k], (unsigned int)ax[k]));
+            rhi = max(rhi, max(x[k], ax[k]));
+        }
+        const int lo = (int)rlo;          // -1 when the neighbourhood is empty
+#pragma unroll
+        for (int k = 0; k < kMD; ++k)
+            more |= (x[k] >= 0 && x[k] != lo && x[k] != rhi) || (ax[k] >= 0 && ax[k] != rhi);
+        // Lt(lo, j), Lt(rhi, j) in L order (the reference's accumulator
+        // order): every slot adds its coefficient times L(j, u), the
+        // coefficient 0 when the slot holds no entry of that row -- adding
+        // an exact zero leaves the sum bitwise unchanged (it is never -0)
+        double l0 = 0.0, l1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < kMD; ++k) {
+            const double l = UNIFORM ? (u[k] == j ? -1.0 : invdeg)
+                                     : ((k < n) ? ldv<T>(p.lap_val, q0 + k) : 0.0);
+            const double a0 = x[k] >= 0 ? ldv<T>(p.in.v0, u[k]) : 0.0;
+            const double a1 = ax[k] >= 0 ? ldv<T>(p.in.v1, u[k]) : 0.0;
+            const double c0 = x[k] == lo ? a0 : 0.0;
+            const double c1 = x[k] == rhi ? a0 : (ax[k] == rhi ? a1 : 0.0);
+            l0 = l0 + c0 * l;
+            l1 = l1 + c1 * l;
         }
         if (!more) {
-            const bool hj = sgj >= 0, prj = sgj >= kPair;
-            const int xj = sgj & ~kPair;
-            const double p0 = (hj && xj == rlo) ? vj0 : 0.0;
-            const double p1 = (hj && xj == rhi) ? vj0 : ((prj && axj == rhi) ? vj1 : 0.0);
+            const int r0 = lo < 0 ? INT_MAX : lo;   // empty neighbourhood: empty skeleton
+            const double p0 = (sgj >= 0 && xj == lo) ? phs : 0.0;
+            const double p1 = (sgj >= 0 && xj == rhi) ? phs : ((prj && axj == rhi) ? vj1 : 0.0);
             VRes res;
             vres_init(res);
             double nv0, nv1;
             unsigned int om;
-            // rlo == INT_MAX: no entry in the neighbourhood, empty skeleton
-            process_two(rhi == rlo ? 1 : 2, rlo, rhi, p0, l0, p1, l1, p.cp, c_recip, res, nv0, nv1, om);
+            process_two(rhi == lo ? 1 : 2, r0, rhi, p0, l0, p1, l1, p.cp, c_recip, res, nv0, nv1, om);
             report_flags(res, j, p);
             cnt_new = res.cnt;
             sk_new = res.nskel;
             bm_new = res.bm;
             acc.md = fmax(acc.md, res.maxd);
             int ns = FT_SIG_EMPTY, na = 0;
-            double x0 = 0.0, x1 = 0.0;
-            if (om == 3u) { ns = rlo | kPair; na = rhi; x0 = nv0; x1 = nv1; }
-            else if (om == 1u) { ns = rlo; x0 = nv0; }
-            else if (om == 2u) { ns = rhi; x0 = nv1; }
+            double y0 = 0.0, y1 = 0.0;
+            if (om == 3u) { ns = lo | kPair; na = rhi; y0 = nv0; y1 = nv1; }
+            else if (om == 1u) { ns = lo; y0 = nv0; }
+            else if (om == 2u) { ns = rhi; y0 = nv1; }
             cnt_old = sig_count(sgj);
-            bm_old = (hj && xj == 0) ? vj0 : 0.0;
-            changed = ns != sgj || (cnt_new >= 1 && !same_bits<T>(x0, vj0)) ||
-                      (cnt_new == 2 && (na != axj || !same_bits<T>(x1, vj1)));
+            bm_old = (sgj >= 0 && xj == 0) ? phs : 0.0;
+            changed = ns != sgj || (cnt_new >= 1 && !same_bits<T>(y0, phs)) ||
+                      (cnt_new == 2 && (na != axj || !same_bits<T>(y1, vj1)));
             p.out.sig[j] = ns;
-            if (cnt_new >= 1) ((T*)p.out.v0)[j] = (T)x0;
-            if (cnt_new == 2) { p.out.aux[j] = na; ((T*)p.out.v1)[j] = (T)x1; }
-            if (!isfinite(x0) || !isfinite(x1)) atomicOr(&p.ws.ctl->nonfinite, 1u);
+            if (cnt_new >= 1) ((T*)p.out.v0)[j] = (T)y0;
+            if (cnt_new == 2) { p.out.aux[j] = na; ((T*)p.out.v1)[j] = (T)y1; }
+            if (!isfinite(y0) || !isfinite(y1)) atomicOr(&p.ws.ctl->nonfinite, 1u);
             fin_here = true;
         }
     }
@@ -492,8 +496,8 @@ __device__ __forceinline__ void band_column(const StepParams& p, int jl, bool ha
     bm_fold(fin_here ? bm_new : 0.0, fin_here ? bm_old : 0.0, full, s_bm);
 }
 
-template <typename T, bool UNIFORM, bool PACKED>
-__global__ void __launch_bounds__(kBandTPB, 4) band_kernel(const StepParams p) {
+template <typename T, bool UNIFORM, bool PACKED, int MINB = 4>
+__global__ void __launch_bounds__(kBandTPB, MINB) band_kernel(const StepParams p) {
     pdl_wait();
     Control* ctl = p.ws.ctl;
     __shared__ long long s_bm[4];
@@ -1794,7 +1798,16 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     int bg = d.band_grid[dtype == FT_F32][uni][packed];
     const int need_b = (n_own + ft::kBandTPB - 1) / ft::kBandTPB;
     if (bg > need_b) bg = need_b;
-    if (kmask & 2) launch_dep(FT_PICK3(ft::band_kernel, dtype, uni, packed), bg, ft::kBandTPB, s, p);
+    const char* bv = getenv("FT_BAND_MINB");   // experiment: register budget of the band kernel
+    const int minb = bv ? atoi(bv) : 0;
+    if ((kmask & 2) && minb && dtype == FT_F64 && packed) {
+        const int g2 = minb * d.sms < need_b ? minb * d.sms : need_b;
+        if (minb == 2) launch_dep(ft::band_kernel<double, true, true, 2>, g2, ft::kBandTPB, s, p);
+        else if (minb == 3) launch_dep(ft::band_kernel<double, true, true, 3>, g2, ft::kBandTPB, s, p);
+        else launch_dep(ft::band_kernel<double, true, true, 4>, g2, ft::kBandTPB, s, p);
+    } else if (kmask & 2) {
+        launch_dep(FT_PICK3(ft::band_kernel, dtype, uni, packed), bg, ft::kBandTPB, s, p);
+    }
     if (kmask & 4) launch_dep(FT_PICK3(ft::wide3_kernel, dtype, uni, packed), 4 * d.sms, ft::kWide3TPB, s, p);
     if (kmask & 8) {
         launch_dep(FT_PICK3(ft::wide_kernel, dtype, uni, packed), 8 * d.sms, ft::kWideTPB, s, p);

@@ -399,13 +399,15 @@ class StepWorkspace:
     With a shared workspace the input field's storage is recycled as a later
     output, so only the newest field stays valid (as in the reference)."""
 
-    def __init__(self):
+    def __init__(self, recycle=True):
         self.ws = None
         self.ws_n = -1
         self.stats = None
         self.spare = None
         self.tiled = {}
         self.realloc_count = 0
+        self.recycle = recycle   # False: scratch only, never hand out a recycled output
+        self._trace = None
 
     def prepare(self, n_v, device):
         torch = _torch()
@@ -427,8 +429,17 @@ class StepWorkspace:
             self.tiled[key] = buf
         return buf
 
+    def trace_buffer(self, n_steps, device):
+        """Device statistics records for n_steps (kept: a stable address lets
+        ft_evolve reuse its captured graph across calls)."""
+        torch = _torch()
+        nbytes = max(n_steps, 1) * _lib.STATS_BYTES
+        if self._trace is None or self._trace.numel() < nbytes or self._trace.device != device:
+            self._trace = torch.zeros(max(nbytes, 256 * _lib.STATS_BYTES), dtype=torch.uint8, device=device)
+        return self._trace
+
     def take_output(self, like, capacity):
-        sp = self.spare
+        sp = self.spare if self.recycle else None
         self.spare = None
         if (sp is not None and sp is not like and sp.n_cols == like.n_cols
                 and sp.n_rows == like.n_rows and sp.values.dtype == like.values.dtype):
@@ -440,6 +451,24 @@ class StepWorkspace:
 
     def ws_args(self):
         return ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel()
+
+
+_SCRATCH = {}
+
+
+def _scratch_workspace(n_v, precision, device):
+    """The per-device scratch used when the caller passes no workspace: its
+    work buffers, statistics records and control block persist between
+    calls (so the evolve graph is captured once per field size), but it
+    never recycles an output -- every call returns independent storage, as
+    the reference's workspace-less calls do (field.py:198-204)."""
+    key = (str(device), int(n_v), precision)
+    ws = _SCRATCH.get(key)
+    if ws is None:
+        if len(_SCRATCH) >= 4:
+            _SCRATCH.pop(next(iter(_SCRATCH)))
+        ws = _SCRATCH[key] = StepWorkspace(recycle=False)
+    return ws
 
 
 def _initial_capacity(dphi):
@@ -485,11 +514,11 @@ def step(field, lap, params, workspace=None):
     canonical CSC (ft_step)."""
     torch = _torch()
     params.validate()
-    ws = workspace if workspace is not None else StepWorkspace()
     n_v = field.n_vertices
     if lap.mat.n_rows != n_v:
         raise ShapeError("Laplacian size does not match field")
     dphi = field.device_phi()
+    ws = workspace if workspace is not None else _scratch_workspace(n_v, field.precision, dphi.values.device)
     device = dphi.values.device
     dl = device_laplacian(lap, field.precision)
     ws.prepare(n_v, device)
@@ -529,7 +558,7 @@ def step(field, lap, params, workspace=None):
         break
     _raise_step_error(rec, field.step_count)
     out.nnz = int(rec["nnz_phi"])
-    ws.spare = dphi if workspace is not None else None
+    ws.spare = dphi if ws.recycle else None
     new_field = LayeredField(out, field.seed_vertices, field.step_count + 1)
     stats = StepStats(max_delta=float(rec["max_delta"]), nnz_phi=int(rec["nnz_phi"]),
                       base_mass=float(rec["base_mass"]),
@@ -551,7 +580,8 @@ def evolve(field, lap, params, max_steps=1000, tol=1e-4, workspace=None, on_step
     if max_steps < 1:
         raise ShapeError("max_steps must be >= 1")
     params.validate()
-    ws = workspace if workspace is not None else StepWorkspace()
+    ws = workspace if workspace is not None else _scratch_workspace(
+        field.n_vertices, field.precision, field.device_phi().values.device)
     base_threshold = BASE_EXHAUSTION_PER_VERTEX * field.n_vertices
     if on_step is not None:
         return _evolve_host(field, lap, params, max_steps, tol, ws, on_step, base_threshold)
@@ -586,7 +616,7 @@ def _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold):
     wa = ws.tiled_buffer("a", src, src.nnz)
     wb = ws.tiled_buffer("b", src, src.nnz)
     out = ws.take_output(src, _initial_capacity(src))
-    trace_dev = torch.zeros(max_steps * _lib.STATS_BYTES, dtype=torch.uint8, device=device)
+    trace_dev = ws.trace_buffer(max_steps, device)
     control = torch.zeros(6, dtype=torch.int64, device=device)
     lap_c = dl.ft_csc(field.precision)
     prm = params.ft_params()
@@ -630,7 +660,7 @@ def _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold):
                 if int(_compact(last_tiled, out, field.precision, ws, stream)["status"]) != 0:
                     raise BackendError("compaction failed after growing the output")
             out.nnz = int(ctl[4])
-            if cur is not src:
+            if cur is not src and ws.recycle:
                 ws.spare = cur
             cur = out
         if status in (_lib.FT_STATUS_NAN, _lib.FT_STATUS_PATTERN):
