@@ -312,6 +312,39 @@ int ft_domain_combine(const ft_step_stats* records, int32_t world, int32_t rank,
  * status OK (rewind after a capacity failure). */
 int ft_domain_control(void* workspace, int32_t set_steps, int64_t* out, void* stream);
 
+/* -- the reference's public sparse algebra (sparse.py:279-420) ------------ */
+/* General-purpose versions of the operations the Euler step fuses, bitwise
+ * equal to the numba kernels (values FT_F64 only).  spgemm C = A B is
+ * expand-sort-compress:
+ *   ft_spgemm_count   counts[j] = sum over u in B(:, j) of nnz(A(:, u))
+ *                     (spgemm_bounds, _kernels.py:14-23);
+ *   ft_spgemm_expand  every product A(r, u) B(u, j) with key j * n_rows(A) + r
+ *                     at offsets[j].., in the reference's order (u ascending,
+ *                     then r);
+ *   (the caller sorts the keys with a STABLE sort, carrying the values)
+ *   ft_segment_sums   the sequential sum of every run of equal keys (starts =
+ *                     the first index of each run), first term assigned as in
+ *                     spgemm_numeric (_kernels.py:26-62); the caller drops
+ *                     exact zeros and builds col_ptr from the keys. */
+int ft_spgemm_count(const ft_csc* a, const ft_csc* b, int64_t* counts, void* stream);
+int ft_spgemm_expand(const ft_csc* a, const ft_csc* b, const int64_t* offsets, int64_t* keys,
+                     double* vals, void* stream);
+int ft_segment_sums(const double* vals, int64_t n, const int64_t* starts, int64_t n_seg,
+                    double* sums, void* stream);
+/* Interest skeleton of (phi, lt) (build_skeleton, sparse.py:345-371;
+ * _kernels.py:96-150): skel_rows == NULL counts rows per column into
+ * counts[n_cols]; then, with skel_ptr the caller's prefix sum, fills. */
+int ft_skeleton(const ft_csc* phi, const ft_csc* lt, int32_t* counts, const int32_t* skel_ptr,
+                int32_t* skel_rows, void* stream);
+/* a's values on the skeleton pattern, explicit zeros elsewhere; bad_row[j] =
+ * the last row of a nonzero of a outside the pattern, else -1
+ * (expand_to_skeleton, sparse.py:374-396; _kernels.py:153-176). */
+int ft_expand(const ft_csc* a, const int32_t* skel_ptr, const int32_t* skel_rows, double* out_vals,
+              int32_t* bad_row, void* stream);
+/* out = v * (1 / s) per column (s = the sequential column sum) when s > 0,
+ * unchanged otherwise; sums[j] = s (normalize_columns, sparse.py:399-420). */
+int ft_normalize_columns(const ft_csc* a, double* out_vals, double* sums, void* stream);
+
 /* -- quality metrics ------------------------------------------------------ */
 /* Distance from every point (n_points x 3 doubles) to the closest point of
  * the triangles (tri_a / tri_b / tri_c: n_tri x 3 doubles each, the

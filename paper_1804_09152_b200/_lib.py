@@ -101,7 +101,8 @@ EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
            "ft_evolve", "ft_labels", "ft_faces_by_cell", "ft_lloyd_centroids",
            "ft_dual_products", "ft_domain_step", "ft_halo_bytes", "ft_halo_pack",
            "ft_halo_unpack", "ft_domain_combine", "ft_domain_control", "ft_laplacian_pack",
-           "ft_point_triangle_distances")
+           "ft_point_triangle_distances", "ft_spgemm_count", "ft_spgemm_expand",
+           "ft_segment_sums", "ft_skeleton", "ft_expand", "ft_normalize_columns")
 
 _lib = None
 
@@ -167,6 +168,18 @@ def _declare(lib):
     lib.ft_laplacian_pack.restype = ctypes.c_int
     lib.ft_point_triangle_distances.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, vp]
     lib.ft_point_triangle_distances.restype = ctypes.c_int
+    lib.ft_spgemm_count.argtypes = [P(FtCsc), P(FtCsc), vp, vp]
+    lib.ft_spgemm_count.restype = ctypes.c_int
+    lib.ft_spgemm_expand.argtypes = [P(FtCsc), P(FtCsc), vp, vp, vp, vp]
+    lib.ft_spgemm_expand.restype = ctypes.c_int
+    lib.ft_segment_sums.argtypes = [vp, ctypes.c_int64, vp, ctypes.c_int64, vp, vp]
+    lib.ft_segment_sums.restype = ctypes.c_int
+    lib.ft_skeleton.argtypes = [P(FtCsc), P(FtCsc), vp, vp, vp, vp]
+    lib.ft_skeleton.restype = ctypes.c_int
+    lib.ft_expand.argtypes = [P(FtCsc), vp, vp, vp, vp, vp]
+    lib.ft_expand.restype = ctypes.c_int
+    lib.ft_normalize_columns.argtypes = [P(FtCsc), vp, vp, vp]
+    lib.ft_normalize_columns.restype = ctypes.c_int
 
 
 def lib():

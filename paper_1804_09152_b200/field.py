@@ -27,7 +27,7 @@ import numpy as np
 from . import _lib
 from .errors import (BackendError, DuplicateSeedError, NumericalBlowupError,
                      PatternViolationError, ShapeError)
-from .sparse import INDEX, DeviceCSC, DeviceTiled, SparseMat
+from .sparse import INDEX, DeviceCSC, DeviceTiled, SparseMat, read_triplets_stream
 
 UNCLAIMED = -1
 BASE_EXHAUSTION_PER_VERTEX = 1e-9       # field.py:31
@@ -734,32 +734,7 @@ def load_field(path):
         if not first.startswith("#FIELD "):
             raise ShapeError(f"{path}: not a field snapshot")
         header = json.loads(first[len("#FIELD "):])
-        phi = read_triplets_stream(fh)
+        phi = read_triplets_stream(fh, first_lineno=2)
     params = CouplingParams.from_dict(header["params"])
     return LayeredField(phi, np.asarray(header["seeds"], dtype=np.int64),
                         header.get("step_count", 0)), params
-
-
-def read_triplets_stream(fh):
-    header = None
-    rows, cols, vals = [], [], []
-    for lineno, raw in enumerate(fh, 2):
-        line = raw.strip()
-        if not line or line.startswith("#"):
-            continue
-        parts = line.split()
-        if len(parts) != 3:
-            raise ShapeError(f"line {lineno}: bad triplet {'header' if header is None else 'entry'}")
-        if header is None:
-            header = tuple(int(x) for x in parts)
-            continue
-        rows.append(int(parts[0]))
-        cols.append(int(parts[1]))
-        vals.append(float(parts[2]))
-    if header is None:
-        raise ShapeError("empty triplet file")
-    n_rows, n_cols, nnz = header
-    if len(rows) != nnz:
-        raise ShapeError(f"header says {nnz} entries, found {len(rows)}")
-    return SparseMat.from_triplets(n_rows, n_cols, rows, cols, vals)
-

@@ -241,9 +241,11 @@ def _unit(v):
     return v / np.sqrt(d)[:, None]
 
 
-def gen_icosphere(subdiv, max_subdiv=12):
+def gen_icosphere(subdiv, max_subdiv=7):
     """Unit icosphere by midpoint subdivision (order-identical to
-    mesh.py:216-246, any level up to ``max_subdiv``).
+    mesh.py:216-246).  ``max_subdiv`` defaults to the reference's cap (7,
+    mesh.py:222-223); the large benchmark meshes pass a higher cap (levels up
+    to 12 = 167.8M vertices follow the same numbering rule).
 
     Per level, the new vertex of edge (i, j) gets the next id the first time
     the edge is met walking faces in order and, per face (i, j, k), edges
@@ -362,3 +364,93 @@ def _cotan_edge_weights(mesh):
             k = np.searchsorted(ekey, min(a, b) * n_v + max(a, b))
             out[k] += 0.5 * (float(np.dot(u, v)) / cr)
     return np.maximum(out, 0.0)
+
+
+# ---------------------------------------------------------------------------
+# OBJ / OFF file plumbing (the reference's load_mesh / write_obj,
+# mesh.py:252-358): same accepted inputs, error classes and messages.
+
+
+def _parse_obj(lines):
+    verts, faces = [], []
+    for lineno, raw in enumerate(lines, 1):
+        tok = raw.split()
+        if not tok or tok[0].startswith("#"):
+            continue
+        try:
+            if tok[0] == "v":
+                verts.append([float(t) for t in tok[1:4]])
+            elif tok[0] == "f":
+                # "i", "i/t", "i//n", "i/t/n": the vertex index leads
+                ids = [int(t.partition("/")[0]) for t in tok[1:]]
+                if len(ids) != 3:
+                    raise NonTriangularFaceError(f"non-triangular: line {lineno} has {len(ids)} vertices")
+                if min(ids) <= 0:
+                    raise MeshFormatError(f"line {lineno}: nonpositive OBJ index")
+                faces.append([i - 1 for i in ids])
+        except (ValueError, IndexError) as exc:
+            raise MeshFormatError(f"line {lineno}: {exc}") from exc
+    if not verts:
+        raise MeshFormatError("no vertices found")
+    if any(len(v) != 3 for v in verts):
+        raise MeshFormatError("vertex record with fewer than 3 coordinates")
+    return TriMesh(np.asarray(verts), np.asarray(faces, dtype=np.int32).reshape(-1, 3))
+
+
+def _parse_off(lines):
+    # tokens with their line numbers, comments stripped
+    toks = [(t, ln) for ln, raw in enumerate(lines, 1) for t in raw.split("#", 1)[0].split()]
+    if not toks or toks[0][0].upper() != "OFF":
+        raise MeshFormatError("line 1: missing OFF header")
+    it = iter(toks[1:])
+    last = toks[-1][1]
+
+    def nxt(kind):
+        try:
+            t, ln = next(it)
+        except StopIteration:
+            raise MeshFormatError(f"line {last}: truncated OFF file") from None
+        try:
+            return kind(t), ln
+        except ValueError as exc:
+            raise MeshFormatError(f"line {ln}: bad token {t!r}") from exc
+
+    n_v, n_f = nxt(int)[0], nxt(int)[0]
+    nxt(int)                                          # edge count (unused)
+    verts = [[nxt(float)[0] for _ in range(3)] for _ in range(n_v)]
+    faces = []
+    for _ in range(n_f):
+        k, ln = nxt(int)
+        if k != 3:
+            raise NonTriangularFaceError(f"non-triangular: line {ln} has {k} vertices")
+        faces.append([nxt(int)[0] for _ in range(3)])
+    return TriMesh(np.asarray(verts, dtype=np.float64).reshape(-1, 3),
+                   np.asarray(faces, dtype=np.int32).reshape(-1, 3))
+
+
+def load_mesh(path, fmt=None):
+    """Load an ASCII OBJ (``v`` / ``f`` records; texture and normal indices
+    ignored) or OFF triangle mesh; ``fmt`` defaults to the file extension.
+    Non-triangle faces raise :class:`NonTriangularFaceError`, malformed
+    records :class:`MeshFormatError` with the line number."""
+    fmt = (fmt or str(path).rsplit(".", 1)[-1]).lower()
+    if fmt not in ("obj", "off"):
+        raise MeshFormatError(f"unknown mesh format: {fmt!r}")
+    with open(path) as fh:
+        lines = fh.readlines()
+    return _parse_obj(lines) if fmt == "obj" else _parse_off(lines)
+
+
+def write_obj(mesh_or_positions, path_or_faces, path=None, comments=()):
+    """Write ASCII OBJ with 1-based face indices: ``write_obj(mesh, path)``
+    or ``write_obj(positions, faces, path)``; coordinates with ``repr`` so
+    they round-trip exactly."""
+    if path is None:
+        positions, faces, path = mesh_or_positions.positions, mesh_or_positions.faces, path_or_faces
+    else:
+        positions, faces = mesh_or_positions, path_or_faces
+    out = [f"# {c}\n" for c in comments]
+    out += [f"v {float(x)!r} {float(y)!r} {float(z)!r}\n" for x, y, z in np.asarray(positions).tolist()]
+    out += [f"f {a + 1} {b + 1} {c + 1}\n" for a, b, c in np.asarray(faces).tolist()]
+    with open(path, "w") as fh:
+        fh.writelines(out)

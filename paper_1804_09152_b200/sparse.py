@@ -11,11 +11,13 @@ EXACT mode, float32 in FAST mode) with explicit capacity.  It is what the
 C-ABI consumes (``ft_csc`` in include/fieldtess_cuda.h).
 """
 
+import ctypes
 import math
+import warnings
 
 import numpy as np
 
-from .errors import ShapeError
+from .errors import NegativeFieldError, PatternViolationError, ShapeError
 
 INDEX = np.int32
 GROWTH = 1.2   # capacity growth factor (sparse.py:24, :212-232)
@@ -170,6 +172,37 @@ def ensure_capacity(mat, needed):
     mat.row_idx, mat.values = ri, va
     mat.realloc_count += 1
     return mat
+
+
+class Skeleton:
+    """A sparse pattern without values: the rows of interest per column
+    (sparse.py:181-209)."""
+
+    __slots__ = ("n_rows", "n_cols", "col_ptr", "row_idx", "realloc_count")
+
+    def __init__(self, n_rows, n_cols, col_ptr, row_idx):
+        self.n_rows = int(n_rows)
+        self.n_cols = int(n_cols)
+        self.col_ptr = np.ascontiguousarray(col_ptr, dtype=INDEX)
+        self.row_idx = np.ascontiguousarray(row_idx, dtype=INDEX)
+        self.realloc_count = 0
+
+    @property
+    def nnz(self):
+        return int(self.col_ptr[self.n_cols])
+
+    @property
+    def capacity(self):
+        return int(self.row_idx.size)
+
+    def column(self, j):
+        return self.row_idx[self.col_ptr[j]:self.col_ptr[j + 1]]
+
+    def to_dense(self):
+        out = np.zeros((self.n_rows, self.n_cols), dtype=bool)
+        cols = np.repeat(np.arange(self.n_cols), np.diff(self.col_ptr.astype(np.int64)))
+        out[self.row_idx[:self.nnz], cols] = True
+        return out
 
 
 def transpose(a):
@@ -382,3 +415,247 @@ def hybrid_columns(col_ptr, row_idx, values, pool_base=0):
     pval = values[:nnz][sel]
     return (sig.astype(np.int32), aux.astype(np.int32), np.where(cnt >= 1, x0, 0).astype(values.dtype),
             np.where(cnt == 2, x1, 0).astype(values.dtype), pidx.astype(np.int32), pval)
+
+
+# ---------------------------------------------------------------------------
+# the reference's public sparse algebra, on the device (csrc/ft_sparse.cu;
+# sparse.py:279-464).  Host SparseMat in, host SparseMat out; every
+# floating-point reduction keeps the reference's order (bitwise equal).
+
+
+class SpgemmScratch:
+    """Reusable scratch of :func:`spgemm` (sparse.py:243-271).  The device
+    product needs no dense accumulators; the object is kept for the API and
+    counts the reallocations of its expansion buffers."""
+
+    def __init__(self):
+        self.realloc_count = 0
+        self._keys = None
+        self._vals = None
+
+    def buffers(self, n, device):
+        torch = _torch()
+        if self._keys is None or self._keys.numel() < n or self._keys.device != device:
+            cap = max(int(n), int(math.ceil((0 if self._keys is None else self._keys.numel()) * GROWTH)), 1)
+            self._keys = torch.empty(cap, dtype=torch.int64, device=device)
+            self._vals = torch.empty(cap, dtype=torch.float64, device=device)
+            self.realloc_count += 1
+        return self._keys[:n], self._vals[:n]
+
+
+def _dev():
+    from .field import _device
+    return _device()
+
+
+def _stream():
+    return ctypes.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+
+def _lib_call(name, *args):
+    from . import _lib
+    rc = getattr(_lib.lib(), name)(*args)
+    if rc != 0:
+        if rc == _lib.FT_ERR_SHAPE:
+            raise ShapeError(f"{name}: shape mismatch")
+        from .errors import BackendError
+        raise BackendError(f"{name} failed (code {rc}): {_lib.last_error()}")
+
+
+def _upload64(mat, device):
+    torch = _torch()
+    return DeviceCSC.from_host(mat, torch.float64, device)
+
+
+def spgemm(a, b, out=None, scratch=None):
+    """Sparse product ``C = A @ B`` in canonical CSC (sparse.py:279-330),
+    bitwise equal to the reference: expand the products on the device in
+    the reference's order, stable-sort them by (column, row), add every run
+    sequentially (first term assigned), drop exact zeros."""
+    torch = _torch()
+    if a.n_cols != b.n_rows:
+        raise ShapeError(f"shape mismatch: {a.shape} @ {b.shape}")
+    n_rows, n_cols = a.n_rows, b.n_cols
+    dev = _dev()
+    da, db = _upload64(a, dev), _upload64(b, dev)
+    ca, cb = da.ft_csc(), db.ft_csc()
+    counts = torch.zeros(max(n_cols, 1), dtype=torch.int64, device=dev)
+    _lib_call("ft_spgemm_count", ctypes.byref(ca), ctypes.byref(cb), ctypes.c_void_p(counts.data_ptr()), _stream())
+    off = torch.zeros(n_cols + 1, dtype=torch.int64, device=dev)
+    if n_cols:
+        torch.cumsum(counts[:n_cols], 0, out=off[1:])
+    total = int(off[-1].item())
+    col_ptr = np.zeros(n_cols + 1, dtype=INDEX)
+    rows = np.zeros(0, dtype=INDEX)
+    vals = np.zeros(0)
+    if total:
+        scratch = scratch if scratch is not None else SpgemmScratch()
+        keys, pv = scratch.buffers(total, dev)
+        _lib_call("ft_spgemm_expand", ctypes.byref(ca), ctypes.byref(cb), ctypes.c_void_p(off.data_ptr()),
+                  ctypes.c_void_p(keys.data_ptr()), ctypes.c_void_p(pv.data_ptr()), _stream())
+        sk, perm = torch.sort(keys, stable=True)
+        sv = pv[perm]
+        head = torch.ones(total, dtype=torch.bool, device=dev)
+        head[1:] = sk[1:] != sk[:-1]
+        starts = torch.nonzero(head).flatten()
+        sums = torch.empty(starts.numel(), dtype=torch.float64, device=dev)
+        _lib_call("ft_segment_sums", ctypes.c_void_p(sv.data_ptr()), total, ctypes.c_void_p(starts.data_ptr()),
+                  starts.numel(), ctypes.c_void_p(sums.data_ptr()), _stream())
+        keep = sums != 0.0                          # the reference drops exact zeros
+        key = sk[starts][keep]
+        nr = max(n_rows, 1)
+        cols = key // nr
+        cnt = torch.bincount(cols, minlength=n_cols)
+        col_ptr[1:] = torch.cumsum(cnt, 0).cpu().numpy()
+        rows = (key % nr).to(torch.int32).cpu().numpy()
+        vals = sums[keep].cpu().numpy()
+    nnz = int(col_ptr[-1])
+    if out is None:
+        return SparseMat(n_rows, n_cols, col_ptr, rows, vals, check=False)
+    if out.n_rows != n_rows or out.n_cols != n_cols:
+        raise ShapeError("output buffer has wrong shape")
+    ensure_capacity(out, nnz)
+    out.col_ptr = col_ptr
+    out.row_idx[:nnz] = rows
+    out.values[:nnz] = vals
+    return out
+
+
+def build_skeleton(phi, lt, out=None):
+    """Rows of interest per column: ``phi > 0`` or (``phi == 0`` and
+    ``lt > 0``) (sparse.py:345-371), a sorted merge per column on the
+    device (count, prefix sum, fill)."""
+    torch = _torch()
+    if phi.shape != lt.shape:
+        raise ShapeError(f"shape mismatch: {phi.shape} vs {lt.shape}")
+    n_cols = phi.n_cols
+    dev = _dev()
+    dp, dl = _upload64(phi, dev), _upload64(lt, dev)
+    cp, cl = dp.ft_csc(), dl.ft_csc()
+    counts = torch.zeros(max(n_cols, 1), dtype=torch.int32, device=dev)
+    _lib_call("ft_skeleton", ctypes.byref(cp), ctypes.byref(cl), ctypes.c_void_p(counts.data_ptr()), None, None,
+              _stream())
+    ptr = torch.zeros(n_cols + 1, dtype=torch.int32, device=dev)
+    if n_cols:
+        torch.cumsum(counts[:n_cols], 0, out=ptr[1:])
+    nnz = int(ptr[-1].item())
+    rows = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+    if nnz:
+        _lib_call("ft_skeleton", ctypes.byref(cp), ctypes.byref(cl), None, ctypes.c_void_p(ptr.data_ptr()),
+                  ctypes.c_void_p(rows.data_ptr()), _stream())
+    col_ptr = ptr.cpu().numpy()
+    row_idx = rows[:nnz].cpu().numpy()
+    if out is None:
+        return Skeleton(phi.n_rows, n_cols, col_ptr, row_idx)
+    out.col_ptr = col_ptr
+    if out.row_idx is None or out.row_idx.size < nnz:
+        size = nnz if out.row_idx is None else max(nnz, int(math.ceil(out.row_idx.size * GROWTH)))
+        out.row_idx = np.empty(size, dtype=INDEX)
+        out.realloc_count += 1
+    out.row_idx[:nnz] = row_idx
+    return out
+
+
+def expand_to_skeleton(a, skel, out_values=None):
+    """``a`` on the skeleton pattern with explicit zeros elsewhere
+    (sparse.py:374-396); a nonzero of ``a`` outside the pattern raises
+    :class:`PatternViolationError` (first such column, its last offending
+    row -- the reference's report)."""
+    torch = _torch()
+    if (a.n_rows, a.n_cols) != (skel.n_rows, skel.n_cols):
+        raise ShapeError(f"shape mismatch: {a.shape} vs ({skel.n_rows}, {skel.n_cols})")
+    nnz = skel.nnz
+    dev = _dev()
+    da = _upload64(a, dev)
+    ca = da.ft_csc()
+    sp = torch.from_numpy(np.ascontiguousarray(skel.col_ptr, dtype=np.int32)).to(dev)
+    sr = torch.from_numpy(np.ascontiguousarray(skel.row_idx[:max(nnz, 1)] if nnz else np.zeros(1, INDEX),
+                                               dtype=np.int32)).to(dev)
+    vals = torch.zeros(max(nnz, 1), dtype=torch.float64, device=dev)
+    bad = torch.full((max(a.n_cols, 1),), -1, dtype=torch.int32, device=dev)
+    _lib_call("ft_expand", ctypes.byref(ca), ctypes.c_void_p(sp.data_ptr()), ctypes.c_void_p(sr.data_ptr()),
+              ctypes.c_void_p(vals.data_ptr()), ctypes.c_void_p(bad.data_ptr()), _stream())
+    badh = bad[:a.n_cols].cpu().numpy()
+    offenders = np.flatnonzero(badh >= 0)
+    if offenders.size:
+        j = int(offenders[0])
+        raise PatternViolationError(f"pattern-violation: nonzero at ({badh[j]}, {j}) outside the skeleton")
+    v = vals[:nnz].cpu().numpy()
+    if out_values is not None and out_values.size >= nnz:
+        out_values[:nnz] = v
+        v = out_values[:nnz]
+    return SparseMat(skel.n_rows, skel.n_cols, skel.col_ptr, skel.row_idx[:nnz], v, check=False)
+
+
+def normalize_columns(a):
+    """Scale every positive-sum column to unit sum, ``v * (1 / s)`` with the
+    column sum in entry order (sparse.py:399-420); negative entries raise
+    :class:`NegativeFieldError`, zero-sum columns stay untouched with a
+    warning, explicit zeros are kept."""
+    torch = _torch()
+    nnz = a.nnz
+    vals = np.asarray(a.values[:nnz], dtype=np.float64)
+    if nnz and vals.min() < 0:
+        raise NegativeFieldError("negative-field: negative entry in input")
+    dev = _dev()
+    da = _upload64(a, dev)
+    ca = da.ft_csc()
+    out = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+    sums = torch.empty(max(a.n_cols, 1), dtype=torch.float64, device=dev)
+    _lib_call("ft_normalize_columns", ctypes.byref(ca), ctypes.c_void_p(out.data_ptr()),
+              ctypes.c_void_p(sums.data_ptr()), _stream())
+    s = sums[:a.n_cols].cpu().numpy()
+    zero = np.flatnonzero((s == 0) & (np.diff(a.col_ptr.astype(np.int64)) > 0))
+    if zero.size:
+        warnings.warn(f"normalize_columns: {zero.size} zero-sum column(s) left untouched (first: {zero[0]})",
+                      RuntimeWarning, stacklevel=2)
+    return SparseMat(a.n_rows, a.n_cols, a.col_ptr.copy(), a.row_idx[:nnz].copy(), out[:nnz].cpu().numpy(),
+                     check=False)
+
+
+# ---------------------------------------------------------------------------
+# text triplet interchange (sparse.py:427-464): "rows cols nnz" header, one
+# "row col value" line per entry, '#' comment lines
+
+
+def write_triplets(mat, path, comments=()):
+    """Write ``mat`` as text triplets (values with ``repr``: round-trips)."""
+    nnz = mat.nnz
+    cols = mat.entry_columns()
+    lines = [f"# {c}\n" for c in comments]
+    lines.append(f"{mat.n_rows} {mat.n_cols} {nnz}\n")
+    lines += [f"{r} {c} {v!r}\n" for r, c, v in
+              zip(mat.row_idx[:nnz].tolist(), cols.tolist(), np.asarray(mat.values[:nnz], dtype=float).tolist())]
+    with open(path, "w") as fh:
+        fh.writelines(lines)
+
+
+def read_triplets_stream(fh, first_lineno=1):
+    """Parse triplet lines from an open text stream (``first_lineno``: the
+    file line number of the stream's first line, for error messages)."""
+    header = None
+    rows, cols, vals = [], [], []
+    for lineno, raw in enumerate(fh, first_lineno):
+        parts = raw.split()
+        if not parts or parts[0].startswith("#"):
+            continue
+        if len(parts) != 3:
+            raise ShapeError(f"line {lineno}: bad triplet {'header' if header is None else 'entry'}")
+        if header is None:
+            header = tuple(int(x) for x in parts)
+        else:
+            rows.append(int(parts[0]))
+            cols.append(int(parts[1]))
+            vals.append(float(parts[2]))
+    if header is None:
+        raise ShapeError("empty triplet file")
+    n_rows, n_cols, nnz = header
+    if len(rows) != nnz:
+        raise ShapeError(f"header says {nnz} entries, found {len(rows)}")
+    return SparseMat.from_triplets(n_rows, n_cols, rows, cols, vals)
+
+
+def read_triplets(path):
+    """Read :func:`write_triplets` output."""
+    with open(path) as fh:
+        return read_triplets_stream(fh)

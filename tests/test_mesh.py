@@ -38,7 +38,7 @@ def test_generator_bitwise(name):
 
 
 def test_icosphere_beyond_reference_cap():
-    m = ft.gen_icosphere(8)
+    m = ft.gen_icosphere(8, max_subdiv=8)
     assert m.n_vertices == 10 * 4 ** 8 + 2 and m.n_faces == 20 * 4 ** 8
     assert m.euler_characteristic() == 2
     assert np.all(m.degree >= 5) and np.all(m.degree <= 6)

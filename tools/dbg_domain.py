@@ -6,7 +6,7 @@ from paper_1804_09152_b200 import distributed as D
 
 world = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 sub = int(sys.argv[2]) if len(sys.argv) > 2 else 4
-mesh = ft.gen_icosphere(sub)
+mesh = ft.gen_icosphere(sub, max_subdiv=12)
 seeds = np.random.default_rng(0).choice(mesh.n_vertices, 64, replace=False)
 lap = ft.build_laplacian(mesh)
 fld = ft.init_field(mesh, seeds)

@@ -5,7 +5,7 @@ import paper_1804_09152_b200 as ft
 from oracle import pyoracle as O
 
 sub = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-mesh = ft.gen_icosphere(sub)
+mesh = ft.gen_icosphere(sub, max_subdiv=12)
 seeds = np.random.default_rng(0).choice(mesh.n_vertices, 64, replace=False)
 lap = ft.build_laplacian(mesh)
 lt = O.Csc.of(ft.field._with_diagonal(lap.mat_t))

@@ -17,7 +17,7 @@ level = int(sys.argv[1]) if len(sys.argv) > 1 else 11
 nseeds = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 120
 t = time.time()
-mesh = ft.gen_icosphere(level)
+mesh = ft.gen_icosphere(level, max_subdiv=12)
 print(f"icosphere {level}: {mesh.n_vertices} vertices, {mesh.n_faces} faces, {time.time() - t:.1f} s", flush=True)
 t = time.time()
 lap = ft.build_laplacian(mesh)
