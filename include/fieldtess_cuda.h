@@ -392,6 +392,14 @@ int ft_lloyd_centroids(const double* positions, int32_t n_vertices,
                        double* point, double* normal, int32_t* status,
                        int32_t* hit_vertex, void* stream);
 
+/* Back-projection alone (backproject, lloyd.py:67-112) from caller-given
+ * points and unit normals (n_cells x 3 doubles, device): status[c] must be
+ * 0 on entry to take part; returns 4 (miss) or the hit vertex as above. */
+int ft_lloyd_backproject(const double* positions, int32_t n_vertices, const int32_t* faces,
+                         int32_t n_faces, const double* period, int32_t n_cells,
+                         const int32_t* cell_ptr, const int32_t* cell_faces, const double* point,
+                         const double* normal, int32_t* status, int32_t* hit_vertex, void* stream);
+
 /* -- dual-mesh adjacency products --------------------------------------- */
 /* One pass over vertices and faces of a (FT_F64) field collects, as keys in
  * four device hash sets (capacity: a power of two; empty slot = ~0):
@@ -408,6 +416,15 @@ int ft_dual_products(const ft_csc* phi, int32_t n_faces, const int32_t* faces,
                      const double* face_area, double threshold, uint64_t* set_v,
                      uint64_t* set_t, uint64_t* set_x, uint64_t* set_3,
                      int64_t set_capacity, int32_t* overflow, void* stream);
+
+/* Candidate triangles of the dual mesh: the 3-cliques i < j < k of a
+ * symmetric cell adjacency in CSR (n rows, sorted, no diagonal) -- the
+ * ring intersection of build_dual (dual.py:331-340).  Count pass: tris ==
+ * NULL, counts[q] for every entry q (nonzero only for q = (i, j), j > i);
+ * fill pass at offsets[q] (the caller's exclusive prefix sum) as int32
+ * triples (i, j, k), k ascending. */
+int ft_clique_triangles(int32_t n, const int32_t* ptr, const int32_t* idx, int64_t* counts,
+                        const int64_t* offsets, int32_t* tris, void* stream);
 
 #ifdef __cplusplus
 }

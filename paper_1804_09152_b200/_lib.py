@@ -102,7 +102,8 @@ EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
            "ft_dual_products", "ft_domain_step", "ft_halo_bytes", "ft_halo_pack",
            "ft_halo_unpack", "ft_domain_combine", "ft_domain_control", "ft_laplacian_pack",
            "ft_point_triangle_distances", "ft_spgemm_count", "ft_spgemm_expand",
-           "ft_segment_sums", "ft_skeleton", "ft_expand", "ft_normalize_columns")
+           "ft_segment_sums", "ft_skeleton", "ft_expand", "ft_normalize_columns",
+           "ft_clique_triangles", "ft_lloyd_backproject")
 
 _lib = None
 
@@ -180,6 +181,10 @@ def _declare(lib):
     lib.ft_expand.restype = ctypes.c_int
     lib.ft_normalize_columns.argtypes = [P(FtCsc), vp, vp, vp]
     lib.ft_normalize_columns.restype = ctypes.c_int
+    lib.ft_clique_triangles.argtypes = [i32, vp, vp, vp, vp, vp, vp]
+    lib.ft_clique_triangles.restype = ctypes.c_int
+    lib.ft_lloyd_backproject.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp]
+    lib.ft_lloyd_backproject.restype = ctypes.c_int
 
 
 def lib():

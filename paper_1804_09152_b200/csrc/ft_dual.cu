@@ -188,7 +188,49 @@ __global__ void dual_face_kernel(const DualParams p) {
                 set_insert(p.set_3, p.mask_3, ((unsigned long long)c[a] * nr + c[b]) * nr + c[d], p.overflow);
 }
 
+// Triangles of the dual: the 3-cliques i < j < k of a symmetric adjacency
+// in CSR (rows sorted, no diagonal).  One thread per undirected edge
+// (i, j), i < j: a sorted merge of the rows of i and j lists the common
+// neighbours k > j.  Count pass (tris == nullptr) into counts[e], fill
+// pass at offsets[e].  Edges are numbered by their position in row i's
+// list (only the entries j > i are edges).
+__global__ void clique_kernel(int n, const int* __restrict__ ptr, const int* __restrict__ idx,
+                              long long* __restrict__ counts, const long long* __restrict__ offsets,
+                              int* __restrict__ tris) {
+    const int i = blockIdx.x;                 // one CTA per row i, threads over its entries
+    if (i >= n) return;
+    for (int q = ptr[i] + threadIdx.x; q < ptr[i + 1]; q += blockDim.x) {
+        const int j = idx[q];
+        long long c = 0, w = tris ? offsets[q] : 0;
+        if (j > i) {
+            int a = ptr[i], b = ptr[j];
+            const int ae = ptr[i + 1], be = ptr[j + 1];
+            while (a < ae && b < be) {
+                const int x = idx[a], y = idx[b];
+                if (x < y) { ++a; continue; }
+                if (y < x) { ++b; continue; }
+                if (x > j) {
+                    if (tris) { tris[3 * w] = i; tris[3 * w + 1] = j; tris[3 * w + 2] = x; ++w; }
+                    ++c;
+                }
+                ++a;
+                ++b;
+            }
+        }
+        if (!tris) counts[q] = c;
+    }
+}
+
 }  // namespace ft
+
+extern "C" int ft_clique_triangles(int32_t n, const int32_t* ptr, const int32_t* idx, int64_t* counts,
+                                   const int64_t* offsets, int32_t* tris, void* stream) {
+    if (n < 0 || !ptr || !idx || (!counts && !tris) || (tris && !offsets)) return FT_ERR_ARG;
+    if (n > 0)
+        ft::clique_kernel<<<n, 128, 0, (cudaStream_t)stream>>>(n, ptr, idx, (long long*)counts,
+                                                              (const long long*)offsets, tris);
+    return cudaGetLastError() == cudaSuccess ? FT_OK : FT_ERR_CUDA;
+}
 
 extern "C" int ft_dual_products(const ft_csc* phi, int32_t n_faces, const int32_t* faces,
                                 const double* face_area, double threshold, uint64_t* set_v,

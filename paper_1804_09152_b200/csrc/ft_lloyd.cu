@@ -447,11 +447,13 @@ extern "C" int ft_faces_by_cell(const ft_csc* phi, int32_t min_row, int32_t n_fa
         ft::face_fill_kernel<<<(n_faces + 255) / 256, 256, 0, s>>>(
             n_faces, faces, phi->col_ptr, phi->row_idx, (const double*)phi->values, min_row, cell_ptr, cursor,
             cell_faces);
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[64] = {};          // the opt-in is per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr[dev & 63]) {
         cudaFuncSetAttribute(ft::segment_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              ft::kSortMax * (int)sizeof(int));
-        attr = true;
+        attr[dev & 63] = true;
     }
     ft::segment_sort_kernel<<<nr < 1184 ? nr : 1184, 1024, ft::kSortMax * sizeof(int), s>>>(
         nr, cell_ptr, cell_faces, big_flag);
@@ -463,15 +465,9 @@ extern "C" int ft_faces_by_cell(const ft_csc* phi, int32_t min_row, int32_t n_fa
     return lcheck("ft_faces_by_cell");
 }
 
-extern "C" int ft_lloyd_centroids(const double* positions, int32_t n_vertices, const int32_t* faces,
-                                  int32_t n_faces, const double* face_area, const double* face_bary,
-                                  const double* face_normal, const double* period /*[6] or NULL*/,
-                                  int32_t n_cells, const int32_t* cell_ptr, const int32_t* cell_faces,
-                                  const int64_t* seeds, double* point, double* normal, int32_t* status,
-                                  int32_t* hit_vertex, void* stream) {
-    if (!positions || !faces || !cell_ptr || !cell_faces || !point || !normal || !status || !hit_vertex)
-        return FT_ERR_ARG;
-    ft::Geo g;
+static int fill_geo(ft::Geo& g, const double* positions, int32_t n_vertices, const int32_t* faces, int32_t n_faces,
+                    const double* face_area, const double* face_bary, const double* face_normal,
+                    const double* period) {
     g.pos = positions; g.faces = faces; g.area = face_area; g.bary = face_bary; g.fnorm = face_normal;
     g.n_v = n_vertices; g.n_f = n_faces;
     g.periodic = period != nullptr;
@@ -485,6 +481,20 @@ extern "C" int ft_lloyd_centroids(const double* positions, int32_t n_vertices, c
         for (int k = 0; k < 3; ++k) { g.pv[0][k] = 0.0; g.pv[1][k] = 0.0; }
         g.a11 = g.a12 = g.a22 = g.r11 = g.r22 = 0.0;
     }
+    return FT_OK;
+}
+
+extern "C" int ft_lloyd_centroids(const double* positions, int32_t n_vertices, const int32_t* faces,
+                                  int32_t n_faces, const double* face_area, const double* face_bary,
+                                  const double* face_normal, const double* period /*[6] or NULL*/,
+                                  int32_t n_cells, const int32_t* cell_ptr, const int32_t* cell_faces,
+                                  const int64_t* seeds, double* point, double* normal, int32_t* status,
+                                  int32_t* hit_vertex, void* stream) {
+    if (!positions || !faces || !cell_ptr || !cell_faces || !point || !normal || !status || !hit_vertex)
+        return FT_ERR_ARG;
+    ft::Geo g;
+    if (fill_geo(g, positions, n_vertices, faces, n_faces, face_area, face_bary, face_normal, period) != FT_OK)
+        return FT_ERR_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     if (n_cells > 0) {
         ft::centroid_kernel<<<(n_cells + 127) / 128, 128, 0, s>>>(g, n_cells, cell_ptr, cell_faces, (const long long*)seeds,
@@ -493,4 +503,20 @@ extern "C" int ft_lloyd_centroids(const double* positions, int32_t n_vertices, c
                                                                            point, normal, status, hit_vertex);
     }
     return lcheck("ft_lloyd_centroids");
+}
+
+extern "C" int ft_lloyd_backproject(const double* positions, int32_t n_vertices, const int32_t* faces,
+                                    int32_t n_faces, const double* period, int32_t n_cells,
+                                    const int32_t* cell_ptr, const int32_t* cell_faces, const double* point,
+                                    const double* normal, int32_t* status, int32_t* hit_vertex, void* stream) {
+    if (!positions || !faces || !cell_ptr || !cell_faces || !point || !normal || !status || !hit_vertex)
+        return FT_ERR_ARG;
+    ft::Geo g;
+    if (fill_geo(g, positions, n_vertices, faces, n_faces, nullptr, nullptr, nullptr, period) != FT_OK)
+        return FT_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n_cells > 0)
+        ft::backproject_kernel<<<(n_cells * 32 + 255) / 256, 256, 0, s>>>(g, n_cells, cell_ptr, cell_faces,
+                                                                           point, normal, status, hit_vertex);
+    return lcheck("ft_lloyd_backproject");
 }

@@ -866,11 +866,11 @@ def lloyd_iterate_partitioned(state, mesh, lap, params, n_iter, transport, parti
     else:
         trace = []
     if not state.history:
-        LL._record(state, mesh, trace, {"reseed_misses": 0, "seed_collisions": 0})
+        state.history.append(LL._history_entry(state, mesh, trace, {"reseed_misses": 0, "seed_collisions": 0}))
     for _ in range(n_iter):
         seeds, report = LL._reseed(state, mesh)
         state.seeds = seeds
         state.iteration += 1
         state.field, trace = run_evolve(seeds)
-        LL._record(state, mesh, trace, report)
+        state.history.append(LL._history_entry(state, mesh, trace, report))
     return state

@@ -14,8 +14,8 @@ collision pass, which stays sequential on the host, as in the reference
 * all cells' centroids and normals, and the back-projected vertices, via
   ``ft_lloyd_centroids``, using numpy's exact reduction orders.
 
-The single-cell helpers ``approx_centroid`` / ``backproject`` are host numpy
-restatements of the reference functions (API convenience).
+The single-cell helpers ``approx_centroid`` / ``backproject`` run the same
+kernels on one cell; ``cell_areas`` is the device sparse product PHI a.
 """
 
 import ctypes
@@ -139,73 +139,87 @@ def cell_triangles(field, mesh, cell, product=None):
     return faces.astype(np.int64)
 
 
+def _single_cell(faces, device):
+    """The one-cell CSR the batched Lloyd kernels take (cell 0 = row 1)."""
+    torch = _torch()
+    f = np.ascontiguousarray(faces, dtype=np.int32)
+    ptr = torch.tensor([0, 0, f.size], dtype=torch.int32, device=device)
+    lst = torch.from_numpy(f if f.size else np.zeros(1, np.int32)).to(device)
+    return ptr, lst
+
+
+def _geometry_status(status, cell):
+    if status == LLOYD_DEGENERATE or status == LLOYD_VANISHED:
+        raise DegenerateCellError(f"degenerate-cell: cell {cell} has zero area")
+    if status == LLOYD_NULLNORMAL:
+        raise NullNormalError(f"null-normal: cell {cell} normals cancel")
+
+
 def approx_centroid(field, mesh, cell, faces=None):
-    """Area-weighted barycenter average and normalised area-weighted normal
-    of the cell's triangles (lloyd.py:42-64)."""
+    """Area-weighted mean barycenter and normalised area-weighted normal of
+    the cell's triangles (lloyd.py:42-64) -- the device centroid kernel on
+    one cell (numpy's reduction orders, periodic barycenters unwrapped
+    around the cell's seed)."""
+    torch = _torch()
     if faces is None:
         faces = cell_triangles(field, mesh, cell)
-    areas = mesh.face_area[faces]
-    total = float(areas.sum())
-    if total <= 0.0:
-        raise DegenerateCellError(f"degenerate-cell: cell {cell} has zero area")
-    barys = mesh.face_barycenter[faces]
-    if mesh.periodic:
-        ref = mesh.positions[field.seed_vertices[cell]]
-        barys = ref + mesh.wrap_deltas(barys - ref)
-    point = (areas[:, None] * barys).sum(axis=0) / total
-    nsum = (areas[:, None] * mesh.face_normal[faces]).sum(axis=0)
-    norm = float(np.linalg.norm(nsum))
-    if norm <= 1e-12 * total:
-        raise NullNormalError(f"null-normal: cell {cell} normals cancel")
-    return point, nsum / norm
+    dm = device_mesh(mesh)
+    dev = dm.positions.device
+    ptr, lst = _single_cell(faces, dev)
+    seed = torch.tensor([int(field.seed_vertices[cell])], dtype=torch.int64, device=dev)
+    out = torch.zeros(6, dtype=torch.float64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    hit = torch.zeros(1, dtype=torch.int32, device=dev)
+    vp = ctypes.c_void_p
+    _check(_lib.lib().ft_lloyd_centroids(
+        vp(dm.positions.data_ptr()), dm.n_vertices, vp(dm.faces.data_ptr()), dm.n_faces,
+        vp(dm.area.data_ptr()), vp(dm.bary.data_ptr()), vp(dm.normal.data_ptr()),
+        ctypes.cast(dm.period, ctypes.c_void_p) if dm.period is not None else None, 1,
+        vp(ptr.data_ptr()), vp(lst.data_ptr()), vp(seed.data_ptr()), vp(out.data_ptr()),
+        vp(out.data_ptr() + 24), vp(status.data_ptr()), vp(hit.data_ptr()), _stream_handle()),
+        "ft_lloyd_centroids")
+    _geometry_status(int(status.item()), cell)
+    o = out.cpu().numpy()
+    return o[:3].copy(), o[3:].copy()
 
 
 def backproject(point, normal, field, mesh, cell, faces=None):
-    """Line point +- t*normal against the cell's triangles; the smallest |t|
-    hit's nearest corner vertex, or None on a miss (lloyd.py:67-112)."""
+    """Cast the line ``point + t normal`` through the cell's triangles;
+    the corner vertex nearest to the hit of smallest |t|, or None on a miss
+    (lloyd.py:67-112) -- the device back-projection kernel on one cell."""
+    torch = _torch()
     if faces is None:
         faces = cell_triangles(field, mesh, cell)
-    point = np.asarray(point, dtype=np.float64)
-    normal = np.asarray(normal, dtype=np.float64)
-    tri = mesh.faces[faces]
-    p0 = mesh.positions[tri[:, 0]]
-    if mesh.periodic:
-        e1 = mesh.wrap_deltas(mesh.positions[tri[:, 1]] - p0)
-        e2 = mesh.wrap_deltas(mesh.positions[tri[:, 2]] - p0)
-        bc = p0 + (e1 + e2) / 3.0
-        p0 = p0 + (point + mesh.wrap_deltas(bc - point)) - bc
-    else:
-        e1 = mesh.positions[tri[:, 1]] - p0
-        e2 = mesh.positions[tri[:, 2]] - p0
-    h = np.cross(np.broadcast_to(normal, e2.shape), e2)
-    det = np.einsum("ij,ij->i", e1, h)
-    scale = np.linalg.norm(e1, axis=1) * np.linalg.norm(e2, axis=1)
-    ok = np.abs(det) > 1e-14 * np.maximum(scale, 1e-300)
-    s = point - p0
-    with np.errstate(divide="ignore", invalid="ignore"):
-        u = np.einsum("ij,ij->i", s, h) / det
-        q = np.cross(s, e1)
-        v = np.einsum("ij,j->i", q, normal) / det
-        t = np.einsum("ij,ij->i", e2, q) / det
-    eps = 1e-12
-    hit = ok & (u >= -eps) & (v >= -eps) & (u + v <= 1.0 + eps)
-    if not hit.any():
-        return None
-    idx = np.flatnonzero(hit)
-    best = idx[np.argmin(np.abs(t[idx]))]
-    hp = point + t[best] * normal
-    corners = np.stack([p0[best], p0[best] + e1[best], p0[best] + e2[best]])
-    return int(tri[best, int(np.argmin(np.linalg.norm(corners - hp, axis=1)))])
+    dm = device_mesh(mesh)
+    dev = dm.positions.device
+    ptr, lst = _single_cell(faces, dev)
+    pn = np.concatenate([np.asarray(point, dtype=np.float64).ravel(), np.asarray(normal, dtype=np.float64).ravel()])
+    pnd = torch.from_numpy(pn).to(dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    hit = torch.full((1,), -1, dtype=torch.int32, device=dev)
+    vp = ctypes.c_void_p
+    _check(_lib.lib().ft_lloyd_backproject(
+        vp(dm.positions.data_ptr()), dm.n_vertices, vp(dm.faces.data_ptr()), dm.n_faces,
+        ctypes.cast(dm.period, ctypes.c_void_p) if dm.period is not None else None, 1,
+        vp(ptr.data_ptr()), vp(lst.data_ptr()), vp(pnd.data_ptr()), vp(pnd.data_ptr() + 24),
+        vp(status.data_ptr()), vp(hit.data_ptr()), _stream_handle()), "ft_lloyd_backproject")
+    h = int(hit.item())
+    return None if h < 0 else h
 
 
 def cell_areas(field, mesh):
-    """Field-weighted area per cell: sum of vertex_area * phi (lloyd.py:115-125)."""
-    phi = field.phi
-    nnz = phi.nnz
-    w = phi.values[:nnz] * mesh.vertex_area[phi.entry_columns()]
-    sums = np.zeros(phi.n_rows)
-    np.add.at(sums, phi.row_idx[:nnz], w)
-    return sums[1:]
+    """Field-weighted area of every cell, sum over vertices of
+    vertex_area * phi (lloyd.py:115-125): the sparse product PHI a on the
+    device (the products phi * area accumulated per row in vertex order,
+    the reference's np.add.at order); the base row is dropped."""
+    from .sparse import spgemm
+    a = SparseMat(mesh.n_vertices, 1, np.array([0, mesh.n_vertices], dtype=INDEX),
+                  np.arange(mesh.n_vertices, dtype=INDEX), np.asarray(mesh.vertex_area, dtype=np.float64),
+                  check=False)
+    prod = spgemm(field.phi, a)
+    out = np.zeros(field.phi.n_rows)
+    out[prod.row_idx[:prod.nnz]] = prod.values[:prod.nnz]
+    return out[1:]
 
 
 def cell_geometry(field, mesh, seeds=None):
@@ -241,7 +255,8 @@ def cell_geometry(field, mesh, seeds=None):
 
 @dataclass
 class LloydState:
-    """Relaxation state: current seeds, field, and per-iteration history."""
+    """Relaxation state (lloyd.py:128-138): the seeds, the current field,
+    the iteration counter and one history record per evolve pass."""
 
     seeds: np.ndarray
     field: object = None
@@ -252,18 +267,19 @@ class LloydState:
         return self.history
 
 
-def _record(state, mesh, trace, reseed_report):
+def _history_entry(state, mesh, trace, report):
+    """One history record (the reference's keys, lloyd.py:141-152)."""
+    seeds = np.asarray(state.seeds, dtype=np.int64)
     areas = cell_areas(state.field, mesh)
-    state.history.append({
-        "iteration": state.iteration,
-        "seeds": [int(s) for s in state.seeds],
-        "seed_positions": mesh.positions[state.seeds].tolist(),
-        "cell_areas": areas.tolist(),
-        "area_variance": float(np.var(areas)),
-        "steps": len(trace),
-        "converged": bool(trace[-1].converged) if trace else True,
-        **reseed_report,
-    })
+    rec = dict(iteration=state.iteration,
+               seeds=seeds.tolist(),
+               seed_positions=mesh.positions[seeds].tolist(),
+               cell_areas=areas.tolist(),
+               area_variance=float(np.var(areas)),
+               steps=len(trace),
+               converged=bool(trace[-1].converged) if len(trace) else True)
+    rec.update(report)
+    return rec
 
 
 def _reseed(state, mesh):
@@ -299,25 +315,29 @@ def _reseed(state, mesh):
 
 
 def lloyd_iterate(state, mesh, lap, params, n_iter, max_steps=1000, tol=1e-4):
-    """``n_iter`` relaxation iterations after the initial evolve; records
-    ``n_iter + 1`` passes in ``state.history`` (lloyd.py:198-229)."""
+    """Lloyd-like relaxation (lloyd.py:198-229): unless the state's field has
+    already been stepped, evolve it first; then ``n_iter`` times reseed at
+    the back-projected centroids, re-seed the field and evolve again.  Each
+    evolve pass appends a history record, so a fresh state ends with
+    ``n_iter + 1`` records."""
     if n_iter < 1:
         raise ShapeError("n_iter must be >= 1")
     ws = StepWorkspace()
+
+    def converge(fld):
+        return evolve(fld, lap, params, max_steps=max_steps, tol=tol, workspace=ws)
+
+    no_reseed = {"reseed_misses": 0, "seed_collisions": 0}
     if state.field is None:
         state.field = init_field(mesh, state.seeds)
+    trace = []
     if state.field.step_count == 0:
-        state.field, trace = evolve(state.field, lap, params, max_steps=max_steps, tol=tol, workspace=ws)
-    else:
-        trace = []
+        state.field, trace = converge(state.field)
     if not state.history:
-        _record(state, mesh, trace, {"reseed_misses": 0, "seed_collisions": 0})
+        state.history.append(_history_entry(state, mesh, trace, no_reseed))
     for _ in range(n_iter):
-        seeds, report = _reseed(state, mesh)
-        state.seeds = seeds
+        state.seeds, report = _reseed(state, mesh)
         state.iteration += 1
-        state.field = init_field(mesh, seeds, precision=state.field.precision)
-        state.field, trace = evolve(state.field, lap, params, max_steps=max_steps, tol=tol, workspace=ws)
-        _record(state, mesh, trace, report)
+        state.field, trace = converge(init_field(mesh, state.seeds, precision=state.field.precision))
+        state.history.append(_history_entry(state, mesh, trace, report))
     return state
-

@@ -256,6 +256,37 @@ def make_c1_dual(fld, mesh, name="c1_dual.json"):
     print(name, "triangles", len(res["triangles"]), "euler", res["euler"])
 
 
+def make_dual_winding():
+    """Exact oriented dual triangles (order and winding) of the reference's
+    build_dual on the C1 / C2 golden fields: without cell normals, and with
+    outward / inward cell normals (the majority-normal flip)."""
+    from fieldtess import dual as dualmod
+    out = {}
+    for name, traj, snap, level in (("c1", "c1_traj.npz", 500, 4), ("c2", "c2_traj.npz", 1000, 7)):
+        path = os.path.join(HERE, traj)
+        if not os.path.exists(path):
+            continue
+        t = np.load(path)
+        shp = t[f"s{snap}_shape"]
+        phi = ft.SparseMat(int(shp[0]), int(shp[1]), t[f"s{snap}_ptr"], t[f"s{snap}_idx"], t[f"s{snap}_val"],
+                           check=False)
+        mesh = ft.gen_icosphere(level)
+        fld = LayeredField(phi, t["seeds"], snap)
+        a_v = dualmod.vertex_adjacency(fld, 0.25)
+        a_t = dualmod.triangle_adjacency(fld, mesh, 0.25)
+        cur = dualmod.confirm_candidates(fld, mesh, a_v, a_t, 0.25)
+        pos = mesh.positions[np.asarray(t["seeds"], dtype=np.int64)]
+        nrm = pos / np.linalg.norm(pos, axis=1)[:, None]
+        out[name] = {
+            "plain": dualmod.build_dual(cur, np.zeros((fld.n_cells, 3))).triangles.tolist(),
+            "outward": dualmod.build_dual(cur, pos, cell_normals=nrm).triangles.tolist(),
+            "inward": dualmod.build_dual(cur, pos, cell_normals=-nrm).triangles.tolist(),
+        }
+        print("winding", name, len(out[name]["plain"]))
+    with open(os.path.join(HERE, "dual_winding.json"), "w") as fh:
+        json.dump(out, fh)
+
+
 def make_cell_geometry(name, mesh, fld):
     """Reference approx_centroid / backproject for every cell of fld."""
     from fieldtess import lloyd as L
@@ -364,7 +395,8 @@ def make_analysis():
 def main():
     if "--only" in sys.argv:
         for name in sys.argv[sys.argv.index("--only") + 1].split(","):
-            {"seeds_collide": make_seed_collisions, "analysis": make_analysis}[name]()
+            {"seeds_collide": make_seed_collisions, "analysis": make_analysis,
+             "winding": make_dual_winding}[name]()
         return
     make_step_cases()
     make_labels_cases()
@@ -373,6 +405,7 @@ def main():
     c1 = trajectory(ico4, seeds["ico4"], {1, 2, 10, 100, 500},
                     os.path.join(HERE, "c1_traj.npz"), 500)
     make_c1_dual(c1, ico4)
+    make_dual_winding()
     geo = make_cell_geometry("c1", ico4, c1)
     torus = ft.gen_periodic_grid(64, 64)
     tfld = trajectory(torus, seeds["torus64"], {1, 60, 300},

@@ -96,3 +96,24 @@ def test_dual_from_partitioned_evolve_matches_reference():
     assert sorted(map(list, cur.pairs())) == ref["curated"]
     dm = ft.build_dual(cur, np.zeros((fld.n_cells, 3)))
     assert sorted(map(sorted, dm.triangles.tolist())) == ref["triangles"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,traj,snap,level", [("c1", "c1_traj.npz", 500, 4), ("c2", "c2_traj.npz", 1000, 7)])
+def test_dual_winding_and_normal_flip_match_reference(name, traj, snap, level):
+    """The exact triangle list of build_dual -- order, winding (the
+    depth-first propagation) and the majority-normal flip with outward and
+    inward cell normals -- equals the reference's (golden dual_winding.json,
+    ref dual.py:284-391)."""
+    ref = golden_json("dual_winding.json").get(name)
+    if ref is None:
+        pytest.skip("no winding golden")
+    mesh = ft.gen_icosphere(level)
+    fld = _field(traj, snap)
+    cur = ft.confirm_candidates(fld, mesh, ft.vertex_adjacency(fld, 0.25), ft.triangle_adjacency(fld, mesh, 0.25),
+                                0.25)
+    pos = mesh.positions[np.asarray(fld.seed_vertices, dtype=np.int64)]
+    nrm = pos / np.linalg.norm(pos, axis=1)[:, None]
+    assert ft.build_dual(cur, np.zeros((fld.n_cells, 3))).triangles.tolist() == ref["plain"]
+    assert ft.build_dual(cur, pos, cell_normals=nrm).triangles.tolist() == ref["outward"]
+    assert ft.build_dual(cur, pos, cell_normals=-nrm).triangles.tolist() == ref["inward"]

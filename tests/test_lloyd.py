@@ -20,9 +20,11 @@ CASES = [("c1", "c1_traj.npz", 500, lambda: ft.gen_icosphere(4)),
          ("torus", "torus_traj.npz", 300, lambda: ft.gen_periodic_grid(64, 64))]
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("name,traj,snap,mk", CASES)
-def test_host_helpers_match_reference(name, traj, snap, mk):
-    """The host single-cell helpers restate the reference exactly."""
+def test_single_cell_helpers_match_reference(name, traj, snap, mk):
+    """approx_centroid / backproject on one cell (the device kernels) equal
+    the reference's, bitwise, for every cell."""
     g = golden_npz("cell_geometry.npz")
     mesh, fld = mk(), _field(traj, snap)
     prod = ft.SparseMat(*g[f"{name}_fbc_shape"], g[f"{name}_fbc_ptr"], g[f"{name}_fbc_idx"],
