@@ -241,9 +241,11 @@ int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
 
 /* -- partitioned fields (one rank per GPU) ------------------------------- */
 /* A field of n_vertices columns split into contiguous owned column ranges,
- * one per rank.  Every rank keeps two tiled buffers over ALL columns (global
- * descriptors) in which its owned columns and its halo (the non-owned
- * columns its owned L^T columns read) are valid; one Euler step is
+ * one per rank.  Every rank keeps two tiled buffers over its LOCAL columns:
+ * the sorted union of its owned columns and its halo (the non-owned columns
+ * its owned L^T columns read), numbered 0 .. n_local-1 in global order, so
+ * the owned ones form the range [col_begin, col_begin + col_count).  One
+ * Euler step is
  *   ft_domain_step     owned columns -> out (entries [0, step_capacity))
  *   ft_halo_pack       per peer: the owned columns the peer reads -> message
  *   (all-gather of the per-rank records; ncclAllGather)
@@ -251,27 +253,32 @@ int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
  *                      on every rank (fixed rank order)
  *   (message exchange with the peers; ncclSend / ncclRecv)
  *   ft_halo_unpack     per peer: message -> halo columns of out (entries
- *                      from step_capacity on, `slots` per column)
- * Every launch is a device-side no-op once the control block's done flag is
- * set (converged / max steps / failure), so a host loop may enqueue steps
- * ahead and read ft_domain_control only every few steps.  The owned columns
- * are bitwise identical to the single-GPU ft_evolve.  Host reference:
+ *                      from step_capacity on, `slots` per column); a halo
+ *                      column that changed stamps its owned readers active
+ * With FT_LAP_SYMMETRIC a rank steps its active set only (as ft_evolve);
+ * ranks decide full / active steps independently.  Every launch is a
+ * device-side no-op once the control block's done flag is set (converged /
+ * max steps / failure), so a host loop may enqueue steps ahead and read
+ * ft_domain_control only every few steps.  The owned columns are bitwise
+ * identical to the single-GPU ft_evolve.  Host reference:
  * paper_1804_09152_b200/distributed.py (the reference is single-process). */
 typedef struct {
-    int32_t col_begin;       /* first owned column (global index)          */
-    int32_t col_count;       /* number of owned columns                    */
+    int32_t col_begin;       /* first owned local column                    */
+    int32_t col_count;       /* number of owned columns                     */
     int64_t step_capacity;   /* entries the step may use in `out`          */
     const int32_t* report_ids;  /* nullable, device [col_count]: the caller's
-                                   vertex ids of the owned columns (a renumbered
-                                   partition); NaN / pattern errors report them */
+                                   vertex ids of the owned columns; NaN /
+                                   pattern errors report them              */
+    int32_t out_id;          /* 0 / 1: which of the two buffers `out` is   */
+    int32_t pad;
 } ft_domain;
 
 #define FT_HALO_FORCE 1      /* pack / unpack even when done is set         */
 
-/* One step of the owned columns (all tiers) plus the local statistics
- * record.  lap_rows: the owned columns of L^T (n_rows = n_vertices, n_cols
- * = col_count, global row indices).  workspace: ft_workspace_bytes(
- * col_count).  `record` (device) receives the local ft_step_stats. */
+/* One step of the owned columns (all kernels) plus the local statistics
+ * record.  lap_rows: the owned columns of L^T (n_rows = n_local, n_cols =
+ * col_count, local row indices).  workspace: ft_workspace_bytes(n_local).
+ * `record` (device) receives the local ft_step_stats. */
 int ft_domain_step(const ft_csc* lap_rows, int32_t lap_flags, const ft_tiled* in,
                    ft_tiled* out, int32_t dtype, const ft_params* params,
                    const ft_domain* dom, void* workspace, size_t ws_bytes,
@@ -291,11 +298,15 @@ int ft_halo_pack(const ft_tiled* src, const int32_t* cols, int32_t n, int32_t sl
 
 /* Column cols[i] of `dst` <- message entry i: in the dense arrays when it
  * holds at most two entries, else at pool entries [region + i*slots,
- * region + i*slots + count).  Skipped when done is set
- * (unless FT_HALO_FORCE). */
+ * region + i*slots + count).  With `prev` (the step's input buffer) and the
+ * readers CSR (readers_ptr[n+1], readers_idx: the owned local columns that
+ * read cols[i]), a column that differs from its copy in `prev` stamps its
+ * readers active for the next step.  Skipped when done is set (unless
+ * FT_HALO_FORCE). */
 int ft_halo_unpack(ft_tiled* dst, const int32_t* cols, int32_t n, int32_t slots,
                    int32_t dtype, const void* msg, int64_t region, void* workspace,
-                   int32_t flags, void* stream);
+                   int32_t flags, const ft_tiled* prev, const int32_t* readers_ptr,
+                   const int32_t* readers_idx, void* stream);
 
 /* Global record from the all-gathered per-rank records (device, `world`
  * records in rank order): max of max_delta, base_mass summed in rank

@@ -68,7 +68,8 @@ class FtTiled(ctypes.Structure):
 
 class FtDomain(ctypes.Structure):
     _fields_ = [("col_begin", ctypes.c_int32), ("col_count", ctypes.c_int32),
-                ("step_capacity", ctypes.c_int64), ("report_ids", ctypes.c_void_p)]
+                ("step_capacity", ctypes.c_int64), ("report_ids", ctypes.c_void_p),
+                ("out_id", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 class FtStepStats(ctypes.Structure):
@@ -158,7 +159,7 @@ def _declare(lib):
     lib.ft_halo_pack.argtypes = [P(FtTiled), vp, i32, i32, i32, vp, vp, vp, vp, i32, vp]
     lib.ft_halo_pack.restype = ctypes.c_int
     lib.ft_halo_unpack.argtypes = [P(FtTiled), vp, i32, i32, i32, vp, ctypes.c_int64, vp, i32,
-                                   vp]
+                                   P(FtTiled), vp, vp, vp]
     lib.ft_halo_unpack.restype = ctypes.c_int
     lib.ft_domain_combine.argtypes = [vp, i32, i32, i32, ctypes.c_double, ctypes.c_double, vp,
                                       vp, vp]

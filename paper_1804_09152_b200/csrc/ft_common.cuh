@@ -58,8 +58,8 @@ static_assert(sizeof(Control) % 16 == 0, "Control must stay 16B aligned");
 //   w2[n]     columns the three-row kernel hands to the warp kernel
 //   skc[n]    interest-skeleton size of each column when it was last computed
 //   stamp[n]  mark: column is active in the step whose sequence number (mod
-//             256) equals the stamp
-//   chunk_off compaction chunk offsets
+//             256) equals the stamp (indexed by buffer column)
+//   chunk_off compaction chunk offsets (first, see carve_workspace)
 struct Workspace {
     Control*       ctl;
     int*           act;
@@ -88,12 +88,15 @@ inline Workspace carve_workspace(void* base, int n_v) {
     p += sizeof(Control);
     w.n = n_v;
     w.num_chunks = num_chunks_for(n_v);
+    // chunk_off first: a compaction of a column range (fewer chunks) carves
+    // the same workspace with a smaller n and must not touch the arrays
+    // after it (the active-set state)
+    w.chunk_off = (long long*)p; p = align16(p + ((size_t)w.num_chunks + 2) * 8);
     w.act = (int*)p;             p = align16(p + (size_t)n_v * 4);
     w.wide = (int*)p;            p = align16(p + (size_t)n_v * 4);
     w.w2 = (int*)p;              p = align16(p + (size_t)n_v * 4);
     w.skc = (int*)p;             p = align16(p + (size_t)n_v * 4);
-    w.stamp = (unsigned char*)p; p = align16(p + (size_t)n_v + 64);   // + padding: prep reads 64 B
-    w.chunk_off = (long long*)p;
+    w.stamp = (unsigned char*)p;   // + 64 bytes of padding: prep reads 64-byte groups
     return w;
 }
 

@@ -31,7 +31,24 @@ struct HaloParams {
     int* need;
     Control* ctl;
     int force;
+    // unpack: the step's input buffer and the owned readers of each halo
+    // column (nullable): a changed halo column stamps its readers active
+    HybIn prev;
+    const int* rd_ptr;
+    const int* rd_idx;
+    unsigned char* stamp;
 };
+
+template <typename T>
+__device__ __forceinline__ bool bits_differ(T a, T b);
+template <>
+__device__ __forceinline__ bool bits_differ<double>(double a, double b) {
+    return __double_as_longlong(a) != __double_as_longlong(b);
+}
+template <>
+__device__ __forceinline__ bool bits_differ<float>(float a, float b) {
+    return __float_as_int(a) != __float_as_int(b);
+}
 
 template <typename T>
 __global__ void __launch_bounds__(256) halo_pack_kernel(const HaloParams h) {
@@ -95,6 +112,21 @@ __global__ void __launch_bounds__(256) halo_unpack_kernel(const HaloParams h) {
     }
     // a peer's non-finite value: this rank's next step checks its inputs
     if (nf) atomicOr(&h.ctl->nonfinite, 1u);
+    if (!h.rd_ptr) return;
+    // the column against its previous value (the step's input buffer)
+    const int ps = h.prev.sig[u];
+    bool changed = sig_count(ps) != c;
+    if (!changed && c > 0) {
+        const int pa = c >= 2 ? h.prev.aux[u] : 0;
+        for (int t = 0; t < c && !changed; ++t) {
+            const int r = ps >= 0 ? (t == 0 ? (ps & ~kPair) : pa) : h.prev.pidx[pa + t];
+            const T x = ps >= 0 ? ((const T*)(t == 0 ? h.prev.v0 : h.prev.v1))[u] : ((const T*)h.prev.pval)[pa + t];
+            changed = r != h.m_rows[o + t] || bits_differ<T>(x, mv[o + t]);
+        }
+    }
+    if (!changed) return;
+    const unsigned char cur = (unsigned char)*(volatile const int*)&h.ctl->seq;   // the next step's stamp
+    for (int q = h.rd_ptr[i]; q < h.rd_ptr[i + 1]; ++q) h.stamp[h.rd_idx[q]] = cur;
 }
 
 __device__ __forceinline__ int failure_rank(int status) {
@@ -160,6 +192,7 @@ __global__ void combine_kernel(const ft_step_stats* rec, int world, int rank, in
 
 __global__ void control_kernel(Control* ctl, int set_steps, long long* out) {
     if (set_steps >= 0) {
+        ctl->full = 1;               // (re)start: the next step recomputes every owned column
         ctl->done = 0;
         ctl->status = FT_STATUS_OK;
         ctl->needed = 0;
@@ -186,6 +219,10 @@ static bool fill_halo(HaloParams& h, ft_tiled* t, const int32_t* cols, int32_t n
     h.record = nullptr; h.need = nullptr;
     h.ctl = (Control*)workspace;          // the control block leads the workspace
     h.force = flags & FT_HALO_FORCE;
+    h.prev = HybIn{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    h.rd_ptr = nullptr;
+    h.rd_idx = nullptr;
+    h.stamp = nullptr;
     return true;
 }
 
@@ -216,12 +253,20 @@ extern "C" int ft_halo_pack(const ft_tiled* src, const int32_t* cols, int32_t n,
 }
 
 extern "C" int ft_halo_unpack(ft_tiled* dst, const int32_t* cols, int32_t n, int32_t slots, int32_t dtype,
-                              const void* msg, int64_t region, void* workspace, int32_t flags, void* stream) {
+                              const void* msg, int64_t region, void* workspace, int32_t flags, const ft_tiled* prev,
+                              const int32_t* readers_ptr, const int32_t* readers_idx, void* stream) {
     ft::HaloParams h;
     if (!ft::fill_halo(h, dst, cols, n, slots, dtype, msg, workspace, flags)) return FT_ERR_ARG;
     if (region < 0 || region + (int64_t)n * slots > dst->capacity || region + (int64_t)n * slots > INT_MAX)
         return FT_ERR_SHAPE;
     h.region = region;
+    if (prev && readers_ptr && readers_idx) {
+        if (prev->n_cols != dst->n_cols) return FT_ERR_SHAPE;
+        h.prev = ft::hyb_in(prev);
+        h.rd_ptr = readers_ptr;
+        h.rd_idx = readers_idx;
+        h.stamp = ft::carve_workspace(workspace, dst->n_cols).stamp;
+    }
     if (n == 0) return FT_OK;
     cudaStream_t s = (cudaStream_t)stream;
     const int grid = (n + 255) / 256;

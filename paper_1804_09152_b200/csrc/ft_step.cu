@@ -253,7 +253,7 @@ __device__ __forceinline__ double recip_deg(int n) { return n - 1 <= 32 ? c_reci
 __device__ __forceinline__ void mark_ring(const StepParams& p, const int (&u)[kMD], int n, unsigned char nxt) {
 #pragma unroll
     for (int k = 0; k < kMD; ++k)
-        if (k < n) p.ws.stamp[u[k] - p.j_base] = nxt;
+        if (k < n) p.ws.stamp[u[k]] = nxt;
 }
 
 // warp-aggregated push of column j onto a list
@@ -286,16 +286,19 @@ __global__ void __launch_bounds__(kPrepTPB) prep_kernel(const StepParams p) {
         return;
     }
     const unsigned int pat = 0x01010101u * (unsigned char)vload(&ctl->seq);
-    // the CTA's 16384 columns as 1024 16-byte words; thread t reads words
-    // t, t + 256, t + 512, t + 768 (coalesced), 16 columns each
-    const int c0 = blockIdx.x * (kPrepTPB * kPrepCols);
+    // owned buffer columns [g_lo, g_hi), scanned from the 64-byte aligned
+    // column below g_lo; each CTA covers 16384 columns as 1024 16-byte
+    // words, thread t reading words t, t + 256, t + 512, t + 768
+    // (coalesced), 16 columns each
+    const int g_lo = p.j_base, g_hi = p.j_base + p.n_v;
+    const int c0 = (g_lo & ~63) + blockIdx.x * (kPrepTPB * kPrepCols);
     const uint4* s4 = reinterpret_cast<const uint4*>(p.ws.stamp + c0);   // padded to 64 bytes
     unsigned int m[4];
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
         const int jw = c0 + 16 * (threadIdx.x + v * kPrepTPB);
         m[v] = 0;
-        if (jw < p.n_v) {
+        if (jw < g_hi) {
             const uint4 x = s4[threadIdx.x + v * kPrepTPB];
             const unsigned int w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -304,8 +307,9 @@ __global__ void __launch_bounds__(kPrepTPB) prep_kernel(const StepParams p) {
                 const unsigned int e = __vcmpeq4(w[q], pat) & 0x01010101u;
                 m[v] |= ((e * 0x01020408u) >> 24) << (4 * q);
             }
-            const int lim = p.n_v - jw;
-            if (lim < 16) m[v] &= (1u << lim) - 1u;
+            const int hi = g_hi - jw, lo = g_lo - jw;       // keep columns in [g_lo, g_hi)
+            if (hi < 16) m[v] &= (1u << hi) - 1u;
+            if (lo > 0) m[v] &= lo >= 16 ? 0u : ~((1u << lo) - 1u);
         }
     }
     int tot;
@@ -321,7 +325,7 @@ __global__ void __launch_bounds__(kPrepTPB) prep_kernel(const StepParams p) {
         while (mm) {
             const int b = __ffs(mm) - 1;
             mm &= mm - 1;
-            p.ws.act[base++] = jw + b;
+            p.ws.act[base++] = jw + b - g_lo;
         }
     }
 }
@@ -975,7 +979,7 @@ __device__ __forceinline__ void deep_column(const StepParams& p, int j, bool ful
     }
     if (p.track && changed) {
         const int q0 = __ldg(&p.lap_ptr[jl]), q1 = __ldg(&p.lap_ptr[jl + 1]);
-        for (int q = q0; q < q1; ++q) p.ws.stamp[__ldg(&p.lap_idx[q]) - p.j_base] = nxt;
+        for (int q = q0; q < q1; ++q) p.ws.stamp[__ldg(&p.lap_idx[q])] = nxt;
     }
 }
 
@@ -1181,7 +1185,7 @@ __device__ __forceinline__ void staged_column(const StepParams& p, int j, WideSt
     }
     if (nf) atomicOr(&p.ws.ctl->nonfinite, 1u);
     if (p.track && changed)
-        for (int k = lane; k < n; k += 32) p.ws.stamp[(pu >= 0 ? pu : __ldg(&p.lap_idx[q0 + k])) - p.j_base] = nxt;
+        for (int k = lane; k < n; k += 32) p.ws.stamp[pu >= 0 ? pu : __ldg(&p.lap_idx[q0 + k])] = nxt;
     const double bm_old = lane == 0 ? base_of<T>(p.in, j) : 0.0;
     __syncwarp();
     bm_fold(lane == 0 ? bm_new : 0.0, bm_old, full, s_bm);
@@ -1766,7 +1770,7 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     if (rc != FT_OK) return rc;
     const long long step_cap = dom ? dom->step_capacity : out->capacity;
     if (step_cap < 0 || step_cap > out->capacity) return set_err(FT_ERR_ARG, "domain step capacity out of range");
-    if (ws_bytes < ft::workspace_bytes(n_own)) return set_err(FT_ERR_ARG, "workspace too small");
+    if (ws_bytes < ft::workspace_bytes(n_v)) return set_err(FT_ERR_ARG, "workspace too small");
     if (out_id != 0 && out_id != 1) return set_err(FT_ERR_ARG, "out_id must be 0 or 1");
     ft::StepParams p;
     p.n_v = n_own;
@@ -1781,9 +1785,9 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     p.cp.w = prm->w; p.cp.a = prm->a; p.cp.e = prm->e; p.cp.eb = prm->e_base; p.cp.mu = prm->mu; p.cp.dt = prm->dt;
     p.cp.finite = std::isfinite(p.cp.w) && std::isfinite(p.cp.a) && std::isfinite(p.cp.e) &&
                   std::isfinite(p.cp.eb) && std::isfinite(p.cp.mu) && std::isfinite(p.cp.dt);
-    p.ws = ft::carve_workspace(workspace, n_own);
+    p.ws = ft::carve_workspace(workspace, n_v);      // the buffer's columns (owned + halo in a domain)
     p.check_done = check_done;
-    p.track = (!dom && (lap_flags & FT_LAP_SYMMETRIC)) ? 1 : 0;
+    p.track = (lap_flags & FT_LAP_SYMMETRIC) ? 1 : 0;
     const bool uni = (lap_flags & FT_LAP_UNIFORM) != 0;
     const bool packed = uni && (lap_flags & FT_LAP_PACKED) != 0;
     p.lap_pack = packed ? (const int4*)lap_t->values : nullptr;
@@ -1793,7 +1797,8 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     DevState& d = dev_state();
     const char* kenv = getenv("FT_KERNELS");   // debug: bit mask of the column kernels to launch
     const int kmask = kenv ? atoi(kenv) : 15;
-    const int prep_grid = (n_own + ft::kPrepCols * ft::kPrepTPB - 1) / (ft::kPrepCols * ft::kPrepTPB);
+    const int prep_span = n_own + (j_base & 63);
+    const int prep_grid = (prep_span + ft::kPrepCols * ft::kPrepTPB - 1) / (ft::kPrepCols * ft::kPrepTPB);
     if (kmask & 1) launch_dep(ft::prep_kernel, prep_grid, ft::kPrepTPB, s, p);
     int bg = d.band_grid[dtype == FT_F32][uni][packed];
     const int need_b = (n_own + ft::kBandTPB - 1) / ft::kBandTPB;
@@ -1821,7 +1826,8 @@ static void launch_finalize(const ft::Workspace& ws, ft_step_stats* trace, long 
     ft::FinalizeParams f;
     f.ws = ws; f.trace = trace; f.tiled_cap = tiled_cap; f.fixed_slot = evolve ? 0 : 1;
     f.evolve = evolve;
-    f.track = (!domain && (lap_flags & FT_LAP_SYMMETRIC)) ? 1 : 0;
+    f.track = (lap_flags & FT_LAP_SYMMETRIC) ? 1 : 0;
+    (void)domain;
     f.out_id = out_id;
     f.next_cap = next_cap;
     launch_dep(ft::finalize_kernel, 1, 1, s, f);
@@ -2056,10 +2062,12 @@ extern "C" int ft_domain_step(const ft_csc* lap_rows, int32_t lap_flags, const f
                               size_t ws_bytes, ft_step_stats* record, void* stream) {
     if (!in || !dom || !record) return set_err(FT_ERR_ARG, "null argument");
     cudaStream_t s = (cudaStream_t)stream;
-    const int rc = launch_columns(lap_rows, lap_flags, in, out, 0, dtype, params, workspace, ws_bytes, 1, s, dom);
+    const int out_id = dom->out_id & 1;
+    const int rc = launch_columns(lap_rows, lap_flags, in, out, out_id, dtype, params, workspace, ws_bytes, 1, s,
+                                  dom);
     if (rc != FT_OK) return rc;
-    launch_finalize(ft::carve_workspace(workspace, dom->col_count), record, dom->step_capacity, 0, lap_flags, 0,
-                    in->capacity, true, s);
+    launch_finalize(ft::carve_workspace(workspace, in->n_cols), record, dom->step_capacity, 0, lap_flags, out_id,
+                    dom->step_capacity, true, s);
     return cuda_check("ft_domain_step");
 }
 

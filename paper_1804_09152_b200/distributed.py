@@ -129,8 +129,9 @@ class LocalProblem:
     ``values`` over them)."""
 
     def __init__(self, rank, partition, n_rows, lap_ptr, lap_idx, lap_val, lap_flags, cols,
-                 col_ptr, row_idx, values):
+                 col_ptr, row_idx, values, symmetric=False):
         self.rank = rank
+        self.symmetric = bool(symmetric)   # L^T pattern symmetric: active-set stepping
         self.partition = partition
         self.n_rows = int(n_rows)
         self.lap_ptr = np.ascontiguousarray(lap_ptr, dtype=INDEX)
@@ -146,7 +147,7 @@ class LocalProblem:
             raise ShapeError("L^T columns do not match the owned range")
 
 
-def _slice_problem(field_phi, mat_t, flags, partition, rank):
+def _slice_problem(field_phi, mat_t, flags, partition, rank, symmetric=False):
     b, e = partition.range(rank)
     cp = np.asarray(mat_t.col_ptr, dtype=np.int64)
     q0, q1 = int(cp[b]), int(cp[e])
@@ -162,7 +163,7 @@ def _slice_problem(field_phi, mat_t, flags, partition, rank):
     src = np.repeat(fcp[cols], cnt) + (np.arange(int(col_ptr[-1])) - np.repeat(col_ptr[:-1], cnt))
     return LocalProblem(rank, partition, field_phi.n_rows, lap_ptr, lap_idx, lap_val, flags, cols,
                         col_ptr, np.asarray(field_phi.row_idx)[src],
-                        np.asarray(field_phi.values, dtype=np.float64)[src])
+                        np.asarray(field_phi.values, dtype=np.float64)[src], symmetric=symmetric)
 
 
 def _laplacian_t(lap):
@@ -175,11 +176,12 @@ def _laplacian_t(lap):
 def local_problem(field_phi, lap, partition, rank, renumbering=None):
     """Slice a host field (SparseMat) and a Laplacian for one rank; with a
     :class:`Renumbering` the partition is over the renumbered vertices."""
+    sym = F._pattern_symmetric(lap)        # a renumbering keeps the pattern symmetric
     if renumbering is not None:
         return _slice_problem(renumbering.field(field_phi), renumbering.laplacian_t(lap),
-                              renumbering.lap_flags, partition, rank)
+                              renumbering.lap_flags, partition, rank, symmetric=sym)
     mat_t, flags = _laplacian_t(lap)
-    return _slice_problem(field_phi, mat_t, flags, partition, rank)
+    return _slice_problem(field_phi, mat_t, flags, partition, rank, symmetric=sym)
 
 
 # -- locality renumbering -------------------------------------------------------
@@ -311,7 +313,7 @@ def periodic_grid_problem(nx, ny, seeds, partition, rank):
     row_idx[dst] = sr
     vals[dst] = 1.0 / claims[sp]
     return LocalProblem(rank, partition, seeds.size + 1, lap_ptr, lap_idx, lap_val,
-                        _lib.FT_LAP_UNIFORM, cols, col_ptr, row_idx, vals)
+                        _lib.FT_LAP_UNIFORM, cols, col_ptr, row_idx, vals, symmetric=True)
 
 
 # ---------------------------------------------------------------------------
@@ -422,7 +424,7 @@ class LoopbackTransport:
 
     def gather_owned(self, ranks, steps_done):
         out = []
-        for r in sorted(ranks, key=lambda x: x.col_begin):
+        for r in sorted(ranks, key=lambda x: x.g_begin):
             h = r.owned_field(steps_done).to_host()
             cp = np.asarray(h.col_ptr, dtype=np.int64)
             out.append((np.diff(cp).astype(np.int32), np.asarray(h.row_idx[:cp[-1]]),
@@ -435,8 +437,13 @@ class LoopbackTransport:
 
 
 class DomainRank:
-    """Device state of one rank: owned L^T columns, two tiled buffers over
-    all columns (owned + halo valid), workspace, records, halo messages."""
+    """Device state of one rank.  Its columns are LOCAL: the sorted union of
+    the owned columns and the halo, numbered 0 .. n_loc-1 in global order,
+    so the owned ones are the range [col_begin, col_begin + n_own) and the
+    buffers scale with the rank's share of the field, not the whole field.
+    Holds the owned L^T columns (local row indices), two tiled buffers over
+    the local columns, the workspace, the statistics records and the halo
+    messages."""
 
     def __init__(self, problem, plan, precision="exact", slots=DEFAULT_SLOTS, device=None,
                  renumbering=None):
@@ -457,24 +464,31 @@ class DomainRank:
         self.vdtype = _value_dtype(precision)
         self.n_rows = problem.n_rows
         self.n_v = problem.partition.n_vertices
-        self.col_begin, e = problem.partition.range(problem.rank)
-        self.n_own = e - self.col_begin
-        lap = SparseMat(self.n_v, self.n_own, problem.lap_ptr, problem.lap_idx, problem.lap_val,
-                        check=False)
+        g_begin, g_end = problem.partition.range(problem.rank)
+        self.g_begin = g_begin
+        self.n_own = g_end - g_begin
+        self.cols = problem.cols                      # local column k = global column cols[k]
+        self.n_loc = int(self.cols.size)
+        local = lambda g: np.searchsorted(self.cols, np.asarray(g, dtype=np.int64)).astype(np.int32)
+        self.col_begin = int(local(g_begin))
+        lap_idx = local(problem.lap_idx)
+        lap = SparseMat(self.n_loc, self.n_own, problem.lap_ptr, lap_idx, problem.lap_val, check=False)
         self.lap = DeviceCSC.from_host(lap, self.vdtype, device)
         self.lap_c = self.lap.ft_csc()
         self.lap_flags = problem.lap_flags
-        # a renumbered partition reports NaN / pattern columns in the caller's ids
-        self.report_ids = None
+        if problem.symmetric and F.ACTIVE_SET:
+            self.lap_flags |= _lib.FT_LAP_SYMMETRIC
+        # NaN / pattern errors report global (caller) vertex ids
+        gids = np.arange(g_begin, g_end, dtype=np.int64)
         if renumbering is not None:
-            ids = renumbering.order[self.col_begin:self.col_begin + self.n_own].astype(np.int32)
-            self.report_ids = torch.from_numpy(ids).to(device)
+            gids = renumbering.order[gids]
+        self.report_ids = torch.from_numpy(gids.astype(np.int32)).to(device)
         self.pack = None
-        if self.lap_flags == _lib.FT_LAP_UNIFORM and F.PACK_LAPLACIAN:
+        if problem.lap_flags == _lib.FT_LAP_UNIFORM and F.PACK_LAPLACIAN:
             self.pack, _ = F.pack_laplacian(self.lap, col_base=self.col_begin)
             self.lap_c.values = self.pack.data_ptr()
             self.lap_flags |= _lib.FT_LAP_PACKED
-        self.ws = torch.zeros(int(self.lib.ft_workspace_bytes(self.n_own)), dtype=torch.int8,
+        self.ws = torch.zeros(int(self.lib.ft_workspace_bytes(self.n_loc)), dtype=torch.int8,
                               device=device)
         self.record = torch.zeros(_lib.STATS_BYTES, dtype=torch.uint8, device=device)
         self.gathered = torch.zeros(self.world * _lib.STATS_BYTES, dtype=torch.uint8, device=device)
@@ -487,16 +501,32 @@ class DomainRank:
         self.trace = None
         self.steps_done = 0            # steps completed by previous evolve calls
         self.step_events = None        # list: (start, end) CUDA events per ft_domain_step
-        # halo layout: peers ascending, columns of a peer consecutive
-        self.recv_cols = {q: torch.from_numpy(v).to(device) for q, v in plan.recv.items()}
-        self.send_cols = {q: torch.from_numpy(v).to(device) for q, v in plan.send.items()}
+        # halo layout (local columns): peers ascending, columns of a peer
+        # consecutive; per received column, the owned columns that read it
+        own_j = np.repeat(np.arange(self.n_own, dtype=np.int64) + self.col_begin,
+                          np.diff(np.asarray(problem.lap_ptr, dtype=np.int64)))
+        order = np.argsort(lap_idx, kind="stable")
+        rd_key, rd_val = lap_idx[order].astype(np.int64), own_j[order]
+        self.recv_cols, self.send_cols, self.readers = {}, {}, {}
+        for q, v in plan.recv.items():
+            lv = local(v)
+            lo = np.searchsorted(rd_key, lv, side="left")
+            hi = np.searchsorted(rd_key, lv, side="right")
+            ptr = np.concatenate([[0], np.cumsum(hi - lo)]).astype(np.int32)
+            idx = (np.concatenate([rd_val[a:b] for a, b in zip(lo, hi)]) if lv.size
+                   else np.zeros(0)).astype(np.int32)
+            self.recv_cols[q] = torch.from_numpy(lv).to(device)
+            self.readers[q] = (torch.from_numpy(ptr).to(device),
+                               torch.from_numpy(idx if idx.size else np.zeros(1, np.int32)).to(device))
+        for q, v in plan.send.items():
+            self.send_cols[q] = torch.from_numpy(local(v)).to(device)
         self.recv_off = {}
         off = 0
         for q in sorted(plan.recv):
             self.recv_off[q] = off
             off += plan.recv[q].size
         self.n_halo = off
-        own_mask = (problem.cols >= self.col_begin) & (problem.cols < e)
+        own_mask = (problem.cols >= g_begin) & (problem.cols < g_end)
         own_nnz = int(np.sum(np.diff(problem.col_ptr)[own_mask]))
         self.step_cap = max(
             int(own_nnz * POOL_FRACTION), POOL_MIN)
@@ -530,7 +560,7 @@ class DomainRank:
             if old is not None:
                 self.reallocs += 1
                 capacity = max(capacity, int(old.capacity * GROWTH))
-            buf = DeviceTiled(self.n_rows, self.n_v, capacity, self.vdtype, self.device)
+            buf = DeviceTiled(self.n_rows, self.n_loc, capacity, self.vdtype, self.device)
             if old is not None:
                 for name in ("sig", "aux", "v0", "v1"):
                     getattr(buf, name).copy_(getattr(old, name))
@@ -544,12 +574,11 @@ class DomainRank:
         sig, aux, v0, v1, pidx, pval = hybrid_columns(problem.col_ptr, problem.row_idx,
                                                       problem.values.astype(np.float64))
         buf = self._buffer(0, max(self._need_capacity(), pidx.size, 1))
-        cols = torch.from_numpy(problem.cols).to(self.device)
         dev = self.device
-        buf.sig[cols] = torch.from_numpy(sig).to(dev)
-        buf.aux[cols] = torch.from_numpy(aux).to(dev)
-        buf.v0[cols] = torch.from_numpy(v0).to(dev, self.vdtype)
-        buf.v1[cols] = torch.from_numpy(v1).to(dev, self.vdtype)
+        buf.sig.copy_(torch.from_numpy(sig).to(dev))          # the local columns, in order
+        buf.aux.copy_(torch.from_numpy(aux).to(dev))
+        buf.v0.copy_(torch.from_numpy(v0).to(dev, self.vdtype))
+        buf.v1.copy_(torch.from_numpy(v1).to(dev, self.vdtype))
         if pidx.size:
             buf.pool_idx[:pidx.size].copy_(torch.from_numpy(pidx).to(dev))
             buf.pool_val[:pidx.size].copy_(torch.from_numpy(pval).to(dev, self.vdtype))
@@ -582,8 +611,7 @@ class DomainRank:
         lib = self.lib
         in_t = self.meta[i % 2][0]
         out_t, step_cap, slots = self._as_output((i + 1) % 2)
-        dom = _lib.FtDomain(self.col_begin, self.n_own, step_cap,
-                            self.report_ids.data_ptr() if self.report_ids is not None else None)
+        dom = _lib.FtDomain(self.col_begin, self.n_own, step_cap, self.report_ids.data_ptr(), (i + 1) % 2, 0)
         wp, wn = ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel()
         rec = ctypes.c_void_p(self.record.data_ptr())
         if self.step_events is not None:
@@ -613,12 +641,18 @@ class DomainRank:
 
     def launch_unpack(self, i, stream, flags=0):
         out_t, step_cap, slots = self.meta[(i + 1) % 2]
+        prev = self.meta[i % 2][0]            # the step's input: the halo's previous values
+        track = bool(self.lap_flags & _lib.FT_LAP_SYMMETRIC)
         for q, cols in self.recv_cols.items():
+            rp, ri = self.readers[q]
             _check(self.lib.ft_halo_unpack(ctypes.byref(out_t), ctypes.c_void_p(cols.data_ptr()),
                                            cols.numel(), slots, self.ftd,
                                            ctypes.c_void_p(self.recv_msg[q].data_ptr()),
                                            step_cap + self.recv_off[q] * slots,
-                                           ctypes.c_void_p(self.ws.data_ptr()), flags, stream),
+                                           ctypes.c_void_p(self.ws.data_ptr()), flags,
+                                           ctypes.byref(prev) if track else None,
+                                           ctypes.c_void_p(rp.data_ptr()) if track else None,
+                                           ctypes.c_void_p(ri.data_ptr()) if track else None, stream),
                    "ft_halo_unpack")
 
     # -- control -------------------------------------------------------------
@@ -796,7 +830,7 @@ def evolve_partitioned(ranks, transport, params, max_steps=1000, tol=1e-4,
 def gather_field(ranks, steps_done=None, n_rows=None, renumbering=None):
     """Host SparseMat of the whole field from local ranks covering every
     owned range (loopback runs; a multi-process run gathers per rank)."""
-    parts = sorted(ranks, key=lambda r: r.col_begin)
+    parts = sorted(ranks, key=lambda r: r.g_begin)
     ptrs, idx, vals = [np.zeros(1, dtype=np.int64)], [], []
     base = 0
     for r in parts:
