@@ -411,6 +411,33 @@ int ft_lloyd_backproject(const double* positions, int32_t n_vertices, const int3
                          const int32_t* cell_ptr, const int32_t* cell_faces, const double* point,
                          const double* normal, int32_t* status, int32_t* hit_vertex, void* stream);
 
+/* Lloyd on a partitioned field: a rank's faces (ascending;
+ * faces / geometry arrays indexed by the rank's face list, vertex ids
+ * global) and the cells' face lists over them (ft_faces_by_cell on the
+ * rank's local field).
+ *   ft_lloyd_partials  per cell: face count, sum of areas, sum of area *
+ *                      barycenter (periodic: unwrapped around the seed), sum
+ *                      of area * normal -> sums[n_cells][8]; summed over the
+ *                      ranks by an all-reduce;
+ *   ft_lloyd_finish    point, unit normal and status (0 ok, 1 vanished, 2
+ *                      degenerate, 3 null normal) from the reduced sums;
+ *   ft_lloyd_backproject_keys  the back-projection over the rank's faces,
+ *                      plus the cross-rank key of its best hit: |t| (inf on
+ *                      a miss) and the global face id (face_ids[face]); the
+ *                      ranks all-reduce min |t|, then the min face id among
+ *                      the ties (np.argmin's first occurrence). */
+int ft_lloyd_partials(const double* positions, int32_t n_vertices, const int32_t* faces, int32_t n_faces,
+                      const double* face_area, const double* face_bary, const double* face_normal,
+                      const double* period, int32_t n_cells, const int32_t* cell_ptr,
+                      const int32_t* cell_faces, const int64_t* seeds, double* sums, void* stream);
+int ft_lloyd_finish(int32_t n_cells, const double* sums, double* point, double* normal, int32_t* status,
+                    void* stream);
+int ft_lloyd_backproject_keys(const double* positions, int32_t n_vertices, const int32_t* faces,
+                              int32_t n_faces, const double* period, int32_t n_cells,
+                              const int32_t* cell_ptr, const int32_t* cell_faces, const int32_t* face_ids,
+                              const double* point, const double* normal, int32_t* status,
+                              int32_t* hit_vertex, double* best_abs_t, int64_t* best_face, void* stream);
+
 /* -- dual-mesh adjacency products --------------------------------------- */
 /* One pass over vertices and faces of a (FT_F64) field collects, as keys in
  * four device hash sets (capacity: a power of two; empty slot = ~0):

@@ -104,7 +104,8 @@ EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
            "ft_halo_unpack", "ft_domain_combine", "ft_domain_control", "ft_laplacian_pack",
            "ft_point_triangle_distances", "ft_spgemm_count", "ft_spgemm_expand",
            "ft_segment_sums", "ft_skeleton", "ft_expand", "ft_normalize_columns",
-           "ft_clique_triangles", "ft_lloyd_backproject")
+           "ft_clique_triangles", "ft_lloyd_backproject", "ft_lloyd_partials", "ft_lloyd_finish",
+           "ft_lloyd_backproject_keys")
 
 _lib = None
 
@@ -186,6 +187,12 @@ def _declare(lib):
     lib.ft_clique_triangles.restype = ctypes.c_int
     lib.ft_lloyd_backproject.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp]
     lib.ft_lloyd_backproject.restype = ctypes.c_int
+    lib.ft_lloyd_partials.argtypes = [vp, i32, vp, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp]
+    lib.ft_lloyd_partials.restype = ctypes.c_int
+    lib.ft_lloyd_finish.argtypes = [i32, vp, vp, vp, vp, vp]
+    lib.ft_lloyd_finish.restype = ctypes.c_int
+    lib.ft_lloyd_backproject_keys.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    lib.ft_lloyd_backproject_keys.restype = ctypes.c_int
 
 
 def lib():

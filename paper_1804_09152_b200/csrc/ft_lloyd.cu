@@ -314,7 +314,9 @@ __global__ void centroid_kernel(Geo g, int n_cells, const int* cell_ptr, const i
 // -- back-projection (lloyd.py:67-112), one warp per cell ---------------------
 
 __global__ void backproject_kernel(Geo g, int n_cells, const int* cell_ptr, const int* cell_faces,
-                                   const double* point, const double* normal, int* status, int* hit_vertex) {
+                                   const double* point, const double* normal, int* status, int* hit_vertex,
+                                   double* best_abs_t = nullptr, long long* best_face = nullptr,
+                                   const int* face_ids = nullptr) {
     const int lane = threadIdx.x & 31;
     const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (c >= n_cells) return;
@@ -368,9 +370,18 @@ __global__ void backproject_kernel(Geo g, int n_cells, const int* cell_ptr, cons
         if (ot < best_t || (ot == best_t && oi < best_i)) { best_t = ot; best_i = oi; }
     }
     if (lane != 0) return;
-    if (best_i == INT_MAX) { hit_vertex[c] = -1; status[c] = FT_LLOYD_MISS; return; }
+    if (best_i == INT_MAX) {
+        hit_vertex[c] = -1;
+        status[c] = FT_LLOYD_MISS;
+        if (best_abs_t) { best_abs_t[c] = INFINITY; best_face[c] = LLONG_MAX; }
+        return;
+    }
     // recompute the winning face's geometry and t (same arithmetic)
     const int f = cell_faces[a + best_i];
+    if (best_abs_t) {   // the cross-rank key of a partitioned back-projection
+        best_abs_t[c] = best_t;
+        best_face[c] = face_ids ? face_ids[f] : f;
+    }
     const int vv[3] = {g.faces[3 * f], g.faces[3 * f + 1], g.faces[3 * f + 2]};
     double p0[3], e1[3], e2[3];
     for (int k = 0; k < 3; ++k) {
@@ -408,6 +419,61 @@ __global__ void backproject_kernel(Geo g, int n_cells, const int* cell_ptr, cons
         if (k == 0 || dd < bd) { bd = dd; nearest = k; }
     }
     hit_vertex[c] = vv[nearest];
+}
+
+// -- a partitioned field: per-rank partial sums of approx_centroid ---------
+// Per cell over the rank's faces (ascending): face count, sum of areas, sum
+// of area * barycenter (periodic: unwrapped around the cell's seed), sum of
+// area * normal -- 8 doubles per cell, summed over the ranks by an
+// all-reduce, then finished by lloyd_finish_kernel.
+
+__global__ void lloyd_partials_kernel(Geo g, int n_cells, const int* cell_ptr, const int* cell_faces,
+                                      const long long* seeds, double* out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_cells) return;
+    const int r = c + 1;
+    const int a = cell_ptr[r], m = cell_ptr[r + 1] - a;
+    double ref[3] = {0.0, 0.0, 0.0};
+    if (g.periodic) {
+        const long long sd = seeds[c];
+        for (int k = 0; k < 3; ++k) ref[k] = g.pos[3 * sd + k];
+    }
+    double tot = 0.0, ps[3] = {0.0, 0.0, 0.0}, ns[3] = {0.0, 0.0, 0.0};
+    for (int i = 0; i < m; ++i) {
+        const int f = cell_faces[a + i];
+        const double ar = g.area[f];
+        double b[3] = {g.bary[3 * f], g.bary[3 * f + 1], g.bary[3 * f + 2]};
+        if (g.periodic) {
+            double dlt[3] = {b[0] - ref[0], b[1] - ref[1], b[2] - ref[2]};
+            wrap(g, dlt);
+            for (int k = 0; k < 3; ++k) b[k] = ref[k] + dlt[k];
+        }
+        tot += ar;
+        for (int k = 0; k < 3; ++k) {
+            ps[k] += ar * b[k];
+            ns[k] += ar * g.fnorm[3 * f + k];
+        }
+    }
+    double* o = out + 8 * (size_t)c;
+    o[0] = (double)m; o[1] = tot;
+    for (int k = 0; k < 3; ++k) { o[2 + k] = ps[k]; o[5 + k] = ns[k]; }
+}
+
+__global__ void lloyd_finish_kernel(int n_cells, const double* sums, double* point, double* normal, int* status) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_cells) return;
+    const double* o = sums + 8 * (size_t)c;
+    if (o[0] == 0.0) { status[c] = FT_LLOYD_VANISHED; return; }
+    const double total = o[1];
+    if (!(total > 0.0)) { status[c] = FT_LLOYD_DEGENERATE; return; }
+    const double ns[3] = {o[5], o[6], o[7]};
+    const double nrm = norm3_blas(ns);
+    if (nrm <= 1e-12 * total) { status[c] = FT_LLOYD_NULLNORMAL; return; }
+    for (int k = 0; k < 3; ++k) {
+        point[3 * c + k] = o[2 + k] / total;
+        normal[3 * c + k] = ns[k] / nrm;
+    }
+    status[c] = FT_LLOYD_OK;
 }
 
 }  // namespace ft
@@ -519,4 +585,46 @@ extern "C" int ft_lloyd_backproject(const double* positions, int32_t n_vertices,
         ft::backproject_kernel<<<(n_cells * 32 + 255) / 256, 256, 0, s>>>(g, n_cells, cell_ptr, cell_faces,
                                                                            point, normal, status, hit_vertex);
     return lcheck("ft_lloyd_backproject");
+}
+
+extern "C" int ft_lloyd_partials(const double* positions, int32_t n_vertices, const int32_t* faces, int32_t n_faces,
+                                 const double* face_area, const double* face_bary, const double* face_normal,
+                                 const double* period, int32_t n_cells, const int32_t* cell_ptr,
+                                 const int32_t* cell_faces, const int64_t* seeds, double* sums, void* stream) {
+    if (!positions || !faces || !cell_ptr || !cell_faces || !sums) return FT_ERR_ARG;
+    ft::Geo g;
+    if (fill_geo(g, positions, n_vertices, faces, n_faces, face_area, face_bary, face_normal, period) != FT_OK)
+        return FT_ERR_ARG;
+    if (n_cells > 0)
+        ft::lloyd_partials_kernel<<<(n_cells + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
+            g, n_cells, cell_ptr, cell_faces, (const long long*)seeds, sums);
+    return lcheck("ft_lloyd_partials");
+}
+
+extern "C" int ft_lloyd_finish(int32_t n_cells, const double* sums, double* point, double* normal, int32_t* status,
+                               void* stream) {
+    if (!sums || !point || !normal || !status) return FT_ERR_ARG;
+    if (n_cells > 0)
+        ft::lloyd_finish_kernel<<<(n_cells + 127) / 128, 128, 0, (cudaStream_t)stream>>>(n_cells, sums, point,
+                                                                                         normal, status);
+    return lcheck("ft_lloyd_finish");
+}
+
+extern "C" int ft_lloyd_backproject_keys(const double* positions, int32_t n_vertices, const int32_t* faces,
+                                         int32_t n_faces, const double* period, int32_t n_cells,
+                                         const int32_t* cell_ptr, const int32_t* cell_faces, const int32_t* face_ids,
+                                         const double* point, const double* normal, int32_t* status,
+                                         int32_t* hit_vertex, double* best_abs_t, int64_t* best_face,
+                                         void* stream) {
+    if (!positions || !faces || !cell_ptr || !cell_faces || !point || !normal || !status || !hit_vertex ||
+        !best_abs_t || !best_face)
+        return FT_ERR_ARG;
+    ft::Geo g;
+    if (fill_geo(g, positions, n_vertices, faces, n_faces, nullptr, nullptr, nullptr, period) != FT_OK)
+        return FT_ERR_ARG;
+    if (n_cells > 0)
+        ft::backproject_kernel<<<(n_cells * 32 + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+            g, n_cells, cell_ptr, cell_faces, point, normal, status, hit_vertex, best_abs_t,
+            (long long*)best_face, face_ids);
+    return lcheck("ft_lloyd_backproject_keys");
 }

@@ -359,6 +359,23 @@ class TorchTransport:
             for req in d.batch_isend_irecv(ops):
                 req.wait()
 
+    def all_reduce(self, tensors, op):
+        """In-place all-reduce ("sum" / "min" / "max") of this rank's tensor."""
+        (t,) = tensors
+        ops = {"sum": self.dist.ReduceOp.SUM, "min": self.dist.ReduceOp.MIN, "max": self.dist.ReduceOp.MAX}
+        if self.nccl or t.device.type == "cpu":
+            self.dist.all_reduce(t, op=ops[op], group=self.group)
+        else:
+            h = t.cpu()
+            self.dist.all_reduce(h, op=ops[op], group=self.group)
+            t.copy_(h)
+
+    def gather_objects(self, objs):
+        (o,) = objs
+        out = [None] * self.world
+        self.dist.all_gather_object(out, o, group=self.group)
+        return out
+
     def max_int(self, values):
         torch = _torch()
         (v,) = values
@@ -421,6 +438,18 @@ class LoopbackTransport:
 
     def max_int(self, values):
         return max(int(v) for v in values)
+
+    def all_reduce(self, tensors, op):
+        torch = _torch()
+        red = {"sum": lambda a, b: a + b, "min": torch.minimum, "max": torch.maximum}[op]
+        acc = tensors[0].clone()
+        for t in tensors[1:]:
+            acc = red(acc, t)
+        for t in tensors:
+            t.copy_(acc)
+
+    def gather_objects(self, objs):
+        return list(objs)
 
     def gather_owned(self, ranks, steps_done):
         out = []
@@ -724,6 +753,78 @@ class DomainRank:
         return out
 
 
+    def pack_final(self, steps_done, stream):
+        """Pack the owned columns the peers read from the field after
+        ``steps_done`` steps (forced: the last step's own pack ran before the
+        stop flag, but its unpack was a no-op)."""
+        buf_t, _cap, slots = self.meta[steps_done % 2]
+        scratch = _torch().zeros(_lib.STATS_BYTES, dtype=_torch().uint8, device=self.device)
+        self._scratch_rec = scratch
+        for q, cols in self.send_cols.items():
+            _check(self.lib.ft_halo_pack(ctypes.byref(buf_t), ctypes.c_void_p(cols.data_ptr()), cols.numel(),
+                                         slots, self.ftd, ctypes.c_void_p(self.send_msg[q].data_ptr()),
+                                         ctypes.c_void_p(scratch.data_ptr()), ctypes.c_void_p(self.need.data_ptr()),
+                                         ctypes.c_void_p(self.ws.data_ptr()), _lib.FT_HALO_FORCE, stream),
+                   "ft_halo_pack")
+
+    def unpack_final(self, steps_done, stream):
+        """The peers' owned columns -> the halo of the field after
+        ``steps_done`` steps (forced, no activity stamps)."""
+        buf_t, cap, slots = self.meta[steps_done % 2]
+        for q, cols in self.recv_cols.items():
+            _check(self.lib.ft_halo_unpack(ctypes.byref(buf_t), ctypes.c_void_p(cols.data_ptr()), cols.numel(),
+                                           slots, self.ftd, ctypes.c_void_p(self.recv_msg[q].data_ptr()),
+                                           cap + self.recv_off[q] * slots, ctypes.c_void_p(self.ws.data_ptr()),
+                                           _lib.FT_HALO_FORCE, None, None, None, stream), "ft_halo_unpack")
+
+    def local_field(self, steps_done):
+        """All local columns (owned + halo) after ``steps_done`` steps as a
+        float64 DeviceCSC (n_rows x n_loc) -- the input of the partitioned
+        Lloyd step, whose faces reach one ring beyond the owned range."""
+        torch = _torch()
+        buf = self.bufs[steps_done % 2]
+        src = buf.ft_tiled()
+        sg = buf.sig
+        counts = torch.where(sg >= (1 << 30), 2, torch.where(sg >= 0, 1, torch.where(sg == -1, 0, -sg)))
+        cap = max(1, int(counts.sum().item()))
+        out = DeviceCSC.allocate(self.n_rows, self.n_loc, cap, self.vdtype, self.device)
+        o_c = out.ft_csc()
+        rec = torch.zeros(_lib.STATS_BYTES, dtype=torch.uint8, device=self.device)
+        _check(self.lib.ft_compact(ctypes.byref(src), ctypes.byref(o_c), self.ftd,
+                                   ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel(),
+                                   ctypes.c_void_p(rec.data_ptr()), _stream_handle()), "ft_compact")
+        r = _stats_from_bytes(rec.cpu().numpy().tobytes())[0]
+        if int(r["status"]) != _lib.FT_STATUS_OK:
+            raise BackendError("compaction of the local columns failed")
+        out.nnz = int(r["nnz_phi"])
+        if out.values.dtype != torch.float64:
+            out.values = out.values.double()
+        return out
+
+    def lloyd_faces(self, mesh, renumbering=None):
+        """The rank's faces for the partitioned Lloyd step (cached per mesh):
+        those whose first vertex the rank owns, ascending.  Returns
+        (faces in local column ids, faces in mesh vertex ids, global face
+        ids, area, barycenter, normal) as device arrays."""
+        torch = _torch()
+        key = id(mesh)
+        if getattr(self, "_lloyd_faces", None) is not None and self._lloyd_faces[0] == key:
+            return self._lloyd_faces[1]
+        f = np.asarray(mesh.faces, dtype=np.int64)
+        fn = renumbering.inverse[f] if renumbering is not None else f       # partition numbering
+        own = (fn[:, 0] >= self.g_begin) & (fn[:, 0] < self.g_begin + self.n_own)
+        ids = np.flatnonzero(own)
+        loc = np.searchsorted(self.cols, fn[ids])
+        if ids.size and not np.all(self.cols[np.minimum(loc, self.cols.size - 1)] == fn[ids]):
+            raise BackendError("a face reaches beyond the rank's one-ring halo")
+        up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(self.device)
+        faces = (up(loc if ids.size else np.zeros((1, 3)), np.int32), up(f[ids] if ids.size else np.zeros((1, 3)), np.int32),
+                 up(ids if ids.size else np.zeros(1), np.int32), up(mesh.face_area[ids], np.float64),
+                 up(mesh.face_barycenter[ids], np.float64), up(mesh.face_normal[ids], np.float64),
+                 int(ids.size))
+        self._lloyd_faces = (key, faces)
+        return faces
+
     def owned_labels(self, steps_done=None, field=None):
         """Argmax cell labels of the owned vertices (ft_labels, field.py:
         324-356) as a device int64 tensor."""
@@ -868,21 +969,193 @@ def gathered_field(ranks, transport, seeds, renumbering=None, precision="exact")
     return LayeredField(phi, seeds, steps, precision=precision)
 
 
+class PartitionedField:
+    """A field that stays on the ranks between Lloyd iterations (the
+    all-reduce exchange never assembles it): the LayeredField attributes a
+    caller reads, and :meth:`gather` for the whole field on demand."""
+
+    def __init__(self, ranks, transport, seeds, n_rows, steps, renumbering=None, precision="exact"):
+        self.ranks = ranks
+        self.transport = transport
+        self.seed_vertices = np.asarray(seeds, dtype=np.int64)
+        self.n_cells = n_rows - 1
+        self.step_count = steps
+        self.renumbering = renumbering
+        self.precision = precision
+
+    def gather(self):
+        return gathered_field(self.ranks, self.transport, self.seed_vertices, self.renumbering, self.precision)
+
+
+def refresh_halo(ranks, transport):
+    """Bring every rank's halo up to date with its peers' final owned
+    columns (the evolve loop skips the last step's unpack once it stops)."""
+    stream = _stream_handle()
+    for r in ranks:
+        r.pack_final(r.steps_done, stream)
+    transport.exchange(ranks)
+    for r in ranks:
+        r.unpack_final(r.steps_done, stream)
+
+
+def _row_sums(dcsc, col_weight):
+    """Per row: the sum over the row's entries of value * col_weight[column],
+    in column order (deterministic: stable sort by row, sequential runs)."""
+    torch = _torch()
+    nnz = dcsc.nnz
+    n_rows = dcsc.n_rows
+    out = torch.zeros(n_rows, dtype=torch.float64, device=dcsc.values.device)
+    if nnz == 0:
+        return out
+    cols = torch.repeat_interleave(torch.arange(dcsc.n_cols, device=out.device),
+                                   (dcsc.col_ptr[1:] - dcsc.col_ptr[:-1]).long())
+    rows = dcsc.row_idx[:nnz].long()
+    prod = dcsc.values[:nnz].double() * col_weight[cols]
+    rs, perm = torch.sort(rows, stable=True)
+    pv = prod[perm].contiguous()
+    head = torch.ones(nnz, dtype=torch.bool, device=out.device)
+    head[1:] = rs[1:] != rs[:-1]
+    starts = torch.nonzero(head).flatten()
+    sums = torch.empty(starts.numel(), dtype=torch.float64, device=out.device)
+    _check(_lib.lib().ft_segment_sums(ctypes.c_void_p(pv.data_ptr()), nnz, ctypes.c_void_p(starts.data_ptr()),
+                                      starts.numel(), ctypes.c_void_p(sums.data_ptr()), _stream_handle()),
+           "ft_segment_sums")
+    out[rs[starts]] = sums
+    return out
+
+
+def _cell_areas_partitioned(ranks, transport, mesh, renumbering):
+    """Field-weighted cell areas (lloyd.py:115-125) as per-rank partial sums
+    over the owned vertices, all-reduced."""
+    torch = _torch()
+    parts = []
+    for r in ranks:
+        f = r.owned_field(r.steps_done)
+        gids = np.arange(r.g_begin, r.g_begin + r.n_own)
+        vid = renumbering.order[gids] if renumbering is not None else gids
+        w = torch.from_numpy(np.asarray(mesh.vertex_area, dtype=np.float64)[vid]).to(r.device)
+        parts.append(_row_sums(f, w))
+    transport.all_reduce(parts, "sum")
+    return parts[0].cpu().numpy()[1:]
+
+
+def _reseed_allreduce(state, mesh, ranks, transport, renumbering):
+    """The Lloyd reseed (lloyd.py:155-195) on a partitioned field: every rank
+    sums approx_centroid's terms over its faces, the sums are all-reduced
+    (8 doubles per cell), each rank back-projects through its faces and the
+    best hit is chosen by all-reduces of (|t|, face id) -- smallest |t|,
+    then the lowest face id, np.argmin's first occurrence.  The collision
+    pass then runs replicated.  The centroid sums are taken in a different
+    order than numpy's pairwise sums, so a point can differ from the
+    single-GPU one in the last bits (the exact path is exchange="gather")."""
+    torch = _torch()
+    from . import lloyd as LL
+    n = int(state.field.n_cells)
+    old = np.asarray(state.seeds, dtype=np.int64)
+    refresh_halo(ranks, transport)
+    vp = ctypes.c_void_p
+    lib = _lib.lib()
+    st = _stream_handle()
+    per = []
+    for r in ranks:
+        dm = LL.device_mesh(mesh)
+        floc, fmesh, fid, area, bary, fnorm, nf = r.lloyd_faces(mesh, renumbering)
+        lf = r.local_field(r.steps_done)
+        cell_ptr, cell_faces, _ = LL.faces_by_cell_arrays(lf, floc, nf, 1, False)
+        seeds_d = torch.from_numpy(old).to(r.device)
+        sums = torch.zeros(max(n, 1) * 8, dtype=torch.float64, device=r.device)
+        period = ctypes.cast(dm.period, ctypes.c_void_p) if dm.period is not None else None
+        _check(lib.ft_lloyd_partials(vp(dm.positions.data_ptr()), dm.n_vertices, vp(fmesh.data_ptr()), nf,
+                                     vp(area.data_ptr()), vp(bary.data_ptr()), vp(fnorm.data_ptr()), period, n,
+                                     vp(cell_ptr.data_ptr()), vp(cell_faces.data_ptr()), vp(seeds_d.data_ptr()),
+                                     vp(sums.data_ptr()), st), "ft_lloyd_partials")
+        per.append((r, dm, fmesh, fid, nf, cell_ptr, cell_faces, sums, period))
+    transport.all_reduce([x[7] for x in per], "sum")
+    keys_t, keys_f, hits, statuses = [], [], [], []
+    for r, dm, fmesh, fid, nf, cell_ptr, cell_faces, sums, period in per:
+        point = torch.zeros(max(n, 1) * 3, dtype=torch.float64, device=r.device)
+        normal = torch.zeros_like(point)
+        status = torch.zeros(max(n, 1), dtype=torch.int32, device=r.device)
+        _check(lib.ft_lloyd_finish(n, vp(sums.data_ptr()), vp(point.data_ptr()), vp(normal.data_ptr()),
+                                   vp(status.data_ptr()), st), "ft_lloyd_finish")
+        local = status.clone()
+        hit = torch.full((max(n, 1),), -1, dtype=torch.int32, device=r.device)
+        bt = torch.full((max(n, 1),), float("inf"), dtype=torch.float64, device=r.device)
+        bf = torch.full((max(n, 1),), np.iinfo(np.int64).max, dtype=torch.int64, device=r.device)
+        _check(lib.ft_lloyd_backproject_keys(vp(dm.positions.data_ptr()), dm.n_vertices, vp(fmesh.data_ptr()), nf,
+                                             period, n, vp(cell_ptr.data_ptr()), vp(cell_faces.data_ptr()),
+                                             vp(fid.data_ptr()), vp(point.data_ptr()), vp(normal.data_ptr()),
+                                             vp(local.data_ptr()), vp(hit.data_ptr()), vp(bt.data_ptr()),
+                                             vp(bf.data_ptr()), st), "ft_lloyd_backproject_keys")
+        keys_t.append(bt)
+        keys_f.append(bf)
+        hits.append(hit)
+        statuses.append(status)
+    best_t = [t.clone() for t in keys_t]
+    transport.all_reduce(best_t, "min")
+    cand = [torch.where(t == b, f, torch.full_like(f, np.iinfo(np.int64).max))
+            for t, b, f in zip(keys_t, best_t, keys_f)]
+    transport.all_reduce(cand, "min")
+    mine = [torch.where((f == c) & torch.isfinite(t), h.long(), torch.full_like(f, -1))
+            for f, c, t, h in zip(keys_f, cand, keys_t, hits)]
+    transport.all_reduce(mine, "max")
+    status = statuses[0][:n].cpu().numpy()
+    hit = mine[0][:n].cpu().numpy()
+    fail = (status != LL.LLOYD_OK) | (hit < 0)
+    candidates = np.where(fail, old, hit)
+
+    def members(c):
+        """The vertices of cell c (any stored phi), ascending, from every rank."""
+        mine_v = []
+        for r in ranks:
+            f = r.owned_field(r.steps_done)
+            cols = torch.repeat_interleave(torch.arange(r.n_own, device=r.device),
+                                           (f.col_ptr[1:] - f.col_ptr[:-1]).long())
+            sel = cols[f.row_idx[:f.nnz].long() == c + 1].cpu().numpy() + r.g_begin
+            mine_v.append(renumbering.order[sel] if renumbering is not None else sel)
+        allv = transport.gather_objects(mine_v)
+        return np.sort(np.concatenate([np.asarray(v, dtype=np.int64) for v in allv]))
+
+    taken, collisions = set(), 0
+    seeds = np.empty(n, dtype=np.int64)
+    for c in range(n):
+        pick = int(candidates[c])
+        if pick in taken:
+            collisions += 1
+            pick = int(old[c])
+        if pick in taken:
+            free = [int(v) for v in members(c) if int(v) not in taken]
+            if not free:
+                from .errors import VanishedCellError
+                raise VanishedCellError(f"vanished-cell: no free vertex left for cell {c}")
+            pick = free[0]
+        taken.add(pick)
+        seeds[c] = pick
+    return seeds, {"reseed_misses": int(fail.sum()), "seed_collisions": collisions}
+
+
 def lloyd_iterate_partitioned(state, mesh, lap, params, n_iter, transport, partition, local_ranks,
-                              max_steps=1000, tol=1e-4, precision="exact", renumbering=None, device=None):
+                              max_steps=1000, tol=1e-4, precision="exact", renumbering=None, device=None,
+                              exchange="allreduce"):
     """:func:`lloyd.lloyd_iterate` (lloyd.py:198-229) with every evolve
-    partitioned over the ranks (vertex row partition, NCCL halo exchange)
-    and the reseed replicated on every rank: the owned fields are
-    all-gathered, then the single-GPU centroid / back-projection
-    kernels and the order-dependent collision pass run on the whole field,
-    identically everywhere.  The seeds and the history equal
-    ``lloyd_iterate``'s (the partitioned evolve is bitwise the single-GPU
-    one); ``local_ranks`` are the rank ids this process drives (one for a
-    TorchTransport, all for a LoopbackTransport)."""
+    partitioned over the ranks (vertex row partition, NCCL halo exchange).
+    ``local_ranks`` are the rank ids this process drives (one for a
+    TorchTransport, all for a LoopbackTransport).
+
+    ``exchange="allreduce"``: the field stays distributed; the
+    reseed all-reduces the per-cell centroid sums and the best-hit keys and
+    the cell areas of the history are all-reduced partial sums (a few KB per
+    cell set per iteration); ``state.field`` is a :class:`PartitionedField`.
+    ``exchange="gather"``: the owned fields are all-gathered and the
+    single-GPU kernels reseed the whole field on every rank -- bitwise the
+    seeds and history of ``lloyd_iterate``, at the cost of moving the field."""
     from . import lloyd as LL
     from .field import LayeredField, init_field
     if n_iter < 1:
         raise ShapeError("n_iter must be >= 1")
+    if exchange not in ("allreduce", "gather"):
+        raise ShapeError("exchange must be 'allreduce' or 'gather'")
+    fresh = state.field is None or state.field.step_count == 0
 
     def run_evolve(seeds, fld=None):
         fld = fld if fld is not None else init_field(mesh, seeds, precision=precision)
@@ -891,20 +1164,40 @@ def lloyd_iterate_partitioned(state, mesh, lap, params, n_iter, transport, parti
         ranks = [DomainRank(pr, pl, precision=precision, device=device, renumbering=renumbering)
                  for pr, pl in zip(problems, plans)]
         steps, trace = evolve_partitioned(ranks, transport, params, max_steps=max_steps, tol=tol)
-        parts = transport.gather_owned(ranks, steps)
-        phi = assemble_owned(parts, fld.phi.n_rows, mesh.n_vertices, renumbering)
-        return LayeredField(phi, seeds, steps, precision=precision), trace
+        if exchange == "gather":
+            parts = transport.gather_owned(ranks, steps)
+            phi = assemble_owned(parts, fld.phi.n_rows, mesh.n_vertices, renumbering)
+            return LayeredField(phi, seeds, steps, precision=precision), trace, None
+        return PartitionedField(ranks, transport, seeds, fld.phi.n_rows, steps, renumbering, precision), trace, ranks
 
-    if state.field is None or state.field.step_count == 0:
-        state.field, trace = run_evolve(np.asarray(state.seeds), state.field)
-    else:
-        trace = []
+    def record(trace, report, ranks):
+        if exchange == "gather":
+            return LL._history_entry(state, mesh, trace, report)
+        areas = _cell_areas_partitioned(ranks, transport, mesh, renumbering)
+        seeds = np.asarray(state.seeds, dtype=np.int64)
+        rec = dict(iteration=state.iteration, seeds=seeds.tolist(),
+                   seed_positions=mesh.positions[seeds].tolist(), cell_areas=areas.tolist(),
+                   area_variance=float(np.var(areas)), steps=len(trace),
+                   converged=bool(trace[-1].converged) if len(trace) else True)
+        rec.update(report)
+        return rec
+
+    ranks = None
+    trace = []
+    if fresh:
+        start = state.field if state.field is not None else None
+        state.field, trace, ranks = run_evolve(np.asarray(state.seeds), start)
+    elif exchange == "allreduce":
+        raise ShapeError("the all-reduce exchange starts from an unstepped state")
     if not state.history:
-        state.history.append(LL._history_entry(state, mesh, trace, {"reseed_misses": 0, "seed_collisions": 0}))
+        state.history.append(record(trace, {"reseed_misses": 0, "seed_collisions": 0}, ranks))
     for _ in range(n_iter):
-        seeds, report = LL._reseed(state, mesh)
+        if exchange == "gather":
+            seeds, report = LL._reseed(state, mesh)
+        else:
+            seeds, report = _reseed_allreduce(state, mesh, ranks, transport, renumbering)
         state.seeds = seeds
         state.iteration += 1
-        state.field, trace = run_evolve(seeds)
-        state.history.append(LL._history_entry(state, mesh, trace, report))
+        state.field, trace, ranks = run_evolve(seeds)
+        state.history.append(record(trace, report, ranks))
     return state

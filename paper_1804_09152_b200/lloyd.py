@@ -84,9 +84,15 @@ def _phi_f64(field):
 
 def _faces_by_cell_device(field, mesh, min_row, with_values):
     """(cell_ptr, cell_faces, values|None) as device tensors."""
-    torch = _torch()
-    dphi = _phi_f64(field)
     dm = device_mesh(mesh)
+    return faces_by_cell_arrays(_phi_f64(field), dm.faces, dm.n_faces, min_row, with_values)
+
+
+def faces_by_cell_arrays(dphi, faces, n_faces, min_row, with_values):
+    """ft_faces_by_cell on a device CSC field (float64) and a device face
+    list (int32 [n_faces][3], vertex ids = the field's columns):
+    (cell_ptr, cell_faces, values|None), faces ascending per row."""
+    torch = _torch()
     dev = dphi.values.device
     n_rows = dphi.n_rows
     cell_ptr = torch.zeros(n_rows + 1, dtype=torch.int32, device=dev)
@@ -96,14 +102,14 @@ def _faces_by_cell_device(field, mesh, min_row, with_values):
     lib = _lib.lib()
     stream = _stream_handle()
     vp = ctypes.c_void_p
-    rc = lib.ft_faces_by_cell(ctypes.byref(c), int(min_row), dm.n_faces, vp(dm.faces.data_ptr()),
+    rc = lib.ft_faces_by_cell(ctypes.byref(c), int(min_row), int(n_faces), vp(faces.data_ptr()),
                               vp(cell_ptr.data_ptr()), None, None, vp(scratch.data_ptr()),
                               vp(big.data_ptr()), stream)
     _check(rc, "ft_faces_by_cell")
     total = int(cell_ptr[n_rows].item())
     cell_faces = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
     values = torch.empty(max(total, 1), dtype=torch.float64, device=dev) if with_values else None
-    rc = lib.ft_faces_by_cell(ctypes.byref(c), int(min_row), dm.n_faces, vp(dm.faces.data_ptr()),
+    rc = lib.ft_faces_by_cell(ctypes.byref(c), int(min_row), int(n_faces), vp(faces.data_ptr()),
                               vp(cell_ptr.data_ptr()), vp(cell_faces.data_ptr()),
                               vp(values.data_ptr()) if values is not None else None,
                               vp(scratch.data_ptr()), vp(big.data_ptr()), stream)

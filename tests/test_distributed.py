@@ -206,6 +206,18 @@ def _gloo_worker(rank, world, port, n_steps, out_q):
         assert np.array_equal(np.asarray(whole.row_idx[:whole.nnz]), np.asarray(ref.row_idx[:ref.nnz]))
         assert np.array_equal(np.asarray(whole.values[:whole.nnz]), np.asarray(ref.values[:ref.nnz]))
         assert tr.max_int([rank + 5]) == world + 4
+        # the partitioned Lloyd step's reductions: per-cell sums, min keys,
+        # max hit vertex, and the object gather of the collision fallback
+        t = torch.arange(6, dtype=torch.float64) * (rank + 1)
+        tr.all_reduce([t], "sum")
+        assert t.tolist() == [float(k * sum(range(1, world + 1))) for k in range(6)]
+        m = torch.tensor([rank, -rank], dtype=torch.int64)
+        tr.all_reduce([m], "min")
+        assert m.tolist() == [0, -(world - 1)]
+        x = torch.tensor([float(rank)], dtype=torch.float64)
+        tr.all_reduce([x], "max")
+        assert x.tolist() == [float(world - 1)]
+        assert tr.gather_objects([np.array([rank])])[world - 1].tolist() == [world - 1]
         out_q.put((rank, "ok"))
     except Exception as exc:                    # pragma: no cover - reported to the parent
         out_q.put((rank, repr(exc)))
@@ -400,8 +412,8 @@ def test_loopback_morton_renumbered_matches_single_gpu():
 @pytest.mark.parametrize("world,morton", [(2, False), (3, True)])
 def test_partitioned_lloyd_matches_single_gpu(world, morton):
     """Lloyd relaxation with every evolve partitioned (loopback ranks) and
-    the reseed replicated on the all-gathered field: seeds and history equal
-    the single-GPU lloyd_iterate."""
+    the reseed replicated on the all-gathered field (exchange="gather"):
+    seeds and history equal the single-GPU lloyd_iterate bitwise."""
     mesh = ft.gen_icosphere(4)
     lap = ft.build_laplacian(mesh)
     seeds = ft.sample_seed_vertices(mesh, 48, 5)
@@ -411,7 +423,7 @@ def test_partitioned_lloyd_matches_single_gpu(world, morton):
     part = D.Partition.even(mesh.n_vertices, world)
     got = D.lloyd_iterate_partitioned(ft.LloydState(seeds=np.array(seeds)), mesh, lap, ft.CouplingParams(),
                                       2, D.LoopbackTransport(), part, list(range(world)),
-                                      max_steps=60, tol=1e-4, renumbering=ren)
+                                      max_steps=60, tol=1e-4, renumbering=ren, exchange="gather")
     assert np.array_equal(np.asarray(got.seeds), np.asarray(ref.seeds))
     assert len(got.history) == len(ref.history)
     for a, b in zip(got.history, ref.history):
@@ -421,3 +433,35 @@ def test_partitioned_lloyd_matches_single_gpu(world, morton):
     assert np.array_equal(np.asarray(a.col_ptr), np.asarray(b.col_ptr))
     assert np.array_equal(np.asarray(a.row_idx[:a.nnz]), np.asarray(b.row_idx[:b.nnz]))
     assert np.array_equal(np.asarray(a.values[:a.nnz]), np.asarray(b.values[:b.nnz]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,morton,torus", [(2, False, False), (3, True, False), (2, False, True)])
+def test_partitioned_lloyd_allreduce(world, morton, torus):
+    """The all-reduce exchange: the field never leaves the
+    ranks; per-cell centroid sums and best-hit keys are all-reduced.  The
+    sums are taken in a different order than the single GPU's, so the test
+    asks for the same seeds (they are vertex ids: a last-bit difference only
+    matters at an exact tie) and cell areas within 1e-12."""
+    if torus:
+        mesh = ft.gen_periodic_grid(64, 64)
+        seeds = ft.sample_seed_vertices(mesh, 24, 3)
+    else:
+        mesh = ft.gen_icosphere(4)
+        seeds = ft.sample_seed_vertices(mesh, 40, 6)
+    lap = ft.build_laplacian(mesh)
+    ref = ft.lloyd_iterate(ft.LloydState(seeds=np.array(seeds)), mesh, lap, ft.CouplingParams(),
+                           n_iter=2, max_steps=60, tol=1e-4)
+    ren = D.Renumbering.morton(mesh) if morton else None
+    part = D.Partition.even(mesh.n_vertices, world)
+    got = D.lloyd_iterate_partitioned(ft.LloydState(seeds=np.array(seeds)), mesh, lap, ft.CouplingParams(),
+                                      2, D.LoopbackTransport(), part, list(range(world)),
+                                      max_steps=60, tol=1e-4, renumbering=ren, exchange="allreduce")
+    assert np.array_equal(np.asarray(got.seeds), np.asarray(ref.seeds))
+    assert isinstance(got.field, D.PartitionedField)
+    for a, b in zip(got.history, ref.history):
+        for key in ("iteration", "seeds", "steps", "reseed_misses", "seed_collisions"):
+            assert a[key] == b[key], key
+        assert np.allclose(a["cell_areas"], b["cell_areas"], rtol=1e-12, atol=0)
+    whole = got.field.gather().phi
+    _assert_same_field(whole, ref.field.phi)
