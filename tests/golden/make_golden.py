@@ -28,6 +28,8 @@ analysis.npz     analysis.py metrics: voronoi labels / margin masks (torus,
                  histogram, directed surface distances and hausdorff.
 --big: c2_traj.npz (icosphere-7, 1024 seeds, steps 0/100/1000) and
        c2_lloyd.json (5 Lloyd iterations, max_steps 1000).
+c1_s10.field / c1_s10.trip  save_field / write_triplets output of the
+                 reference (C1 at step 10) for snapshot compatibility.
 --only a,b: regenerate only the named groups (seeds_collide, analysis).
 """
 
@@ -287,6 +289,21 @@ def make_dual_winding():
         json.dump(out, fh)
 
 
+def make_snapshots():
+    """Snapshot files written by the reference itself: save_field of the C1
+    field at step 10 (with an extra header key) and write_triplets of the
+    same matrix with comment lines (field.py:372-387, sparse.py:427-436)."""
+    t = np.load(os.path.join(HERE, "c1_traj.npz"))
+    phi = ft.SparseMat(int(t["s10_shape"][0]), int(t["s10_shape"][1]), t["s10_ptr"], t["s10_idx"],
+                       t["s10_val"], check=False)
+    fld = LayeredField(phi, t["seeds"], 10)
+    params = ft.CouplingParams(dt=0.05, mu=2.5)
+    from fieldtess.field import save_field
+    from fieldtess.sparse import write_triplets
+    save_field(fld, params, os.path.join(HERE, "c1_s10.field"), extra_header={"mesh": "icosphere-4"})
+    write_triplets(phi, os.path.join(HERE, "c1_s10.trip"), comments=("fieldtess triplets", "step 10"))
+
+
 def make_cell_geometry(name, mesh, fld):
     """Reference approx_centroid / backproject for every cell of fld."""
     from fieldtess import lloyd as L
@@ -396,7 +413,7 @@ def main():
     if "--only" in sys.argv:
         for name in sys.argv[sys.argv.index("--only") + 1].split(","):
             {"seeds_collide": make_seed_collisions, "analysis": make_analysis,
-             "winding": make_dual_winding}[name]()
+             "winding": make_dual_winding, "snapshots": make_snapshots}[name]()
         return
     make_step_cases()
     make_labels_cases()
@@ -406,6 +423,7 @@ def main():
                     os.path.join(HERE, "c1_traj.npz"), 500)
     make_c1_dual(c1, ico4)
     make_dual_winding()
+    make_snapshots()
     geo = make_cell_geometry("c1", ico4, c1)
     torus = ft.gen_periodic_grid(64, 64)
     tfld = trajectory(torus, seeds["torus64"], {1, 60, 300},
