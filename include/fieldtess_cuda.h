@@ -198,6 +198,20 @@ int ft_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
             const ft_params* params, void* workspace, size_t ws_bytes,
             ft_step_stats* stats, void* stream);
 
+/* ft_step with its device time split at the kernel-group boundaries into
+ * phase_ms[5] (host, milliseconds; synchronises the stream), reported in
+ * the reference's five StepStats phase slots (field.py:220-285):
+ *   [0] skeleton_time   layout conversion + active-column selection (prep)
+ *   [1] spgemm_time     band kernel: fused L^T gather + update + normalise
+ *                       of the one/two-layer columns
+ *   [2] expand_time     three-layer kernel
+ *   [3] update_time     warp / serial kernels of the wider columns
+ *   [4] normalize_time  statistics finalize + compaction to CSC */
+int ft_step_phases(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
+                   ft_tiled* scratch_in, ft_tiled* scratch_out, ft_csc* phi_out,
+                   int32_t dtype, const ft_params* params, void* workspace,
+                   size_t ws_bytes, ft_step_stats* stats, float* phase_ms, void* stream);
+
 /* One step from a hybrid-layout input, for callers that drive the step
  * sequence themselves (bench.py brackets the column kernels with CUDA
  * events).  `out_id` (0 / 1) names the target buffer: a sequence of steps
@@ -448,8 +462,10 @@ int ft_lloyd_backproject_keys(const double* positions, int32_t n_vertices, const
  *          positive area                             (dual.py:107-215)
  *   set_3  junction triples i<j<k (key (i*n+j)*n+k) of every face with >= 3
  *          cells                                     (dual.py:223-231)
- * n_faces == 0 computes set_v only.  *overflow (device): 1 = a set is full,
- * 2 = a vertex/face carries more than 32 thresholded cells. */
+ * n_faces == 0 computes set_v only.  *overflow (device): bit flags: 1 = a set
+ * is full, 2 = a vertex/face carries more than 32 thresholded cells; bit 2
+ * (4): some cell pair skipped a zero-area face or a non-finite value in the
+ * crossing test (the reference warns there, dual.py:187-199). */
 int ft_dual_products(const ft_csc* phi, int32_t n_faces, const int32_t* faces,
                      const double* face_area, double threshold, uint64_t* set_v,
                      uint64_t* set_t, uint64_t* set_x, uint64_t* set_3,

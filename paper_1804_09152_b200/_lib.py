@@ -98,7 +98,7 @@ assert STATS_DTYPE.itemsize == STATS_BYTES
 # every symbol include/fieldtess_cuda.h declares
 EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
            "ft_workspace_init", "ft_tiled_from_csc",
-           "ft_step", "ft_step_run", "ft_compact",
+           "ft_step", "ft_step_phases", "ft_step_run", "ft_compact",
            "ft_evolve", "ft_labels", "ft_faces_by_cell", "ft_lloyd_centroids",
            "ft_dual_products", "ft_domain_step", "ft_halo_bytes", "ft_halo_pack",
            "ft_halo_unpack", "ft_domain_combine", "ft_domain_control", "ft_laplacian_pack",
@@ -129,6 +129,10 @@ def _declare(lib):
     lib.ft_step.argtypes = [P(FtCsc), ctypes.c_int32, P(FtCsc), P(FtTiled), P(FtTiled), P(FtCsc),
                             ctypes.c_int32, P(FtParams), vp, ctypes.c_size_t, vp, vp]
     lib.ft_step.restype = ctypes.c_int
+    lib.ft_step_phases.argtypes = [P(FtCsc), ctypes.c_int32, P(FtCsc), P(FtTiled), P(FtTiled), P(FtCsc),
+                                   ctypes.c_int32, P(FtParams), vp, ctypes.c_size_t, vp,
+                                   P(ctypes.c_float), vp]
+    lib.ft_step_phases.restype = ctypes.c_int
     lib.ft_step_run.argtypes = [P(FtCsc), ctypes.c_int32, P(FtTiled), P(FtTiled), ctypes.c_int32,
                                 ctypes.c_int32, P(FtParams), vp, ctypes.c_size_t, ctypes.c_int32,
                                 vp, vp]

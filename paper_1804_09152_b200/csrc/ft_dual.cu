@@ -55,7 +55,7 @@ __device__ __forceinline__ void set_insert(unsigned long long* t, unsigned long 
         if (old == kEmpty || old == key) return;
         h = (h + 1) & mask;
     }
-    atomicExch(overflow, 1);
+    atomicOr(overflow, 1);
 }
 
 // PHI(r, v) or 0.0 (SparseMat.get)
@@ -132,7 +132,7 @@ __global__ void dual_vertex_kernel(const DualParams p) {
     if (v >= p.n_v) return;
     int c[kMaxFaceCells];
     const int n = vertex_cells(p, v, c, kMaxFaceCells);
-    if (n > kMaxFaceCells) { atomicExch(p.overflow, 2); return; }
+    if (n > kMaxFaceCells) { atomicOr(p.overflow, 2); return; }
     for (int a = 0; a < n; ++a)
         for (int b = a + 1; b < n; ++b)
             set_insert(p.set_v, p.mask_v, (unsigned long long)c[a] * p.n_rows + c[b], p.overflow);
@@ -148,13 +148,13 @@ __global__ void dual_face_kernel(const DualParams p) {
     for (int k = 0; k < 3; ++k) {
         int vc[kMaxFaceCells];
         const int m = vertex_cells(p, fv[k], vc, kMaxFaceCells);
-        if (m > kMaxFaceCells) { atomicExch(p.overflow, 2); return; }
+        if (m > kMaxFaceCells) { atomicOr(p.overflow, 2); return; }
         for (int i = 0; i < m; ++i) {
             int x = vc[i], pos = n;
             bool dup = false;
             for (int t = 0; t < n; ++t) dup |= (c[t] == x);
             if (dup) continue;
-            if (n == kMaxFaceCells) { atomicExch(p.overflow, 2); return; }
+            if (n == kMaxFaceCells) { atomicOr(p.overflow, 2); return; }
             while (pos > 0 && c[pos - 1] > x) { c[pos] = c[pos - 1]; --pos; }
             c[pos] = x;
             ++n;
@@ -166,7 +166,10 @@ __global__ void dual_face_kernel(const DualParams p) {
         for (int b = a + 1; b < n; ++b) {
             const unsigned long long key = (unsigned long long)c[a] * p.n_rows + c[b];
             set_insert(p.set_t, p.mask_t, key, p.overflow);
-            if (!live) continue;
+            if (!live) {                 // degenerate face: the host replays the warning
+                atomicOr(p.overflow, 4);
+                continue;
+            }
             double vi[3], vj[3];
             bool fin = true;
             for (int k = 0; k < 3; ++k) {
@@ -174,7 +177,10 @@ __global__ void dual_face_kernel(const DualParams p) {
                 vj[k] = phi_get(p, c[b] + 1, fv[k]);
                 fin &= isfinite(vi[k]) && isfinite(vj[k]);
             }
-            if (!fin) continue;
+            if (!fin) {                  // non-finite interpolation: likewise
+                atomicOr(p.overflow, 4);
+                continue;
+            }
             double si[4], sj[4];
             if (!isoline(vi, p.thr, si) || !isoline(vj, p.thr, sj)) continue;
             if (seg_intersect(si, sj)) set_insert(p.set_x, p.mask_x, key, p.overflow);

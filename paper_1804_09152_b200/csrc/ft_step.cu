@@ -1678,6 +1678,7 @@ struct DevState {
     cudaEvent_t gev[2];
     GraphEntry graphs[8];
     int graph_next;
+    cudaEvent_t pev[7];       // ft_step_phases: phase boundaries (timing events)
 };
 static DevState g_dev[64];
 
@@ -1754,7 +1755,7 @@ static void lib_init() {
 // for the owned columns; every step is a full step).
 static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* in, ft_tiled* out, int out_id,
                           int32_t dtype, const ft_params* prm, void* workspace, size_t ws_bytes, int check_done,
-                          cudaStream_t s, const ft_domain* dom = nullptr) {
+                          cudaStream_t s, const ft_domain* dom = nullptr, const cudaEvent_t* ev = nullptr) {
     if (!lap_t || !out || !in || !prm || !workspace) return set_err(FT_ERR_ARG, "null argument");
     if (dtype != FT_F64 && dtype != FT_F32) return set_err(FT_ERR_ARG, "bad dtype");
     const int n_rows = in->n_rows, n_v = in->n_cols;
@@ -1800,6 +1801,7 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     const int prep_span = n_own + (j_base & 63);
     const int prep_grid = (prep_span + ft::kPrepCols * ft::kPrepTPB - 1) / (ft::kPrepCols * ft::kPrepTPB);
     if (kmask & 1) launch_dep(ft::prep_kernel, prep_grid, ft::kPrepTPB, s, p);
+    if (ev) cudaEventRecord(ev[0], s);
     int bg = d.band_grid[dtype == FT_F32][uni][packed];
     const int need_b = (n_own + ft::kBandTPB - 1) / ft::kBandTPB;
     if (bg > need_b) bg = need_b;
@@ -1813,11 +1815,14 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     } else if (kmask & 2) {
         launch_dep(FT_PICK3(ft::band_kernel, dtype, uni, packed), bg, ft::kBandTPB, s, p);
     }
+    if (ev) cudaEventRecord(ev[1], s);
     if (kmask & 4) launch_dep(FT_PICK3(ft::wide3_kernel, dtype, uni, packed), 4 * d.sms, ft::kWide3TPB, s, p);
+    if (ev) cudaEventRecord(ev[2], s);
     if (kmask & 8) {
         launch_dep(FT_PICK3(ft::wide_kernel, dtype, uni, packed), 8 * d.sms, ft::kWideTPB, s, p);
         launch_dep(FT_PICK2(ft::deep_kernel, dtype, uni), 64, ft::kDeepTPB, s, p);
     }
+    if (ev) cudaEventRecord(ev[3], s);
     return cuda_check("step kernels");
 }
 
@@ -1916,19 +1921,29 @@ extern "C" int ft_compact(const ft_tiled* src, ft_csc* dst, int32_t dtype, void*
     return launch_compact(c, dtype, (cudaStream_t)stream);
 }
 
-extern "C" int ft_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in, ft_tiled* scratch_in,
-                       ft_tiled* scratch_out, ft_csc* phi_out, int32_t dtype, const ft_params* params,
-                       void* workspace, size_t ws_bytes, ft_step_stats* stats, void* stream) {
+static int step_impl(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in, ft_tiled* scratch_in,
+                     ft_tiled* scratch_out, ft_csc* phi_out, int32_t dtype, const ft_params* params,
+                     void* workspace, size_t ws_bytes, ft_step_stats* stats, cudaStream_t s, float* phase_ms) {
     if (!phi_in || !phi_out || !stats || !scratch_in || !scratch_out) return set_err(FT_ERR_ARG, "null argument");
     if (phi_out->n_cols != phi_in->n_cols || phi_out->n_rows != phi_in->n_rows)
         return set_err(FT_ERR_SHAPE, "output buffer has wrong shape");
     if (ws_bytes < ft::workspace_bytes(phi_in->n_cols)) return set_err(FT_ERR_ARG, "workspace too small");
-    cudaStream_t s = (cudaStream_t)stream;
+    const cudaEvent_t* ev = nullptr;
+    if (phase_ms) {
+        DevState& d = dev_state();
+        std::lock_guard<std::mutex> lk(d.mu);
+        if (!d.pev[0])
+            for (int k = 0; k < 7; ++k)
+                if (cudaEventCreate(&d.pev[k]) != cudaSuccess) return set_err(FT_ERR_CUDA, "event create");
+        ev = d.pev;
+        cudaEventRecord(ev[0], s);
+    }
     ft::Workspace ws = ft::carve_workspace(workspace, phi_in->n_cols);
     ft::nonfinite_reset_kernel<<<1, 1, 0, s>>>(ws.ctl);
     int rc = launch_convert(phi_in, scratch_in, dtype, ws, s);
     if (rc != FT_OK) return rc;
-    rc = launch_columns(lap_t, lap_flags, scratch_in, scratch_out, 0, dtype, params, workspace, ws_bytes, 0, s);
+    rc = launch_columns(lap_t, lap_flags, scratch_in, scratch_out, 0, dtype, params, workspace, ws_bytes, 0, s,
+                        nullptr, ev ? ev + 1 : nullptr);
     if (rc != FT_OK) return rc;
     const long long cap = scratch_out->capacity < scratch_in->capacity ? scratch_out->capacity : scratch_in->capacity;
     launch_finalize(ws, stats, cap, 0, lap_flags, 0, scratch_in->capacity, false, s);
@@ -1937,7 +1952,33 @@ extern "C" int ft_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi
     fill_compact(c, scratch_out, nullptr, 0, phi_out, workspace);
     c.stats = stats;
     c.check_status = 1;
-    return launch_compact(c, dtype, s);
+    rc = launch_compact(c, dtype, s);
+    if (rc != FT_OK || !ev) return rc;
+    cudaEventRecord(ev[5], s);
+    if (cudaEventSynchronize(ev[5]) != cudaSuccess) return set_err(FT_ERR_CUDA, "phase timing");
+    // ev: 0 start | convert + prep | 1 | band | 2 | wide3 | 3 | wide + deep | 4 | finalize + compact | 5
+    for (int k = 0; k < 5; ++k) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+        phase_ms[k] = ms;
+    }
+    return cuda_check("ft_step_phases");
+}
+
+extern "C" int ft_step(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in, ft_tiled* scratch_in,
+                       ft_tiled* scratch_out, ft_csc* phi_out, int32_t dtype, const ft_params* params,
+                       void* workspace, size_t ws_bytes, ft_step_stats* stats, void* stream) {
+    return step_impl(lap_t, lap_flags, phi_in, scratch_in, scratch_out, phi_out, dtype, params, workspace, ws_bytes,
+                     stats, (cudaStream_t)stream, nullptr);
+}
+
+extern "C" int ft_step_phases(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in, ft_tiled* scratch_in,
+                              ft_tiled* scratch_out, ft_csc* phi_out, int32_t dtype, const ft_params* params,
+                              void* workspace, size_t ws_bytes, ft_step_stats* stats, float* phase_ms,
+                              void* stream) {
+    if (!phase_ms) return set_err(FT_ERR_ARG, "null argument");
+    return step_impl(lap_t, lap_flags, phi_in, scratch_in, scratch_out, phi_out, dtype, params, workspace, ws_bytes,
+                     stats, (cudaStream_t)stream, phase_ms);
 }
 
 // The steady part of evolve (steps 2, 3, ...: a -> b, b -> a) repeats with

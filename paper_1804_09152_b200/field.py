@@ -119,11 +119,17 @@ class CouplingParams:
 
 @dataclass
 class StepStats:
-    """Per-step diagnostics (field.py:74-92).  The fused kernel has no
-    internal phase boundaries: its device time is reported in
-    ``spgemm_time`` (the other phase fields stay 0) so ``total_time`` is the
-    step time.  ``nnz_skel`` is the interest-skeleton size (layer-nnz
-    updates of the step)."""
+    """Per-step diagnostics (field.py:74-92).  The fused engine has no
+    spgemm / skeleton / expand boundaries; :func:`step` reports the device
+    time of its kernel groups in the five phase slots (ft_step_phases):
+    ``skeleton_time`` layout conversion + active-column selection,
+    ``spgemm_time`` the band kernel (fused gather + update + normalise of
+    one/two-layer columns), ``expand_time`` the three-layer kernel,
+    ``update_time`` the wider-column kernels, ``normalize_time`` statistics
+    + compaction.  The device evolve loop (a CUDA graph, no host between
+    steps) reports each step's mean device time in ``spgemm_time``.
+    ``total_time`` is the step time either way.  ``nnz_skel`` is the
+    interest-skeleton size (layer-nnz updates of the step)."""
 
     max_delta: float
     nnz_phi: int
@@ -532,16 +538,13 @@ def step(field, lap, params, workspace=None):
     stream = _stream_handle()
     lib = _lib.lib()
     wp, wn = ws.ws_args()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    phase_ms = (ctypes.c_float * 5)()
     while True:
         in_c, si_c, sc_c, out_c = dphi.ft_csc(), scratch_in.ft_tiled(), scratch.ft_tiled(), out.ft_csc()
-        ev0.record()
-        rc = lib.ft_step(ctypes.byref(lap_c), dl.launch_flags(), ctypes.byref(in_c), ctypes.byref(si_c),
-                         ctypes.byref(sc_c), ctypes.byref(out_c), _ft_dtype(field.precision), ctypes.byref(prm),
-                         wp, wn, ctypes.c_void_p(ws.stats.data_ptr()), stream)
-        ev1.record()
-        _check(rc, "ft_step")
+        rc = lib.ft_step_phases(ctypes.byref(lap_c), dl.launch_flags(), ctypes.byref(in_c), ctypes.byref(si_c),
+                                ctypes.byref(sc_c), ctypes.byref(out_c), _ft_dtype(field.precision),
+                                ctypes.byref(prm), wp, wn, ctypes.c_void_p(ws.stats.data_ptr()), phase_ms, stream)
+        _check(rc, "ft_step_phases")
         rec = _stats_from_bytes(ws.stats.cpu().numpy().tobytes())[0]
         status = int(rec["status"])
         if status == _lib.FT_STATUS_OVERFLOW:
@@ -562,7 +565,9 @@ def step(field, lap, params, workspace=None):
     new_field = LayeredField(out, field.seed_vertices, field.step_count + 1)
     stats = StepStats(max_delta=float(rec["max_delta"]), nnz_phi=int(rec["nnz_phi"]),
                       base_mass=float(rec["base_mass"]),
-                      spgemm_time=ev0.elapsed_time(ev1) * 1e-3,
+                      skeleton_time=phase_ms[0] * 1e-3, spgemm_time=phase_ms[1] * 1e-3,
+                      expand_time=phase_ms[2] * 1e-3, update_time=phase_ms[3] * 1e-3,
+                      normalize_time=phase_ms[4] * 1e-3,
                       realloc_count=reallocs, nnz_skel=int(rec["nnz_skel"]))
     return new_field, stats
 

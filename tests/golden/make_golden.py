@@ -30,6 +30,8 @@ analysis.npz     analysis.py metrics: voronoi labels / margin masks (torus,
        c2_lloyd.json (5 Lloyd iterations, max_steps 1000).
 c1_s10.field / c1_s10.trip  save_field / write_triplets output of the
                  reference (C1 at step 10) for snapshot compatibility.
+dual_warnings.json  confirm_candidates warnings (degenerate face, NaN
+                 layer value) of the reference on a modified C1.
 --only a,b: regenerate only the named groups (seeds_collide, analysis).
 """
 
@@ -304,6 +306,68 @@ def make_snapshots():
     write_triplets(phi, os.path.join(HERE, "c1_s10.trip"), comments=("fieldtess triplets", "step 10"))
 
 
+def make_dual_warnings():
+    """confirm_candidates on C1 step 500 with (a) one mesh vertex moved onto
+    its neighbour (two zero-area faces) and (b) one NaN written into a
+    layer: the reference's RuntimeWarnings in order (dual.py:187-199) and the
+    curated result, at threshold 0.4 (A_t-only candidates exist there)."""
+    import warnings as wmod
+    THR = 0.4
+    from fieldtess import dual as dualmod
+    t = np.load(os.path.join(HERE, "c1_traj.npz"))
+    shp = t["s500_shape"]
+    base_vals = np.array(t["s500_val"], dtype=np.float64)
+    mesh0 = ft.gen_icosphere(4)
+    fld0 = LayeredField(ft.SparseMat(int(shp[0]), int(shp[1]), t["s500_ptr"], t["s500_idx"], base_vals,
+                                     check=False), t["seeds"], 500)
+    a_v = dualmod.vertex_adjacency(fld0, THR)
+    a_t = dualmod.triangle_adjacency(fld0, mesh0, THR)
+    cand = sorted(set(a_t.pairs()) - set(a_v.pairs()))
+    b = ft.spgemm(dualmod.threshold_rows(fld0, THR), mesh0.incidence)
+    foc = ft.transpose(b)
+
+    def shared(i, j):
+        return np.intersect1d(foc.column(i)[0], foc.column(j)[0])
+
+    out = {}
+    # (a) degenerate: collapse the first shared face of the first candidate
+    i, j = cand[0]
+    f = int(shared(i, j)[0])
+    v_from, v_to = int(mesh0.faces[f][1]), int(mesh0.faces[f][0])
+    pos = mesh0.positions.copy()
+    pos[v_from] = pos[v_to]
+    mesh1 = ft.TriMesh(pos, mesh0.faces.copy())
+    # (b) non-finite: NaN at a stored entry of layer i+1 on a vertex of the
+    # first shared face of the third candidate
+    i2, j2 = cand[2]
+    f2 = int(shared(i2, j2)[0])
+    ptr, idx = t["s500_ptr"], t["s500_idx"]
+    k_nan = -1
+    for v in mesh0.faces[f2]:
+        for k in range(ptr[v], ptr[v + 1]):
+            if idx[k] == i2 + 1:
+                k_nan = k
+        if k_nan >= 0:
+            break
+    vals2 = base_vals.copy()
+    vals2[k_nan] = np.nan
+    fld2 = LayeredField(ft.SparseMat(int(shp[0]), int(shp[1]), ptr, idx, vals2, check=False), t["seeds"], 500)
+    for name, fld, mesh, info in (("degenerate", fld0, mesh1, {"move": [v_from, v_to]}),
+                                  ("nonfinite", fld2, mesh0, {"nan_entry": int(k_nan)})):
+        av = dualmod.vertex_adjacency(fld, THR)
+        at = dualmod.triangle_adjacency(fld, mesh, THR)
+        with wmod.catch_warnings(record=True) as rec:
+            wmod.simplefilter("always")
+            cur = dualmod.confirm_candidates(fld, mesh, av, at, THR)
+        info["warnings"] = [str(w.message) for w in rec if issubclass(w.category, RuntimeWarning)]
+        info["curated"] = sorted(cur.pairs())
+        info["dropped"] = [list(d) for d in cur.dropped]
+        out[name] = info
+        print("dual warnings", name, len(info["warnings"]), info["warnings"][:3])
+    with open(os.path.join(HERE, "dual_warnings.json"), "w") as fh:
+        json.dump(out, fh)
+
+
 def make_cell_geometry(name, mesh, fld):
     """Reference approx_centroid / backproject for every cell of fld."""
     from fieldtess import lloyd as L
@@ -413,7 +477,8 @@ def main():
     if "--only" in sys.argv:
         for name in sys.argv[sys.argv.index("--only") + 1].split(","):
             {"seeds_collide": make_seed_collisions, "analysis": make_analysis,
-             "winding": make_dual_winding, "snapshots": make_snapshots}[name]()
+             "winding": make_dual_winding, "snapshots": make_snapshots,
+             "dual_warnings": make_dual_warnings}[name]()
         return
     make_step_cases()
     make_labels_cases()
@@ -424,6 +489,7 @@ def main():
     make_c1_dual(c1, ico4)
     make_dual_winding()
     make_snapshots()
+    make_dual_warnings()
     geo = make_cell_geometry("c1", ico4, c1)
     torus = ft.gen_periodic_grid(64, 64)
     tfld = trajectory(torus, seeds["torus64"], {1, 60, 300},

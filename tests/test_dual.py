@@ -117,3 +117,45 @@ def test_dual_winding_and_normal_flip_match_reference(name, traj, snap, level):
     assert ft.build_dual(cur, np.zeros((fld.n_cells, 3))).triangles.tolist() == ref["plain"]
     assert ft.build_dual(cur, pos, cell_normals=nrm).triangles.tolist() == ref["outward"]
     assert ft.build_dual(cur, pos, cell_normals=-nrm).triangles.tolist() == ref["inward"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["degenerate", "nonfinite"])
+def test_confirm_candidates_warnings_match_reference(case):
+    """A zero-area face (one vertex moved onto its neighbour) or a NaN in a
+    layer: the device crossing test skips it, the RuntimeWarnings are the
+    reference's in order, and the curated adjacency is unchanged from the
+    reference's (golden dual_warnings.json, ref dual.py:181-205)."""
+    import warnings
+    ref = golden_json("dual_warnings.json")[case]
+    mesh = ft.gen_icosphere(4)
+    fld = _field("c1_traj.npz", 500)
+    if case == "degenerate":
+        v_from, v_to = ref["move"]
+        pos = mesh.positions.copy()
+        pos[v_from] = pos[v_to]
+        mesh = ft.TriMesh(pos, mesh.faces.copy())
+    else:
+        phi = fld.phi
+        vals = np.array(phi.values[:phi.nnz], dtype=np.float64)
+        vals[ref["nan_entry"]] = np.nan
+        fld = ft.LayeredField(ft.SparseMat(phi.n_rows, phi.n_cols, phi.col_ptr, phi.row_idx[:phi.nnz], vals,
+                                           check=False), fld.seed_vertices, step_count=500)
+    a_v = ft.vertex_adjacency(fld, 0.4)
+    a_t = ft.triangle_adjacency(fld, mesh, 0.4)
+    with warnings.catch_warnings(record=True) as rec:
+        warnings.simplefilter("always")
+        cur = ft.confirm_candidates(fld, mesh, a_v, a_t, 0.4)
+    got = [str(w.message) for w in rec if issubclass(w.category, RuntimeWarning)]
+    assert got == ref["warnings"] and got
+    assert sorted(map(list, cur.pairs())) == ref["curated"]
+    assert [list(d) for d in cur.dropped] == ref["dropped"]
+
+
+@pytest.mark.gpu
+def test_confirm_candidates_clean_field_does_not_warn():
+    import warnings
+    mesh, fld = ft.gen_icosphere(4), _field("c1_traj.npz", 500)
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        ft.confirm_candidates(fld, mesh, ft.vertex_adjacency(fld, 0.4), ft.triangle_adjacency(fld, mesh, 0.4), 0.4)

@@ -449,3 +449,17 @@ def test_evolve_step_evolve_with_shared_workspace():
     ref, _ = po.evolve_c(po.Csc.of(fld.phi), lt, DEFAULT, 66)
     assert c.step_count == 66 and len(tr) == 25
     assert_csc_equal(c.phi, ref)
+
+
+def test_step_reports_phase_times():
+    """step() splits its device time over the reference's five StepStats
+    phase slots (ft_step_phases kernel groups, field.py:220-285)."""
+    mesh = ft.gen_icosphere(4)
+    lap = ft.build_laplacian(mesh)
+    fld = ft.init_field(mesh, ft.sample_seed_vertices(mesh, 64, 0))
+    for _ in range(3):
+        fld, st = ft.step(fld, lap, DEFAULT)
+    phases = [st.skeleton_time, st.spgemm_time, st.expand_time, st.update_time, st.normalize_time]
+    assert all(t >= 0.0 for t in phases)
+    assert st.spgemm_time > 0.0 and st.normalize_time > 0.0 and st.skeleton_time > 0.0
+    assert st.total_time == pytest.approx(sum(phases))
