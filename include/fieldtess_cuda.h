@@ -337,6 +337,43 @@ int ft_domain_combine(const ft_step_stats* records, int32_t world, int32_t rank,
  * status OK (rewind after a capacity failure). */
 int ft_domain_control(void* workspace, int32_t set_steps, int64_t* out, void* stream);
 
+/* -- mesh generation, geometry, uniform Laplacian (mesh.py:20-246, 379-431) */
+/* Device replacements of the host generators, bitwise equal to the
+ * reference's outputs (positions, faces, face_area, vertex_area, L^T).
+ * Icosphere level (mesh.py:216-246), half-edge h = 3 f + e (edge e of face
+ * f runs faces[f][e] -> faces[f][(e+1)%3]), twin = opposite half-edge or -1:
+ *   ft_ico_flags      flag[h] = 1 where h is its edge's first encounter;
+ *   ft_ico_midpoints  with incl = inclusive scan of the flags: mid[h] = the
+ *                     midpoint id, new positions unit(p[u] + p[v]) written
+ *                     at n_old.. (positions has room for them);
+ *   ft_ico_children   the 4 child faces per face and their twins;
+ *   ft_renormalize    positions /= norm(positions, axis=1) (final pass).
+ * ft_torus_grid       gen_periodic_grid (mesh.py:168-199).
+ * ft_face_geometry    face area / normal / barycenter and area/3 per face
+ *                     (TriMesh, mesh.py:56-84); period = the 2x3 period
+ *                     vectors or NULL, quarter_r2 = the squared quarter of
+ *                     the shortest lattice offset (TriMesh._wrap).
+ * ft_vertex_area      per-vertex sum of area/3 in (face, corner) order;
+ *                     corner = flattened face-corner positions sorted stably
+ *                     by vertex, ptr = per-vertex offsets into it.
+ * ft_uniform_laplacian  L^T (ptr/idx/val_t, CSC) and L (same pattern, val)
+ *                     from the sorted one-ring nptr/nidx (n_v + 1 / 2E). */
+int ft_ico_flags(int64_t n_half, const int32_t* twin, int32_t* flag, void* stream);
+int ft_ico_midpoints(int32_t n_faces, const int32_t* faces, const int32_t* twin, const int64_t* incl,
+                     int32_t n_old, double* positions, int32_t* mid, void* stream);
+int ft_ico_children(int32_t n_faces, const int32_t* faces, const int32_t* twin, const int32_t* mid,
+                    int32_t* faces_out, int32_t* twin_out, void* stream);
+int ft_renormalize(int32_t n, double* positions, void* stream);
+int ft_torus_grid(int32_t nx, int32_t ny, double spacing, double* positions, int32_t* faces,
+                  void* stream);
+int ft_face_geometry(int32_t n_faces, const double* positions, const int32_t* faces,
+                     const double* period, double quarter_r2, double* area, double* normal,
+                     double* barycenter, double* third, void* stream);
+int ft_vertex_area(int32_t n_v, const int64_t* ptr, const int64_t* corner, const double* third,
+                   double* out, void* stream);
+int ft_uniform_laplacian(int32_t n_v, const int64_t* nptr, const int32_t* nidx, int32_t* ptr,
+                         int32_t* idx, double* val_t, double* val, void* stream);
+
 /* -- the reference's public sparse algebra (sparse.py:279-420) ------------ */
 /* General-purpose versions of the operations the Euler step fuses, bitwise
  * equal to the numba kernels (values FT_F64 only).  spgemm C = A B is

@@ -105,7 +105,8 @@ EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
            "ft_point_triangle_distances", "ft_spgemm_count", "ft_spgemm_expand",
            "ft_segment_sums", "ft_skeleton", "ft_expand", "ft_normalize_columns",
            "ft_clique_triangles", "ft_lloyd_backproject", "ft_lloyd_partials", "ft_lloyd_finish",
-           "ft_lloyd_backproject_keys")
+           "ft_lloyd_backproject_keys", "ft_ico_flags", "ft_ico_midpoints", "ft_ico_children",
+           "ft_renormalize", "ft_torus_grid", "ft_face_geometry", "ft_vertex_area", "ft_uniform_laplacian")
 
 _lib = None
 
@@ -187,6 +188,18 @@ def _declare(lib):
     lib.ft_expand.restype = ctypes.c_int
     lib.ft_normalize_columns.argtypes = [P(FtCsc), vp, vp, vp]
     lib.ft_normalize_columns.restype = ctypes.c_int
+    i64, f64 = ctypes.c_int64, ctypes.c_double
+    lib.ft_ico_flags.argtypes = [i64, vp, vp, vp]
+    lib.ft_ico_midpoints.argtypes = [i32, vp, vp, vp, i32, vp, vp, vp]
+    lib.ft_ico_children.argtypes = [i32, vp, vp, vp, vp, vp, vp]
+    lib.ft_renormalize.argtypes = [i32, vp, vp]
+    lib.ft_torus_grid.argtypes = [i32, i32, f64, vp, vp, vp]
+    lib.ft_face_geometry.argtypes = [i32, vp, vp, vp, f64, vp, vp, vp, vp, vp]
+    lib.ft_vertex_area.argtypes = [i32, vp, vp, vp, vp, vp]
+    lib.ft_uniform_laplacian.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp]
+    for name in ("ft_ico_flags", "ft_ico_midpoints", "ft_ico_children", "ft_renormalize", "ft_torus_grid",
+                 "ft_face_geometry", "ft_vertex_area", "ft_uniform_laplacian"):
+        getattr(lib, name).restype = ctypes.c_int
     lib.ft_clique_triangles.argtypes = [i32, vp, vp, vp, vp, vp, vp]
     lib.ft_clique_triangles.restype = ctypes.c_int
     lib.ft_lloyd_backproject.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp]

@@ -243,6 +243,8 @@ def init_field(mesh, seeds, precision=None):
     n_v = mesh.n_vertices
     if seeds.size and (seeds.min() < 0 or seeds.max() >= n_v):
         raise ShapeError("seed vertex index out of range")
+    if getattr(mesh, "_topo_dev", None) is not None:
+        return _init_field_device(mesh, seeds, precision)
     nptr = np.asarray(mesh.neighbor_ptr, dtype=np.int64)
     nidx = np.asarray(mesh.neighbor_idx, dtype=np.int64)
     deg = nptr[seeds + 1] - nptr[seeds]
@@ -272,6 +274,46 @@ def init_field(mesh, seeds, precision=None):
     vals[dst] = 1.0 / claims[sc]
     phi = SparseMat(seeds.size + 1, n_v, col_ptr.astype(INDEX), row_idx, vals, check=False)
     return LayeredField(phi, seeds, precision=precision)
+
+
+def _init_field_device(mesh, seeds, precision):
+    """init_field on a device-built mesh: the same claim arithmetic on the
+    device one-ring, the field created directly as a device CSC (values
+    1.0 / claims in float64, then the storage precision)."""
+    torch = _torch()
+    topo = mesh._topo_dev
+    nptr, nidx = topo["neighbor_ptr"], topo["neighbor_idx"]
+    dev = nptr.device
+    n_v = mesh.n_vertices
+    n_s = seeds.size
+    s = torch.from_numpy(seeds).to(dev)
+    deg = nptr[s + 1] - nptr[s]
+    cnt = deg + 1
+    seg = torch.cumsum(cnt, 0) - cnt
+    total = int(cnt.sum().item()) if n_s else 0
+    cl_row = torch.repeat_interleave(torch.arange(1, n_s + 1, device=dev), cnt)
+    pos_in = torch.arange(total, device=dev) - torch.repeat_interleave(seg, cnt)
+    starts = torch.repeat_interleave(nptr[s], cnt)
+    ring = nidx[torch.clamp(starts + pos_in - 1, 0, max(nidx.numel() - 1, 0))].long()
+    cl_col = torch.where(pos_in == 0, torch.repeat_interleave(s, cnt), ring)
+    claims = torch.bincount(cl_col, minlength=n_v)
+    col_ptr = torch.zeros(n_v + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(torch.where(claims == 0, 1, claims), 0, out=col_ptr[1:])
+    nnz = int(col_ptr[-1].item())
+    out = DeviceCSC.allocate(n_s + 1, n_v, max(nnz, 1), _value_dtype(precision or _default_precision), dev)
+    out.col_ptr.copy_(col_ptr)
+    out.row_idx.zero_()
+    vals = torch.ones(max(nnz, 1), dtype=torch.float64, device=dev)
+    order = torch.argsort(cl_col * (n_s + 1) + cl_row, stable=True)
+    sc, sr = cl_col[order], cl_row[order]
+    cc = claims[claims > 0]
+    rank = torch.arange(sc.numel(), device=dev) - torch.repeat_interleave(torch.cumsum(cc, 0) - cc, cc)
+    dst = col_ptr[sc] + rank
+    out.row_idx[dst] = sr.to(torch.int32)
+    vals[dst] = 1.0 / claims[sc].double()
+    out.values.copy_(vals.to(out.values.dtype))
+    out.nnz = nnz
+    return LayeredField(out, seeds, precision=precision)
 
 
 # ---------------------------------------------------------------------------
@@ -370,15 +412,34 @@ def _with_diagonal(mat_t):
                                                    np.zeros(miss.size)]))
 
 
+def _lap_size(lap):
+    """Vertex count of a Laplacian without materialising a device-built one."""
+    dev = getattr(lap, "device", None)
+    return dev["n"] if dev is not None else lap.mat.n_rows
+
+
 def device_laplacian(lap, precision):
     """Upload ``lap.mat_t`` once per Laplacian object (cached on it)."""
-    key = (id(lap.mat_t), int(lap.mat_t.col_ptr[lap.mat_t.n_cols]))
+    dev = getattr(lap, "device", None)
+    if dev is not None:
+        key = ("device", id(dev["idx"]))
+    else:
+        key = (id(lap.mat_t), int(lap.mat_t.col_ptr[lap.mat_t.n_cols]))
     cache = getattr(lap, "_ft_device", None)
     if cache is None or cache[0] != key:
-        mat_t = _with_diagonal(lap.mat_t)
-        flags = _lib.FT_LAP_UNIFORM if _uniform_values_exact(mat_t) else _lib.FT_LAP_EXPLICIT
-        dl = _DeviceLap({}, flags, mat_t.n_cols, symmetric=_pattern_symmetric(lap))
-        dl.host = mat_t
+        if dev is not None:
+            # built on the device by ft_uniform_laplacian: the uniform
+            # weights, a diagonal in every column and a symmetric pattern
+            # by construction; the host copy is never needed
+            dl = _DeviceLap({}, _lib.FT_LAP_UNIFORM, dev["n"], symmetric=True)
+            dl.host = None
+            n, nnz = dev["n"], int(dev["idx"].numel())
+            dl.lap_t["exact"] = DeviceCSC(n, n, dev["ptr"], dev["idx"], dev["val_t"], nnz)
+        else:
+            mat_t = _with_diagonal(lap.mat_t)
+            flags = _lib.FT_LAP_UNIFORM if _uniform_values_exact(mat_t) else _lib.FT_LAP_EXPLICIT
+            dl = _DeviceLap({}, flags, mat_t.n_cols, symmetric=_pattern_symmetric(lap))
+            dl.host = mat_t
         cache = (key, dl)
         try:
             lap._ft_device = cache
@@ -386,7 +447,12 @@ def device_laplacian(lap, precision):
             pass
     dl = cache[1]
     if precision not in dl.lap_t:
-        dl.lap_t[precision] = DeviceCSC.from_host(dl.host, _value_dtype(precision), _device())
+        if dl.host is None:
+            ex = dl.lap_t["exact"]
+            dl.lap_t[precision] = DeviceCSC(ex.n_rows, ex.n_cols, ex.col_ptr, ex.row_idx,
+                                            ex.values.to(_value_dtype(precision)), ex.nnz)
+        else:
+            dl.lap_t[precision] = DeviceCSC.from_host(dl.host, _value_dtype(precision), _device())
         if dl.pack is None and dl.flags == _lib.FT_LAP_UNIFORM and PACK_LAPLACIAN:
             dl.pack, dl.n_csr = pack_laplacian(dl.lap_t[precision])
     return dl
@@ -521,7 +587,7 @@ def step(field, lap, params, workspace=None):
     torch = _torch()
     params.validate()
     n_v = field.n_vertices
-    if lap.mat.n_rows != n_v:
+    if _lap_size(lap) != n_v:
         raise ShapeError("Laplacian size does not match field")
     dphi = field.device_phi()
     ws = workspace if workspace is not None else _scratch_workspace(n_v, field.precision, dphi.values.device)
@@ -612,7 +678,7 @@ def _evolve_host(field, lap, params, max_steps, tol, ws, on_step, base_threshold
 def _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold):
     torch = _torch()
     n_v = field.n_vertices
-    if lap.mat.n_rows != n_v:
+    if _lap_size(lap) != n_v:
         raise ShapeError("Laplacian size does not match field")
     src = field.device_phi()
     device = src.values.device

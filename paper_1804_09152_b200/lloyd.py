@@ -49,11 +49,18 @@ class _DeviceMesh:
         def up(a, dt):
             return torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)
 
-        self.positions = up(mesh.positions, np.float64)
-        self.faces = up(mesh.faces, np.int32)
-        self.area = up(mesh.face_area, np.float64)
-        self.bary = up(mesh.face_barycenter, np.float64)
-        self.normal = up(mesh.face_normal, np.float64)
+        da = mesh.device_arrays() if hasattr(mesh, "device_arrays") else None
+        if da is not None and da[0].device == device:
+            # built on this device (devmesh): reuse, no host round trip
+            self.positions, self.faces = da
+            g = mesh._device_geometry()
+            self.area, self.bary, self.normal = g["face_area"], g["face_barycenter"], g["face_normal"]
+        else:
+            self.positions = up(mesh.positions, np.float64)
+            self.faces = up(mesh.faces, np.int32)
+            self.area = up(mesh.face_area, np.float64)
+            self.bary = up(mesh.face_barycenter, np.float64)
+            self.normal = up(mesh.face_normal, np.float64)
         self.period = (None if mesh.period_vectors is None else
                        (ctypes.c_double * 6)(*np.asarray(mesh.period_vectors, dtype=np.float64).ravel()))
         self.n_vertices = mesh.n_vertices

@@ -10,6 +10,10 @@ same numpy reductions as the reference so derived areas are bitwise equal.
 The icosphere generator is not capped at subdivision 7 (the reference's
 limit, mesh.py:222-223): levels 8..12 are produced by the same midpoint
 numbering rule, vectorised.
+
+With a GPU the generators, the derived data and the uniform Laplacian are
+built on the device instead (:mod:`devmesh`, ft_mesh.cu; same bytes) and
+copied to the host only when a host attribute is first read.
 """
 
 import warnings
@@ -18,6 +22,7 @@ import numpy as np
 
 from .errors import (IsolatedVertexError, MeshFormatError,
                      NonTriangularFaceError, ShapeError)
+from . import devmesh
 from .sparse import INDEX, SparseMat, transpose
 
 
@@ -47,7 +52,38 @@ class TriMesh:
         self.period_vectors = (None if period_vectors is None
                                else np.asarray(period_vectors, dtype=np.float64))
         self._cache = {}
+        self._topo = {}
         self._topology()
+
+    @classmethod
+    def _from_device(cls, positions, faces, period_vectors=None):
+        """A generator's output built on the device (valid by construction):
+        host positions / faces now, topology on the device (host copies on
+        first access), geometry on first use."""
+        self = cls.__new__(cls)
+        self.positions = positions.cpu().numpy()
+        self.faces = faces.cpu().numpy()
+        self.period_vectors = (None if period_vectors is None
+                               else np.asarray(period_vectors, dtype=np.float64))
+        self._cache = {"dev_positions": positions, "dev_faces": faces}
+        self._topo = {}
+        self._topo_dev = devmesh.topology(self.positions.shape[0], faces)
+        return self
+
+    def device_arrays(self):
+        """(positions, faces) device tensors of a device-built mesh, else None."""
+        c = self._cache
+        return (c["dev_positions"], c["dev_faces"]) if "dev_positions" in c else None
+
+    def _topo_get(self, name):
+        if name not in self._topo:
+            self._topo[name] = self._topo_dev[name].cpu().numpy()
+        return self._topo[name]
+
+    edges = property(lambda self: self._topo_get("edges"), doc="sorted unique undirected edges (E, 2)")
+    degree = property(lambda self: self._topo_get("degree"))
+    neighbor_ptr = property(lambda self: self._topo_get("neighbor_ptr"))
+    neighbor_idx = property(lambda self: self._topo_get("neighbor_idx"))
 
     # derived data (geometry and incidence are computed lazily: the Euler
     # step only needs the topology, and the torus geometry pass is the
@@ -55,6 +91,11 @@ class TriMesh:
 
     def _geometry(self):
         if "face_area" in self._cache:
+            return self._cache
+        if "dev_positions" in self._cache:
+            dev = self._device_geometry()
+            for k in ("face_area", "face_normal", "face_barycenter", "vertex_area"):
+                self._cache[k] = dev[k].cpu().numpy()
             return self._cache
         p, f = self.positions, self.faces
         e1 = self.wrap_deltas(p[f[:, 1]] - p[f[:, 0]])
@@ -81,10 +122,27 @@ class TriMesh:
             self._cache["incidence_t"] = transpose(inc)
         return self._cache
 
-    face_area = property(lambda self: self._geometry()["face_area"])
-    face_normal = property(lambda self: self._geometry()["face_normal"])
-    face_barycenter = property(lambda self: self._geometry()["face_barycenter"])
-    vertex_area = property(lambda self: self._geometry()["vertex_area"])
+    def _device_geometry(self):
+        """Device geometry tensors of a device-built mesh (computed once)."""
+        c = self._cache
+        if "dev_geometry" not in c:
+            c["dev_geometry"] = devmesh.geometry(c["dev_positions"], c["dev_faces"], self.period_vectors,
+                                                 self._quarter_r2() if self.periodic else 0.0)
+        return c["dev_geometry"]
+
+    def _geo(self, name):
+        c = self._cache
+        if name not in c:
+            if "dev_positions" in c:
+                c[name] = self._device_geometry()[name].cpu().numpy()
+            else:
+                self._geometry()
+        return c[name]
+
+    face_area = property(lambda self: self._geo("face_area"))
+    face_normal = property(lambda self: self._geo("face_normal"))
+    face_barycenter = property(lambda self: self._geo("face_barycenter"))
+    vertex_area = property(lambda self: self._geo("vertex_area"))
     incidence = property(lambda self: self._incidences()["incidence"],
                          doc="binary vertex-face incidence (n_v x n_f), 3 per column")
     incidence_t = property(lambda self: self._incidences()["incidence_t"])
@@ -97,18 +155,19 @@ class TriMesh:
         hi = np.concatenate([f[:, 1], f[:, 2], f[:, 0]]).astype(np.int64)
         a, b = np.minimum(lo, hi), np.maximum(lo, hi)
         keys, counts = np.unique(a * max(n_v, 1) + b, return_counts=True)
-        self.edges = np.stack([keys // max(n_v, 1), keys % max(n_v, 1)], axis=1)
+        edges = np.stack([keys // max(n_v, 1), keys % max(n_v, 1)], axis=1)
         if np.any(counts > 2):
             warnings.warn(f"{int((counts > 2).sum())} non-manifold edge(s) (more than "
                           "2 incident faces); neighbors are treated uniformly",
                           RuntimeWarning, stacklevel=3)
-        src = np.concatenate([self.edges[:, 0], self.edges[:, 1]])
-        dst = np.concatenate([self.edges[:, 1], self.edges[:, 0]])
+        src = np.concatenate([edges[:, 0], edges[:, 1]])
+        dst = np.concatenate([edges[:, 1], edges[:, 0]])
         order = np.argsort(src * max(n_v, 1) + dst, kind="stable")
-        self.degree = np.bincount(src, minlength=n_v)
-        self.neighbor_ptr = np.zeros(n_v + 1, dtype=np.int64)
-        np.cumsum(self.degree, out=self.neighbor_ptr[1:])
-        self.neighbor_idx = dst[order].astype(np.int32)
+        degree = np.bincount(src, minlength=n_v)
+        ptr = np.zeros(n_v + 1, dtype=np.int64)
+        np.cumsum(degree, out=ptr[1:])
+        self._topo = {"edges": edges, "degree": degree, "neighbor_ptr": ptr,
+                      "neighbor_idx": dst[order].astype(np.int32)}
 
     # queries ---------------------------------------------------------------
 
@@ -155,6 +214,16 @@ class TriMesh:
                                    for i in range(0, deltas.shape[0], self._WRAP_CHUNK)])
         return self._wrap(deltas)
 
+    def _quarter_r2(self):
+        """Squared quarter of the shortest nonzero lattice offset: a delta
+        with lattice coordinate 0 shorter than this is its own shortest
+        representative."""
+        if not hasattr(self, "_wrap_r2"):
+            offs = [np.array([di, dj]) @ self.period_vectors for di in (-1.0, 0.0, 1.0)
+                    for dj in (-1.0, 0.0, 1.0) if (di, dj) != (0.0, 0.0)]
+            self._wrap_r2 = (min(float(np.dot(o, o)) for o in offs) ** 0.5 / 4.0) ** 2
+        return self._wrap_r2
+
     def _wrap(self, deltas):
         basis = self.period_vectors[:, :2].T
         frac = np.linalg.solve(basis, deltas[:, :2].T).T
@@ -163,11 +232,7 @@ class TriMesh:
         # shortest lattice offset has (0, 0) as its strict minimum whatever the
         # rounding: its result is deltas - 0 = deltas.  Only the others (faces
         # across the seams) run the 9-candidate search.
-        if not hasattr(self, "_wrap_r2"):
-            offs = [np.array([di, dj]) @ self.period_vectors for di in (-1.0, 0.0, 1.0)
-                    for dj in (-1.0, 0.0, 1.0) if (di, dj) != (0.0, 0.0)]
-            self._wrap_r2 = (min(float(np.dot(o, o)) for o in offs) ** 0.5 / 4.0) ** 2
-        short = (near[:, 0] == 0) & (near[:, 1] == 0) & (np.einsum("ij,ij->i", deltas, deltas) < self._wrap_r2)
+        short = (near[:, 0] == 0) & (near[:, 1] == 0) & (np.einsum("ij,ij->i", deltas, deltas) < self._quarter_r2())
         if short.all():
             return deltas.copy()
         out = deltas.copy()
@@ -205,6 +270,9 @@ def gen_periodic_grid(nx, ny, spacing=1.0):
     s = float(spacing)
     a1 = np.array([s, 0.0, 0.0])
     a2 = np.array([0.5 * s, 0.5 * np.sqrt(3.0) * s, 0.0])
+    if devmesh.enabled():
+        pos, faces = devmesh.torus(int(nx), int(ny), s)
+        return TriMesh._from_device(pos, faces, period_vectors=np.stack([nx * a1, ny * a2]))
     jj, ii = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
     positions = ii.reshape(-1, 1) * a1 + jj.reshape(-1, 1) * a2
     i = np.arange(nx, dtype=np.int64)[None, :]
@@ -255,6 +323,8 @@ def gen_icosphere(subdiv, max_subdiv=7):
         raise MeshFormatError(f"subdiv must be in [0, {max_subdiv}]")
     verts = _unit(_ICO_V.copy())
     faces = _ICO_F.copy()
+    if devmesh.enabled():
+        return TriMesh._from_device(*devmesh.icosphere(int(subdiv), verts, faces))
     for _ in range(subdiv):
         n_old = verts.shape[0]
         e0 = faces[:, [0, 1, 2]].ravel()
@@ -283,12 +353,51 @@ class Laplacian:
     in CSC == L in CSR) is what the device step consumes."""
 
     def __init__(self, mat, mat_t, scheme):
-        self.mat = mat
-        self.mat_t = mat_t
+        self._mat = mat
+        self._mat_t = mat_t
         self.scheme = scheme
+        self.device = None   # device-built: {"ptr", "idx", "val_t", "val", "n"} (host copies lazy)
+
+    @classmethod
+    def _from_device(cls, n_v, ptr, idx, val_t, val, scheme="uniform"):
+        self = cls(None, None, scheme)
+        self.device = {"n": int(n_v), "ptr": ptr, "idx": idx, "val_t": val_t, "val": val}
+        return self
+
+    def _host(self, which):
+        d = self.device
+        n = d["n"]
+        nnz = int(d["idx"].numel()) if n else 0
+        ptr, idx = d["ptr"].cpu().numpy(), d["idx"][:nnz].cpu().numpy()
+        return SparseMat(n, n, ptr, idx, d[which][:nnz].cpu().numpy(), check=False)
+
+    @property
+    def mat(self):
+        if self._mat is None and self.device is not None:
+            self._mat = self._host("val")
+        return self._mat
+
+    @mat.setter
+    def mat(self, m):
+        self._mat = m
+
+    @property
+    def mat_t(self):
+        if self._mat_t is None and self.device is not None:
+            self._mat_t = self._host("val_t")
+        return self._mat_t
+
+    @mat_t.setter
+    def mat_t(self, m):
+        self._mat_t = m
+
+    @property
+    def n_vertices(self):
+        return self.device["n"] if self.device is not None else self.mat_t.n_cols
 
     def __repr__(self):
-        return f"Laplacian({self.scheme}, n={self.mat.n_rows}, nnz={self.mat.nnz})"
+        nnz = int(self.device["idx"].numel()) if self.device is not None else self.mat.nnz
+        return f"Laplacian({self.scheme}, n={self.n_vertices}, nnz={nnz})"
 
 
 def _csr_of_l(n_v, rows, cols, vals):
@@ -305,8 +414,17 @@ def build_laplacian(mesh, scheme="uniform"):
     """``uniform``: L(i,j) = 1/deg(i) on edges, -1 on the diagonal.
     ``cotan-clamped``: clamped cotangent weights, rows rescaled to sum zero,
     diagonal -1, zero-weight vertices fall back to unit weights
-    (mesh.py:379-431)."""
+    (mesh.py:379-431).  A device-built mesh gets its uniform Laplacian
+    built on the device (ft_uniform_laplacian, same bytes)."""
     n_v = mesh.n_vertices
+    topo = getattr(mesh, "_topo_dev", None)
+    if scheme == "uniform" and topo is not None:
+        deg = topo["degree"]
+        if n_v and int(deg.min().item()) == 0:
+            v = int((deg == 0).nonzero()[0, 0].item())
+            raise IsolatedVertexError(f"isolated-vertex: vertex {v} has no edges")
+        return Laplacian._from_device(n_v, *devmesh.uniform_laplacian(n_v, topo["neighbor_ptr"],
+                                                                      topo["neighbor_idx"]))
     deg = mesh.degree
     if np.any(deg == 0):
         raise IsolatedVertexError(
