@@ -72,7 +72,19 @@ STEADY_FROM = 80                                 # steady window 
 FULL_WINDOW = 120
 
 
+C4_LEVEL, C4_SEEDS = 12, 16384                   # BASELINE configs[3]: icosphere ~100M vertices
+
+
+def ico_level(args):
+    return int(args.mesh[3:]) if args.mesh.startswith("ico") else None
+
+
 def workload_name(args):
+    lv = ico_level(args)
+    if lv is not None:
+        n_v = 10 * 4 ** lv + 2
+        tag = "C4: " if (lv, args.seeds) == (C4_LEVEL, C4_SEEDS) else ""
+        return f"{tag}icosphere-{lv} ({n_v:,} vertices), {args.seeds:,} seeds, fused Euler step"
     tag = "C3: " if (args.nx, args.ny, args.seeds) == (NX, NY, N_SEEDS) else ""
     return (f"{tag}torus {args.nx}x{args.ny} ({args.nx * args.ny:,} vertices), "
             f"{args.seeds:,} seeds, fused Euler step")
@@ -93,21 +105,36 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--nx", type=int, default=NX)
     ap.add_argument("--ny", type=int, default=NY)
-    ap.add_argument("--seeds", type=int, default=N_SEEDS)
+    ap.add_argument("--mesh", default=None,
+                    help="torus (default at N=1: C3) or icoL (icosphere level L; default at N>1: "
+                         f"ico{C4_LEVEL}, C4)")
+    ap.add_argument("--seeds", type=int, default=None,
+                    help=f"default {N_SEEDS} on the torus, {C4_SEEDS} on an icosphere")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="bounded CPU-baseline sample (seconds of reference steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--emulate-ranks", type=int, default=0,
                     help="run the partitioned path with N loopback ranks on one GPU")
-    return ap.parse_args()
+    args = ap.parse_args()
+    multi = int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.emulate_ranks > 0
+    if args.mesh is None:
+        args.mesh = f"ico{C4_LEVEL}" if multi else "torus"
+    if args.mesh != "torus" and not (args.mesh.startswith("ico") and args.mesh[3:].isdigit()):
+        ap.error("--mesh must be 'torus' or 'icoL'")
+    if args.seeds is None:
+        args.seeds = N_SEEDS if args.mesh == "torus" else C4_SEEDS
+    return args
 
 
-def build_workload(nx, ny, n_seeds):
+def build_workload(args):
+    """Mesh, uniform Laplacian and seeds, built on the device (devmesh: the
+    reference's generators, bitwise) with the reference's seed sampler."""
     import paper_1804_09152_b200 as ft
-    mesh = ft.gen_periodic_grid(nx, ny)
+    lv = ico_level(args)
+    mesh = ft.gen_icosphere(lv, max_subdiv=12) if lv is not None else ft.gen_periodic_grid(args.nx, args.ny)
     lap = ft.build_laplacian(mesh)
-    seeds = ft.sample_seed_vertices(mesh, n_seeds, 0)      # == reference cli.py:183-215
+    seeds = ft.sample_seed_vertices(mesh, args.seeds, 0)      # == reference cli.py:183-215
     return mesh, lap, seeds
 
 
@@ -237,27 +264,43 @@ def run_reference_arm(args):
     if rank != 0:
         return
     import paper_1804_09152_b200 as ft
-    mesh, lap, seeds = build_workload(args.nx, args.ny, args.seeds)
+    mesh, lap, seeds = build_workload(args)
     w, start, first = window_of(args)
     cpu = ReferenceCPU(lap)
-    cpu.start(ft.init_field(mesh, seeds).phi, seeds)   # host init_field == the reference's (tested)
     t_prep = time.perf_counter()
-    for _ in range(start + w):                          # untimed: steps 1..80 (warm-up included)
-        cpu.step()
+    big = ico_level(args) is not None
+    if big:
+        # C4: the reference needs seconds per step at 168M vertices, so the
+        # untimed steps 1..80 are prepared by the GPU engine (EXACT: bitwise
+        # the reference's own state, pinned by the parity tests) and the
+        # timed sample is bounded in time
+        st, _ = ft.evolve(ft.init_field(mesh, seeds), lap, ft.CouplingParams(), max_steps=first, tol=0.0)
+        cpu.start(st.phi, seeds, first)
+        prep = "prepared by the GPU engine (bitwise the reference's state)"
+    else:
+        cpu.start(ft.init_field(mesh, seeds).phi, seeds)   # host init_field == the reference's (tested)
+        for _ in range(start + w):                          # untimed: steps 1..80 (warm-up included)
+            cpu.step()
+        prep = "run by the reference itself, untimed"
     t_prep = time.perf_counter() - t_prep
     K = max(1, args.steps)
     t0 = time.perf_counter()
-    for _ in range(K):
+    n = 0
+    while n < K:
         cpu.step()
+        n += 1
+        if big and time.perf_counter() - t0 > 6 * args.cpu_seconds:
+            break
     dt = time.perf_counter() - t0
+    K = n
     value = K / dt
-    sample = (f"{K} steps ({first + 1}..{first + K}) of {cpu.label}; steps 1..{first} untimed "
-              f"({t_prep:.0f} s); mesh / L^T / PHI0 from the bitwise-identical vectorised generators")
+    sample = (f"{K} steps ({first + 1}..{first + K}) of {cpu.label}; steps 1..{first} {prep} "
+              f"({t_prep:.0f} s); mesh / L^T / PHI0 from the bitwise-identical generators")
     line = {"impl": "reference", "metric": METRIC,
             "value": value, "unit": "steps/s", "higher_is_better": True,
             "n_gpus": args.gpus, "steps": K, "warmup": w,
             "ms_per_step": 1e3 / value, "dtype": "f64", "data": "synthetic",
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": "strong" if big and args.gpus > 1 else "weak", "vs_baseline": None,
             "config": {"workload": workload_name(args), "precision": "f64 (reference)",
                        "window": f"steps {first + 1}..{first + K} from init_field (BASELINE.md 3 steady window)"},
             "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cpu.cores, "kind": cpu.kind,
@@ -320,7 +363,7 @@ def run_ours(args):
         return float(t.item())
 
     params = ft.CouplingParams()
-    mesh, lap, seeds = build_workload(args.nx, args.ny, args.seeds)
+    mesh, lap, seeds = build_workload(args)
     n_v = mesh.n_vertices
     prec = args.precision
     vbytes = 8 if prec == "exact" else 4
@@ -425,7 +468,7 @@ def run_ours(args):
     nnz_in = [src80.nnz] + [int(r["nnz_phi"]) for r in recs[:-1]]
     nnz_out = [int(r["nnz_phi"]) for r in recs]
     skel = sum(int(r["nnz_skel"]) for r in recs)
-    nnz_l = lap.mat_t.nnz
+    nnz_l = dl.lap_t[prec].nnz
     uniform = dl.flags == _lib.FT_LAP_UNIFORM
     alg = np.array([algorithmic_bytes(n_v, nnz_l, a, b, vbytes, lap_values=not uniform)
                     for a, b in zip(nnz_in, nnz_out)], dtype=np.float64)
@@ -540,7 +583,9 @@ def run_ours(args):
             "ms_per_step": elapsed_ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64" if prec == "exact" else "f32-storage/f64-arith",
             "data": "synthetic",
-            "config": {"workload": workload_name(args), "mesh": f"torus {args.nx}x{args.ny}", "n_vertices": n_v,
+            "config": {"workload": workload_name(args),
+                       "mesh": f"torus {args.nx}x{args.ny}" if ico_level(args) is None
+                       else f"icosphere-{ico_level(args)} (reference numbering)", "n_vertices": n_v,
                        "seeds": args.seeds, "seed_sampler": "reference cli.sample_seed_vertices(mesh, n, rng=0) "
                                                             "(exact replay)",
                        "precision": prec, "laplacian": "uniform",
@@ -599,20 +644,43 @@ def run_partitioned(args, world, rank, local, emulate=0):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    nx, nyg = args.nx, args.ny * W
-    n_v = nx * nyg
-    n_seeds = args.seeds * W
-    seeds = np.random.default_rng(0).choice(n_v, n_seeds, replace=False)
-    part = D.Partition.even(n_v, W, align=nx)
+    prec = args.precision
     mine = list(range(W)) if emulate else [rank]
-    probs = [D.periodic_grid_problem(nx, nyg, seeds, part, r) for r in mine]
+    lv = ico_level(args)
+    t_setup = time.perf_counter()
+    if lv is not None:
+        # C4 (strong scaling): every rank builds the icosphere, L, the seeds
+        # and PHI0 on its own GPU (devmesh, seconds), renumbers the vertices
+        # in Morton order (compact slabs, small halos) and gathers only its
+        # owned + halo columns (local_problem_device)
+        mesh, lap, seeds = build_workload(args)
+        n_v, n_seeds = mesh.n_vertices, seeds.size
+        order = D.morton_order_device(mesh.device_arrays()[0])
+        fld = ft.init_field(mesh, seeds, precision=prec)
+        part = D.Partition.even(n_v, W)
+        probs = [D.local_problem_device(fld.device_phi(), lap, order, part, r) for r in mine]
+        del mesh, lap, fld, order
+        torch.cuda.empty_cache()
+        workload = (f"{workload_name(args)}; Morton-renumbered vertex partition over {W} ranks + halo "
+                    f"exchange (strong scaling: the same mesh at every N)")
+    else:
+        nx, nyg = args.nx, args.ny * W
+        n_v = nx * nyg
+        n_seeds = args.seeds * W
+        seeds = np.random.default_rng(0).choice(n_v, n_seeds, replace=False)
+        part = D.Partition.even(n_v, W, align=nx)
+        probs = [D.periodic_grid_problem(nx, nyg, seeds, part, r) for r in mine]
+        workload = (f"torus {nx}x{nyg} ({n_v:,} vertices), {n_seeds:,} seeds, "
+                    f"vertex row-partition over {W} ranks + halo exchange (weak scaling)")
     transport = D.LoopbackTransport() if emulate else D.TorchTransport()
     plans = D.build_plans(probs, transport)
-    prec = args.precision
     vbytes = 8 if prec == "exact" else 4
     params = ft.CouplingParams()
     ranks = [D.DomainRank(p, pl, precision=prec) for p, pl in zip(probs, plans)]
-    warm = max(3, args.warmup)
+    t_setup = time.perf_counter() - t_setup
+    warm, start, first = window_of(args)
+    if start:
+        D.evolve_partitioned(ranks, transport, params, max_steps=start, tol=0.0)
     D.evolve_partitioned(ranks, transport, params, max_steps=warm, tol=0.0)
     K = args.steps
     for r in ranks:
@@ -679,21 +747,25 @@ def run_partitioned(args, world, rank, local, emulate=0):
                "path": "DomainRank(host slab problem) -> evolve_partitioned(K steps) -> owned "
                        "field + labels on the host, per rank"}
     if rank == 0:
-        value = W * K / (elapsed_ms * 1e-3)
+        strong = lv is not None
+        value = (K if strong else W * K) / (elapsed_ms * 1e-3)
         line = {
             "metric": METRIC,
-            "value": value, "unit": "steps/s (C3-equivalent: 10M-vertex steps)", "n_gpus": world,
+            "value": value, "unit": "steps/s" if strong else "steps/s (C3-equivalent: 10M-vertex steps)",
+            "n_gpus": world,
             "steps": K, "warmup": warm, "ms_per_step": elapsed_ms / K, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": "f64" if prec == "exact" else "f32-storage/f64-arith", "data": "synthetic",
-            "config": {"workload": f"torus {nx}x{nyg} ({n_v:,} vertices), {n_seeds:,} seeds, "
-                                   f"vertex row-partition over {W} ranks + halo exchange",
+            "vertex_steps_per_s": n_v * K / (elapsed_ms * 1e-3),
+            "setup_s": t_setup,
+            "config": {"workload": workload,
                        "n_vertices": n_v, "seeds": n_seeds, "precision": prec,
                        "laplacian": "uniform", "parallelism": f"row-partition x{W} (NCCL halo)"
                        if not emulate else f"{W} loopback ranks on 1 GPU (emulated)",
                        "halo_columns_per_rank": halo_cols[0], "halo_message_bytes_per_rank": msg_bytes,
                        "l2": "working set > 126 MB L2 (no flush needed)",
-                       "window": f"steps {warm + 1}..{warm + K} from init_field"},
+                       "window": f"steps {first + 1}..{first + K} from init_field (BASELINE.md 3 steady "
+                                 f"window 81-120); warm-up steps {start + 1}..{first}"},
             "layer_nnz_updates_per_s": skel / (elapsed_ms * 1e-3),
             "kernel_ms_per_step": float(step_ms.mean()),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -465,3 +465,25 @@ def test_partitioned_lloyd_allreduce(world, morton, torus):
         assert np.allclose(a["cell_areas"], b["cell_areas"], rtol=1e-12, atol=0)
     whole = got.field.gather().phi
     _assert_same_field(whole, ref.field.phi)
+
+
+@pytest.mark.gpu
+def test_local_problem_device_matches_host_renumbering():
+    """The device Morton order and device slicing (C4 bench setup) equal the
+    host Renumbering + local_problem on the same device-built mesh."""
+    mesh = ft.gen_icosphere(5)
+    lap = ft.build_laplacian(mesh)
+    seeds = ft.sample_seed_vertices(mesh, 50, 2)
+    fld = ft.init_field(mesh, seeds)
+    order_d = D.morton_order_device(mesh.device_arrays()[0])
+    order_h = D.morton_order(mesh.positions)
+    assert np.array_equal(order_d.cpu().numpy(), order_h)
+    ren = D.Renumbering(order_h)
+    part = D.Partition.even(mesh.n_vertices, 3)
+    for r in range(3):
+        pd = D.local_problem_device(fld.device_phi(), lap, order_d, part, r)
+        ph = D.local_problem(fld.phi, lap, part, r, renumbering=ren)
+        for a in ("lap_ptr", "lap_idx", "lap_val", "cols", "col_ptr", "row_idx", "values"):
+            x, y = getattr(pd, a), getattr(ph, a)
+            assert x.dtype == y.dtype and np.array_equal(x, y), a
+        assert pd.lap_flags == ph.lap_flags and pd.symmetric and ph.symmetric
