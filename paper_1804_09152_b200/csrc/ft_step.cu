@@ -266,18 +266,47 @@ __device__ __forceinline__ void list_push(bool push, int j, int* count, int* bas
     if (push) base[q + __popc(b & ((1u << lane) - 1u))] = j;
 }
 
+// CTA-staged list: warps push into a shared buffer (shared-memory atomics);
+// list_flush moves it to the global list with one global atomic and a
+// coalesced copy (CTA-collective; call with a uniform control flow)
+struct CtaList {
+    int* buf;
+    int* cnt;
+    int* base;
+};
+
+__device__ __forceinline__ void list_flush(const CtaList& l, int* g_count, int* g_list) {
+    __syncthreads();
+    const int n = *l.cnt;
+    if (n == 0) return;
+    if (threadIdx.x == 0) *l.base = atomicAdd(g_count, n);
+    __syncthreads();
+    const int b = *l.base;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) g_list[b + k] = l.buf[k];
+    __syncthreads();
+    if (threadIdx.x == 0) *l.cnt = 0;
+    __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
-// prep_kernel: this step's stamps -> the active list (64 columns per thread
-// in four coalesced 16-byte words, byte compares with __vcmpeq4, one atomic
-// per CTA of 16384 columns); a full step only resets the target buffer's
-// pool.
+// prep_kernel: this step's stamps -> the active list.  A CTA covers
+// 8 x 2048 columns, warp w a contiguous 2048: in round r lane l reads the
+// 4-byte stamp word of columns base_w + 128 r + 4 l (coalesced) and
+// compares its bytes with __vcmpeq4, keeping a 4-bit mask per round in one
+// 64-bit register.  One atomic per CTA reserves its part of the list, the
+// warps' offsets come from one shared exchange, and each warp then places
+// its matches round by round with shuffle scans (no further CTA barrier),
+// every round one contiguous run of the list.  Nothing downstream depends
+// on the list order (the statistics are order-independent).  A full step
+// only resets the target buffer's pool.
 
 constexpr int kPrepTPB = 256;
-constexpr int kPrepCols = 64;
+constexpr int kPrepRounds = 16;
+constexpr int kPrepCols = 4 * kPrepRounds;   // columns per thread
 
 __global__ void __launch_bounds__(kPrepTPB) prep_kernel(const StepParams p) {
     pdl_wait();
-    __shared__ int s_scan[kPrepTPB / 32];
+    __shared__ int s_warp[kPrepTPB / 32];
     __shared__ int s_base;
     Control* ctl = p.ws.ctl;
     if (p.check_done && vload(&ctl->done)) return;
@@ -286,46 +315,64 @@ __global__ void __launch_bounds__(kPrepTPB) prep_kernel(const StepParams p) {
         return;
     }
     const unsigned int pat = 0x01010101u * (unsigned char)vload(&ctl->seq);
-    // owned buffer columns [g_lo, g_hi), scanned from the 64-byte aligned
-    // column below g_lo; each CTA covers 16384 columns as 1024 16-byte
-    // words, thread t reading words t, t + 256, t + 512, t + 768
-    // (coalesced), 16 columns each
+    // owned buffer columns [g_lo, g_hi), read as aligned words from g_lo & ~3
     const int g_lo = p.j_base, g_hi = p.j_base + p.n_v;
-    const int c0 = (g_lo & ~63) + blockIdx.x * (kPrepTPB * kPrepCols);
-    const uint4* s4 = reinterpret_cast<const uint4*>(p.ws.stamp + c0);   // padded to 64 bytes
-    unsigned int m[4];
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const int cw = (g_lo & ~3) + blockIdx.x * (kPrepTPB * kPrepCols) + wi * (32 * kPrepCols);
+    // all 16 loads issued before any use (clamped to the last word: the
+    // stamp array is padded past n)
+    const int last = (g_hi - 1) & ~3;
+    unsigned int x[kPrepRounds];
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-        const int jw = c0 + 16 * (threadIdx.x + v * kPrepTPB);
-        m[v] = 0;
-        if (jw < g_hi) {
-            const uint4 x = s4[threadIdx.x + v * kPrepTPB];
-            const unsigned int w[4] = {x.x, x.y, x.z, x.w};
+    for (int r = 0; r < kPrepRounds; ++r)
+        x[r] = __ldg(reinterpret_cast<const unsigned int*>(p.ws.stamp + min(cw + 128 * r + 4 * lane, last)));
+    unsigned long long mm = 0;
+    int cnt = 0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                // 0x01 per matching byte, gathered into 4 bits
-                const unsigned int e = __vcmpeq4(w[q], pat) & 0x01010101u;
-                m[v] |= ((e * 0x01020408u) >> 24) << (4 * q);
-            }
-            const int hi = g_hi - jw, lo = g_lo - jw;       // keep columns in [g_lo, g_hi)
-            if (hi < 16) m[v] &= (1u << hi) - 1u;
-            if (lo > 0) m[v] &= lo >= 16 ? 0u : ~((1u << lo) - 1u);
-        }
+    for (int r = 0; r < kPrepRounds; ++r) {
+        const int jw = cw + 128 * r + 4 * lane;
+        const unsigned int e = __vcmpeq4(x[r], pat) & 0x01010101u;   // 0x01 per matching byte
+        unsigned int m = (e * 0x01020408u) >> 24;                     // gathered into 4 bits
+        const int hi = g_hi - jw, lo = g_lo - jw;                      // keep [g_lo, g_hi)
+        if (hi < 4) m &= hi <= 0 ? 0u : (1u << hi) - 1u;
+        if (lo > 0) m &= ~((1u << lo) - 1u);
+        mm |= (unsigned long long)m << (4 * r);
+        cnt += __popc(m);
     }
-    int tot;
-    int base = block_excl_scan<kPrepTPB>(__popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]), s_scan, &tot);
-    if (tot == 0) return;
-    if (threadIdx.x == 0) s_base = atomicAdd(&ctl->n_act, tot);
-    __syncthreads();
-    base += s_base;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-        const int jw = c0 + 16 * (threadIdx.x + v * kPrepTPB);
-        unsigned int mm = m[v];
-        while (mm) {
-            const int b = __ffs(mm) - 1;
-            mm &= mm - 1;
-            p.ws.act[base++] = jw + b - g_lo;
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+    if (lane == 0) s_warp[wi] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+#pragma unroll
+        for (int k = 0; k < kPrepTPB / 32; ++k) {
+            const int c = s_warp[k];
+            s_warp[k] = t;
+            t += c;
+        }
+        s_base = t ? atomicAdd(&ctl->n_act, t) : 0;
+    }
+    __syncthreads();
+    if (cnt == 0) return;
+    int base = s_base + s_warp[wi];
+#pragma unroll
+    for (int r = 0; r < kPrepRounds; ++r) {
+        unsigned int m = (unsigned int)(mm >> (4 * r)) & 15u;
+        const int c = __popc(m);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        int pos = base + incl - c;
+        base += __shfl_sync(kFull, incl, 31);
+        const int jw = cw + 128 * r + 4 * lane;
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            p.ws.act[pos++] = jw + b - g_lo;
         }
     }
 }
@@ -348,10 +395,12 @@ __global__ void __launch_bounds__(kPrepTPB) prep_kernel(const StepParams p) {
 // reference's accumulator order.  Anything else goes to the wide list.
 
 constexpr int kBandTPB = 256;
+constexpr int kBandBuf = 1024;   // CTA-staged wide-list entries
 
 template <typename T, bool UNIFORM, bool PACKED>
 __device__ __forceinline__ void band_column(const StepParams& p, int jl, bool have, bool full, bool chk,
-                                            unsigned char nxt, int lane, Acc& acc, long long* s_bm) {
+                                            unsigned char nxt, int lane, Acc& acc, long long* s_bm,
+                                            const CtaList& wl) {
     const int j = p.j_base + jl;
     // stage 1: the packed L^T row; the column's own signature and value
     int4 pk = make_int4(0, 0, 0, 0);
@@ -490,7 +539,7 @@ __device__ __forceinline__ void band_column(const StepParams& p, int jl, bool ha
         }
     }
     __syncwarp();   // reconverge after the per-lane paths before the collectives
-    list_push(wide || (gen && more), j, &p.ws.ctl->n_wide, p.ws.wide, lane);
+    list_push(wide || (gen && more), j, wl.cnt, wl.buf, lane);
     if (fin_here) {
         acc.dn += cnt_new - (full ? 0 : cnt_old);
         acc.ds += sk_new - (full ? 0 : skc_old);
@@ -507,24 +556,30 @@ __global__ void __launch_bounds__(kBandTPB, MINB) band_kernel(const StepParams p
     __shared__ long long s_bm[4];
     __shared__ double s_md[kBandTPB / 32];
     __shared__ long long s_cnt[2 * (kBandTPB / 32)];
+    __shared__ int s_wbuf[kBandBuf];
+    __shared__ int s_wcnt, s_wbase;
     if (p.check_done && vload(&ctl->done)) return;
     if (threadIdx.x < 4) s_bm[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_wcnt = 0;
     __syncthreads();
+    const CtaList wl{s_wbuf, &s_wcnt, &s_wbase};
     const bool full = step_is_full(p);
     const int n_act = full ? p.n_v : vload(&ctl->n_act);
     const bool chk = p.force_check || vload(&ctl->nonfinite);
     const unsigned char nxt = (unsigned char)(vload(&ctl->seq) + 1);
     const int lane = threadIdx.x & 31;
-    const int nw = gridDim.x * (kBandTPB / 32);
     Acc acc;
     acc_init(acc);
-    for (int base = ((blockIdx.x * kBandTPB + threadIdx.x) >> 5) * 32; base < n_act; base += nw * 32) {
-        const int i = base + lane;
+    // CTA-uniform chunks of kBandTPB columns (the list flush is collective)
+    for (int c = blockIdx.x * kBandTPB; c < n_act; c += gridDim.x * kBandTPB) {
+        const int i = c + threadIdx.x;
         const bool have = i < n_act;
         const int jl = have ? (full ? i : __ldg(&p.ws.act[i])) : 0;
-        band_column<T, UNIFORM, PACKED>(p, jl, have, full, chk, nxt, lane, acc, s_bm);
+        band_column<T, UNIFORM, PACKED>(p, jl, have, full, chk, nxt, lane, acc, s_bm, wl);
+        __syncthreads();
+        if (s_wcnt > kBandBuf - kBandTPB) list_flush(wl, &ctl->n_wide, p.ws.wide);
     }
-    __syncthreads();
+    list_flush(wl, &ctl->n_wide, p.ws.wide);
     acc_flush<kBandTPB>(acc, s_bm, s_md, s_cnt, ctl);
 }
 
@@ -735,9 +790,12 @@ __device__ __forceinline__ void wide3_column(const StepParams& p, int j, bool ha
 }
 
 constexpr int kWide3TPB = 128;
+#ifndef FT_W3_MINB
+#define FT_W3_MINB 4
+#endif
 
 template <typename T, bool UNIFORM, bool PACKED>
-__global__ void __launch_bounds__(kWide3TPB, 4) wide3_kernel(const StepParams p) {
+__global__ void __launch_bounds__(kWide3TPB, FT_W3_MINB) wide3_kernel(const StepParams p) {
     pdl_wait();
     Control* ctl = p.ws.ctl;
     __shared__ long long s_bm[4];
@@ -1798,7 +1856,7 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     DevState& d = dev_state();
     const char* kenv = getenv("FT_KERNELS");   // debug: bit mask of the column kernels to launch
     const int kmask = kenv ? atoi(kenv) : 15;
-    const int prep_span = n_own + (j_base & 63);
+    const int prep_span = n_own + (j_base & 3);   // aligned words from j_base & ~3
     const int prep_grid = (prep_span + ft::kPrepCols * ft::kPrepTPB - 1) / (ft::kPrepCols * ft::kPrepTPB);
     if (kmask & 1) launch_dep(ft::prep_kernel, prep_grid, ft::kPrepTPB, s, p);
     if (ev) cudaEventRecord(ev[0], s);
@@ -1816,7 +1874,8 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
         launch_dep(FT_PICK3(ft::band_kernel, dtype, uni, packed), bg, ft::kBandTPB, s, p);
     }
     if (ev) cudaEventRecord(ev[1], s);
-    if (kmask & 4) launch_dep(FT_PICK3(ft::wide3_kernel, dtype, uni, packed), 4 * d.sms, ft::kWide3TPB, s, p);
+    if (kmask & 4)
+        launch_dep(FT_PICK3(ft::wide3_kernel, dtype, uni, packed), FT_W3_MINB * d.sms, ft::kWide3TPB, s, p);
     if (ev) cudaEventRecord(ev[2], s);
     if (kmask & 8) {
         launch_dep(FT_PICK3(ft::wide_kernel, dtype, uni, packed), 8 * d.sms, ft::kWideTPB, s, p);

@@ -453,8 +453,8 @@ def device_laplacian(lap, precision):
                                             ex.values.to(_value_dtype(precision)), ex.nnz)
         else:
             dl.lap_t[precision] = DeviceCSC.from_host(dl.host, _value_dtype(precision), _device())
-        if dl.pack is None and dl.flags == _lib.FT_LAP_UNIFORM and PACK_LAPLACIAN:
-            dl.pack, dl.n_csr = pack_laplacian(dl.lap_t[precision])
+    if dl.pack is None and dl.flags == _lib.FT_LAP_UNIFORM and PACK_LAPLACIAN:
+        dl.pack, dl.n_csr = pack_laplacian(dl.lap_t[precision])
     return dl
 
 

@@ -94,6 +94,8 @@ def test_device_mesh_evolve_matches_host_mesh(monkeypatch):
     ld = ft.build_laplacian(d)
     out_d, tr_d = ft.evolve(ft.init_field(d, seeds), ld, ft.CouplingParams(), max_steps=60, tol=0.0)
     assert ld._mat_t is None, "the device Laplacian was copied to the host"
+    from paper_1804_09152_b200 import field as F
+    assert F.device_laplacian(ld, "exact").pack is not None, "uniform device Laplacian not packed"
     out_h, tr_h = ft.evolve(ft.init_field(h, seeds), ft.build_laplacian(h), ft.CouplingParams(), max_steps=60,
                             tol=0.0)
     a, b = out_d.phi, out_h.phi
