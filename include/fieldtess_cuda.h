@@ -378,19 +378,21 @@ int ft_uniform_laplacian(int32_t n_v, const int64_t* nptr, const int32_t* nidx, 
 /* General-purpose versions of the operations the Euler step fuses, bitwise
  * equal to the numba kernels (values FT_F64 only).  spgemm C = A B is
  * expand-sort-compress:
- *   ft_spgemm_count   counts[j] = sum over u in B(:, j) of nnz(A(:, u))
- *                     (spgemm_bounds, _kernels.py:14-23);
- *   ft_spgemm_expand  every product A(r, u) B(u, j) with key j * n_rows(A) + r
- *                     at offsets[j].., in the reference's order (u ascending,
+ *   ft_spgemm_count   counts[p] = nnz(A(:, u)) for every entry p (row u) of
+ *                     B, nnz_b = nnz(B) (spgemm_bounds, _kernels.py:14-23,
+ *                     per entry: the work is parallel over B's entries);
+ *   ft_spgemm_expand  with offsets = the exclusive scan of those counts,
+ *                     every product A(r, u) B(u, j) with key j * n_rows(A) + r
+ *                     at offsets[p].., in the reference's order (u ascending,
  *                     then r);
  *   (the caller sorts the keys with a STABLE sort, carrying the values)
  *   ft_segment_sums   the sequential sum of every run of equal keys (starts =
  *                     the first index of each run), first term assigned as in
  *                     spgemm_numeric (_kernels.py:26-62); the caller drops
  *                     exact zeros and builds col_ptr from the keys. */
-int ft_spgemm_count(const ft_csc* a, const ft_csc* b, int64_t* counts, void* stream);
-int ft_spgemm_expand(const ft_csc* a, const ft_csc* b, const int64_t* offsets, int64_t* keys,
-                     double* vals, void* stream);
+int ft_spgemm_count(const ft_csc* a, const ft_csc* b, int64_t nnz_b, int64_t* counts, void* stream);
+int ft_spgemm_expand(const ft_csc* a, const ft_csc* b, int64_t nnz_b, const int64_t* offsets,
+                     int64_t* keys, double* vals, void* stream);
 int ft_segment_sums(const double* vals, int64_t n, const int64_t* starts, int64_t n_seg,
                     double* sums, void* stream);
 /* Interest skeleton of (phi, lt) (build_skeleton, sparse.py:345-371;

@@ -176,9 +176,9 @@ def _declare(lib):
     lib.ft_laplacian_pack.restype = ctypes.c_int
     lib.ft_point_triangle_distances.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, vp]
     lib.ft_point_triangle_distances.restype = ctypes.c_int
-    lib.ft_spgemm_count.argtypes = [P(FtCsc), P(FtCsc), vp, vp]
+    lib.ft_spgemm_count.argtypes = [P(FtCsc), P(FtCsc), ctypes.c_int64, vp, vp]
     lib.ft_spgemm_count.restype = ctypes.c_int
-    lib.ft_spgemm_expand.argtypes = [P(FtCsc), P(FtCsc), vp, vp, vp, vp]
+    lib.ft_spgemm_expand.argtypes = [P(FtCsc), P(FtCsc), ctypes.c_int64, vp, vp, vp, vp]
     lib.ft_spgemm_expand.restype = ctypes.c_int
     lib.ft_segment_sums.argtypes = [vp, ctypes.c_int64, vp, ctypes.c_int64, vp, vp]
     lib.ft_segment_sums.restype = ctypes.c_int

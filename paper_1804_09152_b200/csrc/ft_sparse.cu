@@ -7,8 +7,9 @@
 // Every floating-point reduction keeps the reference's order, so results are
 // bitwise those of the numba kernels.
 //
-// spgemm is expand-sort-compress: ft_spgemm_expand writes every product
-// A(r, u) * B(u, j) with the key j * n_rows + r in the reference's
+// spgemm is expand-sort-compress, parallel over the entries of B (any
+// shape of B, a single column included): ft_spgemm_expand writes every
+// product A(r, u) * B(u, j) with the key j * n_rows + r in the reference's
 // generation order (u ascending over B(:, j), then r over A(:, u)); the host
 // sorts the keys with a STABLE sort, so the products of one (r, j) stay in
 // generation order, and ft_segment_sums adds each run sequentially -- the
@@ -21,34 +22,40 @@
 
 namespace ft {
 
-__global__ void spgemm_count_kernel(const int* __restrict__ a_ptr, const int* __restrict__ b_ptr,
-                                    const int* __restrict__ b_idx, int n_cols, long long* __restrict__ counts) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n_cols) return;
-    long long t = 0;
-    for (int p = b_ptr[j]; p < b_ptr[j + 1]; ++p) {
-        const int u = b_idx[p];
-        t += a_ptr[u + 1] - a_ptr[u];
-    }
-    counts[j] = t;
+// one thread per entry p of B (column j, row u): counts[p] = nnz(A(:, u))
+__global__ void spgemm_count_kernel(const int* __restrict__ a_ptr, const int* __restrict__ b_idx, long long nnz_b,
+                                    long long* __restrict__ counts) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nnz_b) return;
+    const int u = b_idx[p];
+    counts[p] = a_ptr[u + 1] - a_ptr[u];
 }
 
+// entry p of B (column j) writes the products A(r, u) B(u, j), r over A(:, u),
+// at off[p]..: with off the exclusive scan of the counts in B's entry order
+// the products of column j follow u ascending, then r -- the reference's
+// generation order -- whatever the shape of B (a single column included)
 __global__ void spgemm_expand_kernel(const int* __restrict__ a_ptr, const int* __restrict__ a_idx,
                                      const double* __restrict__ a_val, const int* __restrict__ b_ptr,
                                      const int* __restrict__ b_idx, const double* __restrict__ b_val, int n_cols,
-                                     long long n_rows, const long long* __restrict__ off, long long* __restrict__ keys,
-                                     double* __restrict__ vals) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n_cols) return;
-    long long w = off[j];
-    for (int p = b_ptr[j]; p < b_ptr[j + 1]; ++p) {
-        const int u = b_idx[p];
-        const double bv = b_val[p];
-        for (int q = a_ptr[u]; q < a_ptr[u + 1]; ++q) {
-            keys[w] = (long long)j * n_rows + a_idx[q];
-            vals[w] = a_val[q] * bv;
-            ++w;
-        }
+                                     long long nnz_b, long long n_rows, const long long* __restrict__ off,
+                                     long long* __restrict__ keys, double* __restrict__ vals) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nnz_b) return;
+    // the column of entry p: the last j with b_ptr[j] <= p
+    int lo = 0, hi = n_cols;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (b_ptr[mid] <= p) lo = mid; else hi = mid;
+    }
+    const int u = b_idx[p];
+    const double bv = b_val[p];
+    long long w = off[p];
+    const long long kb = (long long)lo * n_rows;
+    for (int q = a_ptr[u]; q < a_ptr[u + 1]; ++q) {
+        keys[w] = kb + a_idx[q];
+        vals[w] = a_val[q] * bv;
+        ++w;
     }
 }
 
@@ -140,24 +147,24 @@ static int grid_of(long long n, int tpb) { return (int)((n + tpb - 1) / tpb); }
 
 static int launch_ok() { return cudaGetLastError() == cudaSuccess ? FT_OK : FT_ERR_CUDA; }
 
-extern "C" int ft_spgemm_count(const ft_csc* a, const ft_csc* b, int64_t* counts, void* stream) {
-    if (!a || !b || !counts) return FT_ERR_ARG;
+extern "C" int ft_spgemm_count(const ft_csc* a, const ft_csc* b, int64_t nnz_b, int64_t* counts, void* stream) {
+    if (!a || !b || !counts || nnz_b < 0 || nnz_b > b->capacity) return FT_ERR_ARG;
     if (a->n_cols != b->n_rows) return FT_ERR_SHAPE;
-    if (b->n_cols > 0)
-        ft::spgemm_count_kernel<<<grid_of(b->n_cols, 256), 256, 0, (cudaStream_t)stream>>>(
-            a->col_ptr, b->col_ptr, b->row_idx, b->n_cols, (long long*)counts);
+    if (nnz_b > 0)
+        ft::spgemm_count_kernel<<<grid_of(nnz_b, 256), 256, 0, (cudaStream_t)stream>>>(
+            a->col_ptr, b->row_idx, nnz_b, (long long*)counts);
     return launch_ok();
 }
 
-extern "C" int ft_spgemm_expand(const ft_csc* a, const ft_csc* b, const int64_t* offsets, int64_t* keys,
-                                double* vals, void* stream) {
-    if (!a || !b || !offsets || !keys || !vals) return FT_ERR_ARG;
+extern "C" int ft_spgemm_expand(const ft_csc* a, const ft_csc* b, int64_t nnz_b, const int64_t* offsets,
+                                int64_t* keys, double* vals, void* stream) {
+    if (!a || !b || !offsets || !keys || !vals || nnz_b < 0 || nnz_b > b->capacity) return FT_ERR_ARG;
     if (a->n_cols != b->n_rows) return FT_ERR_SHAPE;
     const long long nr = a->n_rows > 0 ? a->n_rows : 1;
-    if (b->n_cols > 0)
-        ft::spgemm_expand_kernel<<<grid_of(b->n_cols, 256), 256, 0, (cudaStream_t)stream>>>(
+    if (nnz_b > 0 && b->n_cols > 0)
+        ft::spgemm_expand_kernel<<<grid_of(nnz_b, 256), 256, 0, (cudaStream_t)stream>>>(
             a->col_ptr, a->row_idx, (const double*)a->values, b->col_ptr, b->row_idx, (const double*)b->values,
-            b->n_cols, nr, (const long long*)offsets, (long long*)keys, vals);
+            b->n_cols, nnz_b, nr, (const long long*)offsets, (long long*)keys, vals);
     return launch_ok();
 }
 

@@ -479,11 +479,13 @@ def spgemm(a, b, out=None, scratch=None):
     dev = _dev()
     da, db = _upload64(a, dev), _upload64(b, dev)
     ca, cb = da.ft_csc(), db.ft_csc()
-    counts = torch.zeros(max(n_cols, 1), dtype=torch.int64, device=dev)
-    _lib_call("ft_spgemm_count", ctypes.byref(ca), ctypes.byref(cb), ctypes.c_void_p(counts.data_ptr()), _stream())
-    off = torch.zeros(n_cols + 1, dtype=torch.int64, device=dev)
-    if n_cols:
-        torch.cumsum(counts[:n_cols], 0, out=off[1:])
+    nnz_b = db.nnz
+    counts = torch.zeros(max(nnz_b, 1), dtype=torch.int64, device=dev)
+    _lib_call("ft_spgemm_count", ctypes.byref(ca), ctypes.byref(cb), nnz_b, ctypes.c_void_p(counts.data_ptr()),
+              _stream())
+    off = torch.zeros(nnz_b + 1, dtype=torch.int64, device=dev)
+    if nnz_b:
+        torch.cumsum(counts[:nnz_b], 0, out=off[1:])
     total = int(off[-1].item())
     col_ptr = np.zeros(n_cols + 1, dtype=INDEX)
     rows = np.zeros(0, dtype=INDEX)
@@ -491,7 +493,7 @@ def spgemm(a, b, out=None, scratch=None):
     if total:
         scratch = scratch if scratch is not None else SpgemmScratch()
         keys, pv = scratch.buffers(total, dev)
-        _lib_call("ft_spgemm_expand", ctypes.byref(ca), ctypes.byref(cb), ctypes.c_void_p(off.data_ptr()),
+        _lib_call("ft_spgemm_expand", ctypes.byref(ca), ctypes.byref(cb), nnz_b, ctypes.c_void_p(off.data_ptr()),
                   ctypes.c_void_p(keys.data_ptr()), ctypes.c_void_p(pv.data_ptr()), _stream())
         sk, perm = torch.sort(keys, stable=True)
         sv = pv[perm]

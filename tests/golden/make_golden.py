@@ -32,6 +32,8 @@ c1_s10.field / c1_s10.trip  save_field / write_triplets output of the
                  reference (C1 at step 10) for snapshot compatibility.
 dual_warnings.json  confirm_candidates warnings (degenerate face, NaN
                  layer value) of the reference on a modified C1.
+c5_lloyd.json    (--only c5, ~10 min) C5 reduced window: 2 Lloyd iterations
+                 at max_steps 100 on the 10M torus with 65,536 seeds + dual.
 --only a,b: regenerate only the named groups (seeds_collide, analysis).
 """
 
@@ -415,6 +417,55 @@ def make_c2(seeds_c2):
     print("c2_lloyd", f"{time.time() - t0:.1f}s")
 
 
+def make_c5():
+    """C5 (BASELINE configs[4]) on a reduced window: torus 3200 x 3125
+    (10M vertices), 65,536 seeds (the exact replay of cli.sample_seed_vertices,
+    pinned by seeds.json), lloyd_iterate n_iter=2 with max_steps=100 (C5's
+    Lloyd definition: at the default max_steps=1000 a cell vanishes), then
+    the dual mesh at threshold 0.25.  Digests only (the arrays are large)."""
+    import hashlib
+    from fieldtess.lloyd import LloydState, lloyd_iterate
+    from fieldtess import dual as dualmod
+    sys.path.insert(0, REPO)
+    from paper_1804_09152_b200.seeding import sample_seed_vertices as replay
+    dig = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+    t0 = time.time()
+    mesh = ft.gen_periodic_grid(3200, 3125)
+    lap = ft.build_laplacian(mesh, "uniform")
+    seeds = replay(mesh, 65536, 0)
+    print("c5 setup", f"{time.time() - t0:.1f}s", flush=True)
+    t1 = time.time()
+    state = lloyd_iterate(LloydState(seeds=np.asarray(seeds)), mesh, lap, ft.CouplingParams(), n_iter=2,
+                          max_steps=100)
+    t_lloyd = time.time() - t1
+    hist = [{"iteration": r["iteration"], "seeds_sha": dig(np.asarray(r["seeds"], dtype=np.int64)),
+             "seeds_head": [int(x) for x in r["seeds"][:16]], "area_variance": r["area_variance"],
+             "cell_areas_sha": dig(np.asarray(r["cell_areas"], dtype=np.float64)), "steps": r["steps"],
+             "converged": r["converged"], "reseed_misses": r["reseed_misses"],
+             "seed_collisions": r["seed_collisions"]} for r in state.history]
+    print("c5 lloyd", f"{t_lloyd:.1f}s", flush=True)
+    t2 = time.time()
+    fld = state.field
+    phi = fld.phi
+    a_v = dualmod.vertex_adjacency(fld, 0.25)
+    a_t = dualmod.triangle_adjacency(fld, mesh, 0.25)
+    cur = dualmod.confirm_candidates(fld, mesh, a_v, a_t, 0.25)
+    pos = mesh.positions[np.asarray(fld.seed_vertices, dtype=np.int64)]
+    dm = dualmod.build_dual(cur, pos)
+    pairs = np.asarray(sorted(cur.pairs()), dtype=np.int64)
+    out = {"history": hist, "lloyd_wall_s": t_lloyd, "dual_wall_s": time.time() - t2,
+           "phi_sha": {"col_ptr": dig(np.asarray(phi.col_ptr, dtype=np.int32)),
+                       "row_idx": dig(np.asarray(phi.row_idx[:phi.nnz], dtype=np.int32)),
+                       "values": dig(np.asarray(phi.values[:phi.nnz], dtype=np.float64))},
+           "dual": {"n_pairs": int(pairs.shape[0]), "pairs_sha": dig(pairs),
+                    "n_triangles": int(dm.triangles.shape[0]),
+                    "triangles_sha": dig(np.asarray(dm.triangles, dtype=np.int64)),
+                    "n_dropped": len(cur.dropped), "spurious_removed": len(dm.spurious_removed)}}
+    with open(os.path.join(HERE, "c5_lloyd.json"), "w") as fh:
+        json.dump(out, fh)
+    print("c5 dual", f"{time.time() - t2:.1f}s", flush=True)
+
+
 def make_seed_collisions():
     out = {}
     for name, mesh, count, seed in [("t20x15", ft.gen_periodic_grid(20, 15), 280, 3),
@@ -478,7 +529,7 @@ def main():
         for name in sys.argv[sys.argv.index("--only") + 1].split(","):
             {"seeds_collide": make_seed_collisions, "analysis": make_analysis,
              "winding": make_dual_winding, "snapshots": make_snapshots,
-             "dual_warnings": make_dual_warnings}[name]()
+             "dual_warnings": make_dual_warnings, "c5": make_c5}[name]()
         return
     make_step_cases()
     make_labels_cases()

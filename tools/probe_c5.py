@@ -1,47 +1,41 @@
-"""C5-scale run: 10M-vertex torus, 65,536 seeds -- evolve, one Lloyd
-centroid / back-projection pass, dual extraction (BASELINE configs[4]).
+"""C5 (BASELINE configs[4]): torus 3200 x 3125 (10M vertices), 65,536 seeds
+(reference sampler), Lloyd iterations with a given max_steps, then the dual
+mesh.  Reports per-iteration seconds, misses / collisions / area variance,
+and where a cell vanishes.
 
-A full Lloyd iteration at this density stops in the reference's own
-_reseed (lloyd.py:155-195) with VanishedCellError: ~14% of the cells vanish
-within 1000 steps (C2's reference history shows 16% misses at iteration 1)
-and, among 65,536 cells, a vanished cell's old seed is soon taken by
-another cell's new seed.  This probe times each GPU stage instead."""
-import sys, time
+usage: python tools/probe_c5.py [max_steps] [iterations] [tol]"""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1804_09152_b200 as ft
-from paper_1804_09152_b200 import dual as DU, lloyd as L
 
-max_steps = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
-t = time.time()
+M = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
+IT = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+TOL = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-4
+t0 = time.time()
 mesh = ft.gen_periodic_grid(3200, 3125)
 lap = ft.build_laplacian(mesh)
-print(f"mesh + laplacian {time.time() - t:.1f} s", flush=True)
-t = time.time()
 seeds = ft.sample_seed_vertices(mesh, 65536, 0)
-print(f"seed sampler (65,536 seeds) {time.time() - t:.2f} s", flush=True)
-fld0 = ft.init_field(mesh, seeds)
-ft.evolve(fld0, lap, ft.CouplingParams(), max_steps=5)
-torch.cuda.synchronize(); t = time.time()
-fld, tr = ft.evolve(fld0, lap, ft.CouplingParams(), max_steps=max_steps)
-torch.cuda.synchronize()
-print(f"evolve {len(tr)} steps: {time.time() - t:.2f} s ({len(tr) / (time.time() - t):.0f} steps/s), "
-      f"nnz {fld.device_phi().nnz}, band vertex fraction {ft.band_vertex_fraction(fld):.3f}", flush=True)
-for rep in range(2):
-    torch.cuda.synchronize(); t = time.time()
-    pts, nrm, status, hit = L.cell_geometry(fld, mesh, seeds=np.asarray(seeds))
-    torch.cuda.synchronize()
-    print(f"lloyd centroids + back-projection (all cells): {time.time() - t:.3f} s, "
-          f"vanished {int((status == 1).sum())}, misses {int((hit < 0).sum())}", flush=True)
-for rep in range(2):
-    t = time.time()
-    a_v = DU.vertex_adjacency(fld, 0.25)
-    a_t = DU.triangle_adjacency(fld, mesh, 0.25)
-    cur = DU.confirm_candidates(fld, mesh, a_v, a_t, 0.25)
-    t1 = time.time()
-    try:
-        dm = DU.build_dual(cur, mesh.positions[seeds])
-        out = f"{len(dm.triangles)} triangles"
-    except ft.errors.NonManifoldError as exc:     # the reference's own check (dual.py)
-        out = f"NonManifoldError ({str(exc)[:60]}...)"
-    print(f"dual: products + curation {t1 - t:.2f} s, triangulation {time.time() - t1:.2f} s, {out}",
-          flush=True)
+print(f"setup {time.time() - t0:.1f} s", flush=True)
+st = ft.LloydState(seeds=seeds)
+t = time.time()
+try:
+    for it in range(IT):
+        ft.lloyd_iterate(st, mesh, lap, ft.CouplingParams(), 1, max_steps=M, tol=TOL)
+        torch.cuda.synchronize()
+        h = st.history[-1]
+        print(f"iter {h['iteration']:2d}: {time.time() - t:7.2f} s steps {h['steps']} conv {h['converged']} "
+              f"misses {h['reseed_misses']} coll {h['seed_collisions']} var {h['area_variance']:.6g}", flush=True)
+        t = time.time()
+except Exception as exc:
+    print("FAILED:", type(exc).__name__, exc, flush=True)
+    sys.exit(0)
+t = time.time()
+fld = st.field
+a_v = ft.vertex_adjacency(fld, 0.25)
+a_t = ft.triangle_adjacency(fld, mesh, 0.25)
+cur = ft.confirm_candidates(fld, mesh, a_v, a_t, 0.25)
+pos = mesh.positions[np.asarray(fld.seed_vertices, dtype=np.int64)]
+dm = ft.build_dual(cur, pos)
+print(f"dual: {len(cur.pairs())} edges, {dm.triangles.shape[0]} triangles, chi {dm.euler_characteristic()}, "
+      f"{time.time() - t:.2f} s", flush=True)
