@@ -397,12 +397,27 @@ def run_ours(args):
     e_end = torch.cuda.Event(enable_timing=True)
 
     def evolve_dev(src_dev, steps):
-        s_c = src_dev.ft_csc()
-        rc = lib.ft_evolve(ctypes.byref(lap_c), flags, ctypes.byref(s_c), ctypes.byref(ta_c),
-                           ctypes.byref(tb_c), ctypes.byref(out_c), dt_code, ctypes.byref(prm), steps, 0.0, 0.0,
+        s_c, a_c, b_c = src_dev.ft_csc(), ta.ft_tiled(), tb.ft_tiled()
+        rc = lib.ft_evolve(ctypes.byref(lap_c), flags, ctypes.byref(s_c), ctypes.byref(a_c),
+                           ctypes.byref(b_c), ctypes.byref(out_c), dt_code, ctypes.byref(prm), steps, 0.0, 0.0,
                            wp, wn, ctypes.c_void_p(trace.data_ptr()), ctypes.c_void_p(ev_ctl.data_ptr()), sh)
         if rc:
             raise RuntimeError(_lib.last_error())
+
+    def fit_pools(src_dev, steps):
+        """Untimed run of a window; grows the work buffers' pools until it
+        completes (a window from init_field can need a larger pool than the
+        step-80 state the buffers were sized for)."""
+        for _ in range(12):
+            evolve_dev(src_dev, steps)
+            torch.cuda.synchronize()
+            ctl = ev_ctl.cpu().numpy()
+            if int(ctl[1]) != _lib.FT_STATUS_OVERFLOW:
+                return
+            need = int(ctl[2]) + int(ctl[2]) // 2
+            ta.grow(need)
+            tb.grow(need)
+        raise RuntimeError("work-buffer pools did not converge")
 
     def check_evolve(steps, what):
         ctl = ev_ctl.cpu().numpy()
@@ -416,6 +431,7 @@ def run_ours(args):
 
     # ---- warm-up: W steps (80-W+1 .. 80) through the timed call itself;
     # the first call also captures the evolve graph
+    fit_pools(src, max(W, K))
     evolve_dev(src, W)
     torch.cuda.synchronize()
     check_evolve(W, "warm-up")
@@ -445,6 +461,7 @@ def run_ours(args):
     krec = torch.zeros(K * _lib.STATS_BYTES, dtype=torch.uint8, device=dev)
     evk = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     s80 = src80.ft_csc()
+    ta_c, tb_c = ta.ft_tiled(), tb.ft_tiled()      # the pools may have grown
     if lib.ft_tiled_from_csc(ctypes.byref(s80), ctypes.byref(tb_c), dt_code, wp, wn,
                              ctypes.c_void_p(comp_rec.data_ptr()), sh):
         raise RuntimeError(_lib.last_error())
@@ -489,6 +506,7 @@ def run_ours(args):
 
     # ---- the full window 1..120 from init_field (same buffers, graph warm)
     d0 = fld0.device_phi()
+    fit_pools(d0, FULL_WINDOW)
     torch.cuda.synchronize()
     e_start.record(stream)
     evolve_dev(d0, FULL_WINDOW)

@@ -7,7 +7,8 @@ import numpy as np, torch
 import paper_1804_09152_b200 as ft
 mesh = ft.gen_periodic_grid(3200, 3125)
 lap = ft.build_laplacian(mesh)
-seeds = ft.sample_seed_vertices(mesh, 4096, 0)
+NS = int(os.environ.get("AB_SEEDS", "4096"))
+seeds = ft.sample_seed_vertices(mesh, NS, 0)
 prm = ft.CouplingParams()
 st80, _ = ft.evolve(ft.init_field(mesh, seeds), lap, prm, max_steps=80, tol=0.0)
 best = None
@@ -19,5 +20,6 @@ for r in range(5):
     ms = e0.elapsed_time(e1)
     best = ms if best is None else min(best, ms)
 sig = hash(tuple((t.nnz_phi, t.max_delta) for t in tr))
-print(json.dumps({"lib": os.environ.get("FT_LIB", "default"), "steps_per_s": 40 / (best * 1e-3),
+print(json.dumps({"lib": os.environ.get("FT_LIB", "default"), "seeds": NS,
+                  "env": {k: v for k, v in os.environ.items() if k.startswith("FT_")}, "steps_per_s": 40 / (best * 1e-3),
                   "ms_per_step": best / 40, "trace_sig": sig}))
