@@ -1091,112 +1091,200 @@ __device__ __forceinline__ void staged_column(const StepParams& p, int j, WideSt
         if (lane == 0) p.ws.act[atomicAdd(&p.ws.ctl->n_deep, 1)] = j;
         return;
     }
-    // 2. rank by (row, staging order)
-    for (int e = lane; e < E; e += 32) {
-        const int r = st.row[e];
-        int rank = 0;
-        for (int f = 0; f < E; ++f) {
-            const int rf = st.row[f];
-            rank += (rf < r || (rf == r && f < e)) ? 1 : 0;
-        }
-        st.order[rank] = (short)e;
-    }
-    __syncwarp();
-    // 3. one slot per distinct row: Lt in L order, PHI(r, j)
-    int M = 0;
-    for (int k0 = 0; k0 < E; k0 += 32) {
-        const int k = k0 + lane;
-        bool head = false;
-        int r = 0;
-        if (k < E) {
-            r = st.row[st.order[k]];
-            head = k == 0 || st.row[st.order[k - 1]] != r;
-        }
-        int tot;
-        const int m = M + warp_excl_scan(head ? 1 : 0, lane, tot);
-        if (head) {
-            double lam = 0.0, phv = 0.0;
-            for (int kk = k; kk < E; ++kk) {
-                const int e = st.order[kk];
-                if (st.row[e] != r) break;
-                lam = lam + st.prod[e];
-                if (st.diag[e]) phv = st.ph[e];
-            }
-            st.rrow[m] = r;
-            st.rlam[m] = lam;
-            st.rphi[m] = phv;
-        }
-        M += tot;
-    }
-    __syncwarp();
-    // 4. skeleton, aggregates in ascending row order (every lane, from smem)
     Agg g;
     agg_init(g);
-    for (int m = 0; m < M; ++m) {
-        const double ph = st.rphi[m], lm = st.rlam[m];
-        const bool in = in_skeleton(ph, lm);
-        if (ph != 0.0 && !in) g.bad_phi_row = st.rrow[m];
-        if (lm != 0.0 && !in) g.bad_lt_row = st.rrow[m];
-        if (in) {
-            if (g.n == 0) { g.first_row = st.rrow[m]; g.phi0 = ph; }
-            g.n++;
-            g.sl = g.sl + ((lm != 0.0) ? lm : 0.0);
-            g.sp = g.sp + ph;
-            g.sr = g.sr + sqrt(ph);
-        }
-    }
-    const Coef c = make_coef(g, p.cp, c_recip);
-    bool nan = false;
-    for (int m = lane; m < M; m += 32) {
-        const double ph = st.rphi[m], lm = st.rlam[m];
-        const bool in = in_skeleton(ph, lm);
-        bool nl = false;
-        const double v = update_entry(in ? st.rrow[m] : 1, in ? ph : 0.0, (in && lm != 0.0) ? lm : 0.0, c, p.cp, nl);
-        st.rv[m] = in ? v : 0.0;
-        nan |= in && nl;
-    }
-    __syncwarp();
-    double s = 0.0;
-    for (int m = 0; m < M; ++m)
-        if (in_skeleton(st.rphi[m], st.rlam[m])) s = s + st.rv[m];
-    const bool spos = s > 0.0;
-    const double inv = 1.0 / (spos ? s : 1.0);
-    // 5. normalise, output positions, the change test against the old column
+    int M = 0, cnt = 0;
+    double md = 0.0, bm_new = 0.0;
+    bool changed = false, anynan = false;
     const int so = __ldg(&p.in.sig[j]);
     const int co = sig_count(so);
     const int ao = co >= 2 ? __ldg(&p.in.aux[j]) : 0;
-    int cnt = 0;
-    double md = 0.0, bm_new = 0.0;
-    bool mism = false;
-    for (int m0 = 0; m0 < M; m0 += 32) {
-        const int m = m0 + lane;
-        bool out = false;
-        double nv = 0.0, ph = 0.0;
-        int r = 0;
-        if (m < M) {
-            ph = st.rphi[m];
-            r = st.rrow[m];
-            const bool in = in_skeleton(ph, st.rlam[m]);
-            nv = spos ? st.rv[m] * inv : st.rv[m];
-            out = in && nv != 0.0;
-            if (in) md = fmax(md, fabs(nv - ph));
-            st.rv[m] = nv;
+    if (E <= 32) {
+        // 2-5 with one staged entry per lane: rows grouped by __match_any_sync
+        // (a row's entries are its group's lanes in staging = L order), one
+        // lane per distinct row, the row-order sums by shuffles in order --
+        // the same additions in the same order as the general path below
+        const bool valid = lane < E;
+        const int r = valid ? st.row[lane] : INT_MAX;
+        const unsigned vm = __ballot_sync(kFull, valid);
+        const unsigned grp = __match_any_sync(kFull, r) & vm;
+        const bool leader = valid && (__ffs(grp) - 1 == lane);
+        const unsigned L = __ballot_sync(kFull, leader);
+        M = __popc(L);
+        int rank = 0;
+        for (unsigned mm = L; mm; mm &= mm - 1) {
+            const int rb = __shfl_sync(kFull, r, __ffs(mm) - 1);
+            rank += (leader && rb < r) ? 1 : 0;
         }
-        int tot;
-        const int pos = cnt + warp_excl_scan(out ? 1 : 0, lane, tot);
-        if (m < M) st.rpos[m] = out ? pos : -1;
+        if (leader) {
+            double lam = 0.0, phv = 0.0;
+            for (unsigned gg = grp; gg; gg &= gg - 1) {
+                const int e = __ffs(gg) - 1;
+                lam = lam + st.prod[e];
+                if (st.diag[e]) phv = st.ph[e];
+            }
+            st.rrow[rank] = r;
+            st.rlam[rank] = lam;
+            st.rphi[rank] = phv;
+        }
+        __syncwarp();
+        // lane m now owns distinct row m (ascending)
+        const bool hv = lane < M;
+        const int row = hv ? st.rrow[lane] : 0;
+        const double ph = hv ? st.rphi[lane] : 0.0, lm = hv ? st.rlam[lane] : 0.0;
+        const bool in = hv && in_skeleton(ph, lm);
+        const unsigned bpm = __ballot_sync(kFull, hv && ph != 0.0 && !in);
+        const unsigned blm = __ballot_sync(kFull, hv && lm != 0.0 && !in);
+        const int bpr = __shfl_sync(kFull, row, bpm ? 31 - __clz(bpm) : 0);   // the last such row
+        const int blr = __shfl_sync(kFull, row, blm ? 31 - __clz(blm) : 0);
+        if (bpm) g.bad_phi_row = bpr;
+        if (blm) g.bad_lt_row = blr;
+        const unsigned im = __ballot_sync(kFull, in);
+        const double lh = (in && lm != 0.0) ? lm : 0.0;
+        const double sq = in ? sqrt(ph) : 0.0;
+        g.n = __popc(im);
+        if (im) {
+            const int f0 = __ffs(im) - 1;
+            g.first_row = __shfl_sync(kFull, row, f0);
+            g.phi0 = __shfl_sync(kFull, ph, f0);
+        }
+        for (unsigned mm = im; mm; mm &= mm - 1) {   // ascending rows, sequential sums
+            const int b = __ffs(mm) - 1;
+            g.sl = g.sl + __shfl_sync(kFull, lh, b);
+            g.sp = g.sp + __shfl_sync(kFull, ph, b);
+            g.sr = g.sr + __shfl_sync(kFull, sq, b);
+        }
+        const Coef c = make_coef(g, p.cp, c_recip);
+        bool nl = false;
+        const double v = in ? update_entry_sq(row, ph, lh, sq, c, p.cp, nl) : 0.0;
+        anynan = __any_sync(kFull, in && nl);
+        double s = 0.0;
+        for (unsigned mm = im; mm; mm &= mm - 1) s = s + __shfl_sync(kFull, v, __ffs(mm) - 1);
+        const bool spos = s > 0.0;
+        const double inv = 1.0 / (spos ? s : 1.0);
+        const double nv = spos ? v * inv : v;
+        const bool out = in && nv != 0.0;
+        if (in) md = fabs(nv - ph);
+        const unsigned om = __ballot_sync(kFull, out);
+        const int pos = __popc(om & ((1u << lane) - 1u));
+        cnt = __popc(om);
+        if (hv) {
+            st.rv[lane] = nv;
+            st.rpos[lane] = out ? pos : -1;
+        }
+        bool mism = false;
         if (out) {
-            if (r == 0) bm_new = nv;
-            mism |= pos >= co || hyb_row<T>(p.in, so, ao, pos) != r || !same_bits<T>(nv, hyb_val<T>(p.in, j, so, ao, pos));
+            if (row == 0) bm_new = nv;
+            mism = pos >= co || hyb_row<T>(p.in, so, ao, pos) != row ||
+                   !same_bits<T>(nv, hyb_val<T>(p.in, j, so, ao, pos));
         }
-        cnt += tot;
-    }
-    const bool changed = cnt != co || __any_sync(kFull, mism);
-    const bool anynan = __any_sync(kFull, nan);
+        changed = cnt != co || __any_sync(kFull, mism);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        md = fmax(md, __shfl_xor_sync(kFull, md, o));
-        bm_new = bm_new + __shfl_xor_sync(kFull, bm_new, o);   // at most one nonzero term: exact
+        for (int o = 16; o > 0; o >>= 1) {
+            md = fmax(md, __shfl_xor_sync(kFull, md, o));
+            bm_new = bm_new + __shfl_xor_sync(kFull, bm_new, o);   // at most one nonzero term: exact
+        }
+    } else {
+        // 2. rank by (row, staging order)
+        for (int e = lane; e < E; e += 32) {
+            const int r = st.row[e];
+            int rank = 0;
+            for (int f = 0; f < E; ++f) {
+                const int rf = st.row[f];
+                rank += (rf < r || (rf == r && f < e)) ? 1 : 0;
+            }
+            st.order[rank] = (short)e;
+        }
+        __syncwarp();
+        // 3. one slot per distinct row: Lt in L order, PHI(r, j)
+        for (int k0 = 0; k0 < E; k0 += 32) {
+            const int k = k0 + lane;
+            bool head = false;
+            int r = 0;
+            if (k < E) {
+                r = st.row[st.order[k]];
+                head = k == 0 || st.row[st.order[k - 1]] != r;
+            }
+            int tot;
+            const int m = M + warp_excl_scan(head ? 1 : 0, lane, tot);
+            if (head) {
+                double lam = 0.0, phv = 0.0;
+                for (int kk = k; kk < E; ++kk) {
+                    const int e = st.order[kk];
+                    if (st.row[e] != r) break;
+                    lam = lam + st.prod[e];
+                    if (st.diag[e]) phv = st.ph[e];
+                }
+                st.rrow[m] = r;
+                st.rlam[m] = lam;
+                st.rphi[m] = phv;
+            }
+            M += tot;
+        }
+        __syncwarp();
+        // 4. skeleton, aggregates in ascending row order (every lane, from smem)
+        for (int m = 0; m < M; ++m) {
+            const double ph = st.rphi[m], lm = st.rlam[m];
+            const bool in = in_skeleton(ph, lm);
+            if (ph != 0.0 && !in) g.bad_phi_row = st.rrow[m];
+            if (lm != 0.0 && !in) g.bad_lt_row = st.rrow[m];
+            if (in) {
+                if (g.n == 0) { g.first_row = st.rrow[m]; g.phi0 = ph; }
+                g.n++;
+                g.sl = g.sl + ((lm != 0.0) ? lm : 0.0);
+                g.sp = g.sp + ph;
+                g.sr = g.sr + sqrt(ph);
+            }
+        }
+        const Coef c = make_coef(g, p.cp, c_recip);
+        bool nan = false;
+        for (int m = lane; m < M; m += 32) {
+            const double ph = st.rphi[m], lm = st.rlam[m];
+            const bool in = in_skeleton(ph, lm);
+            bool nl = false;
+            const double v = update_entry(in ? st.rrow[m] : 1, in ? ph : 0.0, (in && lm != 0.0) ? lm : 0.0, c, p.cp, nl);
+            st.rv[m] = in ? v : 0.0;
+            nan |= in && nl;
+        }
+        __syncwarp();
+        double s = 0.0;
+        for (int m = 0; m < M; ++m)
+            if (in_skeleton(st.rphi[m], st.rlam[m])) s = s + st.rv[m];
+        const bool spos = s > 0.0;
+        const double inv = 1.0 / (spos ? s : 1.0);
+        // 5. normalise, output positions, the change test against the old column
+        bool mism = false;
+        for (int m0 = 0; m0 < M; m0 += 32) {
+            const int m = m0 + lane;
+            bool out = false;
+            double nv = 0.0, ph = 0.0;
+            int r = 0;
+            if (m < M) {
+                ph = st.rphi[m];
+                r = st.rrow[m];
+                const bool in = in_skeleton(ph, st.rlam[m]);
+                nv = spos ? st.rv[m] * inv : st.rv[m];
+                out = in && nv != 0.0;
+                if (in) md = fmax(md, fabs(nv - ph));
+                st.rv[m] = nv;
+            }
+            int tot;
+            const int pos = cnt + warp_excl_scan(out ? 1 : 0, lane, tot);
+            if (m < M) st.rpos[m] = out ? pos : -1;
+            if (out) {
+                if (r == 0) bm_new = nv;
+                mism |= pos >= co || hyb_row<T>(p.in, so, ao, pos) != r || !same_bits<T>(nv, hyb_val<T>(p.in, j, so, ao, pos));
+            }
+            cnt += tot;
+        }
+        changed = cnt != co || __any_sync(kFull, mism);
+        anynan = __any_sync(kFull, nan);
+    #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            md = fmax(md, __shfl_xor_sync(kFull, md, o));
+            bm_new = bm_new + __shfl_xor_sync(kFull, bm_new, o);   // at most one nonzero term: exact
+        }
+        __syncwarp();
     }
     __syncwarp();
     // 6. statistics, pool placement, emit, marks
