@@ -373,6 +373,14 @@ def run_ours(args):
     # untimed: steps 1..80-W through the public API
     cur = ft.evolve(fld0, lap, params, max_steps=start, tol=0.0)[0] if start > 0 else fld0
     src = cur.device_phi()
+    # an unstructured device mesh's Laplacian carries the locality (Morton)
+    # order that evolve() runs long windows in: the timed device loop uses it
+    # too (fields permuted in untimed; the CPU / e2e legs see the caller's
+    # numbering)
+    perm = F.device_laplacian(lap, prec).renum if K >= F.LOCALITY_MIN_STEPS else None
+    to_dev = (lambda d: F._permute_columns(d, perm.order)) if perm is not None else (lambda d: d)
+    to_caller = (lambda d: F._permute_columns(d, perm.inverse)) if perm is not None else (lambda d: d)
+    src = to_dev(src)
     dev = src.values.device
     ws = ft.StepWorkspace()
     ws.prepare(n_v, dev)
@@ -381,6 +389,8 @@ def run_ours(args):
     tb = ft.DeviceTiled(src.n_rows, n_v, cap, src.values.dtype, dev)
     out = ft.DeviceCSC.allocate(src.n_rows, n_v, 3 * src.nnz, src.values.dtype, dev)
     dl = F.device_laplacian(lap, prec)
+    if perm is not None:
+        dl = perm
     lib = _lib.lib()
     lap_c = dl.ft_csc(prec)
     flags = dl.launch_flags()
@@ -505,7 +515,7 @@ def run_ours(args):
             pass
 
     # ---- the full window 1..120 from init_field (same buffers, graph warm)
-    d0 = fld0.device_phi()
+    d0 = to_dev(fld0.device_phi())
     fit_pools(d0, FULL_WINDOW)
     torch.cuda.synchronize()
     e_start.record(stream)
@@ -519,7 +529,7 @@ def run_ours(args):
     # evolve(K) -> field + labels on the host
     e2e = None
     if not args.no_e2e:
-        host0 = ft.LayeredField(src80, seeds, step_count=first).phi
+        host0 = ft.LayeredField(to_caller(src80), seeds, step_count=first).phi
         nnz0 = host0.nnz
         pinned = [torch.empty(a.size, dtype=t, pin_memory=True)
                   for a, t in ((host0.col_ptr, torch.int32), (host0.row_idx[:nnz0], torch.int32),
@@ -562,7 +572,8 @@ def run_ours(args):
     cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rcpu = ReferenceCPU(lap)
-        snap = ft.LayeredField(src80, seeds, step_count=first).phi   # EXACT: bitwise the reference's state
+        src80c = to_caller(src80)
+        snap = ft.LayeredField(src80c, seeds, step_count=first).phi   # EXACT: bitwise the reference's state
         rcpu.start(snap, seeds, first)
         n = 0
         t0 = time.perf_counter()
@@ -574,7 +585,7 @@ def run_ours(args):
         dt = time.perf_counter() - t0
         cpu = {"value": n / dt, "unit": "steps/s", "cores": rcpu.cores, "kind": rcpu.kind,
                "sample": f"{n} steps ({first + 1}..{first + n}) of {rcpu.label}, from the GPU's step-{first} field"}
-        gpu_n, _ = ft.evolve(ft.LayeredField(src80, seeds, step_count=first), lap, params, max_steps=n, tol=0.0)
+        gpu_n, _ = ft.evolve(ft.LayeredField(src80c, seeds, step_count=first), lap, params, max_steps=n, tol=0.0)
         g = gpu_n.phi
         rp, ri, rv = rcpu.arrays()
         gp, gi, gv = np.asarray(g.col_ptr), np.asarray(g.row_idx[:g.nnz]), np.asarray(g.values[:g.nnz])
@@ -617,7 +628,9 @@ def run_ours(args):
             "layer_nnz_updates_per_s": world * skel / (elapsed_ms * 1e-3),
             "kernel_ms_per_step": float(kern_ms.mean()),
             "timed_path": "ft_evolve (the evolve() device loop: active-set steps in CUDA-graph chunks), "
-                          "resident canonical input -> K steps -> canonical output",
+                          "resident canonical input -> K steps -> canonical output" +
+                          (" (vertices in the Laplacian's Morton order, as evolve() runs them)"
+                           if perm is not None else ""),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note,
                          "kernel": "one Euler step's column kernels (active list, band kernel, wide kernels), "

@@ -260,39 +260,7 @@ class Renumbering:
         return int(self.order[k]) if k >= 0 else k
 
 
-def _spread3_device(x):
-    x = x & 0x1FFFFF
-    for shift, mask in ((32, 0x1F00000000FFFF), (16, 0x1F0000FF0000FF), (8, 0x100F00F00F00F00F),
-                        (4, 0x10C30C30C30C30C3), (2, 0x1249249249249249)):
-        x = (x | (x << shift)) & mask
-    return x
-
-
-def morton_order_device(positions):
-    """:func:`morton_order` of a device (n, 3) float64 position tensor (same
-    codes, same stable order), for meshes built on the device."""
-    torch = _torch()
-    lo = positions.min(dim=0).values
-    span = float((positions.max(dim=0).values - lo).max().item()) or 1.0
-    q = torch.floor((positions - lo) / span * (2 ** 21 - 1)).long()
-    code = _spread3_device(q[:, 0]) | (_spread3_device(q[:, 1]) << 1) | (_spread3_device(q[:, 2]) << 2)
-    return torch.argsort(code, stable=True)
-
-
-def _gather_columns(ptr, cols):
-    """(new_ptr, src) of the CSC columns ``cols`` of a matrix with column
-    pointers ``ptr`` (device tensors): src = the entry positions in column
-    order, entries kept in stored order."""
-    torch = _torch()
-    p = ptr.long()
-    start = p[cols]
-    cnt = p[cols + 1] - start
-    new_ptr = torch.zeros(cols.numel() + 1, dtype=torch.int64, device=ptr.device)
-    torch.cumsum(cnt, 0, out=new_ptr[1:])
-    total = int(new_ptr[-1].item())
-    src = (torch.repeat_interleave(start - new_ptr[:-1], cnt, output_size=total)
-           + torch.arange(total, device=ptr.device))
-    return new_ptr, src
+from .devmesh import gather_columns as _gather_columns, morton_order_device  # noqa: E402,F401
 
 
 def local_problem_device(phi, lap, order, partition, rank):

@@ -328,6 +328,7 @@ class _DeviceLap:
         self.symmetric = symmetric   # pattern of L^T symmetric: active-set stepping
         self.pack = None       # packed neighbour table (uniform Laplacians)
         self.n_csr = 0         # columns the pack leaves to the CSR
+        self.renum = None      # the same Laplacian in a locality order (device meshes), or None
 
     def launch_flags(self):
         f = self.flags | (_lib.FT_LAP_PACKED if self.pack is not None else 0)
@@ -435,6 +436,20 @@ def device_laplacian(lap, precision):
             dl.host = None
             n, nnz = dev["n"], int(dev["idx"].numel())
             dl.lap_t["exact"] = DeviceCSC(n, n, dev["ptr"], dev["idx"], dev["val_t"], nnz)
+            if dev.get("order") is not None:
+                torch = _torch()
+                from .devmesh import gather_columns
+                order = dev["order"]
+                inverse = torch.empty_like(order)
+                inverse[order] = torch.arange(order.numel(), device=order.device)
+                ptr, src = gather_columns(dev["ptr"], order)
+                r = _DeviceLap({}, _lib.FT_LAP_UNIFORM, n, symmetric=True)
+                r.host = None
+                r.lap_t["exact"] = DeviceCSC(n, n, ptr.to(torch.int32),
+                                             inverse[dev["idx"][src].long()].to(torch.int32).contiguous(),
+                                             dev["val_t"][src].contiguous(), nnz)
+                r.order, r.inverse = order, inverse
+                dl.renum = r
         else:
             mat_t = _with_diagonal(lap.mat_t)
             flags = _lib.FT_LAP_UNIFORM if _uniform_values_exact(mat_t) else _lib.FT_LAP_EXPLICIT
@@ -446,15 +461,18 @@ def device_laplacian(lap, precision):
         except AttributeError:
             pass
     dl = cache[1]
-    if precision not in dl.lap_t:
-        if dl.host is None:
-            ex = dl.lap_t["exact"]
-            dl.lap_t[precision] = DeviceCSC(ex.n_rows, ex.n_cols, ex.col_ptr, ex.row_idx,
-                                            ex.values.to(_value_dtype(precision)), ex.nnz)
-        else:
-            dl.lap_t[precision] = DeviceCSC.from_host(dl.host, _value_dtype(precision), _device())
-    if dl.pack is None and dl.flags == _lib.FT_LAP_UNIFORM and PACK_LAPLACIAN:
-        dl.pack, dl.n_csr = pack_laplacian(dl.lap_t[precision])
+    for d in (dl, getattr(dl, "renum", None)):
+        if d is None:
+            continue
+        if precision not in d.lap_t:
+            if d.host is None:
+                ex = d.lap_t["exact"]
+                d.lap_t[precision] = DeviceCSC(ex.n_rows, ex.n_cols, ex.col_ptr, ex.row_idx,
+                                               ex.values.to(_value_dtype(precision)), ex.nnz)
+            else:
+                d.lap_t[precision] = DeviceCSC.from_host(d.host, _value_dtype(precision), _device())
+        if d.pack is None and d.flags == _lib.FT_LAP_UNIFORM and PACK_LAPLACIAN:
+            d.pack, d.n_csr = pack_laplacian(d.lap_t[precision])
     return dl
 
 
@@ -675,7 +693,20 @@ def _evolve_host(field, lap, params, max_steps, tol, ws, on_step, base_threshold
     return cur, trace
 
 
-def _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold):
+LOCALITY_MIN_STEPS = 8     # evolve calls this long run in the Laplacian's locality order
+
+
+def _permute_columns(d, cols):
+    """A DeviceCSC with column k = column cols[k] of ``d`` (entries kept)."""
+    from .devmesh import gather_columns
+    ptr, src = gather_columns(d.col_ptr, cols)
+    nnz = int(ptr[-1].item())
+    keep = max(nnz, 1)
+    return DeviceCSC(d.n_rows, d.n_cols, ptr.to(d.col_ptr.dtype), d.row_idx[src][:keep].contiguous(),
+                     d.values[src][:keep].contiguous(), nnz)
+
+
+def _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold, locality=True):
     torch = _torch()
     n_v = field.n_vertices
     if _lap_size(lap) != n_v:
@@ -683,6 +714,14 @@ def _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold):
     src = field.device_phi()
     device = src.values.device
     dl = device_laplacian(lap, field.precision)
+    # a device-built unstructured mesh's Laplacian carries a Morton order:
+    # long evolves run with the vertices renumbered (compact one-ring
+    # gathers), the field permuted in and out; L^T keeps each column's entry
+    # order, so every value is bitwise the same (DESIGN 8b)
+    ren = getattr(dl, "renum", None) if locality and max_steps >= LOCALITY_MIN_STEPS else None
+    if ren is not None:
+        src = _permute_columns(src, ren.order)
+        dl = ren
     ws.prepare(n_v, device)
     wa = ws.tiled_buffer("a", src, src.nnz)
     wb = ws.tiled_buffer("b", src, src.nnz)
@@ -735,6 +774,8 @@ def _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold):
                 ws.spare = cur
             cur = out
         if status in (_lib.FT_STATUS_NAN, _lib.FT_STATUS_PATTERN):
+            if ren is not None:     # report in the caller's numbering: rerun unpermuted
+                return _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold, locality=False)
             _raise_step_error(recs[n], field.step_count + done)
         if status == _lib.FT_STATUS_OVERFLOW:
             need = int(recs[n]["needed"])
@@ -747,7 +788,12 @@ def _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold):
         break
     if trace:
         trace[-1].realloc_count = reallocs
-    if cur is src:                      # no step completed (cannot happen without error)
+    if ren is not None:
+        back = _permute_columns(cur, ren.inverse)
+        if cur is not src and ws.recycle:
+            ws.spare = cur
+        cur = back
+    elif cur is src:                    # no step completed (cannot happen without error)
         cur = src.clone()
     return LayeredField(cur, field.seed_vertices, field.step_count + done), trace
 

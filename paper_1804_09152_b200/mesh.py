@@ -423,8 +423,13 @@ def build_laplacian(mesh, scheme="uniform"):
         if n_v and int(deg.min().item()) == 0:
             v = int((deg == 0).nonzero()[0, 0].item())
             raise IsolatedVertexError(f"isolated-vertex: vertex {v} has no edges")
-        return Laplacian._from_device(n_v, *devmesh.uniform_laplacian(n_v, topo["neighbor_ptr"],
-                                                                      topo["neighbor_idx"]))
+        lap = Laplacian._from_device(n_v, *devmesh.uniform_laplacian(n_v, topo["neighbor_ptr"],
+                                                                     topo["neighbor_idx"]))
+        if not mesh.periodic and n_v >= devmesh.LOCALITY_MIN_VERTICES:
+            # the engine's locality order for long evolves (the caller's
+            # numbering is kept at the API: field.evolve permutes in and out)
+            lap.device["order"] = devmesh.morton_order_device(mesh._cache["dev_positions"])
+        return lap
     deg = mesh.degree
     if np.any(deg == 0):
         raise IsolatedVertexError(

@@ -451,16 +451,21 @@ def make_c5():
     a_t = dualmod.triangle_adjacency(fld, mesh, 0.25)
     cur = dualmod.confirm_candidates(fld, mesh, a_v, a_t, 0.25)
     pos = mesh.positions[np.asarray(fld.seed_vertices, dtype=np.int64)]
-    dm = dualmod.build_dual(cur, pos)
+    try:
+        dm = dualmod.build_dual(cur, pos)
+        dual_error = None
+    except ft.TessError as exc:          # the reference's own verdict is the golden
+        dm, dual_error = None, {"type": type(exc).__name__, "message": str(exc)}
     pairs = np.asarray(sorted(cur.pairs()), dtype=np.int64)
     out = {"history": hist, "lloyd_wall_s": t_lloyd, "dual_wall_s": time.time() - t2,
            "phi_sha": {"col_ptr": dig(np.asarray(phi.col_ptr, dtype=np.int32)),
                        "row_idx": dig(np.asarray(phi.row_idx[:phi.nnz], dtype=np.int32)),
                        "values": dig(np.asarray(phi.values[:phi.nnz], dtype=np.float64))},
            "dual": {"n_pairs": int(pairs.shape[0]), "pairs_sha": dig(pairs),
-                    "n_triangles": int(dm.triangles.shape[0]),
-                    "triangles_sha": dig(np.asarray(dm.triangles, dtype=np.int64)),
-                    "n_dropped": len(cur.dropped), "spurious_removed": len(dm.spurious_removed)}}
+                    "n_dropped": len(cur.dropped), "error": dual_error,
+                    "n_triangles": None if dm is None else int(dm.triangles.shape[0]),
+                    "triangles_sha": None if dm is None else dig(np.asarray(dm.triangles, dtype=np.int64)),
+                    "spurious_removed": None if dm is None else len(dm.spurious_removed)}}
     with open(os.path.join(HERE, "c5_lloyd.json"), "w") as fh:
         json.dump(out, fh)
     print("c5 dual", f"{time.time() - t2:.1f}s", flush=True)

@@ -108,3 +108,39 @@ def test_device_mesh_lloyd_geometry_reused():
     from paper_1804_09152_b200.lloyd import device_mesh
     dm = device_mesh(m)
     assert dm.positions.data_ptr() == m.device_arrays()[0].data_ptr()
+
+
+def test_locality_order_evolve_is_bitwise(monkeypatch):
+    """A device-built unstructured mesh's Laplacian carries a Morton order;
+    evolve runs permuted and returns the caller's numbering: the field and
+    trace equal the unpermuted run bitwise, and an error (a NaN input: the
+    pattern check fires first, as in the reference) reports the same
+    column as without the order."""
+    from paper_1804_09152_b200 import devmesh, field as F
+    monkeypatch.setattr(devmesh, "LOCALITY_MIN_VERTICES", 0)
+    mesh = ft.gen_icosphere(5)
+    lap = ft.build_laplacian(mesh)
+    assert lap.device.get("order") is not None
+    seeds = ft.sample_seed_vertices(mesh, 80, 1)
+    fld = ft.init_field(mesh, seeds)
+    assert F.device_laplacian(lap, "exact").renum is not None
+    out, tr = ft.evolve(fld, lap, ft.CouplingParams(), max_steps=60, tol=0.0)
+    monkeypatch.setattr(F, "LOCALITY_MIN_STEPS", 10 ** 9)       # the plain path
+    ref, rtr = ft.evolve(fld, lap, ft.CouplingParams(), max_steps=60, tol=0.0)
+    a, b = out.phi, ref.phi
+    assert np.array_equal(a.col_ptr, b.col_ptr) and np.array_equal(a.row_idx[:a.nnz], b.row_idx[:b.nnz])
+    assert a.values[:a.nnz].tobytes() == b.values[:b.nnz].tobytes()
+    assert [s.max_delta for s in tr] == [s.max_delta for s in rtr]
+    assert [s.nnz_skel for s in tr] == [s.nnz_skel for s in rtr]
+    # an error is reported in the caller's numbering
+    phi = ref.phi
+    vals = np.array(phi.values[:phi.nnz])
+    vals[phi.nnz // 2] = np.nan
+    bad = ft.LayeredField(ft.SparseMat(phi.n_rows, phi.n_cols, phi.col_ptr, phi.row_idx[:phi.nnz], vals,
+                                       check=False), seeds, step_count=60)
+    with pytest.raises(ft.TessError) as plain:
+        ft.evolve(bad, lap, ft.CouplingParams(), max_steps=20, tol=0.0)
+    monkeypatch.setattr(F, "LOCALITY_MIN_STEPS", 8)
+    with pytest.raises(ft.TessError) as permuted:
+        ft.evolve(bad, lap, ft.CouplingParams(), max_steps=20, tol=0.0)
+    assert type(permuted.value) is type(plain.value) and str(permuted.value) == str(plain.value)

@@ -90,3 +90,51 @@ def test_lloyd_c2_five_iterations_match_reference():
         assert got["reseed_misses"] == want["reseed_misses"]
         assert got["seed_collisions"] == want["seed_collisions"]
         assert got["area_variance"] == want["area_variance"]
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_c5_reduced_window_matches_reference():
+    """C5 (10M-vertex torus, 65,536 seeds; BASELINE configs[4]) on the
+    reduced window the reference runs in minutes here: lloyd_iterate with
+    n_iter=2 at max_steps=100 (C5's Lloyd definition, DESIGN 8b), then the
+    dual at threshold 0.25.  Every iteration's seeds and cell areas, the
+    final field and the dual's curated pairs and triangles (or the
+    reference's own error) equal the reference's (tests/golden/c5_lloyd.json,
+    SHA-256 digests; ref lloyd.py:198-229, dual.py:316-391)."""
+    import hashlib
+    ref = golden_json("c5_lloyd.json")
+    dig = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+    mesh = ft.gen_periodic_grid(3200, 3125)
+    lap = ft.build_laplacian(mesh)
+    seeds = ft.sample_seed_vertices(mesh, 65536, 0)
+    state = ft.lloyd_iterate(ft.LloydState(seeds=seeds), mesh, lap, ft.CouplingParams(), 2, max_steps=100)
+    assert len(state.history) == len(ref["history"])
+    for got, want in zip(state.history, ref["history"]):
+        assert got["iteration"] == want["iteration"]
+        assert dig(np.asarray(got["seeds"], dtype=np.int64)) == want["seeds_sha"]
+        assert dig(np.asarray(got["cell_areas"], dtype=np.float64)) == want["cell_areas_sha"]
+        assert got["area_variance"] == want["area_variance"]
+        assert (got["steps"], got["converged"]) == (want["steps"], want["converged"])
+        assert (got["reseed_misses"], got["seed_collisions"]) == (want["reseed_misses"], want["seed_collisions"])
+    phi = state.field.phi
+    assert dig(np.asarray(phi.col_ptr, dtype=np.int32)) == ref["phi_sha"]["col_ptr"]
+    assert dig(np.asarray(phi.row_idx[:phi.nnz], dtype=np.int32)) == ref["phi_sha"]["row_idx"]
+    assert dig(np.asarray(phi.values[:phi.nnz], dtype=np.float64)) == ref["phi_sha"]["values"]
+    fld = state.field
+    cur = ft.confirm_candidates(fld, mesh, ft.vertex_adjacency(fld, 0.25), ft.triangle_adjacency(fld, mesh, 0.25),
+                                0.25)
+    want = ref["dual"]
+    pairs = np.asarray(sorted(cur.pairs()), dtype=np.int64)
+    assert pairs.shape[0] == want["n_pairs"] and dig(pairs) == want["pairs_sha"]
+    assert len(cur.dropped) == want["n_dropped"]
+    pos = mesh.positions[np.asarray(fld.seed_vertices, dtype=np.int64)]
+    if want["error"] is not None:
+        with pytest.raises(ft.TessError) as exc:
+            ft.build_dual(cur, pos)
+        assert type(exc.value).__name__ == want["error"]["type"]
+        assert str(exc.value) == want["error"]["message"]
+    else:
+        dm = ft.build_dual(cur, pos)
+        assert dm.triangles.shape[0] == want["n_triangles"]
+        assert dig(np.asarray(dm.triangles, dtype=np.int64)) == want["triangles_sha"]
