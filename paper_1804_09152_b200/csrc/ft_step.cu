@@ -489,9 +489,12 @@ __device__ __forceinline__ void band_column(const StepParams& p, int jl, bool ha
             rhi = max(rhi, max(x[k], ax[k]));
         }
         const int lo = (int)rlo;          // -1 when the neighbourhood is empty
+        // a third row: a first row strictly between lo and rhi, or a second
+        // row below rhi (absent entries, -1, compare as the largest unsigned)
+        const unsigned span = rhi > lo ? (unsigned)(rhi - lo - 1) : 0u;
 #pragma unroll
         for (int k = 0; k < kMD; ++k)
-            more |= (x[k] >= 0 && x[k] != lo && x[k] != rhi) || (ax[k] >= 0 && ax[k] != rhi);
+            more |= ((unsigned)(x[k] - lo - 1) < span) | ((unsigned)ax[k] < (unsigned)rhi);
         // Lt(lo, j), Lt(rhi, j) in L order (the reference's accumulator
         // order): every slot adds its coefficient times L(j, u), the
         // coefficient 0 when the slot holds no entry of that row -- adding

@@ -79,3 +79,23 @@ def test_fast_mode_single_step_c3():
     flip = np.isin(keys, kg) != np.isin(keys, kr)
     assert np.all(np.maximum(np.abs(a), np.abs(b))[flip] < 1e-6)
     assert np.all(np.abs(a - b) <= 1e-5 * np.abs(b) + 2e-7)
+
+
+def test_icosphere_locality_order_bitwise():
+    """An unstructured mesh at scale through evolve's locality order
+    (icosphere-10, 10.5M vertices, device-built: the Laplacian carries a
+    Morton order, the field is permuted in and out, the packed table falls
+    back to the CSR where the renumbered deltas do not fit int16): 12 steps
+    bitwise against the C oracle in the caller's numbering."""
+    from paper_1804_09152_b200 import field as F
+    mesh = ft.gen_icosphere(10, max_subdiv=10)
+    lap = ft.build_laplacian(mesh)
+    assert lap.device is not None and lap.device.get("order") is not None
+    assert F.device_laplacian(lap, "exact").renum is not None
+    seeds = ft.sample_seed_vertices(mesh, 16384, 0)
+    fld = ft.init_field(mesh, seeds)
+    out, trace = ft.evolve(fld, lap, DEFAULT, max_steps=12, tol=0.0)
+    ref, rtrace = po.evolve_c(po.Csc.of(fld.phi), po.Csc.of(lap.mat_t), DEFAULT, 12, n_threads=THREADS)
+    assert_csc_equal(out.phi, ref)
+    assert [s.max_delta for s in trace] == [r["max_delta"] for r in rtrace]
+    assert [s.nnz_skel for s in trace] == [r["nnz_skel"] for r in rtrace]
