@@ -400,11 +400,10 @@ constexpr int kBandBuf = 1024;   // CTA-staged wide-list entries
 template <typename T, bool UNIFORM, bool PACKED>
 __device__ __forceinline__ void band_column(const StepParams& p, int jl, bool have, bool full, bool chk,
                                             unsigned char nxt, int lane, Acc& acc, long long* s_bm,
-                                            const CtaList& wl) {
+                                            const CtaList& wl, int4 pk) {
     const int j = p.j_base + jl;
-    // stage 1: the packed L^T row; the column's own signature and value
-    int4 pk = make_int4(0, 0, 0, 0);
-    if (PACKED && have) pk = __ldg(&p.lap_pack[jl]);
+    // stage 1: the packed L^T row (prefetched by the caller); the column's
+    // own signature and value
     const double phs = have ? ldv<T>(p.in.v0, j) : 0.0;
     const int sgj = have ? __ldg(&p.in.sig[j]) : FT_SIG_EMPTY;
     int q0 = 0;
@@ -573,14 +572,27 @@ __global__ void __launch_bounds__(kBandTPB, MINB) band_kernel(const StepParams p
     const int lane = threadIdx.x & 31;
     Acc acc;
     acc_init(acc);
-    // CTA-uniform chunks of kBandTPB columns (the list flush is collective)
-    for (int c = blockIdx.x * kBandTPB; c < n_act; c += gridDim.x * kBandTPB) {
-        const int i = c + threadIdx.x;
-        const bool have = i < n_act;
-        const int jl = have ? (full ? i : __ldg(&p.ws.act[i])) : 0;
-        band_column<T, UNIFORM, PACKED>(p, jl, have, full, chk, nxt, lane, acc, s_bm, wl);
+    // CTA-uniform chunks of kBandTPB columns (the list flush is collective);
+    // the next chunk's column index and packed L row are loaded before the
+    // current chunk is processed, taking two levels off its load chain
+    const int stride = gridDim.x * kBandTPB;
+    int c = blockIdx.x * kBandTPB;
+    bool have = c + (int)threadIdx.x < n_act;
+    int jl = have ? (full ? c + (int)threadIdx.x : __ldg(&p.ws.act[c + threadIdx.x])) : 0;
+    int4 pk = make_int4(0, 0, 0, 0);
+    if (PACKED && have) pk = __ldg(&p.lap_pack[jl]);
+    for (; c < n_act; c += stride) {
+        const int in = c + stride + (int)threadIdx.x;
+        const bool hn = in < n_act;
+        const int jn = hn ? (full ? in : __ldg(&p.ws.act[in])) : 0;
+        int4 pn = make_int4(0, 0, 0, 0);
+        if (PACKED && hn) pn = __ldg(&p.lap_pack[jn]);
+        band_column<T, UNIFORM, PACKED>(p, jl, have, full, chk, nxt, lane, acc, s_bm, wl, pk);
         __syncthreads();
         if (s_wcnt > kBandBuf - kBandTPB) list_flush(wl, &ctl->n_wide, p.ws.wide);
+        have = hn;
+        jl = jn;
+        pk = pn;
     }
     list_flush(wl, &ctl->n_wide, p.ws.wide);
     acc_flush<kBandTPB>(acc, s_bm, s_md, s_cnt, ctl);
