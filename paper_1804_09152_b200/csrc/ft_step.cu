@@ -1060,6 +1060,15 @@ template <typename T, bool UNIFORM, bool PACKED>
 __device__ __forceinline__ void staged_column(const StepParams& p, int j, WideStage& st, bool full,
                                               unsigned char nxt, int lane, Acc& acc, long long* s_bm) {
     const int jl = j - p.j_base;
+    // lane 0's bookkeeping loads, issued now so they overlap the staging:
+    // the column's last skeleton size and its slot in the target buffer
+    // (pool range reuse)
+    int skc_pre = 0, osig = 0, oaux = 0;
+    if (lane == 0) {
+        skc_pre = full ? 0 : p.ws.skc[jl];
+        osig = p.out.sig[j];
+        oaux = p.out.aux[j];
+    }
     // the L^T column: the packed row (lanes 0..7) or the CSR
     int n = 0, q0 = 0, pu = -1;
     if (PACKED) {
@@ -1310,11 +1319,11 @@ __device__ __forceinline__ void staged_column(const StepParams& p, int j, WideSt
         res.nan = anynan; res.bad_phi_row = g.bad_phi_row; res.bad_lt_row = g.bad_lt_row;
         report_flags(res, j, p);
         acc.md = fmax(acc.md, md);
-        const int skc_old = full ? 0 : p.ws.skc[jl];
+        const int skc_old = skc_pre;
         acc.dn += cnt - (full ? 0 : co);
         acc.ds += g.n - skc_old;
         if (p.track && (full || g.n != skc_old)) p.ws.skc[jl] = g.n;
-        if (cnt > 2) off = pool_take(p, j, cnt, full);
+        if (cnt > 2) off = (!full && osig <= -cnt) ? (long long)oaux : pool_take(p, j, cnt, true);
         if (cnt == 0) {
             p.out.sig[j] = FT_SIG_EMPTY;
         } else if (cnt > 2 && off >= 0) {
