@@ -78,6 +78,29 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 template <typename T>
 __device__ __forceinline__ T vload(const T* p) { return *(volatile const T*)p; }
 
+// 1-D bulk copies (TMA, cp.async.bulk) global -> shared, completed on an
+// mbarrier with a transaction count
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to the async proxy
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)), "r"(phase) : "memory");
+}
+
 constexpr unsigned int kFull = 0xffffffffu;
 
 struct StepParams {
@@ -290,8 +313,9 @@ __device__ __forceinline__ void list_flush(const CtaList& l, int* g_count, int* 
 
 // ---------------------------------------------------------------------------
 // prep_kernel: this step's stamps -> the active list.  A CTA covers
-// 8 x 2048 columns, warp w a contiguous 2048: in round r lane l reads the
-// 4-byte stamp word of columns base_w + 128 r + 4 l (coalesced) and
+// 8 x 2048 columns: one bulk copy (TMA, cp.async.bulk) brings their 16 KB of
+// stamps into shared memory on an mbarrier; warp w takes a contiguous 2048,
+// in round r lane l reads the 4-byte word of columns base_w + 128 r + 4 l and
 // compares its bytes with __vcmpeq4, keeping a 4-bit mask per round in one
 // 64-bit register.  One atomic per CTA reserves its part of the list, the
 // warps' offsets come from one shared exchange, and each warp then places
@@ -305,27 +329,36 @@ constexpr int kPrepRounds = 16;
 constexpr int kPrepCols = 4 * kPrepRounds;   // columns per thread
 
 __global__ void __launch_bounds__(kPrepTPB) prep_kernel(const StepParams p) {
-    pdl_wait();
+    __shared__ __align__(128) unsigned int s_tile[kPrepTPB * kPrepCols / 4];   // 16 KB of stamps
+    __shared__ __align__(8) unsigned long long s_bar;
     __shared__ int s_warp[kPrepTPB / 32];
     __shared__ int s_base;
+    // owned buffer columns [g_lo, g_hi); the CTA's 16 KB tile of stamps from
+    // the 16-byte aligned column g_lo & ~15 (the stamp array is padded past
+    // n, so the rounded-up tail stays inside it)
+    const int g_lo = p.j_base, g_hi = p.j_base + p.n_v;
+    const int c0 = (g_lo & ~15) + blockIdx.x * (kPrepTPB * kPrepCols);
+    if (threadIdx.x == 0) mbar_init(&s_bar);
+    __syncthreads();
+    pdl_wait();
     Control* ctl = p.ws.ctl;
     if (p.check_done && vload(&ctl->done)) return;
     if (step_is_full(p)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) ctl->pool_next[p.out_id] = 0ULL;
         return;
     }
+    if (threadIdx.x == 0) {
+        const int span = min(kPrepTPB * kPrepCols, ((g_hi - c0) + 15) & ~15);
+        bulk_load(s_tile, p.ws.stamp + c0, (unsigned)span, &s_bar);
+    }
     const unsigned int pat = 0x01010101u * (unsigned char)vload(&ctl->seq);
-    // owned buffer columns [g_lo, g_hi), read as aligned words from g_lo & ~3
-    const int g_lo = p.j_base, g_hi = p.j_base + p.n_v;
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-    const int cw = (g_lo & ~3) + blockIdx.x * (kPrepTPB * kPrepCols) + wi * (32 * kPrepCols);
-    // all 16 loads issued before any use (clamped to the last word: the
-    // stamp array is padded past n)
-    const int last = (g_hi - 1) & ~3;
+    const int tw = wi * (32 * kPrepCols);          // the warp's offset in the tile
+    const int cw = c0 + tw;
+    mbar_wait(&s_bar, 0);
     unsigned int x[kPrepRounds];
 #pragma unroll
-    for (int r = 0; r < kPrepRounds; ++r)
-        x[r] = __ldg(reinterpret_cast<const unsigned int*>(p.ws.stamp + min(cw + 128 * r + 4 * lane, last)));
+    for (int r = 0; r < kPrepRounds; ++r) x[r] = s_tile[(tw + 128 * r) / 4 + lane];   // beyond g_hi: masked below
     unsigned long long mm = 0;
     int cnt = 0;
 #pragma unroll
@@ -1968,7 +2001,7 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     DevState& d = dev_state();
     const char* kenv = getenv("FT_KERNELS");   // debug: bit mask of the column kernels to launch
     const int kmask = kenv ? atoi(kenv) : 15;
-    const int prep_span = n_own + (j_base & 3);   // aligned words from j_base & ~3
+    const int prep_span = n_own + (j_base & 15);  // 16-byte aligned tiles from j_base & ~15
     const int prep_grid = (prep_span + ft::kPrepCols * ft::kPrepTPB - 1) / (ft::kPrepCols * ft::kPrepTPB);
     if (kmask & 1) launch_dep(ft::prep_kernel, prep_grid, ft::kPrepTPB, s, p);
     if (ev) cudaEventRecord(ev[0], s);
