@@ -2008,16 +2008,7 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     int bg = d.band_grid[dtype == FT_F32][uni][packed];
     const int need_b = (n_own + ft::kBandTPB - 1) / ft::kBandTPB;
     if (bg > need_b) bg = need_b;
-    const char* bv = getenv("FT_BAND_MINB");   // experiment: register budget of the band kernel
-    const int minb = bv ? atoi(bv) : 0;
-    if ((kmask & 2) && minb && dtype == FT_F64 && packed) {
-        const int g2 = minb * d.sms < need_b ? minb * d.sms : need_b;
-        if (minb == 2) launch_dep(ft::band_kernel<double, true, true, 2>, g2, ft::kBandTPB, s, p);
-        else if (minb == 3) launch_dep(ft::band_kernel<double, true, true, 3>, g2, ft::kBandTPB, s, p);
-        else launch_dep(ft::band_kernel<double, true, true, 4>, g2, ft::kBandTPB, s, p);
-    } else if (kmask & 2) {
-        launch_dep(FT_PICK3(ft::band_kernel, dtype, uni, packed), bg, ft::kBandTPB, s, p);
-    }
+    if (kmask & 2) launch_dep(FT_PICK3(ft::band_kernel, dtype, uni, packed), bg, ft::kBandTPB, s, p);
     if (ev) cudaEventRecord(ev[1], s);
     if (kmask & 4)
         launch_dep(FT_PICK3(ft::wide3_kernel, dtype, uni, packed), FT_W3_MINB * d.sms, ft::kWide3TPB, s, p);
