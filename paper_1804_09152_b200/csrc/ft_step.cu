@@ -289,26 +289,29 @@ __device__ __forceinline__ void list_push(bool push, int j, int* count, int* bas
     if (push) base[q + __popc(b & ((1u << lane) - 1u))] = j;
 }
 
-// CTA-staged list: warps push into a shared buffer (shared-memory atomics);
-// list_flush moves it to the global list with one global atomic and a
-// coalesced copy (CTA-collective; call with a uniform control flow)
-struct CtaList {
+// warp-staged list: a warp pushes into its own shared buffer (no atomics,
+// no barriers) and moves it to the global list with one atomic and a
+// coalesced copy when it fills (warp-collective)
+struct WarpList {
     int* buf;
-    int* cnt;
-    int* base;
+    int n;        // entries staged (warp-uniform)
 };
 
-__device__ __forceinline__ void list_flush(const CtaList& l, int* g_count, int* g_list) {
-    __syncthreads();
-    const int n = *l.cnt;
-    if (n == 0) return;
-    if (threadIdx.x == 0) *l.base = atomicAdd(g_count, n);
-    __syncthreads();
-    const int b = *l.base;
-    for (int k = threadIdx.x; k < n; k += blockDim.x) g_list[b + k] = l.buf[k];
-    __syncthreads();
-    if (threadIdx.x == 0) *l.cnt = 0;
-    __syncthreads();
+__device__ __forceinline__ void wlist_push(bool push, int j, WarpList& l, int lane) {
+    const unsigned int b = __ballot_sync(kFull, push);
+    if (push) l.buf[l.n + __popc(b & ((1u << lane) - 1u))] = j;
+    l.n += __popc(b);
+}
+
+__device__ __forceinline__ void wlist_flush(WarpList& l, int* g_count, int* g_list, int lane) {
+    __syncwarp();
+    if (l.n == 0) return;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(g_count, l.n);
+    base = __shfl_sync(kFull, base, 0);
+    for (int k = lane; k < l.n; k += 32) g_list[base + k] = l.buf[k];
+    __syncwarp();
+    l.n = 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -428,12 +431,12 @@ __global__ void __launch_bounds__(kPrepTPB) prep_kernel(const StepParams p) {
 // reference's accumulator order.  Anything else goes to the wide list.
 
 constexpr int kBandTPB = 256;
-constexpr int kBandBuf = 1024;   // CTA-staged wide-list entries
+constexpr int kWarpBuf = 128;    // warp-staged wide-list entries
 
 template <typename T, bool UNIFORM, bool PACKED>
 __device__ __forceinline__ void band_column(const StepParams& p, int jl, bool have, bool full, bool chk,
                                             unsigned char nxt, int lane, Acc& acc, long long* s_bm,
-                                            const CtaList& wl, int4 pk) {
+                                            WarpList& wl, int4 pk) {
     const int j = p.j_base + jl;
     // stage 1: the packed L^T row (prefetched by the caller); the column's
     // own signature and value
@@ -574,7 +577,7 @@ __device__ __forceinline__ void band_column(const StepParams& p, int jl, bool ha
         }
     }
     __syncwarp();   // reconverge after the per-lane paths before the collectives
-    list_push(wide || (gen && more), j, wl.cnt, wl.buf, lane);
+    wlist_push(wide || (gen && more), j, wl, lane);
     if (fin_here) {
         acc.dn += cnt_new - (full ? 0 : cnt_old);
         acc.ds += sk_new - (full ? 0 : skc_old);
@@ -591,13 +594,11 @@ __global__ void __launch_bounds__(kBandTPB, MINB) band_kernel(const StepParams p
     __shared__ long long s_bm[4];
     __shared__ double s_md[kBandTPB / 32];
     __shared__ long long s_cnt[2 * (kBandTPB / 32)];
-    __shared__ int s_wbuf[kBandBuf];
-    __shared__ int s_wcnt, s_wbase;
+    __shared__ int s_wl[kBandTPB / 32][kWarpBuf];
     if (p.check_done && vload(&ctl->done)) return;
     if (threadIdx.x < 4) s_bm[threadIdx.x] = 0;
-    if (threadIdx.x == 0) s_wcnt = 0;
     __syncthreads();
-    const CtaList wl{s_wbuf, &s_wcnt, &s_wbase};
+    WarpList wl{s_wl[threadIdx.x >> 5], 0};
     const bool full = step_is_full(p);
     const int n_act = full ? p.n_v : vload(&ctl->n_act);
     const bool chk = p.force_check || vload(&ctl->nonfinite);
@@ -605,9 +606,9 @@ __global__ void __launch_bounds__(kBandTPB, MINB) band_kernel(const StepParams p
     const int lane = threadIdx.x & 31;
     Acc acc;
     acc_init(acc);
-    // CTA-uniform chunks of kBandTPB columns (the list flush is collective);
-    // the next chunk's column index and packed L row are loaded before the
-    // current chunk is processed, taking two levels off its load chain
+    // chunks of kBandTPB columns; the next chunk's column index and packed L
+    // row are loaded before the current chunk is processed, taking two
+    // levels off its load chain
     const int stride = gridDim.x * kBandTPB;
     int c = blockIdx.x * kBandTPB;
     bool have = c + (int)threadIdx.x < n_act;
@@ -621,13 +622,13 @@ __global__ void __launch_bounds__(kBandTPB, MINB) band_kernel(const StepParams p
         int4 pn = make_int4(0, 0, 0, 0);
         if (PACKED && hn) pn = __ldg(&p.lap_pack[jn]);
         band_column<T, UNIFORM, PACKED>(p, jl, have, full, chk, nxt, lane, acc, s_bm, wl, pk);
-        __syncthreads();
-        if (s_wcnt > kBandBuf - kBandTPB) list_flush(wl, &ctl->n_wide, p.ws.wide);
+        if (wl.n > kWarpBuf - 32) wlist_flush(wl, &ctl->n_wide, p.ws.wide, lane);
         have = hn;
         jl = jn;
         pk = pn;
     }
-    list_flush(wl, &ctl->n_wide, p.ws.wide);
+    wlist_flush(wl, &ctl->n_wide, p.ws.wide, lane);
+    __syncthreads();
     acc_flush<kBandTPB>(acc, s_bm, s_md, s_cnt, ctl);
 }
 
