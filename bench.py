@@ -508,7 +508,7 @@ def run_ours(args):
         try:
             tj = json.load(open(tpath))
             if (tj.get("engine_hash") == src_hash and tj.get("precision") == prec
-                    and tj.get("n_vertices") == n_v):
+                    and tj.get("n_vertices") == n_v and tj.get("seeds") == args.seeds):
                 traffic = tj.get("dram_bytes_per_step")
                 traffic_note = tj.get("note", "ncu dram__bytes_read+write per step, same build")
         except (OSError, ValueError):

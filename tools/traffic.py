@@ -33,7 +33,7 @@ for r in rows:
     per_kernel[name][m] += val * scale / steps
 rd, wr = tot["dram__bytes_read.sum"] / steps, tot["dram__bytes_write.sum"] / steps
 print(json.dumps({
-    "engine_hash": h.hexdigest()[:16], "precision": "exact", "n_vertices": 10000000,
+    "engine_hash": h.hexdigest()[:16], "precision": "exact", "n_vertices": 10000000, "seeds": 4096,
     "dram_bytes_per_step": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
     "per_kernel": {k: {"read": v["dram__bytes_read.sum"], "write": v["dram__bytes_write.sum"]}
                    for k, v in per_kernel.items()},
