@@ -595,10 +595,26 @@ def run_ours(args):
             parity = {"steps": n, "window": f"{first + 1}..{first + n}", "bitwise": ok,
                       "against": rcpu.kind, "nnz": int(rp[-1])}
         else:
+            # FAST: labels against the reference's EXACT field; every
+            # disagreement is measured by the gap, in the reference field,
+            # between the reference's label and ours (a near-tie is a gap
+            # within the fp32 storage error)
+            lg = ft.sharp_labels(gpu_n)
+            lr = ft.sharp_labels(ft.LayeredField(ft.SparseMat(g.n_rows, g.n_cols, rp, ri, rv, check=False), seeds))
+            diff = np.flatnonzero(lg != lr)
+
+            def ref_value(v, lab):
+                row = 0 if lab < 0 else lab + 1
+                a, b = int(rp[v]), int(rp[v + 1])
+                k = np.searchsorted(ri[a:b], row)
+                return float(rv[a + k]) if k < b - a and ri[a + k] == row else 0.0
+
+            gaps = [ref_value(v, lr[v]) - ref_value(v, lg[v]) for v in diff.tolist()]
             parity = {"steps": n, "window": f"{first + 1}..{first + n}", "bitwise": False,
                       "same_pattern": bool(same_pattern), "against": rcpu.kind,
-                      "labels_agree": float(np.mean(ft.sharp_labels(gpu_n) == ft.sharp_labels(
-                          ft.LayeredField(ft.SparseMat(g.n_rows, g.n_cols, rp, ri, rv, check=False), seeds))))}
+                      "labels_agree": float(1.0 - diff.size / max(lg.size, 1)),
+                      "label_disagreements": int(diff.size),
+                      "max_ref_gap_at_disagreement": float(max(gaps)) if gaps else 0.0}
 
     if rank == 0:
         value = world * K / (elapsed_ms * 1e-3)

@@ -282,7 +282,10 @@ class DeviceCSC:
             dev.row_idx[:nnz].copy_(torch.from_numpy(
                 np.ascontiguousarray(mat.row_idx[:nnz], dtype=np.int32)))
             vals = torch.from_numpy(np.ascontiguousarray(mat.values[:nnz], dtype=np.float64))
-            dev.values[:nnz].copy_(vals.to(dtype))
+            if dtype == torch.float64:
+                dev.values[:nnz].copy_(vals)
+            else:                       # narrow on the device, not on the host
+                dev.values[:nnz].copy_(vals.to(device))
         dev.nnz = nnz
         return dev
 
