@@ -27,7 +27,7 @@ import numpy as np
 from . import _lib
 from .errors import (BackendError, DuplicateSeedError, NumericalBlowupError,
                      PatternViolationError, ShapeError)
-from .sparse import INDEX, DeviceCSC, DeviceTiled, SparseMat, read_triplets_stream
+from .sparse import INDEX, DeviceCSC, DeviceTiled, SparseMat, read_triplets_stream, warm_pinned_results
 
 UNCLAIMED = -1
 BASE_EXHAUSTION_PER_VERTEX = 1e-9       # field.py:31
@@ -422,6 +422,7 @@ def _lap_size(lap):
 def device_laplacian(lap, precision):
     """Upload ``lap.mat_t`` once per Laplacian object (cached on it)."""
     dev = getattr(lap, "device", None)
+    warm_pinned_results(_lap_size(lap))          # first use per size: background, once
     if dev is not None:
         key = ("device", id(dev["idx"]))
     else:

@@ -425,6 +425,8 @@ def build_laplacian(mesh, scheme="uniform"):
             raise IsolatedVertexError(f"isolated-vertex: vertex {v} has no edges")
         lap = Laplacian._from_device(n_v, *devmesh.uniform_laplacian(n_v, topo["neighbor_ptr"],
                                                                      topo["neighbor_idx"]))
+        from .sparse import warm_pinned_results
+        warm_pinned_results(n_v)     # the results' pinned host blocks, ahead of the first evolve
         if not mesh.periodic and n_v >= devmesh.LOCALITY_MIN_VERTICES:
             # the engine's locality order for long evolves (the caller's
             # numbering is kept at the API: field.evolve permutes in and out)

@@ -13,6 +13,7 @@ C-ABI consumes (``ft_csc`` in include/fieldtess_cuda.h).
 
 import ctypes
 import math
+import threading
 import warnings
 
 import numpy as np
@@ -224,6 +225,43 @@ def transpose(a):
 def _torch():
     import torch
     return torch
+
+
+_WARMED = set()
+_WARM_LOCK = threading.Lock()
+WARM_PINNED_MAX_BYTES = 2 << 30     # largest result set whose pinned blocks are warmed ahead
+
+
+def warm_pinned_results(n_cols, nnz_hint=None):
+    """Pre-allocate (and release into torch's caching host allocator) pinned
+    blocks of the sizes a field of ``n_cols`` vertices returns to the host --
+    col_ptr, row_idx, values, labels -- on a background thread, so the first
+    ``field.phi`` / ``sharp_labels`` of a process does not pay the page
+    pinning (~0.5 ms per MB) on its critical path.  Called when a Laplacian
+    is first put on the device."""
+    n = int(n_cols)
+    nnz = int(nnz_hint) if nnz_hint is not None else n + n // 4     # a typical band: 1.1-1.4 entries/vertex
+    # three sets: a caller usually still holds its previous result (and
+    # perhaps a pinned copy of its input)
+    sizes = [4 * (n + 1), 4 * nnz, 8 * nnz, 8 * n]
+    if sum(sizes) * 3 > WARM_PINNED_MAX_BYTES:
+        return None
+    with _WARM_LOCK:
+        if n in _WARMED:
+            return None
+        _WARMED.add(n)
+
+    def work():
+        torch = _torch()
+        try:
+            blocks = [torch.empty(sz, dtype=torch.uint8, pin_memory=True) for sz in sizes for _ in range(3)]
+            del blocks
+        except RuntimeError:
+            pass
+
+    th = threading.Thread(target=work, name="ft-pinned-warm", daemon=True)
+    th.start()
+    return th
 
 
 def pinned_copy(t):
