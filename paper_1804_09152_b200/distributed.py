@@ -998,6 +998,39 @@ def gathered_field(ranks, transport, seeds, renumbering=None, precision="exact")
     return LayeredField(phi, seeds, steps, precision=precision)
 
 
+def dual_adjacency_partitioned(ranks, transport, mesh, threshold=0.25, renumbering=None):
+    """``vertex_adjacency``, ``triangle_adjacency`` and ``confirm_candidates``
+    (dual.py:85-233) of a partitioned field without gathering it (SURVEY
+    8(e)): every rank runs the device products (ft_dual_products) on its owned
+    + halo columns and the faces whose first vertex it owns, the four key sets
+    are all-gathered and united -- a set union, so the result is exactly the
+    single-GPU products -- and the order-dependent curation runs replicated.
+    Returns ``(a_v, a_t, curated)``; ``build_dual`` then takes ``curated``.
+    A skipped degenerate face or non-finite value (whose warnings the
+    reference raises from the whole field) falls back to the gathered field."""
+    from . import dual
+    refresh_halo(ranks, transport)
+    local = []
+    for r in ranks:
+        dphi = r.local_field(r.steps_done)
+        faces, _, _, area, _, _, n_faces = r.lloyd_faces(mesh, renumbering)
+        local.append(dual.product_keys(dphi, r.n_rows - 1, faces, area, n_faces, threshold))
+    every = transport.gather_objects(local)
+    union = tuple(np.unique(np.concatenate([k[i] for k in every])) for i in range(4))
+    skipped = any(k[4] for k in every)
+    n_cells = ranks[0].n_rows - 1
+    if skipped:
+        fld = gathered_field(ranks, transport, np.zeros(n_cells, dtype=np.int64), renumbering=renumbering)
+        a_v = dual.vertex_adjacency(fld, threshold)
+        a_t = dual.triangle_adjacency(fld, mesh, threshold)
+        return a_v, a_t, dual.confirm_candidates(fld, mesh, a_v, a_t, threshold)
+    pv, pt, px, tri, _ = dual.decode_products(union + (False,), n_cells)
+    a_v = dual.AdjacencyMatrix(dual._pairs_matrix(n_cells, pv))
+    a_v.provenance = {pair: "vertex-shared" for pair in a_v.pairs()}
+    a_t = dual.AdjacencyMatrix(dual._pairs_matrix(n_cells, pt))
+    return a_v, a_t, dual.curate(a_v, a_t, px, tri)
+
+
 class PartitionedField:
     """A field that stays on the ranks between Lloyd iterations (the
     all-reduce exchange never assembles it): the LayeredField attributes a

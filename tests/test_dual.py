@@ -159,3 +159,30 @@ def test_confirm_candidates_clean_field_does_not_warn():
     with warnings.catch_warnings():
         warnings.simplefilter("error")
         ft.confirm_candidates(fld, mesh, ft.vertex_adjacency(fld, 0.4), ft.triangle_adjacency(fld, mesh, 0.4), 0.4)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_dual_adjacency_partitioned_without_gather(world):
+    """The dual adjacency of a partitioned field from per-rank device products
+    united over ranks (distributed.dual_adjacency_partitioned: no field
+    gather): the reference's C1 A_v, A_t, curated pairs, triples and
+    triangles, exactly."""
+    from paper_1804_09152_b200 import distributed as D
+    mesh = ft.gen_icosphere(4)
+    lap = ft.build_laplacian(mesh)
+    f0 = _field("c1_traj.npz", 0)
+    ren = D.Renumbering.morton(mesh)
+    part = D.Partition.even(mesh.n_vertices, world)
+    tr = D.LoopbackTransport()
+    probs = [D.local_problem(f0.phi, lap, part, r, renumbering=ren) for r in range(world)]
+    ranks = [D.DomainRank(p, pl, renumbering=ren) for p, pl in zip(probs, D.build_plans(probs, tr))]
+    D.evolve_partitioned(ranks, tr, ft.CouplingParams(), max_steps=500, tol=0.0)
+    a_v, a_t, cur = D.dual_adjacency_partitioned(ranks, tr, mesh, 0.25, renumbering=ren)
+    ref = golden_json("c1_dual.json")
+    assert sorted(map(list, a_v.pairs())) == ref["a_v"]
+    assert sorted(map(list, a_t.pairs())) == ref["a_t"]
+    assert sorted(map(list, cur.pairs())) == ref["curated"]
+    assert sorted(map(list, cur.junction_triples)) == ref["triples"]
+    dm = ft.build_dual(cur, np.zeros((f0.n_cells, 3)))
+    assert sorted(map(sorted, dm.triangles.tolist())) == ref["triangles"]
