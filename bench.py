@@ -264,6 +264,20 @@ def run_reference_arm(args):
     if rank != 0:
         return
     import paper_1804_09152_b200 as ft
+    lv = ico_level(args)
+    n_est = 10 * 4 ** lv + 2 if lv is not None else args.nx * args.ny
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except ImportError:
+        avail = None
+    # the reference holds ~0.6 kB of host memory per vertex at the benchmark
+    # sizes (mesh, L and L^T, PHI, its Lt / skeleton workspace)
+    if avail is not None and avail < 700 * n_est:
+        print(json.dumps({"impl": "reference", "metric": METRIC,
+                          "unavailable": f"the reference needs ~{700 * n_est / 2**30:.0f} GiB of host memory at "
+                                         f"{n_est:,} vertices; {avail / 2**30:.0f} GiB available"}), flush=True)
+        return
     mesh, lap, seeds = build_workload(args)
     w, start, first = window_of(args)
     cpu = ReferenceCPU(lap)
