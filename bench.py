@@ -819,6 +819,9 @@ def run_partitioned(args, world, rank, local, emulate=0):
             "dtype": "f64" if prec == "exact" else "f32-storage/f64-arith", "data": "synthetic",
             "vertex_steps_per_s": n_v * K / (elapsed_ms * 1e-3),
             "setup_s": t_setup,
+            "single_gpu_baseline": (f"strong scaling of this mesh: its 1-GPU run is `bench.py --mesh {args.mesh} "
+                                    f"--seeds {args.seeds}` (the default N=1 line is C3, a different workload)"
+                                    if strong else "weak scaling: N=1 is the default C3 line"),
             "config": {"workload": workload,
                        "n_vertices": n_v, "seeds": n_seeds, "precision": prec,
                        "laplacian": "uniform", "parallelism": f"row-partition x{W} (NCCL halo)"
