@@ -48,14 +48,15 @@ struct Control {
     double             tol;            // evolve: the stop test (field.py:316-317),
     double             base_threshold; //   set per call by evolve_reset_kernel, so
     int                max_steps;      //   the captured graph does not depend on them
-    int                pad2;
+    int                n_w3;           // per step: columns the four-row kernel hands to the warp kernel
 };
 static_assert(sizeof(Control) % 16 == 0, "Control must stay 16B aligned");
 
 // Workspace: the control block, then per-column arrays.
 //   act[n]    active list of the step (local column indices)
 //   wide[n]   columns the band kernel hands to the three-row kernel
-//   w2[n]     columns the three-row kernel hands to the warp kernel
+//   w2[n]     columns the three-row kernel hands to the four-row kernel
+//             (the four-row kernel's leftovers reuse wide[], read by then)
 //   skc[n]    interest-skeleton size of each column when it was last computed
 //   stamp[n]  mark: column is active in the step whose sequence number (mod
 //             256) equals the stamp (indexed by buffer column)

@@ -872,6 +872,147 @@ __global__ void __launch_bounds__(kWide3TPB, FT_W3_MINB) wide3_kernel(const Step
 }
 
 // ---------------------------------------------------------------------------
+// wide4_kernel: the three-row kernel's leftovers, one lane per column: at
+// most four rows in the union and four entries per neighbour (the C5 band's
+// junction columns).  The neighbourhood goes through the sorted register
+// window (win_insert, L order: each row's Lt in the reference's order) and
+// process_window<4>; anything wider goes on to the warp kernel (the wide[]
+// list, consumed by then).
+
+constexpr int kWide4TPB = 128;
+// below this many leftovers of the three-row kernel the warp kernel takes
+// them all directly (few columns: one warp each finishes sooner than a
+// latency-bound lane-per-column pass followed by the warp kernel)
+constexpr int kWide4Min = 49152;
+
+template <typename T, bool UNIFORM, bool PACKED>
+__device__ __forceinline__ void wide4_column(const StepParams& p, int j, bool have, bool full, unsigned char nxt,
+                                             int lane, Acc& acc, long long* s_bm) {
+    const int jl = j - p.j_base;
+    int4 pk = make_int4(0, 0, 0, 0);
+    if (PACKED && have) pk = __ldg(&p.lap_pack[jl]);
+    int q0 = 0;
+    int u[kMD];
+    const int n = unpack_lrow<PACKED>(p, pk, jl, j, have, u, q0);
+    int sg[kMD], ax[kMD];
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) sg[k] = (k < n) ? __ldg(&p.in.sig[u[k]]) : FT_SIG_EMPTY;
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) ax[k] = (sg[k] >= kPair || sg[k] < -1) ? __ldg(&p.in.aux[u[k]]) : 0;
+    int kd = -1;
+    bool ok = have && n > 0;
+#pragma unroll
+    for (int k = 0; k < kMD; ++k) {
+        kd = (k < n && u[k] == j) ? k : kd;
+        ok &= sg[k] >= -4;
+    }
+    ok &= kd >= 0;
+    const double invdeg = UNIFORM ? recip_deg(n) : 0.0;
+    Win<4> w;
+    w.m = 0;
+    w.more = false;
+    if (ok) {
+#pragma unroll
+        for (int k = 0; k < kMD; ++k) {
+            if (k >= n) continue;
+            const double l = lap_value<T, UNIFORM>(p, k, kd, q0, invdeg);
+            const int c = sig_count(sg[k]);
+            for (int t = 0; t < c; ++t) {
+                const double a = hyb_val<T>(p.in, u[k], sg[k], ax[k], t);
+                win_insert<4>(w, hyb_row<T>(p.in, sg[k], ax[k], t), a * l, k == kd, a);
+            }
+        }
+    }
+    const bool run = ok && !w.more;
+    VRes res;
+    vres_init(res);
+    unsigned int om = 0;
+    if (run) {
+        process_window<4>(w, p.cp, res, om, c_recip);
+        report_flags(res, j, p);
+    }
+    __syncwarp();
+    list_push(have && !run, j, &p.ws.ctl->n_w3, p.ws.wide, lane);
+    const int cnt = __popc(om);
+    const long long off = pool_take_warp(p, j, run ? cnt : 0, full, lane);
+    // the column's old entries (through u == j) for the change test
+    int sgj = FT_SIG_EMPTY, axj = 0;
+#pragma unroll
+    for (int k = 0; k < kMD; ++k)
+        if (k == kd) { sgj = sg[k]; axj = ax[k]; }
+    const int co = sig_count(sgj);
+    bool changed = run && cnt != co;
+    double bm_new = 0.0, bm_old = 0.0;
+    if (run) {
+        bool nf = false;
+        int q = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (!(om & (1u << i))) continue;
+            const int r = w.rows[i];
+            const double nv = w.lam[i];
+            if (q < co) changed |= hyb_row<T>(p.in, sgj, axj, q) != r ||
+                                   !same_bits<T>(nv, hyb_val<T>(p.in, j, sgj, axj, q));
+            nf |= !isfinite(nv);
+            if (cnt <= 2) {
+                if (q == 0) {
+                    p.out.sig[j] = cnt == 2 ? (r | kPair) : r;
+                    ((T*)p.out.v0)[j] = (T)nv;
+                } else {
+                    p.out.aux[j] = r;
+                    ((T*)p.out.v1)[j] = (T)nv;
+                }
+            } else if (off >= 0) {
+                p.out.pidx[off + q] = r;
+                ((T*)p.out.pval)[off + q] = (T)nv;
+            }
+            ++q;
+        }
+        if (cnt == 0) p.out.sig[j] = FT_SIG_EMPTY;
+        else if (cnt > 2 && off >= 0) { p.out.sig[j] = -cnt; p.out.aux[j] = (int)off; }
+        if (nf) atomicOr(&p.ws.ctl->nonfinite, 1u);
+        bm_new = res.bm;
+        bm_old = (co > 0 && hyb_row<T>(p.in, sgj, axj, 0) == 0) ? hyb_val<T>(p.in, j, sgj, axj, 0) : 0.0;
+        acc.md = fmax(acc.md, res.maxd);
+        const int skc_old = full ? 0 : p.ws.skc[jl];
+        acc.dn += cnt - (full ? 0 : co);
+        acc.ds += res.nskel - skc_old;
+        if (p.track && (full || res.nskel != skc_old)) p.ws.skc[jl] = res.nskel;
+        if (p.track && changed) mark_ring(p, u, n, nxt);
+    }
+    __syncwarp();
+    bm_fold(bm_new, bm_old, full, s_bm);
+}
+
+template <typename T, bool UNIFORM, bool PACKED>
+__global__ void __launch_bounds__(kWide4TPB, 4) wide4_kernel(const StepParams p) {
+    pdl_wait();
+    Control* ctl = p.ws.ctl;
+    __shared__ long long s_bm[4];
+    __shared__ double s_md[kWide4TPB / 32];
+    __shared__ long long s_cnt[2 * (kWide4TPB / 32)];
+    if (p.check_done && vload(&ctl->done)) return;
+    const int nc = vload(&ctl->n_w2);
+    if (nc < kWide4Min || (int)blockIdx.x * kWide4TPB >= nc) return;
+    if (threadIdx.x < 4) s_bm[threadIdx.x] = 0;
+    __syncthreads();
+    const bool full = step_is_full(p);
+    const unsigned char nxt = (unsigned char)(vload(&ctl->seq) + 1);
+    const int lane = threadIdx.x & 31;
+    const int stride = gridDim.x * kWide4TPB;
+    Acc acc;
+    acc_init(acc);
+    for (int i0 = blockIdx.x * kWide4TPB; i0 < nc; i0 += stride) {
+        const int i = i0 + threadIdx.x;
+        const bool have = i < nc;
+        wide4_column<T, UNIFORM, PACKED>(p, have ? __ldg(&p.ws.w2[i]) : p.j_base, have, full, nxt, lane, acc,
+                                         s_bm);
+    }
+    __syncthreads();
+    acc_flush<kWide4TPB>(acc, s_bm, s_md, s_cnt, ctl);
+}
+
+// ---------------------------------------------------------------------------
 // the exact windowed algorithm (no width limit) for the rare column whose
 // neighbourhood exceeds the wide kernel's staging capacity: ascending row
 // windows of K rows gathered from global memory, aggregates first, then the
@@ -1404,7 +1545,12 @@ __global__ void __launch_bounds__(kWideTPB) wide_kernel(const StepParams p) {
     __shared__ long long s_cnt[2 * kWideWarps];
     __shared__ WideStage s_st[kWideWarps];
     if (p.check_done && vload(&ctl->done)) return;
-    const int nc = vload(&ctl->n_w2);
+    // the four-row kernel's leftovers (wide[]), or all of the three-row
+    // kernel's (w2[]) when there were too few for the four-row kernel
+    const int n2 = vload(&ctl->n_w2);
+    const bool direct = n2 < kWide4Min;
+    const int nc = direct ? n2 : vload(&ctl->n_w3);
+    const int* list = direct ? p.ws.w2 : p.ws.wide;
     if ((int)blockIdx.x * kWideWarps >= nc) return;
     if (threadIdx.x < 4) s_bm[threadIdx.x] = 0;
     __syncthreads();
@@ -1415,7 +1561,7 @@ __global__ void __launch_bounds__(kWideTPB) wide_kernel(const StepParams p) {
     Acc acc;
     acc_init(acc);
     for (int i = (blockIdx.x * kWideTPB + threadIdx.x) >> 5; i < nc; i += nw)
-        staged_column<T, UNIFORM, PACKED>(p, __ldg(&p.ws.w2[i]), s_st[wi], full, nxt, lane, acc, s_bm);
+        staged_column<T, UNIFORM, PACKED>(p, __ldg(&list[i]), s_st[wi], full, nxt, lane, acc, s_bm);
     __syncthreads();
     acc_flush<kWideTPB>(acc, s_bm, s_md, s_cnt, ctl);
 }
@@ -1533,6 +1679,7 @@ __global__ void finalize_kernel(const FinalizeParams f) {
     ctl->n_act = 0;
     ctl->n_wide = 0;
     ctl->n_w2 = 0;
+    ctl->n_w3 = 0;
     ctl->n_deep = 0;
     ctl->conv_next = 0;
     if (f.evolve) {
@@ -2015,6 +2162,7 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
         launch_dep(FT_PICK3(ft::wide3_kernel, dtype, uni, packed), FT_W3_MINB * d.sms, ft::kWide3TPB, s, p);
     if (ev) cudaEventRecord(ev[2], s);
     if (kmask & 8) {
+        launch_dep(FT_PICK3(ft::wide4_kernel, dtype, uni, packed), 4 * d.sms, ft::kWide4TPB, s, p);
         launch_dep(FT_PICK3(ft::wide_kernel, dtype, uni, packed), 8 * d.sms, ft::kWideTPB, s, p);
         launch_dep(FT_PICK2(ft::deep_kernel, dtype, uni), 64, ft::kDeepTPB, s, p);
     }

@@ -3,18 +3,20 @@ union, max entries of a neighbour): which columns reach tiers 2a / 2b / 3.
 
 usage: PYTHONPATH=. python tools/wide_hist.py [nx ny seeds warm]
 """
+import os
 import sys
 
 import numpy as np
 import torch
 
-import paper_1804_09152_b200 as ft
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1804_09152_b200 as ft  # noqa: E402
 
 a = [int(x) for x in sys.argv[1:]]
 nx, ny, nseeds, warm = (a + [3200, 3125, 4096, 80][len(a):])[:4]
 mesh = ft.gen_periodic_grid(nx, ny)
 lap = ft.build_laplacian(mesh)
-seeds = np.random.default_rng(0).choice(mesh.n_vertices, nseeds, replace=False)
+seeds = ft.sample_seed_vertices(mesh, nseeds, 0)
 cur, _ = ft.evolve(ft.init_field(mesh, seeds), lap, ft.CouplingParams(), max_steps=warm, tol=0.0)
 d = cur.device_phi()
 n = d.n_cols
