@@ -874,7 +874,8 @@ __global__ void __launch_bounds__(kWide3TPB, FT_W3_MINB) wide3_kernel(const Step
 // ---------------------------------------------------------------------------
 // wide4_kernel: the three-row kernel's leftovers, one lane per column: at
 // most four rows in the union and four entries per neighbour (the C5 band's
-// junction columns).  The neighbourhood goes through the sorted register
+// junction columns).  (The same generic window at K = 3 in place of the
+// three-row kernel is 5-16 % slower: its min / mid / max form stays.)  The neighbourhood goes through the sorted register
 // window (win_insert, L order: each row's Lt in the reference's order) and
 // process_window<4>; anything wider goes on to the warp kernel (the wide[]
 // list, consumed by then).
@@ -885,9 +886,9 @@ constexpr int kWide4TPB = 128;
 // latency-bound lane-per-column pass followed by the warp kernel)
 constexpr int kWide4Min = 49152;
 
-template <typename T, bool UNIFORM, bool PACKED>
-__device__ __forceinline__ void wide4_column(const StepParams& p, int j, bool have, bool full, unsigned char nxt,
-                                             int lane, Acc& acc, long long* s_bm) {
+template <typename T, bool UNIFORM, bool PACKED, int K>
+__device__ __forceinline__ void widek_column(const StepParams& p, int j, bool have, bool full, unsigned char nxt,
+                                             int lane, Acc& acc, long long* s_bm, int* out_count, int* out_list) {
     const int jl = j - p.j_base;
     int4 pk = make_int4(0, 0, 0, 0);
     if (PACKED && have) pk = __ldg(&p.lap_pack[jl]);
@@ -904,11 +905,11 @@ __device__ __forceinline__ void wide4_column(const StepParams& p, int j, bool ha
 #pragma unroll
     for (int k = 0; k < kMD; ++k) {
         kd = (k < n && u[k] == j) ? k : kd;
-        ok &= sg[k] >= -4;
+        ok &= sg[k] >= -K;
     }
     ok &= kd >= 0;
     const double invdeg = UNIFORM ? recip_deg(n) : 0.0;
-    Win<4> w;
+    Win<K> w;
     w.m = 0;
     w.more = false;
     if (ok) {
@@ -919,7 +920,7 @@ __device__ __forceinline__ void wide4_column(const StepParams& p, int j, bool ha
             const int c = sig_count(sg[k]);
             for (int t = 0; t < c; ++t) {
                 const double a = hyb_val<T>(p.in, u[k], sg[k], ax[k], t);
-                win_insert<4>(w, hyb_row<T>(p.in, sg[k], ax[k], t), a * l, k == kd, a);
+                win_insert<K>(w, hyb_row<T>(p.in, sg[k], ax[k], t), a * l, k == kd, a);
             }
         }
     }
@@ -928,11 +929,11 @@ __device__ __forceinline__ void wide4_column(const StepParams& p, int j, bool ha
     vres_init(res);
     unsigned int om = 0;
     if (run) {
-        process_window<4>(w, p.cp, res, om, c_recip);
+        process_window<K>(w, p.cp, res, om, c_recip);
         report_flags(res, j, p);
     }
     __syncwarp();
-    list_push(have && !run, j, &p.ws.ctl->n_w3, p.ws.wide, lane);
+    list_push(have && !run, j, out_count, out_list, lane);
     const int cnt = __popc(om);
     const long long off = pool_take_warp(p, j, run ? cnt : 0, full, lane);
     // the column's old entries (through u == j) for the change test
@@ -947,7 +948,7 @@ __device__ __forceinline__ void wide4_column(const StepParams& p, int j, bool ha
         bool nf = false;
         int q = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < K; ++i) {
             if (!(om & (1u << i))) continue;
             const int r = w.rows[i];
             const double nv = w.lam[i];
@@ -1005,8 +1006,8 @@ __global__ void __launch_bounds__(kWide4TPB, 4) wide4_kernel(const StepParams p)
     for (int i0 = blockIdx.x * kWide4TPB; i0 < nc; i0 += stride) {
         const int i = i0 + threadIdx.x;
         const bool have = i < nc;
-        wide4_column<T, UNIFORM, PACKED>(p, have ? __ldg(&p.ws.w2[i]) : p.j_base, have, full, nxt, lane, acc,
-                                         s_bm);
+        widek_column<T, UNIFORM, PACKED, 4>(p, have ? __ldg(&p.ws.w2[i]) : p.j_base, have, full, nxt, lane, acc,
+                                            s_bm, &ctl->n_w3, p.ws.wide);
     }
     __syncthreads();
     acc_flush<kWide4TPB>(acc, s_bm, s_md, s_cnt, ctl);
