@@ -32,6 +32,7 @@ import numpy as np
 
 from . import _lib
 from . import field as F
+from .devmesh import gather_columns as _gather_columns, morton_order_device  # noqa: F401 (public API)
 from .errors import BackendError, ShapeError
 from .field import (BASE_EXHAUSTION_PER_VERTEX, POOL_FRACTION, POOL_MIN, StepStats, _check,
                     _ft_dtype, _raise_step_error, _stats_from_bytes, _stream_handle,
@@ -258,9 +259,6 @@ class Renumbering:
 
     def old_vertex(self, k):
         return int(self.order[k]) if k >= 0 else k
-
-
-from .devmesh import gather_columns as _gather_columns, morton_order_device  # noqa: E402,F401
 
 
 def local_problem_device(phi, lap, order, partition, rank):
