@@ -374,6 +374,13 @@ int ft_vertex_area(int32_t n_v, const int64_t* ptr, const int64_t* corner, const
 int ft_uniform_laplacian(int32_t n_v, const int64_t* nptr, const int32_t* nidx, int32_t* ptr,
                          int32_t* idx, double* val_t, double* val, void* stream);
 
+/* -- host-side sequential steps (CPU, no stream) --------------------------- */
+/* ft_wind_triangles: the consistent winding of m dual triangles (int32
+ * [m][3], host memory, flipped in place) by the reference's depth-first walk
+ * (dual.py:284-313): roots in index order, edges 0-1, 1-2, 2-0, the
+ * triangles of an edge in ascending index. */
+int ft_wind_triangles(int64_t m, int32_t* tris);
+
 /* -- the reference's public sparse algebra (sparse.py:279-420) ------------ */
 /* General-purpose versions of the operations the Euler step fuses, bitwise
  * equal to the numba kernels (values FT_F64 only).  spgemm C = A B is

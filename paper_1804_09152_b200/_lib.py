@@ -106,7 +106,8 @@ EXPORTS = ("ft_abi_version", "ft_last_error", "ft_workspace_bytes",
            "ft_segment_sums", "ft_skeleton", "ft_expand", "ft_normalize_columns",
            "ft_clique_triangles", "ft_lloyd_backproject", "ft_lloyd_partials", "ft_lloyd_finish",
            "ft_lloyd_backproject_keys", "ft_ico_flags", "ft_ico_midpoints", "ft_ico_children",
-           "ft_renormalize", "ft_torus_grid", "ft_face_geometry", "ft_vertex_area", "ft_uniform_laplacian")
+           "ft_renormalize", "ft_torus_grid", "ft_face_geometry", "ft_vertex_area", "ft_uniform_laplacian",
+           "ft_wind_triangles")
 
 _lib = None
 
@@ -200,6 +201,8 @@ def _declare(lib):
     for name in ("ft_ico_flags", "ft_ico_midpoints", "ft_ico_children", "ft_renormalize", "ft_torus_grid",
                  "ft_face_geometry", "ft_vertex_area", "ft_uniform_laplacian"):
         getattr(lib, name).restype = ctypes.c_int
+    lib.ft_wind_triangles.argtypes = [ctypes.c_int64, vp]
+    lib.ft_wind_triangles.restype = ctypes.c_int
     lib.ft_clique_triangles.argtypes = [i32, vp, vp, vp, vp, vp, vp]
     lib.ft_clique_triangles.restype = ctypes.c_int
     lib.ft_lloyd_backproject.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp]

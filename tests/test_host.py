@@ -96,3 +96,56 @@ def test_compute_without_gpu_fails_loudly():
     f = ft.init_field(m, [0])
     with pytest.raises(ft.errors.BackendError):
         ft.step(f, ft.build_laplacian(m), ft.CouplingParams())
+
+
+def _walk(tris):
+    """The winding walk of dual.py:284-313 restated in Python (the checker)."""
+    t = [list(map(int, r)) for r in tris]
+    edges = {}
+    for i, x in enumerate(t):
+        for s in range(3):
+            u, v = x[s], x[(s + 1) % 3]
+            edges.setdefault((min(u, v), max(u, v)), []).append(i)
+    seen = [False] * len(t)
+    for root in range(len(t)):
+        if seen[root]:
+            continue
+        seen[root] = True
+        stack = [root]
+        while stack:
+            cur = stack.pop()
+            x = t[cur]
+            for s in range(3):
+                u, v = x[s], x[(s + 1) % 3]
+                for o in edges[(min(u, v), max(u, v))]:
+                    if o == cur or seen[o]:
+                        continue
+                    y = t[o]
+                    if (y[0] == u and y[1] == v) or (y[1] == u and y[2] == v) or (y[2] == u and y[0] == v):
+                        t[o] = [y[0], y[2], y[1]]
+                    seen[o] = True
+                    stack.append(o)
+    return np.asarray(t, dtype=np.int32).reshape(-1, 3)
+
+
+def test_wind_triangles_matches_the_walk():
+    """ft_wind_triangles (host C++, no GPU) is the reference's depth-first
+    winding, triangle for triangle: a random closed surface, a Moebius strip
+    (non-orientable: the result depends on the visiting order) and a
+    non-manifold fan."""
+    from paper_1804_09152_b200 import dual
+    rng = np.random.default_rng(3)
+    cases = []
+    # an octahedron with random windings
+    octa = np.array([[0, 2, 4], [2, 1, 4], [1, 3, 4], [3, 0, 4], [2, 0, 5], [1, 2, 5], [3, 1, 5], [0, 3, 5]])
+    flip = rng.random(8) < 0.5
+    octa[flip] = octa[flip][:, [0, 2, 1]]
+    cases.append(octa)
+    # Moebius strip of 8 triangles
+    cases.append(np.array([[0, 1, 2], [1, 3, 2], [2, 3, 4], [3, 5, 4], [4, 5, 6], [5, 7, 6], [6, 7, 1], [7, 0, 1]]))
+    # three triangles on one edge, then random soup
+    cases.append(np.array([[0, 1, 2], [1, 0, 3], [0, 1, 4], [2, 1, 5]]))
+    cases.append(rng.integers(0, 40, size=(300, 3)))
+    for c in cases:
+        c = c[(c[:, 0] != c[:, 1]) & (c[:, 1] != c[:, 2]) & (c[:, 0] != c[:, 2])]
+        assert np.array_equal(dual._wind(c), _walk(c))
