@@ -120,6 +120,7 @@ struct StepParams {
     Cp cp;
     Workspace ws;
     const int* report_ids;  // nullable: caller ids of the owned columns (error reports)
+    int wide4_min;       // the four-row kernel runs when the three-row kernel leaves at least this many
 };
 
 // the step recomputes every column (always without tracking)
@@ -994,7 +995,7 @@ __global__ void __launch_bounds__(kWide4TPB, 4) wide4_kernel(const StepParams p)
     __shared__ long long s_cnt[2 * (kWide4TPB / 32)];
     if (p.check_done && vload(&ctl->done)) return;
     const int nc = vload(&ctl->n_w2);
-    if (nc < kWide4Min || (int)blockIdx.x * kWide4TPB >= nc) return;
+    if (nc < p.wide4_min || (int)blockIdx.x * kWide4TPB >= nc) return;
     if (threadIdx.x < 4) s_bm[threadIdx.x] = 0;
     __syncthreads();
     const bool full = step_is_full(p);
@@ -1549,7 +1550,7 @@ __global__ void __launch_bounds__(kWideTPB) wide_kernel(const StepParams p) {
     // the four-row kernel's leftovers (wide[]), or all of the three-row
     // kernel's (w2[]) when there were too few for the four-row kernel
     const int n2 = vload(&ctl->n_w2);
-    const bool direct = n2 < kWide4Min;
+    const bool direct = n2 < p.wide4_min;
     const int nc = direct ? n2 : vload(&ctl->n_w3);
     const int* list = direct ? p.ws.w2 : p.ws.wide;
     if ((int)blockIdx.x * kWideWarps >= nc) return;
@@ -2146,6 +2147,8 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     p.lap_pack = packed ? (const int4*)lap_t->values : nullptr;
     p.force_check = (lap_flags & FT_LAP_CHECK_FINITE) != 0;
     p.report_ids = dom ? dom->report_ids : nullptr;
+    const char* w4 = getenv("FT_WIDE4_MIN");     // tests: exercise the four-row kernel on small fields
+    p.wide4_min = w4 ? atoi(w4) : ft::kWide4Min;
     lib_init();
     DevState& d = dev_state();
     const char* kenv = getenv("FT_KERNELS");   // debug: bit mask of the column kernels to launch
@@ -2395,7 +2398,9 @@ extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* p
         k.caps[0] = work_a->capacity; k.caps[1] = work_b->capacity; k.caps[2] = (long long)ws_bytes;
         const double prm[8] = {params->w, params->a, params->e, params->e_base, params->mu, params->dt, 0.0, 0.0};
         memcpy(k.prm, prm, sizeof(prm));
-        const int ints[6] = {lap_flags, dtype, 0, phi_in->n_cols, phi_in->n_rows, pdl_enabled()};
+        const char* w4 = getenv("FT_WIDE4_MIN");     // baked into the captured launches
+        const int ints[6] = {lap_flags, dtype, w4 ? atoi(w4) : ft::kWide4Min, phi_in->n_cols, phi_in->n_rows,
+                             pdl_enabled()};
         memcpy(k.ints, ints, sizeof(ints));
         std::lock_guard<std::mutex> lk(d.mu);   // the graph cache and the graph stream
         if (graph_stream_init(d) != FT_OK) return cuda_check("ft_evolve(graph stream)");

@@ -463,3 +463,26 @@ def test_step_reports_phase_times():
     assert all(t >= 0.0 for t in phases)
     assert st.spgemm_time > 0.0 and st.normalize_time > 0.0 and st.skeleton_time > 0.0
     assert st.total_time == pytest.approx(sum(phases))
+
+
+@pytest.mark.parametrize("subdiv,n_seeds", [(4, 64), (3, 160)])
+def test_four_row_kernel_bitwise(monkeypatch, subdiv, n_seeds):
+    """The four-row kernel (wide4) on small dense fields: forced on for any
+    number of leftovers (FT_WIDE4_MIN=0; by default it runs only when the
+    three-row kernel leaves >= 48K columns), bitwise against the C oracle
+    through the device evolve and the step loop."""
+    monkeypatch.setenv("FT_WIDE4_MIN", "0")
+    mesh = ft.gen_icosphere(subdiv)
+    lap = ft.build_laplacian(mesh)
+    seeds = np.random.default_rng(0).choice(mesh.n_vertices, n_seeds, replace=False)
+    fld = ft.init_field(mesh, seeds)
+    out, trace = ft.evolve(fld, lap, DEFAULT, max_steps=40, tol=0.0)
+    lt = po.Csc.of(ft.field._with_diagonal(lap.mat_t))
+    ref, rtrace = po.evolve_c(po.Csc.of(fld.phi), lt, DEFAULT, 40, n_threads=4)
+    assert_csc_equal(out.phi, ref)
+    assert [s.max_delta for s in trace] == [s["max_delta"] for s in rtrace]
+    cur = fld
+    for _ in range(12):
+        cur, _st = ft.step(cur, lap, DEFAULT)
+    ref12, _ = po.evolve_c(po.Csc.of(fld.phi), lt, DEFAULT, 12, n_threads=4)
+    assert_csc_equal(cur.phi, ref12)
