@@ -1539,7 +1539,10 @@ __device__ __forceinline__ void staged_column(const StepParams& p, int j, WideSt
 }
 
 template <typename T, bool UNIFORM, bool PACKED>
-__global__ void __launch_bounds__(kWideTPB) wide_kernel(const StepParams p) {
+#ifndef FT_WIDE_MINB
+#define FT_WIDE_MINB 8      // 64 registers: eight CTAs per SM (both limits met, +1 % at C3)
+#endif
+__global__ void __launch_bounds__(kWideTPB, FT_WIDE_MINB) wide_kernel(const StepParams p) {
     pdl_wait();
     Control* ctl = p.ws.ctl;
     __shared__ long long s_bm[4];
