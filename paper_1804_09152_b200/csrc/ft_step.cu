@@ -987,7 +987,10 @@ __device__ __forceinline__ void widek_column(const StepParams& p, int j, bool ha
 }
 
 template <typename T, bool UNIFORM, bool PACKED>
-__global__ void __launch_bounds__(kWide4TPB, 4) wide4_kernel(const StepParams p) {
+#ifndef FT_W4_MINB
+#define FT_W4_MINB 6      // 80 registers: six CTAs per SM (+1.6 % at C5 over 4)
+#endif
+__global__ void __launch_bounds__(kWide4TPB, FT_W4_MINB) wide4_kernel(const StepParams p) {
     pdl_wait();
     Control* ctl = p.ws.ctl;
     __shared__ long long s_bm[4];
@@ -2169,7 +2172,7 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
         launch_dep(FT_PICK3(ft::wide3_kernel, dtype, uni, packed), FT_W3_MINB * d.sms, ft::kWide3TPB, s, p);
     if (ev) cudaEventRecord(ev[2], s);
     if (kmask & 8) {
-        launch_dep(FT_PICK3(ft::wide4_kernel, dtype, uni, packed), 4 * d.sms, ft::kWide4TPB, s, p);
+        launch_dep(FT_PICK3(ft::wide4_kernel, dtype, uni, packed), FT_W4_MINB * d.sms, ft::kWide4TPB, s, p);
         launch_dep(FT_PICK3(ft::wide_kernel, dtype, uni, packed), 8 * d.sms, ft::kWideTPB, s, p);
         launch_dep(FT_PICK2(ft::deep_kernel, dtype, uni), 64, ft::kDeepTPB, s, p);
     }
