@@ -12,6 +12,7 @@ import paper_1804_09152_b200 as ft
 from paper_1804_09152_b200 import _lib, field as F
 
 ap = argparse.ArgumentParser()
+ap.add_argument("--mesh", default="torus", help="torus or icoL")
 ap.add_argument("--nx", type=int, default=3200)
 ap.add_argument("--ny", type=int, default=3125)
 ap.add_argument("--seeds", type=int, default=4096)
@@ -21,7 +22,8 @@ ap.add_argument("--counts", action="store_true")
 ap.add_argument("--precision", default="exact")
 args = ap.parse_args()
 
-mesh = ft.gen_periodic_grid(args.nx, args.ny)
+mesh = (ft.gen_icosphere(int(args.mesh[3:]), max_subdiv=12) if args.mesh.startswith("ico")
+        else ft.gen_periodic_grid(args.nx, args.ny))
 lap = ft.build_laplacian(mesh)
 seeds = ft.sample_seed_vertices(mesh, args.seeds, 0)
 fld = ft.init_field(mesh, seeds, precision=args.precision)
