@@ -1180,15 +1180,22 @@ constexpr int kWideTPB = 128;
 constexpr int kWideWarps = kWideTPB / 32;
 constexpr int kStageCap = 128;    // staged neighbourhood entries per warp
 
+// row/ph are dead once the per-row slots are built (after a __syncwarp),
+// so rpos/rv reuse them: 5.5 KB per warp, eight 4-warp CTAs per SM fit
 struct WideStage {
-    int row[kStageCap];
+    union {
+        int row[kStageCap];       // staged entries' rows
+        int rpos[kStageCap];      // output position of the row (-1: dropped)
+    };
     double prod[kStageCap];       // PHI(r, u) * L(j, u)
-    double ph[kStageCap];         // PHI(r, u) when u == j
+    union {
+        double ph[kStageCap];     // PHI(r, u) when u == j
+        double rv[kStageCap];     // the row's new value
+    };
     unsigned char diag[kStageCap];
     short order[kStageCap];       // staged index of the k-th entry in (row, L order)
     int rrow[kStageCap];          // per distinct row, ascending
-    double rlam[kStageCap], rphi[kStageCap], rv[kStageCap];
-    int rpos[kStageCap];          // output position of the row (-1: dropped)
+    double rlam[kStageCap], rphi[kStageCap];
 };
 
 // exclusive warp scan of v with a running carry
