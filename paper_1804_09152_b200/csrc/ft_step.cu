@@ -687,10 +687,8 @@ __device__ __forceinline__ long long pool_take_warp(const StepParams& p, int j, 
 
 template <typename T, bool UNIFORM, bool PACKED>
 __device__ __forceinline__ void wide3_column(const StepParams& p, int j, bool have, bool full, unsigned char nxt,
-                                             int lane, Acc& acc, long long* s_bm) {
+                                             int lane, Acc& acc, long long* s_bm, int4 pk) {
     const int jl = j - p.j_base;
-    int4 pk = make_int4(0, 0, 0, 0);
-    if (PACKED && have) pk = __ldg(&p.lap_pack[jl]);
     int q0 = 0;
     int u[kMD];
     const int n = unpack_lrow<PACKED>(p, pk, jl, j, have, u, q0);
@@ -862,11 +860,24 @@ __global__ void __launch_bounds__(kWide3TPB, FT_W3_MINB) wide3_kernel(const Step
     const int stride = gridDim.x * kWide3TPB;
     Acc acc;
     acc_init(acc);
+    // the next column's index and packed L row are loaded before the current
+    // column is processed (two levels off its load chain, as in the band kernel)
+    int i = blockIdx.x * kWide3TPB + threadIdx.x;
+    bool have = i < nc;
+    int j = have ? __ldg(&p.ws.wide[i]) : p.j_base;
+    int4 pk = make_int4(0, 0, 0, 0);
+    if (PACKED && have) pk = __ldg(&p.lap_pack[j - p.j_base]);
     for (int i0 = blockIdx.x * kWide3TPB; i0 < nc; i0 += stride) {
-        const int i = i0 + threadIdx.x;
-        const bool have = i < nc;
-        wide3_column<T, UNIFORM, PACKED>(p, have ? __ldg(&p.ws.wide[i]) : p.j_base, have, full, nxt, lane, acc,
-                                         s_bm);
+        const int in = i + stride;
+        const bool hn = in < nc;
+        const int jn = hn ? __ldg(&p.ws.wide[in]) : p.j_base;
+        int4 pn = make_int4(0, 0, 0, 0);
+        if (PACKED && hn) pn = __ldg(&p.lap_pack[jn - p.j_base]);
+        wide3_column<T, UNIFORM, PACKED>(p, j, have, full, nxt, lane, acc, s_bm, pk);
+        i = in;
+        have = hn;
+        j = jn;
+        pk = pn;
     }
     __syncthreads();
     acc_flush<kWide3TPB>(acc, s_bm, s_md, s_cnt, ctl);
