@@ -571,7 +571,8 @@ def run_ours(args):
             barrier()
             held = [phi_back, labels]   # a caller holds the latest result while making the next call
         h2d = 4 * (n_v + 1) + (4 + vbytes) * nnz0
-        d2h = 4 * (n_v + 1) + (4 + vbytes) * phi_back.nnz + 8 * labels.size + _lib.STATS_BYTES * len(tr)
+        d2h = (4 * (n_v + 1) + (4 + phi_back.values.itemsize) * phi_back.nnz + 8 * labels.size
+               + _lib.STATS_BYTES * len(tr))   # field.phi is float64 on the host at either precision
         steady = statistics.median(times[2:])
         e2e = {"value": world * K / steady, "unit": "steps/s",
                "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K),
@@ -795,13 +796,13 @@ def run_partitioned(args, world, rank, local, emulate=0):
             f = r.owned_field(r.steps_done)
             h = f.to_host()
             lab = r.owned_labels(field=f).cpu().numpy()
-            d2h += 4 * (r.n_own + 1) + (4 + vbytes) * h.nnz + 8 * lab.size
+            d2h += 4 * (r.n_own + 1) + (4 + h.values.itemsize) * h.nnz + 8 * lab.size
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         barrier()
         e2e_s = allmax(t1 - t0)
         h2d = sum(4 * (p.lap_ptr.size + p.lap_idx.size) + 8 * p.lap_val.size + 8 * p.cols.size
-                  + 4 * p.row_idx.size + vbytes * p.values.size for p in probs)
+                  + 4 * p.row_idx.size + p.values.nbytes for p in probs)
         del ranks2
         e2e = {"value": W * K / e2e_s, "unit": "steps/s",
                "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K),
