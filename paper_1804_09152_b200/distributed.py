@@ -370,21 +370,32 @@ class TorchTransport:
         (r,) = ranks
         if self.nccl:
             self.dist.all_gather_into_tensor(r.gathered, r.record, group=self.group)
-        else:
+        elif r.record.device.type == "cpu":
             self.dist.all_gather(list(r.gathered.chunk(self.world)), r.record, group=self.group)
+        else:                       # gloo with device buffers: staged through the host
+            g = r.gathered.cpu()
+            self.dist.all_gather(list(g.chunk(self.world)), r.record.cpu(), group=self.group)
+            r.gathered.copy_(g)
 
     def exchange(self, ranks):
         (r,) = ranks
         d = self.dist
+        # gloo cannot send device tensors: stage the messages through the host
+        host = not self.nccl and any(t.device.type != "cpu" for t in r.send_msg.values())
+        recv = {q: (t.cpu() if host else t) for q, t in r.recv_msg.items()}
         ops = []
         for q in r.plan.peers:
             if q in r.plan.send:
-                ops.append(d.P2POp(d.isend, r.send_msg[q], q, group=self.group))
+                m = r.send_msg[q]
+                ops.append(d.P2POp(d.isend, m.cpu() if host else m, q, group=self.group))
             if q in r.plan.recv:
-                ops.append(d.P2POp(d.irecv, r.recv_msg[q], q, group=self.group))
+                ops.append(d.P2POp(d.irecv, recv[q], q, group=self.group))
         if ops:
             for req in d.batch_isend_irecv(ops):
                 req.wait()
+        if host:
+            for q, t in recv.items():
+                r.recv_msg[q].copy_(t)
 
     def all_reduce(self, tensors, op):
         """In-place all-reduce ("sum" / "min" / "max") of this rank's tensor."""

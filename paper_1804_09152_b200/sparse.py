@@ -319,15 +319,11 @@ class DeviceCSC:
         if nnz:
             dev.row_idx[:nnz].copy_(torch.from_numpy(
                 np.ascontiguousarray(mat.row_idx[:nnz], dtype=np.int32)))
-            hv = mat.values[:nnz]
-            if dtype == torch.float32 and hv.dtype == np.float32:   # already narrow: one copy
-                dev.values[:nnz].copy_(torch.from_numpy(np.ascontiguousarray(hv)))
-            else:
-                vals = torch.from_numpy(np.ascontiguousarray(hv, dtype=np.float64))
-                if dtype == torch.float64:
-                    dev.values[:nnz].copy_(vals)
-                else:                   # narrow on the device, not on the host
-                    dev.values[:nnz].copy_(vals.to(device))
+            vals = torch.from_numpy(np.ascontiguousarray(mat.values[:nnz], dtype=np.float64))
+            if dtype == torch.float64:
+                dev.values[:nnz].copy_(vals)
+            else:                       # narrow on the device, not on the host
+                dev.values[:nnz].copy_(vals.to(device))
         dev.nnz = nnz
         return dev
 

@@ -487,3 +487,55 @@ def test_local_problem_device_matches_host_renumbering():
             x, y = getattr(pd, a), getattr(ph, a)
             assert x.dtype == y.dtype and np.array_equal(x, y), a
         assert pd.lap_flags == ph.lap_flags and pd.symmetric and ph.symmetric
+
+
+# -- GPU: two processes, one rank each, TorchTransport ------------------------
+
+
+def _gpu_gloo_worker(rank, world, port, n_steps, out_q):
+    """One rank per process on cuda:0; gloo carries the messages through the
+    host (TorchTransport's staging), so this runs the per-process plumbing
+    of a multi-GPU job -- local problem, plans, DomainRank, the
+    stats gather and halo exchange, gather_owned -- on a one-GPU box."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        mesh, seeds = _grid_case(40, 30, n_seeds=25)
+        part = D.Partition.even(mesh.n_vertices, world, align=40)
+        lap = ft.build_laplacian(mesh)
+        fld = ft.init_field(mesh, seeds)
+        tr = D.TorchTransport()
+        prob = D.local_problem(fld.phi, lap, part, rank)
+        (plan,) = D.build_plans([prob], tr)
+        ranks = [D.DomainRank(prob, plan)]
+        steps, trace = D.evolve_partitioned(ranks, tr, ft.CouplingParams(), max_steps=n_steps, tol=0.0)
+        whole = D.assemble_owned(tr.gather_owned(ranks, steps), prob.n_rows, mesh.n_vertices)
+        if rank == 0:
+            single, tr1 = ft.evolve(fld, lap, ft.CouplingParams(), max_steps=n_steps, tol=0.0)
+            _assert_same_field(whole, single.phi)
+            assert steps == n_steps
+            for a, b in zip(tr1, trace):
+                assert a.max_delta == b.max_delta and a.nnz_phi == b.nnz_phi
+        out_q.put((rank, "ok"))
+    except Exception as exc:                    # pragma: no cover - reported to the parent
+        out_q.put((rank, repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_processes_torch_transport_match_single_gpu():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_gloo_worker, args=(r, 2, port, 40, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=400) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}

@@ -414,27 +414,6 @@ def test_random_fields_every_tier_fast(max_cnt, n_pool, seed):
     assert np.all(np.abs(got - want) <= 1e-5 * np.abs(want) + 2e-7)
 
 
-def test_fast_upload_float32_host_values():
-    """A FAST field given float32 host values uploads them as they are; the
-    same values widened to float64 narrow on the device to the same bits,
-    and both step to the same result (field.phi widened to float64)."""
-    rng = np.random.default_rng(5)
-    mesh = ft.gen_periodic_grid(24, 20)
-    lap = ft.build_laplacian(mesh)
-    phi = _random_field(rng, mesh.n_vertices, 17, 3, np.arange(8))
-    v32 = np.asarray(phi.values[:phi.nnz], dtype=np.float32)
-    a = ft.SparseMat(phi.n_rows, phi.n_cols, phi.col_ptr, phi.row_idx, v32, check=False)
-    b = ft.SparseMat(phi.n_rows, phi.n_cols, phi.col_ptr, phi.row_idx, v32.astype(np.float64), check=False)
-    fa = ft.LayeredField(a, np.arange(16), precision="fast")
-    fb = ft.LayeredField(b, np.arange(16), precision="fast")
-    assert np.array_equal(fa.device_phi().values[:phi.nnz].cpu().numpy(), v32)
-    assert np.array_equal(fb.device_phi().values[:phi.nnz].cpu().numpy(), v32)
-    oa, _ = ft.step(fa, lap, DEFAULT)
-    ob, _ = ft.step(fb, lap, DEFAULT)
-    assert oa.phi.values.dtype == np.float64
-    assert_csc_equal(oa.phi, ob.phi)
-
-
 @pytest.mark.parametrize("max_steps", [1, 2, 3, 16, 17, 18, 33])
 def test_evolve_chunk_boundaries(max_steps):
     """ft_evolve around its CUDA-graph chunking (step 1, then 16-step graph

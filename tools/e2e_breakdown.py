@@ -1,7 +1,7 @@
 #!/usr/bin/env python
-"""Where the e2e time of bench.py goes (C3, EXACT): upload, evolve(K), field.phi, sharp_labels.
+"""Where the e2e time of bench.py goes (C3): upload, evolve(K), field.phi, sharp_labels.
 
-    python tools/e2e_breakdown.py [--steps K]
+    python tools/e2e_breakdown.py [--steps K] [--precision exact|fast]
 
 Each stage is bracketed by torch.cuda.synchronize(); five passes from the
 step-80 field, the caller holding its latest result (as in bench.py's e2e):
@@ -22,6 +22,7 @@ import paper_1804_09152_b200 as ft  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--precision", default="exact")
     args = ap.parse_args()
     wl = argparse.Namespace(mesh="torus", nx=bench.NX, ny=bench.NY, seeds=bench.N_SEEDS)
     mesh, lap, seeds = bench.build_workload(wl)
@@ -29,7 +30,7 @@ def main():
     nnz0 = host0.nnz
     pinned = [torch.empty(a.size, dtype=t, pin_memory=True)
               for a, t in ((host0.col_ptr, torch.int32), (host0.row_idx[:nnz0], torch.int32),
-                           (host0.values[:nnz0], torch.float64))]
+                           (host0.values[:nnz0], torch.float64))]   # SparseMat values are float64
     pinned[0].numpy()[:] = host0.col_ptr
     pinned[1].numpy()[:] = host0.row_idx[:nnz0]
     pinned[2].numpy()[:] = host0.values[:nnz0]
@@ -39,7 +40,7 @@ def main():
     held = None
     for rep in range(5):
         t = [time.perf_counter()]
-        fld = ft.LayeredField(hphi, seeds, precision="exact")
+        fld = ft.LayeredField(hphi, seeds, step_count=80, precision=args.precision)
         fld.device_phi()
         torch.cuda.synchronize(); t.append(time.perf_counter())
         fin, tr = ft.evolve(fld, lap, params, max_steps=args.steps, tol=0.0)
