@@ -714,24 +714,29 @@ __device__ __forceinline__ void wide3_column(const StepParams& p, int j, bool ha
         rr[k][1] = s >= kPair ? ax[k] : (s == -3 ? __ldg(&p.in.pidx[ax[k] + 1]) : INT_MAX);
         rr[k][2] = s == -3 ? __ldg(&p.in.pidx[ax[k] + 2]) : INT_MAX;
     }
+    // rlo / rhi over the present rows (absent = INT_MAX), then the rows
+    // strictly between them: their minimum is the middle row, a larger one
+    // means a fourth row (branch-free min / max chains)
     int rlo = INT_MAX, rhi = -1;
-#pragma unroll
-    for (int k = 0; k < kMD; ++k)
-#pragma unroll
-        for (int t = 0; t < 3; ++t)
-            if (rr[k][t] != INT_MAX) { rlo = min(rlo, rr[k][t]); rhi = max(rhi, rr[k][t]); }
-    int rmid = INT_MAX;
-    bool more = false;
 #pragma unroll
     for (int k = 0; k < kMD; ++k)
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
             const int r = rr[k][t];
-            if (r != INT_MAX && r != rlo && r != rhi) {
-                if (rmid == INT_MAX) rmid = r;
-                else if (r != rmid) more = true;
-            }
+            rlo = min(rlo, r);
+            rhi = max(rhi, r != INT_MAX ? r : -1);
         }
+    int rmid = INT_MAX, rmax_mid = -1;
+#pragma unroll
+    for (int k = 0; k < kMD; ++k)
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            const int r = rr[k][t];
+            const bool mid = r > rlo && r < rhi;
+            rmid = min(rmid, mid ? r : INT_MAX);
+            rmax_mid = max(rmax_mid, mid ? r : -1);
+        }
+    const bool more = rmax_mid > rmid && rmid != INT_MAX;
     const bool run = ok && !more;
     // Lt per row in L order; PHI(r, j) and the old entries through u == j
     const double invdeg = UNIFORM ? recip_deg(n) : 0.0;
