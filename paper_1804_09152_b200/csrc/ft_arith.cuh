@@ -84,6 +84,29 @@ __device__ __forceinline__ bool in_skeleton(double ph, double lm) {
     return (ph > 0.0) || (ph == 0.0 && lm > 0.0);
 }
 
+// sqrt of a skeleton row's PHI (>= 0, never NaN: in_skeleton).  A row held
+// only by Lt has PHI == 0, and sqrt(+-0) leaves CUDA's inline fast path for
+// its out-of-range slow-path call (the warp branches and shuffles registers
+// even when the result is then discarded); the argument is therefore kept
+// in range (behind an empty asm, or the compiler folds the select back into
+// sqrt(x) / sqrt(1)) and +-0 returned as itself (sqrt(+-0) == +-0: bitwise
+// the same).
+__device__ __forceinline__ double sqrt_skel(double x) {
+    double a = x > 0.0 ? x : 1.0;
+    asm("" : "+d"(a));     // opaque: the select is not folded through the sqrt
+    const double r = sqrt(a);
+    return x > 0.0 ? r : x;
+}
+
+// 1 / s for a positive column sum, 0 otherwise; the division never sees
+// s == 0 (the same slow-path concern)
+__device__ __forceinline__ double recip_pos(bool spos, double s) {
+    double d = spos ? s : 1.0;
+    asm("" : "+d"(d));
+    const double q = 1.0 / d;
+    return spos ? q : 0.0;
+}
+
 template <int K>
 __device__ __forceinline__ void pass_aggregate(const Win<K>& w, Agg& g) {
 #pragma unroll
@@ -100,7 +123,7 @@ __device__ __forceinline__ void pass_aggregate(const Win<K>& w, Agg& g) {
                 const double lh = (lm != 0.0) ? lm : 0.0;
                 g.sl = g.sl + lh;
                 g.sp = g.sp + ph;
-                g.sr = g.sr + sqrt(ph);
+                g.sr = g.sr + sqrt_skel(ph);
             }
         }
     }
@@ -115,7 +138,7 @@ struct Coef {
 __device__ __forceinline__ Coef make_coef(const Agg& g, const Cp& p, const double* recip) {
     Coef c;
     c.hb = (g.n > 0) && (g.first_row == 0);
-    c.rb = c.hb ? sqrt(g.phi0) : 0.0;
+    c.rb = c.hb ? sqrt_skel(g.phi0) : 0.0;
     c.spc = c.hb ? g.sp - g.phi0 : g.sp;
     const int n_cells = c.hb ? g.n - 1 : g.n;
     c.inv_ni = (recip && g.n <= 32) ? recip[g.n] : 1.0 / (double)g.n;
@@ -152,7 +175,7 @@ __device__ __forceinline__ double update_entry_sq(int r, double ph, double lh, d
 
 __device__ __forceinline__ double update_entry(int r, double ph, double lh, const Coef& c, const Cp& p,
                                                bool& nan) {
-    return update_entry_sq(r, ph, lh, sqrt(ph), c, p, nan);
+    return update_entry_sq(r, ph, lh, sqrt_skel(ph), c, p, nan);
 }
 
 struct VRes {
@@ -202,7 +225,7 @@ __device__ __forceinline__ void process_window(Win<K>& w, const Cp& p, VRes& res
             if (g.n == 0) { g.first_row = w.rows[i]; g.phi0 = ph; }
             g.n++;
             const double lh = (lm != 0.0) ? lm : 0.0;
-            sq[i] = sqrt(ph);
+            sq[i] = sqrt_skel(ph);
             g.sl = g.sl + lh;
             g.sp = g.sp + ph;
             g.sr = g.sr + sq[i];
@@ -220,7 +243,7 @@ __device__ __forceinline__ void process_window(Win<K>& w, const Cp& p, VRes& res
         }
     }
     const bool spos = s > 0.0;
-    const double inv = spos ? 1.0 / s : 0.0;
+    const double inv = recip_pos(spos, s);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         if (skel_mask & (1u << i)) {
@@ -262,8 +285,8 @@ __device__ __forceinline__ void process_two(int m, int r0, int r1, double ph0, d
     nv1 = 0.0;
     if (n == 0) return;
     // aggregates over the skeleton rows in row order
-    const double sq0 = in0 ? sqrt(ph0) : 0.0;
-    const double sq1 = in1 ? sqrt(ph1) : 0.0;
+    const double sq0 = in0 ? sqrt_skel(ph0) : 0.0;
+    const double sq1 = in1 ? sqrt_skel(ph1) : 0.0;
     const double lh0 = (lm0 != 0.0) ? lm0 : 0.0;
     const double lh1 = (lm1 != 0.0) ? lm1 : 0.0;
     Agg g;
@@ -279,7 +302,7 @@ __device__ __forceinline__ void process_two(int m, int r0, int r1, double ph0, d
     if (in0) { v0 = update_entry_sq(r0, ph0, lh0, sq0, c, p, res.nan); s = s + v0; }
     if (in1) { v1 = update_entry_sq(r1, ph1, lh1, sq1, c, p, res.nan); s = s + v1; }
     const bool spos = s > 0.0;
-    const double inv = spos ? 1.0 / s : 0.0;
+    const double inv = recip_pos(spos, s);
     if (in0) {
         const double nv = spos ? v0 * inv : v0;
         if (nv != 0.0) { res.cnt++; out_mask |= 1u; if (r0 == 0) res.bm = res.bm + nv; }

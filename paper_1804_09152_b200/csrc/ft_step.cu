@@ -1119,7 +1119,7 @@ __device__ __noinline__ void vertex_slow(int j, const StepParams& p, const Src& 
         if (w.m > 0) lo = w.rows[w.m - 1];
     } while (w.more);
     const bool spos = s > 0.0;
-    const double inv = spos ? 1.0 / s : 0.0;
+    const double inv = recip_pos(spos, s);
     bool dummy = false;
     lo = -1;
     do {
@@ -1368,7 +1368,7 @@ __device__ __forceinline__ void staged_column(const StepParams& p, int j, WideSt
         if (blm) g.bad_lt_row = blr;
         const unsigned im = __ballot_sync(kFull, in);
         const double lh = (in && lm != 0.0) ? lm : 0.0;
-        const double sq = in ? sqrt(ph) : 0.0;
+        const double sq = in ? sqrt_skel(ph) : 0.0;
         g.n = __popc(im);
         if (im) {
             const int f0 = __ffs(im) - 1;
@@ -1460,7 +1460,7 @@ __device__ __forceinline__ void staged_column(const StepParams& p, int j, WideSt
                 g.n++;
                 g.sl = g.sl + ((lm != 0.0) ? lm : 0.0);
                 g.sp = g.sp + ph;
-                g.sr = g.sr + sqrt(ph);
+                g.sr = g.sr + sqrt_skel(ph);
             }
         }
         const Coef c = make_coef(g, p.cp, c_recip);

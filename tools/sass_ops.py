@@ -1,7 +1,9 @@
-"""Executed SASS instructions of one kernel grouped by opcode (ncu source page)."""
+"""Executed SASS instructions of one kernel grouped by opcode (ncu source page):
+python tools/sass_ops.py report.ncu-rep [top] [kernel-regex]"""
 import collections, csv, io, subprocess, sys
 rep = sys.argv[1]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+flt = ["--kernel-name", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+raw = subprocess.run(["ncu", "-i", rep, *flt, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr = None
