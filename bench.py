@@ -407,7 +407,6 @@ def run_ours(args):
         dl = perm
     lib = _lib.lib()
     lap_c = dl.ft_csc(prec)
-    flags = dl.launch_flags()
     prm = params.ft_params()
     dt_code = F._ft_dtype(prec)
     wp, wn = ws.ws_args()
@@ -422,6 +421,7 @@ def run_ours(args):
 
     def evolve_dev(src_dev, steps):
         s_c, a_c, b_c = src_dev.ft_csc(), ta.ft_tiled(), tb.ft_tiled()
+        flags = dl.launch_flags(src_dev)    # as field.evolve: + the dense-band hint
         rc = lib.ft_evolve(ctypes.byref(lap_c), flags, ctypes.byref(s_c), ctypes.byref(a_c),
                            ctypes.byref(b_c), ctypes.byref(out_c), dt_code, ctypes.byref(prm), steps, 0.0, 0.0,
                            wp, wn, ctypes.c_void_p(trace.data_ptr()), ctypes.c_void_p(ev_ctl.data_ptr()), sh)
@@ -485,6 +485,7 @@ def run_ours(args):
     krec = torch.zeros(K * _lib.STATS_BYTES, dtype=torch.uint8, device=dev)
     evk = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     s80 = src80.ft_csc()
+    flags = dl.launch_flags(src80)
     ta_c, tb_c = ta.ft_tiled(), tb.ft_tiled()      # the pools may have grown
     if lib.ft_tiled_from_csc(ctypes.byref(s80), ctypes.byref(tb_c), dt_code, wp, wn,
                              ctypes.c_void_p(comp_rec.data_ptr()), sh):

@@ -79,6 +79,13 @@ extern "C" {
                               active-set stepping -- a column whose closed
                               one-ring did not change in the previous step is
                               not recomputed (its value is already in place)  */
+#define FT_HINT_DENSE_BAND 16 /* performance hint only (results are identical
+                              with or without it): the field's band is dense
+                              -- many columns with three layer rows in their
+                              one-ring (reference configs[4], 65,536 seeds on
+                              10M vertices) -- so the three-row kernel trades
+                              registers for occupancy.  The Python layer sets
+                              it when nnz - n_cols >= 2^21                   */
 
 /* status codes written into ft_step_stats.status / evolve control[1] */
 #define FT_STATUS_OK           0

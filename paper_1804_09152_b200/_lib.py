@@ -28,6 +28,7 @@ FT_LAP_UNIFORM = 1
 FT_LAP_PACKED = 2
 FT_LAP_CHECK_FINITE = 4
 FT_LAP_SYMMETRIC = 8
+FT_HINT_DENSE_BAND = 16
 
 FT_PHASE_COLUMNS = 1
 FT_PHASE_FINALIZE = 2

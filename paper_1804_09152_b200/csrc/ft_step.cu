@@ -685,7 +685,7 @@ __device__ __forceinline__ long long pool_take_warp(const StepParams& p, int j, 
 // rlo < rmid < rhi accumulated in L order, then the generic window update
 // (process_window<3>).  Anything wider goes on to the warp kernel.
 
-template <typename T, bool UNIFORM, bool PACKED>
+template <typename T, bool UNIFORM, bool PACKED, bool OWN>
 __device__ __forceinline__ void wide3_column(const StepParams& p, int j, bool have, bool full, unsigned char nxt,
                                              int lane, Acc& acc, long long* s_bm, int4 pk) {
     const int jl = j - p.j_base;
@@ -754,12 +754,33 @@ __device__ __forceinline__ void wide3_column(const StepParams& p, int j, bool ha
                 const int r = rr[k][t];
                 if (r == INT_MAX) continue;
                 const double a = hyb_val<T>(p.in, u[k], sg[k], ax[k], t);
-                if (k == kd) { oj[t] = a; orr[t] = r; }
-                if (r == rlo) { l0 = l0 + a * l; if (k == kd) p0 = a; }
-                else if (r == rhi) { l2 = l2 + a * l; if (k == kd) p2 = a; }
-                else { l1 = l1 + a * l; if (k == kd) p1 = a; }
+                if (OWN) {
+                    if (r == rlo) l0 = l0 + a * l;
+                    else if (r == rhi) l2 = l2 + a * l;
+                    else l1 = l1 + a * l;
+                } else {
+                    if (k == kd) { oj[t] = a; orr[t] = r; }
+                    if (r == rlo) { l0 = l0 + a * l; if (k == kd) p0 = a; }
+                    else if (r == rhi) { l2 = l2 + a * l; if (k == kd) p2 = a; }
+                    else { l1 = l1 + a * l; if (k == kd) p1 = a; }
+                }
             }
-            if (k == kd) { sgj = sg[k]; axj = ax[k]; }
+            if (!OWN && k == kd) { sgj = sg[k]; axj = ax[k]; }
+        }
+        if (OWN) {
+        // the column's own entries (<= 3, rows ascending, a subset of
+        // rlo / rmid / rhi), re-read (L1) instead of tracked through the
+        // neighbour loop: PHI(r, j) per window row.  Fewer registers (117
+        // against 128), which the dense-band variant's fifth CTA per SM needs
+        sgj = __ldg(&p.in.sig[j]);
+        axj = (sgj >= kPair || sgj <= -3) ? __ldg(&p.in.aux[j]) : 0;
+        const int cj = sig_count(sgj);
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+            if (t < cj) { orr[t] = hyb_row<T>(p.in, sgj, axj, t); oj[t] = hyb_val<T>(p.in, j, sgj, axj, t); }
+        p0 = orr[0] == rlo ? oj[0] : 0.0;
+        p1 = rmid == INT_MAX ? 0.0 : (orr[0] == rmid ? oj[0] : (orr[1] == rmid ? oj[1] : 0.0));
+        p2 = orr[0] == rhi ? oj[0] : (orr[1] == rhi ? oj[1] : (orr[2] == rhi ? oj[2] : 0.0));
         }
     }
     Win<3> w;
@@ -847,8 +868,13 @@ constexpr int kWide3TPB = 128;
 #define FT_W3_MINB 4
 #endif
 
-template <typename T, bool UNIFORM, bool PACKED>
-__global__ void __launch_bounds__(kWide3TPB, FT_W3_MINB) wide3_kernel(const StepParams p) {
+// FT_HINT_DENSE_BAND: 5 CTAs per SM (96 registers, a few spills) and the
+// own-entry re-read -- +4 % at C5 (1.7M listed columns, ~18 passes of the
+// grid), -0.7 % at C3 (190K, ~2 passes), so it is chosen by the hint
+constexpr int kWide3DenseMinB = 5;
+
+template <typename T, bool UNIFORM, bool PACKED, bool OWN>
+__device__ __forceinline__ void wide3_body(const StepParams& p) {
     pdl_wait();
     Control* ctl = p.ws.ctl;
     __shared__ long long s_bm[4];
@@ -878,7 +904,7 @@ __global__ void __launch_bounds__(kWide3TPB, FT_W3_MINB) wide3_kernel(const Step
         const int jn = hn ? __ldg(&p.ws.wide[in]) : p.j_base;
         int4 pn = make_int4(0, 0, 0, 0);
         if (PACKED && hn) pn = __ldg(&p.lap_pack[jn - p.j_base]);
-        wide3_column<T, UNIFORM, PACKED>(p, j, have, full, nxt, lane, acc, s_bm, pk);
+        wide3_column<T, UNIFORM, PACKED, OWN>(p, j, have, full, nxt, lane, acc, s_bm, pk);
         i = in;
         have = hn;
         j = jn;
@@ -886,6 +912,16 @@ __global__ void __launch_bounds__(kWide3TPB, FT_W3_MINB) wide3_kernel(const Step
     }
     __syncthreads();
     acc_flush<kWide3TPB>(acc, s_bm, s_md, s_cnt, ctl);
+}
+
+template <typename T, bool UNIFORM, bool PACKED>
+__global__ void __launch_bounds__(kWide3TPB, FT_W3_MINB) wide3_kernel(const StepParams p) {
+    wide3_body<T, UNIFORM, PACKED, false>(p);
+}
+
+template <typename T, bool UNIFORM, bool PACKED>
+__global__ void __launch_bounds__(kWide3TPB, kWide3DenseMinB) wide3_dense_kernel(const StepParams p) {
+    wide3_body<T, UNIFORM, PACKED, true>(p);
 }
 
 // ---------------------------------------------------------------------------
@@ -2191,8 +2227,13 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     if (bg > need_b) bg = need_b;
     if (kmask & 2) launch_dep(FT_PICK3(ft::band_kernel, dtype, uni, packed), bg, ft::kBandTPB, s, p);
     if (ev) cudaEventRecord(ev[1], s);
-    if (kmask & 4)
-        launch_dep(FT_PICK3(ft::wide3_kernel, dtype, uni, packed), FT_W3_MINB * d.sms, ft::kWide3TPB, s, p);
+    if (kmask & 4) {
+        if (lap_flags & FT_HINT_DENSE_BAND)
+            launch_dep(FT_PICK3(ft::wide3_dense_kernel, dtype, uni, packed), ft::kWide3DenseMinB * d.sms,
+                       ft::kWide3TPB, s, p);
+        else
+            launch_dep(FT_PICK3(ft::wide3_kernel, dtype, uni, packed), FT_W3_MINB * d.sms, ft::kWide3TPB, s, p);
+    }
     if (ev) cudaEventRecord(ev[2], s);
     if (kmask & 8) {
         launch_dep(FT_PICK3(ft::wide4_kernel, dtype, uni, packed), FT_W4_MINB * d.sms, ft::kWide4TPB, s, p);

@@ -330,10 +330,14 @@ class _DeviceLap:
         self.n_csr = 0         # columns the pack leaves to the CSR
         self.renum = None      # the same Laplacian in a locality order (device meshes), or None
 
-    def launch_flags(self):
+    def launch_flags(self, phi=None):
+        """FT_LAP_* for the step entry points, plus FT_HINT_DENSE_BAND when
+        the input field ``phi`` (a DeviceCSC) carries a dense band."""
         f = self.flags | (_lib.FT_LAP_PACKED if self.pack is not None else 0)
         if self.symmetric and ACTIVE_SET:
             f |= _lib.FT_LAP_SYMMETRIC
+        if phi is not None and phi.nnz - phi.n_cols >= DENSE_BAND_EXTRA:
+            f |= _lib.FT_HINT_DENSE_BAND
         return f
 
     def ft_csc(self, precision):
@@ -481,6 +485,10 @@ POOL_FRACTION = 0.25    # pool of a hybrid buffer (columns with > 2 entries), re
 PACK_LAPLACIAN = True   # uniform Laplacians: packed neighbour table (one 16-byte load per column)
 POOL_MIN = 4096
 ACTIVE_SET = os.environ.get("FT_ACTIVE_SET", "1") != "0"   # active-set stepping (symmetric L^T)
+# entries beyond one per column at which the step runs its dense-band
+# variant of the three-row kernel (FT_HINT_DENSE_BAND; speed only): C3
+# (4,096 seeds on 10M vertices) carries ~0.9M, C5 (65,536 seeds) ~3.5M
+DENSE_BAND_EXTRA = int(os.environ.get("FT_DENSE_BAND_EXTRA", str(1 << 21)))
 
 
 class StepWorkspace:
@@ -626,7 +634,7 @@ def step(field, lap, params, workspace=None):
     phase_ms = (ctypes.c_float * 5)()
     while True:
         in_c, si_c, sc_c, out_c = dphi.ft_csc(), scratch_in.ft_tiled(), scratch.ft_tiled(), out.ft_csc()
-        rc = lib.ft_step_phases(ctypes.byref(lap_c), dl.launch_flags(), ctypes.byref(in_c), ctypes.byref(si_c),
+        rc = lib.ft_step_phases(ctypes.byref(lap_c), dl.launch_flags(dphi), ctypes.byref(in_c), ctypes.byref(si_c),
                                 ctypes.byref(sc_c), ctypes.byref(out_c), _ft_dtype(field.precision),
                                 ctypes.byref(prm), wp, wn, ctypes.c_void_p(ws.stats.data_ptr()), phase_ms, stream)
         _check(rc, "ft_step_phases")
@@ -744,7 +752,7 @@ def _evolve_device(field, lap, params, max_steps, tol, ws, base_threshold, local
         remaining = max_steps - done
         s_c, a_c, b_c, o_c = cur.ft_csc(), wa.ft_tiled(), wb.ft_tiled(), out.ft_csc()
         ev0.record()
-        rc = lib.ft_evolve(ctypes.byref(lap_c), dl.launch_flags(), ctypes.byref(s_c), ctypes.byref(a_c),
+        rc = lib.ft_evolve(ctypes.byref(lap_c), dl.launch_flags(cur), ctypes.byref(s_c), ctypes.byref(a_c),
                            ctypes.byref(b_c), ctypes.byref(o_c), _ft_dtype(field.precision),
                            ctypes.byref(prm), remaining, float(tol), float(base_threshold),
                            wp, wn, ctypes.c_void_p(trace_dev.data_ptr()),

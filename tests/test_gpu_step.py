@@ -486,3 +486,27 @@ def test_four_row_kernel_bitwise(monkeypatch, subdiv, n_seeds):
         cur, _st = ft.step(cur, lap, DEFAULT)
     ref12, _ = po.evolve_c(po.Csc.of(fld.phi), lt, DEFAULT, 12, n_threads=4)
     assert_csc_equal(cur.phi, ref12)
+
+
+@pytest.mark.parametrize("subdiv,n_seeds", [(4, 64), (5, 400)])
+def test_dense_band_hint_bitwise(monkeypatch, subdiv, n_seeds):
+    """FT_HINT_DENSE_BAND (the three-row kernel's dense-band variant: more
+    CTAs per SM, the column's own entries re-read) changes speed only:
+    forced on for every field (DENSE_BAND_EXTRA = 0), evolve and the step
+    loop are bitwise the C oracle's."""
+    monkeypatch.setattr(ft.field, "DENSE_BAND_EXTRA", 0)
+    mesh = ft.gen_icosphere(subdiv)
+    lap = ft.build_laplacian(mesh)
+    seeds = np.random.default_rng(1).choice(mesh.n_vertices, n_seeds, replace=False)
+    fld = ft.init_field(mesh, seeds)
+    assert ft.field.device_laplacian(lap, "exact").launch_flags(fld.device_phi()) & ft._lib.FT_HINT_DENSE_BAND
+    out, trace = ft.evolve(fld, lap, DEFAULT, max_steps=40, tol=0.0)
+    lt = po.Csc.of(ft.field._with_diagonal(lap.mat_t))
+    ref, rtrace = po.evolve_c(po.Csc.of(fld.phi), lt, DEFAULT, 40, n_threads=4)
+    assert_csc_equal(out.phi, ref)
+    assert [s.max_delta for s in trace] == [s["max_delta"] for s in rtrace]
+    cur = fld
+    for _ in range(6):
+        cur, _st = ft.step(cur, lap, DEFAULT)
+    ref6, _ = po.evolve_c(po.Csc.of(fld.phi), lt, DEFAULT, 6, n_threads=4)
+    assert_csc_equal(cur.phi, ref6)

@@ -38,7 +38,7 @@ tb = ft.DeviceTiled(src.n_rows, n, cap, src.values.dtype, dev)
 dl = F.device_laplacian(lap, args.precision)
 lib = _lib.lib()
 lc, prm, sh = dl.ft_csc(args.precision), ft.CouplingParams().ft_params(), F._stream_handle()
-fl = dl.launch_flags()
+fl = dl.launch_flags(src)
 dt = F._ft_dtype(args.precision)
 wp, wn = ws.ws_args()
 rec = torch.zeros(64, dtype=torch.uint8, device=dev)
