@@ -588,7 +588,10 @@ __device__ __forceinline__ void band_column(const StepParams& p, int jl, bool ha
     bm_fold(fin_here ? bm_new : 0.0, fin_here ? bm_old : 0.0, full, s_bm);
 }
 
-template <typename T, bool UNIFORM, bool PACKED, int MINB = 4>
+#ifndef FT_BAND_MINB
+#define FT_BAND_MINB 4
+#endif
+template <typename T, bool UNIFORM, bool PACKED, int MINB = FT_BAND_MINB>
 __global__ void __launch_bounds__(kBandTPB, MINB) band_kernel(const StepParams p) {
     pdl_wait();
     Control* ctl = p.ws.ctl;
