@@ -381,7 +381,8 @@ class TorchTransport:
         (r,) = ranks
         d = self.dist
         # gloo cannot send device tensors: stage the messages through the host
-        host = not self.nccl and any(t.device.type != "cpu" for t in r.send_msg.values())
+        host = not self.nccl and any(t.device.type != "cpu"
+                                     for t in list(r.send_msg.values()) + list(r.recv_msg.values()))
         recv = {q: (t.cpu() if host else t) for q, t in r.recv_msg.items()}
         ops = []
         for q in r.plan.peers:
