@@ -11,3 +11,4 @@ timeout 600 python bench.py > gpurun_out/f_bench_c3.json 2> gpurun_out/f_bench_c
 timeout 600 python bench.py --seeds 65536 > gpurun_out/f_bench_c5.json 2> gpurun_out/f_bench_c5.err
 timeout 600 python bench.py --precision fast > gpurun_out/f_bench_fast.json 2> gpurun_out/f_bench_fast.err
 timeout 900 python bench.py --mesh ico12 --seeds 16384 > gpurun_out/f_bench_c4.json 2> gpurun_out/f_bench_c4.err
+timeout 900 python bench.py --impl reference > gpurun_out/f_bench_ref.json 2> gpurun_out/f_bench_ref.err
