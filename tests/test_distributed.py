@@ -539,3 +539,52 @@ def test_two_processes_torch_transport_match_single_gpu():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}
+
+
+def _gpu_gloo_lloyd_worker(rank, world, port, out_q):
+    """Partitioned Lloyd (all-reduce exchange) with one rank per process on
+    cuda:0, messages through the host (gloo): per-cell sums, best-hit keys
+    and the collision fallback cross real process boundaries."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        mesh = ft.gen_icosphere(4)
+        seeds = ft.sample_seed_vertices(mesh, 40, 6)
+        lap = ft.build_laplacian(mesh)
+        part = D.Partition.even(mesh.n_vertices, world)
+        got = D.lloyd_iterate_partitioned(ft.LloydState(seeds=np.array(seeds)), mesh, lap, ft.CouplingParams(),
+                                          2, D.TorchTransport(), part, [rank], max_steps=60, tol=1e-4,
+                                          exchange="allreduce")
+        whole = got.field.gather().phi
+        if rank == 0:
+            ref = ft.lloyd_iterate(ft.LloydState(seeds=np.array(seeds)), mesh, lap, ft.CouplingParams(),
+                                   n_iter=2, max_steps=60, tol=1e-4)
+            assert np.array_equal(np.asarray(got.seeds), np.asarray(ref.seeds))
+            for a, b in zip(got.history, ref.history):
+                for key in ("iteration", "seeds", "steps", "reseed_misses", "seed_collisions"):
+                    assert a[key] == b[key], key
+                assert np.allclose(a["cell_areas"], b["cell_areas"], rtol=1e-12, atol=0)
+            _assert_same_field(whole, ref.field.phi)
+        out_q.put((rank, "ok"))
+    except Exception as exc:                    # pragma: no cover - reported to the parent
+        out_q.put((rank, repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_processes_partitioned_lloyd_allreduce():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_gloo_lloyd_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=400) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}
