@@ -393,24 +393,21 @@ __global__ void __launch_bounds__(kPrepTPB) prep_kernel(const StepParams p) {
     __syncthreads();
     if (cnt == 0) return;
     int base = s_base + s_warp[wi];
+    const unsigned int lt = (1u << lane) - 1u;
 #pragma unroll
     for (int r = 0; r < kPrepRounds; ++r) {
-        unsigned int m = (unsigned int)(mm >> (4 * r)) & 15u;
+        const unsigned int m = (unsigned int)(mm >> (4 * r)) & 15u;
         const int c = __popc(m);
-        int incl = c;
+        // the lanes' exclusive prefix of c (0..4) from the ballots of its
+        // three bits, no shuffle scan
+        const unsigned int b0 = __ballot_sync(kFull, c & 1), b1 = __ballot_sync(kFull, c & 2),
+                           b2 = __ballot_sync(kFull, c & 4);
+        const int pos = base + __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
+        base += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
+        const int jw = cw + 128 * r + 4 * lane - g_lo;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += y;
-        }
-        int pos = base + incl - c;
-        base += __shfl_sync(kFull, incl, 31);
-        const int jw = cw + 128 * r + 4 * lane;
-        while (m) {
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            p.ws.act[pos++] = jw + b - g_lo;
-        }
+        for (int b = 0; b < 4; ++b)     // ascending columns, predicated stores
+            if (m & (1u << b)) p.ws.act[pos + __popc(m & ((1u << b) - 1u))] = jw + b;
     }
 }
 
