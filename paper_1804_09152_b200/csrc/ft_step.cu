@@ -29,11 +29,15 @@
 //   wide3_kernel   the listed columns, one lane each: up to three rows and
 //                  three entries per neighbour (process_window<3>); wider
 //                  ones are listed again;
-//   wide_kernel    those, one warp each: the neighbourhood staged in shared
-//                  memory and ranked by row, Lt and the column sums taken in
-//                  the reference's order; beyond the staging capacity the
-//                  exact windowed algorithm from global memory;
-//   finalize       statistics record, status, convergence, next-step mode.
+//   wide4_kernel   (when they are many) those, one lane each: up to four
+//                  rows and four entries per neighbour (process_window<4>);
+//   wide_kernel    the rest, one warp each: the neighbourhood staged in
+//                  shared memory and ranked by row, Lt and the column sums
+//                  taken in the reference's order; beyond the staging
+//                  capacity the column is listed for the deep pass;
+//   finalize       the deep pass (the exact windowed algorithm from global
+//                  memory, one lane per listed column; rare), then the
+//                  statistics record, status, convergence, next-step mode.
 //
 // Statistics are order-independent -- integer nnz / skeleton counts, a max,
 // and the base mass in exact fixed point (ft_common.cuh fx_split) -- so an
@@ -1638,23 +1642,25 @@ __global__ void __launch_bounds__(kWideTPB, FT_WIDE_MINB) wide_kernel(const Step
 // windowed algorithm from global memory
 constexpr int kDeepTPB = 32;
 
+// the deep columns (listed in act by the warp kernel) by one warp, one lane
+// each: run by the finalize kernel before its totals (they are rare -- none
+// at C3-C5 -- and a kernel of their own cost a launch per step, ~1 %)
 template <typename T, bool UNIFORM>
-__global__ void __launch_bounds__(kDeepTPB) deep_kernel(const StepParams p) {
-    pdl_wait();
+__device__ __forceinline__ void deep_pass(const StepParams& p) {
     Control* ctl = p.ws.ctl;
     __shared__ long long s_bm[4];
     __shared__ double s_md[1];
     __shared__ long long s_cnt[2];
     if (p.check_done && vload(&ctl->done)) return;
     const int nd = vload(&ctl->n_deep);
-    if ((int)blockIdx.x * kDeepTPB >= nd) return;
+    if (nd == 0) return;                    // block-uniform
     if (threadIdx.x < 4) s_bm[threadIdx.x] = 0;
     __syncthreads();
     const bool full = step_is_full(p);
     const unsigned char nxt = (unsigned char)(vload(&ctl->seq) + 1);
     Acc acc;
     acc_init(acc);
-    for (int i0 = blockIdx.x * kDeepTPB; i0 < nd; i0 += gridDim.x * kDeepTPB) {
+    for (int i0 = 0; i0 < nd; i0 += kDeepTPB) {
         const int i = i0 + threadIdx.x;
         double bm_new = 0.0, bm_old = 0.0;
         if (i < nd) deep_column<T, UNIFORM>(p, __ldg(&p.ws.act[i]), full, nxt, acc, bm_new, bm_old);
@@ -1662,12 +1668,12 @@ __global__ void __launch_bounds__(kDeepTPB) deep_kernel(const StepParams p) {
         bm_fold(bm_new, bm_old, full, s_bm);
     }
     __syncthreads();
-    acc_flush<kDeepTPB>(acc, s_bm, s_md, s_cnt, ctl);
+    acc_flush<kDeepTPB>(acc, s_bm, s_md, s_cnt, ctl);   // thread 0's atomics precede its reads below
 }
 
 // ---------------------------------------------------------------------------
-// finalize: statistics record, error / convergence flags, the next step's
-// mode, accumulator reset (one thread)
+// finalize: the deep columns (one warp), then statistics record, error /
+// convergence flags, the next step's mode, accumulator reset (one thread)
 
 struct FinalizeParams {
     Workspace ws;
@@ -1681,10 +1687,13 @@ struct FinalizeParams {
     long long next_cap;   // pool capacity of the next step's target (this step's input)
 };
 
-__global__ void finalize_kernel(const FinalizeParams f) {
+template <typename T, bool UNIFORM>
+__global__ void __launch_bounds__(kDeepTPB) finalize_kernel(const FinalizeParams f, const StepParams p) {
     pdl_wait();
     Control* ctl = f.ws.ctl;
     if (f.evolve && vload(&ctl->done)) return;
+    deep_pass<T, UNIFORM>(p);
+    if (threadIdx.x != 0) return;
     const bool full = !f.track || ctl->full != 0;
     long long nnz = ctl->acc_nnz, skel = ctl->acc_skel;
     long long bm[4];
@@ -2171,9 +2180,12 @@ static void lib_init() {
 // the whole field, otherwise the owned column range of a partitioned field
 // (lap_t then holds the owned columns of L^T only and the workspace is sized
 // for the owned columns; every step is a full step).
+// `keep` receives the step's parameters (the finalize kernel's deep pass
+// reads them); launch == false only validates and fills them.
 static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled* in, ft_tiled* out, int out_id,
                           int32_t dtype, const ft_params* prm, void* workspace, size_t ws_bytes, int check_done,
-                          cudaStream_t s, const ft_domain* dom = nullptr, const cudaEvent_t* ev = nullptr) {
+                          cudaStream_t s, const ft_domain* dom = nullptr, const cudaEvent_t* ev = nullptr,
+                          ft::StepParams* keep = nullptr, bool launch = true) {
     if (!lap_t || !out || !in || !prm || !workspace) return set_err(FT_ERR_ARG, "null argument");
     if (dtype != FT_F64 && dtype != FT_F32) return set_err(FT_ERR_ARG, "bad dtype");
     const int n_rows = in->n_rows, n_v = in->n_cols;
@@ -2215,6 +2227,8 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     const char* w4 = getenv("FT_WIDE4_MIN");     // tests: exercise the four-row kernel on small fields
     p.wide4_min = w4 ? atoi(w4) : ft::kWide4Min;
     lib_init();
+    if (keep) *keep = p;
+    if (!launch) return FT_OK;
     DevState& d = dev_state();
     const char* kenv = getenv("FT_KERNELS");   // debug: bit mask of the column kernels to launch
     const int kmask = kenv ? atoi(kenv) : 15;
@@ -2238,14 +2252,16 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     if (kmask & 8) {
         launch_dep(FT_PICK3(ft::wide4_kernel, dtype, uni, packed), FT_W4_MINB * d.sms, ft::kWide4TPB, s, p);
         launch_dep(FT_PICK3(ft::wide_kernel, dtype, uni, packed), 8 * d.sms, ft::kWideTPB, s, p);
-        launch_dep(FT_PICK2(ft::deep_kernel, dtype, uni), 64, ft::kDeepTPB, s, p);
     }
     if (ev) cudaEventRecord(ev[3], s);
     return cuda_check("step kernels");
 }
 
+// the finalize kernel (with the deep pass of the step `p`, launched by
+// launch_columns with the same arguments)
 static void launch_finalize(const ft::Workspace& ws, ft_step_stats* trace, long long tiled_cap, int evolve,
-                            int lap_flags, int out_id, long long next_cap, bool domain, cudaStream_t s) {
+                            int lap_flags, int out_id, long long next_cap, bool domain, cudaStream_t s,
+                            const ft::StepParams& p, int32_t dtype) {
     ft::FinalizeParams f;
     f.ws = ws; f.trace = trace; f.tiled_cap = tiled_cap; f.fixed_slot = evolve ? 0 : 1;
     f.evolve = evolve;
@@ -2253,7 +2269,8 @@ static void launch_finalize(const ft::Workspace& ws, ft_step_stats* trace, long 
     (void)domain;
     f.out_id = out_id;
     f.next_cap = next_cap;
-    launch_dep(ft::finalize_kernel, 1, 1, s, f);
+    const bool uni = (lap_flags & FT_LAP_UNIFORM) != 0;
+    launch_dep(FT_PICK2(ft::finalize_kernel, dtype, uni), 1, ft::kDeepTPB, s, f, p);
 }
 
 static int launch_convert(const ft_csc* src, ft_tiled* dst, int32_t dtype, const ft::Workspace& ws,
@@ -2307,9 +2324,12 @@ extern "C" int ft_step_run(const ft_csc* lap_t, int32_t lap_flags, const ft_tile
     if (phases & FT_PHASE_FINALIZE) {
         if (!stats || !in || !out || !workspace) return set_err(FT_ERR_ARG, "null argument");
         if (ws_bytes < ft::workspace_bytes(in->n_cols)) return set_err(FT_ERR_ARG, "workspace too small");
-        lib_init();
+        ft::StepParams p;
+        const int rc = launch_columns(lap_t, lap_flags, in, out, out_id, dtype, params, workspace, ws_bytes, 0, s,
+                                      nullptr, nullptr, &p, false);
+        if (rc != FT_OK) return rc;
         launch_finalize(ft::carve_workspace(workspace, in->n_cols), stats, out->capacity, 0, lap_flags, out_id,
-                        in->capacity, false, s);
+                        in->capacity, false, s, p, dtype);
     }
     return cuda_check("ft_step_run");
 }
@@ -2360,11 +2380,12 @@ static int step_impl(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_i
     ft::nonfinite_reset_kernel<<<1, 1, 0, s>>>(ws.ctl);
     int rc = launch_convert(phi_in, scratch_in, dtype, ws, s);
     if (rc != FT_OK) return rc;
+    ft::StepParams p;
     rc = launch_columns(lap_t, lap_flags, scratch_in, scratch_out, 0, dtype, params, workspace, ws_bytes, 0, s,
-                        nullptr, ev ? ev + 1 : nullptr);
+                        nullptr, ev ? ev + 1 : nullptr, &p);
     if (rc != FT_OK) return rc;
     const long long cap = scratch_out->capacity < scratch_in->capacity ? scratch_out->capacity : scratch_in->capacity;
-    launch_finalize(ws, stats, cap, 0, lap_flags, 0, scratch_in->capacity, false, s);
+    launch_finalize(ws, stats, cap, 0, lap_flags, 0, scratch_in->capacity, false, s, p, dtype);
     // the compaction always runs; the host ignores it if the step failed
     ft::CompactParams c;
     fill_compact(c, scratch_out, nullptr, 0, phi_out, workspace);
@@ -2374,7 +2395,7 @@ static int step_impl(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_i
     if (rc != FT_OK || !ev) return rc;
     cudaEventRecord(ev[5], s);
     if (cudaEventSynchronize(ev[5]) != cudaSuccess) return set_err(FT_ERR_CUDA, "phase timing");
-    // ev: 0 start | convert + prep | 1 | band | 2 | wide3 | 3 | wide + deep | 4 | finalize + compact | 5
+    // ev: 0 start | convert + prep | 1 | band | 2 | wide3 | 3 | wide4 + wide | 4 | finalize (+ deep) + compact | 5
     for (int k = 0; k < 5; ++k) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
@@ -2436,9 +2457,11 @@ extern "C" int ft_evolve(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* p
     auto step = [&](int i, cudaStream_t ms) -> int {
         ft_tiled* out = (i & 1) ? work_b : work_a;
         const ft_tiled* in_t = (i & 1) ? work_a : work_b;
-        const int r = launch_columns(lap_t, lap_flags, in_t, out, i & 1, dtype, params, workspace, ws_bytes, 1, ms);
+        ft::StepParams p;
+        const int r = launch_columns(lap_t, lap_flags, in_t, out, i & 1, dtype, params, workspace, ws_bytes, 1, ms,
+                                     nullptr, nullptr, &p);
         if (r != FT_OK) return r;
-        launch_finalize(ws, trace, out->capacity, 1, lap_flags, i & 1, in_t->capacity, false, ms);
+        launch_finalize(ws, trace, out->capacity, 1, lap_flags, i & 1, in_t->capacity, false, ms, p, dtype);
         return FT_OK;
     };
     ft::evolve_reset_kernel<<<1, 1, 0, s>>>(ws.ctl, max_steps, tol, base_threshold);
@@ -2524,11 +2547,12 @@ extern "C" int ft_domain_step(const ft_csc* lap_rows, int32_t lap_flags, const f
     if (!in || !dom || !record) return set_err(FT_ERR_ARG, "null argument");
     cudaStream_t s = (cudaStream_t)stream;
     const int out_id = dom->out_id & 1;
+    ft::StepParams p;
     const int rc = launch_columns(lap_rows, lap_flags, in, out, out_id, dtype, params, workspace, ws_bytes, 1, s,
-                                  dom);
+                                  dom, nullptr, &p);
     if (rc != FT_OK) return rc;
     launch_finalize(ft::carve_workspace(workspace, in->n_cols), record, dom->step_capacity, 0, lap_flags, out_id,
-                    dom->step_capacity, true, s);
+                    dom->step_capacity, true, s, p, dtype);
     return cuda_check("ft_domain_step");
 }
 
