@@ -226,9 +226,12 @@ int ft_step_phases(const ft_csc* lap_t, int32_t lap_flags, const ft_csc* phi_in,
  * work_b = 1), starting after ft_tiled_from_csc into buffer 1.
  *   FT_PHASE_COLUMNS   the column kernels: active list, band kernel (one
  *                      lane per column: closed form / two-row update), the
- *                      warp-cooperative and serial kernels for wide columns;
- *   FT_PHASE_FINALIZE  the statistics record into `stats` (device), the
- *                      next step's mode.
+ *                      three- and four-row lane kernels and the
+ *                      warp-cooperative kernel for wide columns;
+ *   FT_PHASE_FINALIZE  the serial pass over the columns beyond the warp
+ *                      kernel's staging capacity (rare), the statistics
+ *                      record into `stats` (device), the next step's mode.
+ * Both phases take the same arguments (the finalize pass reads the step's). 
  * ft_evolve issues exactly this sequence. */
 #define FT_PHASE_COLUMNS  1
 #define FT_PHASE_FINALIZE 2
