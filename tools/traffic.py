@@ -3,7 +3,7 @@ column kernels (the `traffic` figure bench.py reports beside the roofline):
 
     ncu --profile-from-start off --cache-control none --clock-control none \\
         --metrics dram__bytes_read.sum,dram__bytes_write.sum \\
-        -k regex:"prep_kernel|band_kernel|wide3_kernel|wide_kernel|deep_kernel" \\
+        -k regex:"prep_kernel|band_kernel|wide3_kernel|wide4_kernel|wide_kernel|finalize_kernel" \\
         --csv --log-file traffic.csv python tools/prof_window.py --steps 8
     python tools/traffic.py traffic.csv 8 > profiles/step_kernel_traffic.json
 
@@ -37,7 +37,7 @@ print(json.dumps({
     "dram_bytes_per_step": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
     "per_kernel": {k: {"read": v["dram__bytes_read.sum"], "write": v["dram__bytes_write.sum"]}
                    for k, v in per_kernel.items()},
-    "kernels": "one step's column kernels: prep, band, wide3, wide, deep",
+    "kernels": "one step's kernels: prep, band, wide3, wide4, wide, finalize (with the deep pass)",
     "window": f"C3 steps 83..{82 + steps} (tools/prof_window.py)",
     "note": "ncu --cache-control none: L2 carries over between kernels as in the pipeline; per step, "
             "averaged over the window"}, indent=1))
