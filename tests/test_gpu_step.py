@@ -510,3 +510,17 @@ def test_dense_band_hint_bitwise(monkeypatch, subdiv, n_seeds):
         cur, _st = ft.step(cur, lap, DEFAULT)
     ref6, _ = po.evolve_c(po.Csc.of(fld.phi), lt, DEFAULT, 6, n_threads=4)
     assert_csc_equal(cur.phi, ref6)
+
+
+def test_dense_band_hint_fast_identical(monkeypatch):
+    """FAST (fp32 storage) through the dense-band variant: the same bits
+    with and without the hint."""
+    mesh = ft.gen_icosphere(5)
+    lap = ft.build_laplacian(mesh)
+    seeds = np.random.default_rng(2).choice(mesh.n_vertices, 400, replace=False)
+    fld = ft.init_field(mesh, seeds, precision="fast")
+    plain, tp = ft.evolve(fld, lap, DEFAULT, max_steps=30, tol=0.0)
+    monkeypatch.setattr(ft.field, "DENSE_BAND_EXTRA", 0)
+    hinted, th = ft.evolve(fld, lap, DEFAULT, max_steps=30, tol=0.0)
+    assert_csc_equal(hinted.phi, plain.phi)
+    assert [s.max_delta for s in th] == [s.max_delta for s in tp]
