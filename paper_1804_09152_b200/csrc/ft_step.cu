@@ -870,15 +870,18 @@ __device__ __forceinline__ void wide3_column(const StepParams& p, int j, bool ha
     bm_fold(bm_new, bm_old, full, s_bm);
 }
 
-constexpr int kWide3TPB = 128;
+#ifndef FT_W3_TPB
+#define FT_W3_TPB 128
+#endif
+constexpr int kWide3TPB = FT_W3_TPB;
 #ifndef FT_W3_MINB
-#define FT_W3_MINB 4
+#define FT_W3_MINB (512 / FT_W3_TPB)
 #endif
 
 // FT_HINT_DENSE_BAND: 5 CTAs per SM (96 registers, a few spills) and the
 // own-entry re-read -- +4 % at C5 (1.7M listed columns, ~18 passes of the
 // grid), -0.7 % at C3 (190K, ~2 passes), so it is chosen by the hint
-constexpr int kWide3DenseMinB = 5;
+constexpr int kWide3DenseMinB = 640 / FT_W3_TPB;
 
 template <typename T, bool UNIFORM, bool PACKED, bool OWN>
 __device__ __forceinline__ void wide3_body(const StepParams& p) {
@@ -940,7 +943,10 @@ __global__ void __launch_bounds__(kWide3TPB, kWide3DenseMinB) wide3_dense_kernel
 // process_window<4>; anything wider goes on to the warp kernel (the wide[]
 // list, consumed by then).
 
-constexpr int kWide4TPB = 128;
+#ifndef FT_W4_TPB
+#define FT_W4_TPB 128
+#endif
+constexpr int kWide4TPB = FT_W4_TPB;
 // below this many leftovers of the three-row kernel the warp kernel takes
 // them all directly (few columns: one warp each finishes sooner than a
 // latency-bound lane-per-column pass followed by the warp kernel)
@@ -1047,7 +1053,7 @@ __device__ __forceinline__ void widek_column(const StepParams& p, int j, bool ha
 
 template <typename T, bool UNIFORM, bool PACKED>
 #ifndef FT_W4_MINB
-#define FT_W4_MINB 6      // 80 registers: six CTAs per SM (+1.6 % at C5 over 4)
+#define FT_W4_MINB (768 / FT_W4_TPB)      // 80 registers: 768 threads per SM (+1.6 % at C5 over 512)
 #endif
 __global__ void __launch_bounds__(kWide4TPB, FT_W4_MINB) wide4_kernel(const StepParams p) {
     pdl_wait();
@@ -1235,7 +1241,10 @@ __device__ __forceinline__ double base_of(const HybIn& h, int j) {
 // is lane-parallel.  A neighbourhood beyond the staging capacity runs the
 // exact windowed algorithm (vertex_slow) from global memory on lane 0.
 
-constexpr int kWideTPB = 128;
+#ifndef FT_WIDE_TPB
+#define FT_WIDE_TPB 128
+#endif
+constexpr int kWideTPB = FT_WIDE_TPB;
 constexpr int kWideWarps = kWideTPB / 32;
 constexpr int kStageCap = 128;    // staged neighbourhood entries per warp
 
@@ -1609,7 +1618,7 @@ __device__ __forceinline__ void staged_column(const StepParams& p, int j, WideSt
 
 template <typename T, bool UNIFORM, bool PACKED>
 #ifndef FT_WIDE_MINB
-#define FT_WIDE_MINB 8      // 64 registers: eight CTAs per SM (both limits met, +1 % at C3)
+#define FT_WIDE_MINB (1024 / FT_WIDE_TPB)      // 64 registers: 1024 threads per SM (both limits met, +1 % at C3)
 #endif
 __global__ void __launch_bounds__(kWideTPB, FT_WIDE_MINB) wide_kernel(const StepParams p) {
     pdl_wait();
@@ -2254,7 +2263,7 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     if (ev) cudaEventRecord(ev[2], s);
     if (kmask & 8) {
         launch_dep(FT_PICK3(ft::wide4_kernel, dtype, uni, packed), FT_W4_MINB * d.sms, ft::kWide4TPB, s, p);
-        launch_dep(FT_PICK3(ft::wide_kernel, dtype, uni, packed), 8 * d.sms, ft::kWideTPB, s, p);
+        launch_dep(FT_PICK3(ft::wide_kernel, dtype, uni, packed), FT_WIDE_MINB * d.sms, ft::kWideTPB, s, p);
     }
     if (ev) cudaEventRecord(ev[3], s);
     return cuda_check("step kernels");
