@@ -333,7 +333,10 @@ __device__ __forceinline__ void wlist_flush(WarpList& l, int* g_count, int* g_li
 // only resets the target buffer's pool.
 
 constexpr int kPrepTPB = 256;
-constexpr int kPrepRounds = 16;
+#ifndef FT_PREP_ROUNDS
+#define FT_PREP_ROUNDS 16
+#endif
+constexpr int kPrepRounds = FT_PREP_ROUNDS;
 constexpr int kPrepCols = 4 * kPrepRounds;   // columns per thread
 
 __global__ void __launch_bounds__(kPrepTPB) prep_kernel(const StepParams p) {
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(kPrepTPB) prep_kernel(const StepParams p) {
     unsigned int x[kPrepRounds];
 #pragma unroll
     for (int r = 0; r < kPrepRounds; ++r) x[r] = s_tile[(tw + 128 * r) / 4 + lane];   // beyond g_hi: masked below
-    unsigned long long mm = 0;
+    unsigned long long mm[(kPrepRounds + 15) / 16] = {};
     int cnt = 0;
 #pragma unroll
     for (int r = 0; r < kPrepRounds; ++r) {
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(kPrepTPB) prep_kernel(const StepParams p) {
         const int hi = g_hi - jw, lo = g_lo - jw;                      // keep [g_lo, g_hi)
         if (hi < 4) m &= hi <= 0 ? 0u : (1u << hi) - 1u;
         if (lo > 0) m &= ~((1u << lo) - 1u);
-        mm |= (unsigned long long)m << (4 * r);
+        mm[r / 16] |= (unsigned long long)m << (4 * (r % 16));
         cnt += __popc(m);
     }
 #pragma unroll
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(kPrepTPB) prep_kernel(const StepParams p) {
     const unsigned int lt = (1u << lane) - 1u;
 #pragma unroll
     for (int r = 0; r < kPrepRounds; ++r) {
-        const unsigned int m = (unsigned int)(mm >> (4 * r)) & 15u;
+        const unsigned int m = (unsigned int)(mm[r / 16] >> (4 * (r % 16))) & 15u;
         const int c = __popc(m);
         // the lanes' exclusive prefix of c (0..4) from the ballots of its
         // three bits, no shuffle scan
