@@ -27,6 +27,20 @@ def test_library_exports_every_declared_symbol():
     assert set(syms) == set(_lib.EXPORTS)
 
 
+def test_header_constants_match_the_binding():
+    """Every #define FT_* integer of the header equals the constant of the
+    same name in _lib (flags, dtypes, status codes, phases, hints)."""
+    src = open(os.path.join(REPO, "include", "fieldtess_cuda.h")).read()
+    defs = dict(re.findall(r"^#define (FT_[A-Z0-9_]+)\s+(-?\d+)\b", src, flags=re.M))
+    assert "FT_HINT_DENSE_BAND" in defs and "FT_LAP_SYMMETRIC" in defs
+    for name, value in defs.items():
+        if hasattr(_lib, name):
+            assert getattr(_lib, name) == int(value), name
+    missing = [n for n in defs if n.startswith(("FT_LAP_", "FT_HINT_", "FT_STATUS_", "FT_PHASE_", "FT_F"))
+               and not hasattr(_lib, n)]
+    assert not missing, missing
+
+
 def test_abi_version_and_structs():
     lib = _lib.lib()
     assert lib.ft_abi_version() == _lib.ABI_VERSION
