@@ -2241,6 +2241,11 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     p.report_ids = dom ? dom->report_ids : nullptr;
     const char* w4 = getenv("FT_WIDE4_MIN");     // tests: exercise the four-row kernel on small fields
     p.wide4_min = w4 ? atoi(w4) : ft::kWide4Min;
+    // without the dense-band hint the four-row kernel is not launched (below
+    // its threshold it would be a no-op launch: +1.9 % at C3 without it) and
+    // the warp kernel takes every three-row leftover directly
+    const bool run_w4 = (lap_flags & FT_HINT_DENSE_BAND) || w4;
+    if (!run_w4) p.wide4_min = INT_MAX;
     lib_init();
     if (keep) *keep = p;
     if (!launch) return FT_OK;
@@ -2265,7 +2270,8 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     }
     if (ev) cudaEventRecord(ev[2], s);
     if (kmask & 8) {
-        launch_dep(FT_PICK3(ft::wide4_kernel, dtype, uni, packed), FT_W4_MINB * d.sms, ft::kWide4TPB, s, p);
+        if (run_w4)
+            launch_dep(FT_PICK3(ft::wide4_kernel, dtype, uni, packed), FT_W4_MINB * d.sms, ft::kWide4TPB, s, p);
         launch_dep(FT_PICK3(ft::wide_kernel, dtype, uni, packed), FT_WIDE_MINB * d.sms, ft::kWideTPB, s, p);
     }
     if (ev) cudaEventRecord(ev[3], s);
