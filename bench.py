@@ -634,11 +634,12 @@ def run_ours(args):
 
     if rank == 0:
         value = world * K / (elapsed_ms * 1e-3)
-        # launches of one ft_evolve call: reset, conversion (2), step 1 (6:
-        # prep, band, wide3, wide4, wide, finalize with the deep pass),
-        # ceil((K-1)/16) graph replays of 16 steps x 6 kernels (steps past K
+        # launches of one ft_evolve call: reset, conversion (2), step 1 (prep,
+        # band, wide3, [wide4: dense-band hint only], wide, finalize with the
+        # deep pass), ceil((K-1)/16) graph replays of 16 steps (steps past K
         # are device no-ops), report, compaction (3)
-        launches = 3 + 6 + 16 * 6 * -(-(K - 1) // 16) + 1 + 3
+        kps = 6 if flags & _lib.FT_HINT_DENSE_BAND else 5
+        launches = 3 + kps + 16 * kps * -(-(K - 1) // 16) + 1 + 3
         line = {
             "metric": METRIC,
             "value": value, "unit": "steps/s", "n_gpus": world, "steps": K, "warmup": W,
@@ -850,11 +851,11 @@ def run_partitioned(args, world, rank, local, emulate=0):
             "cpu_baseline": None,
             "e2e": e2e,
             "clocks": clk,
-            # per step and rank: the 6 launches of ft_domain_step (prep, band,
-            # wide3, wide4, wide, finalize), one pack per peer sent to, the
-            # combine, one unpack per peer received from; one control snapshot
-            # per 16-step chunk
-            "gpu_launches": (7 + len(r0.send_msg) + len(r0.recv_msg)) * K + -(-K // 16),
+            # per step and rank: the 5 launches of ft_domain_step (prep, band,
+            # wide3, wide, finalize; no dense-band hint on a rank), one pack
+            # per peer sent to, the combine, one unpack per peer received from;
+            # one control snapshot per 16-step chunk
+            "gpu_launches": (6 + len(r0.send_msg) + len(r0.recv_msg)) * K + -(-K // 16),
         }
         if emulate:
             line["emulated"] = True
