@@ -638,7 +638,7 @@ def run_ours(args):
         # band, wide3, [wide4: dense-band hint only], wide, finalize with the
         # deep pass), ceil((K-1)/16) graph replays of 16 steps (steps past K
         # are device no-ops), report, compaction (3)
-        kps = 6 if flags & _lib.FT_HINT_DENSE_BAND else 5
+        kps = 6 if flags & (_lib.FT_HINT_DENSE_BAND | _lib.FT_HINT_FOUR_ROW) else 5
         launches = 3 + kps + 16 * kps * -(-(K - 1) // 16) + 1 + 3
         line = {
             "metric": METRIC,

@@ -85,7 +85,15 @@ extern "C" {
                               one-ring (reference configs[4], 65,536 seeds on
                               10M vertices) -- so the three-row kernel trades
                               registers for occupancy.  The Python layer sets
-                              it when nnz - n_cols >= 2^21                   */
+                              it when nnz - n_cols >= 2^21; it also enables
+                              the four-row kernel                            */
+#define FT_HINT_FOUR_ROW 32 /* performance hint only: launch the four-row
+                              kernel (a no-op unless the three-row kernel
+                              leaves >= 48K columns, but a launch per step).
+                              The Python layer sets it for young fields
+                              (nnz - n_cols < n_cols / 16: a band still
+                              forming from init_field), where those columns
+                              are many in the first steps                    */
 
 /* status codes written into ft_step_stats.status / evolve control[1] */
 #define FT_STATUS_OK           0

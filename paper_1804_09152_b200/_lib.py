@@ -29,6 +29,7 @@ FT_LAP_PACKED = 2
 FT_LAP_CHECK_FINITE = 4
 FT_LAP_SYMMETRIC = 8
 FT_HINT_DENSE_BAND = 16
+FT_HINT_FOUR_ROW = 32
 
 FT_PHASE_COLUMNS = 1
 FT_PHASE_FINALIZE = 2

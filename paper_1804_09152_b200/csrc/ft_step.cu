@@ -2241,10 +2241,11 @@ static int launch_columns(const ft_csc* lap_t, int32_t lap_flags, const ft_tiled
     p.report_ids = dom ? dom->report_ids : nullptr;
     const char* w4 = getenv("FT_WIDE4_MIN");     // tests: exercise the four-row kernel on small fields
     p.wide4_min = w4 ? atoi(w4) : ft::kWide4Min;
-    // without the dense-band hint the four-row kernel is not launched (below
-    // its threshold it would be a no-op launch: +1.9 % at C3 without it) and
-    // the warp kernel takes every three-row leftover directly
-    const bool run_w4 = (lap_flags & FT_HINT_DENSE_BAND) || w4;
+    // the four-row kernel only under a hint (a dense band, or a young field
+    // whose band is still forming): otherwise it is a no-op launch below its
+    // threshold (C3 steady state +1.9 % without it) and the warp kernel takes
+    // every three-row leftover directly
+    const bool run_w4 = (lap_flags & (FT_HINT_DENSE_BAND | FT_HINT_FOUR_ROW)) || w4;
     if (!run_w4) p.wide4_min = INT_MAX;
     lib_init();
     if (keep) *keep = p;

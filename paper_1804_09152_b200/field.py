@@ -331,13 +331,18 @@ class _DeviceLap:
         self.renum = None      # the same Laplacian in a locality order (device meshes), or None
 
     def launch_flags(self, phi=None):
-        """FT_LAP_* for the step entry points, plus FT_HINT_DENSE_BAND when
-        the input field ``phi`` (a DeviceCSC) carries a dense band."""
+        """FT_LAP_* for the step entry points, plus the speed hints from the
+        input field ``phi`` (a DeviceCSC): FT_HINT_DENSE_BAND for a dense
+        band, FT_HINT_FOUR_ROW for a young one."""
         f = self.flags | (_lib.FT_LAP_PACKED if self.pack is not None else 0)
         if self.symmetric and ACTIVE_SET:
             f |= _lib.FT_LAP_SYMMETRIC
-        if phi is not None and phi.nnz - phi.n_cols >= DENSE_BAND_EXTRA:
-            f |= _lib.FT_HINT_DENSE_BAND
+        if phi is not None:
+            extra = phi.nnz - phi.n_cols
+            if extra >= DENSE_BAND_EXTRA:
+                f |= _lib.FT_HINT_DENSE_BAND
+            if extra < phi.n_cols // YOUNG_FIELD_DIV:
+                f |= _lib.FT_HINT_FOUR_ROW
         return f
 
     def ft_csc(self, precision):
@@ -489,6 +494,10 @@ ACTIVE_SET = os.environ.get("FT_ACTIVE_SET", "1") != "0"   # active-set stepping
 # variant of the three-row kernel (FT_HINT_DENSE_BAND; speed only): C3
 # (4,096 seeds on 10M vertices) carries ~0.9M, C5 (65,536 seeds) ~3.5M
 DENSE_BAND_EXTRA = int(os.environ.get("FT_DENSE_BAND_EXTRA", str(1 << 21)))
+# a field with fewer extra entries than n_cols / YOUNG_FIELD_DIV is young (its
+# band still forming, e.g. from init_field): the four-row kernel is launched
+# for it (FT_HINT_FOUR_ROW; C3 at step 80 carries 9 %, init_field ~0 %)
+YOUNG_FIELD_DIV = 16
 
 
 class StepWorkspace:
